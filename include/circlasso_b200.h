@@ -1,0 +1,186 @@
+/* circlasso_b200.h — C-ABI of the B200-native circulant LASSO engine.
+ *
+ * Drop-in boundary for the reference `circlasso` solver path (arxiv
+ * 1707.02244).  The reference is a header-only C++20 library with no FFI;
+ * each entry point below names the reference interface it replaces
+ * (paths relative to /root/reference/proj/include/circlasso/).  A C++
+ * adapter with the reference's own names and signatures
+ * (circlasso_b200::ista_run, cadmm_run, SolverConfig, RecoveryReport, ...)
+ * sits on top of this header in include/circlasso_b200.hpp; the Python
+ * package paper_1707_02244_b200 binds the same symbols with ctypes.
+ *
+ * Conventions: plain pointers and sizes; host arrays are fp64 / int64 like
+ * the reference (Eigen::VectorXd, std::vector<Eigen::Index>); the device
+ * iterates in fp32.  No exception crosses the boundary: every call returns a
+ * cl_status whose numbering mirrors the reference's exception hierarchy
+ * (errors.hpp:12-72) and sets a thread-local message (cl_last_error).
+ * A handle is not thread-safe, like the reference's solver states.
+ */
+#ifndef CIRCLASSO_B200_H_
+#define CIRCLASSO_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CL_ABI_VERSION 1
+
+/* errors.hpp:18-72 — one code per exception type, plus device failures. */
+typedef enum cl_status {
+  CL_OK = 0,
+  CL_EDIM = 1,       /* DimensionError      errors.hpp:19-22 */
+  CL_EPARAM = 2,     /* ParameterError      errors.hpp:25-28 */
+  CL_ESINGULAR = 3,  /* SingularityError    errors.hpp:31-34 */
+  CL_EDIVERGE = 4,   /* DivergenceError     errors.hpp:38-41 */
+  CL_ECAPACITY = 5,  /* CapacityError       errors.hpp:44-47 */
+  CL_EFORMAT = 6,    /* FormatError         errors.hpp:50-53 */
+  CL_ECONSIST = 7,   /* ConsistencyError    errors.hpp:57-60 */
+  CL_EPHASE = 8,     /* PhaseError          errors.hpp:63-72 */
+  CL_ECUDA = 9,      /* CUDA runtime / launch failure (new) */
+  CL_ECOMM = 10      /* collective failure in a sharded solve (new) */
+} cl_status;
+
+typedef enum cl_pairing { CL_PAIRING_LITERAL = 0, CL_PAIRING_PROXIMAL = 1 } cl_pairing; /* solvers.hpp:83 */
+typedef enum cl_kind { CL_KIND_ISTA = 0, CL_KIND_CADMM = 1 } cl_kind;
+typedef enum cl_metric { CL_METRIC_MSE_VS_TRUTH = 0, CL_METRIC_ITERATE_CHANGE = 1 } cl_metric; /* solvers.hpp:130 */
+
+/* SolverConfig, solvers.hpp:112-125 (dense_cap/use_fft have no meaning on
+ * the direct engine and are omitted). */
+typedef struct cl_config {
+  double alpha;       /* l1 weight, default 1e-4 */
+  double tau;         /* ISTA step, 0 = automatic 0.9 */
+  double rho;         /* ADMM penalty, default 0.1 */
+  double sigma;       /* cADMM z-split penalty, default 0.1 */
+  double tau1;        /* dual step (v), default 1 */
+  double tau2;        /* dual step (z), default 1 */
+  int64_t max_iter;   /* default 100000 */
+  double target_mse;  /* NaN = never stop early */
+  int32_t check_every;/* default 10 */
+  int32_t pairing;    /* cl_pairing, default literal */
+} cl_config;
+
+/* RecoveryReport, solvers.hpp:139-150 (final_x and the trace are returned
+ * through caller-owned arrays). */
+typedef struct cl_report {
+  int64_t iterations;
+  double setup_seconds;
+  double total_seconds;
+  uint64_t footprint_bytes;
+  int32_t metric;          /* cl_metric */
+  int32_t reached_target;
+  double final_metric;
+  int64_t trace_len;       /* number of check points (may exceed trace_cap) */
+} cl_report;
+
+typedef struct cl_solver cl_solver;
+
+/* ---- library ------------------------------------------------------------ */
+int cl_abi_version(void);
+const char* cl_last_error(void);
+void cl_config_default(cl_config* cfg);                 /* SolverConfig{} */
+/* Number of CUDA devices visible; CL_ECUDA if the driver/runtime is absent. */
+cl_status cl_device_count(int* count);
+
+/* ---- problem generation (sensing.hpp, host, bit-exact) ------------------- */
+/* make_problem sensing.hpp:198-207: c[n], omega[m] (sorted), x_true[n],
+ * support[k] (sorted), y[m] = P C x_true (fp64, FFT-evaluated). */
+cl_status cl_make_problem(int64_t n, int64_t m, int64_t k, uint64_t seed, double* c, int64_t* omega,
+                          double* x_true, int64_t* support, double* y);
+/* gen_sparse_signal sensing.hpp:129-145 */
+cl_status cl_gen_sparse_signal(int64_t n, int64_t k, uint64_t seed, double* values, int64_t* support);
+/* gen_circulant_sensing sensing.hpp:149-168 */
+cl_status cl_gen_circulant_sensing(int64_t n, int64_t m, uint64_t seed, double* c, int64_t* omega);
+/* measure sensing.hpp:171-182 (y = P C x, fp64) */
+cl_status cl_measure(int64_t n, int64_t m, const double* c, const int64_t* omega, const double* x, double* y);
+/* gen_star_field deblur.hpp:69-86 */
+cl_status cl_gen_star_field(int64_t width, int64_t height, double density, uint64_t seed, double* pixels);
+/* blur_matrix deblur.hpp:26-36 (first row) */
+cl_status cl_blur_row(int64_t n, int64_t L, double* row);
+/* compose_sensing deblur.hpp:53-64 first-row part (identity short-circuit
+ * + circ_compose circulant.hpp:337-343) */
+cl_status cl_compose_rows(int64_t n, const double* c, const double* b, double* out);
+
+/* ---- setup operators (circulant.hpp, fp64) ------------------------------- */
+cl_status cl_spectral_norm(int64_t n, const double* c, double* out);                 /* :347-351 */
+cl_status cl_regularized_gram_inverse(int64_t n, const double* c, double rho, double sigma,
+                                      double* b);                                   /* :297-320 */
+cl_status cl_mask_gram_inverse(int64_t n, int64_t m, const int64_t* omega, double rho,
+                               double* d);                                          /* :324-333 */
+
+/* ---- device products (circulant.hpp:214-291, direct sm_100a kernels) ----
+ * out = C x (transpose=0, rule C(i,j)=c[(j-i) mod n]) or C^T x; partial
+ * forms gather/scatter through omega.  fp32 on device, host fp64 in/out. */
+cl_status cl_circ_matvec(int device, int64_t n, const double* c, const double* x, int transpose,
+                         double* out);                                              /* :216-274 */
+cl_status cl_partial_matvec(int device, int64_t n, int64_t m, const double* c, const int64_t* omega,
+                            const double* x, double* out_m);                        /* :277-282 */
+cl_status cl_partial_transpose_matvec(int device, int64_t n, int64_t m, const double* c,
+                                      const int64_t* omega, const double* r_m,
+                                      double* out_n);                               /* :286-291 */
+
+/* ---- solver handles (IstaState/CadmmState + *_setup, solvers.hpp) ------- */
+/* ista_setup solvers.hpp:222-249 / cadmm_setup :359-395.  Validates exactly
+ * where the reference throws; uploads the normalized operator to `device`. */
+cl_status cl_solver_create(int kind, int64_t n, int64_t m, const double* c, const int64_t* omega,
+                           const double* y, const cl_config* cfg, int device, cl_solver** out);
+void cl_solver_destroy(cl_solver* s);
+/* Optional ground truth: switches the check metric to MSE (run_loop :437). */
+cl_status cl_solver_set_truth(cl_solver* s, const double* truth_n);
+/* ista_step / cadmm_step x iters (solvers.hpp:252-263, 399-415), enqueued on
+ * the solver's stream; asynchronous. */
+cl_status cl_solver_step(cl_solver* s, int64_t iters);
+/* One step that also computes the check metric (MSE vs truth if set, else
+ * |x_t - x_{t-1}|/sqrt(n)) and the non-finite flag; synchronous. */
+cl_status cl_solver_step_checked(cl_solver* s, double* metric, int* nonfinite);
+/* run_loop solvers.hpp:426-472 + ista_run/cadmm_run :479-534: full solve
+ * with the reference's check cadence and stopping rule.  final_x (n, may be
+ * NULL) receives x (ISTA) or z (cADMM); trace arrays may be NULL. */
+cl_status cl_solver_run(cl_solver* s, cl_report* rep, double* final_x, int64_t* trace_iter,
+                        double* trace_value, int64_t trace_cap);
+/* Device -> host copy of a state vector by name:
+ * ISTA: "x","r","delta","c","y"; cADMM: "x","z","nu","mu","v","beta","c","b","d","pty". */
+cl_status cl_solver_get(cl_solver* s, const char* field, double* out);
+/* Host -> device (tests, warm state). Same names. */
+cl_status cl_solver_set(cl_solver* s, const char* field, const double* in);
+cl_status cl_solver_info(cl_solver* s, int64_t* n, int64_t* m, int64_t* t, double* scale,
+                         double* threshold);
+cl_status cl_solver_synchronize(cl_solver* s);
+/* Elapsed device time (ms) of the last cl_solver_step call, CUDA events on
+ * the solver's stream (for benchmarking). */
+cl_status cl_solver_last_step_ms(cl_solver* s, double* ms);
+/* Per-kernel device time of the last step (ms), by phase:
+ * ISTA: [residual, residual_reduce, gradient, update]; cADMM: [ctv, beta,
+ * bbeta, x, cx, duals].  `count` in/out. */
+cl_status cl_solver_phase_ms(cl_solver* s, double* ms, int* count);
+/* Enable per-phase event timing (default off). */
+cl_status cl_solver_profile(cl_solver* s, int enable);
+
+/* ---- sharded solve (one process per GPU; row/output-range sharding) -----
+ * The caller owns the collective: between phases it all-gathers the
+ * per-shard slices this library exposes (e.g. torch.distributed NCCL on the
+ * stream returned by cl_solver_stream).  Shard g of G owns outputs
+ * [g*n/G, (g+1)*n/G) (rounded to the kernel tile) and the matching ISTA rows.
+ * Results are bitwise identical for every G: no reduction crosses shards. */
+cl_status cl_solver_shard(cl_solver* s, int rank, int world);
+cl_status cl_solver_stream(cl_solver* s, void** cuda_stream);
+/* Phase-level stepping for sharded solves: phase ids as in cl_solver_phase_ms;
+ * ISTA: 0 = residual (local rows), 1 = gradient+update (local outputs);
+ * cADMM: 0 = beta, 1 = x, 2 = duals. */
+cl_status cl_solver_run_phase(cl_solver* s, int phase);
+/* Device pointer + [begin,end) element range of the vector a phase produced,
+ * and the full vector length, for the caller's all-gather. */
+cl_status cl_solver_phase_output(cl_solver* s, int phase, void** dev_ptr, int64_t* begin,
+                                 int64_t* end, int64_t* total);
+
+/* ---- roofline helper ----------------------------------------------------- */
+/* FP32 FFMA peak microbenchmark on `device` (TFLOP/s), the roofline
+ * denominator for the direct engine. */
+cl_status cl_ffma_peak(int device, double* tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CIRCLASSO_B200_H_ */

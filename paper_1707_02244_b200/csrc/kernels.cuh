@@ -1,0 +1,94 @@
+// Device kernels of the direct (shift-indexed) circulant engine, sm_100a.
+//
+// Every circulant product of the reference hot path is expressed as one
+// circular convolution
+//     out[i] = sum_j h[(i - j) mod n] * u[j]
+// with h a (possibly index-reversed) first row:
+//   C^T v   (cpadmm primal,   parallel.hpp:178-191)  h = c
+//   B beta  (cpadmm recovery, parallel.hpp:193-205)  h = b_rev, b_rev[k] = b[-k mod n]
+//   C x     (cpadmm duals,    parallel.hpp:207-228)  h = c_rev
+//   A^T r   (cpista gradient, parallel.hpp:258-276)  h = c,     u = P^T r (rows only)
+//   (A x)_t (cpista residual, parallel.hpp:243-256)  h = c_rev, outputs only at rows omega
+//
+// Work decomposition (fixed by n and m only, never by the GPU count, so
+// results are bitwise identical for any sharding):
+//   tile  = kThreads * R consecutive register-owned indices (R per thread),
+//   chunk = kChunk consecutive positions staged in shared memory,
+//   split = a contiguous range of chunks; a unit (tile, split) is one CTA.
+// Partial sums of the splits (or of the tiles, for the residual) are combined
+// in ascending order by the epilogue kernels, which also apply the fused
+// solver updates.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace clb {
+
+constexpr int kWarps = 4;
+constexpr int kThreads = kWarps * 32;   // 128
+constexpr int kP = 32;                  // positions per register window block
+constexpr int kChunk = 2048;            // positions per shared-memory stage
+constexpr int kTargetUnits = 1184;      // 8 x 148: split-count target (constant: G-independent)
+constexpr int kEpiBlocks = 592;         // grid of the elementwise epilogues (fixed -> deterministic metrics)
+
+// Register blocking per kernel (indices owned per thread).
+constexpr int kRDense = 64;
+constexpr int kRGrad = 32;
+constexpr int kRRes = 32;
+
+struct ConvPlan {
+  int64_t n = 0;
+  int64_t tile = 0;     // kThreads * R
+  int64_t tiles = 0;    // ceil(n / tile)
+  int64_t chunks = 0;   // ceil(n / kChunk)
+  int splits = 1;       // S
+  int64_t tile_lo = 0, tile_hi = 0;    // shard: tiles run by this rank
+  int split_lo = 0, split_hi = 0;      // shard: splits run by this rank (residual)
+};
+
+ConvPlan make_plan(int64_t n, int R);
+
+// Epilogue parameter block (device pointers; unused ones may be null).
+struct EpiArgs {
+  const float* partial = nullptr;  // [splits][n] (or [tiles][m] for the residual)
+  int splits = 1;
+  int64_t n = 0, lo = 0, hi = 0;   // element range [lo, hi) processed; n = partial stride
+  // ISTA
+  const float* y = nullptr;        // residual: r = y - sum
+  float* r = nullptr;
+  float* x = nullptr;
+  float* delta = nullptr;
+  float tau = 0.f, thr = 0.f;
+  // cADMM
+  const float *d = nullptr, *pty = nullptr;
+  float *z = nullptr, *nu = nullptr, *mu = nullptr, *v = nullptr, *beta = nullptr;
+  float rho = 0.f, sigma = 0.f, tau1 = 1.f, tau2 = 1.f;
+  // check metrics
+  const float* truth = nullptr;
+  double* blk = nullptr;           // [kEpiBlocks][4]: sum d_iter^2, sum d_truth^2, nonfinite, unused
+  int want_metrics = 0;
+};
+
+// partial[split][i] for the plan's shard tiles (dense u).  plan from make_plan(n, kRDense).
+void launch_conv_dense(const ConvPlan& p, const float* h, const float* u, float* partial, cudaStream_t st);
+// gradient: u = P^T r given as rows (omega32 sorted, rvals), rowstart[chunk].  plan R = kRGrad.
+void launch_conv_rows(const ConvPlan& p, const float* h, const int* omega32, const float* rvals,
+                      const int* rowstart, float* partial, cudaStream_t st);
+// residual: partial[tile][t] = sum_{j in tile} h[omega[t]-j] x[j] for rows of the shard's splits.  R = kRRes.
+void launch_conv_residual(const ConvPlan& p, int64_t m, const float* h, const float* x, const int* omega32,
+                          const int* rowstart, float* partial, cudaStream_t st);
+
+void launch_ista_residual_reduce(const EpiArgs& a, int64_t tiles, cudaStream_t st);
+void launch_ista_update(const EpiArgs& a, cudaStream_t st);
+void launch_admm_beta(const EpiArgs& a, cudaStream_t st);
+void launch_admm_x(const EpiArgs& a, cudaStream_t st);
+void launch_admm_duals(const EpiArgs& a, cudaStream_t st);
+void launch_metrics_final(const double* blk, double* out4, cudaStream_t st);
+
+void conv_kernels_init();
+
+// FFMA throughput microkernel (roofline denominator), returns TFLOP/s.
+double ffma_peak_tflops(int device);
+
+}  // namespace clb

@@ -1,0 +1,885 @@
+// Solver engine + C-ABI of circlasso_b200 (include/circlasso_b200.h).
+//
+// Mirrors the reference solver layer (solvers.hpp): *_setup validates and
+// normalizes exactly where the reference throws, *_step advances the state
+// through the direct sm_100a kernels (kernels.cu), run_loop reproduces the
+// check cadence and stopping rule.  Setup transforms are fp64 on the host
+// (host_setup.cpp); iteration state lives in HBM as fp32.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "host_common.hpp"
+#include "kernels.cuh"
+
+namespace clb {
+void gen_sparse_signal(int64_t n, int64_t k, uint64_t seed, double* values, int64_t* support);
+void gen_circulant_sensing(int64_t n, int64_t m, uint64_t seed, double* c, int64_t* omega);
+void gen_star_field(int64_t width, int64_t height, double density, uint64_t seed, double* px);
+void blur_row(int64_t n, int64_t L, double* row);
+
+namespace {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    std::ostringstream msg;
+    msg << what << ": " << cudaGetErrorString(e);
+    raise(CL_ECUDA, msg.str());
+  }
+}
+#define CU(x) cuda_check((x), #x)
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t count = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  void alloc(size_t c) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    count = c;
+    if (c) CU(cudaMalloc(&p, sizeof(T) * c));
+  }
+  void upload(const T* h, size_t c, cudaStream_t st) {
+    if (c) CU(cudaMemcpyAsync(p, h, sizeof(T) * c, cudaMemcpyHostToDevice, st));
+  }
+  void zero(cudaStream_t st) {
+    if (count) CU(cudaMemsetAsync(p, 0, sizeof(T) * count, st));
+  }
+};
+
+std::vector<float> to_f32(const double* a, int64_t n, double scale = 1.0) {
+  std::vector<float> out(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) out[static_cast<size_t>(i)] = static_cast<float>(a[i] / scale);
+  return out;
+}
+std::vector<float> reversed(const std::vector<float>& a) {  // r[k] = a[(-k) mod n]
+  const size_t n = a.size();
+  std::vector<float> r(n);
+  for (size_t k = 0; k < n; ++k) r[k] = a[(n - k) % n];
+  return r;
+}
+
+double seconds_since(std::chrono::steady_clock::time_point a) {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - a).count();
+}
+
+// solvers.hpp:90-106 (circulant kinds only)
+uint64_t footprint(int kind, int64_t n, uint64_t width) {
+  return (kind == CL_KIND_ISTA ? 4 : 10) * static_cast<uint64_t>(n) * width;
+}
+
+}  // namespace
+
+struct Solver {
+  int kind = CL_KIND_ISTA;
+  int device = 0;
+  int64_t n = 0, m = 0;
+  cl_config cfg{};
+  double scale = 1.0, tau = 0.0, thr = 0.0, setup_seconds = 0.0;
+  int64_t t = 0;
+  int rank = 0, world = 1;
+  bool has_truth = false;
+  bool profile = false;
+  cudaStream_t st = nullptr;
+  ConvPlan plan;     // outputs: gradient (ISTA) or dense (cADMM) products
+  ConvPlan rplan;    // ISTA residual (input tiles x position splits)
+  int64_t row_lo = 0, row_hi = 0;  // ISTA rows owned (residual)
+  int64_t out_lo = 0, out_hi = 0;  // outputs owned
+
+  DevBuf<float> hc, hcr, hbr;      // c~, c~ reversed, b reversed
+  DevBuf<int> omega32, rowstart;
+  DevBuf<float> y, r, x, delta;    // ISTA
+  DevBuf<float> d, pty, z, nu, mu, v, beta;  // cADMM (x shared)
+  DevBuf<float> partial, truth;
+  DevBuf<double> blk, met;
+  double* met_host = nullptr;
+  std::vector<int> rowstart_host;
+  cudaEvent_t ev[8] = {};
+  double phase_ms[8] = {};
+  int nphase = 0;
+  cudaEvent_t step_ev[2] = {};
+  double last_step_ms = 0.0;
+
+  ~Solver() {
+    if (st) cudaStreamSynchronize(st);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : step_ev)
+      if (e) cudaEventDestroy(e);
+    if (met_host) cudaFreeHost(met_host);
+    if (st) cudaStreamDestroy(st);
+  }
+
+  void init_device() {
+    int count = 0;
+    CU(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) raise(CL_ECUDA, "cl_solver_create: no such CUDA device");
+    CU(cudaSetDevice(device));
+    CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    for (auto& e : ev) CU(cudaEventCreate(&e));
+    for (auto& e : step_ev) CU(cudaEventCreate(&e));
+    CU(cudaMallocHost(&met_host, sizeof(double) * 4));
+    conv_kernels_init();
+  }
+
+  void build_rows(const int64_t* omega) {
+    std::vector<int> om(static_cast<size_t>(m));
+    for (int64_t t2 = 0; t2 < m; ++t2) om[static_cast<size_t>(t2)] = static_cast<int>(omega[t2]);
+    rowstart_host.assign(static_cast<size_t>(plan.chunks + 1), 0);
+    int64_t k = 0;
+    for (int64_t c = 0; c <= plan.chunks; ++c) {
+      const int64_t lim = c * kChunk;
+      while (k < m && omega[k] < lim) ++k;
+      rowstart_host[static_cast<size_t>(c)] = static_cast<int>(k);
+    }
+    omega32.alloc(static_cast<size_t>(m));
+    omega32.upload(om.data(), static_cast<size_t>(m), st);
+    rowstart.alloc(rowstart_host.size());
+    rowstart.upload(rowstart_host.data(), rowstart_host.size(), st);
+  }
+
+  void set_shard(int rk, int ws) {
+    if (ws < 1 || rk < 0 || rk >= ws) raise(CL_EPARAM, "cl_solver_shard: need 0 <= rank < world");
+    rank = rk;
+    world = ws;
+    plan.tile_lo = plan.tiles * rk / ws;
+    plan.tile_hi = plan.tiles * (rk + 1) / ws;
+    out_lo = std::min<int64_t>(n, plan.tile_lo * plan.tile);
+    out_hi = std::min<int64_t>(n, plan.tile_hi * plan.tile);
+    if (kind == CL_KIND_ISTA) {
+      rplan.split_lo = static_cast<int>(static_cast<int64_t>(rplan.splits) * rk / ws);
+      rplan.split_hi = static_cast<int>(static_cast<int64_t>(rplan.splits) * (rk + 1) / ws);
+      const int64_t c_lo = static_cast<int64_t>(rplan.split_lo) * rplan.chunks / rplan.splits;
+      const int64_t c_hi = static_cast<int64_t>(rplan.split_hi) * rplan.chunks / rplan.splits;
+      row_lo = rowstart_host[static_cast<size_t>(c_lo)];
+      row_hi = rowstart_host[static_cast<size_t>(c_hi)];
+    }
+  }
+
+  void setup_common(const double* c, const int64_t* omega, const double* yh, const cl_config* config) {
+    if (!config) raise(CL_EPARAM, "cl_solver_create: null config");
+    cfg = *config;
+    check_mask(omega, m, n);
+  }
+
+  // solvers.hpp:170-183
+  double normalization(const double* c, const double* yh) {
+    for (int64_t i = 0; i < m; ++i)
+      if (!std::isfinite(yh[i])) raise(CL_EDIVERGE, "solver: measurements contain non-finite entries");
+    const double s = spectral_norm(c, n);
+    if (s > 0.0) return s;
+    double mx = 0.0;
+    for (int64_t i = 0; i < m; ++i) mx = std::max(mx, std::abs(yh[i]));
+    if (m == 0 || mx == 0.0) return 1.0;
+    raise(CL_ESINGULAR, "solver: sensing operator is zero but measurements are not");
+  }
+
+  void setup_ista(const double* c, const int64_t* omega, const double* yh) {  // solvers.hpp:222-249
+    double tau0 = cfg.tau;
+    if (tau0 == 0.0) tau0 = 0.9;
+    if (!(tau0 > 0.0) || !(tau0 < 1.0))
+      raise(CL_EPARAM,
+            "ista_setup: tau must lie in (0, |A|_2^-2); on the normalized operator the admissible range is (0, 1)");
+    if (!(cfg.alpha > 0.0)) raise(CL_EPARAM, "ista_setup: alpha must be > 0");
+    scale = normalization(c, yh);
+    tau = tau0;
+    thr = cfg.pairing == CL_PAIRING_LITERAL ? cfg.alpha : tau0 * cfg.alpha;
+    init_device();
+    plan = make_plan(n, kRGrad);
+    rplan = make_plan(n, kRRes);
+    const std::vector<float> cf = to_f32(c, n, scale);
+    hc.alloc(static_cast<size_t>(n));
+    hc.upload(cf.data(), cf.size(), st);
+    const std::vector<float> crf = reversed(cf);
+    hcr.alloc(static_cast<size_t>(n));
+    hcr.upload(crf.data(), crf.size(), st);
+    build_rows(omega);
+    const std::vector<float> yf = to_f32(yh, m, scale);
+    y.alloc(static_cast<size_t>(m));
+    y.upload(yf.data(), yf.size(), st);
+    for (DevBuf<float>* b : {&r}) { b->alloc(static_cast<size_t>(m)); b->zero(st); }
+    for (DevBuf<float>* b : {&x, &delta}) { b->alloc(static_cast<size_t>(n)); b->zero(st); }
+    partial.alloc(static_cast<size_t>(std::max<int64_t>(rplan.tiles * m, plan.splits * n)));
+    blk.alloc(kEpiBlocks * 4);
+    met.alloc(4);
+    set_shard(0, 1);
+    CU(cudaStreamSynchronize(st));
+  }
+
+  void setup_cadmm(const double* c, const int64_t* omega, const double* yh) {  // solvers.hpp:359-395
+    if (!(cfg.rho > 0.0) || !(cfg.sigma > 0.0)) raise(CL_EPARAM, "cadmm_setup: rho and sigma must be > 0");
+    if (!(cfg.alpha > 0.0)) raise(CL_EPARAM, "cadmm_setup: alpha must be > 0");
+    constexpr double kGolden = 1.6180339887498949;
+    if (!(cfg.tau1 > 0.0) || cfg.tau1 >= kGolden || !(cfg.tau2 > 0.0) || cfg.tau2 >= kGolden)
+      raise(CL_EPARAM, "cadmm_setup: tau1 and tau2 must lie in (0, (sqrt(5)+1)/2)");
+    scale = normalization(c, yh);
+    std::vector<double> cn(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) cn[static_cast<size_t>(i)] = c[i] / scale;
+    std::vector<double> bh(static_cast<size_t>(n)), dh(static_cast<size_t>(n));
+    regularized_gram_inverse(cn.data(), n, cfg.rho, cfg.sigma, bh.data());
+    mask_gram_inverse(omega, m, n, cfg.rho, dh.data());
+    std::vector<double> ptyh(static_cast<size_t>(n), 0.0);
+    for (int64_t t2 = 0; t2 < m; ++t2) ptyh[static_cast<size_t>(omega[t2])] = yh[t2] / scale;
+    thr = cfg.alpha / cfg.sigma;
+    init_device();
+    plan = make_plan(n, kRDense);
+    const std::vector<float> cf = to_f32(cn.data(), n);
+    hc.alloc(static_cast<size_t>(n));
+    hc.upload(cf.data(), cf.size(), st);
+    const std::vector<float> crf = reversed(cf);
+    hcr.alloc(static_cast<size_t>(n));
+    hcr.upload(crf.data(), crf.size(), st);
+    const std::vector<float> brf = reversed(to_f32(bh.data(), n));
+    hbr.alloc(static_cast<size_t>(n));
+    hbr.upload(brf.data(), brf.size(), st);
+    const std::vector<float> df = to_f32(dh.data(), n), pf = to_f32(ptyh.data(), n);
+    d.alloc(static_cast<size_t>(n));
+    d.upload(df.data(), df.size(), st);
+    pty.alloc(static_cast<size_t>(n));
+    pty.upload(pf.data(), pf.size(), st);
+    for (DevBuf<float>* b : {&x, &z, &nu, &mu, &v, &beta}) { b->alloc(static_cast<size_t>(n)); b->zero(st); }
+    partial.alloc(static_cast<size_t>(plan.splits * n));
+    blk.alloc(kEpiBlocks * 4);
+    met.alloc(4);
+    rowstart_host.assign(static_cast<size_t>(plan.chunks + 1), 0);
+    set_shard(0, 1);
+    CU(cudaStreamSynchronize(st));
+  }
+
+  void mark(int i) {
+    if (profile) CU(cudaEventRecord(ev[i], st));
+  }
+
+  EpiArgs base_args(int want) {
+    EpiArgs a;
+    a.partial = partial.p;
+    a.splits = plan.splits;
+    a.n = n;
+    a.lo = out_lo;
+    a.hi = out_hi;
+    a.truth = has_truth ? truth.p : nullptr;
+    a.blk = blk.p;
+    a.want_metrics = want;
+    return a;
+  }
+
+  // ---- phases -------------------------------------------------------------
+  void ista_residual() {
+    mark(0);
+    launch_conv_residual(rplan, m, hcr.p, x.p, omega32.p, rowstart.p, partial.p, st);
+    mark(1);
+    EpiArgs a;
+    a.partial = partial.p;
+    a.n = m;
+    a.lo = row_lo;
+    a.hi = row_hi;
+    a.y = y.p;
+    a.r = r.p;
+    launch_ista_residual_reduce(a, rplan.tiles, st);
+    mark(2);
+  }
+  void ista_gradient(int want) {
+    launch_conv_rows(plan, hc.p, omega32.p, r.p, rowstart.p, partial.p, st);
+    mark(3);
+    EpiArgs a = base_args(want);
+    a.x = x.p;
+    a.delta = delta.p;
+    a.tau = static_cast<float>(tau);
+    a.thr = static_cast<float>(thr);
+    launch_ista_update(a, st);
+    mark(4);
+    nphase = 4;
+  }
+  void admm_beta_phase() {
+    mark(0);
+    launch_conv_dense(plan, hc.p, v.p, partial.p, st);
+    mark(1);
+    EpiArgs a = base_args(0);
+    a.beta = beta.p;
+    a.z = z.p;
+    a.nu = nu.p;
+    a.rho = static_cast<float>(cfg.rho);
+    a.sigma = static_cast<float>(cfg.sigma);
+    launch_admm_beta(a, st);
+    mark(2);
+  }
+  void admm_x_phase() {
+    launch_conv_dense(plan, hbr.p, beta.p, partial.p, st);
+    mark(3);
+    EpiArgs a = base_args(0);
+    a.x = x.p;
+    launch_admm_x(a, st);
+    mark(4);
+  }
+  void admm_dual_phase(int want) {
+    launch_conv_dense(plan, hcr.p, x.p, partial.p, st);
+    mark(5);
+    EpiArgs a = base_args(want);
+    a.x = x.p;
+    a.z = z.p;
+    a.nu = nu.p;
+    a.mu = mu.p;
+    a.v = v.p;
+    a.d = d.p;
+    a.pty = pty.p;
+    a.rho = static_cast<float>(cfg.rho);
+    a.tau1 = static_cast<float>(cfg.tau1);
+    a.tau2 = static_cast<float>(cfg.tau2);
+    a.thr = static_cast<float>(thr);
+    launch_admm_duals(a, st);
+    mark(6);
+    nphase = 6;
+  }
+
+  void one_step(int want) {
+    if (world != 1) raise(CL_EPARAM, "cl_solver_step: sharded solvers advance with cl_solver_run_phase");
+    if (kind == CL_KIND_ISTA) {
+      ista_residual();
+      ista_gradient(want);
+    } else {
+      admm_beta_phase();
+      admm_x_phase();
+      admm_dual_phase(want);
+    }
+    CU(cudaGetLastError());
+    ++t;
+  }
+
+  void collect_profile() {
+    if (!profile) return;
+    CU(cudaEventSynchronize(ev[nphase]));
+    for (int i = 0; i < nphase; ++i) {
+      float ms = 0.f;
+      CU(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+      phase_ms[i] = ms;
+    }
+  }
+
+  void step(int64_t iters) {
+    CU(cudaEventRecord(step_ev[0], st));
+    for (int64_t k = 0; k < iters; ++k) one_step(0);
+    CU(cudaEventRecord(step_ev[1], st));
+  }
+
+  // Checked step: metric per run_loop solvers.hpp:454-456.
+  void step_checked(double* metric, int* nonfinite) {
+    one_step(1);
+    launch_metrics_final(blk.p, met.p, st);
+    CU(cudaMemcpyAsync(met_host, met.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    collect_profile();
+    const double nn = static_cast<double>(n);
+    *nonfinite = met_host[2] > 0.0;
+    if (has_truth) *metric = n > 0 ? met_host[1] / nn : 0.0;
+    else *metric = std::sqrt(met_host[0]) * (n > 0 ? 1.0 / std::sqrt(nn) : 1.0);
+  }
+
+  float* field_ptr(const std::string& f, int64_t* len) {
+    *len = n;
+    if (kind == CL_KIND_ISTA) {
+      if (f == "x") return x.p;
+      if (f == "delta") return delta.p;
+      if (f == "c") return hc.p;
+      *len = m;
+      if (f == "r") return r.p;
+      if (f == "y") return y.p;
+    } else {
+      if (f == "x") return x.p;
+      if (f == "z") return z.p;
+      if (f == "nu") return nu.p;
+      if (f == "mu") return mu.p;
+      if (f == "v") return v.p;
+      if (f == "beta") return beta.p;
+      if (f == "c") return hc.p;
+      if (f == "d") return d.p;
+      if (f == "pty") return pty.p;
+      if (f == "b") return hbr.p;  // reversed on device; un-reversed on get
+    }
+    raise(CL_EPARAM, "cl_solver_get: unknown field '" + f + "'");
+  }
+};
+
+// ---- device product helpers (cl_circ_matvec & co.) --------------------------
+struct ScratchProduct {
+  static void circ(int device, int64_t n, const double* c, const double* xin, int transpose, double* out) {
+    CU(cudaSetDevice(device));
+    conv_kernels_init();
+    cudaStream_t st;
+    CU(cudaStreamCreate(&st));
+    ConvPlan p = make_plan(n, kRDense);
+    std::vector<float> cf = to_f32(c, n);
+    if (!transpose) cf = reversed(cf);  // C x = conv(c_rev, x)
+    const std::vector<float> xf = to_f32(xin, n);
+    DevBuf<float> h, u, part, o;
+    h.alloc(static_cast<size_t>(n));
+    h.upload(cf.data(), cf.size(), st);
+    u.alloc(static_cast<size_t>(n));
+    u.upload(xf.data(), xf.size(), st);
+    part.alloc(static_cast<size_t>(p.splits * n));
+    o.alloc(static_cast<size_t>(n));
+    launch_conv_dense(p, h.p, u.p, part.p, st);
+    EpiArgs a;
+    a.partial = part.p;
+    a.splits = p.splits;
+    a.n = n;
+    a.lo = 0;
+    a.hi = n;
+    a.x = o.p;
+    launch_admm_x(a, st);
+    CU(cudaGetLastError());
+    std::vector<float> res(static_cast<size_t>(n));
+    CU(cudaMemcpyAsync(res.data(), o.p, sizeof(float) * n, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    CU(cudaStreamDestroy(st));
+    for (int64_t i = 0; i < n; ++i) out[i] = res[static_cast<size_t>(i)];
+  }
+};
+
+}  // namespace clb
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+using namespace clb;
+
+struct cl_solver {
+  std::unique_ptr<Solver> impl;
+};
+
+#define CL_GUARD_BEGIN try {
+#define CL_GUARD_END                              \
+  return CL_OK;                                   \
+  }                                               \
+  catch (const Failure& f) {                      \
+    set_error(f.msg);                             \
+    return f.code;                                \
+  }                                               \
+  catch (const std::bad_alloc&) {                 \
+    set_error("host allocation failed");          \
+    return CL_ECAPACITY;                          \
+  }                                               \
+  catch (const std::exception& e) {               \
+    set_error(e.what());                          \
+    return CL_ECUDA;                              \
+  }
+
+extern "C" {
+
+int cl_abi_version(void) { return CL_ABI_VERSION; }
+const char* cl_last_error(void) { return last_error().c_str(); }
+
+void cl_config_default(cl_config* c) {  // solvers.hpp:112-125
+  c->alpha = 1e-4;
+  c->tau = 0.0;
+  c->rho = 0.1;
+  c->sigma = 0.1;
+  c->tau1 = 1.0;
+  c->tau2 = 1.0;
+  c->max_iter = 100000;
+  c->target_mse = std::numeric_limits<double>::quiet_NaN();
+  c->check_every = 10;
+  c->pairing = CL_PAIRING_LITERAL;
+}
+
+cl_status cl_device_count(int* count) {
+  CL_GUARD_BEGIN
+  *count = 0;
+  CU(cudaGetDeviceCount(count));
+  CL_GUARD_END
+}
+
+cl_status cl_gen_sparse_signal(int64_t n, int64_t k, uint64_t seed, double* values, int64_t* support) {
+  CL_GUARD_BEGIN
+  gen_sparse_signal(n, k, seed, values, support);
+  CL_GUARD_END
+}
+cl_status cl_gen_circulant_sensing(int64_t n, int64_t m, uint64_t seed, double* c, int64_t* omega) {
+  CL_GUARD_BEGIN
+  gen_circulant_sensing(n, m, seed, c, omega);
+  CL_GUARD_END
+}
+cl_status cl_measure(int64_t n, int64_t m, const double* c, const int64_t* omega, const double* x, double* y) {
+  CL_GUARD_BEGIN
+  check_mask(omega, m, n);
+  measure(c, omega, n, m, x, y);
+  CL_GUARD_END
+}
+cl_status cl_make_problem(int64_t n, int64_t m, int64_t k, uint64_t seed, double* c, int64_t* omega, double* x_true,
+                          int64_t* support, double* y) {
+  CL_GUARD_BEGIN
+  gen_sparse_signal(n, k, seed, x_true, support);
+  gen_circulant_sensing(n, m, seed, c, omega);
+  measure(c, omega, n, m, x_true, y);
+  CL_GUARD_END
+}
+cl_status cl_gen_star_field(int64_t w, int64_t h, double density, uint64_t seed, double* px) {
+  CL_GUARD_BEGIN
+  gen_star_field(w, h, density, seed, px);
+  CL_GUARD_END
+}
+cl_status cl_blur_row(int64_t n, int64_t L, double* row) {
+  CL_GUARD_BEGIN
+  blur_row(n, L, row);
+  CL_GUARD_END
+}
+cl_status cl_compose_rows(int64_t n, const double* c, const double* b, double* out) {
+  CL_GUARD_BEGIN
+  compose_rows(c, b, n, out);
+  CL_GUARD_END
+}
+cl_status cl_spectral_norm(int64_t n, const double* c, double* out) {
+  CL_GUARD_BEGIN
+  *out = spectral_norm(c, n);
+  CL_GUARD_END
+}
+cl_status cl_regularized_gram_inverse(int64_t n, const double* c, double rho, double sigma, double* b) {
+  CL_GUARD_BEGIN
+  regularized_gram_inverse(c, n, rho, sigma, b);
+  CL_GUARD_END
+}
+cl_status cl_mask_gram_inverse(int64_t n, int64_t m, const int64_t* omega, double rho, double* d) {
+  CL_GUARD_BEGIN
+  check_mask(omega, m, n);
+  mask_gram_inverse(omega, m, n, rho, d);
+  CL_GUARD_END
+}
+
+cl_status cl_circ_matvec(int device, int64_t n, const double* c, const double* x, int transpose, double* out) {
+  CL_GUARD_BEGIN
+  if (n < 1) raise(CL_EDIM, "circ_matvec: empty operator");
+  ScratchProduct::circ(device, n, c, x, transpose, out);
+  CL_GUARD_END
+}
+
+cl_status cl_partial_matvec(int device, int64_t n, int64_t m, const double* c, const int64_t* omega, const double* xin,
+                            double* out_m) {
+  CL_GUARD_BEGIN
+  check_mask(omega, m, n);
+  // A x through the residual kernel with y = 0: r = -A x.
+  std::vector<double> zero(static_cast<size_t>(m), 0.0);
+  cl_config cfg;
+  cl_config_default(&cfg);
+  Solver s;
+  s.kind = CL_KIND_ISTA;
+  s.device = device;
+  s.n = n;
+  s.m = m;
+  s.cfg = cfg;
+  s.init_device();
+  s.plan = make_plan(n, kRGrad);
+  s.rplan = make_plan(n, kRRes);
+  const std::vector<float> crf = reversed(to_f32(c, n));
+  s.hcr.alloc(static_cast<size_t>(n));
+  s.hcr.upload(crf.data(), crf.size(), s.st);
+  s.build_rows(omega);
+  const std::vector<float> xf = to_f32(xin, n);
+  s.x.alloc(static_cast<size_t>(n));
+  s.x.upload(xf.data(), xf.size(), s.st);
+  s.y.alloc(static_cast<size_t>(m));
+  s.y.zero(s.st);
+  s.r.alloc(static_cast<size_t>(m));
+  s.partial.alloc(static_cast<size_t>(s.rplan.tiles * m));
+  s.set_shard(0, 1);
+  s.ista_residual();
+  CU(cudaGetLastError());
+  std::vector<float> res(static_cast<size_t>(m));
+  CU(cudaMemcpyAsync(res.data(), s.r.p, sizeof(float) * m, cudaMemcpyDeviceToHost, s.st));
+  CU(cudaStreamSynchronize(s.st));
+  for (int64_t i = 0; i < m; ++i) out_m[i] = -static_cast<double>(res[static_cast<size_t>(i)]);
+  CL_GUARD_END
+}
+
+cl_status cl_partial_transpose_matvec(int device, int64_t n, int64_t m, const double* c, const int64_t* omega,
+                                      const double* r_m, double* out_n) {
+  CL_GUARD_BEGIN
+  check_mask(omega, m, n);
+  Solver s;
+  s.kind = CL_KIND_ISTA;
+  s.device = device;
+  s.n = n;
+  s.m = m;
+  s.init_device();
+  s.plan = make_plan(n, kRGrad);
+  const std::vector<float> cf = to_f32(c, n);
+  s.hc.alloc(static_cast<size_t>(n));
+  s.hc.upload(cf.data(), cf.size(), s.st);
+  s.build_rows(omega);
+  const std::vector<float> rf = to_f32(r_m, m);
+  s.r.alloc(static_cast<size_t>(m));
+  s.r.upload(rf.data(), rf.size(), s.st);
+  s.partial.alloc(static_cast<size_t>(s.plan.splits * n));
+  s.x.alloc(static_cast<size_t>(n));
+  launch_conv_rows(s.plan, s.hc.p, s.omega32.p, s.r.p, s.rowstart.p, s.partial.p, s.st);
+  EpiArgs a;
+  a.partial = s.partial.p;
+  a.splits = s.plan.splits;
+  a.n = n;
+  a.lo = 0;
+  a.hi = n;
+  a.x = s.x.p;
+  launch_admm_x(a, s.st);
+  CU(cudaGetLastError());
+  std::vector<float> res(static_cast<size_t>(n));
+  CU(cudaMemcpyAsync(res.data(), s.x.p, sizeof(float) * n, cudaMemcpyDeviceToHost, s.st));
+  CU(cudaStreamSynchronize(s.st));
+  for (int64_t i = 0; i < n; ++i) out_n[i] = res[static_cast<size_t>(i)];
+  CL_GUARD_END
+}
+
+cl_status cl_solver_create(int kind, int64_t n, int64_t m, const double* c, const int64_t* omega, const double* y,
+                           const cl_config* cfg, int device, cl_solver** out) {
+  CL_GUARD_BEGIN
+  *out = nullptr;
+  if (kind != CL_KIND_ISTA && kind != CL_KIND_CADMM) raise(CL_EPARAM, "cl_solver_create: unknown solver kind");
+  if (n < 1) raise(CL_EDIM, "cl_solver_create: n must be >= 1");
+  if (m < 0 || m > n) raise(CL_EDIM, "cl_solver_create: need 0 <= m <= n");
+  if (n > (int64_t(1) << 30)) raise(CL_ECAPACITY, "cl_solver_create: n above 2^30 is not supported");
+  const auto t0 = std::chrono::steady_clock::now();
+  auto s = std::make_unique<Solver>();
+  s->kind = kind;
+  s->device = device;
+  s->n = n;
+  s->m = m;
+  s->setup_common(c, omega, y, cfg);
+  if (kind == CL_KIND_ISTA) s->setup_ista(c, omega, y);
+  else s->setup_cadmm(c, omega, y);
+  s->setup_seconds = seconds_since(t0);
+  *out = new cl_solver{std::move(s)};
+  CL_GUARD_END
+}
+
+void cl_solver_destroy(cl_solver* s) { delete s; }
+
+cl_status cl_solver_set_truth(cl_solver* h, const double* truth_n) {
+  CL_GUARD_BEGIN
+  Solver& s = *h->impl;
+  CU(cudaSetDevice(s.device));
+  if (!truth_n) {
+    s.has_truth = false;
+  } else {
+    const std::vector<float> tf = to_f32(truth_n, s.n);
+    s.truth.alloc(static_cast<size_t>(s.n));
+    s.truth.upload(tf.data(), tf.size(), s.st);
+    CU(cudaStreamSynchronize(s.st));
+    s.has_truth = true;
+  }
+  CL_GUARD_END
+}
+
+cl_status cl_solver_step(cl_solver* h, int64_t iters) {
+  CL_GUARD_BEGIN
+  Solver& s = *h->impl;
+  CU(cudaSetDevice(s.device));
+  if (iters < 0) raise(CL_EPARAM, "cl_solver_step: iters must be >= 0");
+  s.step(iters);
+  CL_GUARD_END
+}
+
+cl_status cl_solver_step_checked(cl_solver* h, double* metric, int* nonfinite) {
+  CL_GUARD_BEGIN
+  Solver& s = *h->impl;
+  CU(cudaSetDevice(s.device));
+  s.step_checked(metric, nonfinite);
+  CL_GUARD_END
+}
+
+cl_status cl_solver_run(cl_solver* h, cl_report* rep, double* final_x, int64_t* trace_iter, double* trace_value,
+                        int64_t trace_cap) {
+  CL_GUARD_BEGIN
+  Solver& s = *h->impl;
+  CU(cudaSetDevice(s.device));
+  const cl_config& cfg = s.cfg;
+  if (cfg.max_iter < 0) raise(CL_EPARAM, "solver: max_iter must be >= 0");   // solvers.hpp:432
+  if (cfg.check_every < 1) raise(CL_EPARAM, "solver: check_every must be >= 1");  // :433-434
+  const auto t0 = std::chrono::steady_clock::now();
+  std::memset(rep, 0, sizeof(*rep));
+  rep->metric = s.has_truth ? CL_METRIC_MSE_VS_TRUTH : CL_METRIC_ITERATE_CHANGE;
+  rep->final_metric = std::numeric_limits<double>::quiet_NaN();
+  const bool has_target = !std::isnan(cfg.target_mse);
+  int64_t t = 0, tl = 0;
+  while (t < cfg.max_iter) {
+    // next check point: t % check_every == 0 or t == max_iter (solvers.hpp:452)
+    int64_t next = ((t / cfg.check_every) + 1) * cfg.check_every;
+    if (next > cfg.max_iter) next = cfg.max_iter;
+    if (next - t > 1) s.step(next - t - 1);
+    double value = 0.0;
+    int nonfinite = 0;
+    s.step_checked(&value, &nonfinite);
+    t = next;
+    if (nonfinite)
+      raise(CL_EDIVERGE, s.kind == CL_KIND_ISTA ? "ista_run: iterate became non-finite"
+                                                : "cadmm_run: iterate became non-finite");
+    if (trace_iter && tl < trace_cap) trace_iter[tl] = t;
+    if (trace_value && tl < trace_cap) trace_value[tl] = value;
+    ++tl;
+    rep->final_metric = value;
+    if (has_target && value <= cfg.target_mse) {
+      rep->reached_target = 1;
+      break;
+    }
+  }
+  rep->iterations = t;
+  rep->trace_len = tl;
+  rep->setup_seconds = s.setup_seconds;
+  rep->total_seconds = seconds_since(t0) + s.setup_seconds;
+  rep->footprint_bytes = footprint(s.kind, s.n, sizeof(float));
+  if (final_x) {
+    int64_t len = 0;
+    float* p = s.field_ptr(s.kind == CL_KIND_ISTA ? "x" : "z", &len);
+    std::vector<float> tmp(static_cast<size_t>(len));
+    CU(cudaMemcpyAsync(tmp.data(), p, sizeof(float) * len, cudaMemcpyDeviceToHost, s.st));
+    CU(cudaStreamSynchronize(s.st));
+    for (int64_t i = 0; i < len; ++i) final_x[i] = tmp[static_cast<size_t>(i)];
+  }
+  CL_GUARD_END
+}
+
+cl_status cl_solver_get(cl_solver* h, const char* field, double* out) {
+  CL_GUARD_BEGIN
+  Solver& s = *h->impl;
+  CU(cudaSetDevice(s.device));
+  int64_t len = 0;
+  const std::string f(field ? field : "");
+  float* p = s.field_ptr(f, &len);
+  std::vector<float> tmp(static_cast<size_t>(len));
+  CU(cudaMemcpyAsync(tmp.data(), p, sizeof(float) * len, cudaMemcpyDeviceToHost, s.st));
+  CU(cudaStreamSynchronize(s.st));
+  if (f == "b") tmp = reversed(tmp);
+  for (int64_t i = 0; i < len; ++i) out[i] = tmp[static_cast<size_t>(i)];
+  CL_GUARD_END
+}
+
+cl_status cl_solver_set(cl_solver* h, const char* field, const double* in) {
+  CL_GUARD_BEGIN
+  Solver& s = *h->impl;
+  CU(cudaSetDevice(s.device));
+  int64_t len = 0;
+  const std::string f(field ? field : "");
+  float* p = s.field_ptr(f, &len);
+  std::vector<float> tmp = to_f32(in, len);
+  if (f == "b") tmp = reversed(tmp);
+  if (f == "c") {  // keep the reversed copy coherent
+    const std::vector<float> rv = reversed(tmp);
+    CU(cudaMemcpyAsync(s.hcr.p, rv.data(), sizeof(float) * len, cudaMemcpyHostToDevice, s.st));
+  }
+  CU(cudaMemcpyAsync(p, tmp.data(), sizeof(float) * len, cudaMemcpyHostToDevice, s.st));
+  CU(cudaStreamSynchronize(s.st));
+  CL_GUARD_END
+}
+
+cl_status cl_solver_info(cl_solver* h, int64_t* n, int64_t* m, int64_t* t, double* scale, double* threshold) {
+  CL_GUARD_BEGIN
+  Solver& s = *h->impl;
+  if (n) *n = s.n;
+  if (m) *m = s.m;
+  if (t) *t = s.t;
+  if (scale) *scale = s.scale;
+  if (threshold) *threshold = s.thr;
+  CL_GUARD_END
+}
+
+cl_status cl_solver_synchronize(cl_solver* h) {
+  CL_GUARD_BEGIN
+  Solver& s = *h->impl;
+  CU(cudaSetDevice(s.device));
+  CU(cudaStreamSynchronize(s.st));
+  s.collect_profile();
+  CL_GUARD_END
+}
+
+cl_status cl_solver_last_step_ms(cl_solver* h, double* ms) {
+  CL_GUARD_BEGIN
+  Solver& s = *h->impl;
+  CU(cudaSetDevice(s.device));
+  CU(cudaEventSynchronize(s.step_ev[1]));
+  float f = 0.f;
+  CU(cudaEventElapsedTime(&f, s.step_ev[0], s.step_ev[1]));
+  *ms = f;
+  CL_GUARD_END
+}
+
+cl_status cl_solver_profile(cl_solver* h, int enable) {
+  CL_GUARD_BEGIN
+  h->impl->profile = enable != 0;
+  CL_GUARD_END
+}
+
+cl_status cl_solver_phase_ms(cl_solver* h, double* ms, int* count) {
+  CL_GUARD_BEGIN
+  Solver& s = *h->impl;
+  CU(cudaSetDevice(s.device));
+  s.collect_profile();
+  const int c = std::min(*count, s.nphase);
+  for (int i = 0; i < c; ++i) ms[i] = s.phase_ms[i];
+  *count = s.nphase;
+  CL_GUARD_END
+}
+
+cl_status cl_solver_shard(cl_solver* h, int rank, int world) {
+  CL_GUARD_BEGIN
+  h->impl->set_shard(rank, world);
+  CL_GUARD_END
+}
+
+cl_status cl_solver_stream(cl_solver* h, void** stream) {
+  CL_GUARD_BEGIN
+  *stream = h->impl->st;
+  CL_GUARD_END
+}
+
+cl_status cl_solver_run_phase(cl_solver* h, int phase) {
+  CL_GUARD_BEGIN
+  Solver& s = *h->impl;
+  CU(cudaSetDevice(s.device));
+  if (s.kind == CL_KIND_ISTA) {
+    if (phase == 0) s.ista_residual();
+    else if (phase == 1) { s.ista_gradient(0); ++s.t; }
+    else raise(CL_EPARAM, "cl_solver_run_phase: ISTA phases are 0 (residual) and 1 (gradient)");
+  } else {
+    if (phase == 0) s.admm_beta_phase();
+    else if (phase == 1) s.admm_x_phase();
+    else if (phase == 2) { s.admm_dual_phase(0); ++s.t; }
+    else raise(CL_EPARAM, "cl_solver_run_phase: cADMM phases are 0 (beta), 1 (x), 2 (duals)");
+  }
+  CU(cudaGetLastError());
+  CL_GUARD_END
+}
+
+cl_status cl_solver_phase_output(cl_solver* h, int phase, void** dev_ptr, int64_t* begin, int64_t* end,
+                                 int64_t* total) {
+  CL_GUARD_BEGIN
+  Solver& s = *h->impl;
+  if (s.kind == CL_KIND_ISTA) {
+    if (phase == 0) { *dev_ptr = s.r.p; *begin = s.row_lo; *end = s.row_hi; *total = s.m; }
+    else { *dev_ptr = s.x.p; *begin = s.out_lo; *end = s.out_hi; *total = s.n; }
+  } else {
+    *dev_ptr = phase == 0 ? s.beta.p : phase == 1 ? s.x.p : s.v.p;
+    *begin = s.out_lo;
+    *end = s.out_hi;
+    *total = s.n;
+  }
+  CL_GUARD_END
+}
+
+cl_status cl_ffma_peak(int device, double* tflops) {
+  CL_GUARD_BEGIN
+  const double v = ffma_peak_tflops(device);
+  if (v <= 0) raise(CL_ECUDA, "cl_ffma_peak: microbenchmark failed");
+  *tflops = v;
+  CL_GUARD_END
+}
+
+}  // extern "C"

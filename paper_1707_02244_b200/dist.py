@@ -1,0 +1,142 @@
+"""Sharded solves: one process per GPU, row/output-range sharding.
+
+Shard g of G owns a contiguous, tile-aligned range of every product's outputs
+(and, for ISTA, the residual rows of its position splits).  Between phases
+each rank publishes its slice and all-gathers the others' slices -- the only
+cross-GPU traffic, n (or m) floats per phase.  No reduction crosses ranks, so
+the iterate is bitwise identical for every G.
+
+The collective is pluggable: ``TorchGather`` uses torch.distributed (NCCL
+over NVLink on GPUs, gloo on CPU tensors in the tests); the phase logic in
+``ShardedRunner`` is backend-agnostic and is exercised on CPU by
+tests/test_dist_gloo.py with a CPU backend defined in the tests.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Protocol, Sequence
+
+from ._native import lib
+from .api import _check
+
+
+class ShardBackend(Protocol):
+    """What ShardedRunner needs from a solver shard."""
+
+    def phases(self) -> Sequence[int]: ...
+
+    def run_phase(self, phase: int) -> None: ...
+
+    def phase_output(self, phase: int):
+        """-> (full-length tensor view of the produced vector, begin, end)."""
+        ...
+
+
+class TorchGather:
+    """All-gather of unequal contiguous slices via torch.distributed.
+
+    Each rank copies its slice into a padded staging row, one
+    all_gather_into_tensor exchanges the rows, and the slices are copied back
+    into the full vector at their offsets.  Offsets are exchanged once per
+    phase (they are static) and cached.
+    """
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self._ranges = {}
+        self._stage = {}
+
+    def ranges(self, key, begin, end, device):
+        import torch
+        if key not in self._ranges:
+            mine = torch.tensor([begin, end], dtype=torch.int64, device=device)
+            allr = torch.zeros(2 * self.world, dtype=torch.int64, device=device)
+            self.dist.all_gather_into_tensor(allr, mine, group=self.group)
+            rr = allr.view(self.world, 2).cpu().tolist()
+            self._ranges[key] = [(int(a), int(b)) for a, b in rr]
+        return self._ranges[key]
+
+    def __call__(self, key, full, begin, end):
+        import torch
+        rr = self.ranges(key, begin, end, full.device)
+        width = max(b - a for a, b in rr)
+        if width == 0:
+            return
+        st = self._stage.get((key, full.device))
+        if st is None or st.numel() != width * (self.world + 1):
+            st = torch.zeros(width * (self.world + 1), dtype=full.dtype, device=full.device)
+            self._stage[(key, full.device)] = st
+        mine = st[self.world * width:(self.world + 1) * width]
+        mine[: end - begin].copy_(full[begin:end])
+        allrows = st[: self.world * width]
+        self.dist.all_gather_into_tensor(allrows, mine, group=self.group)
+        rows = allrows.view(self.world, width)
+        for g, (a, b) in enumerate(rr):
+            if g != self.rank and b > a:
+                full[a:b].copy_(rows[g, : b - a])
+
+
+class ShardedRunner:
+    """Drives one iteration as phase -> all-gather -> phase ...."""
+
+    def __init__(self, backend: ShardBackend, gather):
+        self.b = backend
+        self.gather = gather
+
+    def step(self, iters: int = 1):
+        for _ in range(iters):
+            for ph in self.b.phases():
+                self.b.run_phase(ph)
+                full, begin, end = self.b.phase_output(ph)
+                self.gather(ph, full, begin, end)
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of a library-owned device buffer."""
+
+    def __init__(self, ptr: int, length: int):
+        self.__cuda_array_interface__ = {"shape": (length,), "typestr": "<f4", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class CudaShard:
+    """ShardBackend over a cl_solver handle (ISTA or cADMM) on one GPU."""
+
+    def __init__(self, state, rank: int, world: int):
+        import torch
+        self.state = state
+        self.kind = state.KIND
+        _check(lib.cl_solver_shard(state.handle, rank, world))
+        sp = C.c_void_p()
+        _check(lib.cl_solver_stream(state.handle, C.byref(sp)))
+        self.stream = torch.cuda.ExternalStream(sp.value)
+        self._views = {}
+
+    def phases(self):
+        return (0, 1) if self.kind == 0 else (0, 1, 2)
+
+    def run_phase(self, phase: int):
+        _check(lib.cl_solver_run_phase(self.state.handle, phase))
+
+    def phase_output(self, phase: int):
+        import torch
+        ptr = C.c_void_p()
+        b, e, tot = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(lib.cl_solver_phase_output(self.state.handle, phase, C.byref(ptr), C.byref(b), C.byref(e),
+                                          C.byref(tot)))
+        key = (ptr.value, tot.value)
+        if key not in self._views:
+            self._views[key] = torch.as_tensor(_CudaArray(ptr.value, tot.value), device="cuda")
+        return self._views[key], b.value, e.value
+
+
+def sharded_step(shard: CudaShard, gather: TorchGather, iters: int = 1):
+    """Advance a CudaShard `iters` iterations; collectives run on the solver's stream."""
+    import torch
+    runner = ShardedRunner(shard, gather)
+    with torch.cuda.stream(shard.stream):
+        runner.step(iters)

@@ -1,0 +1,115 @@
+"""CPU-only checks of the product library: it loads, exports the whole C-ABI,
+and its host-side parts (generation, fp64 setup transforms, validation) agree
+with the oracle.  No kernel is launched here."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_1707_02244_b200 as cl
+from paper_1707_02244_b200 import _native
+from oracle import oracle as orc
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    names = set()
+    for fn in os.listdir(os.path.join(ROOT, "include")):
+        if fn.endswith(".h"):
+            src = open(os.path.join(ROOT, "include", fn)).read()
+            src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+            names |= set(re.findall(r"\b(cl_[a-z0-9_]+)\s*\(", src))
+    return names
+
+
+def test_library_exports_every_declared_symbol():
+    names = declared_symbols()
+    assert len(names) > 30
+    missing = [n for n in sorted(names) if not hasattr(_native.lib, n)]
+    assert not missing, missing
+    assert set(_native.EXPORTED) == names
+    assert _native.lib.cl_abi_version() == 1
+
+
+def test_config_defaults_match_reference():
+    cfg = cl.SolverConfig()
+    c = cfg._c()
+    assert (c.alpha, c.tau, c.rho, c.sigma, c.tau1, c.tau2) == (1e-4, 0.0, 0.1, 0.1, 1.0, 1.0)
+    assert c.max_iter == 100000 and np.isnan(c.target_mse) and c.check_every == 10 and c.pairing == 0
+
+
+@pytest.mark.parametrize("n,m,k,seed", [(128, 64, 12, 9), (97, 48, 9, 3), (4096, 1024, 64, 1), (1 << 14, 1 << 12, 64, 7)])
+def test_make_problem_bit_exact_with_oracle(n, m, k, seed):
+    a = cl.make_problem(n, m, k, seed)
+    b = orc.make_problem(n, m, k, seed)
+    assert np.array_equal(a.op.circulant().first_row(), b.row)
+    assert np.array_equal(a.op.mask().omega(), b.omega)
+    assert np.array_equal(a.signal.values, b.x_true)
+    assert np.array_equal(a.signal.support, b.support)
+    # y is DFT-evaluated in fp64 by both (different FFTs): tolerance, as the reference's own tests
+    assert np.max(np.abs(a.measurements - b.y)) <= 1e-12 * max(1.0, np.max(np.abs(b.y)))
+
+
+def test_star_field_and_blur_bit_exact():
+    assert np.array_equal(cl.gen_star_field(64, 64, 0.1, 21), orc.gen_star_field(64, 64, 0.1, 21))
+    assert np.array_equal(cl.blur_matrix(16, 5).first_row(), orc.blur_row(16, 5))
+    with pytest.raises(cl.ParameterError):
+        cl.blur_matrix(8, 9)
+    with pytest.raises(cl.ParameterError):
+        cl.gen_star_field(8, 8, 1.5, 1)
+
+
+@pytest.mark.parametrize("n", [2, 8, 17, 97, 256, 4096])
+def test_setup_transforms_match_oracle(n):
+    row = orc.rng_draws(800 + n, "normal", n)
+    C = cl.CirculantMatrix(row)
+    assert abs(cl.spectral_norm(C) - orc.spectral_norm(row)) <= 1e-12 * orc.spectral_norm(row)
+    b = cl.regularized_gram_inverse(C, 0.1, 0.1).first_row()
+    assert np.max(np.abs(b - orc.regularized_gram_inverse(row, 0.1, 0.1))) < 1e-10
+    row2 = orc.rng_draws(900 + n, "normal", n)
+    comp = cl.compose_sensing(C, cl.CirculantMatrix(row2), cl.SubsamplingMask.Full(n))
+    assert np.max(np.abs(comp.circulant().first_row() - orc.circ_compose(row, row2))) < 1e-10
+
+
+def test_setup_errors_mirror_reference(kats):
+    k = kats["gram_singular"]
+    with pytest.raises(cl.SingularityError):
+        cl.regularized_gram_inverse(cl.CirculantMatrix(k["row"]), k["rho"], k["sigma_singular"])
+    with pytest.raises(cl.ParameterError):
+        cl.regularized_gram_inverse(cl.CirculantMatrix(k["row"]), 0.0, 0.0)
+    k = kats["mask_gram_inverse"]
+    d = cl.mask_gram_inverse(cl.SubsamplingMask(k["omega"], k["n"]), k["rho"]).diag()
+    assert np.allclose(d, k["d"], rtol=1e-15)
+    with pytest.raises(cl.ParameterError):
+        cl.SubsamplingMask([4, 1], 8)
+    with pytest.raises(cl.ParameterError):
+        cl.SubsamplingMask([1, 8], 8)
+
+
+def test_solver_validation_before_device():
+    """ista_setup / cadmm_setup raise exactly where the reference does, before any device work."""
+    p = cl.make_problem(32, 16, 3, 13)
+    for kw in ({"tau": 1.5}, {"tau": -0.2}, {"alpha": 0.0}):
+        with pytest.raises(cl.ParameterError):
+            cl.ista_setup(p.op, p.measurements, cl.SolverConfig(**kw))
+    for kw in ({"alpha": 0.0}, {"rho": 0.0}, {"sigma": 0.0}, {"tau1": 1.7}, {"tau2": 0.0}):
+        with pytest.raises(cl.ParameterError):
+            cl.cadmm_setup(p.op, p.measurements, cl.SolverConfig(**kw))
+    with pytest.raises(cl.DimensionError):
+        cl.ista_setup(p.op, np.zeros(15))
+    bad = p.measurements.copy()
+    bad[3] = np.nan
+    with pytest.raises(cl.DivergenceError):
+        cl.ista_setup(p.op, bad)
+    Z = cl.PartialCirculantOperator(cl.CirculantMatrix(np.zeros(16)), cl.SubsamplingMask.Full(16))
+    with pytest.raises(cl.SingularityError):
+        cl.cadmm_setup(Z, orc.rng_draws(15, "normal", 16))
+
+
+def test_analytic_footprint():
+    n18 = 1 << 18
+    assert cl.analytic_footprint(cl.FootprintKind.kCpista, n18, n18 // 2, 4) == 4 * n18 * 4
+    assert cl.analytic_footprint(cl.FootprintKind.kCpadmm, 1 << 20, 1 << 19, 4) == 40 * 1024 * 1024
+    assert cl.analytic_footprint(cl.FootprintKind.kDenseAdmm, 256, 128, 8) == (256 * 256 + 4 * 256 + 128) * 8
