@@ -1,18 +1,18 @@
 // Direct shift-indexed circulant kernels for sm_100a (see kernels.cuh for the
 // index algebra and the work decomposition).
 //
-// Register tiling.  A thread owns R consecutive indices.  For a block of
-// kP = 32 consecutive positions it loads an (R + kP)-float window of the
-// first row from shared memory ((R + kP) / 4 x LDS.128) and then
+// Register tiling.  A thread owns R consecutive indices.  For a block of PB
+// consecutive positions it loads an (R + PB)-float window of the first row
+// from shared memory ((R + PB) / 4 x LDS.128) and then
 //   * dense / gradient kernels (outer-product form, one broadcast scalar
-//     shared by R consecutive FFMAs):  acc[q] += w[q - s + kP] * u[s]
+//     shared by R consecutive FFMAs):  acc[q] += w[q - s + PB] * u[s]
 //   * residual kernel (dot form, rows are the outputs):
 //       out[s] = sum_q w[s - q + R] * x[q]      x[q] register-resident
 // Every register index is a compile-time constant.  The data-dependent row
-// positions (omega is a random subset, density m/n) are handled by 32
+// positions (omega is a random subset, density m/n) are handled by PB
 // statically indexed bodies per block, each behind a warp-uniform bit test of
-// the block's row mask: straight-line code, no jump table, no dynamic
-// register indexing.
+// the block's row mask (straight-line code; a jump table per row was measured
+// 1.3-1.5x slower: indirect branches are expensive on sm_100a).
 //
 // Shared memory.  Lanes own windows R floats apart; a plain layout would put
 // all 8 lanes of an LDS.128 phase in one bank group.  The staged row is padded
@@ -20,6 +20,7 @@
 // lanes of every phase over 8 distinct bank groups.
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -27,12 +28,11 @@ namespace clb {
 
 namespace {
 
-constexpr int kBlocks = kChunk / kP;  // position blocks per chunk
-static_assert(kChunk % 64 == 0 && kP == 32, "window phase logic assumes kP = 32");
+__device__ int g_force_dense = 0;  // timing experiment: treat every position as a row
 
 template <int R>
 struct Geo {
-  static_assert(R == 32 || R == 64, "R must be 32 or 64");
+  static_assert(R == 16 || R == 32 || R == 64, "R must be 16, 32 or 64");
   static constexpr int kTileR = kThreads * R;
   static constexpr int kSeg = kTileR + kChunk;
   __host__ __device__ static constexpr int pad(int e) { return e + 4 * (e / R); }
@@ -64,12 +64,13 @@ __device__ __forceinline__ void stage_segment(float* __restrict__ hs, const floa
   }
 }
 
-// Lane window w[k] = seg[x + k], k in [0, R + kP), for x a multiple of 32.
-template <int R, int PH>
-__device__ __forceinline__ void load_window_ph(float (&w)[R + kP], const float* __restrict__ p) {
+// Lane window w[k] = seg[x + k], k in [0, R + PB), x a multiple of PB whose
+// phase x mod R is PH (compile time), p = lane window origin for that phase.
+template <int R, int PB, int PH>
+__device__ __forceinline__ void load_window_ph(float (&w)[R + PB], const float* __restrict__ p) {
   using G = Geo<R>;
 #pragma unroll
-  for (int k = 0; k < R + kP; k += 4) {
+  for (int k = 0; k < R + PB; k += 4) {
     const float4 t = *reinterpret_cast<const float4*>(p + (G::pad(PH + k) - PH));
     w[k] = t.x;
     w[k + 1] = t.y;
@@ -77,32 +78,22 @@ __device__ __forceinline__ void load_window_ph(float (&w)[R + kP], const float* 
     w[k + 3] = t.w;
   }
 }
-template <int R>
-__device__ __forceinline__ void window_at(float (&w)[R + kP], const float* __restrict__ lane_base, int x) {
+template <int R, int PB>
+__device__ __forceinline__ void window_at(float (&w)[R + PB], const float* __restrict__ lane_base, int x) {
   const float* p = lane_base + (x / R) * (R + 4) + (x % R);
-  if (R == 64 && (x & 32)) load_window_ph<R, 32 % R>(w, p);
-  else load_window_ph<R, 0>(w, p);
-}
-
-// ---- outer-product body: acc[q] += w[q - S + kP] * r ----------------------
-template <int R, int S>
-__device__ __forceinline__ void grad_body(float (&acc)[R], const float (&w)[R + kP], float r) {
-#pragma unroll
-  for (int q = 0; q < R; ++q) acc[q] = fmaf(w[q - S + kP], r, acc[q]);
-}
-
-// ---- dot body: sum_q w[S - q + R] * x[q] ----------------------------------
-template <int R, int S>
-__device__ __forceinline__ float res_body(const float (&w)[R + kP], const float (&x)[R]) {
-  float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
-#pragma unroll
-  for (int q = 0; q < R; q += 4) {
-    p0 = fmaf(w[S - q + R], x[q], p0);
-    p1 = fmaf(w[S - q - 1 + R], x[q + 1], p1);
-    p2 = fmaf(w[S - q - 2 + R], x[q + 2], p2);
-    p3 = fmaf(w[S - q - 3 + R], x[q + 3], p3);
+  const int ph = x % R;
+  if (PB >= R) { load_window_ph<R, PB, 0>(w, p); return; }
+  if (R / PB == 2) {
+    if (ph) load_window_ph<R, PB, (R / 2) % R>(w, p);
+    else load_window_ph<R, PB, 0>(w, p);
+  } else {  // R / PB == 4
+    switch (ph / PB) {
+      case 1: load_window_ph<R, PB, (PB) % R>(w, p); break;
+      case 2: load_window_ph<R, PB, (2 * PB) % R>(w, p); break;
+      case 3: load_window_ph<R, PB, (3 * PB) % R>(w, p); break;
+      default: load_window_ph<R, PB, 0>(w, p); break;
+    }
   }
-  return (p0 + p1) + (p2 + p3);
 }
 
 // ===========================================================================
@@ -112,6 +103,7 @@ template <int R>
 __global__ void __launch_bounds__(kThreads, 2)
 k_conv_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, int64_t chunks, int splits,
              int64_t tile_lo, float* __restrict__ partial) {
+  constexpr int PB = 32;
   using G = Geo<R>;
   extern __shared__ float4 smem_f4[];
   float* hs = reinterpret_cast<float*>(smem_f4);
@@ -136,17 +128,17 @@ k_conv_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n
       us[s] = j < n ? __ldg(u + j) : 0.f;
     }
     __syncthreads();
-    for (int b = 0; b < kBlocks; ++b) {
-      float w[R + kP];
-      window_at<R>(w, lane_base, kChunk - (b + 1) * kP);
+    for (int b = 0; b < kChunk / PB; ++b) {
+      float w[R + PB];
+      window_at<R, PB>(w, lane_base, kChunk - (b + 1) * PB);
 #pragma unroll
-      for (int s4 = 0; s4 < kP; s4 += 4) {
-        const float4 uu = *reinterpret_cast<const float4*>(us + b * kP + s4);
+      for (int s4 = 0; s4 < PB; s4 += 4) {
+        const float4 uu = *reinterpret_cast<const float4*>(us + b * PB + s4);
         const float uv[4] = {uu.x, uu.y, uu.z, uu.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
 #pragma unroll
-          for (int q = 0; q < R; ++q) acc[q] = fmaf(w[q - (s4 + e) + kP], uv[e], acc[q]);
+          for (int q = 0; q < R; ++q) acc[q] = fmaf(w[q - (s4 + e) + PB], uv[e], acc[q]);
         }
       }
     }
@@ -162,36 +154,46 @@ k_conv_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n
 // ===========================================================================
 // Gradient A^T r: convolution with the sparse input P^T r, rows only.
 // The staged chunk holds r scattered to its positions (zeros elsewhere) and
-// a 32-bit row mask per 32-position block (a zero residual contributes
-// exactly nothing, so value != 0 is the mask).
+// a row mask per PB-position block (a zero residual contributes exactly
+// nothing, so value != 0 is the mask).
 // ===========================================================================
-template <int R, int S>
-__device__ __forceinline__ void grad_pos(float (&acc)[R], const float (&w)[R + kP], uint32_t mask, float r) {
-  if (mask & (1u << S)) grad_body<R, S>(acc, w, r);
-}
-
-template <int R, int G>
-__device__ __forceinline__ void grad_group(float (&acc)[R], const float (&w)[R + kP], uint32_t mask,
-                                           const float* __restrict__ rb) {
-  if (mask & (0xFu << (4 * G))) {
-    const float4 r4 = *reinterpret_cast<const float4*>(rb + 4 * G);
-    grad_pos<R, 4 * G>(acc, w, mask, r4.x);
-    grad_pos<R, 4 * G + 1>(acc, w, mask, r4.y);
-    grad_pos<R, 4 * G + 2>(acc, w, mask, r4.z);
-    grad_pos<R, 4 * G + 3>(acc, w, mask, r4.w);
+template <int R, int PB, int S>
+__device__ __forceinline__ void grad_pos(float (&acc)[R], const float (&w)[R + PB], uint32_t mask, float r) {
+  if (mask & (1u << S)) {
+#pragma unroll
+    for (int q = 0; q < R; ++q) acc[q] = fmaf(w[q - S + PB], r, acc[q]);
   }
 }
 
-template <int R>
-__global__ void __launch_bounds__(kThreads, 3)
+template <int R, int PB, int G>
+__device__ __forceinline__ void grad_group(float (&acc)[R], const float (&w)[R + PB], uint32_t mask,
+                                           const float* __restrict__ rb) {
+  if (G * 4 < PB && (mask & (0xFu << (4 * G)))) {
+    const float4 r4 = *reinterpret_cast<const float4*>(rb + 4 * G);
+    grad_pos<R, PB, 4 * G>(acc, w, mask, r4.x);
+    grad_pos<R, PB, 4 * G + 1>(acc, w, mask, r4.y);
+    grad_pos<R, PB, 4 * G + 2>(acc, w, mask, r4.z);
+    grad_pos<R, PB, 4 * G + 3>(acc, w, mask, r4.w);
+  }
+}
+
+// 32-lane ballot of a flag array into PB-bit masks, one per block.
+template <int PB>
+__device__ __forceinline__ uint32_t block_mask(uint32_t ballot32, int sub) {
+  return PB == 32 ? ballot32 : (ballot32 >> (sub * PB)) & ((1u << PB) - 1u);
+}
+
+template <int R, int PB, int MINB = (R <= 32 ? 3 : 2)>
+__global__ void __launch_bounds__(kThreads, MINB)
 k_conv_rows(const float* __restrict__ h, const int* __restrict__ omega, const float* __restrict__ rv,
             const int* __restrict__ rowstart, int64_t n, int64_t chunks, int splits, int64_t tile_lo,
             float* __restrict__ partial) {
+  constexpr int NB = kChunk / PB;
   using Gm = Geo<R>;
   extern __shared__ float4 smem_f4[];
   float* hs = reinterpret_cast<float*>(smem_f4);
   float* rd = hs + Gm::kSegPhys;                                   // [kChunk] r scattered
-  uint32_t* bmask = reinterpret_cast<uint32_t*>(rd + kChunk);      // [kBlocks]
+  uint32_t* bmask = reinterpret_cast<uint32_t*>(rd + kChunk);      // [NB]
   const int64_t unit = blockIdx.x;
   const int64_t tile = tile_lo + unit / splits;
   const int split = static_cast<int>(unit % splits);
@@ -213,25 +215,96 @@ k_conv_rows(const float* __restrict__ h, const int* __restrict__ omega, const fl
     __syncthreads();
     for (int k = threadIdx.x; k < nr; k += kThreads) rd[omega[r0 + k] - static_cast<int>(Jc)] = __ldg(rv + r0 + k);
     __syncthreads();
-    for (int b = warp; b < kBlocks; b += kWarps) {
-      const uint32_t mk = __ballot_sync(0xffffffffu, rd[b * kP + lane] != 0.f);
-      if (lane == 0) bmask[b] = mk;
+    for (int b32 = warp; b32 < kChunk / 32; b32 += kWarps) {
+      const uint32_t mk = g_force_dense ? 0xffffffffu : __ballot_sync(0xffffffffu, rd[b32 * 32 + lane] != 0.f);
+      if (lane == 0)
+        for (int sub = 0; sub < 32 / PB; ++sub) bmask[b32 * (32 / PB) + sub] = block_mask<PB>(mk, sub);
     }
     __syncthreads();
-    for (int b = 0; b < kBlocks; ++b) {
+    for (int b = 0; b < NB; ++b) {
       const uint32_t mask = bmask[b];
       if (mask == 0u) continue;
-      float w[R + kP];
-      window_at<R>(w, lane_base, kChunk - (b + 1) * kP);
-      const float* rb = rd + b * kP;
-      grad_group<R, 0>(acc, w, mask, rb);
-      grad_group<R, 1>(acc, w, mask, rb);
-      grad_group<R, 2>(acc, w, mask, rb);
-      grad_group<R, 3>(acc, w, mask, rb);
-      grad_group<R, 4>(acc, w, mask, rb);
-      grad_group<R, 5>(acc, w, mask, rb);
-      grad_group<R, 6>(acc, w, mask, rb);
-      grad_group<R, 7>(acc, w, mask, rb);
+      float w[R + PB];
+      window_at<R, PB>(w, lane_base, kChunk - (b + 1) * PB);
+      const float* rb = rd + b * PB;
+      grad_group<R, PB, 0>(acc, w, mask, rb);
+      grad_group<R, PB, 1>(acc, w, mask, rb);
+      grad_group<R, PB, 2>(acc, w, mask, rb);
+      grad_group<R, PB, 3>(acc, w, mask, rb);
+      grad_group<R, PB, 4>(acc, w, mask, rb);
+      grad_group<R, PB, 5>(acc, w, mask, rb);
+      grad_group<R, PB, 6>(acc, w, mask, rb);
+      grad_group<R, PB, 7>(acc, w, mask, rb);
+    }
+    __syncthreads();
+  }
+  const int64_t ib = I0 + own * R;
+  float* out = partial + static_cast<int64_t>(split) * n;
+#pragma unroll
+  for (int q = 0; q < R; ++q)
+    if (ib + q < n) out[ib + q] = acc[q];
+}
+
+
+// Out-of-line layout of the 32 position bodies (R = 32, PB = 32): the common
+// case (position not a row) falls through its test; a row costs a jump to its
+// body and a jump back.
+#define CLB_T(S) if (mask & (1u << S)) goto body##S; ret##S:
+#define CLB_B(S)                                                        \
+  body##S : {                                                           \
+    const float r = rb[S];                                              \
+    _Pragma("unroll") for (int q = 0; q < 32; ++q) acc[q] = fmaf(w[q - S + 32], r, acc[q]); \
+  }                                                                     \
+  goto ret##S;
+#define CLB_ALL32(M) M(0) M(1) M(2) M(3) M(4) M(5) M(6) M(7) M(8) M(9) M(10) M(11) M(12) M(13) M(14) M(15) \
+  M(16) M(17) M(18) M(19) M(20) M(21) M(22) M(23) M(24) M(25) M(26) M(27) M(28) M(29) M(30) M(31)
+
+__global__ void __launch_bounds__(kThreads, 4)
+k_conv_rows_ool(const float* __restrict__ h, const int* __restrict__ omega, const float* __restrict__ rv,
+                const int* __restrict__ rowstart, int64_t n, int64_t chunks, int splits, int64_t tile_lo,
+                float* __restrict__ partial) {
+  constexpr int R = 32, PB = 32, NB = kChunk / PB;
+  using Gm = Geo<R>;
+  extern __shared__ float4 smem_f4[];
+  float* hs = reinterpret_cast<float*>(smem_f4);
+  float* rd = hs + Gm::kSegPhys;
+  uint32_t* bmask = reinterpret_cast<uint32_t*>(rd + kChunk);
+  const int64_t unit = blockIdx.x;
+  const int64_t tile = tile_lo + unit / splits;
+  const int split = static_cast<int>(unit % splits);
+  const int64_t I0 = tile * Gm::kTileR;
+  const int64_t c0 = split * chunks / splits, c1 = (split + 1) * chunks / splits;
+  const int own = threadIdx.x, warp = own >> 5, lane = own & 31;
+  const float* lane_base = hs + own * Gm::kPitch;
+
+  float acc[R];
+#pragma unroll
+  for (int q = 0; q < R; ++q) acc[q] = 0.f;
+
+  for (int64_t ch = c0; ch < c1; ++ch) {
+    const int64_t Jc = ch * kChunk;
+    const int r0 = rowstart[ch], nr = rowstart[ch + 1] - r0;
+    if (nr == 0) continue;
+    stage_segment<R>(hs, h, n, I0 - Jc - kChunk);
+    for (int s = threadIdx.x; s < kChunk; s += kThreads) rd[s] = 0.f;
+    __syncthreads();
+    for (int k = threadIdx.x; k < nr; k += kThreads) rd[omega[r0 + k] - static_cast<int>(Jc)] = __ldg(rv + r0 + k);
+    __syncthreads();
+    for (int b32 = warp; b32 < kChunk / 32; b32 += kWarps) {
+      const uint32_t mk = g_force_dense ? 0xffffffffu : __ballot_sync(0xffffffffu, rd[b32 * 32 + lane] != 0.f);
+      if (lane == 0) bmask[b32] = mk;
+    }
+    __syncthreads();
+    for (int b = 0; b < NB; ++b) {
+      const uint32_t mask = bmask[b];
+      if (mask == 0u) continue;
+      float w[R + PB];
+      window_at<R, PB>(w, lane_base, kChunk - (b + 1) * PB);
+      const float* rb = rd + b * PB;
+      CLB_ALL32(CLB_T)
+      goto block_done;
+      CLB_ALL32(CLB_B)
+    block_done:;
     }
     __syncthreads();
   }
@@ -247,55 +320,73 @@ k_conv_rows(const float* __restrict__ h, const int* __restrict__ omega, const fl
 // unit = (input tile, split of position chunks); partial[tile][t].
 // Per block the selected positions compute their lane-partial dots into
 // statically indexed registers; one transpose-reduce across the warp then
-// leaves lane L with the warp sum of position L, which it stores to the row's
-// slot.  Warps are combined in fixed order at the end of the chunk.
+// leaves lane L with the warp sum of position L mod PB, which it stores to
+// the row's slot.  Warps are combined in fixed order at the end of a chunk.
 // ===========================================================================
-template <int R, int S>
-__device__ __forceinline__ void res_pos(const float (&w)[R + kP], const float (&xr)[R], uint32_t mask,
-                                        float (&out)[kP]) {
-  if (mask & (1u << S)) out[S] = res_body<R, S>(w, xr);
-  else out[S] = 0.f;
-}
-
-template <int R, int G>
-__device__ __forceinline__ void res_group(const float (&w)[R + kP], const float (&xr)[R], uint32_t mask,
-                                          float (&out)[kP]) {
-  if (mask & (0xFu << (4 * G))) {
-    res_pos<R, 4 * G>(w, xr, mask, out);
-    res_pos<R, 4 * G + 1>(w, xr, mask, out);
-    res_pos<R, 4 * G + 2>(w, xr, mask, out);
-    res_pos<R, 4 * G + 3>(w, xr, mask, out);
-  } else {
-    out[4 * G] = out[4 * G + 1] = out[4 * G + 2] = out[4 * G + 3] = 0.f;
-  }
-}
-
-// After the call lane L holds sum over the warp's lanes of v[L] in v[0].
-__device__ __forceinline__ void transpose_reduce32(float (&v)[kP], int lane) {
+template <int R, int PB, int S>
+__device__ __forceinline__ void res_pos(const float (&w)[R + PB], const float (&xr)[R], uint32_t mask,
+                                        float*& lpp) {
+  if (mask & (1u << S)) {
+    float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
 #pragma unroll
-  for (int s = 16; s >= 1; s >>= 1) {
-    const bool upper = (lane & s) != 0;
-#pragma unroll
-    for (int i = 0; i < s; ++i) {
-      const float send = upper ? v[i] : v[i + s];
-      const float keep = upper ? v[i + s] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    for (int q = 0; q < R; q += 4) {
+      p0 = fmaf(w[S - q + R], xr[q], p0);
+      p1 = fmaf(w[S - q - 1 + R], xr[q + 1], p1);
+      p2 = fmaf(w[S - q - 2 + R], xr[q + 2], p2);
+      p3 = fmaf(w[S - q - 3 + R], xr[q + 3], p3);
     }
+    *lpp++ = (p0 + p1) + (p2 + p3);  // lane-major slot list: lp[lane * 33 + slot]
   }
 }
 
-template <int R>
-__global__ void __launch_bounds__(kThreads, 3)
+template <int R, int PB, int G>
+__device__ __forceinline__ void res_group(const float (&w)[R + PB], const float (&xr)[R], uint32_t mask,
+                                          float*& lpp) {
+  if (G * 4 < PB && (mask & (0xFu << (4 * G)))) {
+    res_pos<R, PB, 4 * G>(w, xr, mask, lpp);
+    res_pos<R, PB, 4 * G + 1>(w, xr, mask, lpp);
+    res_pos<R, PB, 4 * G + 2>(w, xr, mask, lpp);
+    res_pos<R, PB, 4 * G + 3>(w, xr, mask, lpp);
+  }
+}
+
+// Sums the K (<= 32) rows of lane partials lp[lane * 33 + row] over the 32
+// lanes: 4 lanes per row, 8 rows per round, fixed order.  Row sums go to
+// redw[base + row].  Conflict-free: bank = (8 part + i + row) mod 32.
+__device__ __forceinline__ void reduce_lane_partials(const float* __restrict__ lp, float* __restrict__ redw,
+                                                     int base, int K, int lane) {
+  for (int g = 0; g < K; g += 8) {
+    const int k = g + (lane >> 2), part = lane & 3;
+    float a0 = 0.f, a1 = 0.f;
+    if (k < K) {
+      const float* col = lp + (part * 8) * 33 + k;
+#pragma unroll
+      for (int i = 0; i < 8; i += 2) {
+        a0 += col[i * 33];
+        a1 += col[(i + 1) * 33];
+      }
+    }
+    float sacc = a0 + a1;
+    sacc += __shfl_xor_sync(0xffffffffu, sacc, 1);
+    sacc += __shfl_xor_sync(0xffffffffu, sacc, 2);
+    if (k < K && part == 0) redw[base + k] = sacc;
+  }
+}
+
+template <int R, int PB>
+__global__ void __launch_bounds__(kThreads, (R <= 32 ? 3 : 2))
 k_conv_residual(const float* __restrict__ h, const float* __restrict__ x, const int* __restrict__ omega,
                 const int* __restrict__ rowstart, int64_t n, int64_t m, int64_t chunks, int splits,
                 int split_lo, int split_cnt, float* __restrict__ partial) {
+  constexpr int NB = kChunk / PB;
   using Gm = Geo<R>;
   extern __shared__ float4 smem_f4[];
   float* hs = reinterpret_cast<float*>(smem_f4);
   int* flag = reinterpret_cast<int*>(hs + Gm::kSegPhys);         // [kChunk]
-  uint32_t* bmask = reinterpret_cast<uint32_t*>(flag + kChunk);  // [kBlocks]
-  int* bbase = reinterpret_cast<int*>(bmask + kBlocks);          // [kBlocks]
-  float* red = reinterpret_cast<float*>(bbase + kBlocks);        // [kWarps][kChunk]
+  uint32_t* bmask = reinterpret_cast<uint32_t*>(flag + kChunk);  // [NB]
+  int* bbase = reinterpret_cast<int*>(bmask + NB);               // [NB]
+  float* red = reinterpret_cast<float*>(bbase + NB);             // [kWarps][kChunk]
+  float* lanep = red + kWarps * kChunk;                          // [kWarps][32 lanes][33]
   const int64_t unit = blockIdx.x;
   const int64_t tile = unit / split_cnt;
   const int split = split_lo + static_cast<int>(unit % split_cnt);
@@ -304,6 +395,8 @@ k_conv_residual(const float* __restrict__ h, const float* __restrict__ x, const 
   const int own = threadIdx.x, warp = own >> 5, lane = own & 31;
   const float* lane_base = hs + (kThreads - 1 - own) * Gm::kPitch;
   float* redw = red + warp * kChunk;
+  float* lp = lanep + warp * 32 * 33;
+  float* const lp_lane = lp + lane * 33;
 
   float xr[R];
   const int64_t jb = I0 + own * R;
@@ -321,32 +414,37 @@ k_conv_residual(const float* __restrict__ h, const float* __restrict__ x, const 
     __syncthreads();
     if (warp == 0) {  // masks + exclusive prefix of row counts per block
       int run = 0;
-      for (int b = 0; b < kBlocks; ++b) {
-        const uint32_t mk = __ballot_sync(0xffffffffu, flag[b * kP + lane] != 0);
+      for (int b32 = 0; b32 < kChunk / 32; ++b32) {
+        const uint32_t mk = g_force_dense ? 0xffffffffu : __ballot_sync(0xffffffffu, flag[b32 * 32 + lane] != 0);
         if (lane == 0) {
-          bmask[b] = mk;
-          bbase[b] = run;
+          for (int sub = 0; sub < 32 / PB; ++sub) {
+            const uint32_t bm = block_mask<PB>(mk, sub);
+            bmask[b32 * (32 / PB) + sub] = bm;
+            bbase[b32 * (32 / PB) + sub] = run;
+            run += __popc(bm);
+          }
         }
-        run += __popc(mk);
+        run = __shfl_sync(0xffffffffu, run, 0);
       }
     }
     __syncthreads();
-    for (int b = 0; b < kBlocks; ++b) {
-      const uint32_t mask = bmask[b];
+    for (int b = 0; b < NB; ++b) {
+      const uint32_t mask = __reduce_or_sync(0xffffffffu, bmask[b]);  // REDUX: uniform register -> uniform branches
       if (mask == 0u) continue;
-      float w[R + kP];
-      window_at<R>(w, lane_base, b * kP);
-      float out[kP];
-      res_group<R, 0>(w, xr, mask, out);
-      res_group<R, 1>(w, xr, mask, out);
-      res_group<R, 2>(w, xr, mask, out);
-      res_group<R, 3>(w, xr, mask, out);
-      res_group<R, 4>(w, xr, mask, out);
-      res_group<R, 5>(w, xr, mask, out);
-      res_group<R, 6>(w, xr, mask, out);
-      res_group<R, 7>(w, xr, mask, out);
-      transpose_reduce32(out, lane);
-      if (mask & (1u << lane)) redw[bbase[b] + __popc(mask & ((1u << lane) - 1u))] = out[0];
+      float w[R + PB];
+      window_at<R, PB>(w, lane_base, b * PB);
+      float* lpp = lp_lane;
+      res_group<R, PB, 0>(w, xr, mask, lpp);
+      res_group<R, PB, 1>(w, xr, mask, lpp);
+      res_group<R, PB, 2>(w, xr, mask, lpp);
+      res_group<R, PB, 3>(w, xr, mask, lpp);
+      res_group<R, PB, 4>(w, xr, mask, lpp);
+      res_group<R, PB, 5>(w, xr, mask, lpp);
+      res_group<R, PB, 6>(w, xr, mask, lpp);
+      res_group<R, PB, 7>(w, xr, mask, lpp);
+      __syncwarp();
+      reduce_lane_partials(lp, redw, bbase[b], __popc(mask), lane);
+      __syncwarp();
     }
     __syncthreads();
     float* outp = partial + tile * m + r0;
@@ -530,12 +628,47 @@ __global__ void __launch_bounds__(256) k_ffma_peak(float* out, int iters) {
 
 template <int R>
 constexpr size_t smem_dense() { return Geo<R>::kSegPhys * 4 + kChunk * 4; }
-template <int R>
-constexpr size_t smem_rows() { return Geo<R>::kSegPhys * 4 + kChunk * 4 + kBlocks * 4; }
-template <int R>
-constexpr size_t smem_res() { return Geo<R>::kSegPhys * 4 + kChunk * 4 + 2 * kBlocks * 4 + kWarps * kChunk * 4; }
+template <int R, int PB>
+constexpr size_t smem_rows() { return Geo<R>::kSegPhys * 4 + kChunk * 4 + (kChunk / PB) * 4; }
+template <int R, int PB>
+constexpr size_t smem_res() {
+  return Geo<R>::kSegPhys * 4 + kChunk * 4 + 2 * (kChunk / PB) * 4 + kWarps * kChunk * 4 + kWarps * 32 * 33 * 4;
+}
+
+// Kernel variant table (CLB_GRAD / CLB_RES select an entry for experiments;
+// the defaults are the measured best on B200).
+struct GradVariant {
+  int R, PB;
+  void (*fn)(const float*, const int*, const float*, const int*, int64_t, int64_t, int, int64_t, float*);
+  size_t smem;
+};
+struct ResVariant {
+  int R, PB;
+  void (*fn)(const float*, const float*, const int*, const int*, int64_t, int64_t, int64_t, int, int, int, float*);
+  size_t smem;
+};
+const GradVariant kGrad[] = {
+    {32, 32, k_conv_rows_ool, smem_rows<32, 32>()},  // default: best measured on B200 (C3)
+    {32, 32, k_conv_rows<32, 32>, smem_rows<32, 32>()},
+    {32, 16, k_conv_rows<32, 16>, smem_rows<32, 16>()},
+    {64, 16, k_conv_rows<64, 16>, smem_rows<64, 16>()},
+    {64, 32, k_conv_rows<64, 32>, smem_rows<64, 32>()},
+    {16, 32, k_conv_rows<16, 32>, smem_rows<16, 32>()},
+    {32, 32, k_conv_rows<32, 32, 4>, smem_rows<32, 32>()},
+};
+const ResVariant kRes[] = {
+    {32, 32, k_conv_residual<32, 32>, smem_res<32, 32>()},
+    {32, 16, k_conv_residual<32, 16>, smem_res<32, 16>()},
+    {64, 16, k_conv_residual<64, 16>, smem_res<64, 16>()},
+    {64, 32, k_conv_residual<64, 32>, smem_res<64, 32>()},
+    {16, 32, k_conv_residual<16, 32>, smem_res<16, 32>()},
+};
+int g_grad = 0, g_res = 0;
 
 }  // namespace
+
+int grad_R() { conv_kernels_init(); return kGrad[g_grad].R; }
+int res_R() { conv_kernels_init(); return kRes[g_res].R; }
 
 ConvPlan make_plan(int64_t n, int R) {
   ConvPlan p;
@@ -557,10 +690,18 @@ ConvPlan make_plan(int64_t n, int R) {
 void conv_kernels_init() {
   static bool done = false;
   if (done) return;
-  cudaFuncSetAttribute(k_conv_dense<kRDense>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dense<kRDense>());
-  cudaFuncSetAttribute(k_conv_rows<kRGrad>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rows<kRGrad>());
-  cudaFuncSetAttribute(k_conv_residual<kRRes>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_res<kRRes>());
   done = true;
+  if (const char* v = getenv("CLB_FORCE_DENSE")) {
+    const int one = atoi(v);
+    cudaMemcpyToSymbol(g_force_dense, &one, sizeof(int));
+  }
+  if (const char* v = getenv("CLB_GRAD")) g_grad = atoi(v) % (int)(sizeof(kGrad) / sizeof(kGrad[0]));
+  if (const char* v = getenv("CLB_RES")) g_res = atoi(v) % (int)(sizeof(kRes) / sizeof(kRes[0]));
+  cudaFuncSetAttribute(k_conv_dense<kRDense>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dense<kRDense>());
+  for (const auto& g : kGrad)
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(g.fn), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
+  for (const auto& r : kRes)
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(r.fn), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)r.smem);
 }
 
 void launch_conv_dense(const ConvPlan& p, const float* h, const float* u, float* partial, cudaStream_t st) {
@@ -574,8 +715,9 @@ void launch_conv_rows(const ConvPlan& p, const float* h, const int* omega32, con
                       float* partial, cudaStream_t st) {
   const int64_t units = (p.tile_hi - p.tile_lo) * p.splits;
   if (units <= 0) return;
-  k_conv_rows<kRGrad><<<static_cast<unsigned>(units), kThreads, smem_rows<kRGrad>(), st>>>(
-      h, omega32, rvals, rowstart, p.n, p.chunks, p.splits, p.tile_lo, partial);
+  const GradVariant& g = kGrad[g_grad];
+  g.fn<<<static_cast<unsigned>(units), kThreads, g.smem, st>>>(h, omega32, rvals, rowstart, p.n, p.chunks, p.splits,
+                                                              p.tile_lo, partial);
 }
 
 void launch_conv_residual(const ConvPlan& p, int64_t m, const float* h, const float* x, const int* omega32,
@@ -583,8 +725,9 @@ void launch_conv_residual(const ConvPlan& p, int64_t m, const float* h, const fl
   const int cnt = p.split_hi - p.split_lo;
   const int64_t units = p.tiles * cnt;
   if (units <= 0) return;
-  k_conv_residual<kRRes><<<static_cast<unsigned>(units), kThreads, smem_res<kRRes>(), st>>>(
-      h, x, omega32, rowstart, p.n, m, p.chunks, p.splits, p.split_lo, cnt, partial);
+  const ResVariant& r = kRes[g_res];
+  r.fn<<<static_cast<unsigned>(units), kThreads, r.smem, st>>>(h, x, omega32, rowstart, p.n, m, p.chunks, p.splits,
+                                                              p.split_lo, cnt, partial);
 }
 
 static unsigned epi_grid(int64_t len) {

@@ -28,14 +28,15 @@ namespace clb {
 constexpr int kWarps = 4;
 constexpr int kThreads = kWarps * 32;   // 128
 constexpr int kP = 32;                  // positions per register window block
-constexpr int kChunk = 2048;            // positions per shared-memory stage
+constexpr int kChunk = 1024;            // positions per shared-memory stage
 constexpr int kTargetUnits = 1184;      // 8 x 148: split-count target (constant: G-independent)
 constexpr int kEpiBlocks = 592;         // grid of the elementwise epilogues (fixed -> deterministic metrics)
 
-// Register blocking per kernel (indices owned per thread).
+// Register blocking of the dense kernel (indices owned per thread); the
+// sparse kernels' R comes from the selected variant (grad_R(), res_R()).
 constexpr int kRDense = 64;
-constexpr int kRGrad = 32;
-constexpr int kRRes = 32;
+int grad_R();
+int res_R();
 
 struct ConvPlan {
   int64_t n = 0;

@@ -198,8 +198,8 @@ struct Solver {
     tau = tau0;
     thr = cfg.pairing == CL_PAIRING_LITERAL ? cfg.alpha : tau0 * cfg.alpha;
     init_device();
-    plan = make_plan(n, kRGrad);
-    rplan = make_plan(n, kRRes);
+    plan = make_plan(n, grad_R());
+    rplan = make_plan(n, res_R());
     const std::vector<float> cf = to_f32(c, n, scale);
     hc.alloc(static_cast<size_t>(n));
     hc.upload(cf.data(), cf.size(), st);
@@ -579,8 +579,8 @@ cl_status cl_partial_matvec(int device, int64_t n, int64_t m, const double* c, c
   s.m = m;
   s.cfg = cfg;
   s.init_device();
-  s.plan = make_plan(n, kRGrad);
-  s.rplan = make_plan(n, kRRes);
+  s.plan = make_plan(n, grad_R());
+  s.rplan = make_plan(n, res_R());
   const std::vector<float> crf = reversed(to_f32(c, n));
   s.hcr.alloc(static_cast<size_t>(n));
   s.hcr.upload(crf.data(), crf.size(), s.st);
@@ -612,7 +612,7 @@ cl_status cl_partial_transpose_matvec(int device, int64_t n, int64_t m, const do
   s.n = n;
   s.m = m;
   s.init_device();
-  s.plan = make_plan(n, kRGrad);
+  s.plan = make_plan(n, grad_R());
   const std::vector<float> cf = to_f32(c, n);
   s.hc.alloc(static_cast<size_t>(n));
   s.hc.upload(cf.data(), cf.size(), s.st);
