@@ -170,6 +170,10 @@ cl_status cl_solver_stream(cl_solver* s, void** cuda_stream);
  * ISTA: 0 = residual (local rows), 1 = gradient+update (local outputs);
  * cADMM: 0 = beta, 1 = x, 2 = duals. */
 cl_status cl_solver_run_phase(cl_solver* s, int phase);
+/* Pure host helper (no device needed): the output range [out_lo, out_hi) and,
+ * for ISTA, the residual row range [row_lo, row_hi) owned by shard `rank`. */
+cl_status cl_shard_ranges(int kind, int64_t n, int64_t m, const int64_t* omega, int rank, int world,
+                          int64_t* out_lo, int64_t* out_hi, int64_t* row_lo, int64_t* row_hi);
 /* Device pointer + [begin,end) element range of the vector a phase produced,
  * and the full vector length, for the caller's all-gather. */
 cl_status cl_solver_phase_output(cl_solver* s, int phase, void** dev_ptr, int64_t* begin,

@@ -72,6 +72,7 @@ _SIGS = {
     "cl_solver_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
     "cl_solver_run_phase": (C.c_int, [_vp, C.c_int]),
     "cl_solver_phase_output": (C.c_int, [_vp, C.c_int, C.POINTER(_vp), _i64, _i64, _i64]),
+    "cl_shard_ranges": (C.c_int, [C.c_int, C.c_int64, C.c_int64, _i64, C.c_int, C.c_int, _i64, _i64, _i64, _i64]),
     "cl_ffma_peak": (C.c_int, [C.c_int, _d]),
 }
 

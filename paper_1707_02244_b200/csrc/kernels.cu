@@ -667,8 +667,17 @@ int g_grad = 0, g_res = 0;
 
 }  // namespace
 
-int grad_R() { conv_kernels_init(); return kGrad[g_grad].R; }
-int res_R() { conv_kernels_init(); return kRes[g_res].R; }
+// Variant selection is pure host logic (no CUDA calls): shard ranges can be
+// computed on a machine without a GPU.
+static void select_variants() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  if (const char* v = getenv("CLB_GRAD")) g_grad = atoi(v) % (int)(sizeof(kGrad) / sizeof(kGrad[0]));
+  if (const char* v = getenv("CLB_RES")) g_res = atoi(v) % (int)(sizeof(kRes) / sizeof(kRes[0]));
+}
+int grad_R() { select_variants(); return kGrad[g_grad].R; }
+int res_R() { select_variants(); return kRes[g_res].R; }
 
 ConvPlan make_plan(int64_t n, int R) {
   ConvPlan p;
@@ -695,8 +704,7 @@ void conv_kernels_init() {
     const int one = atoi(v);
     cudaMemcpyToSymbol(g_force_dense, &one, sizeof(int));
   }
-  if (const char* v = getenv("CLB_GRAD")) g_grad = atoi(v) % (int)(sizeof(kGrad) / sizeof(kGrad[0]));
-  if (const char* v = getenv("CLB_RES")) g_res = atoi(v) % (int)(sizeof(kRes) / sizeof(kRes[0]));
+  select_variants();
   cudaFuncSetAttribute(k_conv_dense<kRDense>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dense<kRDense>());
   for (const auto& g : kGrad)
     cudaFuncSetAttribute(reinterpret_cast<const void*>(g.fn), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);

@@ -83,6 +83,38 @@ uint64_t footprint(int kind, int64_t n, uint64_t width) {
 
 }  // namespace
 
+// Shard g of G: tiles [g*T/G, (g+1)*T/G) of the output plan; for
+// ISTA the residual splits [g*S/G, (g+1)*S/G) and hence the rows of their
+// position chunks.  Pure host logic, shared by the solver and cl_shard_ranges.
+void shard_ranges(int kind, int64_t n, const std::vector<int>& rowstart, int rk, int ws, ConvPlan* plan,
+                  ConvPlan* rplan, int64_t* out_lo, int64_t* out_hi, int64_t* row_lo, int64_t* row_hi) {
+  if (ws < 1 || rk < 0 || rk >= ws) raise(CL_EPARAM, "cl_solver_shard: need 0 <= rank < world");
+  plan->tile_lo = plan->tiles * rk / ws;
+  plan->tile_hi = plan->tiles * (rk + 1) / ws;
+  *out_lo = std::min<int64_t>(n, plan->tile_lo * plan->tile);
+  *out_hi = std::min<int64_t>(n, plan->tile_hi * plan->tile);
+  *row_lo = *row_hi = 0;
+  if (kind == CL_KIND_ISTA) {
+    rplan->split_lo = static_cast<int>(static_cast<int64_t>(rplan->splits) * rk / ws);
+    rplan->split_hi = static_cast<int>(static_cast<int64_t>(rplan->splits) * (rk + 1) / ws);
+    const int64_t c_lo = static_cast<int64_t>(rplan->split_lo) * rplan->chunks / rplan->splits;
+    const int64_t c_hi = static_cast<int64_t>(rplan->split_hi) * rplan->chunks / rplan->splits;
+    *row_lo = rowstart[static_cast<size_t>(c_lo)];
+    *row_hi = rowstart[static_cast<size_t>(c_hi)];
+  }
+}
+
+std::vector<int> chunk_rowstart(const int64_t* omega, int64_t m, int64_t chunks) {
+  std::vector<int> rs(static_cast<size_t>(chunks + 1), 0);
+  int64_t k = 0;
+  for (int64_t c = 0; c <= chunks; ++c) {
+    const int64_t lim = c * kChunk;
+    while (k < m && omega[k] < lim) ++k;
+    rs[static_cast<size_t>(c)] = static_cast<int>(k);
+  }
+  return rs;
+}
+
 struct Solver {
   int kind = CL_KIND_ISTA;
   int device = 0;
@@ -138,13 +170,7 @@ struct Solver {
   void build_rows(const int64_t* omega) {
     std::vector<int> om(static_cast<size_t>(m));
     for (int64_t t2 = 0; t2 < m; ++t2) om[static_cast<size_t>(t2)] = static_cast<int>(omega[t2]);
-    rowstart_host.assign(static_cast<size_t>(plan.chunks + 1), 0);
-    int64_t k = 0;
-    for (int64_t c = 0; c <= plan.chunks; ++c) {
-      const int64_t lim = c * kChunk;
-      while (k < m && omega[k] < lim) ++k;
-      rowstart_host[static_cast<size_t>(c)] = static_cast<int>(k);
-    }
+    rowstart_host = chunk_rowstart(omega, m, plan.chunks);
     omega32.alloc(static_cast<size_t>(m));
     omega32.upload(om.data(), static_cast<size_t>(m), st);
     rowstart.alloc(rowstart_host.size());
@@ -152,21 +178,9 @@ struct Solver {
   }
 
   void set_shard(int rk, int ws) {
-    if (ws < 1 || rk < 0 || rk >= ws) raise(CL_EPARAM, "cl_solver_shard: need 0 <= rank < world");
     rank = rk;
     world = ws;
-    plan.tile_lo = plan.tiles * rk / ws;
-    plan.tile_hi = plan.tiles * (rk + 1) / ws;
-    out_lo = std::min<int64_t>(n, plan.tile_lo * plan.tile);
-    out_hi = std::min<int64_t>(n, plan.tile_hi * plan.tile);
-    if (kind == CL_KIND_ISTA) {
-      rplan.split_lo = static_cast<int>(static_cast<int64_t>(rplan.splits) * rk / ws);
-      rplan.split_hi = static_cast<int>(static_cast<int64_t>(rplan.splits) * (rk + 1) / ws);
-      const int64_t c_lo = static_cast<int64_t>(rplan.split_lo) * rplan.chunks / rplan.splits;
-      const int64_t c_hi = static_cast<int64_t>(rplan.split_hi) * rplan.chunks / rplan.splits;
-      row_lo = rowstart_host[static_cast<size_t>(c_lo)];
-      row_hi = rowstart_host[static_cast<size_t>(c_hi)];
-    }
+    shard_ranges(kind, n, rowstart_host, rk, ws, &plan, &rplan, &out_lo, &out_hi, &row_lo, &row_hi);
   }
 
   void setup_common(const double* c, const int64_t* omega, const double* yh, const cl_config* config) {
@@ -871,6 +885,19 @@ cl_status cl_solver_phase_output(cl_solver* h, int phase, void** dev_ptr, int64_
     *end = s.out_hi;
     *total = s.n;
   }
+  CL_GUARD_END
+}
+
+cl_status cl_shard_ranges(int kind, int64_t n, int64_t m, const int64_t* omega, int rank, int world, int64_t* out_lo,
+                          int64_t* out_hi, int64_t* row_lo, int64_t* row_hi) {
+  CL_GUARD_BEGIN
+  if (kind != CL_KIND_ISTA && kind != CL_KIND_CADMM) raise(CL_EPARAM, "cl_shard_ranges: unknown solver kind");
+  if (n < 1 || m < 0 || m > n) raise(CL_EDIM, "cl_shard_ranges: need n >= 1 and 0 <= m <= n");
+  check_mask(omega, m, n);
+  ConvPlan plan = make_plan(n, kind == CL_KIND_ISTA ? grad_R() : kRDense);
+  ConvPlan rplan = make_plan(n, res_R());
+  const std::vector<int> rs = chunk_rowstart(omega, m, plan.chunks);
+  shard_ranges(kind, n, rs, rank, world, &plan, &rplan, out_lo, out_hi, row_lo, row_hi);
   CL_GUARD_END
 }
 
