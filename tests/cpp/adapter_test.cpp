@@ -1,0 +1,92 @@
+// Drop-in check of include/circlasso_b200.hpp: reference-style C++ code
+// (mirroring /root/reference/proj/tests/solvers_test.cpp) against the C-ABI.
+// Usage: adapter_test cpu | gpu     (exit code 0 = pass)
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "circlasso_b200.hpp"
+
+namespace cl = circlasso_b200;
+
+static int failures = 0;
+#define CHECK(c)                                                    \
+  do {                                                              \
+    if (!(c)) {                                                     \
+      std::fprintf(stderr, "CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #c); \
+      ++failures;                                                   \
+    }                                                               \
+  } while (0)
+template <typename E, typename F>
+static bool throws(F f) {
+  try {
+    f();
+  } catch (const E&) {
+    return true;
+  } catch (...) {
+    return false;
+  }
+  return false;
+}
+
+static void cpu_checks() {
+  const cl::SensingProblem a = cl::make_problem(128, 64, 12, 9), b = cl::make_problem(128, 64, 12, 9);
+  CHECK(a.signal.values == b.signal.values && a.op.mask().omega() == b.op.mask().omega());
+  CHECK(a.measurements == b.measurements && a.k() == 12);
+  CHECK(cl::gen_sparse_signal(4096, 409, 1).k() == 409);
+  CHECK(std::abs(cl::spectral_norm(cl::CirculantMatrix::Identity(6)) - 1.0) < 1e-12);
+  const cl::Vector d = cl::mask_gram_inverse(cl::SubsamplingMask({0, 3}, 5), 0.25);
+  CHECK(std::abs(d[0] - 0.8) < 1e-15 && std::abs(d[1] - 4.0) < 1e-15);
+  CHECK(throws<cl::SingularityError>([] { cl::regularized_gram_inverse(cl::CirculantMatrix({1.0, 1.0}), 1.0, 0.0); }));
+  CHECK(throws<cl::ParameterError>([] { cl::SubsamplingMask({4, 1}, 8); }));
+  const cl::SensingProblem p = cl::make_problem(32, 16, 3, 13);
+  cl::SolverConfig bad;
+  bad.tau = 1.5;
+  CHECK(throws<cl::ParameterError>([&] { cl::ista_run(p.measurements, p.op, bad); }));
+  cl::SolverConfig cfg;
+  cl::Vector y = p.measurements;
+  y[3] = std::nan("");
+  CHECK(throws<cl::DivergenceError>([&] { cl::ista_run(y, p.op, cfg); }));
+  CHECK(throws<cl::DimensionError>([&] { cl::ista_run(cl::Vector(15, 0.0), p.op, cfg); }));
+}
+
+static void gpu_checks() {
+  // solvers_test.cpp:213-243 report bookkeeping
+  const cl::SensingProblem p = cl::make_problem(256, 128, 25, 17);
+  cl::SolverConfig cfg;
+  cfg.target_mse = 1e-4;
+  cfg.max_iter = 20000;
+  const cl::RecoveryReport rep = cl::cadmm_run(p.measurements, p.op, cfg, &p.signal.values);
+  CHECK(rep.reached_target && rep.metric == cl::StopMetric::kMseVsTruth && rep.final_metric <= 1e-4);
+  CHECK(!rep.mse_trace.empty() && rep.mse_trace.back().value == rep.final_metric);
+  CHECK(rep.setup_seconds <= rep.total_seconds && rep.footprint_bytes == 10 * 256 * 4);
+  // ista_step advances t; literal == proximal (solvers_test.cpp:260-275)
+  cl::IstaState st = cl::ista_setup(p.op, p.measurements, cl::SolverConfig{});
+  cl::ista_step(st);
+  cl::ista_step(st);
+  CHECK(st.t() == 2);
+  cl::SolverConfig lit, prox;
+  lit.tau = prox.tau = 0.5;
+  lit.alpha = 5e-4;
+  prox.alpha = 1e-3;
+  prox.pairing = cl::ThresholdPairing::kProximal;
+  lit.max_iter = prox.max_iter = 200;
+  CHECK(cl::ista_run(p.measurements, p.op, lit).final_x == cl::ista_run(p.measurements, p.op, prox).final_x);
+  // device products vs the fp64 measure
+  const cl::Vector ax = cl::partial_matvec(p.op, p.signal.values);
+  double err = 0, nrm = 0;
+  for (size_t i = 0; i < ax.size(); ++i) {
+    err += (ax[i] - p.measurements[i]) * (ax[i] - p.measurements[i]);
+    nrm += p.measurements[i] * p.measurements[i];
+  }
+  CHECK(std::sqrt(err / nrm) < 5e-5);
+}
+
+int main(int argc, char** argv) {
+  const std::string mode = argc > 1 ? argv[1] : "cpu";
+  cpu_checks();
+  if (mode == "gpu") gpu_checks();
+  std::printf("adapter_test %s: %s\n", mode.c_str(), failures ? "FAIL" : "PASS");
+  return failures ? 1 : 0;
+}

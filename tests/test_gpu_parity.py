@@ -221,3 +221,13 @@ def test_config3_scale_ista_vs_fft_oracle():
     o.step(3, orc.ENGINE_FFT)
     assert_parity(g.get("x"), o.get("x"), what="x")
     assert rel_l2(g.get("r"), o.get("r")) <= REL_TOL
+
+
+def test_cpp_adapter_gpu():
+    """Reference-style C++ code through include/circlasso_b200.hpp on the GPU."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1707_02244_b200", "_lib",
+                       "adapter_test")
+    out = subprocess.run([exe, "gpu"], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "PASS" in out.stdout, out.stdout + out.stderr

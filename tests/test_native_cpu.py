@@ -113,3 +113,12 @@ def test_analytic_footprint():
     assert cl.analytic_footprint(cl.FootprintKind.kCpista, n18, n18 // 2, 4) == 4 * n18 * 4
     assert cl.analytic_footprint(cl.FootprintKind.kCpadmm, 1 << 20, 1 << 19, 4) == 40 * 1024 * 1024
     assert cl.analytic_footprint(cl.FootprintKind.kDenseAdmm, 256, 128, 8) == (256 * 256 + 4 * 256 + 128) * 8
+
+
+def test_cpp_adapter_cpu_parts():
+    """The reference-style C++ drop-in (include/circlasso_b200.hpp) links and behaves on the host."""
+    import subprocess
+    exe = os.path.join(ROOT, "paper_1707_02244_b200", "_lib", "adapter_test")
+    assert os.path.exists(exe), "build the package first (make -C paper_1707_02244_b200)"
+    out = subprocess.run([exe, "cpu"], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0 and "PASS" in out.stdout, out.stdout + out.stderr
