@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define CL_ABI_VERSION 1
+#define CL_ABI_VERSION 2
 
 /* errors.hpp:18-72 — one code per exception type, plus device failures. */
 typedef enum cl_status {
@@ -46,9 +46,13 @@ typedef enum cl_status {
 typedef enum cl_pairing { CL_PAIRING_LITERAL = 0, CL_PAIRING_PROXIMAL = 1 } cl_pairing; /* solvers.hpp:83 */
 typedef enum cl_kind { CL_KIND_ISTA = 0, CL_KIND_CADMM = 1 } cl_kind;
 typedef enum cl_metric { CL_METRIC_MSE_VS_TRUTH = 0, CL_METRIC_ITERATE_CHANGE = 1 } cl_metric; /* solvers.hpp:130 */
+/* Product engine (SolverConfig::use_fft, solvers.hpp:123): the direct
+ * shift-indexed kernels (the paper's OpenCL scheme, north star) or the
+ * on-device FFT (the reference's default; power-of-two n). */
+typedef enum cl_engine { CL_ENGINE_DIRECT = 0, CL_ENGINE_FFT = 1 } cl_engine;
 
-/* SolverConfig, solvers.hpp:112-125 (dense_cap/use_fft have no meaning on
- * the direct engine and are omitted). */
+/* SolverConfig, solvers.hpp:112-125 (use_fft -> engine; dense_cap has no
+ * meaning here and is omitted). */
 typedef struct cl_config {
   double alpha;       /* l1 weight, default 1e-4 */
   double tau;         /* ISTA step, 0 = automatic 0.9 */
@@ -60,6 +64,7 @@ typedef struct cl_config {
   double target_mse;  /* NaN = never stop early */
   int32_t check_every;/* default 10 */
   int32_t pairing;    /* cl_pairing, default literal */
+  int32_t engine;     /* cl_engine, default CL_ENGINE_DIRECT */
 } cl_config;
 
 /* RecoveryReport, solvers.hpp:139-150 (final_x and the trace are returned

@@ -81,7 +81,7 @@ struct SolverConfig {
   double target_mse = std::numeric_limits<double>::quiet_NaN();
   int check_every = 10;
   ThresholdPairing pairing = ThresholdPairing::kLiteral;
-  bool use_fft = true;  // accepted for source compatibility; the direct engine always runs
+  bool use_fft = false;  // true: on-device FFT engine (power-of-two n); false: direct sm_100a kernels
   int device = 0;       // new: CUDA device of the solve
 
   cl_config c() const {
@@ -97,6 +97,7 @@ struct SolverConfig {
     k.target_mse = target_mse;
     k.check_every = check_every;
     k.pairing = pairing == ThresholdPairing::kLiteral ? CL_PAIRING_LITERAL : CL_PAIRING_PROXIMAL;
+    k.engine = use_fft ? CL_ENGINE_FFT : CL_ENGINE_DIRECT;
     return k;
   }
 };

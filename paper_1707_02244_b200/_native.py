@@ -27,7 +27,7 @@ _vp = C.c_void_p
 class cl_config(C.Structure):
     _fields_ = [("alpha", C.c_double), ("tau", C.c_double), ("rho", C.c_double), ("sigma", C.c_double),
                 ("tau1", C.c_double), ("tau2", C.c_double), ("max_iter", C.c_int64), ("target_mse", C.c_double),
-                ("check_every", C.c_int32), ("pairing", C.c_int32)]
+                ("check_every", C.c_int32), ("pairing", C.c_int32), ("engine", C.c_int32)]
 
 
 class cl_report(C.Structure):
@@ -83,5 +83,5 @@ for _name, (_res, _args) in _SIGS.items():
 
 EXPORTED = tuple(_SIGS)
 
-if lib.cl_abi_version() != 1:
+if lib.cl_abi_version() != 2:
     raise ImportError("circlasso_b200: C-ABI version mismatch")

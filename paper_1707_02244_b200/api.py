@@ -118,9 +118,14 @@ class StopMetric(enum.IntEnum):
 
 @dataclass
 class SolverConfig:
-    """solvers.hpp:112-125.  ``use_fft`` and ``dense_cap`` are accepted for
-    source compatibility; this engine always runs the direct shift-indexed
-    kernels (the reference's ``use_fft=false`` arithmetic)."""
+    """solvers.hpp:112-125.
+
+    ``use_fft`` selects the product engine.  The reference defaults to its
+    FFT engine; here the default is the direct shift-indexed sm_100a kernels
+    (the paper's scheme and the north-star path, the reference's
+    ``use_fft=false`` arithmetic); ``use_fft=True`` runs the on-device FFT
+    engine (power-of-two n).  ``dense_cap`` is accepted for source
+    compatibility (dense ADMM is out of scope)."""
     alpha: float = 1e-4
     tau: float = 0.0
     rho: float = 0.1
@@ -131,7 +136,7 @@ class SolverConfig:
     target_mse: float = float("nan")
     check_every: int = 10
     pairing: ThresholdPairing = ThresholdPairing.kLiteral
-    use_fft: bool = True
+    use_fft: bool = False
     dense_cap: int = 4096
 
     def _c(self) -> cl_config:
@@ -141,6 +146,7 @@ class SolverConfig:
         c.tau1, c.tau2 = self.tau1, self.tau2
         c.max_iter, c.target_mse = int(self.max_iter), float(self.target_mse)
         c.check_every, c.pairing = int(self.check_every), int(self.pairing)
+        c.engine = 1 if self.use_fft else 0
         return c
 
 

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include "host_common.hpp"
+#include "fft.cuh"
 #include "kernels.cuh"
 
 namespace clb {
@@ -136,6 +137,8 @@ struct Solver {
   DevBuf<float> y, r, x, delta;    // ISTA
   DevBuf<float> d, pty, z, nu, mu, v, beta;  // cADMM (x shared)
   DevBuf<float> partial, truth;
+  DevBuf<float2> chat, bhat, F0, F1;  // FFT engine: spectra of c~ (and of B), work buffers
+  bool fft = false;
   DevBuf<double> blk, met;
   double* met_host = nullptr;
   std::vector<int> rowstart_host;
@@ -178,6 +181,7 @@ struct Solver {
   }
 
   void set_shard(int rk, int ws) {
+    if (fft && ws != 1) raise(CL_EPARAM, "cl_solver_shard: the FFT engine runs unsharded (replicas only)");
     rank = rk;
     world = ws;
     shard_ranges(kind, n, rowstart_host, rk, ws, &plan, &rplan, &out_lo, &out_hi, &row_lo, &row_hi);
@@ -187,6 +191,10 @@ struct Solver {
     if (!config) raise(CL_EPARAM, "cl_solver_create: null config");
     cfg = *config;
     check_mask(omega, m, n);
+    if (cfg.engine != CL_ENGINE_DIRECT && cfg.engine != CL_ENGINE_FFT)
+      raise(CL_EPARAM, "cl_solver_create: unknown engine");
+    fft = cfg.engine == CL_ENGINE_FFT;
+    if (fft && !is_pow2(n)) raise(CL_EPARAM, "cl_solver_create: the FFT engine needs a power-of-two n");
   }
 
   // solvers.hpp:170-183
@@ -230,7 +238,22 @@ struct Solver {
     blk.alloc(kEpiBlocks * 4);
     met.alloc(4);
     set_shard(0, 1);
+    if (fft) {
+      std::vector<double> cn(static_cast<size_t>(n));
+      for (int64_t i = 0; i < n; ++i) cn[static_cast<size_t>(i)] = c[i] / scale;
+      upload_spectrum(chat, dft_real(cn.data(), n));
+      F0.alloc(static_cast<size_t>(n));
+      F1.alloc(static_cast<size_t>(n));
+    }
     CU(cudaStreamSynchronize(st));
+  }
+
+  void upload_spectrum(DevBuf<float2>& dst, const std::vector<cplx>& spec) {
+    std::vector<float2> f(spec.size());
+    for (size_t k = 0; k < spec.size(); ++k)
+      f[k] = make_float2(static_cast<float>(spec[k].real()), static_cast<float>(spec[k].imag()));
+    dst.alloc(f.size());
+    dst.upload(f.data(), f.size(), st);
   }
 
   void setup_cadmm(const double* c, const int64_t* omega, const double* yh) {  // solvers.hpp:359-395
@@ -269,6 +292,16 @@ struct Solver {
     blk.alloc(kEpiBlocks * 4);
     met.alloc(4);
     rowstart_host.assign(static_cast<size_t>(plan.chunks + 1), 0);
+    if (fft) {
+      const std::vector<cplx> cs = dft_real(cn.data(), n);
+      upload_spectrum(chat, cs);
+      // B's spectrum is real: 1 / (rho |c_k|^2 + sigma) (circulant.hpp:306-317), exact before the idft round trip
+      std::vector<cplx> bs(cs.size());
+      for (size_t k = 0; k < cs.size(); ++k) bs[k] = cplx(1.0 / (cfg.rho * std::norm(cs[k]) + cfg.sigma), 0.0);
+      upload_spectrum(bhat, bs);
+      F0.alloc(static_cast<size_t>(n));
+      F1.alloc(static_cast<size_t>(n));
+    }
     set_shard(0, 1);
     CU(cudaStreamSynchronize(st));
   }
@@ -358,8 +391,96 @@ struct Solver {
     nphase = 6;
   }
 
+  // ---- FFT engine (circ_matvec_fft / circ_transpose_matvec, circulant.hpp:236-274) ----
+  // out_real[i] = Re(idft(H^(*) . dft(u)))[i] (conj_h: C x, else C^T x), into `partial`.
+  const float2* fft_product(const float2* H, bool conj_h) {
+    const float2* X = fft_run(F0.p, F1.p, n, false, st);
+    float2* Xm = const_cast<float2*>(X);
+    launch_spec_mul(Xm, H, conj_h, n, st);
+    float2* other = Xm == F0.p ? F1.p : F0.p;
+    return fft_run(Xm, other, n, true, st);
+  }
+  void ista_fft_step(int want) {
+    mark(0);
+    launch_real_to_complex(x.p, F0.p, n, st);
+    const float2* Y = fft_product(chat.p, true);               // C x
+    launch_gather_real(Y, omega32.p, partial.p, n, m, st);      // P C x
+    mark(1);
+    EpiArgs a;
+    a.partial = partial.p;
+    a.n = m;
+    a.lo = 0;
+    a.hi = m;
+    a.y = y.p;
+    a.r = r.p;
+    launch_ista_residual_reduce(a, 1, st);
+    mark(2);
+    launch_embed_rows(r.p, omega32.p, F0.p, n, m, st);         // P^T r
+    const float2* D = fft_product(chat.p, false);              // C^T P^T r
+    launch_extract_real(D, partial.p, n, st);
+    mark(3);
+    EpiArgs b = base_args(want);
+    b.splits = 1;
+    b.x = x.p;
+    b.delta = delta.p;
+    b.tau = static_cast<float>(tau);
+    b.thr = static_cast<float>(thr);
+    launch_ista_update(b, st);
+    mark(4);
+    nphase = 4;
+  }
+  void admm_fft_step(int want) {
+    mark(0);
+    launch_real_to_complex(v.p, F0.p, n, st);
+    launch_extract_real(fft_product(chat.p, false), partial.p, n, st);  // C^T v
+    mark(1);
+    EpiArgs a = base_args(0);
+    a.splits = 1;
+    a.beta = beta.p;
+    a.z = z.p;
+    a.nu = nu.p;
+    a.rho = static_cast<float>(cfg.rho);
+    a.sigma = static_cast<float>(cfg.sigma);
+    launch_admm_beta(a, st);
+    mark(2);
+    launch_real_to_complex(beta.p, F0.p, n, st);
+    launch_extract_real(fft_product(bhat.p, true), partial.p, n, st);   // B beta
+    mark(3);
+    EpiArgs bx = base_args(0);
+    bx.splits = 1;
+    bx.x = x.p;
+    launch_admm_x(bx, st);
+    mark(4);
+    launch_real_to_complex(x.p, F0.p, n, st);
+    launch_extract_real(fft_product(chat.p, true), partial.p, n, st);   // C x
+    mark(5);
+    EpiArgs d2 = base_args(want);
+    d2.splits = 1;
+    d2.x = x.p;
+    d2.z = z.p;
+    d2.nu = nu.p;
+    d2.mu = mu.p;
+    d2.v = v.p;
+    d2.d = d.p;
+    d2.pty = pty.p;
+    d2.rho = static_cast<float>(cfg.rho);
+    d2.tau1 = static_cast<float>(cfg.tau1);
+    d2.tau2 = static_cast<float>(cfg.tau2);
+    d2.thr = static_cast<float>(thr);
+    launch_admm_duals(d2, st);
+    mark(6);
+    nphase = 6;
+  }
+
   void one_step(int want) {
     if (world != 1) raise(CL_EPARAM, "cl_solver_step: sharded solvers advance with cl_solver_run_phase");
+    if (fft) {
+      if (kind == CL_KIND_ISTA) ista_fft_step(want);
+      else admm_fft_step(want);
+      CU(cudaGetLastError());
+      ++t;
+      return;
+    }
     if (kind == CL_KIND_ISTA) {
       ista_residual();
       ista_gradient(want);
@@ -506,6 +627,7 @@ void cl_config_default(cl_config* c) {  // solvers.hpp:112-125
   c->target_mse = std::numeric_limits<double>::quiet_NaN();
   c->check_every = 10;
   c->pairing = CL_PAIRING_LITERAL;
+  c->engine = CL_ENGINE_DIRECT;
 }
 
 cl_status cl_device_count(int* count) {

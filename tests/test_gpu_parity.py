@@ -231,3 +231,50 @@ def test_cpp_adapter_gpu():
                        "adapter_test")
     out = subprocess.run([exe, "gpu"], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0 and "PASS" in out.stdout, out.stdout + out.stderr
+
+
+# --------------------------------------------------------------- FFT engine (SolverConfig.use_fft=True)
+@pytest.mark.parametrize("n,m,k,seed,iters", [(128, 64, 12, 5, 25), (4096, 1024, 64, 1, 200), (1 << 16, 1 << 14, 256, 2, 30)])
+def test_fft_engine_ista_matches_oracle(n, m, k, seed, iters):
+    p = orc.make_problem(n, m, k, seed)
+    g = cl.ista_setup(op_of(p), p.y, cl.SolverConfig(use_fft=True))
+    g.step(iters)
+    o = orc.Ista(p.row, p.omega, p.y)
+    o.step(iters, orc.ENGINE_FFT)
+    assert_parity(g.get("x"), o.get("x"), what="x")
+    assert rel_l2(g.get("r"), o.get("r")) <= REL_TOL
+
+
+@pytest.mark.parametrize("n,m,k,seed,iters", [(128, 64, 12, 5, 25), (4096, 1024, 64, 1, 200), (1 << 16, 1 << 14, 256, 2, 30)])
+def test_fft_engine_cadmm_matches_oracle(n, m, k, seed, iters):
+    p = orc.make_problem(n, m, k, seed)
+    g = cl.cadmm_setup(op_of(p), p.y, cl.SolverConfig(use_fft=True))
+    g.step(iters)
+    o = orc.Cadmm(p.row, p.omega, p.y)
+    o.step(iters, orc.ENGINE_FFT)
+    assert_parity(g.get("z"), o.get("z"), what="z")
+    for f in ("x", "v", "mu", "nu"):
+        assert rel_l2(g.get(f), o.get(f)) <= REL_TOL, f
+
+
+def test_fft_engine_matches_direct_engine_c3():
+    """Both engines on BASELINE config 3 (n = 2^20): same iterate after 5 iterations."""
+    p = orc.make_problem(1 << 20, 1 << 18, 1 << 12, 1)
+    a = cl.ista_setup(op_of(p), p.y, cl.SolverConfig(use_fft=True))
+    b = cl.ista_setup(op_of(p), p.y)
+    a.step(5)
+    b.step(5)
+    assert_parity(a.get("x"), b.get("x"), what="fft vs direct")
+
+
+def test_fft_engine_rejects_non_power_of_two():
+    p = cl.make_problem(1000, 300, 10, 1)
+    with pytest.raises(cl.ParameterError):
+        cl.ista_setup(p.op, p.measurements, cl.SolverConfig(use_fft=True))
+
+
+def test_fft_engine_protocol_recovery():
+    p = cl.make_problem(4096, 2048, 409, 1)
+    rep = cl.cadmm_run(p.measurements, p.op, cl.SolverConfig(target_mse=1e-4, max_iter=20000, use_fft=True),
+                       truth=p.signal.values)
+    assert rep.reached_target

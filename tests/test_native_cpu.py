@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     missing = [n for n in sorted(names) if not hasattr(_native.lib, n)]
     assert not missing, missing
     assert set(_native.EXPORTED) == names
-    assert _native.lib.cl_abi_version() == 1
+    assert _native.lib.cl_abi_version() == 2
 
 
 def test_config_defaults_match_reference():
@@ -38,6 +38,7 @@ def test_config_defaults_match_reference():
     c = cfg._c()
     assert (c.alpha, c.tau, c.rho, c.sigma, c.tau1, c.tau2) == (1e-4, 0.0, 0.1, 0.1, 1.0, 1.0)
     assert c.max_iter == 100000 and np.isnan(c.target_mse) and c.check_every == 10 and c.pairing == 0
+    assert c.engine == 0 and cl.SolverConfig(use_fft=True)._c().engine == 1
 
 
 @pytest.mark.parametrize("n,m,k,seed", [(128, 64, 12, 9), (97, 48, 9, 3), (4096, 1024, 64, 1), (1 << 14, 1 << 12, 64, 7)])
