@@ -6,6 +6,7 @@
 // check cadence and stopping rule.  Setup transforms are fp64 on the host
 // (host_setup.cpp); iteration state lives in HBM as fp32.
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -147,9 +148,13 @@ struct Solver {
   int nphase = 0;
   cudaEvent_t step_ev[2] = {};
   double last_step_ms = 0.0;
+  // One unchecked iteration captured as a CUDA graph (launch-bound small n and
+  // the ~30-launch FFT engine step); replayed by step().  CLB_NO_GRAPH=1 disables.
+  cudaGraphExec_t graph = nullptr;
 
   ~Solver() {
     if (st) cudaStreamSynchronize(st);
+    if (graph) cudaGraphExecDestroy(graph);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     for (auto& e : step_ev)
@@ -503,9 +508,41 @@ struct Solver {
     }
   }
 
+  bool use_graph() const {
+    static const bool off = [] {
+      const char* v = getenv("CLB_NO_GRAPH");
+      return v && v[0] == '1';
+    }();
+    return !off && world == 1 && !profile;  // per-phase event timing runs eagerly
+  }
+
+  void build_graph() {
+    if (graph) return;
+    if (graph) {
+      CU(cudaGraphExecDestroy(graph));
+      graph = nullptr;
+    }
+    const int64_t t0 = t;
+    cudaGraph_t g;
+    CU(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    one_step(0);
+    CU(cudaStreamEndCapture(st, &g));
+    CU(cudaGraphInstantiate(&graph, g, 0));
+    CU(cudaGraphDestroy(g));
+    t = t0;  // capture does not execute
+  }
+
   void step(int64_t iters) {
+    if (iters > 0 && use_graph()) build_graph();
     CU(cudaEventRecord(step_ev[0], st));
-    for (int64_t k = 0; k < iters; ++k) one_step(0);
+    for (int64_t k = 0; k < iters; ++k) {
+      if (graph) {
+        CU(cudaGraphLaunch(graph, st));
+        ++t;
+      } else {
+        one_step(0);
+      }
+    }
     CU(cudaEventRecord(step_ev[1], st));
   }
 
@@ -949,7 +986,14 @@ cl_status cl_solver_last_step_ms(cl_solver* h, double* ms) {
 
 cl_status cl_solver_profile(cl_solver* h, int enable) {
   CL_GUARD_BEGIN
-  h->impl->profile = enable != 0;
+  Solver& s = *h->impl;
+  CU(cudaSetDevice(s.device));
+  CU(cudaStreamSynchronize(s.st));
+  if (s.graph) {  // profiled steps run eagerly; drop the captured step
+    CU(cudaGraphExecDestroy(s.graph));
+    s.graph = nullptr;
+  }
+  s.profile = enable != 0;
   CL_GUARD_END
 }
 
