@@ -364,11 +364,35 @@ def make_problem(n: int, m: int, k: int, seed: int) -> SensingProblem:
     return SensingProblem(SparseSignal(xt, sup), op, y, seed)
 
 
-def gen_star_field(width: int, height: int, density: float, seed: int) -> np.ndarray:
-    """deblur.hpp:69-86 (row-major pixels)"""
+@dataclass
+class GrayImage:
+    """image.hpp:24-38 (row-major pixels in [0, 1])."""
+    width: int
+    height: int
+    pixels: np.ndarray
+
+    def size(self) -> int:
+        return self.width * self.height
+
+    def at(self, row: int, col: int) -> float:
+        return float(self.pixels[row * self.width + col])
+
+
+def make_image(width: int, height: int, values) -> GrayImage:
+    """image.hpp:41-54: clamp into [0, 1]."""
+    if width < 1 or height < 1:
+        raise ParameterError("make_image: dimensions must be positive")
+    values = _f64(values)
+    if len(values) != width * height:
+        raise DimensionError(f"make_image: dimension mismatch, {len(values)} vs {width * height}")
+    return GrayImage(width, height, np.clip(values, 0.0, 1.0))
+
+
+def gen_star_field(width: int, height: int, density: float, seed: int) -> GrayImage:
+    """deblur.hpp:69-86: floor(density n) stars at uniform positions, intensities U[0.3, 1)."""
     px = np.zeros(max(width * height, 0))
     _check(lib.cl_gen_star_field(width, height, density, seed, _pd(px)))
-    return px
+    return GrayImage(width, height, px)
 
 
 def blur_matrix(n: int, L: int) -> CirculantMatrix:
@@ -637,3 +661,56 @@ def ffma_peak_tflops(device: int = 0) -> float:
     v = C.c_double()
     _check(lib.cl_ffma_peak(device, C.byref(v)))
     return v.value
+
+
+# --------------------------------------------------------------------------- deblurring (deblur.hpp)
+
+
+@dataclass
+class DeblurResult:
+    """deblur.hpp:93-101"""
+    recovered: GrayImage
+    report: RecoveryReport
+    error_map: Optional[np.ndarray] = None
+    mse_vs_truth: float = float("nan")
+    error_map_mean: float = float("nan")
+    normalized_mse: float = float("nan")
+
+
+def deblur_recover(y, C_: CirculantMatrix, B: CirculantMatrix, mask: SubsamplingMask, width: int, height: int,
+                   cfg: SolverConfig = None, truth: Optional[GrayImage] = None, device: int = 0) -> DeblurResult:
+    """deblur.hpp:107-136: cadmm_run on A = P C B (iterate-change stopping; truth only for statistics)."""
+    cfg = cfg or SolverConfig()
+    if width < 1 or height < 1:
+        raise ParameterError("deblur_recover: dimensions must be positive")
+    A = compose_sensing(C_, B, mask)
+    if A.n() != width * height:
+        raise DimensionError(f"deblur_recover: dimension mismatch, {A.n()} vs {width * height}")
+    y = _f64(y)
+    if len(y) != A.m():
+        raise DimensionError(f"deblur_recover: dimension mismatch, {len(y)} vs {A.m()}")
+    if truth is not None and len(truth.pixels) != A.n():
+        raise DimensionError("deblur_recover: truth dimension mismatch")
+    rep = cadmm_run(y, A, cfg, None, device)
+    res = DeblurResult(recovered=make_image(width, height, rep.final_x), report=rep)
+    if truth is not None:
+        res.mse_vs_truth = mse(rep.final_x, truth.pixels)
+        mean = float(np.mean(truth.pixels))
+        scale = mean if mean > 0 else 1.0
+        res.error_map = np.abs(rep.final_x - truth.pixels) / scale
+        res.error_map_mean = float(np.mean(res.error_map))
+        res.normalized_mse = res.mse_vs_truth / (scale * scale)
+    return res
+
+
+def run_deblur_experiment(image: GrayImage, L: int, m: int, cfg: SolverConfig = None, seed: int = 1,
+                          device: int = 0) -> DeblurResult:
+    """deblur.hpp:141-156: blur (order L), sense (seeded circulant, m of n rows), recover with cADMM."""
+    n = image.size()
+    if len(image.pixels) != n:
+        raise DimensionError("run_deblur_experiment: dimension mismatch")
+    B = blur_matrix(n, L)
+    sensing = gen_circulant_sensing(n, m, seed)
+    A = compose_sensing(sensing.circulant(), B, sensing.mask())
+    y = measure(A, image.pixels)
+    return deblur_recover(y, sensing.circulant(), B, sensing.mask(), image.width, image.height, cfg, image, device)

@@ -278,3 +278,56 @@ def test_fft_engine_protocol_recovery():
     rep = cl.cadmm_run(p.measurements, p.op, cl.SolverConfig(target_mse=1e-4, max_iter=20000, use_fft=True),
                        truth=p.signal.values)
     assert rep.reached_target
+
+
+# --------------------------------------------------------------- deblurring (deblur.hpp)
+def test_deblur_order1_blur_equals_plain_recovery():
+    """tests/image_deblur_test.cpp:261-280"""
+    n = 256
+    sensing = cl.gen_circulant_sensing(n, n, 9)
+    img = cl.gen_star_field(16, 16, 0.12, 3)
+    y = cl.measure(sensing, img.pixels)
+    cfg = cl.SolverConfig(target_mse=1e-8, max_iter=30000)
+    via = cl.deblur_recover(y, sensing.circulant(), cl.blur_matrix(n, 1), sensing.mask(), 16, 16, cfg, img)
+    direct = cl.cadmm_run(y, sensing, cfg)
+    assert np.array_equal(via.report.final_x, direct.final_x) and via.report.iterations == direct.iterations
+    assert np.isfinite(via.mse_vs_truth)
+
+
+def test_deblur_black_image_and_shape_contract():
+    black = cl.GrayImage(8, 8, np.zeros(64))
+    res = cl.run_deblur_experiment(black, 3, 32, cl.SolverConfig(max_iter=30), 4)
+    assert np.all(res.recovered.pixels == 0) and res.mse_vs_truth == 0 and res.normalized_mse == 0
+    sensing = cl.gen_circulant_sensing(64, 32, 2)
+    with pytest.raises(cl.DimensionError):
+        cl.deblur_recover(np.zeros(32), sensing.circulant(), cl.blur_matrix(64, 2), sensing.mask(), 7, 8)
+    with pytest.raises(cl.ParameterError):
+        cl.deblur_recover(np.zeros(32), sensing.circulant(), cl.blur_matrix(64, 2), sensing.mask(), 0, 8)
+
+
+@pytest.mark.parametrize("use_fft", [False, True])
+def test_deblur_acceptance_64x64(use_fft):
+    """tests/acceptance.cpp:398-427: 64x64 star field, L=5, m=n/2 -> MSE <= 5e-2; control L=1, m=n -> <= 1e-6."""
+    truth = cl.gen_star_field(64, 64, 0.1, 7)
+    main = cl.run_deblur_experiment(truth, 5, 2048, cl.SolverConfig(alpha=1e-2, target_mse=1e-7, max_iter=50000,
+                                                                     use_fft=use_fft), 7)
+    control = cl.run_deblur_experiment(truth, 1, 4096, cl.SolverConfig(alpha=1e-6, target_mse=1e-8, max_iter=50000,
+                                                                        use_fft=use_fft), 7)
+    print(f"deblur 64x64 fft={use_fft}: MSE {main.mse_vs_truth:.3e} in {main.report.iterations} it; "
+          f"control {control.mse_vs_truth:.3e} in {control.report.iterations} it")
+    assert main.mse_vs_truth <= 5e-2 and control.mse_vs_truth <= 1e-6
+    assert np.all((main.recovered.pixels >= 0) & (main.recovered.pixels <= 1))
+
+
+def test_deblur_matches_oracle_iterates():
+    truth = cl.gen_star_field(24, 24, 0.08, 11)
+    n = truth.size()
+    B = cl.blur_matrix(n, 3)
+    sensing = cl.gen_circulant_sensing(n, 288, 11)
+    A = cl.compose_sensing(sensing.circulant(), B, sensing.mask())
+    y = cl.measure(A, truth.pixels)
+    g = cl.cadmm_setup(A, y, cl.SolverConfig(alpha=1e-2))
+    g.step(300)
+    o = orc.Cadmm(A.circulant().first_row(), A.mask().omega(), y, alpha=1e-2)
+    o.step(300, orc.ENGINE_PHASES)
+    assert_parity(g.get("z"), o.get("z"), what="deblur z")

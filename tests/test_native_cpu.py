@@ -54,7 +54,11 @@ def test_make_problem_bit_exact_with_oracle(n, m, k, seed):
 
 
 def test_star_field_and_blur_bit_exact():
-    assert np.array_equal(cl.gen_star_field(64, 64, 0.1, 21), orc.gen_star_field(64, 64, 0.1, 21))
+    assert np.array_equal(cl.gen_star_field(64, 64, 0.1, 21).pixels, orc.gen_star_field(64, 64, 0.1, 21))
+    img = cl.make_image(2, 2, [-1.0, 0.5, 2.0, 1.0])
+    assert np.array_equal(img.pixels, [0.0, 0.5, 1.0, 1.0])
+    with pytest.raises(cl.ParameterError):
+        cl.make_image(0, 2, [])
     assert np.array_equal(cl.blur_matrix(16, 5).first_row(), orc.blur_row(16, 5))
     with pytest.raises(cl.ParameterError):
         cl.blur_matrix(8, 9)
