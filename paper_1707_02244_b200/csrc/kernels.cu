@@ -28,6 +28,21 @@ namespace clb {
 
 namespace {
 
+// Block range [blo, bhi) (32-position blocks) of split `split`: whole chunks
+// when there are at least as many chunks as splits (large n), otherwise
+// fractions of a chunk (small n needs more CTAs than it has chunks).
+__host__ __device__ __forceinline__ void split_blocks(int64_t chunks, int splits, int split, int64_t* blo,
+                                                      int64_t* bhi) {
+  constexpr int64_t kB = kChunk / 32;
+  if (splits <= chunks) {
+    *blo = split * chunks / splits * kB;
+    *bhi = (split + 1) * chunks / splits * kB;
+  } else {
+    *blo = split * (chunks * kB) / splits;
+    *bhi = (split + 1) * (chunks * kB) / splits;
+  }
+}
+
 __device__ int g_force_dense = 0;  // timing experiment: treat every position as a row
 
 template <int R>
@@ -112,7 +127,8 @@ k_conv_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n
   const int64_t tile = tile_lo + unit / splits;
   const int split = static_cast<int>(unit % splits);
   const int64_t I0 = tile * G::kTileR;
-  const int64_t c0 = split * chunks / splits, c1 = (split + 1) * chunks / splits;
+  int64_t blo, bhi;
+  split_blocks(chunks, splits, split, &blo, &bhi);
   const int own = threadIdx.x;
   const float* lane_base = hs + own * G::kPitch;
 
@@ -120,7 +136,7 @@ k_conv_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n
 #pragma unroll
   for (int q = 0; q < R; ++q) acc[q] = 0.f;
 
-  for (int64_t ch = c0; ch < c1; ++ch) {
+  for (int64_t ch = blo / (kChunk / 32); ch * (kChunk / 32) < bhi; ++ch) {
     const int64_t Jc = ch * kChunk;
     stage_segment<R>(hs, h, n, I0 - Jc - kChunk);
     for (int s = threadIdx.x; s < kChunk; s += kThreads) {
@@ -128,7 +144,11 @@ k_conv_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n
       us[s] = j < n ? __ldg(u + j) : 0.f;
     }
     __syncthreads();
+    const int64_t bsub = 32 / (PB), cb = ch * (kChunk / 32);
+    const int b0 = static_cast<int>((blo > cb ? blo - cb : 0) * bsub);
+    const int b1 = static_cast<int>((bhi - cb < kChunk / 32 ? bhi - cb : kChunk / 32) * bsub);
     for (int b = 0; b < kChunk / PB; ++b) {
+      if (b < b0 || b >= b1) continue;  // split covers part of the chunk (small n)
       float w[R + PB];
       window_at<R, PB>(w, lane_base, kChunk - (b + 1) * PB);
 #pragma unroll
@@ -198,7 +218,8 @@ k_conv_rows(const float* __restrict__ h, const int* __restrict__ omega, const fl
   const int64_t tile = tile_lo + unit / splits;
   const int split = static_cast<int>(unit % splits);
   const int64_t I0 = tile * Gm::kTileR;
-  const int64_t c0 = split * chunks / splits, c1 = (split + 1) * chunks / splits;
+  int64_t blo, bhi;
+  split_blocks(chunks, splits, split, &blo, &bhi);
   const int own = threadIdx.x, warp = own >> 5, lane = own & 31;
   const float* lane_base = hs + own * Gm::kPitch;
 
@@ -206,7 +227,7 @@ k_conv_rows(const float* __restrict__ h, const int* __restrict__ omega, const fl
 #pragma unroll
   for (int q = 0; q < R; ++q) acc[q] = 0.f;
 
-  for (int64_t ch = c0; ch < c1; ++ch) {
+  for (int64_t ch = blo / (kChunk / 32); ch * (kChunk / 32) < bhi; ++ch) {
     const int64_t Jc = ch * kChunk;
     const int r0 = rowstart[ch], nr = rowstart[ch + 1] - r0;
     if (nr == 0) continue;  // uniform across the CTA
@@ -221,7 +242,11 @@ k_conv_rows(const float* __restrict__ h, const int* __restrict__ omega, const fl
         for (int sub = 0; sub < 32 / PB; ++sub) bmask[b32 * (32 / PB) + sub] = block_mask<PB>(mk, sub);
     }
     __syncthreads();
-    for (int b = 0; b < NB; ++b) {
+    const int64_t bsub = 32 / (PB), cb = ch * (kChunk / 32);
+    const int b0 = static_cast<int>((blo > cb ? blo - cb : 0) * bsub);
+    const int b1 = static_cast<int>((bhi - cb < kChunk / 32 ? bhi - cb : kChunk / 32) * bsub);
+    for (int b = 0; b < kChunk / PB; ++b) {
+      if (b < b0 || b >= b1) continue;  // split covers part of the chunk (small n)
       const uint32_t mask = bmask[b];
       if (mask == 0u) continue;
       float w[R + PB];
@@ -307,7 +332,8 @@ k_conv_rows_ool(const float* __restrict__ h, const int* __restrict__ omega, cons
   const int64_t tile = tile_lo + unit / splits;
   const int split = static_cast<int>(unit % splits);
   const int64_t I0 = tile * Gm::kTileR;
-  const int64_t c0 = split * chunks / splits, c1 = (split + 1) * chunks / splits;
+  int64_t blo, bhi;
+  split_blocks(chunks, splits, split, &blo, &bhi);
   const int own = threadIdx.x, warp = own >> 5, lane = own & 31;
   const float* lane_base = hs + own * Gm::kPitch;
 
@@ -315,7 +341,7 @@ k_conv_rows_ool(const float* __restrict__ h, const int* __restrict__ omega, cons
 #pragma unroll
   for (int q = 0; q < R; ++q) acc[q] = 0.f;
 
-  for (int64_t ch = c0; ch < c1; ++ch) {
+  for (int64_t ch = blo / (kChunk / 32); ch * (kChunk / 32) < bhi; ++ch) {
     const int64_t Jc = ch * kChunk;
     const int r0 = rowstart[ch], nr = rowstart[ch + 1] - r0;
     if (nr == 0) continue;
@@ -329,7 +355,11 @@ k_conv_rows_ool(const float* __restrict__ h, const int* __restrict__ omega, cons
       if (lane == 0) bmask[b32] = mk;
     }
     __syncthreads();
-    for (int b = 0; b < NB; ++b) {
+    const int64_t bsub = 32 / (PB), cb = ch * (kChunk / 32);
+    const int b0 = static_cast<int>((blo > cb ? blo - cb : 0) * bsub);
+    const int b1 = static_cast<int>((bhi - cb < kChunk / 32 ? bhi - cb : kChunk / 32) * bsub);
+    for (int b = 0; b < kChunk / PB; ++b) {
+      if (b < b0 || b >= b1) continue;  // split covers part of the chunk (small n)
       const uint32_t mask = bmask[b];
       if (mask == 0u) continue;
       float w[R + PB];
@@ -425,7 +455,8 @@ k_conv_residual(const float* __restrict__ h, const float* __restrict__ x, const 
   const int64_t tile = unit / split_cnt;
   const int split = split_lo + static_cast<int>(unit % split_cnt);
   const int64_t I0 = tile * Gm::kTileR;
-  const int64_t c0 = split * chunks / splits, c1 = (split + 1) * chunks / splits;
+  int64_t blo, bhi;
+  split_blocks(chunks, splits, split, &blo, &bhi);
   const int own = threadIdx.x, warp = own >> 5, lane = own & 31;
   const float* lane_base = hs + (kThreads - 1 - own) * Gm::kPitch;
   float* redw = red + warp * kChunk;
@@ -437,7 +468,7 @@ k_conv_residual(const float* __restrict__ h, const float* __restrict__ x, const 
 #pragma unroll
   for (int q = 0; q < R; ++q) xr[q] = (jb + q < n) ? __ldg(x + jb + q) : 0.f;
 
-  for (int64_t ch = c0; ch < c1; ++ch) {
+  for (int64_t ch = blo / (kChunk / 32); ch * (kChunk / 32) < bhi; ++ch) {
     const int64_t Jc = ch * kChunk;
     const int r0 = rowstart[ch], nr = rowstart[ch + 1] - r0;
     if (nr == 0) continue;
@@ -462,7 +493,11 @@ k_conv_residual(const float* __restrict__ h, const float* __restrict__ x, const 
       }
     }
     __syncthreads();
-    for (int b = 0; b < NB; ++b) {
+    const int64_t bsub = 32 / (PB), cb = ch * (kChunk / 32);
+    const int b0 = static_cast<int>((blo > cb ? blo - cb : 0) * bsub);
+    const int b1 = static_cast<int>((bhi - cb < kChunk / 32 ? bhi - cb : kChunk / 32) * bsub);
+    for (int b = 0; b < kChunk / PB; ++b) {
+      if (b < b0 || b >= b1) continue;  // split covers part of the chunk (small n)
       const uint32_t mask = __reduce_or_sync(0xffffffffu, bmask[b]);  // REDUX: uniform register -> uniform branches
       if (mask == 0u) continue;
       float w[R + PB];
@@ -482,689 +517,13 @@ k_conv_residual(const float* __restrict__ h, const float* __restrict__ x, const 
     }
     __syncthreads();
     float* outp = partial + tile * m + r0;
-    for (int kk = threadIdx.x; kk < nr; kk += kThreads) {
+    const int k_lo = b0 < NB ? bbase[b0] : nr;
+    const int k_hi = b1 < NB ? bbase[b1] : nr;
+    for (int kk = k_lo + threadIdx.x; kk < k_hi; kk += kThreads) {
       float s = red[kk];
 #pragma unroll
       for (int wi = 1; wi < kWarps; ++wi) s += red[wi * kChunk + kk];
       outp[kk] = s;
-    }
-    __syncthreads();
-  }
-}
-
-
-// ===========================================================================
-// FFMA2 variants (fma.rn.f32x2, sm_100+): two FMAs per issue slot.  Register
-// pairs must be 64-bit aligned, so odd/even row offsets use different
-// pairings: the gradient keeps a second accumulator set for the odd-offset
-// rows (pairs of outputs (2k+1, 2k+2)), the residual a shifted copy of x.
-// Both halve the FFMA issue count of the scalar kernels above.
-// ===========================================================================
-__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
-  unsigned long long d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;"
-      : "=l"(d)
-      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
-        "l"(*reinterpret_cast<unsigned long long*>(&c)));
-  return *reinterpret_cast<float2*>(&d);
-}
-__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
-  unsigned long long d;
-  asm("add.rn.f32x2 %0, %1, %2;"
-      : "=l"(d)
-      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
-  return *reinterpret_cast<float2*>(&d);
-}
-
-// Window as 32 aligned pairs: W[j] = (w[2j], w[2j+1]).
-__device__ __forceinline__ void load_window2(float2 (&W)[32], const float* __restrict__ p) {
-  using G = Geo<32>;
-#pragma unroll
-  for (int k = 0; k < 64; k += 4) {
-    const float4 t = *reinterpret_cast<const float4*>(p + G::pad(k));
-    W[k / 2] = make_float2(t.x, t.y);
-    W[k / 2 + 1] = make_float2(t.z, t.w);
-  }
-}
-__device__ __forceinline__ float wsel(const float2 (&W)[32], int e) { return (e & 1) ? W[e >> 1].y : W[e >> 1].x; }
-
-// Gradient body, R = 32: acc[q] += w[q - S + 32] * r.
-template <int S>
-__device__ __forceinline__ void grad2_body(float2 (&A)[16], float2 (&B)[15], const float2 (&W)[32], float r) {
-  const float2 rr = make_float2(r, r);
-  if ((S & 1) == 0) {
-#pragma unroll
-    for (int p = 0; p < 16; ++p) A[p] = ffma2(W[(2 * p - S + 32) / 2], rr, A[p]);
-  } else {
-    A[0].x = fmaf(wsel(W, 32 - S), r, A[0].x);
-    A[15].y = fmaf(wsel(W, 63 - S), r, A[15].y);
-#pragma unroll
-    for (int k = 0; k < 15; ++k) B[k] = ffma2(W[(2 * k + 1 - S + 32) / 2], rr, B[k]);
-  }
-}
-
-template <int S>
-__device__ __forceinline__ void grad2_pos(float2 (&A)[16], float2 (&B)[15], const float2 (&W)[32], uint32_t mask,
-                                          float r) {
-  if (mask & (1u << S)) grad2_body<S>(A, B, W, r);
-}
-template <int G>
-__device__ __forceinline__ void grad2_group(float2 (&A)[16], float2 (&B)[15], const float2 (&W)[32], uint32_t mask,
-                                            const float* __restrict__ rb) {
-  if (mask & (0xFu << (4 * G))) {
-    const float4 r4 = *reinterpret_cast<const float4*>(rb + 4 * G);
-    grad2_pos<4 * G>(A, B, W, mask, r4.x);
-    grad2_pos<4 * G + 1>(A, B, W, mask, r4.y);
-    grad2_pos<4 * G + 2>(A, B, W, mask, r4.z);
-    grad2_pos<4 * G + 3>(A, B, W, mask, r4.w);
-  }
-}
-
-__global__ void __launch_bounds__(kThreads, 3)
-k_conv_rows_f2(const float* __restrict__ h, const int* __restrict__ omega, const float* __restrict__ rv,
-               const int* __restrict__ rowstart, int64_t n, int64_t chunks, int splits, int64_t tile_lo,
-               float* __restrict__ partial) {
-  constexpr int R = 32, PB = 32, NB = kChunk / PB;
-  using Gm = Geo<R>;
-  extern __shared__ float4 smem_f4[];
-  float* hs = reinterpret_cast<float*>(smem_f4);
-  float* rd = hs + Gm::kSegPhys;
-  uint32_t* bmask = reinterpret_cast<uint32_t*>(rd + kChunk);
-  const int64_t unit = blockIdx.x;
-  const int64_t tile = tile_lo + unit / splits;
-  const int split = static_cast<int>(unit % splits);
-  const int64_t I0 = tile * Gm::kTileR;
-  const int64_t c0 = split * chunks / splits, c1 = (split + 1) * chunks / splits;
-  const int own = threadIdx.x, warp = own >> 5, lane = own & 31;
-  const float* lane_base = hs + own * Gm::kPitch;
-
-  float2 A[16], B[15];
-#pragma unroll
-  for (int q = 0; q < 16; ++q) A[q] = make_float2(0.f, 0.f);
-#pragma unroll
-  for (int q = 0; q < 15; ++q) B[q] = make_float2(0.f, 0.f);
-
-  for (int64_t ch = c0; ch < c1; ++ch) {
-    const int64_t Jc = ch * kChunk;
-    const int r0 = rowstart[ch], nr = rowstart[ch + 1] - r0;
-    if (nr == 0) continue;
-    stage_segment<R>(hs, h, n, I0 - Jc - kChunk);
-    for (int s = threadIdx.x; s < kChunk; s += kThreads) rd[s] = 0.f;
-    __syncthreads();
-    for (int k = threadIdx.x; k < nr; k += kThreads) rd[omega[r0 + k] - static_cast<int>(Jc)] = __ldg(rv + r0 + k);
-    __syncthreads();
-    for (int b32 = warp; b32 < kChunk / 32; b32 += kWarps) {
-      const uint32_t mk = g_force_dense == 1 ? 0xffffffffu : g_force_dense == 2 ? 0x11111111u : g_force_dense == 3 ? 0x000000ffu : __ballot_sync(0xffffffffu, rd[b32 * 32 + lane] != 0.f);
-      if (lane == 0) bmask[b32] = mk;
-    }
-    __syncthreads();
-    for (int b = 0; b < NB; ++b) {
-      const uint32_t mask = __reduce_or_sync(0xffffffffu, bmask[b]);
-      if (mask == 0u) continue;
-      float2 W[32];
-      load_window2(W, lane_base + Gm::pad(kChunk - (b + 1) * PB));
-      const float* rb = rd + b * PB;
-      grad2_group<0>(A, B, W, mask, rb);
-      grad2_group<1>(A, B, W, mask, rb);
-      grad2_group<2>(A, B, W, mask, rb);
-      grad2_group<3>(A, B, W, mask, rb);
-      grad2_group<4>(A, B, W, mask, rb);
-      grad2_group<5>(A, B, W, mask, rb);
-      grad2_group<6>(A, B, W, mask, rb);
-      grad2_group<7>(A, B, W, mask, rb);
-    }
-    __syncthreads();
-  }
-  float acc[R];
-#pragma unroll
-  for (int p = 0; p < 16; ++p) {
-    acc[2 * p] = A[p].x;
-    acc[2 * p + 1] = A[p].y;
-  }
-#pragma unroll
-  for (int k = 0; k < 15; ++k) {
-    acc[2 * k + 1] += B[k].x;
-    acc[2 * k + 2] += B[k].y;
-  }
-  const int64_t ib = I0 + own * R;
-  float* out = partial + static_cast<int64_t>(split) * n;
-#pragma unroll
-  for (int q = 0; q < R; ++q)
-    if (ib + q < n) out[ib + q] = acc[q];
-}
-
-// Residual body, R = 32: dot = sum_{q'} w[S + 1 + q'] * xrev[q'], xrev[q'] = x[31 - q'].
-// X[k] = (xrev[2k], xrev[2k+1]); XS[k] = (xrev[2k+1], xrev[2k+2]).
-template <int S>
-__device__ __forceinline__ float res2_body(const float2 (&W)[32], const float2 (&X)[16], const float2 (&XS)[15]) {
-  float2 c0 = make_float2(0.f, 0.f), c1 = c0, c2 = c0, c3 = c0;
-  if (S & 1) {
-#pragma unroll
-    for (int k = 0; k < 16; k += 4) {
-      c0 = ffma2(W[(S + 1) / 2 + k], X[k], c0);
-      c1 = ffma2(W[(S + 1) / 2 + k + 1], X[k + 1], c1);
-      c2 = ffma2(W[(S + 1) / 2 + k + 2], X[k + 2], c2);
-      c3 = ffma2(W[(S + 1) / 2 + k + 3], X[k + 3], c3);
-    }
-  } else {
-    c0.x = W[S / 2].y * X[0].x;              // q' = 0:  w[S+1] * xrev[0]
-    c0.y = W[(S + 32) / 2].x * X[15].y;      // q' = 31: w[S+32] * xrev[31]
-#pragma unroll
-    for (int k = 0; k < 15; k += 4) {
-      c1 = ffma2(W[(S + 2) / 2 + k], XS[k], c1);
-      if (k + 1 < 15) c2 = ffma2(W[(S + 2) / 2 + k + 1], XS[k + 1], c2);
-      if (k + 2 < 15) c3 = ffma2(W[(S + 2) / 2 + k + 2], XS[k + 2], c3);
-      if (k + 3 < 15) c0 = ffma2(W[(S + 2) / 2 + k + 3], XS[k + 3], c0);
-    }
-  }
-  const float2 t = fadd2(fadd2(c0, c1), fadd2(c2, c3));
-  return t.x + t.y;
-}
-
-template <int S>
-__device__ __forceinline__ void res2_pos(const float2 (&W)[32], const float2 (&X)[16], const float2 (&XS)[15],
-                                         uint32_t mask, float*& lpp) {
-  if (mask & (1u << S)) *lpp++ = res2_body<S>(W, X, XS);
-}
-template <int G>
-__device__ __forceinline__ void res2_group(const float2 (&W)[32], const float2 (&X)[16], const float2 (&XS)[15],
-                                           uint32_t mask, float*& lpp) {
-  if (mask & (0xFu << (4 * G))) {
-    res2_pos<4 * G>(W, X, XS, mask, lpp);
-    res2_pos<4 * G + 1>(W, X, XS, mask, lpp);
-    res2_pos<4 * G + 2>(W, X, XS, mask, lpp);
-    res2_pos<4 * G + 3>(W, X, XS, mask, lpp);
-  }
-}
-
-__global__ void __launch_bounds__(kThreads, 3)
-k_conv_residual_f2(const float* __restrict__ h, const float* __restrict__ x, const int* __restrict__ omega,
-                   const int* __restrict__ rowstart, int64_t n, int64_t m, int64_t chunks, int splits, int split_lo,
-                   int split_cnt, float* __restrict__ partial) {
-  constexpr int R = 32, PB = 32, NB = kChunk / PB;
-  using Gm = Geo<R>;
-  extern __shared__ float4 smem_f4[];
-  float* hs = reinterpret_cast<float*>(smem_f4);
-  int* flag = reinterpret_cast<int*>(hs + Gm::kSegPhys);
-  uint32_t* bmask = reinterpret_cast<uint32_t*>(flag + kChunk);
-  int* bbase = reinterpret_cast<int*>(bmask + NB);
-  float* red = reinterpret_cast<float*>(bbase + NB);
-  float* lanep = red + kWarps * kChunk;
-  const int64_t unit = blockIdx.x;
-  const int64_t tile = unit / split_cnt;
-  const int split = split_lo + static_cast<int>(unit % split_cnt);
-  const int64_t I0 = tile * Gm::kTileR;
-  const int64_t c0 = split * chunks / splits, c1 = (split + 1) * chunks / splits;
-  const int own = threadIdx.x, warp = own >> 5, lane = own & 31;
-  const float* lane_base = hs + (kThreads - 1 - own) * Gm::kPitch;
-  float* redw = red + warp * kChunk;
-  float* lp = lanep + warp * 32 * 33;
-  float* const lp_lane = lp + lane * 33;
-
-  float xv[R];
-  const int64_t jb = I0 + own * R;
-#pragma unroll
-  for (int q = 0; q < R; ++q) xv[q] = (jb + q < n) ? __ldg(x + jb + q) : 0.f;
-  float2 X[16], XS[15];
-#pragma unroll
-  for (int k = 0; k < 16; ++k) X[k] = make_float2(xv[R - 1 - 2 * k], xv[R - 2 - 2 * k]);
-#pragma unroll
-  for (int k = 0; k < 15; ++k) XS[k] = make_float2(xv[R - 2 - 2 * k], xv[R - 3 - 2 * k]);
-
-  for (int64_t ch = c0; ch < c1; ++ch) {
-    const int64_t Jc = ch * kChunk;
-    const int r0 = rowstart[ch], nr = rowstart[ch + 1] - r0;
-    if (nr == 0) continue;
-    stage_segment<R>(hs, h, n, Jc - I0 - Gm::kTileR);
-    for (int s = threadIdx.x; s < kChunk; s += kThreads) flag[s] = 0;
-    __syncthreads();
-    for (int k = threadIdx.x; k < nr; k += kThreads) flag[omega[r0 + k] - static_cast<int>(Jc)] = 1;
-    __syncthreads();
-    if (warp == 0) {
-      int run = 0;
-      for (int b32 = 0; b32 < NB; ++b32) {
-        const uint32_t mk = g_force_dense ? 0xffffffffu : __ballot_sync(0xffffffffu, flag[b32 * 32 + lane] != 0);
-        if (lane == 0) {
-          bmask[b32] = mk;
-          bbase[b32] = run;
-        }
-        run += __popc(mk);
-      }
-    }
-    __syncthreads();
-    for (int b = 0; b < NB; ++b) {
-      const uint32_t mask = __reduce_or_sync(0xffffffffu, bmask[b]);
-      if (mask == 0u) continue;
-      float2 W[32];
-      load_window2(W, lane_base + Gm::pad(b * PB));
-      float* lpp = lp_lane;
-      res2_group<0>(W, X, XS, mask, lpp);
-      res2_group<1>(W, X, XS, mask, lpp);
-      res2_group<2>(W, X, XS, mask, lpp);
-      res2_group<3>(W, X, XS, mask, lpp);
-      res2_group<4>(W, X, XS, mask, lpp);
-      res2_group<5>(W, X, XS, mask, lpp);
-      res2_group<6>(W, X, XS, mask, lpp);
-      res2_group<7>(W, X, XS, mask, lpp);
-      __syncwarp();
-      reduce_lane_partials(lp, redw, bbase[b], __popc(mask), lane);
-      __syncwarp();
-    }
-    __syncthreads();
-    float* outp = partial + tile * m + r0;
-    for (int kk = threadIdx.x; kk < nr; kk += kThreads) {
-      float sum = red[kk];
-#pragma unroll
-      for (int wi = 1; wi < kWarps; ++wi) sum += red[wi * kChunk + kk];
-      outp[kk] = sum;
-    }
-    __syncthreads();
-  }
-}
-
-
-// ===========================================================================
-// Ring-buffered windows (R = 32, PB = 32).  Consecutive blocks' windows
-// overlap by R floats, so each block loads only the PB new floats (8 x
-// LDS.128 instead of 16) into the half of a 64-register ring that the block
-// no longer needs.  The ring has two phases; blocks alternate between two
-// statically indexed copies of the block code.  At 1/4 row density the
-// un-ringed kernels are bound by shared-memory bandwidth (one 512-byte
-// window load per ~8 rows x 32 FFMA); the ring halves that traffic.
-// ===========================================================================
-template <int PH>
-__device__ __forceinline__ float ringw(const float (&V)[64], int k) {  // window element k at phase PH
-  return V[(k + 32 * PH) & 63];
-}
-__device__ __forceinline__ void load_half(float (&V)[64], int base_slot, const float* __restrict__ p) {
-#pragma unroll
-  for (int k = 0; k < 32; k += 4) {
-    const float4 t = *reinterpret_cast<const float4*>(p + k);
-    V[(base_slot + k) & 63] = t.x;
-    V[(base_slot + k + 1) & 63] = t.y;
-    V[(base_slot + k + 2) & 63] = t.z;
-    V[(base_slot + k + 3) & 63] = t.w;
-  }
-}
-
-template <int PH, int S>
-__device__ __forceinline__ void gring_pos(float (&acc)[32], const float (&V)[64], uint32_t mask, float r) {
-  if (mask & (1u << S)) {
-#pragma unroll
-    for (int q = 0; q < 32; ++q) acc[q] = fmaf(V[(q - S + 32 + 32 * PH) & 63], r, acc[q]);
-  }
-}
-template <int PH, int G>
-__device__ __forceinline__ void gring_group(float (&acc)[32], const float (&V)[64], uint32_t mask,
-                                            const float* __restrict__ rb) {
-  if (mask & (0xFu << (4 * G))) {
-    const float4 r4 = *reinterpret_cast<const float4*>(rb + 4 * G);
-    gring_pos<PH, 4 * G>(acc, V, mask, r4.x);
-    gring_pos<PH, 4 * G + 1>(acc, V, mask, r4.y);
-    gring_pos<PH, 4 * G + 2>(acc, V, mask, r4.z);
-    gring_pos<PH, 4 * G + 3>(acc, V, mask, r4.w);
-  }
-}
-// Gradient block b at phase PH: window w[k] = seg[X_b + k], X_b = kChunk - (b+1)*32; the
-// new half is w[0..32) -> ring slots [32 PH, 32 PH + 32).
-template <int PH>
-__device__ __forceinline__ void gring_block(float (&acc)[32], float (&V)[64], const float* __restrict__ lane_base,
-                                            const uint32_t* __restrict__ bmask, const float* __restrict__ rd, int b) {
-  using G = Geo<32>;
-  const int X = kChunk - (b + 1) * 32;
-  load_half(V, 32 * PH, lane_base + G::pad(X));
-  const uint32_t mask = __reduce_or_sync(0xffffffffu, bmask[b]);
-  if (mask == 0u) return;
-  const float* rb = rd + b * 32;
-  gring_group<PH, 0>(acc, V, mask, rb);
-  gring_group<PH, 1>(acc, V, mask, rb);
-  gring_group<PH, 2>(acc, V, mask, rb);
-  gring_group<PH, 3>(acc, V, mask, rb);
-  gring_group<PH, 4>(acc, V, mask, rb);
-  gring_group<PH, 5>(acc, V, mask, rb);
-  gring_group<PH, 6>(acc, V, mask, rb);
-  gring_group<PH, 7>(acc, V, mask, rb);
-}
-
-__global__ void __launch_bounds__(kThreads, 4)
-k_conv_rows_ring(const float* __restrict__ h, const int* __restrict__ omega, const float* __restrict__ rv,
-                 const int* __restrict__ rowstart, int64_t n, int64_t chunks, int splits, int64_t tile_lo,
-                 float* __restrict__ partial) {
-  constexpr int R = 32, NB = kChunk / 32;
-  using Gm = Geo<R>;
-  extern __shared__ float4 smem_f4[];
-  float* hs = reinterpret_cast<float*>(smem_f4);
-  float* rd = hs + Gm::kSegPhys;
-  uint32_t* bmask = reinterpret_cast<uint32_t*>(rd + kChunk);
-  const int64_t unit = blockIdx.x;
-  const int64_t tile = tile_lo + unit / splits;
-  const int split = static_cast<int>(unit % splits);
-  const int64_t I0 = tile * Gm::kTileR;
-  const int64_t c0 = split * chunks / splits, c1 = (split + 1) * chunks / splits;
-  const int own = threadIdx.x, warp = own >> 5, lane = own & 31;
-  const float* lane_base = hs + own * Gm::kPitch;
-
-  float acc[R];
-#pragma unroll
-  for (int q = 0; q < R; ++q) acc[q] = 0.f;
-
-  for (int64_t ch = c0; ch < c1; ++ch) {
-    const int64_t Jc = ch * kChunk;
-    const int r0 = rowstart[ch], nr = rowstart[ch + 1] - r0;
-    if (nr == 0) continue;
-    stage_segment<R>(hs, h, n, I0 - Jc - kChunk);
-    for (int s = threadIdx.x; s < kChunk; s += kThreads) rd[s] = 0.f;
-    __syncthreads();
-    for (int k = threadIdx.x; k < nr; k += kThreads) rd[omega[r0 + k] - static_cast<int>(Jc)] = __ldg(rv + r0 + k);
-    __syncthreads();
-    for (int b32 = warp; b32 < NB; b32 += kWarps) {
-      const uint32_t mk = g_force_dense ? 0xffffffffu : __ballot_sync(0xffffffffu, rd[b32 * 32 + lane] != 0.f);
-      if (lane == 0) bmask[b32] = mk;
-    }
-    __syncthreads();
-    float V[64];
-    // block 0 at phase 0 needs the whole window: upper half first (block -1's new half)
-    load_half(V, 32, lane_base + Gm::pad(kChunk - 32 + 32));
-    for (int b = 0; b < NB; b += 2) {
-      gring_block<0>(acc, V, lane_base, bmask, rd, b);
-      gring_block<1>(acc, V, lane_base, bmask, rd, b + 1);
-    }
-    __syncthreads();
-  }
-  const int64_t ib = I0 + own * R;
-  float* out = partial + static_cast<int64_t>(split) * n;
-#pragma unroll
-  for (int q = 0; q < R; ++q)
-    if (ib + q < n) out[ib + q] = acc[q];
-}
-
-// Residual with the ring: window w[k] = seg[X_b + k], X_b = b*32 (slides up); at phase PH
-// the new half is w[32..64) -> ring slots [32 (1 - PH), 32 (1 - PH) + 32).
-template <int PH, int S>
-__device__ __forceinline__ void rring_pos(const float (&V)[64], const float (&xr)[32], uint32_t mask,
-                                          float*& lpp) {
-  if (mask & (1u << S)) {
-    float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
-#pragma unroll
-    for (int q = 0; q < 32; q += 4) {
-      p0 = fmaf(V[(S - q + 32 + 32 * PH) & 63], xr[q], p0);
-      p1 = fmaf(V[(S - q - 1 + 32 + 32 * PH) & 63], xr[q + 1], p1);
-      p2 = fmaf(V[(S - q - 2 + 32 + 32 * PH) & 63], xr[q + 2], p2);
-      p3 = fmaf(V[(S - q - 3 + 32 + 32 * PH) & 63], xr[q + 3], p3);
-    }
-    *lpp++ = (p0 + p1) + (p2 + p3);
-  }
-}
-template <int PH, int G>
-__device__ __forceinline__ void rring_group(const float (&V)[64], const float (&xr)[32], uint32_t mask,
-                                            float*& lpp) {
-  if (mask & (0xFu << (4 * G))) {
-    rring_pos<PH, 4 * G>(V, xr, mask, lpp);
-    rring_pos<PH, 4 * G + 1>(V, xr, mask, lpp);
-    rring_pos<PH, 4 * G + 2>(V, xr, mask, lpp);
-    rring_pos<PH, 4 * G + 3>(V, xr, mask, lpp);
-  }
-}
-template <int PH>
-__device__ __forceinline__ void rring_block(float (&V)[64], const float (&xr)[32], const float* __restrict__ lane_base,
-                                            const uint32_t* __restrict__ bmask, const int* __restrict__ bbase,
-                                            float* __restrict__ lp, float* __restrict__ lp_lane,
-                                            float* __restrict__ redw, int lane, int b) {
-  using G = Geo<32>;
-  load_half(V, 32 * (1 - PH), lane_base + G::pad(b * 32 + 32));
-  const uint32_t mask = __reduce_or_sync(0xffffffffu, bmask[b]);
-  if (mask == 0u) return;
-  float* lpp = lp_lane;
-  rring_group<PH, 0>(V, xr, mask, lpp);
-  rring_group<PH, 1>(V, xr, mask, lpp);
-  rring_group<PH, 2>(V, xr, mask, lpp);
-  rring_group<PH, 3>(V, xr, mask, lpp);
-  rring_group<PH, 4>(V, xr, mask, lpp);
-  rring_group<PH, 5>(V, xr, mask, lpp);
-  rring_group<PH, 6>(V, xr, mask, lpp);
-  rring_group<PH, 7>(V, xr, mask, lpp);
-  __syncwarp();
-  reduce_lane_partials(lp, redw, bbase[b], __popc(mask), lane);
-  __syncwarp();
-}
-
-__global__ void __launch_bounds__(kThreads, 3)
-k_conv_residual_ring(const float* __restrict__ h, const float* __restrict__ x, const int* __restrict__ omega,
-                     const int* __restrict__ rowstart, int64_t n, int64_t m, int64_t chunks, int splits,
-                     int split_lo, int split_cnt, float* __restrict__ partial) {
-  constexpr int R = 32, NB = kChunk / 32;
-  using Gm = Geo<R>;
-  extern __shared__ float4 smem_f4[];
-  float* hs = reinterpret_cast<float*>(smem_f4);
-  int* flag = reinterpret_cast<int*>(hs + Gm::kSegPhys);
-  uint32_t* bmask = reinterpret_cast<uint32_t*>(flag + kChunk);
-  int* bbase = reinterpret_cast<int*>(bmask + NB);
-  float* red = reinterpret_cast<float*>(bbase + NB);
-  float* lanep = red + kWarps * kChunk;
-  const int64_t unit = blockIdx.x;
-  const int64_t tile = unit / split_cnt;
-  const int split = split_lo + static_cast<int>(unit % split_cnt);
-  const int64_t I0 = tile * Gm::kTileR;
-  const int64_t c0 = split * chunks / splits, c1 = (split + 1) * chunks / splits;
-  const int own = threadIdx.x, warp = own >> 5, lane = own & 31;
-  const float* lane_base = hs + (kThreads - 1 - own) * Gm::kPitch;
-  float* redw = red + warp * kChunk;
-  float* lp = lanep + warp * 32 * 33;
-  float* const lp_lane = lp + lane * 33;
-
-  float xr[R];
-  const int64_t jb = I0 + own * R;
-#pragma unroll
-  for (int q = 0; q < R; ++q) xr[q] = (jb + q < n) ? __ldg(x + jb + q) : 0.f;
-
-  for (int64_t ch = c0; ch < c1; ++ch) {
-    const int64_t Jc = ch * kChunk;
-    const int r0 = rowstart[ch], nr = rowstart[ch + 1] - r0;
-    if (nr == 0) continue;
-    stage_segment<R>(hs, h, n, Jc - I0 - Gm::kTileR);
-    for (int s = threadIdx.x; s < kChunk; s += kThreads) flag[s] = 0;
-    __syncthreads();
-    for (int k = threadIdx.x; k < nr; k += kThreads) flag[omega[r0 + k] - static_cast<int>(Jc)] = 1;
-    __syncthreads();
-    if (warp == 0) {
-      int run = 0;
-      for (int b32 = 0; b32 < NB; ++b32) {
-        const uint32_t mk = g_force_dense ? 0xffffffffu : __ballot_sync(0xffffffffu, flag[b32 * 32 + lane] != 0);
-        if (lane == 0) {
-          bmask[b32] = mk;
-          bbase[b32] = run;
-        }
-        run += __popc(mk);
-      }
-    }
-    __syncthreads();
-    float V[64];
-    // block 0 at phase 0: w[k] = V[k]; lower half w[0..32) = seg[0..32) loaded here
-    load_half(V, 0, lane_base);
-    for (int b = 0; b < NB; b += 2) {
-      rring_block<0>(V, xr, lane_base, bmask, bbase, lp, lp_lane, redw, lane, b);
-      rring_block<1>(V, xr, lane_base, bmask, bbase, lp, lp_lane, redw, lane, b + 1);
-    }
-    __syncthreads();
-    float* outp = partial + tile * m + r0;
-    for (int kk = threadIdx.x; kk < nr; kk += kThreads) {
-      float sum = red[kk];
-#pragma unroll
-      for (int wi = 1; wi < kWarps; ++wi) sum += red[wi * kChunk + kk];
-      outp[kk] = sum;
-    }
-    __syncthreads();
-  }
-}
-
-// Shift-window variants (R = PB = 32): the overlapping half of the window is
-// moved register-to-register (32 MOVs) and only the 32 new floats are loaded
-// (8 x LDS.128): half the shared-memory traffic with a single copy of the
-// block code (the two-phase ring doubles the code and thrashes the I-cache).
-__global__ void __launch_bounds__(kThreads, 3)
-k_conv_rows_shift(const float* __restrict__ h, const int* __restrict__ omega, const float* __restrict__ rv,
-                 const int* __restrict__ rowstart, int64_t n, int64_t chunks, int splits, int64_t tile_lo,
-                 float* __restrict__ partial) {
-  constexpr int R = 32, NB = kChunk / 32;
-  using Gm = Geo<R>;
-  extern __shared__ float4 smem_f4[];
-  float* hs = reinterpret_cast<float*>(smem_f4);
-  float* rd = hs + Gm::kSegPhys;
-  uint32_t* bmask = reinterpret_cast<uint32_t*>(rd + kChunk);
-  const int64_t unit = blockIdx.x;
-  const int64_t tile = tile_lo + unit / splits;
-  const int split = static_cast<int>(unit % splits);
-  const int64_t I0 = tile * Gm::kTileR;
-  const int64_t c0 = split * chunks / splits, c1 = (split + 1) * chunks / splits;
-  const int own = threadIdx.x, warp = own >> 5, lane = own & 31;
-  const float* lane_base = hs + own * Gm::kPitch;
-
-  float acc[R];
-#pragma unroll
-  for (int q = 0; q < R; ++q) acc[q] = 0.f;
-
-  for (int64_t ch = c0; ch < c1; ++ch) {
-    const int64_t Jc = ch * kChunk;
-    const int r0 = rowstart[ch], nr = rowstart[ch + 1] - r0;
-    if (nr == 0) continue;
-    stage_segment<R>(hs, h, n, I0 - Jc - kChunk);
-    for (int s = threadIdx.x; s < kChunk; s += kThreads) rd[s] = 0.f;
-    __syncthreads();
-    for (int k = threadIdx.x; k < nr; k += kThreads) rd[omega[r0 + k] - static_cast<int>(Jc)] = __ldg(rv + r0 + k);
-    __syncthreads();
-    for (int b32 = warp; b32 < NB; b32 += kWarps) {
-      const uint32_t mk = g_force_dense ? 0xffffffffu : __ballot_sync(0xffffffffu, rd[b32 * 32 + lane] != 0.f);
-      if (lane == 0) bmask[b32] = mk;
-    }
-    __syncthreads();
-    float w[64];
-    {  // w_0[32..64) = seg[kChunk .. kChunk + 32) goes to the low half first; shifted up at block 0
-      const float* p = lane_base + Gm::pad(kChunk);
-#pragma unroll
-      for (int k = 0; k < 32; k += 4) {
-        const float4 t = *reinterpret_cast<const float4*>(p + k);
-        w[k] = t.x; w[k + 1] = t.y; w[k + 2] = t.z; w[k + 3] = t.w;
-      }
-    }
-    for (int b = 0; b < NB; ++b) {
-#pragma unroll
-      for (int k = 32; k < 64; ++k) w[k] = w[k - 32];  // w_b[k] = w_{b-1}[k - 32]
-      const float* p = lane_base + Gm::pad(kChunk - (b + 1) * 32);
-#pragma unroll
-      for (int k = 0; k < 32; k += 4) {
-        const float4 t = *reinterpret_cast<const float4*>(p + k);
-        w[k] = t.x; w[k + 1] = t.y; w[k + 2] = t.z; w[k + 3] = t.w;
-      }
-      const uint32_t mask = __reduce_or_sync(0xffffffffu, bmask[b]);
-      if (mask == 0u) continue;
-      const float* rb = rd + b * 32;
-      grad_group<32, 32, 0>(acc, w, mask, rb);
-      grad_group<32, 32, 1>(acc, w, mask, rb);
-      grad_group<32, 32, 2>(acc, w, mask, rb);
-      grad_group<32, 32, 3>(acc, w, mask, rb);
-      grad_group<32, 32, 4>(acc, w, mask, rb);
-      grad_group<32, 32, 5>(acc, w, mask, rb);
-      grad_group<32, 32, 6>(acc, w, mask, rb);
-      grad_group<32, 32, 7>(acc, w, mask, rb);
-    }
-    __syncthreads();
-  }
-  const int64_t ib = I0 + own * R;
-  float* out = partial + static_cast<int64_t>(split) * n;
-#pragma unroll
-  for (int q = 0; q < R; ++q)
-    if (ib + q < n) out[ib + q] = acc[q];
-}
-
-__global__ void __launch_bounds__(kThreads, 3)
-k_conv_residual_shift(const float* __restrict__ h, const float* __restrict__ x, const int* __restrict__ omega,
-                     const int* __restrict__ rowstart, int64_t n, int64_t m, int64_t chunks, int splits,
-                     int split_lo, int split_cnt, float* __restrict__ partial) {
-  constexpr int R = 32, NB = kChunk / 32;
-  using Gm = Geo<R>;
-  extern __shared__ float4 smem_f4[];
-  float* hs = reinterpret_cast<float*>(smem_f4);
-  int* flag = reinterpret_cast<int*>(hs + Gm::kSegPhys);
-  uint32_t* bmask = reinterpret_cast<uint32_t*>(flag + kChunk);
-  int* bbase = reinterpret_cast<int*>(bmask + NB);
-  float* red = reinterpret_cast<float*>(bbase + NB);
-  float* lanep = red + kWarps * kChunk;
-  const int64_t unit = blockIdx.x;
-  const int64_t tile = unit / split_cnt;
-  const int split = split_lo + static_cast<int>(unit % split_cnt);
-  const int64_t I0 = tile * Gm::kTileR;
-  const int64_t c0 = split * chunks / splits, c1 = (split + 1) * chunks / splits;
-  const int own = threadIdx.x, warp = own >> 5, lane = own & 31;
-  const float* lane_base = hs + (kThreads - 1 - own) * Gm::kPitch;
-  float* redw = red + warp * kChunk;
-  float* lp = lanep + warp * 32 * 33;
-  float* const lp_lane = lp + lane * 33;
-
-  float xr[R];
-  const int64_t jb = I0 + own * R;
-#pragma unroll
-  for (int q = 0; q < R; ++q) xr[q] = (jb + q < n) ? __ldg(x + jb + q) : 0.f;
-
-  for (int64_t ch = c0; ch < c1; ++ch) {
-    const int64_t Jc = ch * kChunk;
-    const int r0 = rowstart[ch], nr = rowstart[ch + 1] - r0;
-    if (nr == 0) continue;
-    stage_segment<R>(hs, h, n, Jc - I0 - Gm::kTileR);
-    for (int s = threadIdx.x; s < kChunk; s += kThreads) flag[s] = 0;
-    __syncthreads();
-    for (int k = threadIdx.x; k < nr; k += kThreads) flag[omega[r0 + k] - static_cast<int>(Jc)] = 1;
-    __syncthreads();
-    if (warp == 0) {
-      int run = 0;
-      for (int b32 = 0; b32 < NB; ++b32) {
-        const uint32_t mk = g_force_dense ? 0xffffffffu : __ballot_sync(0xffffffffu, flag[b32 * 32 + lane] != 0);
-        if (lane == 0) {
-          bmask[b32] = mk;
-          bbase[b32] = run;
-        }
-        run += __popc(mk);
-      }
-    }
-    __syncthreads();
-    float w[64];
-    {  // w_0[0..32) = seg[0..32) goes to the high half first; shifted down at block 0
-#pragma unroll
-      for (int k = 0; k < 32; k += 4) {
-        const float4 t = *reinterpret_cast<const float4*>(lane_base + k);
-        w[32 + k] = t.x; w[33 + k] = t.y; w[34 + k] = t.z; w[35 + k] = t.w;
-      }
-    }
-    for (int b = 0; b < NB; ++b) {
-#pragma unroll
-      for (int k = 0; k < 32; ++k) w[k] = w[k + 32];  // w_b[k] = w_{b-1}[k + 32]
-      const float* p = lane_base + Gm::pad(b * 32 + 32);
-#pragma unroll
-      for (int k = 0; k < 32; k += 4) {
-        const float4 t = *reinterpret_cast<const float4*>(p + k);
-        w[32 + k] = t.x; w[33 + k] = t.y; w[34 + k] = t.z; w[35 + k] = t.w;
-      }
-      const uint32_t mask = __reduce_or_sync(0xffffffffu, bmask[b]);
-      if (mask == 0u) continue;
-      float* lpp = lp_lane;
-      res_group<32, 32, 0>(w, xr, mask, lpp);
-      res_group<32, 32, 1>(w, xr, mask, lpp);
-      res_group<32, 32, 2>(w, xr, mask, lpp);
-      res_group<32, 32, 3>(w, xr, mask, lpp);
-      res_group<32, 32, 4>(w, xr, mask, lpp);
-      res_group<32, 32, 5>(w, xr, mask, lpp);
-      res_group<32, 32, 6>(w, xr, mask, lpp);
-      res_group<32, 32, 7>(w, xr, mask, lpp);
-      __syncwarp();
-      reduce_lane_partials(lp, redw, bbase[b], __popc(mask), lane);
-      __syncwarp();
-    }
-    __syncthreads();
-    float* outp = partial + tile * m + r0;
-    for (int kk = threadIdx.x; kk < nr; kk += kThreads) {
-      float sum = red[kk];
-#pragma unroll
-      for (int wi = 1; wi < kWarps; ++wi) sum += red[wi * kChunk + kk];
-      outp[kk] = sum;
     }
     __syncthreads();
   }
@@ -1360,12 +719,9 @@ struct ResVariant {
   size_t smem;
 };
 const GradVariant kGrad[] = {
-    {32, 32, k_conv_rows_ool, smem_rows<32, 32>()},  // default: best measured on B200 (C3, 17.1 ms)
+    {32, 32, k_conv_rows_ool, smem_rows<32, 32>()},  // default: best measured on B200 (C3, 17.0 ms)
     {32, 32, k_conv_rows<32, 32, 4>, smem_rows<32, 32>()},
     {32, 32, k_conv_rows<32, 32>, smem_rows<32, 32>()},
-    {32, 32, k_conv_rows_shift, smem_rows<32, 32>()},
-    {32, 32, k_conv_rows_ring, smem_rows<32, 32>()},
-    {32, 32, k_conv_rows_f2, smem_rows<32, 32>()},
     {32, 16, k_conv_rows<32, 16>, smem_rows<32, 16>()},
     {64, 16, k_conv_rows<64, 16, 3>, smem_rows<64, 16>()},
     {64, 32, k_conv_rows<64, 32, 3>, smem_rows<64, 32>()},
@@ -1373,9 +729,6 @@ const GradVariant kGrad[] = {
 };
 const ResVariant kRes[] = {
     {32, 32, k_conv_residual<32, 32>, smem_res<32, 32>()},  // default: best measured on B200 (C3, 27.7 ms)
-    {32, 32, k_conv_residual_shift, smem_res<32, 32>()},
-    {32, 32, k_conv_residual_ring, smem_res<32, 32>()},
-    {32, 32, k_conv_residual_f2, smem_res<32, 32>()},
     {32, 16, k_conv_residual<32, 16>, smem_res<32, 16>()},
     {64, 16, k_conv_residual<64, 16>, smem_res<64, 16>()},
     {64, 32, k_conv_residual<64, 32>, smem_res<64, 32>()},
@@ -1397,6 +750,10 @@ static void select_variants() {
 int grad_R() { select_variants(); return kGrad[g_grad].R; }
 int res_R() { select_variants(); return kRes[g_res].R; }
 
+void split_block_range(const ConvPlan& p, int split, int64_t* blo, int64_t* bhi) {
+  split_blocks(p.chunks, p.splits, split, blo, bhi);
+}
+
 ConvPlan make_plan(int64_t n, int R) {
   ConvPlan p;
   p.n = n;
@@ -1404,8 +761,9 @@ ConvPlan make_plan(int64_t n, int R) {
   p.tiles = (n + p.tile - 1) / p.tile;
   p.chunks = (n + kChunk - 1) / kChunk;
   int64_t s = (kTargetUnits + p.tiles - 1) / p.tiles;
+  const int64_t blocks32 = p.chunks * (kChunk / 32);  // splits are ranges of 32-position blocks
   if (s < 1) s = 1;
-  if (s > p.chunks) s = p.chunks;
+  if (s > blocks32) s = blocks32;
   p.splits = static_cast<int>(s);
   p.tile_lo = 0;
   p.tile_hi = p.tiles;

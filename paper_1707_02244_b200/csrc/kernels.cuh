@@ -14,7 +14,8 @@
 // results are bitwise identical for any sharding):
 //   tile  = kThreads * R consecutive register-owned indices (R per thread),
 //   chunk = kChunk consecutive positions staged in shared memory,
-//   split = a contiguous range of chunks; a unit (tile, split) is one CTA.
+//   split = a contiguous range of 32-position blocks (whole chunks at large n,
+//           fractions of a chunk at small n); a unit (tile, split) is one CTA.
 // Partial sums of the splits (or of the tiles, for the residual) are combined
 // in ascending order by the epilogue kernels, which also apply the fused
 // solver updates.
@@ -49,6 +50,8 @@ struct ConvPlan {
 };
 
 ConvPlan make_plan(int64_t n, int R);
+// [blo, bhi) in 32-position blocks covered by split `split` of a plan.
+void split_block_range(const ConvPlan& p, int split, int64_t* blo, int64_t* bhi);
 
 // Epilogue parameter block (device pointers; unused ones may be null).
 struct EpiArgs {

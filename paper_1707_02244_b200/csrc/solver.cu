@@ -5,6 +5,7 @@
 // through the direct sm_100a kernels (kernels.cu), run_loop reproduces the
 // check cadence and stopping rule.  Setup transforms are fp64 on the host
 // (host_setup.cpp); iteration state lives in HBM as fp32.
+#include <algorithm>
 #include <chrono>
 #include <cstdlib>
 #include <cmath>
@@ -88,7 +89,7 @@ uint64_t footprint(int kind, int64_t n, uint64_t width) {
 // Shard g of G: tiles [g*T/G, (g+1)*T/G) of the output plan; for
 // ISTA the residual splits [g*S/G, (g+1)*S/G) and hence the rows of their
 // position chunks.  Pure host logic, shared by the solver and cl_shard_ranges.
-void shard_ranges(int kind, int64_t n, const std::vector<int>& rowstart, int rk, int ws, ConvPlan* plan,
+void shard_ranges(int kind, int64_t n, const int64_t* omega, int64_t m, int rk, int ws, ConvPlan* plan,
                   ConvPlan* rplan, int64_t* out_lo, int64_t* out_hi, int64_t* row_lo, int64_t* row_hi) {
   if (ws < 1 || rk < 0 || rk >= ws) raise(CL_EPARAM, "cl_solver_shard: need 0 <= rank < world");
   plan->tile_lo = plan->tiles * rk / ws;
@@ -99,10 +100,13 @@ void shard_ranges(int kind, int64_t n, const std::vector<int>& rowstart, int rk,
   if (kind == CL_KIND_ISTA) {
     rplan->split_lo = static_cast<int>(static_cast<int64_t>(rplan->splits) * rk / ws);
     rplan->split_hi = static_cast<int>(static_cast<int64_t>(rplan->splits) * (rk + 1) / ws);
-    const int64_t c_lo = static_cast<int64_t>(rplan->split_lo) * rplan->chunks / rplan->splits;
-    const int64_t c_hi = static_cast<int64_t>(rplan->split_hi) * rplan->chunks / rplan->splits;
-    *row_lo = rowstart[static_cast<size_t>(c_lo)];
-    *row_hi = rowstart[static_cast<size_t>(c_hi)];
+    int64_t b_lo, b_hi, dummy;
+    split_block_range(*rplan, rplan->split_lo, &b_lo, &dummy);
+    split_block_range(*rplan, rplan->split_hi - 1, &dummy, &b_hi);
+    if (rplan->split_hi <= rplan->split_lo) b_hi = b_lo;
+    const int64_t p_lo = b_lo * 32, p_hi = b_hi * 32;
+    *row_lo = std::lower_bound(omega, omega + m, p_lo) - omega;  // rows with positions in the splits' blocks
+    *row_hi = std::lower_bound(omega, omega + m, p_hi) - omega;
   }
 }
 
@@ -143,6 +147,7 @@ struct Solver {
   DevBuf<double> blk, met;
   double* met_host = nullptr;
   std::vector<int> rowstart_host;
+  std::vector<int64_t> omega_host;
   cudaEvent_t ev[8] = {};
   double phase_ms[8] = {};
   int nphase = 0;
@@ -176,6 +181,7 @@ struct Solver {
   }
 
   void build_rows(const int64_t* omega) {
+    omega_host.assign(omega, omega + m);
     std::vector<int> om(static_cast<size_t>(m));
     for (int64_t t2 = 0; t2 < m; ++t2) om[static_cast<size_t>(t2)] = static_cast<int>(omega[t2]);
     rowstart_host = chunk_rowstart(omega, m, plan.chunks);
@@ -189,7 +195,7 @@ struct Solver {
     if (fft && ws != 1) raise(CL_EPARAM, "cl_solver_shard: the FFT engine runs unsharded (replicas only)");
     rank = rk;
     world = ws;
-    shard_ranges(kind, n, rowstart_host, rk, ws, &plan, &rplan, &out_lo, &out_hi, &row_lo, &row_hi);
+    shard_ranges(kind, n, omega_host.data(), m, rk, ws, &plan, &rplan, &out_lo, &out_hi, &row_lo, &row_hi);
   }
 
   void setup_common(const double* c, const int64_t* omega, const double* yh, const cl_config* config) {
@@ -1062,8 +1068,7 @@ cl_status cl_shard_ranges(int kind, int64_t n, int64_t m, const int64_t* omega, 
   check_mask(omega, m, n);
   ConvPlan plan = make_plan(n, kind == CL_KIND_ISTA ? grad_R() : kRDense);
   ConvPlan rplan = make_plan(n, res_R());
-  const std::vector<int> rs = chunk_rowstart(omega, m, plan.chunks);
-  shard_ranges(kind, n, rs, rank, world, &plan, &rplan, out_lo, out_hi, row_lo, row_hi);
+  shard_ranges(kind, n, omega, m, rank, world, &plan, &rplan, out_lo, out_hi, row_lo, row_hi);
   CL_GUARD_END
 }
 
