@@ -43,6 +43,11 @@ __host__ __device__ __forceinline__ void split_blocks(int64_t chunks, int splits
   }
 }
 
+#ifndef CLB_RES_CHAINS
+#define CLB_RES_CHAINS 4
+#endif
+constexpr int kResChains = CLB_RES_CHAINS;  // dot-form chains in the residual
+
 __device__ int g_force_dense = 0;  // timing experiment: treat every position as a row
 
 template <int R>
@@ -391,15 +396,19 @@ template <int R, int PB, int S>
 __device__ __forceinline__ void res_pos(const float (&w)[R + PB], const float (&xr)[R], uint32_t mask,
                                         float*& lpp) {
   if (mask & (1u << S)) {
-    float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
+    // CH independent chains: the dot form has no shared operand, so its FFMA rate is
+    // latency-bound with few chains (microbench: 4 chains 45 TF, 8 chains 69 TF).
+    float p[kResChains];
 #pragma unroll
-    for (int q = 0; q < R; q += 4) {
-      p0 = fmaf(w[S - q + R], xr[q], p0);
-      p1 = fmaf(w[S - q - 1 + R], xr[q + 1], p1);
-      p2 = fmaf(w[S - q - 2 + R], xr[q + 2], p2);
-      p3 = fmaf(w[S - q - 3 + R], xr[q + 3], p3);
-    }
-    *lpp++ = (p0 + p1) + (p2 + p3);  // lane-major slot list: lp[lane * 33 + slot]
+    for (int c = 0; c < kResChains; ++c) p[c] = w[S - c + R] * xr[c];
+#pragma unroll
+    for (int q = kResChains; q < R; ++q) p[q % kResChains] = fmaf(w[S - q + R], xr[q], p[q % kResChains]);
+    // fixed-order pairwise fold of the chains (any chain count)
+#pragma unroll
+    for (int width = kResChains; width > 1; width = (width + 1) / 2)
+#pragma unroll
+      for (int c = 0; c < width / 2; ++c) p[c] += p[c + (width + 1) / 2];
+    *lpp++ = p[0];  // lane-major slot list: lp[lane * 33 + slot]
   }
 }
 

@@ -19,8 +19,12 @@ def probe(kind, n, m, k, iters=3):
     flops = 4.0 * m * n if kind == "ista" else 6.0 * n * n
     print(f"{kind} n={n} m={m}: gen {t1-t0:.2f}s setup {t2-t1:.2f}s  {ms:.3f} ms/iter  {flops/ms/1e9:.2f} TFLOP/s  phases(ms)={['%.3f'%v for v in ph]}", flush=True)
 
-print("ffma peak TF/s", cl.ffma_peak_tflops(0))
-probe("ista", 4096, 1024, 64, 20)
-probe("cadmm", 4096, 1024, 64, 20)
-probe("ista", 1 << 20, 1 << 18, 1 << 12, 3)
-probe("cadmm", 1 << 18, 1 << 16, 1 << 10, 3)
+if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "ista20":
+        probe("ista", 1 << 20, 1 << 18, 1 << 12, 3)
+        sys.exit(0)
+    print("ffma peak TF/s", cl.ffma_peak_tflops(0))
+    probe("ista", 4096, 1024, 64, 20)
+    probe("cadmm", 4096, 1024, 64, 20)
+    probe("ista", 1 << 20, 1 << 18, 1 << 12, 3)
+    probe("cadmm", 1 << 18, 1 << 16, 1 << 10, 3)
