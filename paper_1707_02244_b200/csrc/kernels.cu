@@ -283,7 +283,7 @@ k_conv_rows(const float* __restrict__ h, const int* __restrict__ omega, const fl
 #define CLB_B(S)                                                        \
   body##S : {                                                           \
     const float r = rb[S];                                              \
-    _Pragma("unroll") for (int q = 0; q < 32; ++q) acc[q] = fmaf(w[q - S + 32], r, acc[q]); \
+    _Pragma("unroll") for (int q = 0; q < R; ++q) acc[q] = fmaf(w[q - S + PB], r, acc[q]); \
   }                                                                     \
   goto ret##S;
 #define S_COMP(S) S_COMP_##S
@@ -320,14 +320,33 @@ k_conv_rows(const float* __restrict__ h, const int* __restrict__ omega, const fl
 #define S_COMP_29 y
 #define S_COMP_30 z
 #define S_COMP_31 w
-#define CLB_ALL32(M) M(0) M(1) M(2) M(3) M(4) M(5) M(6) M(7) M(8) M(9) M(10) M(11) M(12) M(13) M(14) M(15) \
+#define CLB_ALL16(M) M(0) M(1) M(2) M(3) M(4) M(5) M(6) M(7) M(8) M(9) M(10) M(11) M(12) M(13) M(14) M(15)
+#define CLB_ALL32(M) CLB_ALL16(M) \
   M(16) M(17) M(18) M(19) M(20) M(21) M(22) M(23) M(24) M(25) M(26) M(27) M(28) M(29) M(30) M(31)
 
-__global__ void __launch_bounds__(kThreads, 4)
+template <int R>
+__device__ __forceinline__ void ool_block32(float (&acc)[R], const float (&w)[R + 32], uint32_t mask,
+                                            const float* __restrict__ rb) {
+  constexpr int PB = 32;
+  CLB_ALL32(CLB_T)
+  return;
+  CLB_ALL32(CLB_B)
+}
+template <int R>
+__device__ __forceinline__ void ool_block16(float (&acc)[R], const float (&w)[R + 16], uint32_t mask,
+                                            const float* __restrict__ rb) {
+  constexpr int PB = 16;
+  CLB_ALL16(CLB_T)
+  return;
+  CLB_ALL16(CLB_B)
+}
+
+template <int MINB, int R = 32, int PB = 32>
+__global__ void __launch_bounds__(kThreads, MINB)
 k_conv_rows_ool(const float* __restrict__ h, const int* __restrict__ omega, const float* __restrict__ rv,
                 const int* __restrict__ rowstart, int64_t n, int64_t chunks, int splits, int64_t tile_lo,
                 float* __restrict__ partial) {
-  constexpr int R = 32, PB = 32, NB = kChunk / PB;
+  static_assert(PB == 32 || PB == 16, "PB must be 16 or 32");
   using Gm = Geo<R>;
   extern __shared__ float4 smem_f4[];
   float* hs = reinterpret_cast<float*>(smem_f4);
@@ -357,7 +376,8 @@ k_conv_rows_ool(const float* __restrict__ h, const int* __restrict__ omega, cons
     __syncthreads();
     for (int b32 = warp; b32 < kChunk / 32; b32 += kWarps) {
       const uint32_t mk = g_force_dense == 1 ? 0xffffffffu : g_force_dense == 2 ? 0x11111111u : g_force_dense == 3 ? 0x000000ffu : __ballot_sync(0xffffffffu, rd[b32 * 32 + lane] != 0.f);
-      if (lane == 0) bmask[b32] = mk;
+      if (lane == 0)
+        for (int sub = 0; sub < 32 / PB; ++sub) bmask[b32 * (32 / PB) + sub] = block_mask<PB>(mk, sub);
     }
     __syncthreads();
     const int64_t bsub = 32 / (PB), cb = ch * (kChunk / 32);
@@ -370,10 +390,8 @@ k_conv_rows_ool(const float* __restrict__ h, const int* __restrict__ omega, cons
       float w[R + PB];
       window_at<R, PB>(w, lane_base, kChunk - (b + 1) * PB);
       const float* rb = rd + b * PB;
-      CLB_ALL32(CLB_T)
-      goto block_done;
-      CLB_ALL32(CLB_B)
-    block_done:;
+      if constexpr (PB == 32) ool_block32<R>(acc, w, mask, rb);
+      else ool_block16<R>(acc, w, mask, rb);
     }
     __syncthreads();
   }
@@ -446,8 +464,8 @@ __device__ __forceinline__ void reduce_lane_partials(const float* __restrict__ l
   }
 }
 
-template <int R, int PB>
-__global__ void __launch_bounds__(kThreads, (R <= 32 ? 3 : 2))
+template <int R, int PB, int MINB = (R <= 32 ? 3 : 2)>
+__global__ void __launch_bounds__(kThreads, MINB)
 k_conv_residual(const float* __restrict__ h, const float* __restrict__ x, const int* __restrict__ omega,
                 const int* __restrict__ rowstart, int64_t n, int64_t m, int64_t chunks, int splits,
                 int split_lo, int split_cnt, float* __restrict__ partial) {
@@ -455,11 +473,11 @@ k_conv_residual(const float* __restrict__ h, const float* __restrict__ x, const 
   using Gm = Geo<R>;
   extern __shared__ float4 smem_f4[];
   float* hs = reinterpret_cast<float*>(smem_f4);
-  int* flag = reinterpret_cast<int*>(hs + Gm::kSegPhys);         // [kChunk]
-  uint32_t* bmask = reinterpret_cast<uint32_t*>(flag + kChunk);  // [NB]
-  int* bbase = reinterpret_cast<int*>(bmask + NB);               // [NB]
-  float* red = reinterpret_cast<float*>(bbase + NB);             // [kWarps][kChunk]
-  float* lanep = red + kWarps * kChunk;                          // [kWarps][32 lanes][33]
+  uint32_t* bmask = reinterpret_cast<uint32_t*>(hs + Gm::kSegPhys);  // [NB]
+  int* bbase = reinterpret_cast<int*>(bmask + NB);                    // [NB]
+  float* red = reinterpret_cast<float*>(bbase + NB);                  // [kWarps][kChunk]
+  int* flag = reinterpret_cast<int*>(red);  // [kChunk] row flags, dead before red is written
+  float* lanep = red + kWarps * kChunk;     // [kWarps][32 lanes][33]
   const int64_t unit = blockIdx.x;
   const int64_t tile = unit / split_cnt;
   const int split = split_lo + static_cast<int>(unit % split_cnt);
@@ -712,7 +730,7 @@ template <int R, int PB>
 constexpr size_t smem_rows() { return Geo<R>::kSegPhys * 4 + kChunk * 4 + (kChunk / PB) * 4; }
 template <int R, int PB>
 constexpr size_t smem_res() {
-  return Geo<R>::kSegPhys * 4 + kChunk * 4 + 2 * (kChunk / PB) * 4 + kWarps * kChunk * 4 + kWarps * 32 * 33 * 4;
+  return Geo<R>::kSegPhys * 4 + 2 * (kChunk / PB) * 4 + kWarps * kChunk * 4 + kWarps * 32 * 33 * 4;
 }
 
 // Kernel variant table (CLB_GRAD / CLB_RES select an entry for experiments;
@@ -728,20 +746,23 @@ struct ResVariant {
   size_t smem;
 };
 const GradVariant kGrad[] = {
-    {32, 32, k_conv_rows_ool, smem_rows<32, 32>()},  // default: best measured on B200 (C3, 17.0 ms)
+    {32, 32, k_conv_rows_ool<4>, smem_rows<32, 32>()},  // default: best measured on B200 (C3, 17.0 ms)
     {32, 32, k_conv_rows<32, 32, 4>, smem_rows<32, 32>()},
     {32, 32, k_conv_rows<32, 32>, smem_rows<32, 32>()},
     {32, 16, k_conv_rows<32, 16>, smem_rows<32, 16>()},
     {64, 16, k_conv_rows<64, 16, 3>, smem_rows<64, 16>()},
     {64, 32, k_conv_rows<64, 32, 3>, smem_rows<64, 32>()},
     {16, 32, k_conv_rows<16, 32>, smem_rows<16, 32>()},
+    {64, 16, k_conv_rows_ool<3, 64, 16>, smem_rows<64, 16>()},
 };
 const ResVariant kRes[] = {
-    {32, 32, k_conv_residual<32, 32>, smem_res<32, 32>()},  // default: best measured on B200 (C3, 27.7 ms)
+    // default: 4 CTAs/SM (120 registers, 55.3 KB smem): best measured on B200 (C3, 27.5 ms vs 29.0 at 3 CTAs/SM)
+    {32, 32, k_conv_residual<32, 32, 4>, smem_res<32, 32>()},
     {32, 16, k_conv_residual<32, 16>, smem_res<32, 16>()},
     {64, 16, k_conv_residual<64, 16>, smem_res<64, 16>()},
     {64, 32, k_conv_residual<64, 32>, smem_res<64, 32>()},
     {16, 32, k_conv_residual<16, 32>, smem_res<16, 32>()},
+    {32, 32, k_conv_residual<32, 32>, smem_res<32, 32>()},
 };
 int g_grad = 0, g_res = 0;
 
