@@ -365,11 +365,16 @@ static int ista_setup(Ista& st, int64_t n, int64_t m, const double* c, const int
 // cpista_phases: residual phase parallel.hpp:243-256, gradient phase :258-276.
 // The inner loops are split at the wrap point instead of branching per
 // element (circ_entry :161-166); the accumulation order is unchanged.
-static void ista_step_phases(Ista& st, int threads) {
+// rows_hi / outs_hi < m / n restrict the phases to a leading sample of their
+// outputs (timing only: bench.py's CPU baseline); phase_s receives the wall
+// time of each phase.
+static void ista_step_phases(Ista& st, int threads, int64_t rows_hi = -1, int64_t outs_hi = -1,
+                             double* phase_s = nullptr) {
   const int64_t n = st.n, m = st.m;
   const double* c = st.c.data();
   const double* x = st.x.data();
-  parallel_for(m, threads, [&](int64_t b, int64_t e) {
+  const auto t0 = std::chrono::steady_clock::now();
+  parallel_for(rows_hi < 0 ? m : rows_hi, threads, [&](int64_t b, int64_t e) {
     for (int64_t t = b; t < e; ++t) {
       const int64_t w = st.omega[static_cast<size_t>(t)];
       double acc = 0.0;
@@ -378,9 +383,10 @@ static void ista_step_phases(Ista& st, int threads) {
       st.r[static_cast<size_t>(t)] = st.y[static_cast<size_t>(t)] - acc;
     }
   });
+  const auto t1 = std::chrono::steady_clock::now();
   const double* r = st.r.data();
   const int64_t* om = st.omega.data();
-  parallel_for(n, threads, [&](int64_t b, int64_t e) {
+  parallel_for(outs_hi < 0 ? n : outs_hi, threads, [&](int64_t b, int64_t e) {
     for (int64_t i = b; i < e; ++i) {
       double acc = 0.0;
       for (int64_t t = 0; t < m; ++t) {
@@ -391,6 +397,11 @@ static void ista_step_phases(Ista& st, int threads) {
       st.x[static_cast<size_t>(i)] = soft(st.x[static_cast<size_t>(i)] + st.tau * acc, st.threshold);
     }
   });
+  if (phase_s) {
+    const auto t2 = std::chrono::steady_clock::now();
+    phase_s[0] = std::chrono::duration<double>(t1 - t0).count();
+    phase_s[1] = std::chrono::duration<double>(t2 - t1).count();
+  }
   ++st.t;
 }
 
@@ -438,11 +449,13 @@ static int cadmm_setup(Cadmm& st, int64_t n, int64_t m, const double* c, const i
 }
 
 // cpadmm_phases parallel.hpp:173-231 (primal :178-191, recovery :193-205, duals :207-228)
-static void cadmm_step_phases(Cadmm& st, int threads) {
+static void cadmm_step_phases(Cadmm& st, int threads, int64_t outs_hi = -1, double* phase_s = nullptr) {
   const int64_t n = st.n;
+  const int64_t nh = outs_hi < 0 ? n : outs_hi;
   const double* c = st.c.data();
   const double* b = st.b.data();
-  parallel_for(n, threads, [&](int64_t lo, int64_t hi) {
+  const auto t0 = std::chrono::steady_clock::now();
+  parallel_for(nh, threads, [&](int64_t lo, int64_t hi) {
     for (int64_t i = lo; i < hi; ++i) {  // acc += c[(i-j) mod n] * v[j]   (circ_entry(row, j, i))
       double acc = 0.0;
       for (int64_t j = 0; j <= i; ++j) acc += c[i - j] * st.v[static_cast<size_t>(j)];
@@ -450,7 +463,8 @@ static void cadmm_step_phases(Cadmm& st, int threads) {
       st.beta[static_cast<size_t>(i)] = st.rho * acc + st.sigma * (st.z[static_cast<size_t>(i)] - st.nu[static_cast<size_t>(i)]);
     }
   });
-  parallel_for(n, threads, [&](int64_t lo, int64_t hi) {
+  const auto t1 = std::chrono::steady_clock::now();
+  parallel_for(nh, threads, [&](int64_t lo, int64_t hi) {
     for (int64_t i = lo; i < hi; ++i) {  // acc += b[(j-i) mod n] * beta[j]
       double acc = 0.0;
       for (int64_t j = 0; j < i; ++j) acc += b[j - i + n] * st.beta[static_cast<size_t>(j)];
@@ -458,7 +472,8 @@ static void cadmm_step_phases(Cadmm& st, int threads) {
       st.x[static_cast<size_t>(i)] = acc;
     }
   });
-  parallel_for(n, threads, [&](int64_t lo, int64_t hi) {
+  const auto t2 = std::chrono::steady_clock::now();
+  parallel_for(nh, threads, [&](int64_t lo, int64_t hi) {
     for (int64_t i = lo; i < hi; ++i) {
       double cx = 0.0;
       for (int64_t j = 0; j < i; ++j) cx += c[j - i + n] * st.x[static_cast<size_t>(j)];
@@ -471,6 +486,12 @@ static void cadmm_step_phases(Cadmm& st, int threads) {
       st.v[k] = v_new + st.mu[k];
     }
   });
+  if (phase_s) {
+    const auto t3 = std::chrono::steady_clock::now();
+    phase_s[0] = std::chrono::duration<double>(t1 - t0).count();
+    phase_s[1] = std::chrono::duration<double>(t2 - t1).count();
+    phase_s[2] = std::chrono::duration<double>(t3 - t2).count();
+  }
   ++st.t;
 }
 
@@ -643,6 +664,14 @@ int orc_ista_step(void* h, int64_t iters, int engine, int threads) {
   }
   return OK;
 }
+// Timing sample of the phase engine (bench CPU baseline): the residual phase
+// over rows [0, rows), the gradient phase over outputs [0, outs).
+int orc_ista_phase_sample(void* h, int64_t rows, int64_t outs, int threads, double* phase_s) {
+  auto* st = static_cast<Ista*>(h);
+  if (rows < 0 || rows > st->m || outs < 0 || outs > st->n) return fail(EPARAM, "orc_ista_phase_sample: bad range");
+  ista_step_phases(*st, threads, rows, outs, phase_s);
+  return OK;
+}
 // which: 0 x, 1 r, 2 delta, 3 c~, 4 y~
 int orc_ista_get(void* h, int which, double* out) {
   auto* st = static_cast<Ista*>(h);
@@ -671,6 +700,13 @@ int orc_cadmm_step(void* h, int64_t iters, int engine, int threads) {
     if (engine == 1) { if (int rc = cadmm_step_fft(*st)) return rc; }
     else cadmm_step_phases(*st, threads);
   }
+  return OK;
+}
+// Timing sample: the three phases over outputs [0, outs).
+int orc_cadmm_phase_sample(void* h, int64_t outs, int threads, double* phase_s) {
+  auto* st = static_cast<Cadmm*>(h);
+  if (outs < 0 || outs > st->n) return fail(EPARAM, "orc_cadmm_phase_sample: bad range");
+  cadmm_step_phases(*st, threads, outs, phase_s);
   return OK;
 }
 // which: 0 x, 1 z, 2 nu, 3 mu, 4 v, 5 beta, 6 c~, 7 b, 8 d, 9 pty

@@ -80,6 +80,8 @@ def _decl(L):
                                  C.POINTER(C.c_int)]
     L.orc_ista_step.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int]
     L.orc_ista_get.argtypes = [C.c_void_p, C.c_int, _d]
+    L.orc_ista_phase_sample.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int, _d]
+    L.orc_cadmm_phase_sample.argtypes = [C.c_void_p, C.c_int64, C.c_int, _d]
     L.orc_ista_scalars.argtypes = [C.c_void_p, _d, _d, _d]
     L.orc_ista_free.argtypes = [C.c_void_p]
     L.orc_cadmm_setup.restype = C.c_void_p
@@ -267,6 +269,12 @@ class Ista(_Handle):
     def step(self, iters=1, engine=ENGINE_PHASES, threads=None):
         _check(lib().orc_ista_step(self._h, iters, engine, threads or os.cpu_count() or 1))
 
+    def phase_sample(self, rows, outs, threads=None):
+        """Times the phase engine on rows [0, rows) / outputs [0, outs) -> (t_residual, t_gradient) s."""
+        t = np.zeros(2)
+        _check(lib().orc_ista_phase_sample(self._h, rows, outs, threads or os.cpu_count() or 1, _pd(t)))
+        return float(t[0]), float(t[1])
+
     def get(self, name):
         which = {"x": 0, "r": 1, "delta": 2, "c": 3, "y": 4}[name]
         out = np.zeros(self.m if name in ("r", "y") else self.n)
@@ -298,6 +306,12 @@ class Cadmm(_Handle):
 
     def step(self, iters=1, engine=ENGINE_PHASES, threads=None):
         _check(lib().orc_cadmm_step(self._h, iters, engine, threads or os.cpu_count() or 1))
+
+    def phase_sample(self, outs, threads=None):
+        """Times the three phases on outputs [0, outs) -> (t_primal, t_recovery, t_duals) s."""
+        t = np.zeros(3)
+        _check(lib().orc_cadmm_phase_sample(self._h, outs, threads or os.cpu_count() or 1, _pd(t)))
+        return float(t[0]), float(t[1]), float(t[2])
 
     def get(self, name):
         out = np.zeros(self.n)

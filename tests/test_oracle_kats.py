@@ -271,3 +271,21 @@ def test_protocol_recovery_1024(kats):
     assert rep.reached_target and rep.final_metric <= k["target"]
     assert rep.trace[-1][1] == rep.final_metric
     assert all(a[0] < b[0] for a, b in zip(rep.trace, rep.trace[1:]))
+
+
+def test_phase_sample_full_range_is_a_step():
+    # bench.py's CPU baseline times phase_sample(); over the full ranges it is exactly one phase step
+    p = orc.make_problem(512, 128, 8, 3)
+    a, b = orc.Ista(p.row, p.omega, p.y), orc.Ista(p.row, p.omega, p.y)
+    for _ in range(3):
+        a.step(1, orc.ENGINE_PHASES, 2)
+        tr, tg = b.phase_sample(128, 512, 2)
+        assert tr >= 0 and tg >= 0
+    assert np.array_equal(a.get("x"), b.get("x"))
+    ca, cb = orc.Cadmm(p.row, p.omega, p.y), orc.Cadmm(p.row, p.omega, p.y)
+    for _ in range(3):
+        ca.step(1, orc.ENGINE_PHASES, 2)
+        assert len(cb.phase_sample(512, 2)) == 3
+    assert np.array_equal(ca.get("z"), cb.get("z"))
+    with pytest.raises(orc.OracleError):
+        b.phase_sample(129, 512)

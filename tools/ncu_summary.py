@@ -29,12 +29,23 @@ KEYS = {
 }
 
 
+DIRECT = ("k_conv_residual", "k_conv_rows", "k_conv_dense", "k_ista_update", "k_residual_reduce", "k_admm_beta",
+          "k_admm_x", "k_admm_duals", "k_metrics_final")
+FFT = ("k_fft_pass<16, -1>", "k_fft_pass<16, 1>", "k_fft_pass<8, -1>", "k_fft_pass<8, 1>", "k_fft_pass<4, -1>",
+       "k_fft_pass<4, 1>", "k_fft_pass<2, -1>", "k_fft_pass<2, 1>", "k_real_to_complex", "k_spec_mul",
+       "k_extract_real", "k_gather_real", "k_zero_c", "k_scatter_rows")
+
+
 def short(name):
-    for k in ("k_conv_residual", "k_conv_rows", "k_conv_dense", "k_ista_update", "k_residual_reduce", "k_admm_beta",
-              "k_admm_x", "k_admm_duals", "k_metrics_final", "k_ffma_peak"):
+    for k in DIRECT + FFT + ("k_ffma_peak",):
         if k in name:
             return k
     return name.split("(")[0][-40:]
+
+
+def group(k):
+    # k_residual_reduce / k_ista_update are shared by both engines; attribute them to the direct step
+    return "direct_engine" if k in DIRECT else "fft_engine" if k in FFT else "other"
 
 
 def load(rep):
@@ -79,8 +90,12 @@ def launches(path):
         a = agg.setdefault(k, [0, 0.0])
         a[0] += 1
         a[1] += float(r[vi].replace(",", ""))
-    tot = sum(v[1] for v in agg.values())
-    return {k: {"launches": v[0], "total_ns": v[1], "share": v[1] / tot} for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1])}
+    tot = {}
+    for k, v in agg.items():
+        tot[group(k)] = tot.get(group(k), 0.0) + v[1]
+    return {k: {"launches": v[0], "total_ns": v[1], "mean_ns": v[1] / v[0], "group": group(k),
+                "share_of_group": v[1] / tot[group(k)]}
+            for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1])}
 
 
 def main():
