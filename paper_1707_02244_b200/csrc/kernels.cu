@@ -557,6 +557,307 @@ k_conv_residual(const float* __restrict__ h, const float* __restrict__ x, const 
 }
 
 // ===========================================================================
+// Streamed-window sparse kernels.
+//
+// Layout: the staged row is NOT padded.  Lanes own R consecutive indices with
+// R = 4 (mod 8), so the window origins of the 8 lanes of an LDS.128 phase are
+// R/4 (odd) 16-byte units apart and land in 8 distinct bank groups; every
+// window address is then lane_base + compile-time offset.
+//
+// Streaming: the 32 positions of a block are processed in 8 groups of 4.  A
+// position needs R window floats; consecutive groups need windows 4 floats
+// apart, so each group issues ONE LDS.128 for the next group (prefetch) and
+// the compiler retires the 4 floats the group no longer needs: about R + 8
+// window registers are live instead of R + 32, which pays for the larger R
+// (fewer (warp, block) visits per row -> less per-block skeleton per FMA).
+// The row values of the next group are prefetched the same way, so no body
+// waits on a shared-memory load.
+// ===========================================================================
+template <int R>
+struct GeoU {
+  static_assert(R % 8 == 4, "unpadded layout needs R = 4 mod 8 (conflict-free LDS.128 phases)");
+  static constexpr int kTileR = kThreads * R;
+  static constexpr int kSeg = kTileR + kChunk;
+  static constexpr int kSegPhys = kSeg + 4;
+};
+
+// hs[e] = h[(base + e) mod n] for e in [0, kSeg).
+template <int kSeg>
+__device__ __forceinline__ void stage_plain(float* __restrict__ hs, const float* __restrict__ h, int64_t n,
+                                            int64_t base) {
+  int64_t b = base % n;
+  if (b < 0) b += n;
+  if ((n & 3) == 0) {
+    if (b + kSeg <= n) {
+      const float4* src = reinterpret_cast<const float4*>(h + b);
+      for (int e = threadIdx.x; e < kSeg / 4; e += kThreads) reinterpret_cast<float4*>(hs)[e] = __ldg(src + e);
+    } else {
+      for (int e = threadIdx.x * 4; e < kSeg; e += kThreads * 4) {
+        int64_t s = b + e;
+        if (s >= n) s %= n;
+        *reinterpret_cast<float4*>(hs + e) = __ldg(reinterpret_cast<const float4*>(h + s));
+      }
+    }
+  } else {
+    for (int e = threadIdx.x; e < kSeg; e += kThreads) hs[e] = __ldg(h + (b + e) % n);
+  }
+}
+
+template <int N, int K>
+__device__ __forceinline__ void ld4(float (&w)[N], const float* __restrict__ p) {
+  const float4 t = *reinterpret_cast<const float4*>(p + K);
+  w[K] = t.x;
+  w[K + 1] = t.y;
+  w[K + 2] = t.z;
+  w[K + 3] = t.w;
+}
+
+// Gradient block: acc[q] += w[q - s + 32] * r[s] for the rows s of the block,
+// ascending s (the reference's ascending-row order).  w[k] = wp[k].
+// Row test of position s.  PAIR: positions are first tested in pairs, so an
+// empty pair (9/16 of pairs at density 1/4) costs one taken branch over two
+// bodies instead of two (a taken branch over a body lands on code that was
+// never fetched: an instruction-cache miss).
+__device__ __forceinline__ bool row_at(uint32_t mask, int s) { return (mask >> s) & 1u; }
+template <bool PAIR>
+__device__ __forceinline__ bool pair_live(uint32_t mask, int s) { return !PAIR || ((mask >> s) & 3u); }
+
+template <int R, int G, bool PAIR>
+__device__ __forceinline__ void grad_group_s(float (&acc)[R], float (&w)[R + 32], uint32_t mask,
+                                             const float* __restrict__ wp, const float* __restrict__ rb,
+                                             float4& r4) {
+  float4 rn;
+  if constexpr (G < 7) {
+    rn = *reinterpret_cast<const float4*>(rb + 4 * (G + 1));
+    ld4<R + 32, 24 - 4 * G>(w, wp);
+  }
+  const float rr[4] = {r4.x, r4.y, r4.z, r4.w};
+#pragma unroll
+  for (int e2 = 0; e2 < 4; e2 += 2) {
+    if (pair_live<PAIR>(mask, 4 * G + e2)) {
+#pragma unroll
+      for (int e = e2; e < e2 + 2; ++e) {
+        const int s = 4 * G + e;
+        if (row_at(mask, s)) {
+#pragma unroll
+          for (int q = 0; q < R; ++q) acc[q] = fmaf(w[q - s + 32], rr[e], acc[q]);
+        }
+      }
+    }
+  }
+  if constexpr (G < 7) r4 = rn;
+}
+
+template <int R, bool PAIR>
+__device__ __forceinline__ void grad_block_s(float (&acc)[R], const float* __restrict__ wp,
+                                             const float* __restrict__ rb, uint32_t mask) {
+  float w[R + 32];
+#pragma unroll
+  for (int k = 28; k < R + 32; k += 4) {
+    const float4 t = *reinterpret_cast<const float4*>(wp + k);
+    w[k] = t.x;
+    w[k + 1] = t.y;
+    w[k + 2] = t.z;
+    w[k + 3] = t.w;
+  }
+  float4 r4 = *reinterpret_cast<const float4*>(rb);
+  grad_group_s<R, 0, PAIR>(acc, w, mask, wp, rb, r4);
+  grad_group_s<R, 1, PAIR>(acc, w, mask, wp, rb, r4);
+  grad_group_s<R, 2, PAIR>(acc, w, mask, wp, rb, r4);
+  grad_group_s<R, 3, PAIR>(acc, w, mask, wp, rb, r4);
+  grad_group_s<R, 4, PAIR>(acc, w, mask, wp, rb, r4);
+  grad_group_s<R, 5, PAIR>(acc, w, mask, wp, rb, r4);
+  grad_group_s<R, 6, PAIR>(acc, w, mask, wp, rb, r4);
+  grad_group_s<R, 7, PAIR>(acc, w, mask, wp, rb, r4);
+}
+
+template <int R, int MINB, bool PAIR = false>
+__global__ void __launch_bounds__(kThreads, MINB)
+k_grad_s(const float* __restrict__ h, const int* __restrict__ omega, const float* __restrict__ rv,
+         const int* __restrict__ rowstart, int64_t n, int64_t chunks, int splits, int64_t tile_lo,
+         float* __restrict__ partial) {
+  constexpr int PB = 32;
+  using G = GeoU<R>;
+  extern __shared__ float4 smem_f4[];
+  float* hs = reinterpret_cast<float*>(smem_f4);
+  float* rd = hs + G::kSegPhys;
+  uint32_t* bmask = reinterpret_cast<uint32_t*>(rd + kChunk);
+  const int64_t unit = blockIdx.x;
+  const int64_t tile = tile_lo + unit / splits;
+  const int split = static_cast<int>(unit % splits);
+  const int64_t I0 = tile * G::kTileR;
+  int64_t blo, bhi;
+  split_blocks(chunks, splits, split, &blo, &bhi);
+  const int own = threadIdx.x, warp = own >> 5, lane = own & 31;
+
+  float acc[R];
+#pragma unroll
+  for (int q = 0; q < R; ++q) acc[q] = 0.f;
+
+  for (int64_t ch = blo / (kChunk / 32); ch * (kChunk / 32) < bhi; ++ch) {
+    const int64_t Jc = ch * kChunk;
+    const int r0 = rowstart[ch], nr = rowstart[ch + 1] - r0;
+    if (nr == 0) continue;
+    stage_plain<G::kSeg>(hs, h, n, I0 - Jc - kChunk);
+    for (int s = threadIdx.x; s < kChunk; s += kThreads) rd[s] = 0.f;
+    __syncthreads();
+    for (int k = threadIdx.x; k < nr; k += kThreads) rd[omega[r0 + k] - static_cast<int>(Jc)] = __ldg(rv + r0 + k);
+    __syncthreads();
+    for (int b32 = warp; b32 < kChunk / 32; b32 += kWarps) {
+      const uint32_t mk = g_force_dense ? 0xffffffffu : __ballot_sync(0xffffffffu, rd[b32 * 32 + lane] != 0.f);
+      if (lane == 0) bmask[b32] = mk;
+    }
+    __syncthreads();
+    const int64_t cb = ch * (kChunk / 32);
+    const int b0 = static_cast<int>(blo > cb ? blo - cb : 0);
+    const int b1 = static_cast<int>(bhi - cb < kChunk / 32 ? bhi - cb : kChunk / 32);
+    const float* wl = hs + own * R + kChunk - PB;
+    for (int b = b0; b < b1; ++b) {
+      const uint32_t mask = __reduce_or_sync(0xffffffffu, bmask[b]);
+      if (mask == 0u) continue;
+      grad_block_s<R, PAIR>(acc, wl - b * PB, rd + b * PB, mask);
+    }
+    __syncthreads();
+  }
+  const int64_t ib = I0 + own * R;
+  float* out = partial + static_cast<int64_t>(split) * n;
+#pragma unroll
+  for (int q = 0; q < R; ++q)
+    if (ib + q < n) out[ib + q] = acc[q];
+}
+
+// Residual block (dot form, x register-resident): row s computes
+// sum_q w[s - q + R] x[q]; position s needs w[s+1 .. s+R], so the window
+// moves up by 4 per group.
+template <int R, int S>
+__device__ __forceinline__ void res_row_s(const float (&w)[R + 32], const float (&xr)[R], float*& lpp) {
+  float p[kResChains];
+#pragma unroll
+  for (int c = 0; c < kResChains; ++c) p[c] = w[S - c + R] * xr[c];
+#pragma unroll
+  for (int q = kResChains; q < R; ++q) p[q % kResChains] = fmaf(w[S - q + R], xr[q], p[q % kResChains]);
+#pragma unroll
+  for (int width = kResChains; width > 1; width = (width + 1) / 2)
+#pragma unroll
+    for (int c = 0; c < width / 2; ++c) p[c] += p[c + (width + 1) / 2];
+  *lpp++ = p[0];
+}
+
+template <int R, int G, bool PAIR>
+__device__ __forceinline__ void res_group_s(float (&w)[R + 32], const float (&xr)[R], uint32_t mask,
+                                            const float* __restrict__ wp, float*& lpp) {
+  if constexpr (G < 7) ld4<R + 32, R + 4 + 4 * G>(w, wp);
+  if (pair_live<PAIR>(mask, 4 * G)) {
+    if (row_at(mask, 4 * G)) res_row_s<R, 4 * G>(w, xr, lpp);
+    if (row_at(mask, 4 * G + 1)) res_row_s<R, 4 * G + 1>(w, xr, lpp);
+  }
+  if (pair_live<PAIR>(mask, 4 * G + 2)) {
+    if (row_at(mask, 4 * G + 2)) res_row_s<R, 4 * G + 2>(w, xr, lpp);
+    if (row_at(mask, 4 * G + 3)) res_row_s<R, 4 * G + 3>(w, xr, lpp);
+  }
+}
+
+template <int R, bool PAIR>
+__device__ __forceinline__ void res_block_s(const float* __restrict__ wp, const float (&xr)[R], uint32_t mask,
+                                            float*& lpp) {
+  float w[R + 32];
+#pragma unroll
+  for (int k = 0; k < R + 4; k += 4) {
+    const float4 t = *reinterpret_cast<const float4*>(wp + k);
+    w[k] = t.x;
+    w[k + 1] = t.y;
+    w[k + 2] = t.z;
+    w[k + 3] = t.w;
+  }
+  res_group_s<R, 0, PAIR>(w, xr, mask, wp, lpp);
+  res_group_s<R, 1, PAIR>(w, xr, mask, wp, lpp);
+  res_group_s<R, 2, PAIR>(w, xr, mask, wp, lpp);
+  res_group_s<R, 3, PAIR>(w, xr, mask, wp, lpp);
+  res_group_s<R, 4, PAIR>(w, xr, mask, wp, lpp);
+  res_group_s<R, 5, PAIR>(w, xr, mask, wp, lpp);
+  res_group_s<R, 6, PAIR>(w, xr, mask, wp, lpp);
+  res_group_s<R, 7, PAIR>(w, xr, mask, wp, lpp);
+}
+
+template <int R, int MINB, bool PAIR = false>
+__global__ void __launch_bounds__(kThreads, MINB)
+k_res_s(const float* __restrict__ h, const float* __restrict__ x, const int* __restrict__ omega,
+        const int* __restrict__ rowstart, int64_t n, int64_t m, int64_t chunks, int splits, int split_lo,
+        int split_cnt, float* __restrict__ partial) {
+  constexpr int PB = 32, NB = kChunk / PB;
+  using G = GeoU<R>;
+  extern __shared__ float4 smem_f4[];
+  float* hs = reinterpret_cast<float*>(smem_f4);
+  uint32_t* bmask = reinterpret_cast<uint32_t*>(hs + G::kSegPhys);  // [NB]
+  int* bbase = reinterpret_cast<int*>(bmask + NB);                   // [NB]
+  float* red = reinterpret_cast<float*>(bbase + NB);                 // [kWarps][kChunk]
+  int* flag = reinterpret_cast<int*>(red);  // [kChunk] row flags, dead before red is written
+  float* lanep = red + kWarps * kChunk;     // [kWarps][32 lanes][33]
+  const int64_t unit = blockIdx.x;
+  const int64_t tile = unit / split_cnt;
+  const int split = split_lo + static_cast<int>(unit % split_cnt);
+  const int64_t I0 = tile * G::kTileR;
+  int64_t blo, bhi;
+  split_blocks(chunks, splits, split, &blo, &bhi);
+  const int own = threadIdx.x, warp = own >> 5, lane = own & 31;
+  const float* lane_base = hs + (kThreads - 1 - own) * R;
+  float* redw = red + warp * kChunk;
+  float* lp = lanep + warp * 32 * 33;
+  float* const lp_lane = lp + lane * 33;
+
+  float xr[R];
+  const int64_t jb = I0 + own * R;
+#pragma unroll
+  for (int q = 0; q < R; ++q) xr[q] = (jb + q < n) ? __ldg(x + jb + q) : 0.f;
+
+  for (int64_t ch = blo / (kChunk / 32); ch * (kChunk / 32) < bhi; ++ch) {
+    const int64_t Jc = ch * kChunk;
+    const int r0 = rowstart[ch], nr = rowstart[ch + 1] - r0;
+    if (nr == 0) continue;
+    stage_plain<G::kSeg>(hs, h, n, Jc - I0 - G::kTileR);
+    for (int s = threadIdx.x; s < kChunk; s += kThreads) flag[s] = 0;
+    __syncthreads();
+    for (int k = threadIdx.x; k < nr; k += kThreads) flag[omega[r0 + k] - static_cast<int>(Jc)] = 1;
+    __syncthreads();
+    if (warp == 0) {  // masks + exclusive prefix of row counts per block
+      int run = 0;
+      for (int b32 = 0; b32 < NB; ++b32) {
+        const uint32_t mk = g_force_dense ? 0xffffffffu : __ballot_sync(0xffffffffu, flag[b32 * 32 + lane] != 0);
+        if (lane == 0) {
+          bmask[b32] = mk;
+          bbase[b32] = run;
+        }
+        run += __popc(mk);
+      }
+    }
+    __syncthreads();
+    const int64_t cb = ch * (kChunk / 32);
+    const int b0 = static_cast<int>(blo > cb ? blo - cb : 0);
+    const int b1 = static_cast<int>(bhi - cb < kChunk / 32 ? bhi - cb : kChunk / 32);
+    for (int b = b0; b < b1; ++b) {
+      const uint32_t mask = __reduce_or_sync(0xffffffffu, bmask[b]);
+      if (mask == 0u) continue;
+      float* lpp = lp_lane;
+      res_block_s<R, PAIR>(lane_base + b * PB, xr, mask, lpp);
+      __syncwarp();
+      reduce_lane_partials(lp, redw, bbase[b], __popc(mask), lane);
+      __syncwarp();
+    }
+    __syncthreads();
+    float* outp = partial + tile * m + r0;
+    const int k_lo = b0 < NB ? bbase[b0] : nr;
+    const int k_hi = b1 < NB ? bbase[b1] : nr;
+    for (int kk = k_lo + threadIdx.x; kk < k_hi; kk += kThreads) {
+      float s = red[kk];
+#pragma unroll
+      for (int wi = 1; wi < kWarps; ++wi) s += red[wi * kChunk + kk];
+      outp[kk] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// ===========================================================================
 // Elementwise epilogues (fixed grid kEpiBlocks -> deterministic metrics).
 // ===========================================================================
 __device__ __forceinline__ float soft(float v, float g) {  // solvers.hpp:39-44
@@ -728,6 +1029,12 @@ template <int R>
 constexpr size_t smem_dense() { return Geo<R>::kSegPhys * 4 + kChunk * 4; }
 template <int R, int PB>
 constexpr size_t smem_rows() { return Geo<R>::kSegPhys * 4 + kChunk * 4 + (kChunk / PB) * 4; }
+template <int R>
+constexpr size_t smem_grad_s() { return (GeoU<R>::kSegPhys + kChunk + kChunk / 32) * 4; }
+template <int R>
+constexpr size_t smem_res_s() {
+  return (GeoU<R>::kSegPhys + 2 * (kChunk / 32) + kWarps * kChunk + kWarps * 32 * 33) * 4;
+}
 template <int R, int PB>
 constexpr size_t smem_res() {
   return Geo<R>::kSegPhys * 4 + 2 * (kChunk / PB) * 4 + kWarps * kChunk * 4 + kWarps * 32 * 33 * 4;
@@ -746,7 +1053,7 @@ struct ResVariant {
   size_t smem;
 };
 const GradVariant kGrad[] = {
-    {32, 32, k_conv_rows_ool<4>, smem_rows<32, 32>()},  // default: best measured on B200 (C3, 17.0 ms)
+    {32, 32, k_conv_rows_ool<4>, smem_rows<32, 32>()},  // small-n default (C3: 17.2 ms)
     {32, 32, k_conv_rows<32, 32, 4>, smem_rows<32, 32>()},
     {32, 32, k_conv_rows<32, 32>, smem_rows<32, 32>()},
     {32, 16, k_conv_rows<32, 16>, smem_rows<32, 16>()},
@@ -754,17 +1061,37 @@ const GradVariant kGrad[] = {
     {64, 32, k_conv_rows<64, 32, 3>, smem_rows<64, 32>()},
     {16, 32, k_conv_rows<16, 32>, smem_rows<16, 32>()},
     {64, 16, k_conv_rows_ool<3, 64, 16>, smem_rows<64, 16>()},
+    {60, 32, k_grad_s<60, 3>, smem_grad_s<60>()},  // 8: streamed window, unpadded layout
+    {52, 32, k_grad_s<52, 3>, smem_grad_s<52>()},
+    {44, 32, k_grad_s<44, 4>, smem_grad_s<44>()},
+    {36, 32, k_grad_s<36, 4>, smem_grad_s<36>()},
+    {44, 32, k_grad_s<44, 3>, smem_grad_s<44>()},
+    {44, 32, k_grad_s<44, 4, true>, smem_grad_s<44>()},  // 13: pair tests; large-n default (C3: 16.0 ms)
+    {52, 32, k_grad_s<52, 3, true>, smem_grad_s<52>()},
 };
 const ResVariant kRes[] = {
-    // default: 4 CTAs/SM (120 registers, 55.3 KB smem): best measured on B200 (C3, 27.5 ms vs 29.0 at 3 CTAs/SM)
+    // small-n default: 4 CTAs/SM (120 registers, 55.3 KB smem; C3: 27.5 ms vs 29.0 at 3 CTAs/SM)
     {32, 32, k_conv_residual<32, 32, 4>, smem_res<32, 32>()},
     {32, 16, k_conv_residual<32, 16>, smem_res<32, 16>()},
     {64, 16, k_conv_residual<64, 16>, smem_res<64, 16>()},
     {64, 32, k_conv_residual<64, 32>, smem_res<64, 32>()},
     {16, 32, k_conv_residual<16, 32>, smem_res<16, 32>()},
     {32, 32, k_conv_residual<32, 32>, smem_res<32, 32>()},
+    {60, 32, k_res_s<60, 3>, smem_res_s<60>()},  // 6: streamed window, unpadded layout
+    {52, 32, k_res_s<52, 3>, smem_res_s<52>()},
+    {44, 32, k_res_s<44, 4>, smem_res_s<44>()},
+    {36, 32, k_res_s<36, 4>, smem_res_s<36>()},
+    {44, 32, k_res_s<44, 3>, smem_res_s<44>()},
+    {60, 32, k_res_s<60, 2>, smem_res_s<60>()},
+    {52, 32, k_res_s<52, 3, true>, smem_res_s<52>()},  // 12: pair tests; large-n default (C3: 23.3 ms)
+    {44, 32, k_res_s<44, 3, true>, smem_res_s<44>()},
 };
-int g_grad = 0, g_res = 0;
+// Defaults (measured best on B200, tools/variants.py): the streamed-window
+// kernels with pair tests at large n; the R = 32 padded kernels at small n,
+// where a 4096-index tile already covers the whole problem.
+constexpr int64_t kLargeN = int64_t(1) << 17;
+constexpr int kGradLarge = 13, kGradSmall = 0, kResLarge = 12, kResSmall = 0;
+int g_grad = -1, g_res = -1;  // -1: choose by n
 
 }  // namespace
 
@@ -777,8 +1104,16 @@ static void select_variants() {
   if (const char* v = getenv("CLB_GRAD")) g_grad = atoi(v) % (int)(sizeof(kGrad) / sizeof(kGrad[0]));
   if (const char* v = getenv("CLB_RES")) g_res = atoi(v) % (int)(sizeof(kRes) / sizeof(kRes[0]));
 }
-int grad_R() { select_variants(); return kGrad[g_grad].R; }
-int res_R() { select_variants(); return kRes[g_res].R; }
+static const GradVariant& grad_variant(int64_t n) {
+  select_variants();
+  return kGrad[g_grad >= 0 ? g_grad : (n >= kLargeN ? kGradLarge : kGradSmall)];
+}
+static const ResVariant& res_variant(int64_t n) {
+  select_variants();
+  return kRes[g_res >= 0 ? g_res : (n >= kLargeN ? kResLarge : kResSmall)];
+}
+int grad_R(int64_t n) { return grad_variant(n).R; }
+int res_R(int64_t n) { return res_variant(n).R; }
 
 void split_block_range(const ConvPlan& p, int split, int64_t* blo, int64_t* bhi) {
   split_blocks(p.chunks, p.splits, split, blo, bhi);
@@ -829,7 +1164,7 @@ void launch_conv_rows(const ConvPlan& p, const float* h, const int* omega32, con
                       float* partial, cudaStream_t st) {
   const int64_t units = (p.tile_hi - p.tile_lo) * p.splits;
   if (units <= 0) return;
-  const GradVariant& g = kGrad[g_grad];
+  const GradVariant& g = grad_variant(p.n);
   g.fn<<<static_cast<unsigned>(units), kThreads, g.smem, st>>>(h, omega32, rvals, rowstart, p.n, p.chunks, p.splits,
                                                               p.tile_lo, partial);
 }
@@ -839,7 +1174,7 @@ void launch_conv_residual(const ConvPlan& p, int64_t m, const float* h, const fl
   const int cnt = p.split_hi - p.split_lo;
   const int64_t units = p.tiles * cnt;
   if (units <= 0) return;
-  const ResVariant& r = kRes[g_res];
+  const ResVariant& r = res_variant(p.n);
   r.fn<<<static_cast<unsigned>(units), kThreads, r.smem, st>>>(h, x, omega32, rowstart, p.n, m, p.chunks, p.splits,
                                                               p.split_lo, cnt, partial);
 }

@@ -34,10 +34,10 @@ constexpr int kTargetUnits = 1184;      // 8 x 148: split-count target (constant
 constexpr int kEpiBlocks = 592;         // grid of the elementwise epilogues (fixed -> deterministic metrics)
 
 // Register blocking of the dense kernel (indices owned per thread); the
-// sparse kernels' R comes from the selected variant (grad_R(), res_R()).
+// sparse kernels' R comes from the variant selected for n (grad_R(n), res_R(n)).
 constexpr int kRDense = 64;
-int grad_R();
-int res_R();
+int grad_R(int64_t n);
+int res_R(int64_t n);
 
 struct ConvPlan {
   int64_t n = 0;

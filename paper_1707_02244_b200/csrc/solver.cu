@@ -231,8 +231,8 @@ struct Solver {
     tau = tau0;
     thr = cfg.pairing == CL_PAIRING_LITERAL ? cfg.alpha : tau0 * cfg.alpha;
     init_device();
-    plan = make_plan(n, grad_R());
-    rplan = make_plan(n, res_R());
+    plan = make_plan(n, grad_R(n));
+    rplan = make_plan(n, res_R(n));
     const std::vector<float> cf = to_f32(c, n, scale);
     hc.alloc(static_cast<size_t>(n));
     hc.upload(cf.data(), cf.size(), st);
@@ -758,8 +758,8 @@ cl_status cl_partial_matvec(int device, int64_t n, int64_t m, const double* c, c
   s.m = m;
   s.cfg = cfg;
   s.init_device();
-  s.plan = make_plan(n, grad_R());
-  s.rplan = make_plan(n, res_R());
+  s.plan = make_plan(n, grad_R(n));
+  s.rplan = make_plan(n, res_R(n));
   const std::vector<float> crf = reversed(to_f32(c, n));
   s.hcr.alloc(static_cast<size_t>(n));
   s.hcr.upload(crf.data(), crf.size(), s.st);
@@ -791,7 +791,7 @@ cl_status cl_partial_transpose_matvec(int device, int64_t n, int64_t m, const do
   s.n = n;
   s.m = m;
   s.init_device();
-  s.plan = make_plan(n, grad_R());
+  s.plan = make_plan(n, grad_R(n));
   const std::vector<float> cf = to_f32(c, n);
   s.hc.alloc(static_cast<size_t>(n));
   s.hc.upload(cf.data(), cf.size(), s.st);
@@ -1066,8 +1066,8 @@ cl_status cl_shard_ranges(int kind, int64_t n, int64_t m, const int64_t* omega, 
   if (kind != CL_KIND_ISTA && kind != CL_KIND_CADMM) raise(CL_EPARAM, "cl_shard_ranges: unknown solver kind");
   if (n < 1 || m < 0 || m > n) raise(CL_EDIM, "cl_shard_ranges: need n >= 1 and 0 <= m <= n");
   check_mask(omega, m, n);
-  ConvPlan plan = make_plan(n, kind == CL_KIND_ISTA ? grad_R() : kRDense);
-  ConvPlan rplan = make_plan(n, res_R());
+  ConvPlan plan = make_plan(n, kind == CL_KIND_ISTA ? grad_R(n) : kRDense);
+  ConvPlan rplan = make_plan(n, res_R(n));
   shard_ranges(kind, n, omega, m, rank, world, &plan, &rplan, out_lo, out_hi, row_lo, row_hi);
   CL_GUARD_END
 }
