@@ -176,6 +176,63 @@ def run_reference(args, w, rank):
     print(json.dumps(line), flush=True)
 
 
+def admm_line(cl, torch, prob, local_rank, flush, steps=5, warmup=3):
+    """cADMM (the paper's CPADMM, the metric's "ADMM") on the same n=2^20 problem:
+    device-timed iterations/s of the direct engine (3 dense circulant products
+    per iteration, 6 n^2 flop) and the dense kernel's FFMA fraction."""
+    import ctypes as C
+    from paper_1707_02244_b200._native import lib as L
+    st = cl.cadmm_setup(prob.op, prob.measurements, cl.SolverConfig(), device=local_rank)
+    sp = C.c_void_p()
+    L.cl_solver_stream(st.handle, C.byref(sp))
+    stream = torch.cuda.ExternalStream(sp.value)
+    st.step(warmup)
+    st.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for i in range(steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            ev[i][0].record(stream)
+        st.step(1)
+        with torch.cuda.stream(stream):
+            ev[i][1].record(stream)
+    st.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in ev) / steps
+    st.profile(True)
+    st.step(1)
+    st.synchronize()
+    ph = st.phase_ms()
+    st.profile(False)
+    n = prob.op.n()
+    dense_ms = (ph[0] + ph[2] + ph[4]) / 3.0
+    return {"value": 1e3 / ms, "unit": "iterations/s", "ms_per_step": ms, "steps": steps, "warmup": warmup,
+            "workload": f"cADMM n={n}, m={prob.op.m()}, k={prob.k()}, rho=sigma=0.1, tau1=tau2=1, alpha=1e-4 "
+                        "(make_problem(2^20, 2^18, 2^12, 1), the config-3 problem)",
+            "engine": "direct shift-indexed sm_100a kernels",
+            "dense_kernel": {"kernel": "k_conv_dense", "ms": dense_ms,
+                             "achieved_tflops": 2.0 * n * n / (dense_ms * 1e-3) / 1e12},
+            "step_tflops": 6.0 * n * n / (ms * 1e-3) / 1e12, "phase_ms": ph}
+
+
+def recovery_line(cl, prob, local_rank, target=1e-4):
+    """Time to recovery (paper protocol: stop at MSE(x, x*) <= 1e-4)
+    through the public API (ista_run / cadmm_run with truth, check_every=10):
+    host buffers in, setup, iterations, result out; host clock."""
+    out = {"target_mse": target, "check_every": 10,
+           "note": "ista_run/cadmm_run(y, A, SolverConfig(target_mse=1e-4), truth=x*) from host fp64 buffers; "
+                   "seconds = the call's wall time (setup + iterations + download)"}
+    for kind, run, cap in (("ista", cl.ista_run, 6000), ("cadmm", cl.cadmm_run, 1000)):
+        out[kind] = {}
+        for eng in ("direct", "fft"):
+            cfg = cl.SolverConfig(max_iter=cap, check_every=10, target_mse=target, use_fft=(eng == "fft"))
+            t0 = time.perf_counter()
+            rep = run(prob.measurements, prob.op, cfg, truth=prob.signal.values, device=local_rank)
+            wall = time.perf_counter() - t0
+            out[kind][eng] = {"seconds": wall, "iterations": rep.iterations, "reached": bool(rep.reached_target),
+                              "final_mse": rep.final_metric, "setup_seconds": rep.setup_seconds}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -184,6 +241,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="skip the cADMM line and time-to-recovery")
     args = ap.parse_args()
     w = WORKLOADS[args.workload]
 
@@ -266,11 +324,11 @@ def main():
         phase_ms.append(st.phase_ms())
     st.profile(False)
 
-    # dominant kernel (~60% of the step, profiles/r1/launches_r1.csv): live CUDA-event durations
+    # dominant kernel (the residual, ~59% of the step, profiles/r1/launches_r1b.csv): live CUDA-event durations
     if w["kind"] == "ista":
         k_ms = statistics.mean(p[0] for p in phase_ms)
         k_flops = 2.0 * w["m"] * w["n"] / world
-        k_name = "k_conv_residual"
+        k_name = "k_res_s"
     else:
         k_ms = statistics.mean(p[0] for p in phase_ms)
         k_flops = 2.0 * w["n"] * w["n"] / world
@@ -341,6 +399,11 @@ def main():
                     "note": "same metric and workload, SolverConfig(use_fft=True); L2 flushed between steps"}
         del fst
 
+    admm = recovery = None
+    if world == 1 and w["kind"] == "ista" and w["n"] == (1 << 20) and not args.quick:
+        admm = admm_line(cl, torch, prob, local_rank, flush)
+        recovery = recovery_line(cl, prob, local_rank)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu, _ = cpu_baseline_line(w, 3 if w["n"] >= (1 << 20) else 20, 1)
@@ -348,6 +411,17 @@ def main():
             fft_line["cpu_fft_engine"] = {
                 "value": cpu_fft_rate(w, 2 if w["n"] >= (1 << 20) else 20), "unit": "iterations/s", "cores": 1,
                 "kind": "port", "sample": "full iterations of the reference-default FFT engine (single thread)"}
+        if admm is not None:
+            step, threads, sample = cpu_phase_sampler(dict(w, kind="cadmm"))
+            step()
+            secs = [step() for _ in range(2)]
+            admm["cpu_baseline"] = {"value": len(secs) / sum(secs), "unit": "iterations/s", "cores": threads,
+                                    "kind": "port", "sample": f"2 steps of the cADMM phase engine (fp64): {sample}"}
+        if recovery is not None:
+            for kind, rate in (("ista", cpu["value"]), ("cadmm", admm["cpu_baseline"]["value"] if admm else None)):
+                if rate:
+                    it = recovery[kind]["direct"]["iterations"]
+                    recovery[kind]["cpu_phase_engine_seconds_extrapolated"] = it / rate
 
     if rank == 0:
         line = {
@@ -367,6 +441,8 @@ def main():
             "gpu_launches": (4 if w["kind"] == "ista" else 6) * args.steps,
             "e2e": e2e,
             "fft_engine": fft_line,
+            "admm": admm,
+            "time_to_recovery": recovery,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
