@@ -729,35 +729,35 @@ k_grad_s(const float* __restrict__ h, const int* __restrict__ omega, const float
 // Residual block (dot form, x register-resident): row s computes
 // sum_q w[s - q + R] x[q]; position s needs w[s+1 .. s+R], so the window
 // moves up by 4 per group.
-template <int R, int S>
+template <int R, int S, int CH>
 __device__ __forceinline__ void res_row_s(const float (&w)[R + 32], const float (&xr)[R], float*& lpp) {
-  float p[kResChains];
+  float p[CH];
 #pragma unroll
-  for (int c = 0; c < kResChains; ++c) p[c] = w[S - c + R] * xr[c];
+  for (int c = 0; c < CH; ++c) p[c] = w[S - c + R] * xr[c];
 #pragma unroll
-  for (int q = kResChains; q < R; ++q) p[q % kResChains] = fmaf(w[S - q + R], xr[q], p[q % kResChains]);
+  for (int q = CH; q < R; ++q) p[q % CH] = fmaf(w[S - q + R], xr[q], p[q % CH]);
 #pragma unroll
-  for (int width = kResChains; width > 1; width = (width + 1) / 2)
+  for (int width = CH; width > 1; width = (width + 1) / 2)
 #pragma unroll
     for (int c = 0; c < width / 2; ++c) p[c] += p[c + (width + 1) / 2];
   *lpp++ = p[0];
 }
 
-template <int R, int G, bool PAIR>
+template <int R, int G, bool PAIR, int CH>
 __device__ __forceinline__ void res_group_s(float (&w)[R + 32], const float (&xr)[R], uint32_t mask,
                                             const float* __restrict__ wp, float*& lpp) {
   if constexpr (G < 7) ld4<R + 32, R + 4 + 4 * G>(w, wp);
   if (pair_live<PAIR>(mask, 4 * G)) {
-    if (row_at(mask, 4 * G)) res_row_s<R, 4 * G>(w, xr, lpp);
-    if (row_at(mask, 4 * G + 1)) res_row_s<R, 4 * G + 1>(w, xr, lpp);
+    if (row_at(mask, 4 * G)) res_row_s<R, 4 * G, CH>(w, xr, lpp);
+    if (row_at(mask, 4 * G + 1)) res_row_s<R, 4 * G + 1, CH>(w, xr, lpp);
   }
   if (pair_live<PAIR>(mask, 4 * G + 2)) {
-    if (row_at(mask, 4 * G + 2)) res_row_s<R, 4 * G + 2>(w, xr, lpp);
-    if (row_at(mask, 4 * G + 3)) res_row_s<R, 4 * G + 3>(w, xr, lpp);
+    if (row_at(mask, 4 * G + 2)) res_row_s<R, 4 * G + 2, CH>(w, xr, lpp);
+    if (row_at(mask, 4 * G + 3)) res_row_s<R, 4 * G + 3, CH>(w, xr, lpp);
   }
 }
 
-template <int R, bool PAIR>
+template <int R, bool PAIR, int CH>
 __device__ __forceinline__ void res_block_s(const float* __restrict__ wp, const float (&xr)[R], uint32_t mask,
                                             float*& lpp) {
   float w[R + 32];
@@ -769,17 +769,17 @@ __device__ __forceinline__ void res_block_s(const float* __restrict__ wp, const 
     w[k + 2] = t.z;
     w[k + 3] = t.w;
   }
-  res_group_s<R, 0, PAIR>(w, xr, mask, wp, lpp);
-  res_group_s<R, 1, PAIR>(w, xr, mask, wp, lpp);
-  res_group_s<R, 2, PAIR>(w, xr, mask, wp, lpp);
-  res_group_s<R, 3, PAIR>(w, xr, mask, wp, lpp);
-  res_group_s<R, 4, PAIR>(w, xr, mask, wp, lpp);
-  res_group_s<R, 5, PAIR>(w, xr, mask, wp, lpp);
-  res_group_s<R, 6, PAIR>(w, xr, mask, wp, lpp);
-  res_group_s<R, 7, PAIR>(w, xr, mask, wp, lpp);
+  res_group_s<R, 0, PAIR, CH>(w, xr, mask, wp, lpp);
+  res_group_s<R, 1, PAIR, CH>(w, xr, mask, wp, lpp);
+  res_group_s<R, 2, PAIR, CH>(w, xr, mask, wp, lpp);
+  res_group_s<R, 3, PAIR, CH>(w, xr, mask, wp, lpp);
+  res_group_s<R, 4, PAIR, CH>(w, xr, mask, wp, lpp);
+  res_group_s<R, 5, PAIR, CH>(w, xr, mask, wp, lpp);
+  res_group_s<R, 6, PAIR, CH>(w, xr, mask, wp, lpp);
+  res_group_s<R, 7, PAIR, CH>(w, xr, mask, wp, lpp);
 }
 
-template <int R, int MINB, bool PAIR = false>
+template <int R, int MINB, bool PAIR = false, int CH = kResChains>
 __global__ void __launch_bounds__(kThreads, MINB)
 k_res_s(const float* __restrict__ h, const float* __restrict__ x, const int* __restrict__ omega,
         const int* __restrict__ rowstart, int64_t n, int64_t m, int64_t chunks, int splits, int split_lo,
@@ -838,7 +838,7 @@ k_res_s(const float* __restrict__ h, const float* __restrict__ x, const int* __r
       const uint32_t mask = __reduce_or_sync(0xffffffffu, bmask[b]);
       if (mask == 0u) continue;
       float* lpp = lp_lane;
-      res_block_s<R, PAIR>(lane_base + b * PB, xr, mask, lpp);
+      res_block_s<R, PAIR, CH>(lane_base + b * PB, xr, mask, lpp);
       __syncwarp();
       reduce_lane_partials(lp, redw, bbase[b], __popc(mask), lane);
       __syncwarp();
@@ -1083,14 +1083,26 @@ const ResVariant kRes[] = {
     {36, 32, k_res_s<36, 4>, smem_res_s<36>()},
     {44, 32, k_res_s<44, 3>, smem_res_s<44>()},
     {60, 32, k_res_s<60, 2>, smem_res_s<60>()},
-    {52, 32, k_res_s<52, 3, true>, smem_res_s<52>()},  // 12: pair tests; large-n default (C3: 23.3 ms)
+    {52, 32, k_res_s<52, 3, true>, smem_res_s<52>()},  // 12: pair tests (C3: 23.3 ms)
     {44, 32, k_res_s<44, 3, true>, smem_res_s<44>()},
+    {52, 32, k_res_s<52, 3, true, 3>, smem_res_s<52>()},  // 14: dot chains 3 / 6 / 8 / 2
+    {52, 32, k_res_s<52, 3, true, 6>, smem_res_s<52>()},
+    {52, 32, k_res_s<52, 3, true, 8>, smem_res_s<52>()},
+    {52, 32, k_res_s<52, 3, true, 2>, smem_res_s<52>()},  // 17: large-n default (C3: 21.2 ms)
+    {52, 32, k_res_s<52, 2, true, 4>, smem_res_s<52>()},  // 18: 2 CTAs/SM (more registers)
+    {52, 32, k_res_s<52, 2, true, 8>, smem_res_s<52>()},
+    {52, 32, k_res_s<52, 3, true, 1>, smem_res_s<52>()},  // 20: one chain
+    {60, 32, k_res_s<60, 3, true, 2>, smem_res_s<60>()},
+    {44, 32, k_res_s<44, 4, true, 2>, smem_res_s<44>()},
+    {52, 32, k_res_s<52, 4, true, 2>, smem_res_s<52>()},
+    {68, 32, k_res_s<68, 3, true, 2>, smem_res_s<68>()},
+    {44, 32, k_res_s<44, 3, true, 2>, smem_res_s<44>()},
 };
 // Defaults (measured best on B200, tools/variants.py): the streamed-window
 // kernels with pair tests at large n; the R = 32 padded kernels at small n,
 // where a 4096-index tile already covers the whole problem.
 constexpr int64_t kLargeN = int64_t(1) << 17;
-constexpr int kGradLarge = 13, kGradSmall = 0, kResLarge = 12, kResSmall = 0;
+constexpr int kGradLarge = 13, kGradSmall = 0, kResLarge = 17, kResSmall = 0;
 int g_grad = -1, g_res = -1;  // -1: choose by n
 
 }  // namespace
