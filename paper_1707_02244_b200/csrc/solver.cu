@@ -39,21 +39,31 @@ void cuda_check(cudaError_t e, const char* what) {
 }
 #define CU(x) cuda_check((x), #x)
 
+// Device buffer from the device's stream-ordered memory pool (cudaMallocAsync;
+// the pool keeps freed memory reserved, see reserve_pool), so creating and
+// destroying solver states does not pay cudaMalloc/cudaFree (a cudaFree of
+// the residual's 165 MB partial buffer synchronizes the device and unmaps:
+// ~0.2-1.6 s per state destruction at n = 2^20, measured).  `st` orders the
+// allocation and the free after the work on that stream; it must outlive the
+// buffer (nullptr: the legacy stream, after the caller synchronized).
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
   size_t count = 0;
+  cudaStream_t s = nullptr;
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  ~DevBuf() {
-    if (p) cudaFree(p);
-  }
-  void alloc(size_t c) {
-    if (p) cudaFree(p);
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
     p = nullptr;
+  }
+  void alloc(size_t c, cudaStream_t st = nullptr) {
+    release();
     count = c;
-    if (c) CU(cudaMalloc(&p, sizeof(T) * c));
+    s = st;
+    if (c) CU(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * c, st));
   }
   void upload(const T* h, size_t c, cudaStream_t st) {
     if (c) CU(cudaMemcpyAsync(p, h, sizeof(T) * c, cudaMemcpyHostToDevice, st));
@@ -73,6 +83,16 @@ std::vector<float> reversed(const std::vector<float>& a) {  // r[k] = a[(-k) mod
   std::vector<float> r(n);
   for (size_t k = 0; k < n; ++k) r[k] = a[(n - k) % n];
   return r;
+}
+
+// Keep freed pool memory reserved for the next state (HBM is not returned to
+// the OS between solves; 180 GB per GPU).
+void reserve_pool(int device) {
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
 }
 
 double seconds_since(std::chrono::steady_clock::time_point a) {
@@ -132,6 +152,16 @@ struct Solver {
   bool has_truth = false;
   bool profile = false;
   cudaStream_t st = nullptr;
+  // Destroys st after every DevBuf member (declared below) has queued its free.
+  struct StreamOwner {
+    cudaStream_t* s;
+    ~StreamOwner() {
+      if (*s) {
+        cudaStreamSynchronize(*s);
+        cudaStreamDestroy(*s);
+      }
+    }
+  } st_owner{&st};
   ConvPlan plan;     // outputs: gradient (ISTA) or dense (cADMM) products
   ConvPlan rplan;    // ISTA residual (input tiles x position splits)
   int64_t row_lo = 0, row_hi = 0;  // ISTA rows owned (residual)
@@ -158,6 +188,7 @@ struct Solver {
   cudaGraphExec_t graph = nullptr;
 
   ~Solver() {
+    if (st) cudaSetDevice(device);
     if (st) cudaStreamSynchronize(st);
     if (graph) cudaGraphExecDestroy(graph);
     for (auto& e : ev)
@@ -165,7 +196,6 @@ struct Solver {
     for (auto& e : step_ev)
       if (e) cudaEventDestroy(e);
     if (met_host) cudaFreeHost(met_host);
-    if (st) cudaStreamDestroy(st);
   }
 
   void init_device() {
@@ -174,6 +204,7 @@ struct Solver {
     if (device < 0 || device >= count) raise(CL_ECUDA, "cl_solver_create: no such CUDA device");
     CU(cudaSetDevice(device));
     CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    reserve_pool(device);
     for (auto& e : ev) CU(cudaEventCreate(&e));
     for (auto& e : step_ev) CU(cudaEventCreate(&e));
     CU(cudaMallocHost(&met_host, sizeof(double) * 4));
@@ -185,9 +216,9 @@ struct Solver {
     std::vector<int> om(static_cast<size_t>(m));
     for (int64_t t2 = 0; t2 < m; ++t2) om[static_cast<size_t>(t2)] = static_cast<int>(omega[t2]);
     rowstart_host = chunk_rowstart(omega, m, plan.chunks);
-    omega32.alloc(static_cast<size_t>(m));
+    omega32.alloc(static_cast<size_t>(m), st);
     omega32.upload(om.data(), static_cast<size_t>(m), st);
-    rowstart.alloc(rowstart_host.size());
+    rowstart.alloc(rowstart_host.size(), st);
     rowstart.upload(rowstart_host.data(), rowstart_host.size(), st);
   }
 
@@ -208,16 +239,61 @@ struct Solver {
     if (fft && !is_pow2(n)) raise(CL_EPARAM, "cl_solver_create: the FFT engine needs a power-of-two n");
   }
 
-  // solvers.hpp:170-183
-  double normalization(const double* c, const double* yh) {
-    for (int64_t i = 0; i < m; ++i)
-      if (!std::isfinite(yh[i])) raise(CL_EDIVERGE, "solver: measurements contain non-finite entries");
-    const double s = spectral_norm(c, n);
+  // solvers.hpp:170-183.  `s` = max_k |DFT(c)_k| (host or device transform).
+  double normalization_from(double s, const double* yh) {
     if (s > 0.0) return s;
     double mx = 0.0;
     for (int64_t i = 0; i < m; ++i) mx = std::max(mx, std::abs(yh[i]));
     if (m == 0 || mx == 0.0) return 1.0;
     raise(CL_ESINGULAR, "solver: sensing operator is zero but measurements are not");
+  }
+  void check_finite_y(const double* yh) {
+    for (int64_t i = 0; i < m; ++i)
+      if (!std::isfinite(yh[i])) raise(CL_EDIVERGE, "solver: measurements contain non-finite entries");
+  }
+
+  // ---- setup transforms on the device (power-of-two n) ----------------------
+  // The reference runs them once per solve in fp64 (circulant.hpp:297-351);
+  // so do we, with the fp64 Stockham FFT of fft.cu, instead of a host FFT.
+  bool device_setup() const {
+    const char* v = std::getenv("CLB_HOST_SETUP");  // 1: host fp64 transforms (parity tests)
+    return !(v && v[0] == '1') && is_pow2(n) && n >= (int64_t(1) << 14);
+  }
+  DevBuf<double> c64, b64;
+  DevBuf<double2> X64, W64, B64;
+  DevBuf<unsigned long long> red;  // [absmax, min denominator, max |re|, max |im|] as IEEE bits
+  const double2* spec64 = nullptr;   // DFT(c), in X64 or W64
+
+  void red_reset() {
+    const unsigned long long init[4] = {0ull, 0x7ff0000000000000ull /* +inf */, 0ull, 0ull};
+    if (!red.p) red.alloc(4, st);
+    CU(cudaMemcpyAsync(red.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    CU(cudaStreamSynchronize(st));  // `init` is a stack array
+  }
+  void red_read(double out[4]) {
+    unsigned long long h[4];
+    CU(cudaMemcpyAsync(h, red.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    for (int i = 0; i < 4; ++i) std::memcpy(&out[i], &h[i], sizeof(double));
+  }
+  // uploads c (fp64), spec64 = DFT(c); returns max_k |DFT(c)_k|
+  double device_spectrum(const double* c) {
+    c64.alloc(static_cast<size_t>(n), st);
+    c64.upload(c, static_cast<size_t>(n), st);
+    X64.alloc(static_cast<size_t>(n), st);
+    W64.alloc(static_cast<size_t>(n), st);
+    launch_real_to_complex64(c64.p, X64.p, n, st);
+    spec64 = fft64_run(X64.p, W64.p, n, false, st);
+    red_reset();
+    launch_absmax64(spec64, n, red.p, st);
+    double r[4];
+    red_read(r);
+    return r[0];
+  }
+  void device_setup_release() {
+    for (DevBuf<double>* b : {&c64, &b64}) b->release();
+    for (DevBuf<double2>* b : {&X64, &W64, &B64}) b->release();
+    spec64 = nullptr;
   }
 
   void setup_ista(const double* c, const int64_t* omega, const double* yh) {  // solvers.hpp:222-249
@@ -227,35 +303,49 @@ struct Solver {
       raise(CL_EPARAM,
             "ista_setup: tau must lie in (0, |A|_2^-2); on the normalized operator the admissible range is (0, 1)");
     if (!(cfg.alpha > 0.0)) raise(CL_EPARAM, "ista_setup: alpha must be > 0");
-    scale = normalization(c, yh);
+    check_finite_y(yh);
+    const bool dev = device_setup();
+    if (dev) init_device();
+    scale = normalization_from(dev ? device_spectrum(c) : spectral_norm(c, n), yh);
     tau = tau0;
     thr = cfg.pairing == CL_PAIRING_LITERAL ? cfg.alpha : tau0 * cfg.alpha;
-    init_device();
+    if (!dev) init_device();
     plan = make_plan(n, grad_R(n));
     rplan = make_plan(n, res_R(n));
-    const std::vector<float> cf = to_f32(c, n, scale);
-    hc.alloc(static_cast<size_t>(n));
-    hc.upload(cf.data(), cf.size(), st);
-    const std::vector<float> crf = reversed(cf);
-    hcr.alloc(static_cast<size_t>(n));
-    hcr.upload(crf.data(), crf.size(), st);
+    hc.alloc(static_cast<size_t>(n), st);
+    hcr.alloc(static_cast<size_t>(n), st);
+    if (dev) {
+      launch_rows_f32(c64.p, scale, hc.p, hcr.p, n, st);
+    } else {
+      const std::vector<float> cf = to_f32(c, n, scale);
+      hc.upload(cf.data(), cf.size(), st);
+      const std::vector<float> crf = reversed(cf);
+      hcr.upload(crf.data(), crf.size(), st);
+    }
     build_rows(omega);
     const std::vector<float> yf = to_f32(yh, m, scale);
-    y.alloc(static_cast<size_t>(m));
+    y.alloc(static_cast<size_t>(m), st);
     y.upload(yf.data(), yf.size(), st);
-    for (DevBuf<float>* b : {&r}) { b->alloc(static_cast<size_t>(m)); b->zero(st); }
-    for (DevBuf<float>* b : {&x, &delta}) { b->alloc(static_cast<size_t>(n)); b->zero(st); }
-    partial.alloc(static_cast<size_t>(std::max<int64_t>(rplan.tiles * m, plan.splits * n)));
-    blk.alloc(kEpiBlocks * 4);
-    met.alloc(4);
+    for (DevBuf<float>* b : {&r}) { b->alloc(static_cast<size_t>(m), st); b->zero(st); }
+    for (DevBuf<float>* b : {&x, &delta}) { b->alloc(static_cast<size_t>(n), st); b->zero(st); }
+    partial.alloc(static_cast<size_t>(std::max<int64_t>(rplan.tiles * m, plan.splits * n)), st);
+    blk.alloc(kEpiBlocks * 4, st);
+    met.alloc(4, st);
     set_shard(0, 1);
     if (fft) {
-      std::vector<double> cn(static_cast<size_t>(n));
-      for (int64_t i = 0; i < n; ++i) cn[static_cast<size_t>(i)] = c[i] / scale;
-      upload_spectrum(chat, dft_real(cn.data(), n));
-      F0.alloc(static_cast<size_t>(n));
-      F1.alloc(static_cast<size_t>(n));
+      if (dev) {
+        chat.alloc(static_cast<size_t>(n), st);
+        launch_spectrum_f32(spec64, scale, chat.p, n, st);
+      } else {
+        std::vector<double> cn(static_cast<size_t>(n));
+        for (int64_t i = 0; i < n; ++i) cn[static_cast<size_t>(i)] = c[i] / scale;
+        upload_spectrum(chat, dft_real(cn.data(), n));
+      }
+      F0.alloc(static_cast<size_t>(n), st);
+      F1.alloc(static_cast<size_t>(n), st);
     }
+    CU(cudaGetLastError());
+    device_setup_release();
     CU(cudaStreamSynchronize(st));
   }
 
@@ -263,8 +353,38 @@ struct Solver {
     std::vector<float2> f(spec.size());
     for (size_t k = 0; k < spec.size(); ++k)
       f[k] = make_float2(static_cast<float>(spec[k].real()), static_cast<float>(spec[k].imag()));
-    dst.alloc(f.size());
+    dst.alloc(f.size(), st);
     dst.upload(f.data(), f.size(), st);
+  }
+
+  // B = (rho C~^T C~ + sigma I)^-1 on the device: b = idft(1 / (rho |DFT(c)/s|^2 + sigma))
+  // with the reference's floor (circulant.hpp:309-316) and residue check (fft.hpp:74-89).
+  void device_gram_inverse(double s) {
+    if (cfg.rho < 0.0 || cfg.sigma < 0.0 || (cfg.rho == 0.0 && cfg.sigma == 0.0))
+      raise(CL_EPARAM,
+            "regularized_gram_inverse: rho and sigma must be nonnegative with at least one strictly positive");
+    B64.alloc(static_cast<size_t>(n), st);
+    if (fft) bhat.alloc(static_cast<size_t>(n), st);
+    red_reset();
+    launch_gram_spectrum(spec64, s, cfg.rho, cfg.sigma, B64.p, fft ? bhat.p : nullptr, red.p + 1, n, st);
+    double2* scratch = spec64 == X64.p ? W64.p : X64.p;
+    const double2* Y = fft64_run(B64.p, scratch, n, true, st);
+    b64.alloc(static_cast<size_t>(n), st);
+    launch_real_part64(Y, b64.p, red.p + 2, red.p + 3, n, st);
+    double r[4];
+    red_read(r);
+    if (r[1] < 1e-14) {
+      std::ostringstream msg;
+      msg << "regularized_gram_inverse: an eigenvalue of (rho C^T C + sigma I) is " << r[1]
+          << ", below the invertibility floor 1e-14";
+      raise(CL_ESINGULAR, msg.str());
+    }
+    const double sc = std::max(1.0, r[2]);
+    if (r[3] > 1e-10 * sc) {
+      std::ostringstream msg;
+      msg << "inverse DFT of a real-valued quantity has imaginary residue " << r[3] << " (relative tolerance 1e-10)";
+      raise(CL_ECONSIST, msg.str());
+    }
   }
 
   void setup_cadmm(const double* c, const int64_t* omega, const double* yh) {  // solvers.hpp:359-395
@@ -273,47 +393,65 @@ struct Solver {
     constexpr double kGolden = 1.6180339887498949;
     if (!(cfg.tau1 > 0.0) || cfg.tau1 >= kGolden || !(cfg.tau2 > 0.0) || cfg.tau2 >= kGolden)
       raise(CL_EPARAM, "cadmm_setup: tau1 and tau2 must lie in (0, (sqrt(5)+1)/2)");
-    scale = normalization(c, yh);
-    std::vector<double> cn(static_cast<size_t>(n));
-    for (int64_t i = 0; i < n; ++i) cn[static_cast<size_t>(i)] = c[i] / scale;
-    std::vector<double> bh(static_cast<size_t>(n)), dh(static_cast<size_t>(n));
-    regularized_gram_inverse(cn.data(), n, cfg.rho, cfg.sigma, bh.data());
+    check_finite_y(yh);
+    const bool dev = device_setup();
+    if (dev) init_device();
+    scale = normalization_from(dev ? device_spectrum(c) : spectral_norm(c, n), yh);
+    if (!dev) init_device();
+    plan = make_plan(n, kRDense);
+    hc.alloc(static_cast<size_t>(n), st);
+    hcr.alloc(static_cast<size_t>(n), st);
+    hbr.alloc(static_cast<size_t>(n), st);
+    if (dev) {
+      device_gram_inverse(scale);
+      launch_rows_f32(c64.p, scale, hc.p, hcr.p, n, st);
+      launch_rows_f32(b64.p, 1.0, nullptr, hbr.p, n, st);
+      if (fft) {
+        chat.alloc(static_cast<size_t>(n), st);
+        launch_spectrum_f32(spec64, scale, chat.p, n, st);
+      }
+    } else {
+      std::vector<double> cn(static_cast<size_t>(n));
+      for (int64_t i = 0; i < n; ++i) cn[static_cast<size_t>(i)] = c[i] / scale;
+      std::vector<double> bh(static_cast<size_t>(n));
+      regularized_gram_inverse(cn.data(), n, cfg.rho, cfg.sigma, bh.data());
+      const std::vector<float> cf = to_f32(cn.data(), n);
+      hc.upload(cf.data(), cf.size(), st);
+      const std::vector<float> crf = reversed(cf);
+      hcr.upload(crf.data(), crf.size(), st);
+      const std::vector<float> brf = reversed(to_f32(bh.data(), n));
+      hbr.upload(brf.data(), brf.size(), st);
+      if (fft) {
+        const std::vector<cplx> cs = dft_real(cn.data(), n);
+        upload_spectrum(chat, cs);
+        // B's spectrum is real: 1 / (rho |c_k|^2 + sigma) (circulant.hpp:306-317), exact before the idft round trip
+        std::vector<cplx> bs(cs.size());
+        for (size_t k = 0; k < cs.size(); ++k) bs[k] = cplx(1.0 / (cfg.rho * std::norm(cs[k]) + cfg.sigma), 0.0);
+        upload_spectrum(bhat, bs);
+      }
+    }
+    std::vector<double> dh(static_cast<size_t>(n));
     mask_gram_inverse(omega, m, n, cfg.rho, dh.data());
     std::vector<double> ptyh(static_cast<size_t>(n), 0.0);
     for (int64_t t2 = 0; t2 < m; ++t2) ptyh[static_cast<size_t>(omega[t2])] = yh[t2] / scale;
     thr = cfg.alpha / cfg.sigma;
-    init_device();
-    plan = make_plan(n, kRDense);
-    const std::vector<float> cf = to_f32(cn.data(), n);
-    hc.alloc(static_cast<size_t>(n));
-    hc.upload(cf.data(), cf.size(), st);
-    const std::vector<float> crf = reversed(cf);
-    hcr.alloc(static_cast<size_t>(n));
-    hcr.upload(crf.data(), crf.size(), st);
-    const std::vector<float> brf = reversed(to_f32(bh.data(), n));
-    hbr.alloc(static_cast<size_t>(n));
-    hbr.upload(brf.data(), brf.size(), st);
     const std::vector<float> df = to_f32(dh.data(), n), pf = to_f32(ptyh.data(), n);
-    d.alloc(static_cast<size_t>(n));
+    d.alloc(static_cast<size_t>(n), st);
     d.upload(df.data(), df.size(), st);
-    pty.alloc(static_cast<size_t>(n));
+    pty.alloc(static_cast<size_t>(n), st);
     pty.upload(pf.data(), pf.size(), st);
-    for (DevBuf<float>* b : {&x, &z, &nu, &mu, &v, &beta}) { b->alloc(static_cast<size_t>(n)); b->zero(st); }
-    partial.alloc(static_cast<size_t>(plan.splits * n));
-    blk.alloc(kEpiBlocks * 4);
-    met.alloc(4);
+    for (DevBuf<float>* b : {&x, &z, &nu, &mu, &v, &beta}) { b->alloc(static_cast<size_t>(n), st); b->zero(st); }
+    partial.alloc(static_cast<size_t>(plan.splits * n), st);
+    blk.alloc(kEpiBlocks * 4, st);
+    met.alloc(4, st);
     rowstart_host.assign(static_cast<size_t>(plan.chunks + 1), 0);
     if (fft) {
-      const std::vector<cplx> cs = dft_real(cn.data(), n);
-      upload_spectrum(chat, cs);
-      // B's spectrum is real: 1 / (rho |c_k|^2 + sigma) (circulant.hpp:306-317), exact before the idft round trip
-      std::vector<cplx> bs(cs.size());
-      for (size_t k = 0; k < cs.size(); ++k) bs[k] = cplx(1.0 / (cfg.rho * std::norm(cs[k]) + cfg.sigma), 0.0);
-      upload_spectrum(bhat, bs);
-      F0.alloc(static_cast<size_t>(n));
-      F1.alloc(static_cast<size_t>(n));
+      F0.alloc(static_cast<size_t>(n), st);
+      F1.alloc(static_cast<size_t>(n), st);
     }
     set_shard(0, 1);
+    CU(cudaGetLastError());
+    device_setup_release();
     CU(cudaStreamSynchronize(st));
   }
 
@@ -595,6 +733,7 @@ struct ScratchProduct {
   static void circ(int device, int64_t n, const double* c, const double* xin, int transpose, double* out) {
     CU(cudaSetDevice(device));
     conv_kernels_init();
+    reserve_pool(device);
     cudaStream_t st;
     CU(cudaStreamCreate(&st));
     ConvPlan p = make_plan(n, kRDense);
@@ -761,16 +900,16 @@ cl_status cl_partial_matvec(int device, int64_t n, int64_t m, const double* c, c
   s.plan = make_plan(n, grad_R(n));
   s.rplan = make_plan(n, res_R(n));
   const std::vector<float> crf = reversed(to_f32(c, n));
-  s.hcr.alloc(static_cast<size_t>(n));
+  s.hcr.alloc(static_cast<size_t>(n), s.st);
   s.hcr.upload(crf.data(), crf.size(), s.st);
   s.build_rows(omega);
   const std::vector<float> xf = to_f32(xin, n);
-  s.x.alloc(static_cast<size_t>(n));
+  s.x.alloc(static_cast<size_t>(n), s.st);
   s.x.upload(xf.data(), xf.size(), s.st);
-  s.y.alloc(static_cast<size_t>(m));
+  s.y.alloc(static_cast<size_t>(m), s.st);
   s.y.zero(s.st);
-  s.r.alloc(static_cast<size_t>(m));
-  s.partial.alloc(static_cast<size_t>(s.rplan.tiles * m));
+  s.r.alloc(static_cast<size_t>(m), s.st);
+  s.partial.alloc(static_cast<size_t>(s.rplan.tiles * m), s.st);
   s.set_shard(0, 1);
   s.ista_residual();
   CU(cudaGetLastError());
@@ -793,14 +932,14 @@ cl_status cl_partial_transpose_matvec(int device, int64_t n, int64_t m, const do
   s.init_device();
   s.plan = make_plan(n, grad_R(n));
   const std::vector<float> cf = to_f32(c, n);
-  s.hc.alloc(static_cast<size_t>(n));
+  s.hc.alloc(static_cast<size_t>(n), s.st);
   s.hc.upload(cf.data(), cf.size(), s.st);
   s.build_rows(omega);
   const std::vector<float> rf = to_f32(r_m, m);
-  s.r.alloc(static_cast<size_t>(m));
+  s.r.alloc(static_cast<size_t>(m), s.st);
   s.r.upload(rf.data(), rf.size(), s.st);
-  s.partial.alloc(static_cast<size_t>(s.plan.splits * n));
-  s.x.alloc(static_cast<size_t>(n));
+  s.partial.alloc(static_cast<size_t>(s.plan.splits * n), s.st);
+  s.x.alloc(static_cast<size_t>(n), s.st);
   launch_conv_rows(s.plan, s.hc.p, s.omega32.p, s.r.p, s.rowstart.p, s.partial.p, s.st);
   EpiArgs a;
   a.partial = s.partial.p;
@@ -850,7 +989,7 @@ cl_status cl_solver_set_truth(cl_solver* h, const double* truth_n) {
     s.has_truth = false;
   } else {
     const std::vector<float> tf = to_f32(truth_n, s.n);
-    s.truth.alloc(static_cast<size_t>(s.n));
+    s.truth.alloc(static_cast<size_t>(s.n), s.st);
     s.truth.upload(tf.data(), tf.size(), s.st);
     CU(cudaStreamSynchronize(s.st));
     s.has_truth = true;

@@ -396,3 +396,53 @@ def test_sharded_step_over_nccl_world1():
         assert np.array_equal(st.get("x"), ref.get("x"))
     finally:
         dist.destroy_process_group()
+
+
+# ------------------------------------------------- setup transforms on the device
+def _states(kind, p, host_setup, iters=20, use_fft=False):
+    import os
+    old = os.environ.get("CLB_HOST_SETUP")
+    os.environ["CLB_HOST_SETUP"] = "1" if host_setup else "0"
+    try:
+        setup = cl.ista_setup if kind == "ista" else cl.cadmm_setup
+        g = setup(op_of(p), p.y, cl.SolverConfig(use_fft=use_fft))
+        g.step(iters)
+        return {f: g.get(f) for f in (("x", "r", "delta") if kind == "ista" else ("x", "z", "v", "mu", "nu", "beta"))}
+    finally:
+        if old is None:
+            del os.environ["CLB_HOST_SETUP"]
+        else:
+            os.environ["CLB_HOST_SETUP"] = old
+
+
+@pytest.mark.parametrize("kind,use_fft", [("ista", False), ("cadmm", False), ("ista", True), ("cadmm", True)])
+def test_device_setup_matches_host_setup(kind, use_fft):
+    """Spectral norm, Gram inverse and operator rows computed by the device fp64 FFT (n >= 2^14, power of
+    two) agree with the host fp64 transforms: the two setups differ only in fp64 rounding, far below fp32."""
+    p = orc.make_problem(1 << 16, 1 << 14, 1 << 8, 4)
+    dev = _states(kind, p, host_setup=False, use_fft=use_fft)
+    host = _states(kind, p, host_setup=True, use_fft=use_fft)
+    for f in dev:
+        assert rel_l2(dev[f], host[f]) <= 1e-6, (f, rel_l2(dev[f], host[f]))
+
+
+def test_cadmm_2p16_vs_fft_oracle():
+    """cADMM at n = 2^16 (device setup path) against the oracle's FFT engine."""
+    p = orc.make_problem(1 << 16, 1 << 14, 1 << 8, 6)
+    g = cl.cadmm_setup(op_of(p), p.y)
+    g.step(10)
+    o = orc.Cadmm(p.row, p.omega, p.y)
+    o.step(10, orc.ENGINE_FFT)
+    assert_parity(g.get("z"), o.get("z"), what="z")
+    for f in ("x", "v", "mu", "nu", "beta"):
+        assert rel_l2(g.get(f), o.get(f)) <= REL_TOL, f
+
+
+def test_device_gram_floor_raises():
+    """regularized_gram_inverse's 1e-14 invertibility floor (circulant.hpp:309-316) on the device path:
+    a constant first row has a zero spectrum off k = 0, so rho |c_k|^2 + sigma = sigma = 1e-15."""
+    n = 1 << 14
+    c = np.ones(n)
+    op = cl.PartialCirculantOperator(cl.CirculantMatrix(c), cl.SubsamplingMask(np.arange(0, n, 2), n))
+    with pytest.raises(cl.SingularityError):
+        cl.cadmm_setup(op, np.zeros(n // 2), cl.SolverConfig(sigma=1e-15))
