@@ -1,0 +1,389 @@
+// Four-step FFT engine for the circulant products (the reference's default
+// `use_fft=true` path, circulant.hpp:236-274), power-of-two 2^14 <= n <= 2^24.
+//
+// n = N1 * N2, natural index j = n1 * N2 + n2, spectral index k = k1 + N1 * k2.
+// One product y = idft(H . dft(u)) is three kernels and three passes over n
+// complex values (the Stockham engine of fft.cu needs ~4 log16(n) passes plus
+// the pointwise ones):
+//   cols_fwd : per column n2, DIF FFT over n1 (in shared memory) -> T[p][n2],
+//              p = a digit-reversed k1 (no reordering: convolution does not
+//              care about the spectral order as long as H uses the same one);
+//              the input is real (x, v, beta, or P^T r kept dense).
+//   rows     : per row p, twiddle w_n^{n2 k1}, DIF FFT over n2, multiply by
+//              H~[p][q] (H permuted to the same order), DIT inverse FFT over
+//              n2 (natural order again), twiddle w_n^{-n2 k1}; in place.
+//   cols_inv : per column, DIT inverse FFT over p -> natural n1, real part
+//              times 1/n, written as the product (or gathered at the rows).
+// DIF forward + DIT inverse = no bit reversal anywhere.  Every stage is an
+// in-place radix-16 (then 8/4/2) butterfly on shared memory with a twiddle
+// table; global loads and stores are coalesced row segments.
+#include <cstdint>
+#include <cstdio>
+#include <cmath>
+#include <vector>
+
+#include "fft4.cuh"
+
+namespace clb {
+namespace {
+
+constexpr int kThr = 256;
+constexpr int kElems = 4096;  // complex values per CTA (32 KB of shared memory + padding)
+
+__device__ __forceinline__ float2 cmulf(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cmulf_conj(float2 a, float2 b) {  // a * conj(b)
+  return make_float2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+
+__device__ constexpr float kC16[16] = {1.0f, 0.92387953251128674f, 0.70710678118654757f, 0.38268343236508978f, 0.0f,
+                                       -0.38268343236508978f, -0.70710678118654757f, -0.92387953251128674f, -1.0f,
+                                       -0.92387953251128674f, -0.70710678118654757f, -0.38268343236508978f, -0.0f,
+                                       0.38268343236508978f, 0.70710678118654757f, 0.92387953251128674f};
+__device__ constexpr float kS16[16] = {0.0f, 0.38268343236508978f, 0.70710678118654757f, 0.92387953251128674f, 1.0f,
+                                       0.92387953251128674f, 0.70710678118654757f, 0.38268343236508978f, 0.0f,
+                                       -0.38268343236508978f, -0.70710678118654757f, -0.92387953251128674f, -1.0f,
+                                       -0.92387953251128674f, -0.70710678118654757f, -0.38268343236508978f};
+
+// Radix-R DFT in registers, natural order in and out, sign SG.
+template <int R, int SG>
+__device__ __forceinline__ void dftr(float2 (&v)[R]) {
+  float2 t[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    int r = 0;
+#pragma unroll
+    for (int b = 1, j = i; b < R; b <<= 1, j >>= 1) r = (r << 1) | (j & 1);
+    t[r] = v[i];
+  }
+#pragma unroll
+  for (int half = 1; half < R; half <<= 1) {
+#pragma unroll
+    for (int base = 0; base < R; base += 2 * half) {
+#pragma unroll
+      for (int k = 0; k < half; ++k) {
+        const int e = k * (16 / (2 * half));
+        const float2 w = make_float2(kC16[e], SG * kS16[e]);
+        const float2 u = t[base + k];
+        const float2 x = cmulf(t[base + k + half], w);
+        t[base + k] = make_float2(u.x + x.x, u.y + x.y);
+        t[base + k + half] = make_float2(u.x - x.x, u.y - x.y);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < R; ++i) v[i] = t[i];
+}
+
+// Shared-memory layout: element i of sequence s at buf[s * sstride + pad(i)],
+// one complex of padding every 16 (the last DIF / first DIT stage reads 16
+// consecutive elements per thread; unpadded, all lanes would hit one bank).
+__host__ __device__ __forceinline__ int pad16(int i) { return i + (i >> 4); }
+
+constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
+// Radix schedule of a length-N transform: the remainder radix 2^(log2 N mod 4) first
+// (a large stride, conflict-free), then radix 16 down to the last stage.
+template <int N, int L>
+struct Radix {
+  static constexpr int value = (L == N && (ilog2(N) % 4) != 0) ? (1 << (ilog2(N) % 4)) : 16;
+};
+
+// One in-place stage on nseq sequences of length N in shared memory; sub-length L = R * M.
+//   DIF (SG = -1): V = DFT_R(v_r at j + rM); V_q *= w_L^{jq}; store at j + qM.
+//   DIT (SG = +1): v_q = x(j + qM) * w_L^{-jq}; V = IDFT_R(v); store V_r at j + rM.
+// tw[k] = e^{-2 pi i k / N}.
+template <int N, int L, int SG, int NSEQ>
+__device__ __forceinline__ void stage(float2* buf, int sstride, const float2* __restrict__ tw) {
+  constexpr int R = Radix<N, L>::value;
+  constexpr int M = L / R;
+  constexpr int per_seq = N / R;
+  constexpr int total = NSEQ * per_seq;
+  constexpr int twstep = N / L;
+  for (int idx = threadIdx.x; idx < total; idx += kThr) {
+    const int s = idx / per_seq, rem = idx - s * per_seq;
+    const int blk = rem / M, j = rem - blk * M;
+    float2* p = buf + s * sstride;
+    const int i0 = blk * L + j;
+    float2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = p[pad16(i0 + r * M)];
+    if (SG < 0) {
+      dftr<R, -1>(v);
+      if (M > 1) {
+#pragma unroll
+        for (int q = 1; q < R; ++q) v[q] = cmulf(v[q], __ldg(tw + j * q * twstep));
+      }
+    } else {
+      if (M > 1) {
+#pragma unroll
+        for (int q = 1; q < R; ++q) v[q] = cmulf_conj(v[q], __ldg(tw + j * q * twstep));
+      }
+      dftr<R, +1>(v);
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) p[pad16(i0 + r * M)] = v[r];
+  }
+}
+
+// Forward DIF over all stages (natural in, digit-reversed out).
+template <int N, int L, int NSEQ>
+__device__ __forceinline__ void dif_from(float2* buf, int sstride, const float2* tw) {
+  stage<N, L, -1, NSEQ>(buf, sstride, tw);
+  __syncthreads();
+  constexpr int next = L / Radix<N, L>::value;
+  if constexpr (next > 1) dif_from<N, next, NSEQ>(buf, sstride, tw);
+}
+// Inverse DIT: the DIF stages undone in reverse order (digit-reversed in, natural out; scale N).
+template <int N, int L, int NSEQ>
+__device__ __forceinline__ void dit_from(float2* buf, int sstride, const float2* tw) {
+  constexpr int next = L / Radix<N, L>::value;
+  if constexpr (next > 1) dit_from<N, next, NSEQ>(buf, sstride, tw);
+  stage<N, L, +1, NSEQ>(buf, sstride, tw);
+  __syncthreads();
+}
+
+// position p of a DIF output of length N holds frequency rev(p) (same radix schedule)
+__host__ __device__ __forceinline__ int digit_rev(int p, int N) {
+  int k = 0, mult = 1, lg = 0;
+  while ((1 << lg) < N) ++lg;
+  for (int L = N; L > 1;) {
+    const int R = (L == N && (lg % 4) != 0) ? (1 << (lg % 4)) : 16;
+    L /= R;
+    const int q = p / L;
+    p -= q * L;
+    k += q * mult;
+    mult *= R;
+  }
+  return k;
+}
+
+// ---- kernels -----------------------------------------------------------------
+// Columns per CTA and the column pitch: pitch = (16 / B) mod 16 (complex) keeps
+// the coalesced row-segment loads (B columns x 4 rows per half-warp) conflict-free.
+__host__ __device__ constexpr int cols_per_cta(int N1) { return N1 <= 1024 ? kElems / N1 : 4; }
+__host__ __device__ constexpr int col_pitch(int N1) {
+  return N1 + N1 / 16 + (cols_per_cta(N1) <= 16 ? 16 / cols_per_cta(N1) : 1);
+}
+__host__ __device__ constexpr int row_count(int N2) { return N2 >= kElems ? 1 : kElems / N2; }
+__host__ __device__ constexpr int row_pitch(int N2) { return N2 + N2 / 16 + 1; }
+
+// w_n^idx = e^{-2 pi i idx / n} = twB[idx >> 12] * twA[idx & 4095]
+__device__ __forceinline__ float2 tw_n(const float2* __restrict__ twA, const float2* __restrict__ twB, int idx) {
+  return cmulf(__ldg(twB + (idx >> 12)), __ldg(twA + (idx & 4095)));
+}
+
+// Columns forward: input real u[j] (j = n1 N2 + n2).
+template <int N1>
+__global__ void __launch_bounds__(kThr) k_cols_fwd(const float* __restrict__ u, float2* __restrict__ T, int N2,
+                                                   const float2* __restrict__ tw1) {
+  extern __shared__ float2 sm[];
+  constexpr int B = cols_per_cta(N1), P = col_pitch(N1), cnt = B * N1;
+  const int c0 = blockIdx.x * B;
+#pragma unroll
+  for (int e = threadIdx.x; e < cnt; e += kThr) {
+    const int i = e / B, w = e - i * B;
+    sm[w * P + pad16(i)] = make_float2(__ldg(u + static_cast<int64_t>(i) * N2 + c0 + w), 0.f);
+  }
+  __syncthreads();
+  dif_from<N1, N1, B>(sm, P, tw1);
+#pragma unroll
+  for (int e = threadIdx.x; e < cnt; e += kThr) {
+    const int i = e / B, w = e - i * B;
+    T[static_cast<int64_t>(i) * N2 + c0 + w] = sm[w * P + pad16(i)];
+  }
+}
+
+// Rows: row_count(N2) rows per CTA, in place on T.
+template <int N2>
+__global__ void __launch_bounds__(kThr) k_rows(float2* __restrict__ T, const float2* __restrict__ H, int conj_h, int N1,
+                                               const float2* __restrict__ tw2, const float2* __restrict__ twA,
+                                               const float2* __restrict__ twB) {
+  extern __shared__ float2 sm[];
+  constexpr int rows = row_count(N2), P = row_pitch(N2), cnt = rows * N2;
+  constexpr int per = (cnt + kThr - 1) / kThr;
+  __shared__ int k1s[rows];
+  const int p0 = blockIdx.x * rows;
+  if (threadIdx.x < rows) k1s[threadIdx.x] = digit_rev(p0 + threadIdx.x, N1);
+  __syncthreads();
+  float2 tw[per];  // w_n^{n2 k1} of this thread's elements (reused for the inverse twiddle)
+#pragma unroll
+  for (int k = 0; k < per; ++k) {
+    const int e = threadIdx.x + k * kThr;
+    if (e < cnt) {
+      const int rr = e / N2, n2 = e - rr * N2;
+      tw[k] = tw_n(twA, twB, n2 * k1s[rr]);
+      sm[rr * P + pad16(n2)] = cmulf(T[static_cast<int64_t>(p0) * N2 + e], tw[k]);
+    }
+  }
+  __syncthreads();
+  dif_from<N2, N2, rows>(sm, P, tw2);
+#pragma unroll
+  for (int e = threadIdx.x; e < cnt; e += kThr) {
+    const int rr = e / N2, q = e - rr * N2;
+    const float2 h = H[static_cast<int64_t>(p0) * N2 + e];
+    float2& a = sm[rr * P + pad16(q)];
+    a = conj_h ? cmulf_conj(a, h) : cmulf(a, h);
+  }
+  __syncthreads();
+  dit_from<N2, N2, rows>(sm, P, tw2);
+#pragma unroll
+  for (int k = 0; k < per; ++k) {
+    const int e = threadIdx.x + k * kThr;
+    if (e < cnt) {
+      const int rr = e / N2, n2 = e - rr * N2;
+      T[static_cast<int64_t>(p0) * N2 + e] = cmulf_conj(sm[rr * P + pad16(n2)], tw[k]);
+    }
+  }
+}
+
+// Columns inverse: out[j] = Re(.) / n (rowid == nullptr), or out[rowid[j]] for rows only.
+template <int N1>
+__global__ void __launch_bounds__(kThr) k_cols_inv(const float2* __restrict__ T, float* __restrict__ out,
+                                                   const int* __restrict__ rowid, int N2,
+                                                   const float2* __restrict__ tw1, float inv_n) {
+  extern __shared__ float2 sm[];
+  constexpr int B = cols_per_cta(N1), P = col_pitch(N1), cnt = B * N1;
+  const int c0 = blockIdx.x * B;
+#pragma unroll
+  for (int e = threadIdx.x; e < cnt; e += kThr) {
+    const int i = e / B, w = e - i * B;
+    sm[w * P + pad16(i)] = T[static_cast<int64_t>(i) * N2 + c0 + w];
+  }
+  __syncthreads();
+  dit_from<N1, N1, B>(sm, P, tw1);
+#pragma unroll
+  for (int e = threadIdx.x; e < cnt; e += kThr) {
+    const int i = e / B, w = e - i * B;
+    const int64_t j = static_cast<int64_t>(i) * N2 + c0 + w;
+    const float v = sm[w * P + pad16(i)].x * inv_n;
+    if (!rowid) {
+      out[j] = v;
+    } else {
+      const int t = __ldg(rowid + j);
+      if (t >= 0) out[t] = v;
+    }
+  }
+}
+
+// H~[p N2 + q] = spec[rev1(p) + N1 rev2(q)] / s  (fp64 spectrum -> permuted fp32)
+__global__ void k_perm_spectrum(const double2* __restrict__ spec, double s, float2* __restrict__ out, int N1, int N2) {
+  const int64_t n = static_cast<int64_t>(N1) * N2;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int p = static_cast<int>(e / N2), q = static_cast<int>(e - static_cast<int64_t>(p) * N2);
+    const int64_t k = digit_rev(p, N1) + static_cast<int64_t>(N1) * digit_rev(q, N2);
+    const double2 v = spec[k];
+    out[e] = make_float2(static_cast<float>(v.x / s), static_cast<float>(v.y / s));
+  }
+}
+
+__global__ void k_scatter_real(const float* __restrict__ r, const int* __restrict__ omega, float* __restrict__ u,
+                               int64_t m) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x)
+    u[omega[t]] = r[t];
+}
+
+
+}  // namespace
+
+bool fft4_supported(int64_t n) { return n >= (int64_t(1) << 14) && n <= (int64_t(1) << 24) && (n & (n - 1)) == 0; }
+
+Fft4Plan fft4_plan(int64_t n) {
+  Fft4Plan p;
+  int L = 0;
+  while ((int64_t(1) << L) < n) ++L;
+  p.n = n;
+  int l1 = L / 2;
+  if (l1 > 11) l1 = 11;
+  p.N1 = 1 << l1;
+  p.N2 = static_cast<int>(n >> l1);
+  return p;
+}
+
+void fft4_twiddles(const Fft4Plan& p, std::vector<float2>* tw1, std::vector<float2>* tw2, std::vector<float2>* twA,
+                   std::vector<float2>* twB) {
+  auto table = [](std::vector<float2>& t, int count, double step) {
+    t.resize(static_cast<size_t>(count));
+    for (int k = 0; k < count; ++k) {
+      const double a = -2.0 * M_PI * k * step;
+      t[static_cast<size_t>(k)] = make_float2(static_cast<float>(std::cos(a)), static_cast<float>(std::sin(a)));
+    }
+  };
+  table(*tw1, p.N1, 1.0 / p.N1);
+  table(*tw2, p.N2, 1.0 / p.N2);
+  const double nn = static_cast<double>(p.n);
+  table(*twA, 4096, 1.0 / nn);                                              // e^{-2 pi i a / n}
+  table(*twB, static_cast<int>(std::max<int64_t>(1, p.n / 4096)), 4096.0 / nn);  // e^{-2 pi i 4096 b / n}
+}
+
+template <int N>
+static size_t cols_smem_t() { return static_cast<size_t>(cols_per_cta(N)) * col_pitch(N) * sizeof(float2); }
+template <int N>
+static size_t rows_smem_t() { return static_cast<size_t>(row_count(N)) * row_pitch(N) * sizeof(float2); }
+
+#define CLB_FFT4_SIZES(X) X(128) X(256) X(512) X(1024) X(2048) X(4096) X(8192)
+
+void fft4_init_attributes() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+#define CLB_ATTR(N)                                                                                             \
+  cudaFuncSetAttribute(k_cols_fwd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem_t<N>());     \
+  cudaFuncSetAttribute(k_cols_inv<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem_t<N>());     \
+  cudaFuncSetAttribute(k_rows<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem_t<N>());
+  CLB_FFT4_SIZES(CLB_ATTR)
+#undef CLB_ATTR
+}
+
+void launch_fft4_cols_fwd(const Fft4Plan& p, const float* u, float2* T, const float2* tw1, cudaStream_t st) {
+  switch (p.N1) {
+#define CLB_CASE(N) \
+  case N: k_cols_fwd<N><<<p.N2 / cols_per_cta(N), kThr, cols_smem_t<N>(), st>>>(u, T, p.N2, tw1); break;
+    CLB_FFT4_SIZES(CLB_CASE)
+#undef CLB_CASE
+  }
+}
+void launch_fft4_rows(const Fft4Plan& p, float2* T, const float2* H, bool conj_h, const float2* tw2,
+                      const float2* twA, const float2* twB, cudaStream_t st) {
+  switch (p.N2) {
+#define CLB_CASE(N)                                                                                   \
+  case N:                                                                                             \
+    k_rows<N><<<p.N1 / row_count(N), kThr, rows_smem_t<N>(), st>>>(T, H, conj_h ? 1 : 0, p.N1, tw2, twA, twB); \
+    break;
+    CLB_FFT4_SIZES(CLB_CASE)
+#undef CLB_CASE
+  }
+}
+void launch_fft4_cols_inv(const Fft4Plan& p, const float2* T, float* out, const int* rowid, const float2* tw1,
+                          cudaStream_t st) {
+  const float inv_n = 1.0f / static_cast<float>(p.n);
+  switch (p.N1) {
+#define CLB_CASE(N)                                                                                     \
+  case N:                                                                                               \
+    k_cols_inv<N><<<p.N2 / cols_per_cta(N), kThr, cols_smem_t<N>(), st>>>(T, out, rowid, p.N2, tw1, inv_n); \
+    break;
+    CLB_FFT4_SIZES(CLB_CASE)
+#undef CLB_CASE
+  }
+}
+void launch_fft4_perm_spectrum(const Fft4Plan& p, const double2* spec, double s, float2* out, cudaStream_t st) {
+  k_perm_spectrum<<<148 * 8, 256, 0, st>>>(spec, s, out, p.N1, p.N2);
+}
+void launch_scatter_real(const float* r, const int* omega, float* u, int64_t m, cudaStream_t st) {
+  if (m > 0) k_scatter_real<<<148 * 4, 256, 0, st>>>(r, omega, u, m);
+}
+
+}  // namespace clb
+
+namespace clb {
+namespace {
+__global__ void k_rowid(const int* __restrict__ omega, int* __restrict__ rowid, int64_t m) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x)
+    rowid[omega[t]] = static_cast<int>(t);
+}
+}  // namespace
+void launch_rowid(const int* omega, int* rowid, int64_t n, int64_t m, cudaStream_t st) {
+  cudaMemsetAsync(rowid, 0xff, sizeof(int) * n, st);  // -1: not a row
+  if (m > 0) k_rowid<<<148 * 4, 256, 0, st>>>(omega, rowid, m);
+}
+}  // namespace clb

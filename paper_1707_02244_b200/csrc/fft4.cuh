@@ -1,0 +1,33 @@
+// Four-step FFT engine (fp32 complex, power-of-two 2^14 <= n <= 2^24); see fft4.cu.
+#pragma once
+#include <cstdint>
+#include <vector>
+#include <cuda_runtime.h>
+
+namespace clb {
+struct Fft4Plan {
+  int64_t n = 0;
+  int N1 = 0, N2 = 0;  // n = N1 * N2; columns of length N1, rows of length N2
+};
+bool fft4_supported(int64_t n);
+Fft4Plan fft4_plan(int64_t n);
+// twiddle tables (host, fp64-accurate fp32): e^{-2 pi i k / N1}, e^{-2 pi i k / N2}, and the
+// two factors of e^{-2 pi i idx / n} = twB[idx >> 12] * twA[idx & 4095]
+void fft4_twiddles(const Fft4Plan& p, std::vector<float2>* tw1, std::vector<float2>* tw2, std::vector<float2>* twA,
+                   std::vector<float2>* twB);
+void fft4_init_attributes();
+// u real (n) -> T: column DIF FFTs (spectral order permuted)
+void launch_fft4_cols_fwd(const Fft4Plan& p, const float* u, float2* T, const float2* tw1, cudaStream_t st);
+// in place: twiddle, row DIF FFT, times H~ (or conj), row DIT inverse FFT, inverse twiddle
+void launch_fft4_rows(const Fft4Plan& p, float2* T, const float2* H, bool conj_h, const float2* tw2,
+                      const float2* twA, const float2* twB, cudaStream_t st);
+// T -> column DIT inverse FFTs; out[j] = Re / n, or (rowid) out[rowid[j]] for positions with rowid[j] >= 0
+void launch_fft4_cols_inv(const Fft4Plan& p, const float2* T, float* out, const int* rowid, const float2* tw1,
+                          cudaStream_t st);
+// natural-order fp64 spectrum / s -> the engine's permuted fp32 order
+void launch_fft4_perm_spectrum(const Fft4Plan& p, const double2* spec, double s, float2* out, cudaStream_t st);
+// rowid[j] = t for j = omega[t], -1 elsewhere
+void launch_rowid(const int* omega, int* rowid, int64_t n, int64_t m, cudaStream_t st);
+// u[omega[t]] = r[t]
+void launch_scatter_real(const float* r, const int* omega, float* u, int64_t m, cudaStream_t st);
+}  // namespace clb

@@ -14,12 +14,14 @@
 #include <memory>
 #include <sstream>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include <cuda_runtime.h>
 
 #include "host_common.hpp"
 #include "fft.cuh"
+#include "fft4.cuh"
 #include "kernels.cuh"
 
 namespace clb {
@@ -174,6 +176,13 @@ struct Solver {
   DevBuf<float> partial, truth;
   DevBuf<float2> chat, bhat, F0, F1;  // FFT engine: spectra of c~ (and of B), work buffers
   bool fft = false;
+  // Four-step FFT engine (fft4.cu; power-of-two 2^14 <= n <= 2^24 with the device setup): the
+  // spectra in its permuted order, twiddle tables, the row map and P^T r kept dense.
+  bool fft4 = false;
+  Fft4Plan f4;
+  DevBuf<float2> tw1, tw2, twA, twB, chatp, bhatp;
+  DevBuf<int> rowid;
+  DevBuf<float> ud;
   DevBuf<double> blk, met;
   double* met_host = nullptr;
   std::vector<int> rowstart_host;
@@ -290,6 +299,27 @@ struct Solver {
     red_read(r);
     return r[0];
   }
+  bool want_fft4(bool dev) const {
+    const char* v = std::getenv("CLB_FFT_STOCKHAM");  // 1: the multi-pass Stockham engine (fft.cu)
+    return fft && dev && fft4_supported(n) && !(v && v[0] == '1');
+  }
+  void setup_fft4_common() {
+    fft4 = true;
+    f4 = fft4_plan(n);
+    fft4_init_attributes();
+    std::vector<float2> t1, t2, ta, tb;
+    fft4_twiddles(f4, &t1, &t2, &ta, &tb);
+    for (auto& pr : {std::make_pair(&tw1, &t1), std::make_pair(&tw2, &t2), std::make_pair(&twA, &ta),
+                     std::make_pair(&twB, &tb)}) {
+      pr.first->alloc(pr.second->size(), st);
+      pr.first->upload(pr.second->data(), pr.second->size(), st);
+    }
+    chatp.alloc(static_cast<size_t>(n), st);
+    launch_fft4_perm_spectrum(f4, spec64, scale, chatp.p, st);
+    F0.alloc(static_cast<size_t>(n), st);
+    CU(cudaStreamSynchronize(st));  // the host twiddle vectors go out of scope
+  }
+
   void device_setup_release() {
     for (DevBuf<double>* b : {&c64, &b64}) b->release();
     for (DevBuf<double2>* b : {&X64, &W64, &B64}) b->release();
@@ -332,7 +362,13 @@ struct Solver {
     blk.alloc(kEpiBlocks * 4, st);
     met.alloc(4, st);
     set_shard(0, 1);
-    if (fft) {
+    if (want_fft4(dev)) {
+      setup_fft4_common();
+      rowid.alloc(static_cast<size_t>(n), st);
+      launch_rowid(omega32.p, rowid.p, n, m, st);
+      ud.alloc(static_cast<size_t>(n), st);
+      ud.zero(st);
+    } else if (fft) {
       if (dev) {
         chat.alloc(static_cast<size_t>(n), st);
         launch_spectrum_f32(spec64, scale, chat.p, n, st);
@@ -367,6 +403,11 @@ struct Solver {
     if (fft) bhat.alloc(static_cast<size_t>(n), st);
     red_reset();
     launch_gram_spectrum(spec64, s, cfg.rho, cfg.sigma, B64.p, fft ? bhat.p : nullptr, red.p + 1, n, st);
+    if (want_fft4(true)) {  // B's spectrum in the four-step engine's order (before the inverse FFT reuses B64)
+      const Fft4Plan p4 = fft4_plan(n);
+      bhatp.alloc(static_cast<size_t>(n), st);
+      launch_fft4_perm_spectrum(p4, B64.p, 1.0, bhatp.p, st);
+    }
     double2* scratch = spec64 == X64.p ? W64.p : X64.p;
     const double2* Y = fft64_run(B64.p, scratch, n, true, st);
     b64.alloc(static_cast<size_t>(n), st);
@@ -406,7 +447,9 @@ struct Solver {
       device_gram_inverse(scale);
       launch_rows_f32(c64.p, scale, hc.p, hcr.p, n, st);
       launch_rows_f32(b64.p, 1.0, nullptr, hbr.p, n, st);
-      if (fft) {
+      if (want_fft4(dev)) {
+        setup_fft4_common();
+      } else if (fft) {
         chat.alloc(static_cast<size_t>(n), st);
         launch_spectrum_f32(spec64, scale, chat.p, n, st);
       }
@@ -445,7 +488,7 @@ struct Solver {
     blk.alloc(kEpiBlocks * 4, st);
     met.alloc(4, st);
     rowstart_host.assign(static_cast<size_t>(plan.chunks + 1), 0);
-    if (fft) {
+    if (fft && !fft4) {
       F0.alloc(static_cast<size_t>(n), st);
       F1.alloc(static_cast<size_t>(n), st);
     }
@@ -549,6 +592,77 @@ struct Solver {
     float2* other = Xm == F0.p ? F1.p : F0.p;
     return fft_run(Xm, other, n, true, st);
   }
+  // Four-step engine: one product = cols_fwd -> rows (twiddle, FFT, x H~, IFFT, twiddle) -> cols_inv.
+  void fft4_product(const float* u, const float2* H, bool conj_h, float* out, const int* rows_only) {
+    launch_fft4_cols_fwd(f4, u, F0.p, tw1.p, st);
+    launch_fft4_rows(f4, F0.p, H, conj_h, tw2.p, twA.p, twB.p, st);
+    launch_fft4_cols_inv(f4, F0.p, out, rows_only, tw1.p, st);
+  }
+  void ista_fft4_step(int want) {
+    mark(0);
+    fft4_product(x.p, chatp.p, true, partial.p, rowid.p);     // P C x
+    mark(1);
+    EpiArgs a;
+    a.partial = partial.p;
+    a.n = m;
+    a.lo = 0;
+    a.hi = m;
+    a.y = y.p;
+    a.r = r.p;
+    launch_ista_residual_reduce(a, 1, st);
+    mark(2);
+    launch_scatter_real(r.p, omega32.p, ud.p, m, st);          // P^T r (off-row entries stay 0)
+    fft4_product(ud.p, chatp.p, false, partial.p, nullptr);    // C^T P^T r
+    mark(3);
+    EpiArgs b = base_args(want);
+    b.splits = 1;
+    b.x = x.p;
+    b.delta = delta.p;
+    b.tau = static_cast<float>(tau);
+    b.thr = static_cast<float>(thr);
+    launch_ista_update(b, st);
+    mark(4);
+    nphase = 4;
+  }
+  void admm_fft4_step(int want) {
+    mark(0);
+    fft4_product(v.p, chatp.p, false, partial.p, nullptr);     // C^T v
+    mark(1);
+    EpiArgs a = base_args(0);
+    a.splits = 1;
+    a.beta = beta.p;
+    a.z = z.p;
+    a.nu = nu.p;
+    a.rho = static_cast<float>(cfg.rho);
+    a.sigma = static_cast<float>(cfg.sigma);
+    launch_admm_beta(a, st);
+    mark(2);
+    fft4_product(beta.p, bhatp.p, true, partial.p, nullptr);   // B beta
+    mark(3);
+    EpiArgs bx = base_args(0);
+    bx.splits = 1;
+    bx.x = x.p;
+    launch_admm_x(bx, st);
+    mark(4);
+    fft4_product(x.p, chatp.p, true, partial.p, nullptr);      // C x
+    mark(5);
+    EpiArgs d2 = base_args(want);
+    d2.splits = 1;
+    d2.x = x.p;
+    d2.z = z.p;
+    d2.nu = nu.p;
+    d2.mu = mu.p;
+    d2.v = v.p;
+    d2.d = d.p;
+    d2.pty = pty.p;
+    d2.rho = static_cast<float>(cfg.rho);
+    d2.tau1 = static_cast<float>(cfg.tau1);
+    d2.tau2 = static_cast<float>(cfg.tau2);
+    d2.thr = static_cast<float>(thr);
+    launch_admm_duals(d2, st);
+    mark(6);
+    nphase = 6;
+  }
   void ista_fft_step(int want) {
     mark(0);
     launch_real_to_complex(x.p, F0.p, n, st);
@@ -623,6 +737,13 @@ struct Solver {
 
   void one_step(int want) {
     if (world != 1) raise(CL_EPARAM, "cl_solver_step: sharded solvers advance with cl_solver_run_phase");
+    if (fft4) {
+      if (kind == CL_KIND_ISTA) ista_fft4_step(want);
+      else admm_fft4_step(want);
+      CU(cudaGetLastError());
+      ++t;
+      return;
+    }
     if (fft) {
       if (kind == CL_KIND_ISTA) ista_fft_step(want);
       else admm_fft_step(want);

@@ -446,3 +446,41 @@ def test_device_gram_floor_raises():
     op = cl.PartialCirculantOperator(cl.CirculantMatrix(c), cl.SubsamplingMask(np.arange(0, n, 2), n))
     with pytest.raises(cl.SingularityError):
         cl.cadmm_setup(op, np.zeros(n // 2), cl.SolverConfig(sigma=1e-15))
+
+
+# ------------------------------------------------------- four-step FFT engine
+@pytest.mark.parametrize("kind,lg", [("ista", 14), ("ista", 15), ("ista", 17), ("cadmm", 14), ("cadmm", 17)])
+def test_fft4_engine_matches_oracle(kind, lg):
+    """The four-step engine (n >= 2^14; N1 = N2 and N1 != N2 splits) against the oracle's FFT engine."""
+    n = 1 << lg
+    p = orc.make_problem(n, n // 4, n // 256, 3)
+    setup = cl.ista_setup if kind == "ista" else cl.cadmm_setup
+    g = setup(op_of(p), p.y, cl.SolverConfig(use_fft=True))
+    g.step(20)
+    o = (orc.Ista if kind == "ista" else orc.Cadmm)(p.row, p.omega, p.y)
+    o.step(20, orc.ENGINE_FFT)
+    f = "x" if kind == "ista" else "z"
+    assert_parity(g.get(f), o.get(f), what=f)
+    for h in (("r", "delta") if kind == "ista" else ("x", "v", "mu", "nu")):
+        assert rel_l2(g.get(h), o.get(h)) <= (1e-3 if h == "delta" else REL_TOL), h
+
+
+@pytest.mark.parametrize("kind,lg", [("ista", 20), ("ista", 23), ("cadmm", 22), ("ista", 24)])
+def test_fft4_engine_matches_stockham_engine(kind, lg):
+    """Four-step engine vs the multi-pass Stockham engine (CLB_FFT_STOCKHAM=1) up to n = 2^24."""
+    import os
+    n = 1 << lg
+    p = orc.make_problem(n, n // 4, n // 256, 1)
+    setup = cl.ista_setup if kind == "ista" else cl.cadmm_setup
+    got = {}
+    for stock in ("0", "1"):
+        os.environ["CLB_FFT_STOCKHAM"] = stock
+        try:
+            g = setup(op_of(p), p.y, cl.SolverConfig(use_fft=True))
+            g.step(4)
+            got[stock] = {f: g.get(f) for f in (("x", "r") if kind == "ista" else ("z", "x", "v"))}
+            del g
+        finally:
+            del os.environ["CLB_FFT_STOCKHAM"]
+    for f in got["0"]:
+        assert rel_l2(got["0"][f], got["1"][f]) <= 1e-5, (f, rel_l2(got["0"][f], got["1"][f]))
