@@ -327,9 +327,12 @@ void fft4_init_attributes() {
   static bool done = false;
   if (done) return;
   done = true;
+  // columns are at most 2048 long (fft4_plan); longer column kernels are never launched
 #define CLB_ATTR(N)                                                                                             \
-  cudaFuncSetAttribute(k_cols_fwd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem_t<N>());     \
-  cudaFuncSetAttribute(k_cols_inv<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem_t<N>());     \
+  if (N <= 2048) {                                                                                              \
+    cudaFuncSetAttribute(k_cols_fwd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem_t<N>());   \
+    cudaFuncSetAttribute(k_cols_inv<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem_t<N>());   \
+  }                                                                                                             \
   cudaFuncSetAttribute(k_rows<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem_t<N>());
   CLB_FFT4_SIZES(CLB_ATTR)
 #undef CLB_ATTR

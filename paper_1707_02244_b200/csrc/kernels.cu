@@ -573,16 +573,16 @@ k_conv_residual(const float* __restrict__ h, const float* __restrict__ x, const 
 // The row values of the next group are prefetched the same way, so no body
 // waits on a shared-memory load.
 // ===========================================================================
-template <int R>
+template <int R, int NT = kThreads>
 struct GeoU {
   static_assert(R % 8 == 4, "unpadded layout needs R = 4 mod 8 (conflict-free LDS.128 phases)");
-  static constexpr int kTileR = kThreads * R;
+  static constexpr int kTileR = NT * R;
   static constexpr int kSeg = kTileR + kChunk;
   static constexpr int kSegPhys = kSeg + 4;
 };
 
 // hs[e] = h[(base + e) mod n] for e in [0, kSeg).
-template <int kSeg>
+template <int kSeg, int NT = kThreads>
 __device__ __forceinline__ void stage_plain(float* __restrict__ hs, const float* __restrict__ h, int64_t n,
                                             int64_t base) {
   int64_t b = base % n;
@@ -590,16 +590,16 @@ __device__ __forceinline__ void stage_plain(float* __restrict__ hs, const float*
   if ((n & 3) == 0) {
     if (b + kSeg <= n) {
       const float4* src = reinterpret_cast<const float4*>(h + b);
-      for (int e = threadIdx.x; e < kSeg / 4; e += kThreads) reinterpret_cast<float4*>(hs)[e] = __ldg(src + e);
+      for (int e = threadIdx.x; e < kSeg / 4; e += NT) reinterpret_cast<float4*>(hs)[e] = __ldg(src + e);
     } else {
-      for (int e = threadIdx.x * 4; e < kSeg; e += kThreads * 4) {
+      for (int e = threadIdx.x * 4; e < kSeg; e += NT * 4) {
         int64_t s = b + e;
         if (s >= n) s %= n;
         *reinterpret_cast<float4*>(hs + e) = __ldg(reinterpret_cast<const float4*>(h + s));
       }
     }
   } else {
-    for (int e = threadIdx.x; e < kSeg; e += kThreads) hs[e] = __ldg(h + (b + e) % n);
+    for (int e = threadIdx.x; e < kSeg; e += NT) hs[e] = __ldg(h + (b + e) % n);
   }
 }
 
@@ -671,13 +671,13 @@ __device__ __forceinline__ void grad_block_s(float (&acc)[R], const float* __res
   grad_group_s<R, 7, PAIR>(acc, w, mask, wp, rb, r4);
 }
 
-template <int R, int MINB, bool PAIR = false>
-__global__ void __launch_bounds__(kThreads, MINB)
+template <int R, int MINB, bool PAIR = false, int NT = kThreads>
+__global__ void __launch_bounds__(NT, MINB)
 k_grad_s(const float* __restrict__ h, const int* __restrict__ omega, const float* __restrict__ rv,
          const int* __restrict__ rowstart, int64_t n, int64_t chunks, int splits, int64_t tile_lo,
          float* __restrict__ partial) {
   constexpr int PB = 32;
-  using G = GeoU<R>;
+  using G = GeoU<R, NT>;
   extern __shared__ float4 smem_f4[];
   float* hs = reinterpret_cast<float*>(smem_f4);
   float* rd = hs + G::kSegPhys;
@@ -698,12 +698,12 @@ k_grad_s(const float* __restrict__ h, const int* __restrict__ omega, const float
     const int64_t Jc = ch * kChunk;
     const int r0 = rowstart[ch], nr = rowstart[ch + 1] - r0;
     if (nr == 0) continue;
-    stage_plain<G::kSeg>(hs, h, n, I0 - Jc - kChunk);
-    for (int s = threadIdx.x; s < kChunk; s += kThreads) rd[s] = 0.f;
+    stage_plain<G::kSeg, NT>(hs, h, n, I0 - Jc - kChunk);
+    for (int s = threadIdx.x; s < kChunk; s += NT) rd[s] = 0.f;
     __syncthreads();
-    for (int k = threadIdx.x; k < nr; k += kThreads) rd[omega[r0 + k] - static_cast<int>(Jc)] = __ldg(rv + r0 + k);
+    for (int k = threadIdx.x; k < nr; k += NT) rd[omega[r0 + k] - static_cast<int>(Jc)] = __ldg(rv + r0 + k);
     __syncthreads();
-    for (int b32 = warp; b32 < kChunk / 32; b32 += kWarps) {
+    for (int b32 = warp; b32 < kChunk / 32; b32 += NT / 32) {
       const uint32_t mk = g_force_dense ? 0xffffffffu : __ballot_sync(0xffffffffu, rd[b32 * 32 + lane] != 0.f);
       if (lane == 0) bmask[b32] = mk;
     }
@@ -1029,8 +1029,8 @@ template <int R>
 constexpr size_t smem_dense() { return Geo<R>::kSegPhys * 4 + kChunk * 4; }
 template <int R, int PB>
 constexpr size_t smem_rows() { return Geo<R>::kSegPhys * 4 + kChunk * 4 + (kChunk / PB) * 4; }
-template <int R>
-constexpr size_t smem_grad_s() { return (GeoU<R>::kSegPhys + kChunk + kChunk / 32) * 4; }
+template <int R, int NT = kThreads>
+constexpr size_t smem_grad_s() { return (GeoU<R, NT>::kSegPhys + kChunk + kChunk / 32) * 4; }
 template <int R>
 constexpr size_t smem_res_s() {
   return (GeoU<R>::kSegPhys + 2 * (kChunk / 32) + kWarps * kChunk + kWarps * 32 * 33) * 4;
@@ -1046,6 +1046,7 @@ struct GradVariant {
   int R, PB;
   void (*fn)(const float*, const int*, const float*, const int*, int64_t, int64_t, int, int64_t, float*);
   size_t smem;
+  int nt = kThreads;  // threads per CTA
 };
 struct ResVariant {
   int R, PB;
@@ -1068,6 +1069,10 @@ const GradVariant kGrad[] = {
     {44, 32, k_grad_s<44, 3>, smem_grad_s<44>()},
     {44, 32, k_grad_s<44, 4, true>, smem_grad_s<44>()},  // 13: pair tests; large-n default (C3: 16.0 ms)
     {52, 32, k_grad_s<52, 3, true>, smem_grad_s<52>()},
+    {44, 32, k_grad_s<44, 1, true, 512>, smem_grad_s<44, 512>(), 512},  // 15: 16-warp CTAs (one mask per SM)
+    {44, 32, k_grad_s<44, 2, true, 256>, smem_grad_s<44, 256>(), 256},
+    {36, 32, k_grad_s<36, 1, true, 512>, smem_grad_s<36, 512>(), 512},
+    {52, 32, k_grad_s<52, 1, true, 512>, smem_grad_s<52, 512>(), 512},
 };
 const ResVariant kRes[] = {
     // small-n default: 4 CTAs/SM (120 registers, 55.3 KB smem; C3: 27.5 ms vs 29.0 at 3 CTAs/SM)
@@ -1124,7 +1129,8 @@ static const ResVariant& res_variant(int64_t n) {
   select_variants();
   return kRes[g_res >= 0 ? g_res : (n >= kLargeN ? kResLarge : kResSmall)];
 }
-int grad_R(int64_t n) { return grad_variant(n).R; }
+// plan "R" = indices per 128 threads (the tile is kThreads * R)
+int grad_R(int64_t n) { return grad_variant(n).R * grad_variant(n).nt / kThreads; }
 int res_R(int64_t n) { return res_variant(n).R; }
 
 void split_block_range(const ConvPlan& p, int split, int64_t* blo, int64_t* bhi) {
@@ -1177,7 +1183,7 @@ void launch_conv_rows(const ConvPlan& p, const float* h, const int* omega32, con
   const int64_t units = (p.tile_hi - p.tile_lo) * p.splits;
   if (units <= 0) return;
   const GradVariant& g = grad_variant(p.n);
-  g.fn<<<static_cast<unsigned>(units), kThreads, g.smem, st>>>(h, omega32, rvals, rowstart, p.n, p.chunks, p.splits,
+  g.fn<<<static_cast<unsigned>(units), g.nt, g.smem, st>>>(h, omega32, rvals, rowstart, p.n, p.chunks, p.splits,
                                                               p.tile_lo, partial);
 }
 

@@ -22,6 +22,7 @@
 #include "host_common.hpp"
 #include "fft.cuh"
 #include "fft4.cuh"
+#include "small.cuh"
 #include "kernels.cuh"
 
 namespace clb {
@@ -797,7 +798,19 @@ struct Solver {
     t = t0;  // capture does not execute
   }
 
+  // Small ISTA (n in {2048, 4096, 8192}): all unchecked iterations in one persistent cluster launch
+  // (small.cu); the checked iteration of the run loop still goes through one_step.
+  bool use_small() const { return kind == CL_KIND_ISTA && !fft && world == 1 && !profile && small_ista_supported(n, m); }
+
   void step(int64_t iters) {
+    if (iters > 0 && use_small()) {
+      CU(cudaEventRecord(step_ev[0], st));
+      CU(launch_small_ista(n, m, hc.p, omega32.p, y.p, x.p, r.p, delta.p, static_cast<float>(tau),
+                           static_cast<float>(thr), static_cast<int>(iters), st));
+      t += iters;
+      CU(cudaEventRecord(step_ev[1], st));
+      return;
+    }
     if (iters > 0 && use_graph()) build_graph();
     CU(cudaEventRecord(step_ev[0], st));
     for (int64_t k = 0; k < iters; ++k) {

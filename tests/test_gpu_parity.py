@@ -484,3 +484,35 @@ def test_fft4_engine_matches_stockham_engine(kind, lg):
             del os.environ["CLB_FFT_STOCKHAM"]
     for f in got["0"]:
         assert rel_l2(got["0"][f], got["1"][f]) <= 1e-5, (f, rel_l2(got["0"][f], got["1"][f]))
+
+
+# ------------------------------------------------- persistent small-n ISTA (one cluster)
+@pytest.mark.parametrize("n,m,k,seed,iters", [(4096, 1024, 64, 1, 300), (2048, 700, 40, 4, 120),
+                                              (8192, 2048, 100, 5, 80), (4096, 4096, 64, 2, 50)])
+def test_small_cluster_ista_matches_oracle(n, m, k, seed, iters):
+    """The single-launch cluster kernel (all iterations in one launch) against the oracle's phase engine."""
+    p = orc.make_problem(n, m, k, seed)
+    g = cl.ista_setup(op_of(p), p.y)
+    g.step(iters)
+    o = orc.Ista(p.row, p.omega, p.y)
+    o.step(iters, orc.ENGINE_PHASES)
+    assert g.t == iters
+    assert_parity(g.get("x"), o.get("x"), what="x")
+    assert rel_l2(g.get("r"), o.get("r")) <= REL_TOL
+    assert rel_l2(g.get("delta"), o.get("delta")) <= 1e-3
+
+
+def test_small_cluster_ista_matches_multikernel():
+    """Cluster kernel vs the multi-kernel path (CLB_NO_SMALL=1) on config 1, seed 3: same iterates."""
+    import os
+    p = orc.make_problem(4096, 1024, 64, 3)
+    got = {}
+    for off in ("0", "1"):
+        os.environ["CLB_NO_SMALL"] = off
+        try:
+            g = cl.ista_setup(op_of(p), p.y)
+            g.step(200)
+            got[off] = g.get("x")
+        finally:
+            del os.environ["CLB_NO_SMALL"]
+    assert rel_l2(got["0"], got["1"]) <= 1e-5
