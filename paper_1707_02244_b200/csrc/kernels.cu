@@ -779,7 +779,93 @@ __device__ __forceinline__ void res_block_s(const float* __restrict__ wp, const 
   res_group_s<R, 7, PAIR, CH>(w, xr, mask, wp, lpp);
 }
 
-template <int R, int MINB, bool PAIR = false, int CH = kResChains>
+// ---- FFMA2 residual (fma.rn.f32x2: two FMAs per issue slot) ------------------
+// The dot form's three-register FFMAs chain on each other; with packed pairs a
+// row needs R/2 (+1) FFMA2s and the issue slots in between are free for the
+// block skeleton.  Window pairs are the natural (w[2b], w[2b+1]) register pairs
+// from LDS.128; the two row parities pair them with two register layouts of x:
+//   S + R even:  W[(S+R)/2 - a] . (x[2a], x[2a-1]),   a = 0 .. R/2  (x[-1] = 0)
+//   S + R odd:   W[(S+R-1)/2 - a] . (x[2a+1], x[2a]), a = 0 .. R/2-1
+// (row S: sum_q w[S - q + R] x[q]; an even term uses x[R] = 0 at the edge).
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 up2(unsigned long long u) {
+  float2 v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(u));
+  return v;
+}
+__device__ __forceinline__ unsigned long long fma2(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+template <int NP, int K>  // pairs K, K+1 <- LDS.128 at float offset 2K
+__device__ __forceinline__ void ld2p(unsigned long long (&W)[NP], const float* __restrict__ wp) {
+  const ulonglong2 t = *reinterpret_cast<const ulonglong2*>(wp + 2 * K);
+  W[K] = t.x;
+  W[K + 1] = t.y;
+}
+template <int R, int S>
+__device__ __forceinline__ void res_row_f2(const unsigned long long (&W)[(R + 40) / 2],
+                                           const unsigned long long (&XE)[R / 2 + 1],
+                                           const unsigned long long (&XO)[R / 2], float*& lpp) {
+  unsigned long long c0 = 0ull, c1 = 0ull;
+  if constexpr (((S + R) & 1) == 0) {
+#pragma unroll
+    for (int a = 0; a <= R / 2; a += 2) {
+      c0 = fma2(W[(S + R) / 2 - a], XE[a], c0);
+      if (a + 1 <= R / 2) c1 = fma2(W[(S + R) / 2 - a - 1], XE[a + 1], c1);
+    }
+  } else {
+#pragma unroll
+    for (int a = 0; a < R / 2; a += 2) {
+      c0 = fma2(W[(S + R - 1) / 2 - a], XO[a], c0);
+      if (a + 1 < R / 2) c1 = fma2(W[(S + R - 1) / 2 - a - 1], XO[a + 1], c1);
+    }
+  }
+  const float2 u = up2(c0), v = up2(c1);
+  *lpp++ = (u.x + u.y) + (v.x + v.y);
+}
+template <int R, int G, bool PAIR>
+__device__ __forceinline__ void res_group_f2(unsigned long long (&W)[(R + 40) / 2],
+                                             const unsigned long long (&XE)[R / 2 + 1],
+                                             const unsigned long long (&XO)[R / 2], uint32_t mask,
+                                             const float* __restrict__ wp, float*& lpp) {
+  if constexpr (G < 7) ld2p<(R + 40) / 2, (R + 8 + 4 * G) / 2>(W, wp);
+  if (pair_live<PAIR>(mask, 4 * G)) {
+    if (row_at(mask, 4 * G)) res_row_f2<R, 4 * G>(W, XE, XO, lpp);
+    if (row_at(mask, 4 * G + 1)) res_row_f2<R, 4 * G + 1>(W, XE, XO, lpp);
+  }
+  if (pair_live<PAIR>(mask, 4 * G + 2)) {
+    if (row_at(mask, 4 * G + 2)) res_row_f2<R, 4 * G + 2>(W, XE, XO, lpp);
+    if (row_at(mask, 4 * G + 3)) res_row_f2<R, 4 * G + 3>(W, XE, XO, lpp);
+  }
+}
+template <int R, bool PAIR>
+__device__ __forceinline__ void res_block_f2(const float* __restrict__ wp, const unsigned long long (&XE)[R / 2 + 1],
+                                             const unsigned long long (&XO)[R / 2], uint32_t mask, float*& lpp) {
+  static_assert(R % 4 == 0, "R must be a multiple of 4");
+  unsigned long long W[(R + 40) / 2];
+#pragma unroll
+  for (int k = 0; k < (R + 8) / 2; k += 2) {
+    const ulonglong2 t = *reinterpret_cast<const ulonglong2*>(wp + 2 * k);
+    W[k] = t.x;
+    W[k + 1] = t.y;
+  }
+  res_group_f2<R, 0, PAIR>(W, XE, XO, mask, wp, lpp);
+  res_group_f2<R, 1, PAIR>(W, XE, XO, mask, wp, lpp);
+  res_group_f2<R, 2, PAIR>(W, XE, XO, mask, wp, lpp);
+  res_group_f2<R, 3, PAIR>(W, XE, XO, mask, wp, lpp);
+  res_group_f2<R, 4, PAIR>(W, XE, XO, mask, wp, lpp);
+  res_group_f2<R, 5, PAIR>(W, XE, XO, mask, wp, lpp);
+  res_group_f2<R, 6, PAIR>(W, XE, XO, mask, wp, lpp);
+  res_group_f2<R, 7, PAIR>(W, XE, XO, mask, wp, lpp);
+}
+
+template <int R, int MINB, bool PAIR = false, int CH = kResChains, bool F2 = false>
 __global__ void __launch_bounds__(kThreads, MINB)
 k_res_s(const float* __restrict__ h, const float* __restrict__ x, const int* __restrict__ omega,
         const int* __restrict__ rowstart, int64_t n, int64_t m, int64_t chunks, int splits, int split_lo,
@@ -809,12 +895,20 @@ k_res_s(const float* __restrict__ h, const float* __restrict__ x, const int* __r
   const int64_t jb = I0 + own * R;
 #pragma unroll
   for (int q = 0; q < R; ++q) xr[q] = (jb + q < n) ? __ldg(x + jb + q) : 0.f;
+  unsigned long long XE[F2 ? R / 2 + 1 : 1], XO[F2 ? R / 2 : 1];
+  if constexpr (F2) {
+#pragma unroll
+    for (int a = 0; a <= R / 2; ++a) XE[a] = pk2(a < R / 2 ? xr[2 * a] : 0.f, a > 0 ? xr[2 * a - 1] : 0.f);
+#pragma unroll
+    for (int a = 0; a < R / 2; ++a) XO[a] = pk2(xr[2 * a + 1], xr[2 * a]);
+  }
 
   for (int64_t ch = blo / (kChunk / 32); ch * (kChunk / 32) < bhi; ++ch) {
     const int64_t Jc = ch * kChunk;
     const int r0 = rowstart[ch], nr = rowstart[ch + 1] - r0;
     if (nr == 0) continue;
-    stage_plain<G::kSeg>(hs, h, n, Jc - I0 - G::kTileR);
+    // (+4: the FFMA2 form reads one element past the window, multiplied by an x of 0)
+    stage_plain<G::kSeg + (F2 ? 4 : 0)>(hs, h, n, Jc - I0 - G::kTileR);
     for (int s = threadIdx.x; s < kChunk; s += kThreads) flag[s] = 0;
     __syncthreads();
     for (int k = threadIdx.x; k < nr; k += kThreads) flag[omega[r0 + k] - static_cast<int>(Jc)] = 1;
@@ -838,7 +932,8 @@ k_res_s(const float* __restrict__ h, const float* __restrict__ x, const int* __r
       const uint32_t mask = __reduce_or_sync(0xffffffffu, bmask[b]);
       if (mask == 0u) continue;
       float* lpp = lp_lane;
-      res_block_s<R, PAIR, CH>(lane_base + b * PB, xr, mask, lpp);
+      if constexpr (F2) res_block_f2<R, PAIR>(lane_base + b * PB, XE, XO, mask, lpp);
+      else res_block_s<R, PAIR, CH>(lane_base + b * PB, xr, mask, lpp);
       __syncwarp();
       reduce_lane_partials(lp, redw, bbase[b], __popc(mask), lane);
       __syncwarp();
@@ -1102,6 +1197,11 @@ const ResVariant kRes[] = {
     {52, 32, k_res_s<52, 4, true, 2>, smem_res_s<52>()},
     {68, 32, k_res_s<68, 3, true, 2>, smem_res_s<68>()},
     {44, 32, k_res_s<44, 3, true, 2>, smem_res_s<44>()},
+    {52, 32, k_res_s<52, 2, true, 2, true>, smem_res_s<52>()},  // 26: FFMA2 bodies (25.9-31.3 ms: rejected)
+    {44, 32, k_res_s<44, 3, true, 2, true>, smem_res_s<44>()},
+    {36, 32, k_res_s<36, 3, true, 2, true>, smem_res_s<36>()},
+    {36, 32, k_res_s<36, 4, true, 2, true>, smem_res_s<36>()},
+    {60, 32, k_res_s<60, 2, true, 2, true>, smem_res_s<60>()},
 };
 // Defaults (measured best on B200, tools/variants.py): the streamed-window
 // kernels with pair tests at large n; the R = 32 padded kernels at small n,
