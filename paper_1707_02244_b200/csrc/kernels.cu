@@ -726,6 +726,55 @@ k_grad_s(const float* __restrict__ h, const int* __restrict__ omega, const float
     if (ib + q < n) out[ib + q] = acc[q];
 }
 
+// Dense product with the streamed-window layout (all 32 positions of every block,
+// no tests): out[i] = sum_j h[(i - j) mod n] u[j].  Experiment beside k_conv_dense.
+template <int R>
+__device__ __forceinline__ void dense_block_s(float (&acc)[R], const float* __restrict__ wp,
+                                              const float* __restrict__ ub) {
+  grad_block_s<R, false>(acc, wp, ub, 0xffffffffu);
+}
+
+template <int R, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+k_dense_s(const float* __restrict__ h, const float* __restrict__ u, int64_t n, int64_t chunks, int splits,
+          int64_t tile_lo, float* __restrict__ partial) {
+  constexpr int PB = 32;
+  using G = GeoU<R>;
+  extern __shared__ float4 smem_f4[];
+  float* hs = reinterpret_cast<float*>(smem_f4);
+  float* us = hs + G::kSegPhys;
+  const int64_t unit = blockIdx.x;
+  const int64_t tile = tile_lo + unit / splits;
+  const int split = static_cast<int>(unit % splits);
+  const int64_t I0 = tile * G::kTileR;
+  int64_t blo, bhi;
+  split_blocks(chunks, splits, split, &blo, &bhi);
+  const int own = threadIdx.x;
+  float acc[R];
+#pragma unroll
+  for (int q = 0; q < R; ++q) acc[q] = 0.f;
+  for (int64_t ch = blo / (kChunk / 32); ch * (kChunk / 32) < bhi; ++ch) {
+    const int64_t Jc = ch * kChunk;
+    stage_plain<G::kSeg>(hs, h, n, I0 - Jc - kChunk);
+    for (int s = threadIdx.x; s < kChunk; s += kThreads) {
+      const int64_t j = Jc + s;
+      us[s] = j < n ? __ldg(u + j) : 0.f;
+    }
+    __syncthreads();
+    const int64_t cb = ch * (kChunk / 32);
+    const int b0 = static_cast<int>(blo > cb ? blo - cb : 0);
+    const int b1 = static_cast<int>(bhi - cb < kChunk / 32 ? bhi - cb : kChunk / 32);
+    const float* wl = hs + own * R + kChunk - PB;
+    for (int b = b0; b < b1; ++b) dense_block_s<R>(acc, wl - b * PB, us + b * PB);
+    __syncthreads();
+  }
+  const int64_t ib = I0 + own * R;
+  float* out = partial + static_cast<int64_t>(split) * n;
+#pragma unroll
+  for (int q = 0; q < R; ++q)
+    if (ib + q < n) out[ib + q] = acc[q];
+}
+
 // Residual block (dot form, x register-resident): row s computes
 // sum_q w[s - q + R] x[q]; position s needs w[s+1 .. s+R], so the window
 // moves up by 4 per group.
@@ -1203,6 +1252,23 @@ const ResVariant kRes[] = {
     {36, 32, k_res_s<36, 4, true, 2, true>, smem_res_s<36>()},
     {60, 32, k_res_s<60, 2, true, 2, true>, smem_res_s<60>()},
 };
+struct DenseVariant {
+  int R;
+  void (*fn)(const float*, const float*, int64_t, int64_t, int, int64_t, float*);
+  size_t smem;
+};
+template <int R>
+constexpr size_t smem_dense_s() { return (GeoU<R>::kSegPhys + kChunk) * 4; }
+const DenseVariant kDense[] = {
+    {64, k_conv_dense<64>, smem_dense<64>()},  // 0: padded R = 64 (default)
+    {60, k_dense_s<60, 3>, smem_dense_s<60>()},
+    {60, k_dense_s<60, 2>, smem_dense_s<60>()},
+    {68, k_dense_s<68, 2>, smem_dense_s<68>()},
+    {52, k_dense_s<52, 3>, smem_dense_s<52>()},
+    {76, k_dense_s<76, 2>, smem_dense_s<76>()},
+};
+int g_dense = 0;
+
 // Defaults (measured best on B200, tools/variants.py): the streamed-window
 // kernels with pair tests at large n; the R = 32 padded kernels at small n,
 // where a 4096-index tile already covers the whole problem.
@@ -1220,6 +1286,7 @@ static void select_variants() {
   done = true;
   if (const char* v = getenv("CLB_GRAD")) g_grad = atoi(v) % (int)(sizeof(kGrad) / sizeof(kGrad[0]));
   if (const char* v = getenv("CLB_RES")) g_res = atoi(v) % (int)(sizeof(kRes) / sizeof(kRes[0]));
+  if (const char* v = getenv("CLB_DENSE")) g_dense = atoi(v) % (int)(sizeof(kDense) / sizeof(kDense[0]));
 }
 static const GradVariant& grad_variant(int64_t n) {
   select_variants();
@@ -1228,6 +1295,11 @@ static const GradVariant& grad_variant(int64_t n) {
 static const ResVariant& res_variant(int64_t n) {
   select_variants();
   return kRes[g_res >= 0 ? g_res : (n >= kLargeN ? kResLarge : kResSmall)];
+}
+int dense_R(int64_t n) {
+  (void)n;
+  select_variants();
+  return kDense[g_dense].R;
 }
 // plan "R" = indices per 128 threads (the tile is kThreads * R)
 int grad_R(int64_t n) { return grad_variant(n).R * grad_variant(n).nt / kThreads; }
@@ -1264,7 +1336,8 @@ void conv_kernels_init() {
     cudaMemcpyToSymbol(g_force_dense, &one, sizeof(int));
   }
   select_variants();
-  cudaFuncSetAttribute(k_conv_dense<kRDense>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dense<kRDense>());
+  for (const auto& d : kDense)
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(d.fn), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d.smem);
   for (const auto& g : kGrad)
     cudaFuncSetAttribute(reinterpret_cast<const void*>(g.fn), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
   for (const auto& r : kRes)
@@ -1274,8 +1347,8 @@ void conv_kernels_init() {
 void launch_conv_dense(const ConvPlan& p, const float* h, const float* u, float* partial, cudaStream_t st) {
   const int64_t units = (p.tile_hi - p.tile_lo) * p.splits;
   if (units <= 0) return;
-  k_conv_dense<kRDense><<<static_cast<unsigned>(units), kThreads, smem_dense<kRDense>(), st>>>(
-      h, u, p.n, p.chunks, p.splits, p.tile_lo, partial);
+  const DenseVariant& d = kDense[g_dense];
+  d.fn<<<static_cast<unsigned>(units), kThreads, d.smem, st>>>(h, u, p.n, p.chunks, p.splits, p.tile_lo, partial);
 }
 
 void launch_conv_rows(const ConvPlan& p, const float* h, const int* omega32, const float* rvals, const int* rowstart,

@@ -37,6 +37,7 @@ constexpr int kEpiBlocks = 592;         // grid of the elementwise epilogues (fi
 // sparse kernels' R comes from the variant selected for n (grad_R(n), res_R(n)).
 constexpr int kRDense = 64;
 int grad_R(int64_t n);
+int dense_R(int64_t n);  // R of the selected dense-product kernel (kRDense by default)
 int res_R(int64_t n);
 
 struct ConvPlan {
