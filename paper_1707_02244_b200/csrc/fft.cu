@@ -294,6 +294,14 @@ __global__ void k_rows_f32(const double* __restrict__ x, double s, float* __rest
     if (rev) rev[i == 0 ? 0 : n - i] = v;
   }
 }
+// Y[k] = (conj_x ? conj(X[k]) : X[k]) * Y[k]
+__global__ void k_cmul64(const double2* __restrict__ X, double2* __restrict__ Y, int conj_x, int64_t n) {
+  CLB_GRID_LOOP(k, n) {
+    const double2 a = X[k], b = Y[k];
+    const double ay = conj_x ? -a.y : a.y;
+    Y[k] = make_double2(a.x * b.x - ay * b.y, a.x * b.y + ay * b.x);
+  }
+}
 // spectrum of x / s in fp32 (the FFT engine's operator spectrum)
 __global__ void k_spectrum_f32(const double2* __restrict__ X, double s, float2* __restrict__ out, int64_t n) {
   CLB_GRID_LOOP(k, n) out[k] = make_float2(static_cast<float>(X[k].x / s), static_cast<float>(X[k].y / s));
@@ -316,6 +324,9 @@ void launch_real_part64(const double2* Y, double* out, unsigned long long* mre, 
 }
 void launch_rows_f32(const double* x, double s, float* out, float* rev, int64_t n, cudaStream_t st) {
   k_rows_f32<<<pw_grid(n), kPw, 0, st>>>(x, s, out, rev, n);
+}
+void launch_cmul64(const double2* X, double2* Y, bool conj_x, int64_t n, cudaStream_t st) {
+  k_cmul64<<<pw_grid(n), kPw, 0, st>>>(X, Y, conj_x ? 1 : 0, n);
 }
 void launch_spectrum_f32(const double2* X, double s, float2* out, int64_t n, cudaStream_t st) {
   k_spectrum_f32<<<pw_grid(n), kPw, 0, st>>>(X, s, out, n);

@@ -26,4 +26,6 @@ void launch_real_part64(const double2* Y, double* out, unsigned long long* mre, 
                         cudaStream_t st);
 void launch_rows_f32(const double* x, double s, float* out, float* rev, int64_t n, cudaStream_t st);
 void launch_spectrum_f32(const double2* X, double s, float2* out, int64_t n, cudaStream_t st);
+// Y = conj?(X) * Y (fp64 complex, pointwise)
+void launch_cmul64(const double2* X, double2* Y, bool conj_x, int64_t n, cudaStream_t st);
 }  // namespace clb

@@ -862,6 +862,91 @@ struct Solver {
   }
 };
 
+// ---- fp64 circulant products of host vectors on the device -------------------
+// out = Re idft(conj?(dft(a)) . dft(b)) (fft.hpp:74-89 residue check), the
+// transform behind measure (circulant.hpp:277-282) and compose_rows
+// (circulant.hpp:337-343).  Power-of-two n >= 2^14 with a CUDA device;
+// otherwise the host fp64 DFT (host_setup.cpp) runs.
+static bool device_product_ok(int64_t n) {
+  const char* v = std::getenv("CLB_HOST_SETUP");
+  if ((v && v[0] == '1') || !is_pow2(n) || n < (int64_t(1) << 14)) return false;
+  int count = 0;
+  return cudaGetDeviceCount(&count) == cudaSuccess && count > 0;
+}
+static void device_product(const double* a, const double* b, int64_t n, bool conj_a, double* out) {
+  cudaStream_t st;
+  CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  struct Guard {
+    cudaStream_t s;
+    ~Guard() {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  } guard{st};
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  reserve_pool(dev);
+  const size_t nn = static_cast<size_t>(n);
+  DevBuf<double> ra, rb, ro;
+  DevBuf<double2> A, B, W;
+  DevBuf<unsigned long long> red;
+  ra.alloc(nn, st);
+  rb.alloc(nn, st);
+  ro.alloc(nn, st);
+  A.alloc(nn, st);
+  B.alloc(nn, st);
+  W.alloc(nn, st);
+  red.alloc(4, st);
+  ra.upload(a, nn, st);
+  rb.upload(b, nn, st);
+  CU(cudaMemsetAsync(red.p, 0, sizeof(unsigned long long) * 4, st));
+  launch_real_to_complex64(ra.p, A.p, n, st);
+  const double2* SA = fft64_run(A.p, W.p, n, false, st);
+  double2* freeAW = SA == A.p ? W.p : A.p;
+  launch_real_to_complex64(rb.p, B.p, n, st);
+  double2* SB = const_cast<double2*>(fft64_run(B.p, freeAW, n, false, st));
+  launch_cmul64(SA, SB, conj_a, n, st);
+  double2* scratch = SB == B.p ? freeAW : B.p;  // neither SB nor (needed no more) SA's live data
+  const double2* Y = fft64_run(SB, scratch, n, true, st);
+  launch_real_part64(Y, ro.p, red.p + 2, red.p + 3, n, st);
+  CU(cudaGetLastError());
+  unsigned long long h[4];
+  CU(cudaMemcpyAsync(h, red.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(out, ro.p, sizeof(double) * nn, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  double re, im;
+  std::memcpy(&re, &h[2], sizeof(double));
+  std::memcpy(&im, &h[3], sizeof(double));
+  if (im > 1e-10 * std::max(1.0, re)) {
+    std::ostringstream msg;
+    msg << "inverse DFT of a real-valued quantity has imaginary residue " << im << " (relative tolerance 1e-10)";
+    raise(CL_ECONSIST, msg.str());
+  }
+}
+// y[t] = (C x)[omega[t]] (measure, sensing.hpp:171-182)
+static void measure_any(const double* c, const int64_t* omega, int64_t n, int64_t m, const double* x, double* y) {
+  if (!device_product_ok(n)) {
+    measure(c, omega, n, m, x, y);
+    return;
+  }
+  std::vector<double> cx(static_cast<size_t>(n));
+  device_product(c, x, n, true, cx.data());  // C x = idft(conj(c^) x^)
+  for (int64_t t = 0; t < m; ++t) y[t] = cx[static_cast<size_t>(omega[t])];
+}
+static bool identity_row(const double* r, int64_t n) {  // deblur.hpp:41-46
+  if (n < 1 || r[0] != 1.0) return false;
+  for (int64_t i = 1; i < n; ++i)
+    if (r[i] != 0.0) return false;
+  return true;
+}
+static void compose_any(const double* c, const double* b, int64_t n, double* out) {
+  if (!device_product_ok(n) || identity_row(b, n) || identity_row(c, n)) {
+    compose_rows(c, b, n, out);  // (also the identity short-circuits of deblur.hpp:53-64)
+    return;
+  }
+  device_product(c, b, n, false, out);
+}
+
 // ---- device product helpers (cl_circ_matvec & co.) --------------------------
 struct ScratchProduct {
   static void circ(int device, int64_t n, const double* c, const double* xin, int transpose, double* out) {
@@ -966,7 +1051,7 @@ cl_status cl_gen_circulant_sensing(int64_t n, int64_t m, uint64_t seed, double* 
 cl_status cl_measure(int64_t n, int64_t m, const double* c, const int64_t* omega, const double* x, double* y) {
   CL_GUARD_BEGIN
   check_mask(omega, m, n);
-  measure(c, omega, n, m, x, y);
+  measure_any(c, omega, n, m, x, y);
   CL_GUARD_END
 }
 cl_status cl_make_problem(int64_t n, int64_t m, int64_t k, uint64_t seed, double* c, int64_t* omega, double* x_true,
@@ -974,7 +1059,7 @@ cl_status cl_make_problem(int64_t n, int64_t m, int64_t k, uint64_t seed, double
   CL_GUARD_BEGIN
   gen_sparse_signal(n, k, seed, x_true, support);
   gen_circulant_sensing(n, m, seed, c, omega);
-  measure(c, omega, n, m, x_true, y);
+  measure_any(c, omega, n, m, x_true, y);
   CL_GUARD_END
 }
 cl_status cl_gen_star_field(int64_t w, int64_t h, double density, uint64_t seed, double* px) {
@@ -989,7 +1074,7 @@ cl_status cl_blur_row(int64_t n, int64_t L, double* row) {
 }
 cl_status cl_compose_rows(int64_t n, const double* c, const double* b, double* out) {
   CL_GUARD_BEGIN
-  compose_rows(c, b, n, out);
+  compose_any(c, b, n, out);
   CL_GUARD_END
 }
 cl_status cl_spectral_norm(int64_t n, const double* c, double* out) {

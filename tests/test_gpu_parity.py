@@ -516,3 +516,24 @@ def test_small_cluster_ista_matches_multikernel():
         finally:
             del os.environ["CLB_NO_SMALL"]
     assert rel_l2(got["0"], got["1"]) <= 1e-5
+
+
+def test_device_measure_and_compose_match_host():
+    """measure / compose_rows through the device fp64 FFT (power-of-two n >= 2^14) agree with the host
+    fp64 DFT to the reference's own FFT tolerance (tests/fft_test.cpp:136-148: 1e-10)."""
+    import os
+    n = 1 << 16
+    p = orc.make_problem(n, n // 4, 256, 9)
+    blur = cl.blur_matrix(n, 5)
+    out = {}
+    for host in ("0", "1"):
+        os.environ["CLB_HOST_SETUP"] = host
+        try:
+            A = op_of(p)
+            out[host] = (cl.measure(A, p.x_true), cl.compose_sensing(A.circulant(), blur, A.mask()).circulant().first_row(),
+                         cl.make_problem(n, n // 4, 256, 9).measurements)
+        finally:
+            del os.environ["CLB_HOST_SETUP"]
+    for a, b in zip(out["0"], out["1"]):
+        assert np.max(np.abs(a - b)) <= 1e-12 * max(1.0, np.max(np.abs(b)))
+    assert np.max(np.abs(out["0"][0] - p.y)) <= 1e-12 * max(1.0, np.max(np.abs(p.y)))
