@@ -1309,13 +1309,23 @@ void split_block_range(const ConvPlan& p, int split, int64_t* blo, int64_t* bhi)
   split_blocks(p.chunks, p.splits, split, blo, bhi);
 }
 
+int64_t target_units(int64_t n) {
+  static const int64_t forced = [] {
+    const char* v = getenv("CLB_UNITS");
+    return v ? static_cast<int64_t>(atoll(v)) : int64_t(0);
+  }();
+  if (forced > 0) return forced;
+  return n >= kUnitsLargeN ? kTargetUnitsLarge : kTargetUnits;
+}
+
 ConvPlan make_plan(int64_t n, int R) {
   ConvPlan p;
   p.n = n;
   p.tile = static_cast<int64_t>(kThreads) * R;
   p.tiles = (n + p.tile - 1) / p.tile;
   p.chunks = (n + kChunk - 1) / kChunk;
-  int64_t s = (kTargetUnits + p.tiles - 1) / p.tiles;
+  const int64_t units = target_units(n);
+  int64_t s = (units + p.tiles - 1) / p.tiles;
   const int64_t blocks32 = p.chunks * (kChunk / 32);  // splits are ranges of 32-position blocks
   if (s < 1) s = 1;
   if (s > blocks32) s = blocks32;

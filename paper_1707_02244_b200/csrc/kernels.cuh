@@ -30,7 +30,15 @@ constexpr int kWarps = 4;
 constexpr int kThreads = kWarps * 32;   // 128
 constexpr int kP = 32;                  // positions per register window block
 constexpr int kChunk = 1024;            // positions per shared-memory stage
-constexpr int kTargetUnits = 1184;      // 8 x 148: split-count target (constant: G-independent)
+// Split-count target (CTAs per product), a function of n only, so the decomposition and the
+// results are independent of the GPU count.  Large n: 96 x 148 units -- smaller CTAs balance the
+// waves (C3 step 37.3 -> 34.1 ms, cADMM products 40.8 -> 36.3 ms at n = 2^20; flat from 64 to
+// 128 x 148) and leave 12 CTAs per SM when a product is sharded over 8 GPUs.  Below 2^19 the
+// split-K partial traffic would dominate, so 8 x 148.
+constexpr int kTargetUnits = 1184;
+constexpr int kTargetUnitsLarge = 14208;
+constexpr int64_t kUnitsLargeN = int64_t(1) << 19;
+int64_t target_units(int64_t n);  // CLB_UNITS overrides (experiments)
 constexpr int kEpiBlocks = 592;         // grid of the elementwise epilogues (fixed -> deterministic metrics)
 
 // Register blocking of the dense kernel (indices owned per thread); the

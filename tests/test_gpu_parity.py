@@ -403,12 +403,14 @@ def _states(kind, p, host_setup, iters=20, use_fft=False):
     import os
     old = os.environ.get("CLB_HOST_SETUP")
     os.environ["CLB_HOST_SETUP"] = "1" if host_setup else "0"
+    os.environ["CLB_FFT_STOCKHAM"] = "1"  # same FFT engine either way (the four-step one needs the device setup)
     try:
         setup = cl.ista_setup if kind == "ista" else cl.cadmm_setup
         g = setup(op_of(p), p.y, cl.SolverConfig(use_fft=use_fft))
         g.step(iters)
         return {f: g.get(f) for f in (("x", "r", "delta") if kind == "ista" else ("x", "z", "v", "mu", "nu", "beta"))}
     finally:
+        del os.environ["CLB_FFT_STOCKHAM"]
         if old is None:
             del os.environ["CLB_HOST_SETUP"]
         else:
