@@ -539,3 +539,59 @@ def test_device_measure_and_compose_match_host():
     for a, b in zip(out["0"], out["1"]):
         assert np.max(np.abs(a - b)) <= 1e-12 * max(1.0, np.max(np.abs(b)))
     assert np.max(np.abs(out["0"][0] - p.y)) <= 1e-12 * max(1.0, np.max(np.abs(p.y)))
+
+
+# ------------------------------------------- large, ragged sizes (streamed kernels, 96x148 units)
+@pytest.mark.parametrize("n,m,seed", [(131075, 32771, 7), (524309, 131073, 8), (1 << 19, 1 << 17, 9)])
+def test_partial_products_large_ragged(n, m, seed):
+    """Streamed-window kernels at n >= 2^17: n not a multiple of 4 (scalar staging path), ragged last
+    tile, and the large unit target (n >= 2^19)."""
+    row, om = orc.gen_circulant_sensing(n, m, seed)
+    A = cl.PartialCirculantOperator(cl.CirculantMatrix(row), cl.SubsamplingMask(om, n))
+    x = orc.rng_draws(seed + 100, "normal", n)
+    r = orc.rng_draws(seed + 200, "normal", m)
+    full = orc.circ_matvec(row, x, use_fft=True)
+    assert rel_l2(cl.partial_matvec(A, x), full[om]) <= 5e-5
+    emb = np.zeros(n)
+    emb[om] = r
+    assert rel_l2(cl.partial_transpose_matvec(A, r), orc.circ_matvec(row, emb, transpose=True, use_fft=True)) <= 5e-5
+
+
+def test_sparse_edge_masks_large():
+    """Rows only at the ends and at chunk boundaries, m = 1 and m = n, at a size the streamed kernels run."""
+    n = 200003
+    row = orc.rng_draws(21, "normal", n)
+    x = orc.rng_draws(22, "normal", n)
+    full = orc.circ_matvec(row, x, use_fft=True)
+    for om in (np.array([0]), np.array([n - 1]), np.array([0, 1023, 1024, 2047, 2048, 131071, 131072, n - 1]),
+               np.arange(n)):
+        A = cl.PartialCirculantOperator(cl.CirculantMatrix(row), cl.SubsamplingMask(om, n))
+        assert rel_l2(cl.partial_matvec(A, x), full[om]) <= 5e-5
+        r = orc.rng_draws(23, "normal", len(om))
+        emb = np.zeros(n)
+        emb[om] = r
+        assert rel_l2(cl.partial_transpose_matvec(A, r), orc.circ_matvec(row, emb, transpose=True, use_fft=True)) <= 5e-5
+
+
+@pytest.mark.parametrize("n", [524291])
+def test_circ_products_large_ragged(n):
+    """Dense products at n >= 2^19 (large unit target), n odd."""
+    row = orc.rng_draws(50, "normal", n)
+    x = orc.rng_draws(51, "normal", n)
+    C = cl.CirculantMatrix(row)
+    assert rel_l2(cl.circ_matvec(C, x), orc.circ_matvec(row, x, use_fft=True)) <= 5e-5
+    assert rel_l2(cl.circ_transpose_matvec(C, x), orc.circ_matvec(row, x, transpose=True, use_fft=True)) <= 5e-5
+
+
+@pytest.mark.parametrize("kind", ["ista", "cadmm"])
+def test_steps_large_ragged_vs_fft_oracle(kind):
+    """Solver steps at n = 262147 (odd, streamed sparse kernels / dense kernel) vs the oracle's FFT engine."""
+    n = 262147
+    p = orc.make_problem(n, n // 4, 1000, 11)
+    setup = cl.ista_setup if kind == "ista" else cl.cadmm_setup
+    g = setup(op_of(p), p.y)
+    g.step(3)
+    o = (orc.Ista if kind == "ista" else orc.Cadmm)(p.row, p.omega, p.y)
+    o.step(3, orc.ENGINE_FFT)
+    f = "x" if kind == "ista" else "z"
+    assert_parity(g.get(f), o.get(f), what=f)
