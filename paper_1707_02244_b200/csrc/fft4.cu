@@ -18,6 +18,7 @@
 // in-place radix-16 (then 8/4/2) butterfly on shared memory with a twiddle
 // table; global loads and stores are coalesced row segments.
 #include <cstdint>
+#include <cstdlib>
 #include <cstdio>
 #include <cmath>
 #include <vector>
@@ -284,6 +285,63 @@ __global__ void k_scatter_real(const float* __restrict__ r, const int* __restric
 }
 
 
+// ---- one-CTA FFT-engine ISTA for small n -------------------------------------
+// Config 1 (n = 4096) on the FFT engine: the whole iteration in one CTA's shared
+// memory, all unchecked iterations in one launch.  A length-n DIF FFT, the
+// spectral multiply in the DIF output order (H permuted to match), a DIT inverse
+// FFT -- per product, twice per iteration (circulant.hpp:236-274):
+//   r = y - P C x,   delta = C^T P^T r,   x = eta(x + tau delta).
+template <int N>
+__global__ void __launch_bounds__(kThr, 1)
+k_small_fft_ista(const float2* __restrict__ Hp, const float2* __restrict__ tw, const int* __restrict__ omega,
+                 const float* __restrict__ y, float* __restrict__ x, float* __restrict__ r, float* __restrict__ delta,
+                 int m, float tau, float thr, int iters) {
+  extern __shared__ float4 smem_f4[];
+  float2* A = reinterpret_cast<float2*>(smem_f4);          // padded N complex
+  float* xs = reinterpret_cast<float*>(A + pad16(N) + 4);  // N
+  float* rs = xs + N;                                      // m (<= N)
+  const float inv_n = 1.0f / static_cast<float>(N);
+  for (int i = threadIdx.x; i < N; i += kThr) xs[i] = x[i];
+  __syncthreads();
+  for (int it = 0; it < iters; ++it) {
+    // residual: A = x -> DIF -> * conj(H) -> DIT -> r = y - Re(A[omega]) / n
+    for (int i = threadIdx.x; i < N; i += kThr) A[pad16(i)] = make_float2(xs[i], 0.f);
+    __syncthreads();
+    dif_from<N, N, 1>(A, 0, tw);
+    for (int i = threadIdx.x; i < N; i += kThr) A[pad16(i)] = cmulf_conj(A[pad16(i)], __ldg(Hp + i));
+    __syncthreads();
+    dit_from<N, N, 1>(A, 0, tw);
+    for (int t = threadIdx.x; t < m; t += kThr) rs[t] = __ldg(y + t) - A[pad16(__ldg(omega + t))].x * inv_n;
+    __syncthreads();
+    // gradient: A = P^T r -> DIF -> * H -> DIT -> delta = Re(A) / n; x update
+    for (int i = threadIdx.x; i < N; i += kThr) A[pad16(i)] = make_float2(0.f, 0.f);
+    __syncthreads();
+    for (int t = threadIdx.x; t < m; t += kThr) A[pad16(__ldg(omega + t))] = make_float2(rs[t], 0.f);
+    __syncthreads();
+    dif_from<N, N, 1>(A, 0, tw);
+    for (int i = threadIdx.x; i < N; i += kThr) A[pad16(i)] = cmulf(A[pad16(i)], __ldg(Hp + i));
+    __syncthreads();
+    dit_from<N, N, 1>(A, 0, tw);
+    for (int i = threadIdx.x; i < N; i += kThr) {
+      const float d = A[pad16(i)].x * inv_n;
+      const float v = __fadd_rn(xs[i], __fmul_rn(tau, d));  // parallel.hpp:269-271
+      xs[i] = v > thr ? v - thr : (v < -thr ? v + thr : 0.f);
+      if (it == iters - 1) delta[i] = d;
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < N; i += kThr) x[i] = xs[i];
+  for (int t = threadIdx.x; t < m; t += kThr) r[t] = rs[t];
+}
+
+// Hp[p] = H[digit_rev(p, N)] (fp32 natural-order spectrum -> the DIF output order)
+__global__ void k_perm_small(const float2* __restrict__ H, float2* __restrict__ Hp, int N) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < N; p += gridDim.x * blockDim.x) Hp[p] = H[digit_rev(p, N)];
+}
+
+template <int N>
+size_t small_fft_smem() { return (static_cast<size_t>(pad16(N) + 4) * 2 + 2 * N) * sizeof(float); }
+
 }  // namespace
 
 bool fft4_supported(int64_t n) { return n >= (int64_t(1) << 14) && n <= (int64_t(1) << 24) && (n & (n - 1)) == 0; }
@@ -372,6 +430,39 @@ void launch_fft4_cols_inv(const Fft4Plan& p, const float2* T, float* out, const 
 void launch_fft4_perm_spectrum(const Fft4Plan& p, const double2* spec, double s, float2* out, cudaStream_t st) {
   k_perm_spectrum<<<148 * 8, 256, 0, st>>>(spec, s, out, p.N1, p.N2);
 }
+bool small_fft_supported(int64_t n) {
+  const char* v = std::getenv("CLB_NO_SMALL");
+  return !(v && v[0] == '1') && (n == 1024 || n == 2048 || n == 4096 || n == 8192);
+}
+void launch_small_fft_perm(const float2* H, float2* Hp, int64_t n, cudaStream_t st) {
+  k_perm_small<<<8, 256, 0, st>>>(H, Hp, static_cast<int>(n));
+}
+cudaError_t launch_small_fft_ista(int64_t n, int64_t m, const float2* Hp, const float2* tw, const int* omega,
+                                  const float* y, float* x, float* r, float* delta, float tau, float thr, int iters,
+                                  cudaStream_t st) {
+  switch (n) {
+#define CLB_SMALL_CASE(N)                                                                                   \
+  case N: {                                                                                                 \
+    static bool attr = false;                                                                               \
+    if (!attr) {                                                                                            \
+      attr = true;                                                                                          \
+      cudaFuncSetAttribute(k_small_fft_ista<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,                \
+                           static_cast<int>(small_fft_smem<N>()));                                          \
+    }                                                                                                       \
+    k_small_fft_ista<N><<<1, kThr, small_fft_smem<N>(), st>>>(Hp, tw, omega, y, x, r, delta,                \
+                                                               static_cast<int>(m), tau, thr, iters);       \
+    return cudaGetLastError();                                                                              \
+  }
+    CLB_SMALL_CASE(1024)
+    CLB_SMALL_CASE(2048)
+    CLB_SMALL_CASE(4096)
+    CLB_SMALL_CASE(8192)
+#undef CLB_SMALL_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
 void launch_scatter_real(const float* r, const int* omega, float* u, int64_t m, cudaStream_t st) {
   if (m > 0) k_scatter_real<<<148 * 4, 256, 0, st>>>(r, omega, u, m);
 }

@@ -30,4 +30,12 @@ void launch_fft4_perm_spectrum(const Fft4Plan& p, const double2* spec, double s,
 void launch_rowid(const int* omega, int* rowid, int64_t n, int64_t m, cudaStream_t st);
 // u[omega[t]] = r[t]
 void launch_scatter_real(const float* r, const int* omega, float* u, int64_t m, cudaStream_t st);
+// One-CTA FFT-engine ISTA for n in {1024, 2048, 4096, 8192} (CLB_NO_SMALL unset): all unchecked
+// iterations in one launch.  Hp = the operator spectrum in the DIF output order (launch_small_fft_perm),
+// tw = e^{-2 pi i k / n}, k < n.
+bool small_fft_supported(int64_t n);
+void launch_small_fft_perm(const float2* H, float2* Hp, int64_t n, cudaStream_t st);
+cudaError_t launch_small_fft_ista(int64_t n, int64_t m, const float2* Hp, const float2* tw, const int* omega,
+                                  const float* y, float* x, float* r, float* delta, float tau, float thr, int iters,
+                                  cudaStream_t st);
 }  // namespace clb

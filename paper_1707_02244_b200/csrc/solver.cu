@@ -184,6 +184,9 @@ struct Solver {
   DevBuf<float2> tw1, tw2, twA, twB, chatp, bhatp;
   DevBuf<int> rowid;
   DevBuf<float> ud;
+  // One-CTA FFT-engine ISTA at small n (fft4.cu): spectrum in DIF order and the twiddle table.
+  bool small_fft = false;
+  DevBuf<float2> chatS, twS;
   DevBuf<double> blk, met;
   double* met_host = nullptr;
   std::vector<int> rowstart_host;
@@ -380,10 +383,25 @@ struct Solver {
       }
       F0.alloc(static_cast<size_t>(n), st);
       F1.alloc(static_cast<size_t>(n), st);
+      if (small_fft_supported(n)) setup_small_fft();
     }
     CU(cudaGetLastError());
     device_setup_release();
     CU(cudaStreamSynchronize(st));
+  }
+
+  void setup_small_fft() {
+    small_fft = true;
+    std::vector<float2> t(static_cast<size_t>(n));
+    for (int64_t k = 0; k < n; ++k) {
+      const double a = -2.0 * 3.14159265358979323846 * static_cast<double>(k) / static_cast<double>(n);
+      t[static_cast<size_t>(k)] = make_float2(static_cast<float>(std::cos(a)), static_cast<float>(std::sin(a)));
+    }
+    twS.alloc(t.size(), st);
+    twS.upload(t.data(), t.size(), st);
+    chatS.alloc(static_cast<size_t>(n), st);
+    launch_small_fft_perm(chat.p, chatS.p, n, st);
+    CU(cudaStreamSynchronize(st));  // t goes out of scope
   }
 
   void upload_spectrum(DevBuf<float2>& dst, const std::vector<cplx>& spec) {
@@ -801,8 +819,19 @@ struct Solver {
   // Small ISTA (n in {2048, 4096, 8192}): all unchecked iterations in one persistent cluster launch
   // (small.cu); the checked iteration of the run loop still goes through one_step.
   bool use_small() const { return kind == CL_KIND_ISTA && !fft && world == 1 && !profile && small_ista_supported(n, m); }
+  bool use_small_fft() const {
+    return kind == CL_KIND_ISTA && fft && !fft4 && small_fft && world == 1 && !profile && small_fft_supported(n);
+  }
 
   void step(int64_t iters) {
+    if (iters > 0 && use_small_fft()) {
+      CU(cudaEventRecord(step_ev[0], st));
+      CU(launch_small_fft_ista(n, m, chatS.p, twS.p, omega32.p, y.p, x.p, r.p, delta.p, static_cast<float>(tau),
+                               static_cast<float>(thr), static_cast<int>(iters), st));
+      t += iters;
+      CU(cudaEventRecord(step_ev[1], st));
+      return;
+    }
     if (iters > 0 && use_small()) {
       CU(cudaEventRecord(step_ev[0], st));
       CU(launch_small_ista(n, m, hc.p, omega32.p, y.p, x.p, r.p, delta.p, static_cast<float>(tau),

@@ -595,3 +595,17 @@ def test_steps_large_ragged_vs_fft_oracle(kind):
     o.step(3, orc.ENGINE_FFT)
     f = "x" if kind == "ista" else "z"
     assert_parity(g.get(f), o.get(f), what=f)
+
+
+@pytest.mark.parametrize("n,m,k,seed,iters", [(4096, 1024, 64, 1, 500), (1024, 300, 20, 2, 100), (8192, 2048, 80, 3, 60)])
+def test_small_fft_engine_ista_matches_oracle(n, m, k, seed, iters):
+    """One-CTA FFT-engine ISTA (all iterations in one launch) against the oracle's FFT engine."""
+    p = orc.make_problem(n, m, k, seed)
+    g = cl.ista_setup(op_of(p), p.y, cl.SolverConfig(use_fft=True))
+    g.step(iters)
+    o = orc.Ista(p.row, p.omega, p.y)
+    o.step(iters, orc.ENGINE_FFT)
+    assert g.t == iters
+    assert_parity(g.get("x"), o.get("x"), what="x")
+    assert rel_l2(g.get("r"), o.get("r")) <= REL_TOL
+    assert rel_l2(g.get("delta"), o.get("delta")) <= 1e-3
