@@ -334,6 +334,87 @@ k_small_fft_ista(const float2* __restrict__ Hp, const float2* __restrict__ tw, c
   for (int t = threadIdx.x; t < m; t += kThr) r[t] = rs[t];
 }
 
+// One-CTA FFT-engine cADMM (config 2) in the same style (cpadmm_phases, parallel.hpp:173-231):
+//   beta = rho C^T v + sigma (z - nu);  x = B beta;  cx = C x;  the D/z/mu/nu/v updates.
+template <int N>
+__global__ void __launch_bounds__(kThr, 1)
+k_small_fft_cadmm(const float2* __restrict__ Hc, const float2* __restrict__ Hb, const float2* __restrict__ tw,
+                  const float* __restrict__ d, const float* __restrict__ pty, float* __restrict__ xg,
+                  float* __restrict__ zg, float* __restrict__ nug, float* __restrict__ mug, float* __restrict__ vg,
+                  float* __restrict__ betag, float rho, float sigma, float tau1, float tau2, float thr, int iters) {
+  extern __shared__ float4 smem_f4[];
+  float2* A = reinterpret_cast<float2*>(smem_f4);
+  float* xs = reinterpret_cast<float*>(A + pad16(N) + 4);
+  float* zs = xs + N;
+  float* nus = zs + N;
+  float* mus = nus + N;
+  float* vs = mus + N;
+  const float inv_n = 1.0f / static_cast<float>(N);
+  for (int i = threadIdx.x; i < N; i += kThr) {
+    xs[i] = xg[i];
+    zs[i] = zg[i];
+    nus[i] = nug[i];
+    mus[i] = mug[i];
+    vs[i] = vg[i];
+  }
+  __syncthreads();
+  for (int it = 0; it < iters; ++it) {
+    const bool last = it == iters - 1;
+    // beta = rho C^T v + sigma (z - nu)
+    for (int i = threadIdx.x; i < N; i += kThr) A[pad16(i)] = make_float2(vs[i], 0.f);
+    __syncthreads();
+    dif_from<N, N, 1>(A, 0, tw);
+    for (int i = threadIdx.x; i < N; i += kThr) A[pad16(i)] = cmulf(A[pad16(i)], __ldg(Hc + i));
+    __syncthreads();
+    dit_from<N, N, 1>(A, 0, tw);
+    for (int i = threadIdx.x; i < N; i += kThr) {
+      const float sct = A[pad16(i)].x * inv_n;
+      const float b = __fadd_rn(__fmul_rn(rho, sct), __fmul_rn(sigma, __fsub_rn(zs[i], nus[i])));
+      A[pad16(i)] = make_float2(b, 0.f);
+      if (last) betag[i] = b;
+    }
+    __syncthreads();
+    // x = B beta
+    dif_from<N, N, 1>(A, 0, tw);
+    for (int i = threadIdx.x; i < N; i += kThr) A[pad16(i)] = cmulf_conj(A[pad16(i)], __ldg(Hb + i));
+    __syncthreads();
+    dit_from<N, N, 1>(A, 0, tw);
+    for (int i = threadIdx.x; i < N; i += kThr) {
+      const float xv = A[pad16(i)].x * inv_n;
+      xs[i] = xv;
+      A[pad16(i)] = make_float2(xv, 0.f);
+    }
+    __syncthreads();
+    // cx = C x; duals
+    dif_from<N, N, 1>(A, 0, tw);
+    for (int i = threadIdx.x; i < N; i += kThr) A[pad16(i)] = cmulf_conj(A[pad16(i)], __ldg(Hc + i));
+    __syncthreads();
+    dit_from<N, N, 1>(A, 0, tw);
+    for (int i = threadIdx.x; i < N; i += kThr) {
+      const float cx = A[pad16(i)].x * inv_n;
+      const float xi = xs[i], nui = nus[i];
+      const float vn = __fmul_rn(__ldg(d + i), __fadd_rn(__fmul_rn(rho, __fsub_rn(cx, mus[i])), __ldg(pty + i)));
+      const float sv = __fadd_rn(xi, nui);
+      const float zn = sv > thr ? sv - thr : (sv < -thr ? sv + thr : 0.f);
+      const float mun = __fadd_rn(mus[i], __fmul_rn(tau1, __fsub_rn(vn, cx)));
+      zs[i] = zn;
+      mus[i] = mun;
+      nus[i] = __fadd_rn(nui, __fmul_rn(tau2, __fsub_rn(xi, zn)));
+      vs[i] = __fadd_rn(vn, mun);
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < N; i += kThr) {
+    xg[i] = xs[i];
+    zg[i] = zs[i];
+    nug[i] = nus[i];
+    mug[i] = mus[i];
+    vg[i] = vs[i];
+  }
+}
+template <int N>
+size_t small_fft_cadmm_smem() { return (static_cast<size_t>(pad16(N) + 4) * 2 + 5 * N) * sizeof(float); }
+
 // Hp[p] = H[digit_rev(p, N)] (fp32 natural-order spectrum -> the DIF output order)
 __global__ void k_perm_small(const float2* __restrict__ H, float2* __restrict__ Hp, int N) {
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < N; p += gridDim.x * blockDim.x) Hp[p] = H[digit_rev(p, N)];
@@ -457,6 +538,33 @@ cudaError_t launch_small_fft_ista(int64_t n, int64_t m, const float2* Hp, const 
     CLB_SMALL_CASE(2048)
     CLB_SMALL_CASE(4096)
     CLB_SMALL_CASE(8192)
+#undef CLB_SMALL_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+bool small_fft_cadmm_supported(int64_t n) { return small_fft_supported(n) && n <= 4096; }
+cudaError_t launch_small_fft_cadmm(int64_t n, const float2* Hc, const float2* Hb, const float2* tw, const float* d,
+                                   const float* pty, float* x, float* z, float* nu, float* mu, float* v, float* beta,
+                                   float rho, float sigma, float tau1, float tau2, float thr, int iters,
+                                   cudaStream_t st) {
+  switch (n) {
+#define CLB_SMALL_CASE(N)                                                                                   \
+  case N: {                                                                                                 \
+    static bool attr = false;                                                                               \
+    if (!attr) {                                                                                            \
+      attr = true;                                                                                          \
+      cudaFuncSetAttribute(k_small_fft_cadmm<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,               \
+                           static_cast<int>(small_fft_cadmm_smem<N>()));                                    \
+    }                                                                                                       \
+    k_small_fft_cadmm<N><<<1, kThr, small_fft_cadmm_smem<N>(), st>>>(Hc, Hb, tw, d, pty, x, z, nu, mu, v,    \
+                                                                     beta, rho, sigma, tau1, tau2, thr, iters); \
+    return cudaGetLastError();                                                                              \
+  }
+    CLB_SMALL_CASE(1024)
+    CLB_SMALL_CASE(2048)
+    CLB_SMALL_CASE(4096)
 #undef CLB_SMALL_CASE
     default:
       return cudaErrorInvalidValue;

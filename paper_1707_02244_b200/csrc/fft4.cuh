@@ -38,4 +38,10 @@ void launch_small_fft_perm(const float2* H, float2* Hp, int64_t n, cudaStream_t 
 cudaError_t launch_small_fft_ista(int64_t n, int64_t m, const float2* Hp, const float2* tw, const int* omega,
                                   const float* y, float* x, float* r, float* delta, float tau, float thr, int iters,
                                   cudaStream_t st);
+// One-CTA FFT-engine cADMM for n in {1024, 2048, 4096}; Hc, Hb in the DIF output order.
+bool small_fft_cadmm_supported(int64_t n);
+cudaError_t launch_small_fft_cadmm(int64_t n, const float2* Hc, const float2* Hb, const float2* tw, const float* d,
+                                   const float* pty, float* x, float* z, float* nu, float* mu, float* v, float* beta,
+                                   float rho, float sigma, float tau1, float tau2, float thr, int iters,
+                                   cudaStream_t st);
 }  // namespace clb

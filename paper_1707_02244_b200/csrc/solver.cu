@@ -186,7 +186,7 @@ struct Solver {
   DevBuf<float> ud;
   // One-CTA FFT-engine ISTA at small n (fft4.cu): spectrum in DIF order and the twiddle table.
   bool small_fft = false;
-  DevBuf<float2> chatS, twS;
+  DevBuf<float2> chatS, bhatS, twS;
   DevBuf<double> blk, met;
   double* met_host = nullptr;
   std::vector<int> rowstart_host;
@@ -401,6 +401,10 @@ struct Solver {
     twS.upload(t.data(), t.size(), st);
     chatS.alloc(static_cast<size_t>(n), st);
     launch_small_fft_perm(chat.p, chatS.p, n, st);
+    if (kind == CL_KIND_CADMM) {
+      bhatS.alloc(static_cast<size_t>(n), st);
+      launch_small_fft_perm(bhat.p, bhatS.p, n, st);
+    }
     CU(cudaStreamSynchronize(st));  // t goes out of scope
   }
 
@@ -510,6 +514,7 @@ struct Solver {
     if (fft && !fft4) {
       F0.alloc(static_cast<size_t>(n), st);
       F1.alloc(static_cast<size_t>(n), st);
+      if (small_fft_cadmm_supported(n)) setup_small_fft();
     }
     set_shard(0, 1);
     CU(cudaGetLastError());
@@ -820,14 +825,21 @@ struct Solver {
   // (small.cu); the checked iteration of the run loop still goes through one_step.
   bool use_small() const { return kind == CL_KIND_ISTA && !fft && world == 1 && !profile && small_ista_supported(n, m); }
   bool use_small_fft() const {
-    return kind == CL_KIND_ISTA && fft && !fft4 && small_fft && world == 1 && !profile && small_fft_supported(n);
+    return fft && !fft4 && small_fft && world == 1 && !profile &&
+           (kind == CL_KIND_ISTA ? small_fft_supported(n) : small_fft_cadmm_supported(n));
   }
 
   void step(int64_t iters) {
     if (iters > 0 && use_small_fft()) {
       CU(cudaEventRecord(step_ev[0], st));
-      CU(launch_small_fft_ista(n, m, chatS.p, twS.p, omega32.p, y.p, x.p, r.p, delta.p, static_cast<float>(tau),
-                               static_cast<float>(thr), static_cast<int>(iters), st));
+      if (kind == CL_KIND_ISTA)
+        CU(launch_small_fft_ista(n, m, chatS.p, twS.p, omega32.p, y.p, x.p, r.p, delta.p, static_cast<float>(tau),
+                                 static_cast<float>(thr), static_cast<int>(iters), st));
+      else
+        CU(launch_small_fft_cadmm(n, chatS.p, bhatS.p, twS.p, d.p, pty.p, x.p, z.p, nu.p, mu.p, v.p, beta.p,
+                                  static_cast<float>(cfg.rho), static_cast<float>(cfg.sigma),
+                                  static_cast<float>(cfg.tau1), static_cast<float>(cfg.tau2),
+                                  static_cast<float>(thr), static_cast<int>(iters), st));
       t += iters;
       CU(cudaEventRecord(step_ev[1], st));
       return;

@@ -609,3 +609,16 @@ def test_small_fft_engine_ista_matches_oracle(n, m, k, seed, iters):
     assert_parity(g.get("x"), o.get("x"), what="x")
     assert rel_l2(g.get("r"), o.get("r")) <= REL_TOL
     assert rel_l2(g.get("delta"), o.get("delta")) <= 1e-3
+
+
+@pytest.mark.parametrize("n,m,k,seed,iters", [(4096, 1024, 64, 2, 200), (2048, 1024, 40, 4, 80)])
+def test_small_fft_engine_cadmm_matches_oracle(n, m, k, seed, iters):
+    """One-CTA FFT-engine cADMM against the oracle's FFT engine."""
+    p = orc.make_problem(n, m, k, seed)
+    g = cl.cadmm_setup(op_of(p), p.y, cl.SolverConfig(use_fft=True))
+    g.step(iters)
+    o = orc.Cadmm(p.row, p.omega, p.y)
+    o.step(iters, orc.ENGINE_FFT)
+    assert_parity(g.get("z"), o.get("z"), what="z")
+    for f in ("x", "v", "mu", "nu", "beta"):
+        assert rel_l2(g.get(f), o.get(f)) <= REL_TOL, f
