@@ -184,6 +184,35 @@ cl_status cl_shard_ranges(int kind, int64_t n, int64_t m, const int64_t* omega, 
 cl_status cl_solver_phase_output(cl_solver* s, int phase, void** dev_ptr, int64_t* begin,
                                  int64_t* end, int64_t* total);
 
+/* ---- artifact formats (io.hpp:1-170) -------------------------------------
+ * Vectors: magic "CIRCVEC1", u64 length, little-endian f64 data.
+ * Operators: magic "CIRCOPR1", u64 n, u64 m, f64 first row[n], u64 omega[m].
+ * Errors are CL_EFORMAT with the reference's messages ("cannot open", "bad
+ * magic", "truncated ...", "m exceeds n").  Readers report the stored sizes
+ * in *len / *n, *m; a NULL or too-small output buffer only queries them. */
+cl_status cl_write_vector(const char* path, const double* v, int64_t n);          /* io.hpp:80-87 */
+cl_status cl_read_vector(const char* path, double* out, int64_t cap, int64_t* len); /* io.hpp:89-97 */
+cl_status cl_write_operator(const char* path, int64_t n, int64_t m, const double* row,
+                            const int64_t* omega);                                   /* io.hpp:99-112 */
+cl_status cl_read_operator(const char* path, double* row, int64_t cap_n, int64_t* omega, int64_t cap_m,
+                           int64_t* n, int64_t* m);                                  /* io.hpp:114-131 */
+/* One benchmark run in the reference's pinned CSV schema (io.hpp:133-170). */
+typedef struct cl_bench_row {
+  const char* algorithm;
+  int64_t n, m, k;
+  uint64_t seed;
+  int64_t iterations;
+  double setup_seconds, total_seconds, final_mse;
+  uint64_t footprint_bytes;
+  const char* status;
+} cl_bench_row;
+/* iterations / (total - setup), 0 without active time or iterations (io.hpp:148-152) */
+double cl_bench_iters_per_second(const cl_bench_row* row);
+/* The header line / one row, without the newline, formatted exactly as the
+ * reference's std::ostream writer; *len = the text length (buf may be NULL). */
+cl_status cl_bench_csv_header(char* buf, int64_t cap, int64_t* len);
+cl_status cl_bench_csv_row(const cl_bench_row* row, char* buf, int64_t cap, int64_t* len);
+
 /* ---- roofline helper ----------------------------------------------------- */
 /* FP32 FFMA peak microbenchmark on `device` (TFLOP/s), the roofline
  * denominator for the direct engine. */

@@ -30,6 +30,13 @@ class cl_config(C.Structure):
                 ("check_every", C.c_int32), ("pairing", C.c_int32), ("engine", C.c_int32)]
 
 
+class cl_bench_row(C.Structure):
+    _fields_ = [("algorithm", C.c_char_p), ("n", C.c_int64), ("m", C.c_int64), ("k", C.c_int64),
+                ("seed", C.c_uint64), ("iterations", C.c_int64), ("setup_seconds", C.c_double),
+                ("total_seconds", C.c_double), ("final_mse", C.c_double), ("footprint_bytes", C.c_uint64),
+                ("status", C.c_char_p)]
+
+
 class cl_report(C.Structure):
     _fields_ = [("iterations", C.c_int64), ("setup_seconds", C.c_double), ("total_seconds", C.c_double),
                 ("footprint_bytes", C.c_uint64), ("metric", C.c_int32), ("reached_target", C.c_int32),
@@ -74,6 +81,13 @@ _SIGS = {
     "cl_solver_phase_output": (C.c_int, [_vp, C.c_int, C.POINTER(_vp), _i64, _i64, _i64]),
     "cl_shard_ranges": (C.c_int, [C.c_int, C.c_int64, C.c_int64, _i64, C.c_int, C.c_int, _i64, _i64, _i64, _i64]),
     "cl_ffma_peak": (C.c_int, [C.c_int, _d]),
+    "cl_write_vector": (C.c_int, [C.c_char_p, _d, C.c_int64]),
+    "cl_read_vector": (C.c_int, [C.c_char_p, _d, C.c_int64, _i64]),
+    "cl_write_operator": (C.c_int, [C.c_char_p, C.c_int64, C.c_int64, _d, _i64]),
+    "cl_read_operator": (C.c_int, [C.c_char_p, _d, C.c_int64, _i64, C.c_int64, _i64, _i64]),
+    "cl_bench_iters_per_second": (C.c_double, [C.POINTER(cl_bench_row)]),
+    "cl_bench_csv_header": (C.c_int, [C.c_char_p, C.c_int64, _i64]),
+    "cl_bench_csv_row": (C.c_int, [C.POINTER(cl_bench_row), C.c_char_p, C.c_int64, _i64]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

@@ -47,4 +47,13 @@ void measure(const double* c, const int64_t* omega, int64_t n, int64_t m, const 
 // circulant.hpp:134-146
 void check_mask(const int64_t* omega, int64_t m, int64_t n);
 
+// ---- artifact formats (io.hpp; io.cpp) ------------------------------------
+void write_vector_file(const std::string& path, const double* v, int64_t n);
+std::vector<double> read_vector_file(const std::string& path);
+void write_operator_file(const std::string& path, int64_t n, int64_t m, const double* row, const int64_t* omega);
+void read_operator_file(const std::string& path, std::vector<double>* row, std::vector<int64_t>* omega);
+double bench_iters_per_second(const cl_bench_row& r);
+std::string bench_csv_header();
+std::string bench_csv_row(const cl_bench_row& r);
+
 }  // namespace clb

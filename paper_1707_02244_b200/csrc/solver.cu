@@ -1118,6 +1118,60 @@ cl_status cl_compose_rows(int64_t n, const double* c, const double* b, double* o
   compose_any(c, b, n, out);
   CL_GUARD_END
 }
+cl_status cl_write_vector(const char* path, const double* v, int64_t n) {
+  CL_GUARD_BEGIN
+  if (!path) raise(CL_EPARAM, "write_vector: null path");
+  if (n < 0 || (n > 0 && !v)) raise(CL_EPARAM, "write_vector: bad vector");
+  write_vector_file(path, v, n);
+  CL_GUARD_END
+}
+cl_status cl_read_vector(const char* path, double* out, int64_t cap, int64_t* len) {
+  CL_GUARD_BEGIN
+  if (!path || !len) raise(CL_EPARAM, "read_vector: null argument");
+  const std::vector<double> v = read_vector_file(path);
+  *len = static_cast<int64_t>(v.size());
+  if (out && cap >= *len) std::copy(v.begin(), v.end(), out);
+  CL_GUARD_END
+}
+cl_status cl_write_operator(const char* path, int64_t n, int64_t m, const double* row, const int64_t* omega) {
+  CL_GUARD_BEGIN
+  if (!path) raise(CL_EPARAM, "write_operator: null path");
+  if (n < 0 || m < 0 || m > n) raise(CL_EDIM, "write_operator: need 0 <= m <= n");
+  write_operator_file(path, n, m, row, omega);
+  CL_GUARD_END
+}
+cl_status cl_read_operator(const char* path, double* row, int64_t cap_n, int64_t* omega, int64_t cap_m, int64_t* n,
+                           int64_t* m) {
+  CL_GUARD_BEGIN
+  if (!path || !n || !m) raise(CL_EPARAM, "read_operator: null argument");
+  std::vector<double> r;
+  std::vector<int64_t> om;
+  read_operator_file(path, &r, &om);
+  *n = static_cast<int64_t>(r.size());
+  *m = static_cast<int64_t>(om.size());
+  if (row && cap_n >= *n) std::copy(r.begin(), r.end(), row);
+  if (omega && cap_m >= *m) std::copy(om.begin(), om.end(), omega);
+  CL_GUARD_END
+}
+double cl_bench_iters_per_second(const cl_bench_row* row) { return row ? bench_iters_per_second(*row) : 0.0; }
+static void copy_text(const std::string& t, char* buf, int64_t cap, int64_t* len) {
+  if (len) *len = static_cast<int64_t>(t.size());
+  if (buf && cap > static_cast<int64_t>(t.size())) {
+    std::memcpy(buf, t.data(), t.size());
+    buf[t.size()] = '\0';
+  }
+}
+cl_status cl_bench_csv_header(char* buf, int64_t cap, int64_t* len) {
+  CL_GUARD_BEGIN
+  copy_text(bench_csv_header(), buf, cap, len);
+  CL_GUARD_END
+}
+cl_status cl_bench_csv_row(const cl_bench_row* row, char* buf, int64_t cap, int64_t* len) {
+  CL_GUARD_BEGIN
+  if (!row) raise(CL_EPARAM, "bench row: null");
+  copy_text(bench_csv_row(*row), buf, cap, len);
+  CL_GUARD_END
+}
 cl_status cl_spectral_norm(int64_t n, const double* c, double* out) {
   CL_GUARD_BEGIN
   *out = spectral_norm(c, n);

@@ -622,3 +622,21 @@ def test_small_fft_engine_cadmm_matches_oracle(n, m, k, seed, iters):
     assert_parity(g.get("z"), o.get("z"), what="z")
     for f in ("x", "v", "mu", "nu", "beta"):
         assert rel_l2(g.get(f), o.get(f)) <= REL_TOL, f
+
+
+def test_bench_sweeps_the_protocol_problem():
+    """The reference's `bench` sweep (io_cli_test.cpp:317-336) through the GPU solvers: pinned CSV, m = n/2,
+    k = n/10, status ok at the protocol target."""
+    import io
+    from paper_1707_02244_b200 import io as cio
+    out = io.StringIO()
+    cio.bench([128, 4096], solvers=("cadmm", "ista", "admm"), seeds=1,
+              cfg=cl.SolverConfig(target_mse=1e-4, max_iter=20000), out=out)
+    lines = out.getvalue().splitlines()
+    assert lines[0] == cio.kBenchCsvHeader and len(lines) == 7
+    f = lines[1].split(",")
+    assert f[:4] == ["cadmm", "128", "64", "12"] and f[11] == "ok"
+    rows = [ln.split(",") for ln in lines[1:]]
+    assert all(len(r) == 12 for r in rows)
+    assert [r[11] for r in rows if r[0] == "admm"] == ["skipped", "skipped"]
+    assert all(r[11] == "ok" and float(r[8]) <= 1e-4 for r in rows if r[0] != "admm")

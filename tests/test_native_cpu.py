@@ -127,3 +127,84 @@ def test_cpp_adapter_cpu_parts():
     assert os.path.exists(exe), "build the package first (make -C paper_1707_02244_b200)"
     out = subprocess.run([exe, "cpu"], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0 and "PASS" in out.stdout, out.stdout + out.stderr
+
+
+# ---------------------------------------------------------------- artifact formats (io.hpp)
+def test_vector_files_roundtrip_bit_for_bit(tmp_path):
+    """io_cli_test.cpp:81-95"""
+    from paper_1707_02244_b200 import io as cio
+    v = np.array([0.0, -0.0, 5e-324, np.finfo(float).max, -1e-300, 3.141592653589793, np.nan, -np.inf])
+    path = tmp_path / "vector.bin"
+    cio.write_vector(v, path)
+    assert path.read_bytes() == b"CIRCVEC1" + (8).to_bytes(8, "little") + v.astype("<f8").tobytes()
+    back = cio.read_vector(path)
+    assert back.tobytes() == v.tobytes()
+    cio.write_vector(np.zeros(0), path)
+    assert len(cio.read_vector(path)) == 0
+
+
+def test_operator_files_roundtrip_exactly(tmp_path):
+    """io_cli_test.cpp:97-107 (and the byte layout io.hpp:99-112)"""
+    from paper_1707_02244_b200 import io as cio
+    A = cl.gen_circulant_sensing(64, 24, 99)
+    path = tmp_path / "operator.bin"
+    cio.write_operator(A, path)
+    raw = path.read_bytes()
+    assert raw[:8] == b"CIRCOPR1" and int.from_bytes(raw[8:16], "little") == 64
+    assert int.from_bytes(raw[16:24], "little") == 24 and len(raw) == 24 + 64 * 8 + 24 * 8
+    back = cio.read_operator(path)
+    assert back.n() == 64 and back.m() == 24
+    assert np.array_equal(back.circulant().first_row(), A.circulant().first_row())
+    assert np.array_equal(back.mask().omega(), A.mask().omega())
+
+
+def test_binary_readers_reject_malformed_files(tmp_path):
+    """io_cli_test.cpp:109-152"""
+    from paper_1707_02244_b200 import io as cio
+    path = tmp_path / "malformed.bin"
+    with pytest.raises(cl.FormatError, match="cannot open"):
+        cio.read_vector(tmp_path / "missing.bin")
+    path.write_bytes(b"CIRCVEX1\x02\x00\x00\x00\x00\x00\x00\x00")
+    with pytest.raises(cl.FormatError, match="bad magic"):
+        cio.read_vector(path)
+    with pytest.raises(cl.FormatError, match="bad magic"):
+        cio.read_operator(path)
+    path.write_bytes(b"CIRC")
+    with pytest.raises(cl.FormatError):
+        cio.read_vector(path)
+    path.write_bytes(b"CIRCVEC1" + (10).to_bytes(8, "little") + np.full(3, 1.5).tobytes())
+    with pytest.raises(cl.FormatError, match="truncated"):
+        cio.read_vector(path)
+    path.write_bytes(b"CIRCOPR1" + (4).to_bytes(8, "little") + (5).to_bytes(8, "little"))
+    with pytest.raises(cl.FormatError, match="m exceeds n"):
+        cio.read_operator(path)
+
+
+def test_bench_rows_compute_throughput_defensively():
+    """io_cli_test.cpp:154-167"""
+    from paper_1707_02244_b200 import io as cio
+    row = cio.BenchRow(iterations=1000, setup_seconds=0.5, total_seconds=2.5)
+    assert row.iterations_per_second() == pytest.approx(500.0)
+    row.iterations = 0
+    assert row.iterations_per_second() == 0.0
+    row.iterations, row.total_seconds = 10, row.setup_seconds
+    assert row.iterations_per_second() == 0.0
+
+
+def test_bench_csv_schema_is_pinned():
+    """io_cli_test.cpp:169-206"""
+    import io
+    from paper_1707_02244_b200 import io as cio
+    assert cio.kBenchCsvHeader == ("algorithm,n,m,k,seed,iterations,setup_s,total_s,final_mse,"
+                                   "footprint_bytes,iters_per_s,status")
+    row = cio.BenchRow("cadmm", 1024, 512, 102, 7, 1180, 0.25, 1.5, 9.41674e-05, 40960)
+    out = io.StringIO()
+    cio.write_bench_header(out)
+    cio.write_bench_row(out, row)
+    header, line = out.getvalue().splitlines()
+    assert header == cio.kBenchCsvHeader
+    f = line.split(",")
+    assert len(f) == 12 and f[0] == "cadmm" and f[1] == "1024" and f[4] == "7" and f[5] == "1180"
+    assert float(f[8]) == row.final_mse and f[9] == "40960" and f[11] == "ok"
+    assert float(f[10]) == pytest.approx(1180.0 / 1.25)
+    assert f[6] == "0.25" and f[7] == "1.5"  # ostream setprecision(9) general format
