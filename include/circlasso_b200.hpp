@@ -14,6 +14,7 @@
 #include <cstdint>
 #include <limits>
 #include <memory>
+#include <ostream>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -367,6 +368,62 @@ inline RecoveryReport cadmm_run(const Vector& y, const PartialCirculantOperator&
                                 const Vector* truth = nullptr) {
   CadmmState st(A, y, cfg);
   return detail::run(st, truth, cfg, A.n());
+}
+
+// ---- artifact formats (io.hpp) ---------------------------------------------------
+inline void write_vector(const Vector& v, const std::string& path) {  // io.hpp:80-87
+  check(cl_write_vector(path.c_str(), v.data(), static_cast<int64_t>(v.size())));
+}
+inline Vector read_vector(const std::string& path) {  // io.hpp:89-97
+  int64_t n = 0;
+  check(cl_read_vector(path.c_str(), nullptr, 0, &n));
+  Vector v(static_cast<size_t>(n));
+  check(cl_read_vector(path.c_str(), v.data(), n, &n));
+  return v;
+}
+inline void write_operator(const PartialCirculantOperator& A, const std::string& path) {  // io.hpp:99-112
+  const std::vector<Index>& om = A.mask().omega();
+  std::vector<int64_t> o(om.begin(), om.end());
+  check(cl_write_operator(path.c_str(), A.n(), A.m(), A.circulant().first_row().data(), o.data()));
+}
+inline PartialCirculantOperator read_operator(const std::string& path) {  // io.hpp:114-131
+  int64_t n = 0, m = 0;
+  check(cl_read_operator(path.c_str(), nullptr, 0, nullptr, 0, &n, &m));
+  Vector row(static_cast<size_t>(n));
+  std::vector<int64_t> om(static_cast<size_t>(m));
+  check(cl_read_operator(path.c_str(), row.data(), n, om.data(), m, &n, &m));
+  return PartialCirculantOperator(CirculantMatrix(std::move(row)),
+                                  SubsamplingMask(std::vector<Index>(om.begin(), om.end()), n));
+}
+
+struct BenchRow {  // io.hpp:133-153
+  std::string algorithm;
+  Index n = 0, m = 0, k = 0;
+  std::uint64_t seed = 0;
+  long iterations = 0;
+  double setup_seconds = 0.0, total_seconds = 0.0, final_mse = 0.0;
+  std::uint64_t footprint_bytes = 0;
+  std::string status = "ok";
+  cl_bench_row c() const {
+    return cl_bench_row{algorithm.c_str(), n, m, k, seed, iterations, setup_seconds, total_seconds, final_mse,
+                        footprint_bytes, status.c_str()};
+  }
+  double iterations_per_second() const {
+    const cl_bench_row r = c();
+    return cl_bench_iters_per_second(&r);
+  }
+};
+inline constexpr const char* kBenchCsvHeader =
+    "algorithm,n,m,k,seed,iterations,setup_s,total_s,final_mse,footprint_bytes,iters_per_s,status";
+inline void write_bench_header(std::ostream& out) { out << kBenchCsvHeader << "\n"; }  // io.hpp:157-159
+inline void write_bench_row(std::ostream& out, const BenchRow& row) {                 // io.hpp:161-168
+  const cl_bench_row r = row.c();
+  int64_t len = 0;
+  check(cl_bench_csv_row(&r, nullptr, 0, &len));
+  std::string text(static_cast<size_t>(len) + 1, '\0');
+  check(cl_bench_csv_row(&r, text.data(), len + 1, &len));
+  text.resize(static_cast<size_t>(len));
+  out << text << "\n";
 }
 
 }  // namespace circlasso_b200

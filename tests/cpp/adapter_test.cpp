@@ -49,6 +49,29 @@ static void cpu_checks() {
   y[3] = std::nan("");
   CHECK(throws<cl::DivergenceError>([&] { cl::ista_run(y, p.op, cfg); }));
   CHECK(throws<cl::DimensionError>([&] { cl::ista_run(cl::Vector(15, 0.0), p.op, cfg); }));
+  // artifact formats (io.hpp), the same names as the reference
+  {
+    const cl::PartialCirculantOperator A = cl::gen_circulant_sensing(64, 24, 99);
+    cl::write_operator(A, "/tmp/clb_adapter_op.bin");
+    const cl::PartialCirculantOperator back = cl::read_operator("/tmp/clb_adapter_op.bin");
+    CHECK(back.n() == 64 && back.m() == 24 && back.circulant().first_row() == A.circulant().first_row() &&
+          back.mask().omega() == A.mask().omega());
+    cl::write_vector(A.circulant().first_row(), "/tmp/clb_adapter_vec.bin");
+    CHECK(cl::read_vector("/tmp/clb_adapter_vec.bin") == A.circulant().first_row());
+    bool threw = false;
+    try {
+      cl::read_vector("/tmp/clb_adapter_missing.bin");
+    } catch (const cl::FormatError&) {
+      threw = true;
+    }
+    CHECK(threw);
+    cl::BenchRow row;
+    row.algorithm = "cadmm";
+    row.iterations = 1180;
+    row.setup_seconds = 0.25;
+    row.total_seconds = 1.5;
+    CHECK(std::abs(row.iterations_per_second() - 944.0) < 1e-9);
+  }
 }
 
 static void gpu_checks() {
