@@ -213,6 +213,16 @@ double cl_bench_iters_per_second(const cl_bench_row* row);
 cl_status cl_bench_csv_header(char* buf, int64_t cap, int64_t* len);
 cl_status cl_bench_csv_row(const cl_bench_row* row, char* buf, int64_t cap, int64_t* len);
 
+/* ---- matvec scheme benchmark (parallel.hpp:318-406; the paper's Fig. 5) ---
+ * `repeats` timed products (CUDA events) of the same seeded Gaussian circulant
+ * and input: scheme 0 = the direct circulant engine (2n unique fetches),
+ * scheme 1 = a dense row-major copy streamed by a plain GEMV (n^2 + n unique
+ * fetches; CL_ECAPACITY above dense_cap, the reference's kDenseCap = 4096 by
+ * default; B200's 180 GB allow fp32 copies up to n = 2^17).  fp32 on device. */
+cl_status cl_matvec_scheme_bench(int device, int64_t n, int scheme, int repeats, uint64_t seed, int64_t dense_cap,
+                                 double* min_s, double* mean_s, uint64_t* unique_fetches, uint64_t* vector_fetches,
+                                 double* checksum);
+
 /* ---- roofline helper ----------------------------------------------------- */
 /* FP32 FFMA peak microbenchmark on `device` (TFLOP/s), the roofline
  * denominator for the direct engine. */

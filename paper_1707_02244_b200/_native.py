@@ -88,6 +88,8 @@ _SIGS = {
     "cl_bench_iters_per_second": (C.c_double, [C.POINTER(cl_bench_row)]),
     "cl_bench_csv_header": (C.c_int, [C.c_char_p, C.c_int64, _i64]),
     "cl_bench_csv_row": (C.c_int, [C.POINTER(cl_bench_row), C.c_char_p, C.c_int64, _i64]),
+    "cl_matvec_scheme_bench": (C.c_int, [C.c_int, C.c_int64, C.c_int, C.c_int, C.c_uint64, C.c_int64, _d, _d,
+                                         C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), _d]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

@@ -47,6 +47,9 @@ void measure(const double* c, const int64_t* omega, int64_t n, int64_t m, const 
 // circulant.hpp:134-146
 void check_mask(const int64_t* omega, int64_t m, int64_t n);
 
+// matvec_scheme_bench inputs (parallel.hpp:343-348)
+void scheme_bench_inputs(int64_t n, uint64_t seed, double* row, double* x);
+
 // ---- artifact formats (io.hpp; io.cpp) ------------------------------------
 void write_vector_file(const std::string& path, const double* v, int64_t n);
 std::vector<double> read_vector_file(const std::string& path);

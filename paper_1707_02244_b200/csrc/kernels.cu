@@ -1148,6 +1148,43 @@ __global__ void k_metrics_final(const double* __restrict__ blk, double* __restri
   }
 }
 
+// ---- matvec scheme benchmark (parallel.hpp:318-406, paper Fig. 5) -------------
+// The "reference" scheme streams a dense row-major copy of the circulant
+// (n^2 + n unique fetches); the circulant scheme is the direct engine's dense
+// product (2n unique fetches).  M[i][j] = c[(j - i) mod n]  (circ_entry).
+__global__ void k_materialize_circulant(const float* __restrict__ c, float* __restrict__ M, int64_t n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / n, j = e - i * n;
+    int64_t k = j - i;
+    if (k < 0) k += n;
+    M[e] = c[k];
+  }
+}
+// out[i] = sum_j M[i][j] x[j]: one warp per row, coalesced float4 streaming, fixed-order warp tree.
+__global__ void __launch_bounds__(256) k_dense_gemv(const float* __restrict__ M, const float* __restrict__ x,
+                                                    float* __restrict__ out, int64_t n) {
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  const float* mr = M + row * n;
+  float acc = 0.f;
+  if ((n & 3) == 0) {
+    const float4* m4 = reinterpret_cast<const float4*>(mr);
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    for (int64_t j = lane; j < n / 4; j += 32) {
+      const float4 a = __ldcs(m4 + j), b = __ldg(x4 + j);
+      acc = fmaf(a.x, b.x, acc);
+      acc = fmaf(a.y, b.y, acc);
+      acc = fmaf(a.z, b.z, acc);
+      acc = fmaf(a.w, b.w, acc);
+    }
+  } else {
+    for (int64_t j = lane; j < n; j += 32) acc = fmaf(__ldcs(mr + j), __ldg(x + j), acc);
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) out[row] = acc;
+}
+
 // FP32 FFMA roofline microkernel: independent outer-product chains, one
 // shared multiplier per 32 FFMAs (the shape of the gradient/dense kernels).
 __global__ void __launch_bounds__(256) k_ffma_peak(float* out, int iters) {
@@ -1399,6 +1436,12 @@ void launch_admm_beta(const EpiArgs& a, cudaStream_t st) { k_admm_beta<<<epi_gri
 void launch_admm_x(const EpiArgs& a, cudaStream_t st) { k_admm_x<<<epi_grid(a.hi - a.lo), kThreads, 0, st>>>(a); }
 void launch_admm_duals(const EpiArgs& a, cudaStream_t st) {
   k_admm_duals<<<a.want_metrics ? kEpiBlocks : epi_grid(a.hi - a.lo), kThreads, 0, st>>>(a);
+}
+void launch_materialize_circulant(const float* c, float* M, int64_t n, cudaStream_t st) {
+  k_materialize_circulant<<<148 * 16, 256, 0, st>>>(c, M, n);
+}
+void launch_dense_gemv(const float* M, const float* x, float* out, int64_t n, cudaStream_t st) {
+  k_dense_gemv<<<static_cast<unsigned>((n * 32 + 255) / 256), 256, 0, st>>>(M, x, out, n);
 }
 void launch_metrics_final(const double* blk, double* out4, cudaStream_t st) {
   k_metrics_final<<<1, 256, 0, st>>>(blk, out4);

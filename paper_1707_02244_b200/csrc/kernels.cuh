@@ -101,6 +101,10 @@ void launch_metrics_final(const double* blk, double* out4, cudaStream_t st);
 
 void conv_kernels_init();
 
+// matvec scheme benchmark: dense row-major copy of the circulant and a plain dense GEMV
+void launch_materialize_circulant(const float* c, float* M, int64_t n, cudaStream_t st);
+void launch_dense_gemv(const float* M, const float* x, float* out, int64_t n, cudaStream_t st);
+
 // FFMA throughput microkernel (roofline denominator), returns TFLOP/s.
 double ffma_peak_tflops(int device);
 

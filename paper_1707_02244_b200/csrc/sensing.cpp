@@ -86,6 +86,13 @@ void gen_sparse_signal(int64_t n, int64_t k, uint64_t seed, double* values, int6
   }
 }
 
+// matvec_scheme_bench inputs (parallel.hpp:343-348): n row draws then n x draws of one "row" stream.
+void scheme_bench_inputs(int64_t n, uint64_t seed, double* row, double* x) {
+  Stream rng(stream_seed(seed, kTagRow));
+  for (int64_t i = 0; i < n; ++i) row[i] = rng.gauss();
+  for (int64_t i = 0; i < n; ++i) x[i] = rng.gauss();
+}
+
 void gen_circulant_sensing(int64_t n, int64_t m, uint64_t seed, double* c, int64_t* omega) {
   if (m < 1 || m > n) raise(CL_EPARAM, "gen_circulant_sensing: need 1 <= m <= n");
   Stream rs(stream_seed(seed, kTagRow));

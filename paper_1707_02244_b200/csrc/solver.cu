@@ -1172,6 +1172,92 @@ cl_status cl_bench_csv_row(const cl_bench_row* row, char* buf, int64_t cap, int6
   copy_text(bench_csv_row(*row), buf, cap, len);
   CL_GUARD_END
 }
+cl_status cl_matvec_scheme_bench(int device, int64_t n, int scheme, int repeats, uint64_t seed, int64_t dense_cap,
+                                 double* min_s, double* mean_s, uint64_t* unique_fetches, uint64_t* vector_fetches,
+                                 double* checksum) {
+  CL_GUARD_BEGIN
+  if (n < 1) raise(CL_EPARAM, "matvec_scheme_bench: n must be >= 1");
+  if (repeats < 1) raise(CL_EPARAM, "matvec_scheme_bench: repeats must be >= 1");
+  if (scheme != 0 && scheme != 1) raise(CL_EPARAM, "matvec_scheme_bench: scheme must be 0 (circulant) or 1 (reference)");
+  if (scheme == 1 && n > dense_cap) {
+    std::ostringstream msg;
+    msg << "matvec_scheme_bench: n = " << n << " exceeds the dense cap " << dense_cap;
+    raise(CL_ECAPACITY, msg.str());
+  }
+  const uint64_t un = static_cast<uint64_t>(n);
+  *unique_fetches = scheme == 0 ? 2 * un : un * un + un;  // parallel.hpp:355-361
+  *vector_fetches = scheme == 0 ? 2 * un : 3 * un;
+  std::vector<double> row(static_cast<size_t>(n)), xin(static_cast<size_t>(n));
+  scheme_bench_inputs(n, seed, row.data(), xin.data());
+  CU(cudaSetDevice(device));
+  conv_kernels_init();
+  reserve_pool(device);
+  cudaStream_t st;
+  CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  struct Guard {
+    cudaStream_t s;
+    cudaEvent_t e[2] = {};
+    ~Guard() {
+      cudaStreamSynchronize(s);
+      for (auto& v : e)
+        if (v) cudaEventDestroy(v);
+      cudaStreamDestroy(s);
+    }
+  } g{st};
+  CU(cudaEventCreate(&g.e[0]));
+  CU(cudaEventCreate(&g.e[1]));
+  const size_t nn = static_cast<size_t>(n);
+  DevBuf<float> h, x, out, part, M;
+  const std::vector<float> xf = to_f32(xin.data(), n);
+  x.alloc(nn, st);
+  x.upload(xf.data(), nn, st);
+  out.alloc(nn, st);
+  ConvPlan plan;
+  if (scheme == 0) {
+    plan = make_plan(n, dense_R(n));
+    const std::vector<float> crf = reversed(to_f32(row.data(), n));  // C x = conv(c_rev, x)
+    h.alloc(nn, st);
+    h.upload(crf.data(), nn, st);
+    part.alloc(static_cast<size_t>(plan.splits) * nn, st);
+  } else {
+    const std::vector<float> cf = to_f32(row.data(), n);
+    h.alloc(nn, st);
+    h.upload(cf.data(), nn, st);
+    M.alloc(nn * nn, st);
+    launch_materialize_circulant(h.p, M.p, n, st);
+  }
+  std::vector<float> res(nn);
+  double total = 0.0, best = 1e300, sum = 0.0;
+  for (int rep = 0; rep < repeats; ++rep) {
+    CU(cudaEventRecord(g.e[0], st));
+    if (scheme == 0) {
+      launch_conv_dense(plan, h.p, x.p, part.p, st);
+      EpiArgs a;
+      a.partial = part.p;
+      a.splits = plan.splits;
+      a.n = n;
+      a.lo = 0;
+      a.hi = n;
+      a.x = out.p;
+      launch_admm_x(a, st);
+    } else {
+      launch_dense_gemv(M.p, x.p, out.p, n, st);
+    }
+    CU(cudaEventRecord(g.e[1], st));
+    CU(cudaMemcpyAsync(res.data(), out.p, sizeof(float) * nn, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    CU(cudaGetLastError());
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, g.e[0], g.e[1]));
+    total += ms * 1e-3;
+    best = std::min(best, ms * 1e-3);
+    for (float v : res) sum += v;
+  }
+  *min_s = best;
+  *mean_s = total / repeats;
+  *checksum = sum;
+  CL_GUARD_END
+}
 cl_status cl_spectral_norm(int64_t n, const double* c, double* out) {
   CL_GUARD_BEGIN
   *out = spectral_norm(c, n);

@@ -141,3 +141,51 @@ def bench(sizes: Iterable[int], solvers: Iterable[str] = ("ista", "cadmm"), seed
                 except Exception as e:  # DivergenceError -> "diverged", others -> "error" (cli:313-320)
                     row.status = "diverged" if type(e).__name__ == "DivergenceError" else "error"
                 write_bench_row(out, row)
+
+
+# ---- matvec scheme benchmark (parallel.hpp:318-406, cli:334-372; the paper's Fig. 5) ----
+kDenseCap = 4096  # circulant.hpp:31
+
+
+@dataclass
+class SchemeTiming:
+    """parallel.hpp:329-338"""
+    scheme: str = "circulant"
+    n: int = 0
+    repeats: int = 0
+    min_seconds: float = 0.0
+    mean_seconds: float = 0.0
+    unique_fetches: int = 0
+    vector_fetches: int = 0
+    checksum: float = 0.0
+
+
+def matvec_scheme_bench(n: int, scheme: str = "circulant", repeats: int = 1, seed: int = 1,
+                        dense_cap: int = kDenseCap, device: int = 0) -> SchemeTiming:
+    """`repeats` device-timed products of the seeded circulant: "circulant" = the direct engine,
+    "reference" = a dense row-major copy through a plain GEMV (fp32 on the GPU)."""
+    if scheme not in ("circulant", "reference"):
+        raise ValueError("scheme must be 'circulant' or 'reference'")
+    mn, me, ck = C.c_double(0), C.c_double(0), C.c_double(0)
+    uf, vf = C.c_uint64(0), C.c_uint64(0)
+    _check(lib.cl_matvec_scheme_bench(device, n, 0 if scheme == "circulant" else 1, repeats, seed, dense_cap,
+                                      C.byref(mn), C.byref(me), C.byref(uf), C.byref(vf), C.byref(ck)))
+    return SchemeTiming(scheme, n, repeats, mn.value, me.value, uf.value, vf.value, ck.value)
+
+
+def matvec_bench(sizes: Iterable[int], repeats: int = 5, seed: int = 1, out: Optional[TextIO] = None,
+                 dense_cap: int = kDenseCap, device: int = 0) -> None:
+    """cli:334-372: one pinned-CSV row per (n, scheme); the dense scheme above the cap is "skipped"."""
+    out = out or sys.stdout
+    write_bench_header(out)
+    for n in sizes:
+        for scheme in ("circulant", "reference"):
+            row = BenchRow(algorithm=f"matvec-{scheme}", n=n, m=n, k=0, seed=seed)
+            if scheme == "reference" and n > dense_cap:
+                row.status = "skipped"
+                write_bench_row(out, row)
+                continue
+            t = matvec_scheme_bench(n, scheme, repeats, seed, dense_cap, device)
+            row.iterations, row.setup_seconds, row.total_seconds = repeats, 0.0, t.mean_seconds * repeats
+            row.final_mse, row.footprint_bytes = 0.0, t.unique_fetches * 8
+            write_bench_row(out, row)

@@ -640,3 +640,26 @@ def test_bench_sweeps_the_protocol_problem():
     assert all(len(r) == 12 for r in rows)
     assert [r[11] for r in rows if r[0] == "admm"] == ["skipped", "skipped"]
     assert all(r[11] == "ok" and float(r[8]) <= 1e-4 for r in rows if r[0] != "admm")
+
+
+def test_matvec_scheme_bench_accounts_fetches():
+    """parallel_test.cpp:259-277 and io_cli_test.cpp:297-315 on the GPU: fetch accounting, both schemes compute
+    the same product (fp32: to tolerance, the reference's loops agree exactly in fp64), pinned CSV rows."""
+    import io
+    from paper_1707_02244_b200 import io as cio
+    n = 64
+    c = cio.matvec_scheme_bench(n, "circulant", 3, 9)
+    r = cio.matvec_scheme_bench(n, "reference", 3, 9)
+    assert c.unique_fetches == 2 * n and c.vector_fetches == 2 * n
+    assert r.unique_fetches == n * n + n and r.vector_fetches == 3 * n
+    assert abs(c.checksum - r.checksum) <= 1e-4 * max(1.0, abs(r.checksum))
+    assert c.min_seconds <= c.mean_seconds and r.min_seconds <= r.mean_seconds and c.repeats == 3
+    big = cio.matvec_scheme_bench(cio.kDenseCap + 1, "circulant", 1)  # no cap on the circulant scheme
+    assert big.unique_fetches == 2 * (cio.kDenseCap + 1)
+    out = io.StringIO()
+    cio.matvec_bench([64], repeats=2, out=out)
+    lines = out.getvalue().splitlines()
+    assert lines[0] == cio.kBenchCsvHeader and len(lines) == 3
+    circ, ref = lines[1].split(","), lines[2].split(",")
+    assert circ[0] == "matvec-circulant" and ref[0] == "matvec-reference" and circ[5] == "2"
+    assert circ[9] == "1024" and ref[9] == "33280"

@@ -208,3 +208,14 @@ def test_bench_csv_schema_is_pinned():
     assert float(f[8]) == row.final_mse and f[9] == "40960" and f[11] == "ok"
     assert float(f[10]) == pytest.approx(1180.0 / 1.25)
     assert f[6] == "0.25" and f[7] == "1.5"  # ostream setprecision(9) general format
+
+
+def test_matvec_scheme_bench_validation_before_device():
+    """parallel_test.cpp:279-289: argument and capacity errors are raised before any device work."""
+    from paper_1707_02244_b200 import io as cio
+    with pytest.raises(cl.ParameterError):
+        cio.matvec_scheme_bench(0, "circulant", 1)
+    with pytest.raises(cl.ParameterError):
+        cio.matvec_scheme_bench(8, "circulant", 0)
+    with pytest.raises(cl.CapacityError):
+        cio.matvec_scheme_bench(cio.kDenseCap + 1, "reference", 1)
