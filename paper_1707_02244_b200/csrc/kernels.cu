@@ -177,104 +177,16 @@ k_conv_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n
 }
 
 // ===========================================================================
-// Gradient A^T r: convolution with the sparse input P^T r, rows only.
-// The staged chunk holds r scattered to its positions (zeros elsewhere) and
-// a row mask per PB-position block (a zero residual contributes exactly
-// nothing, so value != 0 is the mask).
+// Gradient A^T r (padded R = 32 layout; the small-n kernel): convolution with
+// the sparse input P^T r, rows only.  The staged chunk holds r scattered to its
+// positions (zeros elsewhere) and a row mask per PB-position block (a zero
+// residual contributes exactly nothing, so value != 0 is the mask).
 // ===========================================================================
-template <int R, int PB, int S>
-__device__ __forceinline__ void grad_pos(float (&acc)[R], const float (&w)[R + PB], uint32_t mask, float r) {
-  if (mask & (1u << S)) {
-#pragma unroll
-    for (int q = 0; q < R; ++q) acc[q] = fmaf(w[q - S + PB], r, acc[q]);
-  }
-}
-
-template <int R, int PB, int G>
-__device__ __forceinline__ void grad_group(float (&acc)[R], const float (&w)[R + PB], uint32_t mask,
-                                           const float* __restrict__ rb) {
-  if (G * 4 < PB && (mask & (0xFu << (4 * G)))) {
-    const float4 r4 = *reinterpret_cast<const float4*>(rb + 4 * G);
-    grad_pos<R, PB, 4 * G>(acc, w, mask, r4.x);
-    grad_pos<R, PB, 4 * G + 1>(acc, w, mask, r4.y);
-    grad_pos<R, PB, 4 * G + 2>(acc, w, mask, r4.z);
-    grad_pos<R, PB, 4 * G + 3>(acc, w, mask, r4.w);
-  }
-}
-
 // 32-lane ballot of a flag array into PB-bit masks, one per block.
 template <int PB>
 __device__ __forceinline__ uint32_t block_mask(uint32_t ballot32, int sub) {
   return PB == 32 ? ballot32 : (ballot32 >> (sub * PB)) & ((1u << PB) - 1u);
 }
-
-template <int R, int PB, int MINB = (R <= 32 ? 3 : 2)>
-__global__ void __launch_bounds__(kThreads, MINB)
-k_conv_rows(const float* __restrict__ h, const int* __restrict__ omega, const float* __restrict__ rv,
-            const int* __restrict__ rowstart, int64_t n, int64_t chunks, int splits, int64_t tile_lo,
-            float* __restrict__ partial) {
-  constexpr int NB = kChunk / PB;
-  using Gm = Geo<R>;
-  extern __shared__ float4 smem_f4[];
-  float* hs = reinterpret_cast<float*>(smem_f4);
-  float* rd = hs + Gm::kSegPhys;                                   // [kChunk] r scattered
-  uint32_t* bmask = reinterpret_cast<uint32_t*>(rd + kChunk);      // [NB]
-  const int64_t unit = blockIdx.x;
-  const int64_t tile = tile_lo + unit / splits;
-  const int split = static_cast<int>(unit % splits);
-  const int64_t I0 = tile * Gm::kTileR;
-  int64_t blo, bhi;
-  split_blocks(chunks, splits, split, &blo, &bhi);
-  const int own = threadIdx.x, warp = own >> 5, lane = own & 31;
-  const float* lane_base = hs + own * Gm::kPitch;
-
-  float acc[R];
-#pragma unroll
-  for (int q = 0; q < R; ++q) acc[q] = 0.f;
-
-  for (int64_t ch = blo / (kChunk / 32); ch * (kChunk / 32) < bhi; ++ch) {
-    const int64_t Jc = ch * kChunk;
-    const int r0 = rowstart[ch], nr = rowstart[ch + 1] - r0;
-    if (nr == 0) continue;  // uniform across the CTA
-    stage_segment<R>(hs, h, n, I0 - Jc - kChunk);
-    for (int s = threadIdx.x; s < kChunk; s += kThreads) rd[s] = 0.f;
-    __syncthreads();
-    for (int k = threadIdx.x; k < nr; k += kThreads) rd[omega[r0 + k] - static_cast<int>(Jc)] = __ldg(rv + r0 + k);
-    __syncthreads();
-    for (int b32 = warp; b32 < kChunk / 32; b32 += kWarps) {
-      const uint32_t mk = g_force_dense == 1 ? 0xffffffffu : g_force_dense == 2 ? 0x11111111u : g_force_dense == 3 ? 0x000000ffu : __ballot_sync(0xffffffffu, rd[b32 * 32 + lane] != 0.f);
-      if (lane == 0)
-        for (int sub = 0; sub < 32 / PB; ++sub) bmask[b32 * (32 / PB) + sub] = block_mask<PB>(mk, sub);
-    }
-    __syncthreads();
-    const int64_t bsub = 32 / (PB), cb = ch * (kChunk / 32);
-    const int b0 = static_cast<int>((blo > cb ? blo - cb : 0) * bsub);
-    const int b1 = static_cast<int>((bhi - cb < kChunk / 32 ? bhi - cb : kChunk / 32) * bsub);
-    for (int b = 0; b < kChunk / PB; ++b) {
-      if (b < b0 || b >= b1) continue;  // split covers part of the chunk (small n)
-      const uint32_t mask = bmask[b];
-      if (mask == 0u) continue;
-      float w[R + PB];
-      window_at<R, PB>(w, lane_base, kChunk - (b + 1) * PB);
-      const float* rb = rd + b * PB;
-      grad_group<R, PB, 0>(acc, w, mask, rb);
-      grad_group<R, PB, 1>(acc, w, mask, rb);
-      grad_group<R, PB, 2>(acc, w, mask, rb);
-      grad_group<R, PB, 3>(acc, w, mask, rb);
-      grad_group<R, PB, 4>(acc, w, mask, rb);
-      grad_group<R, PB, 5>(acc, w, mask, rb);
-      grad_group<R, PB, 6>(acc, w, mask, rb);
-      grad_group<R, PB, 7>(acc, w, mask, rb);
-    }
-    __syncthreads();
-  }
-  const int64_t ib = I0 + own * R;
-  float* out = partial + static_cast<int64_t>(split) * n;
-#pragma unroll
-  for (int q = 0; q < R; ++q)
-    if (ib + q < n) out[ib + q] = acc[q];
-}
-
 
 // Out-of-line layout of the 32 position bodies (R = 32, PB = 32): the common
 // case (position not a row) falls through its test; a row costs a jump to its
@@ -1235,59 +1147,18 @@ struct ResVariant {
   size_t smem;
 };
 const GradVariant kGrad[] = {
-    {32, 32, k_conv_rows_ool<4>, smem_rows<32, 32>()},  // small-n default (C3: 17.2 ms)
-    {32, 32, k_conv_rows<32, 32, 4>, smem_rows<32, 32>()},
-    {32, 32, k_conv_rows<32, 32>, smem_rows<32, 32>()},
-    {32, 16, k_conv_rows<32, 16>, smem_rows<32, 16>()},
-    {64, 16, k_conv_rows<64, 16, 3>, smem_rows<64, 16>()},
-    {64, 32, k_conv_rows<64, 32, 3>, smem_rows<64, 32>()},
-    {16, 32, k_conv_rows<16, 32>, smem_rows<16, 32>()},
-    {64, 16, k_conv_rows_ool<3, 64, 16>, smem_rows<64, 16>()},
-    {60, 32, k_grad_s<60, 3>, smem_grad_s<60>()},  // 8: streamed window, unpadded layout
-    {52, 32, k_grad_s<52, 3>, smem_grad_s<52>()},
-    {44, 32, k_grad_s<44, 4>, smem_grad_s<44>()},
-    {36, 32, k_grad_s<36, 4>, smem_grad_s<36>()},
-    {44, 32, k_grad_s<44, 3>, smem_grad_s<44>()},
-    {44, 32, k_grad_s<44, 4, true>, smem_grad_s<44>()},  // 13: pair tests; large-n default (C3: 16.0 ms)
-    {52, 32, k_grad_s<52, 3, true>, smem_grad_s<52>()},
-    {44, 32, k_grad_s<44, 1, true, 512>, smem_grad_s<44, 512>(), 512},  // 15: 16-warp CTAs (one mask per SM)
-    {44, 32, k_grad_s<44, 2, true, 256>, smem_grad_s<44, 256>(), 256},
-    {36, 32, k_grad_s<36, 1, true, 512>, smem_grad_s<36, 512>(), 512},
-    {52, 32, k_grad_s<52, 1, true, 512>, smem_grad_s<52, 512>(), 512},
+    {32, 32, k_conv_rows_ool<4>, smem_rows<32, 32>()},            // 0: small-n default (padded R = 32; C3: 17.2 ms)
+    {44, 32, k_grad_s<44, 4, true>, smem_grad_s<44>()},           // 1: large-n default (streamed, pair tests)
+    {44, 32, k_grad_s<44, 4, false>, smem_grad_s<44>()},          // 2: without pair tests
+    {52, 32, k_grad_s<52, 3, true>, smem_grad_s<52>()},           // 3: R = 52 at 3 CTAs/SM
+    {44, 32, k_grad_s<44, 1, true, 512>, smem_grad_s<44, 512>(), 512},  // 4: 16-warp CTAs
 };
 const ResVariant kRes[] = {
-    // small-n default: 4 CTAs/SM (120 registers, 55.3 KB smem; C3: 27.5 ms vs 29.0 at 3 CTAs/SM)
-    {32, 32, k_conv_residual<32, 32, 4>, smem_res<32, 32>()},
-    {32, 16, k_conv_residual<32, 16>, smem_res<32, 16>()},
-    {64, 16, k_conv_residual<64, 16>, smem_res<64, 16>()},
-    {64, 32, k_conv_residual<64, 32>, smem_res<64, 32>()},
-    {16, 32, k_conv_residual<16, 32>, smem_res<16, 32>()},
-    {32, 32, k_conv_residual<32, 32>, smem_res<32, 32>()},
-    {60, 32, k_res_s<60, 3>, smem_res_s<60>()},  // 6: streamed window, unpadded layout
-    {52, 32, k_res_s<52, 3>, smem_res_s<52>()},
-    {44, 32, k_res_s<44, 4>, smem_res_s<44>()},
-    {36, 32, k_res_s<36, 4>, smem_res_s<36>()},
-    {44, 32, k_res_s<44, 3>, smem_res_s<44>()},
-    {60, 32, k_res_s<60, 2>, smem_res_s<60>()},
-    {52, 32, k_res_s<52, 3, true>, smem_res_s<52>()},  // 12: pair tests (C3: 23.3 ms)
-    {44, 32, k_res_s<44, 3, true>, smem_res_s<44>()},
-    {52, 32, k_res_s<52, 3, true, 3>, smem_res_s<52>()},  // 14: dot chains 3 / 6 / 8 / 2
-    {52, 32, k_res_s<52, 3, true, 6>, smem_res_s<52>()},
-    {52, 32, k_res_s<52, 3, true, 8>, smem_res_s<52>()},
-    {52, 32, k_res_s<52, 3, true, 2>, smem_res_s<52>()},  // 17: large-n default (C3: 21.2 ms)
-    {52, 32, k_res_s<52, 2, true, 4>, smem_res_s<52>()},  // 18: 2 CTAs/SM (more registers)
-    {52, 32, k_res_s<52, 2, true, 8>, smem_res_s<52>()},
-    {52, 32, k_res_s<52, 3, true, 1>, smem_res_s<52>()},  // 20: one chain
-    {60, 32, k_res_s<60, 3, true, 2>, smem_res_s<60>()},
-    {44, 32, k_res_s<44, 4, true, 2>, smem_res_s<44>()},
-    {52, 32, k_res_s<52, 4, true, 2>, smem_res_s<52>()},
-    {68, 32, k_res_s<68, 3, true, 2>, smem_res_s<68>()},
-    {44, 32, k_res_s<44, 3, true, 2>, smem_res_s<44>()},
-    {52, 32, k_res_s<52, 2, true, 2, true>, smem_res_s<52>()},  // 26: FFMA2 bodies (25.9-31.3 ms: rejected)
-    {44, 32, k_res_s<44, 3, true, 2, true>, smem_res_s<44>()},
-    {36, 32, k_res_s<36, 3, true, 2, true>, smem_res_s<36>()},
-    {36, 32, k_res_s<36, 4, true, 2, true>, smem_res_s<36>()},
-    {60, 32, k_res_s<60, 2, true, 2, true>, smem_res_s<60>()},
+    {32, 32, k_conv_residual<32, 32, 4>, smem_res<32, 32>()},     // 0: small-n default (padded R = 32, 4 CTAs/SM)
+    {52, 32, k_res_s<52, 3, true, 2>, smem_res_s<52>()},          // 1: large-n default (streamed, pair tests, 2 chains)
+    {52, 32, k_res_s<52, 3, true, 4>, smem_res_s<52>()},          // 2: 4 dot chains
+    {44, 32, k_res_s<44, 4, true, 2>, smem_res_s<44>()},          // 3: R = 44 at 4 CTAs/SM
+    {44, 32, k_res_s<44, 3, true, 2, true>, smem_res_s<44>()},    // 4: FFMA2 bodies (rejected: 25.9 ms)
 };
 struct DenseVariant {
   int R;
@@ -1297,12 +1168,8 @@ struct DenseVariant {
 template <int R>
 constexpr size_t smem_dense_s() { return (GeoU<R>::kSegPhys + kChunk) * 4; }
 const DenseVariant kDense[] = {
-    {64, k_conv_dense<64>, smem_dense<64>()},  // 0: padded R = 64 (default)
-    {60, k_dense_s<60, 3>, smem_dense_s<60>()},
-    {60, k_dense_s<60, 2>, smem_dense_s<60>()},
-    {68, k_dense_s<68, 2>, smem_dense_s<68>()},
-    {52, k_dense_s<52, 3>, smem_dense_s<52>()},
-    {76, k_dense_s<76, 2>, smem_dense_s<76>()},
+    {64, k_conv_dense<64>, smem_dense<64>()},   // 0: padded R = 64 (default)
+    {68, k_dense_s<68, 2>, smem_dense_s<68>()},  // 1: streamed window (within 1.3%, not adopted)
 };
 int g_dense = 0;
 
@@ -1310,7 +1177,7 @@ int g_dense = 0;
 // kernels with pair tests at large n; the R = 32 padded kernels at small n,
 // where a 4096-index tile already covers the whole problem.
 constexpr int64_t kLargeN = int64_t(1) << 17;
-constexpr int kGradLarge = 13, kGradSmall = 0, kResLarge = 17, kResSmall = 0;
+constexpr int kGradLarge = 1, kGradSmall = 0, kResLarge = 1, kResSmall = 0;
 int g_grad = -1, g_res = -1;  // -1: choose by n
 
 }  // namespace

@@ -1,6 +1,6 @@
 """Kernel-variant sweep (experiment driver, not the bench).
 
-    python tools/variants.py GRAD:RES [GRAD:RES ...]     e.g. 0:0 8:6 10:8
+    python tools/variants.py GRAD:RES [GRAD:RES ...]     e.g. 1:1 2:1 1:2   (table indices, csrc/kernels.cu)
 
 Each pair runs in its own process (CLB_GRAD / CLB_RES select a variant of the
 sparse kernels at library load).  Per variant: C3 ISTA, per-phase kernel times
