@@ -217,14 +217,23 @@ __global__ void __launch_bounds__(kThr) k_rows(float2* __restrict__ T, const flo
       sm[rr * P + pad16(n2)] = cmulf(T[static_cast<int64_t>(p0) * N2 + e], tw[k]);
     }
   }
+  // the spectrum is fetched before the forward stages (its latency hides behind them)
+  float2 hv[per];
+#pragma unroll
+  for (int k = 0; k < per; ++k) {
+    const int e = threadIdx.x + k * kThr;
+    if (e < cnt) hv[k] = __ldg(H + static_cast<int64_t>(p0) * N2 + e);
+  }
   __syncthreads();
   dif_from<N2, N2, rows>(sm, P, tw2);
 #pragma unroll
-  for (int e = threadIdx.x; e < cnt; e += kThr) {
-    const int rr = e / N2, q = e - rr * N2;
-    const float2 h = H[static_cast<int64_t>(p0) * N2 + e];
-    float2& a = sm[rr * P + pad16(q)];
-    a = conj_h ? cmulf_conj(a, h) : cmulf(a, h);
+  for (int k = 0; k < per; ++k) {
+    const int e = threadIdx.x + k * kThr;
+    if (e < cnt) {
+      const int rr = e / N2, q = e - rr * N2;
+      float2& a = sm[rr * P + pad16(q)];
+      a = conj_h ? cmulf_conj(a, hv[k]) : cmulf(a, hv[k]);
+    }
   }
   __syncthreads();
   dit_from<N2, N2, rows>(sm, P, tw2);
@@ -238,10 +247,14 @@ __global__ void __launch_bounds__(kThr) k_rows(float2* __restrict__ T, const flo
   }
 }
 
-// Columns inverse: out[j] = Re(.) / n (rowid == nullptr), or out[rowid[j]] for rows only.
+// Columns inverse, with the consumer of the product fused into the write-out:
+//   Fft4Out::kProduct  out[j] = Re / n
+//   Fft4Out::kRows     out[rowid[j]] = Re / n at the rows
+//   Fft4Out::kResidual r[t] = y[t] - Re / n and u[j] = r[t] at the rows (P^T r kept dense)
+//   Fft4Out::kIstaStep delta[j] = Re / n, x[j] = eta(x[j] + tau delta[j])  (unchecked iterations)
+//   Fft4Out::kBeta     beta[j] = rho Re / n + sigma (z[j] - nu[j])
 template <int N1>
-__global__ void __launch_bounds__(kThr) k_cols_inv(const float2* __restrict__ T, float* __restrict__ out,
-                                                   const int* __restrict__ rowid, int N2,
+__global__ void __launch_bounds__(kThr) k_cols_inv(const float2* __restrict__ T, Fft4Out o, int N2,
                                                    const float2* __restrict__ tw1, float inv_n) {
   extern __shared__ float2 sm[];
   constexpr int B = cols_per_cta(N1), P = col_pitch(N1), cnt = B * N1;
@@ -258,11 +271,26 @@ __global__ void __launch_bounds__(kThr) k_cols_inv(const float2* __restrict__ T,
     const int i = e / B, w = e - i * B;
     const int64_t j = static_cast<int64_t>(i) * N2 + c0 + w;
     const float v = sm[w * P + pad16(i)].x * inv_n;
-    if (!rowid) {
-      out[j] = v;
+    if (o.mode == Fft4Out::kProduct) {
+      o.out[j] = v;
+    } else if (o.mode == Fft4Out::kBeta) {  // parallel.hpp:186-187
+      o.out[j] = __fadd_rn(__fmul_rn(o.rho, v), __fmul_rn(o.sigma, __fsub_rn(o.z[j], o.nu[j])));
+    } else if (o.mode == Fft4Out::kIstaStep) {
+      const float xo = o.x[j];
+      const float xn = __fadd_rn(xo, __fmul_rn(o.tau, v));  // parallel.hpp:269-271
+      o.x[j] = xn > o.thr ? xn - o.thr : (xn < -o.thr ? xn + o.thr : 0.f);
+      o.out[j] = v;
     } else {
-      const int t = __ldg(rowid + j);
-      if (t >= 0) out[t] = v;
+      const int t = __ldg(o.rowid + j);
+      if (t >= 0) {
+        if (o.mode == Fft4Out::kRows) {
+          o.out[t] = v;
+        } else {  // kResidual: cpista residual, parallel.hpp:252
+          const float rv = __ldg(o.y + t) - v;
+          o.out[t] = rv;
+          o.u[j] = rv;
+        }
+      }
     }
   }
 }
@@ -496,13 +524,13 @@ void launch_fft4_rows(const Fft4Plan& p, float2* T, const float2* H, bool conj_h
 #undef CLB_CASE
   }
 }
-void launch_fft4_cols_inv(const Fft4Plan& p, const float2* T, float* out, const int* rowid, const float2* tw1,
+void launch_fft4_cols_inv(const Fft4Plan& p, const float2* T, const Fft4Out& o, const float2* tw1,
                           cudaStream_t st) {
   const float inv_n = 1.0f / static_cast<float>(p.n);
   switch (p.N1) {
 #define CLB_CASE(N)                                                                                     \
   case N:                                                                                               \
-    k_cols_inv<N><<<p.N2 / cols_per_cta(N), kThr, cols_smem_t<N>(), st>>>(T, out, rowid, p.N2, tw1, inv_n); \
+    k_cols_inv<N><<<p.N2 / cols_per_cta(N), kThr, cols_smem_t<N>(), st>>>(T, o, p.N2, tw1, inv_n);     \
     break;
     CLB_FFT4_SIZES(CLB_CASE)
 #undef CLB_CASE

@@ -21,9 +21,21 @@ void launch_fft4_cols_fwd(const Fft4Plan& p, const float* u, float2* T, const fl
 // in place: twiddle, row DIF FFT, times H~ (or conj), row DIT inverse FFT, inverse twiddle
 void launch_fft4_rows(const Fft4Plan& p, float2* T, const float2* H, bool conj_h, const float2* tw2,
                       const float2* twA, const float2* twB, cudaStream_t st);
-// T -> column DIT inverse FFTs; out[j] = Re / n, or (rowid) out[rowid[j]] for positions with rowid[j] >= 0
-void launch_fft4_cols_inv(const Fft4Plan& p, const float2* T, float* out, const int* rowid, const float2* tw1,
-                          cudaStream_t st);
+// What the inverse column pass does with Re(y)/n (see k_cols_inv).
+struct Fft4Out {
+  enum Mode { kProduct = 0, kRows = 1, kResidual = 2, kIstaStep = 3, kBeta = 4 } mode = kProduct;
+  float* out = nullptr;         // product (n), rows (m), residual r (m), or delta (n)
+  const int* rowid = nullptr;   // position -> row (kRows, kResidual)
+  const float* y = nullptr;     // kResidual
+  float* u = nullptr;           // kResidual: dense P^T r
+  float* x = nullptr;           // kIstaStep
+  float tau = 0.f, thr = 0.f;   // kIstaStep
+  const float* z = nullptr;     // kBeta: out = rho * Re/n + sigma (z - nu)
+  const float* nu = nullptr;
+  float rho = 0.f, sigma = 0.f;
+};
+// T -> column DIT inverse FFTs, then `o`.
+void launch_fft4_cols_inv(const Fft4Plan& p, const float2* T, const Fft4Out& o, const float2* tw1, cudaStream_t st);
 // natural-order fp64 spectrum / s -> the engine's permuted fp32 order
 void launch_fft4_perm_spectrum(const Fft4Plan& p, const double2* spec, double s, float2* out, cudaStream_t st);
 // rowid[j] = t for j = omega[t], -1 elsewhere

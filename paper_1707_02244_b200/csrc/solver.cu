@@ -617,26 +617,41 @@ struct Solver {
     return fft_run(Xm, other, n, true, st);
   }
   // Four-step engine: one product = cols_fwd -> rows (twiddle, FFT, x H~, IFFT, twiddle) -> cols_inv.
-  void fft4_product(const float* u, const float2* H, bool conj_h, float* out, const int* rows_only) {
+  void fft4_product(const float* u, const float2* H, bool conj_h, const Fft4Out& o) {
     launch_fft4_cols_fwd(f4, u, F0.p, tw1.p, st);
     launch_fft4_rows(f4, F0.p, H, conj_h, tw2.p, twA.p, twB.p, st);
-    launch_fft4_cols_inv(f4, F0.p, out, rows_only, tw1.p, st);
+    launch_fft4_cols_inv(f4, F0.p, o, tw1.p, st);
+  }
+  static Fft4Out product_to(float* out) {
+    Fft4Out o;
+    o.out = out;
+    return o;
   }
   void ista_fft4_step(int want) {
     mark(0);
-    fft4_product(x.p, chatp.p, true, partial.p, rowid.p);     // P C x
+    Fft4Out res;  // r = y - P C x, and P^T r into the dense ud, in the inverse pass
+    res.mode = Fft4Out::kResidual;
+    res.out = r.p;
+    res.rowid = rowid.p;
+    res.y = y.p;
+    res.u = ud.p;
+    fft4_product(x.p, chatp.p, true, res);
     mark(1);
-    EpiArgs a;
-    a.partial = partial.p;
-    a.n = m;
-    a.lo = 0;
-    a.hi = m;
-    a.y = y.p;
-    a.r = r.p;
-    launch_ista_residual_reduce(a, 1, st);
     mark(2);
-    launch_scatter_real(r.p, omega32.p, ud.p, m, st);          // P^T r (off-row entries stay 0)
-    fft4_product(ud.p, chatp.p, false, partial.p, nullptr);    // C^T P^T r
+    if (!want) {  // unchecked iteration: the x update fused into the inverse pass
+      Fft4Out up;
+      up.mode = Fft4Out::kIstaStep;
+      up.out = delta.p;
+      up.x = x.p;
+      up.tau = static_cast<float>(tau);
+      up.thr = static_cast<float>(thr);
+      fft4_product(ud.p, chatp.p, false, up);
+      mark(3);
+      mark(4);
+      nphase = 4;
+      return;
+    }
+    fft4_product(ud.p, chatp.p, false, product_to(partial.p));  // C^T P^T r
     mark(3);
     EpiArgs b = base_args(want);
     b.splits = 1;
@@ -650,25 +665,20 @@ struct Solver {
   }
   void admm_fft4_step(int want) {
     mark(0);
-    fft4_product(v.p, chatp.p, false, partial.p, nullptr);     // C^T v
+    Fft4Out bo;  // beta = rho C^T v + sigma (z - nu), fused into the inverse pass
+    bo.mode = Fft4Out::kBeta;
+    bo.out = beta.p;
+    bo.z = z.p;
+    bo.nu = nu.p;
+    bo.rho = static_cast<float>(cfg.rho);
+    bo.sigma = static_cast<float>(cfg.sigma);
+    fft4_product(v.p, chatp.p, false, bo);
     mark(1);
-    EpiArgs a = base_args(0);
-    a.splits = 1;
-    a.beta = beta.p;
-    a.z = z.p;
-    a.nu = nu.p;
-    a.rho = static_cast<float>(cfg.rho);
-    a.sigma = static_cast<float>(cfg.sigma);
-    launch_admm_beta(a, st);
     mark(2);
-    fft4_product(beta.p, bhatp.p, true, partial.p, nullptr);   // B beta
+    fft4_product(beta.p, bhatp.p, true, product_to(x.p));      // x = B beta
     mark(3);
-    EpiArgs bx = base_args(0);
-    bx.splits = 1;
-    bx.x = x.p;
-    launch_admm_x(bx, st);
     mark(4);
-    fft4_product(x.p, chatp.p, true, partial.p, nullptr);      // C x
+    fft4_product(x.p, chatp.p, true, product_to(partial.p));      // C x
     mark(5);
     EpiArgs d2 = base_args(want);
     d2.splits = 1;
