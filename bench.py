@@ -15,7 +15,11 @@ CUDA events on the solver's stream; L2 is flushed (256 MiB write) between
 timed iterations outside the events.  Barrier + synchronize around the timed
 region, max over ranks.  `e2e` is the same metric through the public API
 (ista_run from host numpy buffers: setup, upload, K iterations, result
-download) timed on the host clock.  Rank 0 prints one JSON line.
+download) timed on the host clock (sharded: setup + K sharded iterations +
+download, max over ranks).  Rank 0 prints one JSON line; native output (NCCL
+banners) goes to stderr.  The default line also carries the FFT engine, the
+cADMM rate at n=2^20 and the time to recovery (MSE <= 1e-4) on both engines.
+BENCH_FORCE_SHARDED=1 runs the sharded NCCL path with a single rank.
 """
 from __future__ import annotations
 
@@ -246,10 +250,18 @@ def main():
     w = WORKLOADS[args.workload]
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    # the sharded (NCCL) path; BENCH_FORCE_SHARDED=1 exercises it with a single rank under torchrun
+    sharded = world > 1 or os.environ.get("BENCH_FORCE_SHARDED") == "1"
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, w, rank)
+
+    # stdout carries exactly one JSON line: anything native code prints while the bench runs (NCCL's
+    # version banner, library diagnostics) is routed to stderr at the file-descriptor level
+    sys.stdout.flush()
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
 
     import numpy as np
     import torch
@@ -257,7 +269,7 @@ def main():
     from paper_1707_02244_b200 import dist as cdist
 
     torch.cuda.set_device(local_rank)
-    if world > 1:
+    if sharded:
         import torch.distributed as tdist
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     assert args.warmup >= 3 or os.environ.get("BENCH_ALLOW_SHORT_WARMUP"), "need >= 3 warm-up steps"
@@ -267,7 +279,7 @@ def main():
     setup = cl.ista_setup if w["kind"] == "ista" else cl.cadmm_setup
     st = setup(prob.op, prob.measurements, cfg, device=local_rank)
     shard = gather = None
-    if world > 1:
+    if sharded:
         shard = cdist.CudaShard(st, rank, world)
         gather = cdist.TorchGather()
 
@@ -289,7 +301,7 @@ def main():
     st.synchronize()
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    if world > 1:
+    if sharded:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local_rank) as clocks:
@@ -302,11 +314,11 @@ def main():
                 ev[i][1].record(sp_stream)
         st.synchronize()
         torch.cuda.synchronize()
-    if world > 1:
+    if sharded:
         torch.distributed.barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(step_ms)
-    if world > 1:
+    if sharded:
         t = torch.tensor([total_ms], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
@@ -343,8 +355,14 @@ def main():
         pass
 
     # e2e: the public API from host buffers (setup + upload + K iterations + download)
+    n, m = w["n"], w["m"]
+    chunks = (n + 1023) // 1024
+    # bytes the setup moves host->device (device fp64 setup for power-of-two n >= 2^14: the fp64 row; the
+    # fp32 y, int32 omega and the chunk row index for ISTA; the fp32 D and P^T y for cADMM)
+    h2d = (8 * n + 4 * m + 4 * m + 4 * (chunks + 1)) if w["kind"] == "ista" else (16 * n)
+    d2h = 4 * n + 32  # the iterate and the fused check metrics
     e2e = None
-    if world == 1:
+    if not sharded:
         cfg_e2e = cl.SolverConfig(max_iter=args.steps, check_every=args.steps)
         run = cl.ista_run if w["kind"] == "ista" else cl.cadmm_run
         torch.cuda.synchronize()
@@ -352,19 +370,36 @@ def main():
         rep = run(prob.measurements, prob.op, cfg_e2e, device=local_rank)
         e2e_s = time.perf_counter() - t0
         assert rep.iterations == args.steps
-        n, m = w["n"], w["m"]
-        chunks = (n + 1023) // 1024
-        h2d = (8 * n + 8 * m + 4 * (chunks + 1)) if w["kind"] == "ista" else (20 * n)
-        d2h = 4 * n + 32
         e2e = {"value": args.steps / e2e_s, "unit": "iterations/s", "h2d_bytes_per_step": h2d / args.steps,
                "d2h_bytes_per_step": d2h / args.steps, "wall_s": e2e_s, "report_setup_s": rep.setup_seconds,
                "report_total_s": rep.total_seconds,
                "note": "ista_run/cadmm_run from host fp64 buffers incl. setup (spectral norm, Gram inverse), "
                        "upload, K iterations and final download; host clock"}
+    else:
+        # sharded: every rank sets up from host buffers, runs K sharded iterations (all-gathers over NCCL) and
+        # rank 0 downloads the iterate; the slowest rank's wall time
+        torch.distributed.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        st2 = setup(prob.op, prob.measurements, cfg, device=local_rank)
+        sh2 = cdist.CudaShard(st2, rank, world)
+        cdist.sharded_step(sh2, gather, args.steps)
+        st2.synchronize()
+        if rank == 0:
+            st2.get("x" if w["kind"] == "ista" else "z")
+        e2e_s = time.perf_counter() - t0
+        t = torch.tensor([e2e_s], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+        e2e = {"value": args.steps / e2e_s, "unit": "iterations/s", "h2d_bytes_per_step": world * h2d / args.steps,
+               "d2h_bytes_per_step": d2h / args.steps, "wall_s": e2e_s,
+               "note": f"{world} ranks: setup from host fp64 buffers, K sharded iterations with NCCL all-gathers, "
+                       "iterate download on rank 0; max wall time over ranks"}
+        del sh2, st2
 
     # the same workload through the on-device FFT engine (use_fft=True, the reference's default engine)
     fft_line = None
-    if world == 1 and (w["n"] & (w["n"] - 1)) == 0:
+    if not sharded and (w["n"] & (w["n"] - 1)) == 0:
         fst = setup(prob.op, prob.measurements, cl.SolverConfig(use_fft=True), device=local_rank)
         fst.step(3)
         fst.synchronize()
@@ -403,12 +438,12 @@ def main():
         del fst
 
     admm = recovery = None
-    if world == 1 and w["kind"] == "ista" and w["n"] == (1 << 20) and not args.quick:
+    if not sharded and w["kind"] == "ista" and w["n"] == (1 << 20) and not args.quick:
         admm = admm_line(cl, torch, prob, local_rank, flush)
         recovery = recovery_line(cl, prob, local_rank)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not sharded and not args.no_cpu_baseline:
         cpu, _ = cpu_baseline_line(w, 3 if w["n"] >= (1 << 20) else 20, 1)
         if fft_line is not None:
             fft_line["cpu_fft_engine"] = {
@@ -426,6 +461,8 @@ def main():
                     it = recovery[kind]["direct"]["iterations"]
                     recovery[kind]["cpu_phase_engine_seconds_extrapolated"] = it / rate
 
+    sys.stdout.flush()
+    os.dup2(json_fd, 1)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world, "steps": args.steps,
@@ -433,7 +470,7 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (make_problem, seeded)",
             "config": {"workload": w["desc"], "n": w["n"], "m": w["m"], "k": w["k"], "seed": w["seed"],
                        "engine": "direct shift-indexed sm_100a kernels", "l2": "flushed (256 MiB) between steps",
-                       "parallelism": f"row/output shards x{world}" if world > 1 else "single GPU"},
+                       "parallelism": f"row/output shards x{world}" if sharded else "single GPU"},
             "roofline": {"bound": "fp32_ffma", "kernel": k_name, "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                          "peak_source": "live FFMA microbenchmark (cl_ffma_peak); MEASURED_PEAKS.json has no FP32 entry",
@@ -449,7 +486,7 @@ def main():
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded:
         torch.distributed.destroy_process_group()
 
 
