@@ -1230,6 +1230,9 @@ ConvPlan make_plan(int64_t n, int R) {
   p.chunks = (n + kChunk - 1) / kChunk;
   const int64_t units = target_units(n);
   int64_t s = (units + p.tiles - 1) / p.tiles;
+  // a multiple of 8 splits: the residual is sharded by splits, so 2, 4 and 8 ranks get equal chunk
+  // counts (a function of n only, like everything in the plan)
+  if (s >= 8) s = (s + 7) / 8 * 8;
   const int64_t blocks32 = p.chunks * (kChunk / 32);  // splits are ranges of 32-position blocks
   if (s < 1) s = 1;
   if (s > blocks32) s = blocks32;
