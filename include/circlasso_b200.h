@@ -48,7 +48,8 @@ typedef enum cl_kind { CL_KIND_ISTA = 0, CL_KIND_CADMM = 1 } cl_kind;
 typedef enum cl_metric { CL_METRIC_MSE_VS_TRUTH = 0, CL_METRIC_ITERATE_CHANGE = 1 } cl_metric; /* solvers.hpp:130 */
 /* Product engine (SolverConfig::use_fft, solvers.hpp:123): the direct
  * shift-indexed kernels (the paper's OpenCL scheme, north star) or the
- * on-device FFT (the reference's default; power-of-two n). */
+ * on-device FFT (the reference's default; any n: non-power-of-two n runs as a
+ * linear convolution in the next power of two >= 2n-1). */
 typedef enum cl_engine { CL_ENGINE_DIRECT = 0, CL_ENGINE_FFT = 1 } cl_engine;
 
 /* SolverConfig, solvers.hpp:112-125 (use_fft -> engine; dense_cap has no

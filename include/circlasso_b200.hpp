@@ -82,7 +82,7 @@ struct SolverConfig {
   double target_mse = std::numeric_limits<double>::quiet_NaN();
   int check_every = 10;
   ThresholdPairing pairing = ThresholdPairing::kLiteral;
-  bool use_fft = false;  // true: on-device FFT engine (power-of-two n); false: direct sm_100a kernels
+  bool use_fft = false;  // true: on-device FFT engine (any n); false: direct sm_100a kernels
   int device = 0;       // new: CUDA device of the solve
 
   cl_config c() const {

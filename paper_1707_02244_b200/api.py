@@ -124,7 +124,8 @@ class SolverConfig:
     FFT engine; here the default is the direct shift-indexed sm_100a kernels
     (the paper's scheme and the north-star path, the reference's
     ``use_fft=false`` arithmetic); ``use_fft=True`` runs the on-device FFT
-    engine (power-of-two n).  ``dense_cap`` is accepted for source
+    engine (any n: non-power-of-two n is embedded as a linear convolution in the
+    next power of two >= 2n-1).  ``dense_cap`` is accepted for source
     compatibility (dense ADMM is out of scope)."""
     alpha: float = 1e-4
     tau: float = 0.0

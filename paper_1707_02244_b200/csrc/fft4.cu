@@ -271,6 +271,7 @@ __global__ void __launch_bounds__(kThr) k_cols_inv(const float2* __restrict__ T,
     const int i = e / B, w = e - i * B;
     const int64_t j = static_cast<int64_t>(i) * N2 + c0 + w;
     const float v = sm[w * P + pad16(i)].x * inv_n;
+    if (j >= o.n_valid) continue;
     if (o.mode == Fft4Out::kProduct) {
       o.out[j] = v;
     } else if (o.mode == Fft4Out::kBeta) {  // parallel.hpp:186-187

@@ -1,5 +1,6 @@
 // Four-step FFT engine (fp32 complex, power-of-two 2^14 <= n <= 2^24); see fft4.cu.
 #pragma once
+#include <climits>
 #include <cstdint>
 #include <vector>
 #include <cuda_runtime.h>
@@ -33,6 +34,7 @@ struct Fft4Out {
   const float* z = nullptr;     // kBeta: out = rho * Re/n + sigma (z - nu)
   const float* nu = nullptr;
   float rho = 0.f, sigma = 0.f;
+  int64_t n_valid = INT64_MAX;  // outputs j >= n_valid (the padded engine's convolution tail) are not written
 };
 // T -> column DIT inverse FFTs, then `o`.
 void launch_fft4_cols_inv(const Fft4Plan& p, const float2* T, const Fft4Out& o, const float2* tw1, cudaStream_t st);

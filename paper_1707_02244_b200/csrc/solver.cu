@@ -177,6 +177,11 @@ struct Solver {
   DevBuf<float> partial, truth;
   DevBuf<float2> chat, bhat, F0, F1;  // FFT engine: spectra of c~ (and of B), work buffers
   bool fft = false;
+  // FFT length: n for power-of-two n; otherwise the next power of two >= 2n - 1, with the circulant
+  // embedded as a linear convolution (g[k] = h[k mod n], k in (-n, n), placed mod nfft; inputs zero-padded)
+  // so any n runs on power-of-two transforms, like the reference's kissfft runs any n.
+  int64_t nfft = 0;
+  std::vector<double> padded_cn, padded_bn;  // cADMM setup hand-over (normalized c and b rows)
   // Four-step FFT engine (fft4.cu; power-of-two 2^14 <= n <= 2^24 with the device setup): the
   // spectra in its permuted order, twiddle tables, the row map and P^T r kept dense.
   bool fft4 = false;
@@ -249,7 +254,14 @@ struct Solver {
     if (cfg.engine != CL_ENGINE_DIRECT && cfg.engine != CL_ENGINE_FFT)
       raise(CL_EPARAM, "cl_solver_create: unknown engine");
     fft = cfg.engine == CL_ENGINE_FFT;
-    if (fft && !is_pow2(n)) raise(CL_EPARAM, "cl_solver_create: the FFT engine needs a power-of-two n");
+    if (fft) {
+      nfft = n;
+      if (!is_pow2(n)) {
+        nfft = 1;
+        while (nfft < 2 * n - 1) nfft <<= 1;
+        if (nfft > (int64_t(1) << 26)) raise(CL_ECAPACITY, "cl_solver_create: n too large for the padded FFT engine");
+      }
+    }
   }
 
   // solvers.hpp:170-183.  `s` = max_k |DFT(c)_k| (host or device transform).
@@ -360,9 +372,10 @@ struct Solver {
     const std::vector<float> yf = to_f32(yh, m, scale);
     y.alloc(static_cast<size_t>(m), st);
     y.upload(yf.data(), yf.size(), st);
+    const int64_t nv = std::max(n, nfft);  // the FFT engine reads zero-padded inputs of length nfft
     for (DevBuf<float>* b : {&r}) { b->alloc(static_cast<size_t>(m), st); b->zero(st); }
-    for (DevBuf<float>* b : {&x, &delta}) { b->alloc(static_cast<size_t>(n), st); b->zero(st); }
-    partial.alloc(static_cast<size_t>(std::max<int64_t>(rplan.tiles * m, plan.splits * n)), st);
+    for (DevBuf<float>* b : {&x, &delta}) { b->alloc(static_cast<size_t>(nv), st); b->zero(st); }
+    partial.alloc(static_cast<size_t>(std::max<int64_t>(std::max<int64_t>(rplan.tiles * m, plan.splits * n), nv)), st);
     blk.alloc(kEpiBlocks * 4, st);
     met.alloc(4, st);
     set_shard(0, 1);
@@ -372,6 +385,10 @@ struct Solver {
       launch_rowid(omega32.p, rowid.p, n, m, st);
       ud.alloc(static_cast<size_t>(n), st);
       ud.zero(st);
+    } else if (fft && nfft != n) {
+      std::vector<double> cn(static_cast<size_t>(n));
+      for (int64_t i = 0; i < n; ++i) cn[static_cast<size_t>(i)] = c[i] / scale;
+      setup_padded_fft(cn.data(), nullptr);
     } else if (fft) {
       if (dev) {
         chat.alloc(static_cast<size_t>(n), st);
@@ -388,6 +405,58 @@ struct Solver {
     CU(cudaGetLastError());
     device_setup_release();
     CU(cudaStreamSynchronize(st));
+  }
+
+  // spectrum (length nfft, fp64, host) of the circulant with first row h embedded for a linear
+  // convolution: g[k mod nfft] = h[k mod n], k in (-n, n)
+  std::vector<cplx> padded_spectrum(const double* h) const {
+    std::vector<double> g(static_cast<size_t>(nfft), 0.0);
+    for (int64_t k = 0; k < n; ++k) g[static_cast<size_t>(k)] = h[k];
+    for (int64_t k = 1; k < n; ++k) g[static_cast<size_t>(nfft - k)] = h[n - k];
+    return dft_real(g.data(), nfft);
+  }
+  void upload_engine_spectrum(const std::vector<cplx>& spec, DevBuf<float2>& natural, DevBuf<float2>& perm) {
+    if (!fft4) {
+      upload_spectrum(natural, spec);
+      return;
+    }
+    std::vector<double2> d(spec.size());
+    for (size_t k = 0; k < spec.size(); ++k) d[k] = make_double2(spec[k].real(), spec[k].imag());
+    DevBuf<double2> tmp;
+    tmp.alloc(d.size(), st);
+    tmp.upload(d.data(), d.size(), st);
+    perm.alloc(d.size(), st);
+    launch_fft4_perm_spectrum(f4, tmp.p, 1.0, perm.p, st);
+    CU(cudaStreamSynchronize(st));  // d goes out of scope
+  }
+  // the padded (non-power-of-two n) FFT engine: four-step if nfft fits it, else Stockham passes
+  void setup_padded_fft(const double* cn, const double* bn) {
+    const char* v = std::getenv("CLB_FFT_STOCKHAM");
+    if (fft4_supported(nfft) && !(v && v[0] == '1')) {
+      fft4 = true;
+      f4 = fft4_plan(nfft);
+      fft4_init_attributes();
+      std::vector<float2> t1, t2, ta, tb;
+      fft4_twiddles(f4, &t1, &t2, &ta, &tb);
+      for (auto& pr : {std::make_pair(&tw1, &t1), std::make_pair(&tw2, &t2), std::make_pair(&twA, &ta),
+                       std::make_pair(&twB, &tb)}) {
+        pr.first->alloc(pr.second->size(), st);
+        pr.first->upload(pr.second->data(), pr.second->size(), st);
+      }
+      CU(cudaStreamSynchronize(st));
+    }
+    upload_engine_spectrum(padded_spectrum(cn), chat, chatp);
+    if (bn) upload_engine_spectrum(padded_spectrum(bn), bhat, bhatp);
+    F0.alloc(static_cast<size_t>(nfft), st);
+    if (!fft4) F1.alloc(static_cast<size_t>(nfft), st);
+    if (kind == CL_KIND_ISTA) {
+      if (fft4) {
+        rowid.alloc(static_cast<size_t>(nfft), st);
+        launch_rowid(omega32.p, rowid.p, nfft, m, st);
+      }
+      ud.alloc(static_cast<size_t>(nfft), st);
+      ud.zero(st);
+    }
   }
 
   void setup_small_fft() {
@@ -487,7 +556,10 @@ struct Solver {
       hcr.upload(crf.data(), crf.size(), st);
       const std::vector<float> brf = reversed(to_f32(bh.data(), n));
       hbr.upload(brf.data(), brf.size(), st);
-      if (fft) {
+      if (fft && nfft != n) {
+        padded_cn.assign(cn.begin(), cn.end());
+        padded_bn.assign(bh.begin(), bh.end());
+      } else if (fft) {
         const std::vector<cplx> cs = dft_real(cn.data(), n);
         upload_spectrum(chat, cs);
         // B's spectrum is real: 1 / (rho |c_k|^2 + sigma) (circulant.hpp:306-317), exact before the idft round trip
@@ -506,12 +578,17 @@ struct Solver {
     d.upload(df.data(), df.size(), st);
     pty.alloc(static_cast<size_t>(n), st);
     pty.upload(pf.data(), pf.size(), st);
-    for (DevBuf<float>* b : {&x, &z, &nu, &mu, &v, &beta}) { b->alloc(static_cast<size_t>(n), st); b->zero(st); }
-    partial.alloc(static_cast<size_t>(plan.splits * n), st);
+    const int64_t nv = std::max(n, nfft);  // the FFT engine reads zero-padded inputs of length nfft
+    for (DevBuf<float>* b : {&x, &z, &nu, &mu, &v, &beta}) { b->alloc(static_cast<size_t>(nv), st); b->zero(st); }
+    partial.alloc(static_cast<size_t>(std::max<int64_t>(plan.splits * n, nv)), st);
     blk.alloc(kEpiBlocks * 4, st);
     met.alloc(4, st);
     rowstart_host.assign(static_cast<size_t>(plan.chunks + 1), 0);
-    if (fft && !fft4) {
+    if (fft && nfft != n) {
+      setup_padded_fft(padded_cn.data(), padded_bn.data());
+      padded_cn.clear();
+      padded_bn.clear();
+    } else if (fft && !fft4) {
       F0.alloc(static_cast<size_t>(n), st);
       F1.alloc(static_cast<size_t>(n), st);
       if (small_fft_cadmm_supported(n)) setup_small_fft();
@@ -610,11 +687,11 @@ struct Solver {
   // ---- FFT engine (circ_matvec_fft / circ_transpose_matvec, circulant.hpp:236-274) ----
   // out_real[i] = Re(idft(H^(*) . dft(u)))[i] (conj_h: C x, else C^T x), into `partial`.
   const float2* fft_product(const float2* H, bool conj_h) {
-    const float2* X = fft_run(F0.p, F1.p, n, false, st);
+    const float2* X = fft_run(F0.p, F1.p, nfft, false, st);
     float2* Xm = const_cast<float2*>(X);
-    launch_spec_mul(Xm, H, conj_h, n, st);
+    launch_spec_mul(Xm, H, conj_h, nfft, st);
     float2* other = Xm == F0.p ? F1.p : F0.p;
-    return fft_run(Xm, other, n, true, st);
+    return fft_run(Xm, other, nfft, true, st);
   }
   // Four-step engine: one product = cols_fwd -> rows (twiddle, FFT, x H~, IFFT, twiddle) -> cols_inv.
   void fft4_product(const float* u, const float2* H, bool conj_h, const Fft4Out& o) {
@@ -622,14 +699,16 @@ struct Solver {
     launch_fft4_rows(f4, F0.p, H, conj_h, tw2.p, twA.p, twB.p, st);
     launch_fft4_cols_inv(f4, F0.p, o, tw1.p, st);
   }
-  static Fft4Out product_to(float* out) {
+  Fft4Out product_to(float* out) const {
     Fft4Out o;
     o.out = out;
+    o.n_valid = n;
     return o;
   }
   void ista_fft4_step(int want) {
     mark(0);
     Fft4Out res;  // r = y - P C x, and P^T r into the dense ud, in the inverse pass
+    res.n_valid = n;
     res.mode = Fft4Out::kResidual;
     res.out = r.p;
     res.rowid = rowid.p;
@@ -640,6 +719,7 @@ struct Solver {
     mark(2);
     if (!want) {  // unchecked iteration: the x update fused into the inverse pass
       Fft4Out up;
+      up.n_valid = n;
       up.mode = Fft4Out::kIstaStep;
       up.out = delta.p;
       up.x = x.p;
@@ -666,6 +746,7 @@ struct Solver {
   void admm_fft4_step(int want) {
     mark(0);
     Fft4Out bo;  // beta = rho C^T v + sigma (z - nu), fused into the inverse pass
+    bo.n_valid = n;
     bo.mode = Fft4Out::kBeta;
     bo.out = beta.p;
     bo.z = z.p;
@@ -699,9 +780,9 @@ struct Solver {
   }
   void ista_fft_step(int want) {
     mark(0);
-    launch_real_to_complex(x.p, F0.p, n, st);
+    launch_real_to_complex(x.p, F0.p, nfft, st);
     const float2* Y = fft_product(chat.p, true);               // C x
-    launch_gather_real(Y, omega32.p, partial.p, n, m, st);      // P C x
+    launch_gather_real(Y, omega32.p, partial.p, nfft, m, st);   // P C x
     mark(1);
     EpiArgs a;
     a.partial = partial.p;
@@ -712,9 +793,9 @@ struct Solver {
     a.r = r.p;
     launch_ista_residual_reduce(a, 1, st);
     mark(2);
-    launch_embed_rows(r.p, omega32.p, F0.p, n, m, st);         // P^T r
+    launch_embed_rows(r.p, omega32.p, F0.p, nfft, m, st);      // P^T r
     const float2* D = fft_product(chat.p, false);              // C^T P^T r
-    launch_extract_real(D, partial.p, n, st);
+    launch_extract_real(D, partial.p, nfft, st);
     mark(3);
     EpiArgs b = base_args(want);
     b.splits = 1;
@@ -728,8 +809,8 @@ struct Solver {
   }
   void admm_fft_step(int want) {
     mark(0);
-    launch_real_to_complex(v.p, F0.p, n, st);
-    launch_extract_real(fft_product(chat.p, false), partial.p, n, st);  // C^T v
+    launch_real_to_complex(v.p, F0.p, nfft, st);
+    launch_extract_real(fft_product(chat.p, false), partial.p, nfft, st);  // C^T v
     mark(1);
     EpiArgs a = base_args(0);
     a.splits = 1;
@@ -740,16 +821,16 @@ struct Solver {
     a.sigma = static_cast<float>(cfg.sigma);
     launch_admm_beta(a, st);
     mark(2);
-    launch_real_to_complex(beta.p, F0.p, n, st);
-    launch_extract_real(fft_product(bhat.p, true), partial.p, n, st);   // B beta
+    launch_real_to_complex(beta.p, F0.p, nfft, st);
+    launch_extract_real(fft_product(bhat.p, true), partial.p, nfft, st);   // B beta
     mark(3);
     EpiArgs bx = base_args(0);
     bx.splits = 1;
     bx.x = x.p;
     launch_admm_x(bx, st);
     mark(4);
-    launch_real_to_complex(x.p, F0.p, n, st);
-    launch_extract_real(fft_product(chat.p, true), partial.p, n, st);   // C x
+    launch_real_to_complex(x.p, F0.p, nfft, st);
+    launch_extract_real(fft_product(chat.p, true), partial.p, nfft, st);   // C x
     mark(5);
     EpiArgs d2 = base_args(want);
     d2.splits = 1;

@@ -267,10 +267,22 @@ def test_fft_engine_matches_direct_engine_c3():
     assert_parity(a.get("x"), b.get("x"), what="fft vs direct")
 
 
-def test_fft_engine_rejects_non_power_of_two():
-    p = cl.make_problem(1000, 300, 10, 1)
-    with pytest.raises(cl.ParameterError):
-        cl.ista_setup(p.op, p.measurements, cl.SolverConfig(use_fft=True))
+@pytest.mark.parametrize("kind,n,m,k,seed,iters", [("ista", 1000, 300, 10, 1, 60), ("cadmm", 1000, 500, 10, 2, 40),
+                                                   ("ista", 10007, 2500, 40, 3, 30), ("cadmm", 10007, 5000, 40, 4, 20),
+                                                   ("ista", 300007, 75000, 1000, 5, 5)])
+def test_fft_engine_non_power_of_two_matches_oracle(kind, n, m, k, seed, iters):
+    """use_fft=True (the reference's default engine) at any n: the circulant is embedded as a linear
+    convolution in the next power of two >= 2n-1 (Stockham passes below 2^14, four-step above)."""
+    p = orc.make_problem(n, m, k, seed)
+    setup = cl.ista_setup if kind == "ista" else cl.cadmm_setup
+    g = setup(op_of(p), p.y, cl.SolverConfig(use_fft=True))
+    g.step(iters)
+    o = (orc.Ista if kind == "ista" else orc.Cadmm)(p.row, p.omega, p.y)
+    o.step(iters, orc.ENGINE_FFT)
+    f = "x" if kind == "ista" else "z"
+    assert_parity(g.get(f), o.get(f), what=f)
+    for h in (("r",) if kind == "ista" else ("x", "v", "mu", "nu", "beta")):
+        assert rel_l2(g.get(h), o.get(h)) <= REL_TOL, h
 
 
 def test_fft_engine_protocol_recovery():
