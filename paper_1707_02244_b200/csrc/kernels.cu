@@ -1168,10 +1168,16 @@ struct DenseVariant {
 template <int R>
 constexpr size_t smem_dense_s() { return (GeoU<R>::kSegPhys + kChunk) * 4; }
 const DenseVariant kDense[] = {
-    {64, k_conv_dense<64>, smem_dense<64>()},   // 0: padded R = 64 (default)
+    {64, k_conv_dense<64>, smem_dense<64>()},   // 0: padded R = 64 (default for n > 4096)
     {68, k_dense_s<68, 2>, smem_dense_s<68>()},  // 1: streamed window (within 1.3%, not adopted)
+    {32, k_conv_dense<32>, smem_dense<32>()},   // 2: R = 32: a 4096-index tile (default for 2048 < n <= 4096)
+    {16, k_conv_dense<16>, smem_dense<16>()},   // 3: R = 16: a 2048-index tile (default for n <= 2048)
 };
-int g_dense = 0;
+int g_dense = -1;  // -1: choose by n (a tile no longer than n: no idle threads at small n)
+static int dense_index(int64_t n) {
+  if (g_dense >= 0) return g_dense;
+  return n <= 2048 ? 3 : n <= 4096 ? 2 : 0;
+}
 
 // Defaults (measured best on B200, tools/variants.py): the streamed-window
 // kernels with pair tests at large n; the R = 32 padded kernels at small n,
@@ -1201,9 +1207,8 @@ static const ResVariant& res_variant(int64_t n) {
   return kRes[g_res >= 0 ? g_res : (n >= kLargeN ? kResLarge : kResSmall)];
 }
 int dense_R(int64_t n) {
-  (void)n;
   select_variants();
-  return kDense[g_dense].R;
+  return kDense[dense_index(n)].R;
 }
 // plan "R" = indices per 128 threads (the tile is kThreads * R)
 int grad_R(int64_t n) { return grad_variant(n).R * grad_variant(n).nt / kThreads; }
@@ -1264,7 +1269,8 @@ void conv_kernels_init() {
 void launch_conv_dense(const ConvPlan& p, const float* h, const float* u, float* partial, cudaStream_t st) {
   const int64_t units = (p.tile_hi - p.tile_lo) * p.splits;
   if (units <= 0) return;
-  const DenseVariant& d = kDense[g_dense];
+  select_variants();
+  const DenseVariant& d = kDense[dense_index(p.n)];
   d.fn<<<static_cast<unsigned>(units), kThreads, d.smem, st>>>(h, u, p.n, p.chunks, p.splits, p.tile_lo, partial);
 }
 
