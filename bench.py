@@ -340,7 +340,7 @@ def main():
     if w["kind"] == "ista":
         k_ms = statistics.mean(p[0] for p in phase_ms)
         k_flops = 2.0 * w["m"] * w["n"] / world
-        k_name = "k_res_s"
+        k_name = "k_res_s" if w["n"] >= (1 << 17) else "k_conv_residual"  # large-n / small-n residual kernel
     else:
         k_ms = statistics.mean(p[0] for p in phase_ms)
         k_flops = 2.0 * w["n"] * w["n"] / world
