@@ -22,7 +22,11 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "kernels.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace clb {
 
@@ -914,6 +918,260 @@ k_res_s(const float* __restrict__ h, const float* __restrict__ x, const int* __r
 }
 
 // ===========================================================================
+// Persistent cooperative cADMM for small n (config 2: n = 4096).
+// One launch runs all unchecked iterations; CTA b owns position block b (the
+// 32 inputs of each product it multiplies in, with the three operator rows'
+// segments staged once in shared memory) and outputs [32 b, 32 b + 32) for the
+// fused updates.  Per iteration (cpadmm_phases, parallel.hpp:173-231):
+//   C^T v -> beta -> B beta -> x -> C x -> duals, a grid barrier after each
+// product (split-K partials) and each update.  The tile is the whole problem
+// (128 threads x R = n); partials are summed in ascending block order.
+// ===========================================================================
+template <int R>
+__device__ __forceinline__ void coop_product(float (&acc)[R], const float* __restrict__ lane_base,
+                                             const float* __restrict__ us) {
+  constexpr int PB = 32;
+#pragma unroll
+  for (int q = 0; q < R; ++q) acc[q] = 0.f;
+  float w[R + PB];
+  window_at<R, PB>(w, lane_base, 0);
+#pragma unroll
+  for (int s4 = 0; s4 < PB; s4 += 4) {
+    const float4 uu = *reinterpret_cast<const float4*>(us + s4);
+    const float uv[4] = {uu.x, uu.y, uu.z, uu.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+#pragma unroll
+      for (int q = 0; q < R; ++q) acc[q] = fmaf(w[q - (s4 + e) + PB], uv[e], acc[q]);
+    }
+  }
+}
+
+struct CoopArgs {
+  const float *hc, *hbr, *hcr, *d, *pty;
+  float *x, *z, *nu, *mu, *v, *beta, *partial;
+  int64_t n;
+  float rho, sigma, tau1, tau2, thr;
+  int iters;
+};
+
+template <int R>
+__global__ void __launch_bounds__(kThreads, 1) k_coop_cadmm(CoopArgs a) {
+  using G = Geo<R>;
+  constexpr int PB = 32;
+  constexpr int SEG = G::pad(G::kTileR + PB) + 4;  // one block's segment (logical kTileR + 32)
+  extern __shared__ float4 smem_f4[];
+  float* s_c = reinterpret_cast<float*>(smem_f4);
+  float* s_b = s_c + SEG;
+  float* s_r = s_b + SEG;
+  float* us = s_r + SEG;          // [32]
+  float* red = us + PB;           // [4][32]
+  cg::grid_group grid = cg::this_grid();
+  const int64_t n = a.n;
+  const int b = blockIdx.x, own = threadIdx.x;
+  const int64_t Jb = static_cast<int64_t>(b) * PB;
+  // segments hs[pad(e)] = h[(-Jb - 32 + e) mod n], e < kTileR + 32 (I0 = 0: one tile)
+  for (int e = threadIdx.x; e < G::kTileR + PB; e += kThreads) {
+    int64_t k = (e - Jb - PB) % n;
+    if (k < 0) k += n;
+    s_c[G::pad(e)] = a.hc[k];
+    s_b[G::pad(e)] = a.hbr[k];
+    s_r[G::pad(e)] = a.hcr[k];
+  }
+  __syncthreads();
+  const int ib = own * R;
+  float acc[R];
+  const int o = own & 31, part = own >> 5;
+  const int64_t i_out = Jb + o;  // this thread's output in the update phases (parts combined by thread o)
+  auto sum_partials = [&](void) -> float {  // fixed order: 4 parts of 32 blocks, ascending
+    const int nb = static_cast<int>(gridDim.x);
+    const int k0 = part * ((nb + 3) / 4), k1 = min(nb, k0 + (nb + 3) / 4);
+    float sacc = 0.f;
+    for (int k = k0; k < k1; ++k) sacc += a.partial[static_cast<int64_t>(k) * n + i_out];
+    red[part * 32 + o] = sacc;
+    __syncthreads();
+    const float tot = (red[o] + red[32 + o]) + (red[64 + o] + red[96 + o]);
+    __syncthreads();
+    return tot;
+  };
+  auto product = [&](const float* seg, const float* u) {
+    if (threadIdx.x < PB) us[threadIdx.x] = u[Jb + threadIdx.x];
+    __syncthreads();
+    coop_product<R>(acc, seg + own * G::kPitch, us);
+    float* out = a.partial + static_cast<int64_t>(b) * n;
+#pragma unroll
+    for (int q = 0; q < R; ++q) out[ib + q] = acc[q];
+    __syncthreads();
+  };
+  for (int it = 0; it < a.iters; ++it) {
+    product(s_c, a.v);  // C^T v
+    grid.sync();
+    {
+      const float sct = sum_partials();
+      if (part == 0)  // parallel.hpp:186-187
+        a.beta[i_out] = __fadd_rn(__fmul_rn(a.rho, sct), __fmul_rn(a.sigma, __fsub_rn(a.z[i_out], a.nu[i_out])));
+    }
+    grid.sync();
+    product(s_b, a.beta);  // B beta
+    grid.sync();
+    {
+      const float xs = sum_partials();
+      if (part == 0) a.x[i_out] = xs;
+    }
+    grid.sync();
+    product(s_r, a.x);  // C x
+    grid.sync();
+    {
+      const float cx = sum_partials();
+      if (part == 0) {  // parallel.hpp:215-221
+        const float xi = a.x[i_out], nui = a.nu[i_out];
+        const float vn = __fmul_rn(a.d[i_out], __fadd_rn(__fmul_rn(a.rho, __fsub_rn(cx, a.mu[i_out])), a.pty[i_out]));
+        const float sv = __fadd_rn(xi, nui);
+        const float zn = sv > a.thr ? sv - a.thr : (sv < -a.thr ? sv + a.thr : 0.f);
+        const float mun = __fadd_rn(a.mu[i_out], __fmul_rn(a.tau1, __fsub_rn(vn, cx)));
+        a.z[i_out] = zn;
+        a.mu[i_out] = mun;
+        a.nu[i_out] = __fadd_rn(nui, __fmul_rn(a.tau2, __fsub_rn(xi, zn)));
+        a.v[i_out] = __fadd_rn(vn, mun);
+      }
+    }
+    grid.sync();
+  }
+}
+
+// Persistent cooperative ISTA for small n (config 1): CTA b owns position block
+// b.  Per iteration (cpista_phases, parallel.hpp:236-279) it computes the
+// residual of block b's rows (x in registers, lane partials reduced in fixed
+// order), keeps those r values in shared memory, multiplies them into a split-K
+// partial of the gradient for all n outputs, and -- after one grid barrier --
+// sums the partials of outputs [32 b, 32 b + 32) and applies the threshold.
+// Only x crosses CTAs (a second barrier), so two barriers per iteration.
+struct CoopIstaArgs {
+  const float *hc, *hcr, *y;
+  const int* omega;
+  float *x, *r, *delta, *partial;
+  int64_t n, m;
+  float tau, thr;
+  int iters;
+};
+
+template <int R>
+__global__ void __launch_bounds__(kThreads, 1) k_coop_ista(CoopIstaArgs a) {
+  using G = Geo<R>;
+  constexpr int PB = 32;
+  constexpr int SEG = G::pad(G::kTileR + PB) + 4;
+  extern __shared__ float4 smem_f4[];
+  float* s_g = reinterpret_cast<float*>(smem_f4);  // gradient segment: h = c~, base -Jb - 32
+  float* s_r = s_g + SEG;                             // residual segment: h = c~_rev, base Jb - kTileR
+  float* rd = s_r + SEG;                              // [32] r at the block's positions (0 elsewhere)
+  float* red = rd + PB;                               // [kWarps][32] per-warp row sums; update parts
+  float* lanep = red + kWarps * PB;                   // [kWarps][32][33]
+  int* meta = reinterpret_cast<int*>(lanep + kWarps * 32 * 33);  // [0] mask, [1] first row, [2] rows
+  cg::grid_group grid = cg::this_grid();
+  const int64_t n = a.n;
+  const int b = blockIdx.x, own = threadIdx.x, warp = own >> 5, lane = own & 31;
+  const int64_t Jb = static_cast<int64_t>(b) * PB;
+  for (int e = threadIdx.x; e < G::kTileR + PB; e += kThreads) {
+    int64_t kg = (e - Jb - PB) % n;
+    if (kg < 0) kg += n;
+    int64_t kr = (Jb - G::kTileR + e) % n;
+    if (kr < 0) kr += n;
+    s_g[G::pad(e)] = a.hc[kg];
+    s_r[G::pad(e)] = a.hcr[kr];
+  }
+  if (threadIdx.x == 0) {  // this block's rows: omega is sorted, so they are one contiguous run
+    int64_t lo = 0, hi = a.m;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      if (a.omega[mid] < Jb) lo = mid + 1;
+      else hi = mid;
+    }
+    uint32_t mask = 0u;
+    int64_t t = lo;
+    while (t < a.m && a.omega[t] < Jb + PB) mask |= 1u << (a.omega[t++] - Jb);
+    meta[0] = static_cast<int>(mask);
+    meta[1] = static_cast<int>(lo);
+    meta[2] = static_cast<int>(t - lo);
+  }
+  __syncthreads();
+  const uint32_t mask = __reduce_or_sync(0xffffffffu, static_cast<uint32_t>(meta[0]));
+  const int t0 = meta[1], nrow = meta[2];
+  const int o = own & 31, part = own >> 5;
+  const int64_t i_out = Jb + o;
+  float* lp = lanep + warp * 32 * 33;
+  float* const lp_lane = lp + lane * 33;
+  for (int it = 0; it < a.iters; ++it) {
+    // residual rows of block b: r_t = y_t - sum_j c~[(j - omega_t) mod n] x_j
+    float xr[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) xr[q] = a.x[own * R + q];
+    if (mask) {
+      float w[R + PB];
+      window_at<R, PB>(w, s_r + (kThreads - 1 - own) * G::kPitch, 0);
+      float* lpp = lp_lane;
+      res_group<R, PB, 0>(w, xr, mask, lpp);
+      res_group<R, PB, 1>(w, xr, mask, lpp);
+      res_group<R, PB, 2>(w, xr, mask, lpp);
+      res_group<R, PB, 3>(w, xr, mask, lpp);
+      res_group<R, PB, 4>(w, xr, mask, lpp);
+      res_group<R, PB, 5>(w, xr, mask, lpp);
+      res_group<R, PB, 6>(w, xr, mask, lpp);
+      res_group<R, PB, 7>(w, xr, mask, lpp);
+      __syncwarp();
+      reduce_lane_partials(lp, red + warp * PB, 0, nrow, lane);
+    }
+    __syncthreads();
+    if (threadIdx.x < PB) rd[threadIdx.x] = 0.f;
+    __syncthreads();
+    if (threadIdx.x < nrow) {  // fixed-order warp sum; the block's r values stay in shared memory
+      const float sres = (red[threadIdx.x] + red[PB + threadIdx.x]) + (red[2 * PB + threadIdx.x] + red[3 * PB + threadIdx.x]);
+      const float rv = a.y[t0 + threadIdx.x] - sres;  // parallel.hpp:252
+      const int pos = a.omega[t0 + threadIdx.x];
+      rd[pos - Jb] = rv;
+      if (it == a.iters - 1) a.r[t0 + threadIdx.x] = rv;
+    }
+    __syncthreads();
+    // gradient partial of block b for all outputs: acc[q] += c~[(i - omega_t) mod n] r_t
+    float acc[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) acc[q] = 0.f;
+    if (mask) {
+      float w[R + PB];
+      window_at<R, PB>(w, s_g + own * G::kPitch, 0);
+      ool_block32<R>(acc, w, mask, rd);
+    }
+    float* outp = a.partial + static_cast<int64_t>(b) * n + own * R;
+#pragma unroll
+    for (int q = 0; q < R; ++q) outp[q] = acc[q];
+    grid.sync();
+    // update of outputs [32 b, 32 b + 32): delta = sum of the block partials (fixed order), x = eta(x + tau delta)
+    {
+      const int nb = static_cast<int>(gridDim.x);
+      const int k0 = part * ((nb + 3) / 4), k1 = min(nb, k0 + (nb + 3) / 4);
+      float sacc = 0.f;
+      for (int k = k0; k < k1; ++k) sacc += a.partial[static_cast<int64_t>(k) * n + i_out];
+      red[part * 32 + o] = sacc;
+      __syncthreads();
+      if (part == 0) {
+        const float d = (red[o] + red[32 + o]) + (red[64 + o] + red[96 + o]);
+        const float xn = __fadd_rn(a.x[i_out], __fmul_rn(a.tau, d));  // parallel.hpp:269-271
+        a.x[i_out] = xn > a.thr ? xn - a.thr : (xn < -a.thr ? xn + a.thr : 0.f);
+        if (it == a.iters - 1) a.delta[i_out] = d;
+      }
+    }
+    grid.sync();
+  }
+}
+
+template <int R>
+constexpr size_t coop_ista_smem() {
+  return (2 * (Geo<R>::pad(Geo<R>::kTileR + 32) + 4) + 32 + kWarps * 32 + kWarps * 32 * 33 + 4) * 4;
+}
+
+template <int R>
+constexpr size_t coop_smem() { return (3 * (Geo<R>::pad(Geo<R>::kTileR + 32) + 4) + 32 + 128) * 4; }
+
+// ===========================================================================
 // Elementwise epilogues (fixed grid kEpiBlocks -> deterministic metrics).
 // ===========================================================================
 __device__ __forceinline__ float soft(float v, float g) {  // solvers.hpp:39-44
@@ -1321,6 +1579,63 @@ void launch_dense_gemv(const float* M, const float* x, float* out, int64_t n, cu
 }
 void launch_metrics_final(const double* blk, double* out4, cudaStream_t st) {
   k_metrics_final<<<1, 256, 0, st>>>(blk, out4);
+}
+
+bool coop_cadmm_supported(int64_t n) {
+  const char* v = getenv("CLB_NO_SMALL");
+  return !(v && v[0] == '1') && (n == 2048 || n == 4096 || n == 8192);
+}
+cudaError_t launch_coop_cadmm(int64_t n, const float* hc, const float* hbr, const float* hcr, const float* d,
+                              const float* pty, float* x, float* z, float* nu, float* mu, float* v, float* beta,
+                              float* partial, float rho, float sigma, float tau1, float tau2, float thr, int iters,
+                              cudaStream_t st) {
+  CoopArgs a{hc, hbr, hcr, d, pty, x, z, nu, mu, v, beta, partial, n, rho, sigma, tau1, tau2, thr, iters};
+  void* args[] = {&a};
+  const dim3 grid(static_cast<unsigned>(n / 32)), block(kThreads);
+  switch (n) {
+#define CLB_COOP(N, R)                                                                                      \
+  case N: {                                                                                                 \
+    static bool attr = false;                                                                               \
+    if (!attr) {                                                                                            \
+      attr = true;                                                                                          \
+      cudaFuncSetAttribute(k_coop_cadmm<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coop_smem<R>()); \
+    }                                                                                                       \
+    return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_coop_cadmm<R>), grid, block, args,   \
+                                       coop_smem<R>(), st);                                                 \
+  }
+    CLB_COOP(2048, 16)
+    CLB_COOP(4096, 32)
+    CLB_COOP(8192, 64)
+#undef CLB_COOP
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_coop_ista(int64_t n, int64_t m, const float* hc, const float* hcr, const int* omega,
+                             const float* y, float* x, float* r, float* delta, float* partial, float tau, float thr,
+                             int iters, cudaStream_t st) {
+  CoopIstaArgs a{hc, hcr, y, omega, x, r, delta, partial, n, m, tau, thr, iters};
+  void* args[] = {&a};
+  const dim3 grid(static_cast<unsigned>(n / 32)), block(kThreads);
+  switch (n) {
+#define CLB_COOPI(N, R)                                                                                     \
+  case N: {                                                                                                 \
+    static bool attr = false;                                                                               \
+    if (!attr) {                                                                                            \
+      attr = true;                                                                                          \
+      cudaFuncSetAttribute(k_coop_ista<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coop_ista_smem<R>()); \
+    }                                                                                                       \
+    return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_coop_ista<R>), grid, block, args,    \
+                                       coop_ista_smem<R>(), st);                                            \
+  }
+    CLB_COOPI(2048, 16)
+    CLB_COOPI(4096, 32)
+    CLB_COOPI(8192, 64)
+#undef CLB_COOPI
+    default:
+      return cudaErrorInvalidValue;
+  }
 }
 
 double ffma_peak_tflops(int device) {

@@ -105,6 +105,19 @@ void conv_kernels_init();
 void launch_materialize_circulant(const float* c, float* M, int64_t n, cudaStream_t st);
 void launch_dense_gemv(const float* M, const float* x, float* out, int64_t n, cudaStream_t st);
 
+// Persistent cooperative cADMM for n in {2048, 4096, 8192} (CLB_NO_SMALL unset): all unchecked iterations
+// in one launch; partial holds n/32 x n floats.
+bool coop_cadmm_supported(int64_t n);
+cudaError_t launch_coop_cadmm(int64_t n, const float* hc, const float* hbr, const float* hcr, const float* d,
+                              const float* pty, float* x, float* z, float* nu, float* mu, float* v, float* beta,
+                              float* partial, float rho, float sigma, float tau1, float tau2, float thr, int iters,
+                              cudaStream_t st);
+
+// Persistent cooperative ISTA (same n); partial holds n/32 x n floats.
+cudaError_t launch_coop_ista(int64_t n, int64_t m, const float* hc, const float* hcr, const int* omega,
+                             const float* y, float* x, float* r, float* delta, float* partial, float tau, float thr,
+                             int iters, cudaStream_t st);
+
 // FFMA throughput microkernel (roofline denominator), returns TFLOP/s.
 double ffma_peak_tflops(int device);
 

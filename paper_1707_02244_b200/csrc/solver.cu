@@ -920,7 +920,32 @@ struct Solver {
            (kind == CL_KIND_ISTA ? small_fft_supported(n) : small_fft_cadmm_supported(n));
   }
 
+  bool use_coop_ista() const {
+    const char* v = std::getenv("CLB_SMALL_CLUSTER");  // 1: the single-cluster kernel (small.cu) instead
+    return kind == CL_KIND_ISTA && !fft && world == 1 && !profile && coop_cadmm_supported(n) && !(v && v[0] == '1');
+  }
+  bool use_coop_cadmm() const {
+    return kind == CL_KIND_CADMM && !fft && world == 1 && !profile && coop_cadmm_supported(n);
+  }
+
   void step(int64_t iters) {
+    if (iters > 0 && use_coop_ista()) {
+      CU(cudaEventRecord(step_ev[0], st));
+      CU(launch_coop_ista(n, m, hc.p, hcr.p, omega32.p, y.p, x.p, r.p, delta.p, partial.p, static_cast<float>(tau),
+                          static_cast<float>(thr), static_cast<int>(iters), st));
+      t += iters;
+      CU(cudaEventRecord(step_ev[1], st));
+      return;
+    }
+    if (iters > 0 && use_coop_cadmm()) {
+      CU(cudaEventRecord(step_ev[0], st));
+      CU(launch_coop_cadmm(n, hc.p, hbr.p, hcr.p, d.p, pty.p, x.p, z.p, nu.p, mu.p, v.p, beta.p, partial.p,
+                           static_cast<float>(cfg.rho), static_cast<float>(cfg.sigma), static_cast<float>(cfg.tau1),
+                           static_cast<float>(cfg.tau2), static_cast<float>(thr), static_cast<int>(iters), st));
+      t += iters;
+      CU(cudaEventRecord(step_ev[1], st));
+      return;
+    }
     if (iters > 0 && use_small_fft()) {
       CU(cudaEventRecord(step_ev[0], st));
       if (kind == CL_KIND_ISTA)

@@ -503,8 +503,11 @@ def test_fft4_engine_matches_stockham_engine(kind, lg):
 # ------------------------------------------------- persistent small-n ISTA (one cluster)
 @pytest.mark.parametrize("n,m,k,seed,iters", [(4096, 1024, 64, 1, 300), (2048, 700, 40, 4, 120),
                                               (8192, 2048, 100, 5, 80), (4096, 4096, 64, 2, 50)])
-def test_small_cluster_ista_matches_oracle(n, m, k, seed, iters):
-    """The single-launch cluster kernel (all iterations in one launch) against the oracle's phase engine."""
+@pytest.mark.parametrize("cluster", ["0", "1"])
+def test_small_cluster_ista_matches_oracle(n, m, k, seed, iters, cluster, monkeypatch):
+    """The single-launch small-n ISTA kernels -- the cooperative grid kernel (default) and the 8-CTA cluster
+    kernel (CLB_SMALL_CLUSTER=1) -- against the oracle's phase engine."""
+    monkeypatch.setenv("CLB_SMALL_CLUSTER", cluster)
     p = orc.make_problem(n, m, k, seed)
     g = cl.ista_setup(op_of(p), p.y)
     g.step(iters)
@@ -675,3 +678,18 @@ def test_matvec_scheme_bench_accounts_fetches():
     circ, ref = lines[1].split(","), lines[2].split(",")
     assert circ[0] == "matvec-circulant" and ref[0] == "matvec-reference" and circ[5] == "2"
     assert circ[9] == "1024" and ref[9] == "33280"
+
+
+@pytest.mark.parametrize("n,m,k,seed,iters", [(4096, 1024, 64, 1, 200), (2048, 1024, 40, 2, 100), (8192, 2048, 80, 3, 40)])
+def test_coop_cadmm_matches_oracle(n, m, k, seed, iters):
+    """Persistent cooperative cADMM (all iterations in one launch, grid barriers between phases) against the
+    oracle's phase engine."""
+    p = orc.make_problem(n, m, k, seed)
+    g = cl.cadmm_setup(op_of(p), p.y)
+    g.step(iters)
+    o = orc.Cadmm(p.row, p.omega, p.y)
+    o.step(iters, orc.ENGINE_PHASES)
+    assert g.t == iters
+    assert_parity(g.get("z"), o.get("z"), what="z")
+    for f in ("x", "v", "mu", "nu", "beta"):
+        assert rel_l2(g.get(f), o.get(f)) <= REL_TOL, f
