@@ -26,6 +26,8 @@ KEYS = {
     "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum": "smem_ld_bank_conflicts",
     "sm__cycles_elapsed.avg.per_second": "sm_clock_hz",
+    "sm__pipe_fma_cycles_active.sum.pct_of_peak_sustained_active": "fma_pipe_active_pct",
+    "sm__inst_executed_pipe_fma.sum.pct_of_peak_sustained_active": "fma_pipe_inst_pct",
 }
 
 
@@ -66,6 +68,8 @@ def load(rep):
                     pass
         if "dram_read_bytes" in e:
             e["dram_bytes_per_launch"] = e["dram_read_bytes"] + e.get("dram_write_bytes", 0.0)
+            if e.get("duration_ns"):
+                e["dram_gbs"] = e["dram_bytes_per_launch"] / e["duration_ns"]  # bytes/ns = GB/s
         stalls = {}
         for k in hdr:
             if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio"):
