@@ -25,6 +25,7 @@
 #include <cooperative_groups.h>
 
 #include "kernels.cuh"
+#include "tc_dense.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -1516,6 +1517,7 @@ void conv_kernels_init() {
     cudaMemcpyToSymbol(g_force_dense, &one, sizeof(int));
   }
   select_variants();
+  tc_dense_init();
   for (const auto& d : kDense)
     cudaFuncSetAttribute(reinterpret_cast<const void*>(d.fn), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d.smem);
   for (const auto& g : kGrad)
@@ -1524,7 +1526,24 @@ void conv_kernels_init() {
     cudaFuncSetAttribute(reinterpret_cast<const void*>(r.fn), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)r.smem);
 }
 
+ConvPlan make_dense_plan(int64_t n) {
+  static const bool no_tc = [] {
+    const char* v = getenv("CLB_NO_TC");
+    return v && atoi(v) != 0;
+  }();
+  if (!no_tc && tc_dense_supported(n)) {
+    ConvPlan p = make_tc_plan(n);
+    p.tc = true;
+    return p;
+  }
+  return make_plan(n, dense_R(n));
+}
+
 void launch_conv_dense(const ConvPlan& p, const float* h, const float* u, float* partial, cudaStream_t st) {
+  if (p.tc) {
+    launch_tc_dense(p, h, u, partial, st);
+    return;
+  }
   const int64_t units = (p.tile_hi - p.tile_lo) * p.splits;
   if (units <= 0) return;
   select_variants();

@@ -56,9 +56,13 @@ struct ConvPlan {
   int splits = 1;       // S
   int64_t tile_lo = 0, tile_hi = 0;    // shard: tiles run by this rank
   int split_lo = 0, split_hi = 0;      // shard: splits run by this rank (residual)
+  bool tc = false;                     // dense product on the tensor cores (tc_dense.cu)
 };
 
 ConvPlan make_plan(int64_t n, int R);
+// Plan of the cADMM dense products: the tcgen05 kernel (tc_dense.cu) for power-of-two
+// n >= 2^15 unless CLB_NO_TC=1, else the FFMA kernel.  Pure host logic.
+ConvPlan make_dense_plan(int64_t n);
 // [blo, bhi) in 32-position blocks covered by split `split` of a plan.
 void split_block_range(const ConvPlan& p, int split, int64_t* blo, int64_t* bhi);
 

@@ -531,7 +531,7 @@ struct Solver {
     if (dev) init_device();
     scale = normalization_from(dev ? device_spectrum(c) : spectral_norm(c, n), yh);
     if (!dev) init_device();
-    plan = make_plan(n, dense_R(n));
+    plan = make_dense_plan(n);
     hc.alloc(static_cast<size_t>(n), st);
     hcr.alloc(static_cast<size_t>(n), st);
     hbr.alloc(static_cast<size_t>(n), st);
@@ -1112,7 +1112,7 @@ struct ScratchProduct {
     reserve_pool(device);
     cudaStream_t st;
     CU(cudaStreamCreate(&st));
-    ConvPlan p = make_plan(n, dense_R(n));
+    ConvPlan p = make_dense_plan(n);
     std::vector<float> cf = to_f32(c, n);
     if (!transpose) cf = reversed(cf);  // C x = conv(c_rev, x)
     const std::vector<float> xf = to_f32(xin, n);
@@ -1330,7 +1330,7 @@ cl_status cl_matvec_scheme_bench(int device, int64_t n, int scheme, int repeats,
   out.alloc(nn, st);
   ConvPlan plan;
   if (scheme == 0) {
-    plan = make_plan(n, dense_R(n));
+    plan = make_dense_plan(n);
     const std::vector<float> crf = reversed(to_f32(row.data(), n));  // C x = conv(c_rev, x)
     h.alloc(nn, st);
     h.upload(crf.data(), nn, st);
@@ -1721,7 +1721,7 @@ cl_status cl_shard_ranges(int kind, int64_t n, int64_t m, const int64_t* omega, 
   if (kind != CL_KIND_ISTA && kind != CL_KIND_CADMM) raise(CL_EPARAM, "cl_shard_ranges: unknown solver kind");
   if (n < 1 || m < 0 || m > n) raise(CL_EDIM, "cl_shard_ranges: need n >= 1 and 0 <= m <= n");
   check_mask(omega, m, n);
-  ConvPlan plan = make_plan(n, kind == CL_KIND_ISTA ? grad_R(n) : dense_R(n));
+  ConvPlan plan = (kind == CL_KIND_ISTA ? make_plan(n, grad_R(n)) : make_dense_plan(n));
   ConvPlan rplan = make_plan(n, res_R(n));
   shard_ranges(kind, n, omega, m, rank, world, &plan, &rplan, out_lo, out_hi, row_lo, row_hi);
   CL_GUARD_END
