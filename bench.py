@@ -180,10 +180,35 @@ def run_reference(args, w, rank):
     print(json.dumps(line), flush=True)
 
 
+TF32_DENSE_TFLOPS = 1100.0  # B200 dense TF32 tensor peak (/opt/skills/guides/B200_PROFILING.md; not in MEASURED_PEAKS.json)
+
+
+def dense_uses_tc(n):
+    """cADMM dense products run on the tcgen05 kernel (csrc/tc_dense.cu) for power-of-two n >= 2^15."""
+    return n >= (1 << 15) and (n & (n - 1)) == 0 and os.environ.get("CLB_NO_TC", "0") in ("", "0")
+
+
+def dense_kernel_info(n, ms):
+    flops = 2.0 * n * n
+    if dense_uses_tc(n):
+        return {"kernel": "k_tc_dense", "ms": ms, "achieved_tflops": flops / (ms * 1e-3) / 1e12,
+                "bound": "tensor", "peak_tflops": TF32_DENSE_TFLOPS,
+                "frac": flops / (ms * 1e-3) / 1e12 / TF32_DENSE_TFLOPS,
+                "tensor_pipe_tflops": 3 * flops / (ms * 1e-3) / 1e12,
+                "note": "3xTF32 (hi.hi + hi.lo + lo.hi) for fp32 accuracy: 3 tensor flops per algorithmic flop; "
+                        "achieved/frac count algorithmic flops (2 n^2)"}
+    return {"kernel": "k_conv_dense", "ms": ms, "achieved_tflops": flops / (ms * 1e-3) / 1e12, "bound": "fp32_ffma"}
+
+
+def ista_uses_tc(n):
+    """ISTA's direct engine embeds both sparse products in dense tcgen05 products for n >= 2^18."""
+    return n >= (1 << 18) and dense_uses_tc(n)
+
+
 def admm_line(cl, torch, prob, local_rank, flush, steps=5, warmup=3):
     """cADMM (the paper's CPADMM, the metric's "ADMM") on the same n=2^20 problem:
     device-timed iterations/s of the direct engine (3 dense circulant products
-    per iteration, 6 n^2 flop) and the dense kernel's FFMA fraction."""
+    per iteration, 6 n^2 flop) and the dense kernel's roofline fraction."""
     import ctypes as C
     from paper_1707_02244_b200._native import lib as L
     st = cl.cadmm_setup(prob.op, prob.measurements, cl.SolverConfig(), device=local_rank)
@@ -212,9 +237,9 @@ def admm_line(cl, torch, prob, local_rank, flush, steps=5, warmup=3):
     return {"value": 1e3 / ms, "unit": "iterations/s", "ms_per_step": ms, "steps": steps, "warmup": warmup,
             "workload": f"cADMM n={n}, m={prob.op.m()}, k={prob.k()}, rho=sigma=0.1, tau1=tau2=1, alpha=1e-4 "
                         "(make_problem(2^20, 2^18, 2^12, 1), the config-3 problem)",
-            "engine": "direct shift-indexed sm_100a kernels",
-            "dense_kernel": {"kernel": "k_conv_dense", "ms": dense_ms,
-                             "achieved_tflops": 2.0 * n * n / (dense_ms * 1e-3) / 1e12},
+            "engine": "direct circulant products on tcgen05 tensor cores (3xTF32)" if dense_uses_tc(n)
+                      else "direct shift-indexed sm_100a kernels",
+            "dense_kernel": dense_kernel_info(n, dense_ms),
             "step_tflops": 6.0 * n * n / (ms * 1e-3) / 1e12, "phase_ms": ph}
 
 
@@ -340,12 +365,15 @@ def main():
     if w["kind"] == "ista":
         k_ms = statistics.mean(p[0] for p in phase_ms)
         k_flops = 2.0 * w["m"] * w["n"] / world
-        k_name = "k_res_s" if w["n"] >= (1 << 17) else "k_conv_residual"  # large-n / small-n residual kernel
+        if ista_uses_tc(w["n"]):
+            k_name = "k_tc_dense"  # residual = dense tensor-core product C x, rows Omega gathered
+        else:
+            k_name = "k_res_s" if w["n"] >= (1 << 17) else "k_conv_residual"  # large-n / small-n residual kernel
     else:
         k_ms = statistics.mean(p[0] for p in phase_ms)
         k_flops = 2.0 * w["n"] * w["n"] / world
-        k_name = "k_conv_dense"
-    peak = cl.ffma_peak_tflops(local_rank)
+        k_name = "k_tc_dense" if dense_uses_tc(w["n"]) else "k_conv_dense"
+    peak = TF32_DENSE_TFLOPS if k_name == "k_tc_dense" else cl.ffma_peak_tflops(local_rank)
     achieved = k_flops / (k_ms * 1e-3) / 1e12
     traffic = None
     try:
@@ -479,16 +507,28 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (make_problem, seeded)",
             "config": {"workload": w["desc"], "n": w["n"], "m": w["m"], "k": w["k"], "seed": w["seed"],
-                       "engine": "direct shift-indexed sm_100a kernels", "l2": "flushed (256 MiB) between steps",
+                       "engine": ("direct circulant products on tcgen05 tensor cores (3xTF32; ISTA's sparse products "
+                                  "embedded in dense ones)" if k_name == "k_tc_dense" else
+                                  "direct shift-indexed sm_100a kernels"),
+                       "l2": "flushed (256 MiB) between steps",
                        "parallelism": f"row/output shards x{world}" if sharded else "single GPU"},
-            "roofline": {"bound": "fp32_ffma", "kernel": k_name, "achieved": achieved, "peak": peak,
+            "roofline": {"bound": "tensor" if k_name == "k_tc_dense" else "fp32_ffma", "kernel": k_name,
+                         "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                         "peak_source": "live FFMA microbenchmark (cl_ffma_peak); MEASURED_PEAKS.json has no FP32 entry",
+                         "peak_source": ("B200 dense TF32 1.1 PF (B200_PROFILING.md); 3xTF32 emulation, achieved counts "
+                                         "algorithmic flops" if k_name == "k_tc_dense" else
+                                         "live FFMA microbenchmark (cl_ffma_peak); MEASURED_PEAKS.json has no FP32 entry"),
+                         **({"dense_product_tflops": 2.0 * w["n"] * w["n"] / world / (k_ms * 1e-3) / 1e12,
+                             "tensor_pipe_tflops": 6.0 * w["n"] * w["n"] / world / (k_ms * 1e-3) / 1e12,
+                             "tensor_pipe_frac": 6.0 * w["n"] * w["n"] / world / (k_ms * 1e-3) / 1e12 / peak,
+                             "work_note": "the kernel computes the dense product C x (2 n^2 flop; ISTA needs the m rows "
+                                          "of Omega, 2 m n) in 3xTF32 (3 tensor flops per flop)"}
+                            if k_name == "k_tc_dense" else {}),
                          "step_tflops": algorithmic_flops(w) / (ms_per_step * 1e-3) / 1e12,
                          "step_frac": algorithmic_flops(w) / (ms_per_step * 1e-3) / 1e12 / peak,
                          "phase_ms": [statistics.mean(p[i] for p in phase_ms) for i in range(len(phase_ms[0]))]},
             "clocks": clocks.summary(),
-            "gpu_launches": (4 if w["kind"] == "ista" else 6) * args.steps,
+            "gpu_launches": (((5 if ista_uses_tc(w["n"]) else 4) if w["kind"] == "ista" else 6) * args.steps),
             "e2e": e2e,
             "fft_engine": fft_line,
             "admm": admm,

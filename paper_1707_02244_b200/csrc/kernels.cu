@@ -1225,6 +1225,15 @@ __global__ void __launch_bounds__(kThreads) k_residual_reduce(EpiArgs a, int64_t
   }
 }
 
+__global__ void __launch_bounds__(kThreads) k_residual_gather(EpiArgs a, const int* __restrict__ omega) {
+  // r[t] = y[t] - (C x)[omega[t]], C x from the dense product's split partials (a.n = n)
+  for (int64_t t = a.lo + blockIdx.x * (int64_t)kThreads + threadIdx.x; t < a.hi;
+       t += (int64_t)gridDim.x * kThreads) {
+    const float s = sum_partials(a.partial, a.splits, a.n, omega[t]);
+    a.r[t] = a.y[t] - s;
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) k_ista_update(EpiArgs a) {
   // delta[i] = sum_s partial; x[i] = eta_g(x[i] + tau * delta[i])   (parallel.hpp:269-271)
   double m0 = 0, m1 = 0, m2 = 0;
@@ -1539,6 +1548,8 @@ ConvPlan make_dense_plan(int64_t n) {
   return make_plan(n, dense_R(n));
 }
 
+bool ista_uses_tc(int64_t n) { return n >= (int64_t(1) << 18) && make_dense_plan(n).tc; }
+
 void launch_conv_dense(const ConvPlan& p, const float* h, const float* u, float* partial, cudaStream_t st) {
   if (p.tc) {
     launch_tc_dense(p, h, u, partial, st);
@@ -1582,6 +1593,9 @@ void launch_ista_residual_reduce(const EpiArgs& a, int64_t tiles, cudaStream_t s
 }
 // Metric-producing epilogues always use the full fixed grid so the
 // per-block partial layout (and hence the metric) does not depend on n.
+void launch_ista_residual_gather(const EpiArgs& a, const int* omega, cudaStream_t st) {
+  k_residual_gather<<<epi_grid(a.hi - a.lo), kThreads, 0, st>>>(a, omega);
+}
 void launch_ista_update(const EpiArgs& a, cudaStream_t st) {
   k_ista_update<<<a.want_metrics ? kEpiBlocks : epi_grid(a.hi - a.lo), kThreads, 0, st>>>(a);
 }

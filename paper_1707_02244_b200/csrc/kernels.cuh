@@ -63,6 +63,9 @@ ConvPlan make_plan(int64_t n, int R);
 // Plan of the cADMM dense products: the tcgen05 kernel (tc_dense.cu) for power-of-two
 // n >= 2^15 unless CLB_NO_TC=1, else the FFMA kernel.  Pure host logic.
 ConvPlan make_dense_plan(int64_t n);
+// ISTA's direct engine embeds both sparse products in dense tensor-core products for
+// n >= 2^18 (where that beats the FFMA sparse kernels).  Pure host logic.
+bool ista_uses_tc(int64_t n);
 // [blo, bhi) in 32-position blocks covered by split `split` of a plan.
 void split_block_range(const ConvPlan& p, int split, int64_t* blo, int64_t* bhi);
 
@@ -97,6 +100,8 @@ void launch_conv_residual(const ConvPlan& p, int64_t m, const float* h, const fl
                           const int* rowstart, float* partial, cudaStream_t st);
 
 void launch_ista_residual_reduce(const EpiArgs& a, int64_t tiles, cudaStream_t st);
+// r[t] = y[t] - sum_s partial[s][omega[t]] for t in [a.lo, a.hi) (dense-embedded residual)
+void launch_ista_residual_gather(const EpiArgs& a, const int* omega, cudaStream_t st);
 void launch_ista_update(const EpiArgs& a, cudaStream_t st);
 void launch_admm_beta(const EpiArgs& a, cudaStream_t st);
 void launch_admm_x(const EpiArgs& a, cudaStream_t st);

@@ -120,7 +120,10 @@ void shard_ranges(int kind, int64_t n, const int64_t* omega, int64_t m, int rk, 
   *out_lo = std::min<int64_t>(n, plan->tile_lo * plan->tile);
   *out_hi = std::min<int64_t>(n, plan->tile_hi * plan->tile);
   *row_lo = *row_hi = 0;
-  if (kind == CL_KIND_ISTA) {
+  if (kind == CL_KIND_ISTA && plan->tc) {  // dense-embedded products: rows = Omega within the owned outputs
+    *row_lo = std::lower_bound(omega, omega + m, *out_lo) - omega;
+    *row_hi = std::lower_bound(omega, omega + m, *out_hi) - omega;
+  } else if (kind == CL_KIND_ISTA) {
     rplan->split_lo = static_cast<int>(static_cast<int64_t>(rplan->splits) * rk / ws);
     rplan->split_hi = static_cast<int>(static_cast<int64_t>(rplan->splits) * (rk + 1) / ws);
     int64_t b_lo, b_hi, dummy;
@@ -167,6 +170,7 @@ struct Solver {
   } st_owner{&st};
   ConvPlan plan;     // outputs: gradient (ISTA) or dense (cADMM) products
   ConvPlan rplan;    // ISTA residual (input tiles x position splits)
+  bool ista_tc = false;  // ISTA products embedded in dense tensor-core products (plan == rplan, tc)
   int64_t row_lo = 0, row_hi = 0;  // ISTA rows owned (residual)
   int64_t out_lo = 0, out_hi = 0;  // outputs owned
 
@@ -356,8 +360,9 @@ struct Solver {
     tau = tau0;
     thr = cfg.pairing == CL_PAIRING_LITERAL ? cfg.alpha : tau0 * cfg.alpha;
     if (!dev) init_device();
-    plan = make_plan(n, grad_R(n));
-    rplan = make_plan(n, res_R(n));
+    ista_tc = !fft && ista_uses_tc(n);
+    plan = ista_tc ? make_dense_plan(n) : make_plan(n, grad_R(n));
+    rplan = ista_tc ? plan : make_plan(n, res_R(n));
     hc.alloc(static_cast<size_t>(n), st);
     hcr.alloc(static_cast<size_t>(n), st);
     if (dev) {
@@ -379,6 +384,10 @@ struct Solver {
     blk.alloc(kEpiBlocks * 4, st);
     met.alloc(4, st);
     set_shard(0, 1);
+    if (ista_tc) {
+      ud.alloc(static_cast<size_t>(n), st);  // r scattered to its positions (zero elsewhere)
+      ud.zero(st);
+    }
     if (want_fft4(dev)) {
       setup_fft4_common();
       rowid.alloc(static_cast<size_t>(n), st);
@@ -619,6 +628,21 @@ struct Solver {
   // ---- phases -------------------------------------------------------------
   void ista_residual() {
     mark(0);
+    if (ista_tc) {  // C x on the tensor cores, rows Omega gathered in the epilogue
+      launch_conv_dense(plan, hcr.p, x.p, partial.p, st);
+      mark(1);
+      EpiArgs a;
+      a.partial = partial.p;
+      a.splits = plan.splits;
+      a.n = n;
+      a.lo = row_lo;
+      a.hi = row_hi;
+      a.y = y.p;
+      a.r = r.p;
+      launch_ista_residual_gather(a, omega32.p, st);
+      mark(2);
+      return;
+    }
     launch_conv_residual(rplan, m, hcr.p, x.p, omega32.p, rowstart.p, partial.p, st);
     mark(1);
     EpiArgs a;
@@ -632,7 +656,12 @@ struct Solver {
     mark(2);
   }
   void ista_gradient(int want) {
-    launch_conv_rows(plan, hc.p, omega32.p, r.p, rowstart.p, partial.p, st);
+    if (ista_tc) {  // C^T P^T r: scatter r (all rows, after any exchange), dense product
+      launch_scatter_real(r.p, omega32.p, ud.p, m, st);
+      launch_conv_dense(plan, hc.p, ud.p, partial.p, st);
+    } else {
+      launch_conv_rows(plan, hc.p, omega32.p, r.p, rowstart.p, partial.p, st);
+    }
     mark(3);
     EpiArgs a = base_args(want);
     a.x = x.p;
@@ -1721,7 +1750,7 @@ cl_status cl_shard_ranges(int kind, int64_t n, int64_t m, const int64_t* omega, 
   if (kind != CL_KIND_ISTA && kind != CL_KIND_CADMM) raise(CL_EPARAM, "cl_shard_ranges: unknown solver kind");
   if (n < 1 || m < 0 || m > n) raise(CL_EDIM, "cl_shard_ranges: need n >= 1 and 0 <= m <= n");
   check_mask(omega, m, n);
-  ConvPlan plan = (kind == CL_KIND_ISTA ? make_plan(n, grad_R(n)) : make_dense_plan(n));
+  ConvPlan plan = (kind == CL_KIND_ISTA ? (ista_uses_tc(n) ? make_dense_plan(n) : make_plan(n, grad_R(n))) : make_dense_plan(n));
   ConvPlan rplan = make_plan(n, res_R(n));
   shard_ranges(kind, n, omega, m, rank, world, &plan, &rplan, out_lo, out_hi, row_lo, row_hi);
   CL_GUARD_END

@@ -28,10 +28,13 @@ KEYS = {
     "sm__cycles_elapsed.avg.per_second": "sm_clock_hz",
     "sm__pipe_fma_cycles_active.sum.pct_of_peak_sustained_active": "fma_pipe_active_pct",
     "sm__inst_executed_pipe_fma.sum.pct_of_peak_sustained_active": "fma_pipe_inst_pct",
+    "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed": "tensor_pipe_active_pct",
+    "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed": "tensor_pipe_active_pct",
+    "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active": "tensor_smem_operand_active_pct",
 }
 
 
-DIRECT = ("k_res_s", "k_grad_s", "k_conv_residual", "k_conv_rows", "k_conv_dense", "k_ista_update", "k_residual_reduce", "k_admm_beta",
+DIRECT = ("k_res_s", "k_grad_s", "k_tc_dense", "k_conv_residual", "k_conv_rows", "k_conv_dense", "k_ista_update", "k_residual_reduce", "k_admm_beta",
           "k_admm_x", "k_admm_duals", "k_metrics_final")
 FFT = ("k_fft_pass<16, -1>", "k_fft_pass<16, 1>", "k_fft_pass<8, -1>", "k_fft_pass<8, 1>", "k_fft_pass<4, -1>",
        "k_fft_pass<4, 1>", "k_fft_pass<2, -1>", "k_fft_pass<2, 1>", "k_real_to_complex", "k_spec_mul",
