@@ -1536,10 +1536,8 @@ void conv_kernels_init() {
 }
 
 ConvPlan make_dense_plan(int64_t n) {
-  static const bool no_tc = [] {
-    const char* v = getenv("CLB_NO_TC");
-    return v && atoi(v) != 0;
-  }();
+  const char* v = getenv("CLB_NO_TC");  // read per call (setup time): tests switch it per solver
+  const bool no_tc = v && atoi(v) != 0;
   if (!no_tc && tc_dense_supported(n)) {
     ConvPlan p = make_tc_plan(n);
     p.tc = true;

@@ -693,3 +693,57 @@ def test_coop_cadmm_matches_oracle(n, m, k, seed, iters):
     assert_parity(g.get("z"), o.get("z"), what="z")
     for f in ("x", "v", "mu", "nu", "beta"):
         assert rel_l2(g.get(f), o.get(f)) <= REL_TOL, f
+
+
+# ------------------------------------------------- tensor-core products (csrc/tc_dense.cu)
+@pytest.mark.parametrize("kind,lg,iters", [("ista", 18, 4), ("cadmm", 16, 3), ("cadmm", 15, 3)])
+def test_tensor_core_products_match_ffma_kernels(kind, lg, iters, monkeypatch):
+    """k_tc_dense (3xTF32, TMEM drained to fp32) against the FFMA kernels (CLB_NO_TC=1), which are
+    themselves oracle-checked: same iterates to fp32 accuracy after a few iterations."""
+    n = 1 << lg
+    p = orc.make_problem(n, n // 4, max(1, n // 256), 3)
+    setup = cl.ista_setup if kind == "ista" else cl.cadmm_setup
+    fields = ("x", "r", "delta") if kind == "ista" else ("z", "x", "v", "beta")
+    got = {}
+    for off in ("0", "1"):
+        monkeypatch.setenv("CLB_NO_TC", off)
+        g = setup(op_of(p), p.y)
+        g.step(iters)
+        got[off] = {f: g.get(f) for f in fields}
+        del g
+    for f in fields:
+        tol = 1e-3 if f == "delta" else 2e-5
+        assert rel_l2(got["0"][f], got["1"][f]) <= tol, (f, rel_l2(got["0"][f], got["1"][f]))
+
+
+@pytest.mark.parametrize("kind,lg", [("ista", 18), ("cadmm", 17)])
+def test_tensor_core_sharded_matches_unsharded(kind, lg):
+    """Two shards of one solve on one GPU, slices exchanged locally after every phase (the
+    all-gather's effect), against the unsharded solve: bitwise identical iterates, since the
+    split-K decomposition depends on n only."""
+    import torch
+    from paper_1707_02244_b200.dist import CudaShard
+    n = 1 << lg
+    p = orc.make_problem(n, n // 4, max(1, n // 256), 5)
+    setup = cl.ista_setup if kind == "ista" else cl.cadmm_setup
+    iters = 3
+    ref = setup(op_of(p), p.y)
+    ref.step(iters)
+    want = ref.get("x")
+    states = [setup(op_of(p), p.y) for _ in range(2)]
+    shards = [CudaShard(s, r, 2) for r, s in enumerate(states)]
+    for _ in range(iters):
+        for ph in shards[0].phases():
+            outs = []
+            for sh in shards:
+                sh.run_phase(ph)
+                sh.state.synchronize()
+                outs.append(sh.phase_output(ph))
+            (f0, b0, e0), (f1, b1, e1) = outs
+            f1[b0:e0].copy_(f0[b0:e0])
+            f0[b1:e1].copy_(f1[b1:e1])
+            torch.cuda.synchronize()
+    for s in states:
+        s.synchronize()
+    got = states[0].get("x")
+    assert np.array_equal(got, want), rel_l2(got, want)
