@@ -44,7 +44,7 @@ constexpr int kOffB = kAStages * 2 * kSlabBytes;
 constexpr int kOffBar = kOffB + kBStages * 2 * kTileBytes;
 constexpr int kTcSmem = kOffBar + (8 + 2 * kBStages) * 8 + 16;
 #ifndef TC_SPD
-#define TC_SPD 2
+#define TC_SPD 4
 #endif
 constexpr int kSPD = TC_SPD;  // steps accumulated in TMEM between drains (divides 8)
 constexpr int kTmemCols = 512;  // two 128 x 256 fp32 accumulators
@@ -105,11 +105,13 @@ __device__ __forceinline__ void st_split(float* hi, float* lo, float4 v) {
 }
 
 // unit = (tile, split); split s covers offsets [s Dn, (s + 1) Dn), Dn = (n / 256) / splits.
-// A step is one (offset D, K group g) pair: 12 MMAs (4 K-steps x 3 TF32 products) into
-// one of two TMEM accumulators, started from zero.  The tensor core's fp32 accumulation
-// truncates, so its error grows with the accumulator's magnitude; draining every step
-// into fp32 registers (round-to-nearest FADD) keeps the sums at FFMA accuracy
-// (tools/microbench/tc_probe.cu: 8.4e-7 -> ~1e-8 of sum|terms| at n = 2^20).
+// A step is one (offset D, K group g) pair: 12 MMAs (4 K-steps x 3 TF32 products).  kSPD
+// steps accumulate into one of two TMEM accumulators, started from zero.  The tensor core's
+// fp32 accumulation truncates, so its error grows with the accumulator's magnitude; draining
+// every kSPD steps into fp32 registers (round-to-nearest FADD) keeps the sums at FFMA accuracy
+// (tools/microbench/tc_probe.cu at n = 2^20, max error / sum|terms|: 8.4e-7 never drained;
+// 3.3e-9 / 3.4e-9 / 6.0e-9 / 8.0e-9 drained every 1 / 2 / 4 / 8 steps, at 7.8 / 7.6 / 7.05 /
+// 7.1 ms).
 // Steps run in the order (D block, g, D): one A slab per (block, g), one Hankel tile per step.
 __global__ void __launch_bounds__(kTcThreads, 1)
 k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, int splits, int64_t tile_lo,
