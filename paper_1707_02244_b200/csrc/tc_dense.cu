@@ -20,6 +20,8 @@
 // the fp32 TMEM accumulator.  The dropped Alo.Blo term is ~2^-22 relative.
 #include "tc_dense.cuh"
 
+#include <cuda_fp16.h>
+
 #include <cstdlib>
 
 namespace clb {
@@ -38,8 +40,10 @@ constexpr int kTileBytes = kRB * 16;
 #define TC_BST 8
 #endif
 constexpr int kAStages = 2, kBStages = TC_BST;
-constexpr int kProducers = 256;
-constexpr int kTcThreads = kProducers + 32;  // warps 0-7 produce and drain, warp 8 issues MMAs
+constexpr int kDrainers = 256;                 // warps 0-7: drain TMEM into fp32 registers
+constexpr int kProducers = 64;                 // warps 8-9: A slabs and Hankel tiles
+constexpr int kMmaWarp = (kDrainers + kProducers) / 32;  // warp 10: TMEM allocation, MMA issue
+constexpr int kTcThreads = kDrainers + kProducers + 32;
 constexpr int kOffB = kAStages * 2 * kSlabBytes;
 constexpr int kOffBar = kOffB + kBStages * 2 * kTileBytes;
 constexpr int kTcSmem = kOffBar + (8 + 2 * kBStages) * 8 + 16;
@@ -97,6 +101,64 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void mma_f16(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// 8 scaled values -> 16-byte rows of fp16 hi = rn(x) and lo = rn(x - hi) (x - hi is exact in fp32)
+__device__ __forceinline__ void st_split8(unsigned char* hi, unsigned char* lo, const float (&v)[8], float sc) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float a = v[2 * q] * sc, b = v[2 * q + 1] * sc;
+    const __half ha = __float2half_rn(a), hb = __float2half_rn(b);
+    const __half la = __float2half_rn(a - __half2float(ha)), lb = __float2half_rn(b - __half2float(hb));
+    h[q] = static_cast<uint32_t>(__half_as_ushort(ha)) | (static_cast<uint32_t>(__half_as_ushort(hb)) << 16);
+    l[q] = static_cast<uint32_t>(__half_as_ushort(la)) | (static_cast<uint32_t>(__half_as_ushort(lb)) << 16);
+  }
+  *reinterpret_cast<uint4*>(hi) = make_uint4(h[0], h[1], h[2], h[3]);
+  *reinterpret_cast<uint4*>(lo) = make_uint4(l[0], l[1], l[2], l[3]);
+}
+// power-of-two scale putting max|x| in [2^13, 2^14) (fp16 max 65504); 1 for 0 / non-finite
+__device__ __forceinline__ float f16_scale(float mx) {
+  if (!(mx > 0.f) || !isfinite(mx)) return 1.f;
+  int e;
+  frexpf(mx, &e);  // mx < 2^e
+  return ldexpf(1.f, 14 - e);
+}
+
+__global__ void k_absmax2(const float* __restrict__ h, const float* __restrict__ u, int64_t n, float* __restrict__ out) {
+  float a = 0.f, b = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    a = fmaxf(a, fabsf(h[i]));
+    b = fmaxf(b, fabsf(u[i]));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
+    b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, o));
+  }
+  __shared__ float sa[32], sb[32];
+  if ((threadIdx.x & 31) == 0) {
+    sa[threadIdx.x >> 5] = a;
+    sb[threadIdx.x >> 5] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      a = fmaxf(a, sa[w]);
+      b = fmaxf(b, sb[w]);
+    }
+    out[blockIdx.x] = a;
+    out[gridDim.x + blockIdx.x] = b;
+  }
+}
+constexpr int kMaxBlocks = 148 * 4;
+
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 __device__ __forceinline__ void st_split(float* hi, float* lo, float4 v) {
   const float4 a = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
@@ -113,13 +175,23 @@ __device__ __forceinline__ void st_split(float* hi, float* lo, float4 v) {
 // 3.3e-9 / 3.4e-9 / 6.0e-9 / 8.0e-9 drained every 1 / 2 / 4 / 8 steps, at 7.8 / 7.6 / 7.05 /
 // 7.1 ms).
 // Steps run in the order (D block, g, D): one A slab per (block, g), one Hankel tile per step.
+// Roles: warps 0-7 drain, warps 8-9 produce, one thread of warp 10 issues the MMAs, so tile
+// production never waits behind a drain.  F16: fp16 operands with a 2-term split of
+// power-of-two-scaled values (hi.hi + hi.lo + lo.hi, kind::f16: twice the MMA rate and half the
+// operand bytes of TF32); `maxes` holds k_absmax2's per-block maxima of |h| and |u|.
+template <bool F16>
 __global__ void __launch_bounds__(kTcThreads, 1)
 k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, int splits, int64_t tile_lo,
-           float* __restrict__ partial) {
+           float* __restrict__ partial, const float* __restrict__ maxes) {
+  constexpr int kEl = F16 ? 8 : 4;       // elements per 16-byte chunk
+  constexpr int kCh = kKG / kEl;         // chunks per K group
+  constexpr int kKS = F16 ? 16 : 8;      // K per MMA
+  constexpr uint32_t kLboB = 16u * kEl;  // Hankel: the next chunk starts kEl rows on
   extern __shared__ __align__(1024) unsigned char sm[];
+  __shared__ float scl[2];
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + kOffBar);
-  uint64_t* a_full = bar;        // [2]
-  uint64_t* a_empty = bar + 2;   // [2]
+  uint64_t* a_full = bar;                     // [2]
+  uint64_t* a_empty = bar + 2;                // [2]
   uint64_t* b_full = bar + 4;                 // [kBStages]
   uint64_t* b_empty = b_full + kBStages;      // [kBStages]
   uint64_t* t_full = b_empty + kBStages;      // [2]
@@ -149,40 +221,93 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&t_full[i], 1);
-      mbar_init(&t_empty[i], kProducers);
+      mbar_init(&t_empty[i], kDrainers);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == kProducers / 32) {
+  if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "n"(kTmemCols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
+  if (F16 && warp == 1) {
+    float a = 0.f, b = 0.f;
+    for (int i = lane; i < kMaxBlocks; i += 32) {
+      a = fmaxf(a, maxes[i]);
+      b = fmaxf(b, maxes[kMaxBlocks + i]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
+      b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, o));
+    }
+    if (lane == 0) {
+      scl[0] = f16_scale(a);
+      scl[1] = f16_scale(b);
+    }
+  }
   tc_before_sync();
   __syncthreads();
   tc_after_sync();
   const uint32_t tmem = *tmem_slot;
+  const float sh = F16 ? scl[0] : 1.f, su = F16 ? scl[1] : 1.f;
 
-  if (warp < kProducers / 32) {
-    // ---- producers (A slabs, Hankel tiles) and accumulator drain ----
+  if (warp < kDrainers / 32) {
+    // ---- drain: every kSPD steps, TMEM accumulator -> fp32 registers (round to nearest) ----
+    float acc[kB / 2];
+#pragma unroll
+    for (int q = 0; q < kB / 2; ++q) acc[q] = 0.f;
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + (warp >> 2) * (kB / 2);
+    for (int64_t cyc = 0; cyc < steps / kSPD; ++cyc) {
+      const int buf = static_cast<int>(cyc & 1);
+      mbar_wait(&t_full[buf], (cyc >> 1) & 1);
+      tc_after_sync();
+#pragma unroll
+      for (int c0 = 0; c0 < kB / 2; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld32(lane_base + buf * kB + c0, v);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) acc[c0 + e] += __uint_as_float(v[e]);
+      }
+      tc_before_sync();
+      mbar_arrive(&t_empty[buf]);
+    }
+    // ---- partial[s][256 I + p]: this thread's row I, columns [128 (warp / 4), +128) ----
+    float* out = partial + static_cast<int64_t>(s) * n + (I0 + (warp & 3) * 32 + lane) * kB + (warp >> 2) * (kB / 2);
+    const float inv = 1.f / (sh * su);  // powers of two: exact
+#pragma unroll
+    for (int q = 0; q < kB / 2; q += 4)
+      *reinterpret_cast<float4*>(out + q) = make_float4(acc[q] * inv, acc[q + 1] * inv, acc[q + 2] * inv, acc[q + 3] * inv);
+  } else if (warp < kMmaWarp) {
+    // ---- producers: A slabs and Hankel tiles, in consumption order, up to kBStages ahead ----
+    const int ptid = tid - kDrainers;
     int a_use = 0;
-    auto produce = [&](int64_t j) {
+    for (int64_t j = 0; j < steps; ++j) {
       const int64_t blk = j >> (lgDB + 3), rem = j & (kNG * DBn - 1);
       const int g = static_cast<int>(rem >> lgDB);
       const int64_t dd = rem & (DBn - 1), d0 = Dlo + blk * DBn, D = d0 + dd;
       if (dd == 0) {
         const int st = a_use & 1;
         mbar_wait(&a_empty[st], ((a_use >> 1) & 1) ^ 1);
-        float* hi = reinterpret_cast<float*>(sm + (st * 2) * kSlabBytes);
-        float* lo = reinterpret_cast<float*>(sm + (st * 2 + 1) * kSlabBytes);
+        unsigned char* hi = sm + (st * 2) * kSlabBytes;
+        unsigned char* lo = sm + (st * 2 + 1) * kSlabBytes;
         const int64_t ibase = I0 - d0 - DBn + 1;  // I - D of slab row 0
-        for (int idx = tid; idx < rows * (kKG / 4); idx += kProducers) {
+        for (int idx = ptid; idx < rows * kCh; idx += kProducers) {
           const int rho = idx % rows, c = idx / rows;
           const int64_t Ip = (ibase + rho) & nbm;
-          const float4 v = __ldg(reinterpret_cast<const float4*>(u + Ip * kB + (kB - 4) - kKG * g - 4 * c));
-          const int off = (c * rows + rho) * 4;
-          st_split(hi + off, lo + off, make_float4(v.w, v.z, v.y, v.x));
+          const int off = (c * rows + rho) * 16;
+          if constexpr (F16) {
+            const float* src = u + Ip * kB + (kB - 8) - kKG * g - 8 * c;
+            const float4 v0 = __ldg(reinterpret_cast<const float4*>(src));
+            const float4 v1 = __ldg(reinterpret_cast<const float4*>(src + 4));
+            const float v[8] = {v1.w, v1.z, v1.y, v1.x, v0.w, v0.z, v0.y, v0.x};
+            st_split8(hi + off, lo + off, v, su);
+          } else {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(u + Ip * kB + (kB - 4) - kKG * g - 4 * c));
+            st_split(reinterpret_cast<float*>(hi + off), reinterpret_cast<float*>(lo + off),
+                     make_float4(v.w, v.z, v.y, v.x));
+          }
         }
         fence_async_smem();
         mbar_arrive(&a_full[st]);
@@ -190,55 +315,36 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
       }
       const int bs = static_cast<int>(j & (kBStages - 1));
       mbar_wait(&b_empty[bs], ((j / kBStages) & 1) ^ 1);
-      float* thi = reinterpret_cast<float*>(sm + kOffB + (bs * 2) * kTileBytes);
-      float* tlo = reinterpret_cast<float*>(sm + kOffB + (bs * 2 + 1) * kTileBytes);
+      unsigned char* thi = sm + kOffB + (bs * 2) * kTileBytes;
+      unsigned char* tlo = sm + kOffB + (bs * 2 + 1) * kTileBytes;
       const int64_t t0 = D * kB - (kB - 1) + kKG * g;
-      for (int r = tid; r < kRB; r += kProducers) {
-        const int64_t t = t0 + r;
-        const float4 v = make_float4(__ldg(h + (t & nm)), __ldg(h + ((t + 1) & nm)), __ldg(h + ((t + 2) & nm)),
-                                     __ldg(h + ((t + 3) & nm)));
-        st_split(thi + r * 4, tlo + r * 4, v);
+      constexpr int kRows = (kRB + kProducers - 1) / kProducers;
+      float v[kRows][kEl];
+#pragma unroll
+      for (int q = 0; q < kRows; ++q) {  // all loads first: one L2 latency per tile
+        const int64_t t = t0 + ptid + q * kProducers;
+#pragma unroll
+        for (int e = 0; e < kEl; ++e) v[q][e] = __ldg(h + ((t + e) & nm));
+      }
+#pragma unroll
+      for (int q = 0; q < kRows; ++q) {
+        const int r = ptid + q * kProducers;
+        if (r < kRB) {
+          if constexpr (F16) {
+            st_split8(thi + r * 16, tlo + r * 16, v[q], sh);
+          } else {
+            st_split(reinterpret_cast<float*>(thi + r * 16), reinterpret_cast<float*>(tlo + r * 16),
+                     make_float4(v[q][0], v[q][1], v[q][2], v[q][3]));
+          }
+        }
       }
       fence_async_smem();
       mbar_arrive(&b_full[bs]);
-    };
-    float acc[kB / 2];
-#pragma unroll
-    for (int q = 0; q < kB / 2; ++q) acc[q] = 0.f;
-    const uint32_t lane_base = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + (warp >> 2) * (kB / 2);
-    // Tiles run `ahead` steps ahead of the drain.  Tile j + ahead reuses the B stage of step
-    // j + ahead - kBStages (issued before step j), and a slab it starts reuses the A stage of
-    // step j + ahead - DBn - 1 at the latest: ahead <= DBn keeps both waits free of any drain
-    // this loop has not done yet (no deadlock when slabs change every step, e.g. n = 2^16).
-    const int64_t ahead = DBn < kBStages - 1 ? DBn : kBStages - 1;
-    for (int64_t j = 0; j < ahead && j < steps; ++j) produce(j);
-    for (int64_t j = 0; j < steps; ++j) {
-      if (j % kSPD == kSPD - 1) {
-        const int64_t cyc = j / kSPD;
-        const int buf = static_cast<int>(cyc & 1);
-        mbar_wait(&t_full[buf], (cyc >> 1) & 1);
-        tc_after_sync();
-#ifndef TC_NODRAIN
-#pragma unroll
-        for (int c0 = 0; c0 < kB / 2; c0 += 32) {
-          uint32_t v[32];
-          tmem_ld32(lane_base + buf * kB + c0, v);
-#pragma unroll
-          for (int e = 0; e < 32; ++e) acc[c0 + e] += __uint_as_float(v[e]);
-        }
-#endif
-        tc_before_sync();
-        mbar_arrive(&t_empty[buf]);
-      }
-      if (j + ahead < steps) produce(j + ahead);
     }
-    // ---- partial[s][256 I + p]: this thread's row I, columns [128 (warp / 4), +128) ----
-    float* out = partial + static_cast<int64_t>(s) * n + (I0 + (warp & 3) * 32 + lane) * kB + (warp >> 2) * (kB / 2);
-#pragma unroll
-    for (int q = 0; q < kB / 2; q += 4) *reinterpret_cast<float4*>(out + q) = make_float4(acc[q], acc[q + 1], acc[q + 2], acc[q + 3]);
   } else if (lane == 0) {
     // ---- MMA issue (one thread) ----
-    constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(kB >> 3) << 17) |
+    constexpr uint32_t kFmt = F16 ? 0u : 2u;  // operand format: F16 (kind::f16) / TF32 (kind::tf32)
+    constexpr uint32_t idesc = (1u << 4) | (kFmt << 7) | (kFmt << 10) | (static_cast<uint32_t>(kB >> 3) << 17) |
                                (static_cast<uint32_t>(kMT >> 4) << 24);
     const uint32_t abase = smem_u32(sm), bbase = smem_u32(sm + kOffB);
     int a_use = 0;
@@ -262,14 +368,20 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
       const uint32_t bhi = bbase + (bs * 2) * kTileBytes, blo = bhi + kTileBytes;
       const uint32_t tacc = tmem + buf * kB;
 #pragma unroll
-      for (int kk = 0; kk < kKG / 8; ++kk) {
+      for (int kk = 0; kk < kKG / kKS; ++kk) {
         const uint64_t dah = sdesc(ahi + row0 + 2u * kk * lboA, lboA, 128);
         const uint64_t dal = sdesc(alo + row0 + 2u * kk * lboA, lboA, 128);
-        const uint64_t dbh = sdesc(bhi + 128u * kk, 64, 128);
-        const uint64_t dbl = sdesc(blo + 128u * kk, 64, 128);
-        mma_tf32(tacc, dah, dbh, idesc, (first && kk == 0) ? 0u : 1u);
-        mma_tf32(tacc, dah, dbl, idesc, 1);
-        mma_tf32(tacc, dal, dbh, idesc, 1);
+        const uint64_t dbh = sdesc(bhi + 2u * kLboB * kk, kLboB, 128);
+        const uint64_t dbl = sdesc(blo + 2u * kLboB * kk, kLboB, 128);
+        if constexpr (F16) {
+          mma_f16(tacc, dah, dbh, idesc, (first && kk == 0) ? 0u : 1u);
+          mma_f16(tacc, dah, dbl, idesc, 1);
+          mma_f16(tacc, dal, dbh, idesc, 1);
+        } else {
+          mma_tf32(tacc, dah, dbh, idesc, (first && kk == 0) ? 0u : 1u);
+          mma_tf32(tacc, dah, dbl, idesc, 1);
+          mma_tf32(tacc, dal, dbh, idesc, 1);
+        }
       }
       tc_commit(&b_empty[bs]);
       if (j % kSPD == kSPD - 1) tc_commit(&t_full[buf]);
@@ -281,7 +393,7 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
   }
   tc_before_sync();
   __syncthreads();
-  if (warp == kProducers / 32) {
+  if (warp == kMmaWarp) {
     tc_after_sync();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
   }
@@ -312,19 +424,41 @@ ConvPlan make_tc_plan(int64_t n) {
   return p;
 }
 
+namespace {
+float* g_maxes[64] = {};  // per device: k_absmax2 output (2 x kMaxBlocks floats)
+bool use_f16() {
+  const char* v = getenv("CLB_TC_F16");
+  return v && atoi(v) != 0;
+}
+}  // namespace
+
 void tc_dense_init() {
-  static bool done = false;
-  if (done) return;
-  done = true;
-  cudaFuncSetAttribute(reinterpret_cast<const void*>(k_tc_dense), cudaFuncAttributeMaxDynamicSharedMemorySize,
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static bool done[64] = {};
+  if (dev < 0 || dev >= 64 || done[dev]) return;
+  done[dev] = true;
+  cudaFuncSetAttribute(reinterpret_cast<const void*>(k_tc_dense<false>), cudaFuncAttributeMaxDynamicSharedMemorySize,
                        kTcSmem);
+  cudaFuncSetAttribute(reinterpret_cast<const void*>(k_tc_dense<true>), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       kTcSmem);
+  cudaMalloc(&g_maxes[dev], 2 * kMaxBlocks * sizeof(float));
 }
 
 void launch_tc_dense(const ConvPlan& p, const float* h, const float* u, float* partial, cudaStream_t st) {
   const int64_t units = (p.tile_hi - p.tile_lo) * p.splits;
   if (units <= 0) return;
   tc_dense_init();
-  k_tc_dense<<<static_cast<unsigned>(units), kTcThreads, kTcSmem, st>>>(h, u, p.n, p.splits, p.tile_lo, partial);
+  if (use_f16()) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    k_absmax2<<<kMaxBlocks, 256, 0, st>>>(h, u, p.n, g_maxes[dev]);
+    k_tc_dense<true><<<static_cast<unsigned>(units), kTcThreads, kTcSmem, st>>>(h, u, p.n, p.splits, p.tile_lo,
+                                                                                partial, g_maxes[dev]);
+  } else {
+    k_tc_dense<false><<<static_cast<unsigned>(units), kTcThreads, kTcSmem, st>>>(h, u, p.n, p.splits, p.tile_lo,
+                                                                                 partial, nullptr);
+  }
 }
 
 }  // namespace clb
