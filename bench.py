@@ -181,6 +181,23 @@ def run_reference(args, w, rank):
 
 
 TF32_DENSE_TFLOPS = 1100.0  # B200 dense TF32 tensor peak (/opt/skills/guides/B200_PROFILING.md; not in MEASURED_PEAKS.json)
+F16_DENSE_TFLOPS = 2250.0   # B200 dense fp16/bf16 tensor peak (same guide; MEASURED_PEAKS.json bf16 matmul: see bench line)
+
+
+def tc_f16(n):
+    """The tcgen05 kernel uses fp16 operands (2-term split) for n >= 2^20, 3xTF32 below (CLB_TC_F16 forces)."""
+    v = os.environ.get("CLB_TC_F16", "")
+    return (v not in ("", "0")) if v else n >= (1 << 20)
+
+
+def tc_peak(n):
+    return F16_DENSE_TFLOPS if tc_f16(n) else TF32_DENSE_TFLOPS
+
+
+def tc_note(n):
+    return ("fp16 operands, power-of-two scaled, 2-term split (hi.hi + hi.lo + lo.hi, kind::f16)" if tc_f16(n) else
+            "3xTF32 (hi.hi + hi.lo + lo.hi, kind::tf32)") + \
+        ": 3 tensor flops per algorithmic flop; achieved/frac count algorithmic flops"
 
 
 def dense_uses_tc(n):
@@ -192,11 +209,11 @@ def dense_kernel_info(n, ms):
     flops = 2.0 * n * n
     if dense_uses_tc(n):
         return {"kernel": "k_tc_dense", "ms": ms, "achieved_tflops": flops / (ms * 1e-3) / 1e12,
-                "bound": "tensor", "peak_tflops": TF32_DENSE_TFLOPS,
-                "frac": flops / (ms * 1e-3) / 1e12 / TF32_DENSE_TFLOPS,
+                "bound": "tensor", "peak_tflops": tc_peak(n),
+                "frac": flops / (ms * 1e-3) / 1e12 / tc_peak(n),
                 "tensor_pipe_tflops": 3 * flops / (ms * 1e-3) / 1e12,
-                "note": "3xTF32 (hi.hi + hi.lo + lo.hi) for fp32 accuracy: 3 tensor flops per algorithmic flop; "
-                        "achieved/frac count algorithmic flops (2 n^2)"}
+                "tensor_pipe_frac": 3 * flops / (ms * 1e-3) / 1e12 / tc_peak(n),
+                "note": tc_note(n)}
     return {"kernel": "k_conv_dense", "ms": ms, "achieved_tflops": flops / (ms * 1e-3) / 1e12, "bound": "fp32_ffma"}
 
 
@@ -237,7 +254,7 @@ def admm_line(cl, torch, prob, local_rank, flush, steps=5, warmup=3):
     return {"value": 1e3 / ms, "unit": "iterations/s", "ms_per_step": ms, "steps": steps, "warmup": warmup,
             "workload": f"cADMM n={n}, m={prob.op.m()}, k={prob.k()}, rho=sigma=0.1, tau1=tau2=1, alpha=1e-4 "
                         "(make_problem(2^20, 2^18, 2^12, 1), the config-3 problem)",
-            "engine": "direct circulant products on tcgen05 tensor cores (3xTF32)" if dense_uses_tc(n)
+            "engine": "direct circulant products on tcgen05 tensor cores" if dense_uses_tc(n)
                       else "direct shift-indexed sm_100a kernels",
             "dense_kernel": dense_kernel_info(n, dense_ms),
             "step_tflops": 6.0 * n * n / (ms * 1e-3) / 1e12, "phase_ms": ph}
@@ -373,7 +390,7 @@ def main():
         k_ms = statistics.mean(p[0] for p in phase_ms)
         k_flops = 2.0 * w["n"] * w["n"] / world
         k_name = "k_tc_dense" if dense_uses_tc(w["n"]) else "k_conv_dense"
-    peak = TF32_DENSE_TFLOPS if k_name == "k_tc_dense" else cl.ffma_peak_tflops(local_rank)
+    peak = tc_peak(w["n"]) if k_name == "k_tc_dense" else cl.ffma_peak_tflops(local_rank)
     achieved = k_flops / (k_ms * 1e-3) / 1e12
     traffic = None
     try:
@@ -507,7 +524,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (make_problem, seeded)",
             "config": {"workload": w["desc"], "n": w["n"], "m": w["m"], "k": w["k"], "seed": w["seed"],
-                       "engine": ("direct circulant products on tcgen05 tensor cores (3xTF32; ISTA's sparse products "
+                       "engine": ("direct circulant products on tcgen05 tensor cores (ISTA's sparse products "
                                   "embedded in dense ones)" if k_name == "k_tc_dense" else
                                   "direct shift-indexed sm_100a kernels"),
                        "l2": "flushed (256 MiB) between steps",
@@ -515,14 +532,14 @@ def main():
             "roofline": {"bound": "tensor" if k_name == "k_tc_dense" else "fp32_ffma", "kernel": k_name,
                          "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                         "peak_source": ("B200 dense TF32 1.1 PF (B200_PROFILING.md); 3xTF32 emulation, achieved counts "
-                                         "algorithmic flops" if k_name == "k_tc_dense" else
+                         "peak_source": (("B200 dense fp16 2.25 PF" if tc_f16(w["n"]) else "B200 dense TF32 1.1 PF") +
+                                         " (B200_PROFILING.md); " + tc_note(w["n"]) if k_name == "k_tc_dense" else
                                          "live FFMA microbenchmark (cl_ffma_peak); MEASURED_PEAKS.json has no FP32 entry"),
                          **({"dense_product_tflops": 2.0 * w["n"] * w["n"] / world / (k_ms * 1e-3) / 1e12,
                              "tensor_pipe_tflops": 6.0 * w["n"] * w["n"] / world / (k_ms * 1e-3) / 1e12,
                              "tensor_pipe_frac": 6.0 * w["n"] * w["n"] / world / (k_ms * 1e-3) / 1e12 / peak,
                              "work_note": "the kernel computes the dense product C x (2 n^2 flop; ISTA needs the m rows "
-                                          "of Omega, 2 m n) in 3xTF32 (3 tensor flops per flop)"}
+                                          "of Omega, 2 m n) with 3 tensor flops per flop"}
                             if k_name == "k_tc_dense" else {}),
                          "step_tflops": algorithmic_flops(w) / (ms_per_step * 1e-3) / 1e12,
                          "step_frac": algorithmic_flops(w) / (ms_per_step * 1e-3) / 1e12 / peak,

@@ -46,7 +46,9 @@ constexpr int kMmaWarp = (kDrainers + kProducers) / 32;  // warp 10: TMEM alloca
 constexpr int kTcThreads = kDrainers + kProducers + 32;
 constexpr int kOffB = kAStages * 2 * kSlabBytes;
 constexpr int kOffBar = kOffB + kBStages * 2 * kTileBytes;
-constexpr int kTcSmem = kOffBar + (8 + 2 * kBStages) * 8 + 16;
+constexpr int kStg = kRB + 8;  // fp16 staging row (packed hi | lo) per tile, double-buffered
+constexpr int kOffStg = kOffBar + (8 + 2 * kBStages) * 8 + 16;
+constexpr int kTcSmem = kOffStg + 2 * kStg * 4;
 #ifndef TC_SPD
 #define TC_SPD 4
 #endif
@@ -319,6 +321,44 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
       unsigned char* tlo = sm + kOffB + (bs * 2 + 1) * kTileBytes;
       const int64_t t0 = D * kB - (kB - 1) + kKG * g;
       constexpr int kRows = (kRB + kProducers - 1) / kProducers;
+      if constexpr (F16) {
+        // Split each of the tile's kRB + 8 values once into a packed (hi | lo << 16) fp16 word in a
+        // double-buffered staging row, then build the 8-wide Hankel rows from it with byte permutes.
+        uint32_t* stg = reinterpret_cast<uint32_t*>(sm + kOffStg) + (j & 1) * kStg;
+        constexpr int kSt = (kStg + kProducers - 1) / kProducers;
+        float x[kSt];
+#pragma unroll
+        for (int q = 0; q < kSt; ++q) x[q] = __ldg(h + ((t0 + ptid + q * kProducers) & nm));
+#pragma unroll
+        for (int q = 0; q < kSt; ++q) {
+          const int i = ptid + q * kProducers;
+          if (i < kStg) {
+            const float a = x[q] * sh;
+            const __half ha = __float2half_rn(a);
+            stg[i] = static_cast<uint32_t>(__half_as_ushort(ha)) |
+                     (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(a - __half2float(ha)))) << 16);
+          }
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kProducers) : "memory");
+#pragma unroll
+        for (int q = 0; q < kRows; ++q) {
+          const int r = ptid + q * kProducers;
+          if (r < kRB) {
+            uint32_t w[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) w[e] = stg[r + e];
+            *reinterpret_cast<uint4*>(thi + r * 16) =
+                make_uint4(__byte_perm(w[0], w[1], 0x5410), __byte_perm(w[2], w[3], 0x5410),
+                           __byte_perm(w[4], w[5], 0x5410), __byte_perm(w[6], w[7], 0x5410));
+            *reinterpret_cast<uint4*>(tlo + r * 16) =
+                make_uint4(__byte_perm(w[0], w[1], 0x7632), __byte_perm(w[2], w[3], 0x7632),
+                           __byte_perm(w[4], w[5], 0x7632), __byte_perm(w[6], w[7], 0x7632));
+          }
+        }
+        fence_async_smem();
+        mbar_arrive(&b_full[bs]);
+        continue;
+      }
       float v[kRows][kEl];
 #pragma unroll
       for (int q = 0; q < kRows; ++q) {  // all loads first: one L2 latency per tile
@@ -426,9 +466,12 @@ ConvPlan make_tc_plan(int64_t n) {
 
 namespace {
 float* g_maxes[64] = {};  // per device: k_absmax2 output (2 x kMaxBlocks floats)
-bool use_f16() {
+// fp16 operands win where slabs are long (n >= 2^20: 5.5 vs 7.0 ms at 2^20); below, slab rebuilds
+// make the fp16 producer the bottleneck (0.63 vs 0.53 ms at 2^18).  CLB_TC_F16=0/1 forces either.
+bool use_f16(int64_t n) {
   const char* v = getenv("CLB_TC_F16");
-  return v && atoi(v) != 0;
+  if (v && *v) return atoi(v) != 0;
+  return n >= (int64_t(1) << 20);
 }
 }  // namespace
 
@@ -449,7 +492,7 @@ void launch_tc_dense(const ConvPlan& p, const float* h, const float* u, float* p
   const int64_t units = (p.tile_hi - p.tile_lo) * p.splits;
   if (units <= 0) return;
   tc_dense_init();
-  if (use_f16()) {
+  if (use_f16(p.n)) {
     int dev = 0;
     cudaGetDevice(&dev);
     k_absmax2<<<kMaxBlocks, 256, 0, st>>>(h, u, p.n, g_maxes[dev]);
