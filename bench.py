@@ -524,8 +524,9 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (make_problem, seeded)",
             "config": {"workload": w["desc"], "n": w["n"], "m": w["m"], "k": w["k"], "seed": w["seed"],
-                       "engine": ("direct circulant products on tcgen05 tensor cores (ISTA's sparse products "
-                                  "embedded in dense ones)" if k_name == "k_tc_dense" else
+                       "engine": ("direct circulant products on tcgen05 tensor cores" +
+                                  (" (ISTA's sparse products embedded in dense ones)" if w["kind"] == "ista" else "")
+                                  if k_name == "k_tc_dense" else
                                   "direct shift-indexed sm_100a kernels"),
                        "l2": "flushed (256 MiB) between steps",
                        "parallelism": f"row/output shards x{world}" if sharded else "single GPU"},
@@ -545,7 +546,11 @@ def main():
                          "step_frac": algorithmic_flops(w) / (ms_per_step * 1e-3) / 1e12 / peak,
                          "phase_ms": [statistics.mean(p[i] for p in phase_ms) for i in range(len(phase_ms[0]))]},
             "clocks": clocks.summary(),
-            "gpu_launches": (((5 if ista_uses_tc(w["n"]) else 4) if w["kind"] == "ista" else 6) * args.steps),
+            # per step: ISTA 2 products + gather/scatter + update; cADMM 3 products + 3 epilogues; each
+            # fp16 tensor-core product adds its k_absmax2 scale pass
+            "gpu_launches": args.steps * (
+                (5 + (2 if tc_f16(w["n"]) else 0) if ista_uses_tc(w["n"]) else 4) if w["kind"] == "ista" else
+                (6 + (3 if dense_uses_tc(w["n"]) and tc_f16(w["n"]) else 0))),
             "e2e": e2e,
             "fft_engine": fft_line,
             "admm": admm,

@@ -34,7 +34,7 @@ KEYS = {
 }
 
 
-DIRECT = ("k_res_s", "k_grad_s", "k_tc_dense", "k_conv_residual", "k_conv_rows", "k_conv_dense", "k_ista_update", "k_residual_reduce", "k_admm_beta",
+DIRECT = ("k_res_s", "k_grad_s", "k_tc_dense", "k_absmax2", "k_residual_gather", "k_scatter_real", "k_conv_residual", "k_conv_rows", "k_conv_dense", "k_ista_update", "k_residual_reduce", "k_admm_beta",
           "k_admm_x", "k_admm_duals", "k_metrics_final")
 FFT = ("k_fft_pass<16, -1>", "k_fft_pass<16, 1>", "k_fft_pass<8, -1>", "k_fft_pass<8, 1>", "k_fft_pass<4, -1>",
        "k_fft_pass<4, 1>", "k_fft_pass<2, -1>", "k_fft_pass<2, 1>", "k_real_to_complex", "k_spec_mul",
