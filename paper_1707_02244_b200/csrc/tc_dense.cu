@@ -285,6 +285,17 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
     // ---- producers: A slabs and Hankel tiles, in consumption order, up to kBStages ahead ----
     const int ptid = tid - kDrainers;
     int a_use = 0;
+    // fp16: the next tile's h values are loaded one tile ahead (their latency overlaps this tile)
+    constexpr int kSt = (kStg + kProducers - 1) / kProducers;
+    auto tile_t0 = [&](int64_t j) {
+      const int64_t rem = j & (kNG * DBn - 1);
+      return (Dlo + (j >> (lgDB + 3)) * DBn + (rem & (DBn - 1))) * kB - (kB - 1) + kKG * (rem >> lgDB);
+    };
+    float xn[F16 ? kSt : 1];
+    if constexpr (F16) {
+#pragma unroll
+      for (int q = 0; q < kSt; ++q) xn[q] = __ldg(h + ((tile_t0(0) + ptid + q * kProducers) & nm));
+    }
     for (int64_t j = 0; j < steps; ++j) {
       const int64_t blk = j >> (lgDB + 3), rem = j & (kNG * DBn - 1);
       const int g = static_cast<int>(rem >> lgDB);
@@ -295,20 +306,35 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
         unsigned char* hi = sm + (st * 2) * kSlabBytes;
         unsigned char* lo = sm + (st * 2 + 1) * kSlabBytes;
         const int64_t ibase = I0 - d0 - DBn + 1;  // I - D of slab row 0
-        for (int idx = ptid; idx < rows * kCh; idx += kProducers) {
-          const int rho = idx % rows, c = idx / rows;
-          const int64_t Ip = (ibase + rho) & nbm;
-          const int off = (c * rows + rho) * 16;
-          if constexpr (F16) {
-            const float* src = u + Ip * kB + (kB - 8) - kKG * g - 8 * c;
-            const float4 v0 = __ldg(reinterpret_cast<const float4*>(src));
-            const float4 v1 = __ldg(reinterpret_cast<const float4*>(src + 4));
-            const float v[8] = {v1.w, v1.z, v1.y, v1.x, v0.w, v0.z, v0.y, v0.x};
-            st_split8(hi + off, lo + off, v, su);
-          } else {
-            const float4 v = __ldg(reinterpret_cast<const float4*>(u + Ip * kB + (kB - 4) - kKG * g - 4 * c));
-            st_split(reinterpret_cast<float*>(hi + off), reinterpret_cast<float*>(lo + off),
-                     make_float4(v.w, v.z, v.y, v.x));
+        // kBatch items per thread per pass, all loads first (one L2 latency per pass)
+        constexpr int kBatch = 4;
+        for (int base = ptid; base < rows * kCh; base += kBatch * kProducers) {
+          float4 v0[kBatch], v1[kBatch];
+#pragma unroll
+          for (int b = 0; b < kBatch; ++b) {
+            const int idx = base + b * kProducers;
+            const int rho = idx % rows, c = idx / rows;
+            const int64_t Ip = (ibase + rho) & nbm;
+            if (idx < rows * kCh) {
+              const float* src = u + Ip * kB + (kB - kEl) - kKG * g - kEl * c;
+              v0[b] = __ldg(reinterpret_cast<const float4*>(src));
+              if constexpr (F16) v1[b] = __ldg(reinterpret_cast<const float4*>(src + 4));
+            }
+          }
+#pragma unroll
+          for (int b = 0; b < kBatch; ++b) {
+            const int idx = base + b * kProducers;
+            if (idx < rows * kCh) {
+              const int rho = idx % rows, c = idx / rows;
+              const int off = (c * rows + rho) * 16;
+              if constexpr (F16) {
+                const float v[8] = {v1[b].w, v1[b].z, v1[b].y, v1[b].x, v0[b].w, v0[b].z, v0[b].y, v0[b].x};
+                st_split8(hi + off, lo + off, v, su);
+              } else {
+                st_split(reinterpret_cast<float*>(hi + off), reinterpret_cast<float*>(lo + off),
+                         make_float4(v0[b].w, v0[b].z, v0[b].y, v0[b].x));
+              }
+            }
           }
         }
         fence_async_smem();
@@ -325,10 +351,14 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
         // Split each of the tile's kRB + 8 values once into a packed (hi | lo << 16) fp16 word in a
         // double-buffered staging row, then build the 8-wide Hankel rows from it with byte permutes.
         uint32_t* stg = reinterpret_cast<uint32_t*>(sm + kOffStg) + (j & 1) * kStg;
-        constexpr int kSt = (kStg + kProducers - 1) / kProducers;
         float x[kSt];
 #pragma unroll
-        for (int q = 0; q < kSt; ++q) x[q] = __ldg(h + ((t0 + ptid + q * kProducers) & nm));
+        for (int q = 0; q < kSt; ++q) x[q] = xn[q];
+        if (j + 1 < steps) {
+          const int64_t t1 = tile_t0(j + 1);
+#pragma unroll
+          for (int q = 0; q < kSt; ++q) xn[q] = __ldg(h + ((t1 + ptid + q * kProducers) & nm));
+        }
 #pragma unroll
         for (int q = 0; q < kSt; ++q) {
           const int i = ptid + q * kProducers;
