@@ -52,7 +52,7 @@ constexpr int kTcSmem = kOffStg + 2 * kStg * 4;
 #ifndef TC_SPD
 #define TC_SPD 4
 #endif
-constexpr int kSPD = TC_SPD;  // steps accumulated in TMEM between drains (divides 8)
+constexpr int kSPD = TC_SPD;  // TF32: steps accumulated in TMEM between drains (divides 8)
 constexpr int kTmemCols = 512;  // two 128 x 256 fp32 accumulators
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -189,6 +189,8 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
   constexpr int kCh = kKG / kEl;         // chunks per K group
   constexpr int kKS = F16 ? 16 : 8;      // K per MMA
   constexpr uint32_t kLboB = 16u * kEl;  // Hankel: the next chunk starts kEl rows on
+  // steps per drain: the same 48 MMAs per accumulator for both formats (an fp16 step has 6 MMAs)
+  constexpr int kSpd = F16 ? 2 * kSPD : kSPD;
   extern __shared__ __align__(1024) unsigned char sm[];
   __shared__ float scl[2];
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + kOffBar);
@@ -261,7 +263,7 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
 #pragma unroll
     for (int q = 0; q < kB / 2; ++q) acc[q] = 0.f;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + (warp >> 2) * (kB / 2);
-    for (int64_t cyc = 0; cyc < steps / kSPD; ++cyc) {
+    for (int64_t cyc = 0; cyc < steps / kSpd; ++cyc) {
       const int buf = static_cast<int>(cyc & 1);
       mbar_wait(&t_full[buf], (cyc >> 1) & 1);
       tc_after_sync();
@@ -429,9 +431,9 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
       }
       const int bs = static_cast<int>(j & (kBStages - 1));
       mbar_wait(&b_full[bs], (j / kBStages) & 1);
-      const int64_t cyc = j / kSPD;
+      const int64_t cyc = j / kSpd;
       const int buf = static_cast<int>(cyc & 1);
-      const bool first = j % kSPD == 0;
+      const bool first = j % kSpd == 0;
       if (first) mbar_wait(&t_empty[buf], ((cyc >> 1) & 1) ^ 1);
       tc_after_sync();
       const uint32_t row0 = static_cast<uint32_t>(DBn - 1 - dd) * 16u;
@@ -454,7 +456,7 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
         }
       }
       tc_commit(&b_empty[bs]);
-      if (j % kSPD == kSPD - 1) tc_commit(&t_full[buf]);
+      if (j % kSpd == kSpd - 1) tc_commit(&t_full[buf]);
       if (dd == DBn - 1) {
         tc_commit(&a_empty[st]);
         ++a_use;
