@@ -130,7 +130,7 @@ __device__ __forceinline__ float f16_scale(float mx) {
   if (!(mx > 0.f) || !isfinite(mx)) return 1.f;
   int e;
   frexpf(mx, &e);  // mx < 2^e
-  return ldexpf(1.f, 14 - e);
+  return ldexpf(1.f, min(14 - e, 127));  // subnormal max: 2^127 (keeps the scale finite)
 }
 
 __global__ void k_absmax2(const float* __restrict__ h, const float* __restrict__ u, int64_t n, float* __restrict__ out) {
@@ -279,10 +279,12 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
     }
     // ---- partial[s][256 I + p]: this thread's row I, columns [128 (warp / 4), +128) ----
     float* out = partial + static_cast<int64_t>(s) * n + (I0 + (warp & 3) * 32 + lane) * kB + (warp >> 2) * (kB / 2);
-    const float inv = 1.f / (sh * su);  // powers of two: exact
+    // powers of two, applied one at a time: exact, and sh * su itself may overflow (tiny inputs)
+    const float ih = 1.f / sh, iu = 1.f / su;
 #pragma unroll
     for (int q = 0; q < kB / 2; q += 4)
-      *reinterpret_cast<float4*>(out + q) = make_float4(acc[q] * inv, acc[q + 1] * inv, acc[q + 2] * inv, acc[q + 3] * inv);
+      *reinterpret_cast<float4*>(out + q) = make_float4(acc[q] * iu * ih, acc[q + 1] * iu * ih, acc[q + 2] * iu * ih,
+                                                        acc[q + 3] * iu * ih);
   } else if (warp < kMmaWarp) {
     // ---- producers: A slabs and Hankel tiles, in consumption order, up to kBStages ahead ----
     const int ptid = tid - kDrainers;

@@ -750,3 +750,32 @@ def test_tensor_core_sharded_matches_unsharded(kind, lg):
         s.synchronize()
     got = states[0].get("x")
     assert np.array_equal(got, want), rel_l2(got, want)
+
+
+@pytest.mark.parametrize("f16", ["0", "1"])
+@pytest.mark.parametrize("case", ["wide", "tiny", "huge", "sparse"])
+def test_tensor_core_product_scaling(case, f16, monkeypatch):
+    """k_tc_dense at n = 2^20 on inputs that stress the fp16 path's power-of-two scaling (and the
+    3xTF32 path on the same data): 12 decades of dynamic range, uniformly tiny (1e-30) or huge
+    (1e30) magnitudes, and a vector that is zero except for a few entries.  Same 5e-5 bar as every
+    other product."""
+    monkeypatch.setenv("CLB_TC_F16", f16)
+    n = 1 << 20
+    rng = np.random.default_rng(11)
+    row = rng.standard_normal(n)
+    x = rng.standard_normal(n)
+    if case == "wide":
+        x *= 10.0 ** rng.uniform(-6, 6, n)
+    elif case == "tiny":
+        x *= 1e-30
+        row *= 1e-5
+    elif case == "huge":
+        x *= 1e30
+    else:
+        x[:] = 0.0
+        x[rng.choice(n, 7, replace=False)] = rng.standard_normal(7)
+    C = cl.CirculantMatrix(row)
+    want = orc.circ_matvec(row, x, use_fft=True)
+    assert rel_l2(cl.circ_matvec(C, x), want) <= 5e-5
+    want_t = orc.circ_matvec(row, x, transpose=True, use_fft=True)
+    assert rel_l2(cl.circ_transpose_matvec(C, x), want_t) <= 5e-5
