@@ -500,12 +500,13 @@ ConvPlan make_tc_plan(int64_t n) {
 
 namespace {
 float* g_maxes[64] = {};  // per device: k_absmax2 output (2 x kMaxBlocks floats)
-// fp16 operands win where slabs are long (n >= 2^20: 5.5 vs 7.0 ms at 2^20); below, slab rebuilds
-// make the fp16 producer the bottleneck (0.63 vs 0.53 ms at 2^18).  CLB_TC_F16=0/1 forces either.
+// fp16 operands win where slabs are long (n = 2^20: 4.43 vs 6.96 ms; 2^19: 1.31 vs 1.74 ms); at
+// 2^18 they tie (0.51 ms) and below slab rebuilds make the fp16 producer the bottleneck.
+// CLB_TC_F16=0/1 forces either.
 bool use_f16(int64_t n) {
   const char* v = getenv("CLB_TC_F16");
   if (v && *v) return atoi(v) != 0;
-  return n >= (int64_t(1) << 20);
+  return n >= (int64_t(1) << 19);
 }
 }  // namespace
 
