@@ -1,4 +1,5 @@
-// Dense circulant product on the tcgen05 tensor cores (see tc_dense.cuh).
+// Dense circulant product on the tcgen05 tensor cores (see tc_dense.cuh; DESIGN.md §3,
+// "Tensor-core products").
 //
 // Blocking.  i = 256 I + p, j = 256 (I - D) + 255 - k  (p, k in [0, 256)):
 //   out[256 I + p] = sum_D sum_k  h[256 D - 255 + p + k] * u[256 (I - D) + 255 - k]
@@ -15,9 +16,13 @@
 //  * B: row r of a tile holds h[t0 + r .. t0 + r + 3]; with LBO = 64 B (four rows) the
 //    descriptor reads element (p, k) at row p + k - (k mod 4), lane k mod 4 = h[t0 + p + k]:
 //    a Hankel matrix from 4x-redundant rows (overlapping core matrices).
-// Precision: 3xTF32.  x = hi + lo with hi = x with the low 13 mantissa bits cleared
-// (exact in TF32) and lo = x - hi (exact in fp32); A.B ~ Ahi.Bhi + Ahi.Blo + Alo.Bhi in
-// the fp32 TMEM accumulator.  The dropped Alo.Blo term is ~2^-22 relative.
+// Precision, two formats with the same three products A.B ~ Ahi.Bhi + Ahi.Blo + Alo.Bhi in
+// the fp32 TMEM accumulator (the dropped Alo.Blo term is ~2^-22 relative):
+//  * 3xTF32 (kind::tf32): hi = x with the low 13 mantissa bits cleared (exact in TF32),
+//    lo = x - hi (exact in fp32).  Chunks hold 4 values; Hankel LBO = 64 B.
+//  * fp16 2-term split (kind::f16, n >= 2^19): x scaled by a power of two putting max|x| in
+//    [2^13, 2^14), hi = rn16(x), lo = rn16(x - hi).  Chunks hold 8 values, Hankel rows
+//    h[t0 + r .. t0 + r + 7] with LBO = 128 B; K = 16 per MMA (twice the rate, half the bytes).
 #include "tc_dense.cuh"
 
 #include <cuda_fp16.h>

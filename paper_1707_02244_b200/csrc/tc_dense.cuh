@@ -1,9 +1,11 @@
-// Dense circulant product on the 5th-generation tensor cores (tcgen05, kind::tf32, 3xTF32).
+// Dense circulant product on the 5th-generation tensor cores (tcgen05; 3xTF32 or an fp16
+// 2-term split, both fp32-grade).
 //
 //   out[i] = sum_j h[(i - j) mod n] u[j]        (the cADMM products, parallel.hpp:173-231)
 //
 // Blocking n into b = 256 turns the product into a sum over block offsets D of
-// GEMMs between a Hankel tile of h and a row-shifted view of u.
+// GEMMs between a Hankel tile of h and a row-shifted view of u ("Tensor-core
+// products").
 // Both operands are shared-memory descriptor views; the accumulator lives in TMEM.
 // Output: split-K partials partial[s * n + i], summed by the same epilogues as the
 // FFMA dense kernel (fixed split order: deterministic, a function of n only).
