@@ -223,6 +223,20 @@ def test_config3_scale_ista_vs_fft_oracle():
     assert rel_l2(g.get("r"), o.get("r")) <= REL_TOL
 
 
+def test_config3_scale_cadmm_vs_fft_oracle():
+    """cADMM at n = 2^20 (the bench's `admm` line; tensor-core products with fp16 operands):
+    3 GPU iterations vs the oracle's FFT engine."""
+    n, m = 1 << 20, 1 << 18
+    p = orc.make_problem(n, m, 1 << 12, 1)
+    g = cl.cadmm_setup(op_of(p), p.y)
+    g.step(3)
+    o = orc.Cadmm(p.row, p.omega, p.y)
+    o.step(3, orc.ENGINE_FFT)
+    assert_parity(g.get("z"), o.get("z"), what="z")
+    for f in ("x", "v"):
+        assert rel_l2(g.get(f), o.get(f)) <= REL_TOL, f
+
+
 def test_cpp_adapter_gpu():
     """Reference-style C++ code through include/circlasso_b200.hpp on the GPU."""
     import os
