@@ -185,9 +185,9 @@ F16_DENSE_TFLOPS = 2250.0   # B200 dense fp16/bf16 tensor peak (same guide; MEAS
 
 
 def tc_f16(n):
-    """The tcgen05 kernel uses fp16 operands (2-term split) for n >= 2^19, 3xTF32 below (CLB_TC_F16 forces)."""
+    """The tcgen05 kernel uses fp16 operands (2-term split) for n >= 2^18, 3xTF32 below (CLB_TC_F16 forces)."""
     v = os.environ.get("CLB_TC_F16", "")
-    return (v not in ("", "0")) if v else n >= (1 << 19)
+    return (v not in ("", "0")) if v else n >= (1 << 18)
 
 
 def tc_peak(n):

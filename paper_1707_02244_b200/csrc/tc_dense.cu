@@ -20,7 +20,7 @@
 // the fp32 TMEM accumulator (the dropped Alo.Blo term is ~2^-22 relative):
 //  * 3xTF32 (kind::tf32): hi = x with the low 13 mantissa bits cleared (exact in TF32),
 //    lo = x - hi (exact in fp32).  Chunks hold 4 values; Hankel LBO = 64 B.
-//  * fp16 2-term split (kind::f16, n >= 2^19): x scaled by a power of two putting max|x| in
+//  * fp16 2-term split (kind::f16, n >= 2^18): x scaled by a power of two putting max|x| in
 //    [2^13, 2^14), hi = rn16(x), lo = rn16(x - hi).  Chunks hold 8 values, Hankel rows
 //    h[t0 + r .. t0 + r + 7] with LBO = 128 B; K = 16 per MMA (twice the rate, half the bytes).
 #include "tc_dense.cuh"
@@ -46,8 +46,8 @@ constexpr int kTileBytes = kRB * 16;
 #endif
 constexpr int kAStages = 2, kBStages = TC_BST;
 constexpr int kDrainers = 256;                 // warps 0-7: drain TMEM into fp32 registers
-constexpr int kProducers = 64;                 // warps 8-9: A slabs and Hankel tiles
-constexpr int kMmaWarp = (kDrainers + kProducers) / 32;  // warp 10: TMEM allocation, MMA issue
+constexpr int kProducers = 96;                 // warps 8-10: A slabs and Hankel tiles
+constexpr int kMmaWarp = (kDrainers + kProducers) / 32;  // warp 11: TMEM allocation, MMA issue
 constexpr int kTcThreads = kDrainers + kProducers + 32;
 constexpr int kOffB = kAStages * 2 * kSlabBytes;
 constexpr int kOffBar = kOffB + kBStages * 2 * kTileBytes;
@@ -505,13 +505,13 @@ ConvPlan make_tc_plan(int64_t n) {
 
 namespace {
 float* g_maxes[64] = {};  // per device: k_absmax2 output (2 x kMaxBlocks floats)
-// fp16 operands win where slabs are long (n = 2^20: 4.43 vs 6.96 ms; 2^19: 1.31 vs 1.74 ms); at
-// 2^18 they tie (0.51 ms) and below slab rebuilds make the fp16 producer the bottleneck.
-// CLB_TC_F16=0/1 forces either.
+// fp16 operands win from n = 2^18 (4.19 vs 6.97 ms at 2^20, 1.09 vs 1.94 at 2^19, 0.43 vs 0.51
+// at 2^18); below, slab rebuilds make the fp16 producers the bottleneck.  CLB_TC_F16=0/1 forces
+// either.
 bool use_f16(int64_t n) {
   const char* v = getenv("CLB_TC_F16");
   if (v && *v) return atoi(v) != 0;
-  return n >= (int64_t(1) << 19);
+  return n >= (int64_t(1) << 18);
 }
 }  // namespace
 
