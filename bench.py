@@ -218,8 +218,8 @@ def dense_kernel_info(n, ms):
 
 
 def ista_uses_tc(n):
-    """ISTA's direct engine embeds both sparse products in dense tcgen05 products for n >= 2^18."""
-    return n >= (1 << 18) and dense_uses_tc(n)
+    """ISTA's direct engine embeds both sparse products in dense tcgen05 products for n >= 2^17."""
+    return n >= (1 << 17) and dense_uses_tc(n)
 
 
 def admm_line(cl, torch, prob, local_rank, flush, steps=5, warmup=3):

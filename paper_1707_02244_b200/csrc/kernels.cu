@@ -1546,7 +1546,7 @@ ConvPlan make_dense_plan(int64_t n) {
   return make_plan(n, dense_R(n));
 }
 
-bool ista_uses_tc(int64_t n) { return n >= (int64_t(1) << 18) && make_dense_plan(n).tc; }
+bool ista_uses_tc(int64_t n) { return n >= (int64_t(1) << 17) && make_dense_plan(n).tc; }
 
 void launch_conv_dense(const ConvPlan& p, const float* h, const float* u, float* partial, cudaStream_t st) {
   if (p.tc) {

@@ -64,7 +64,7 @@ ConvPlan make_plan(int64_t n, int R);
 // n >= 2^15 unless CLB_NO_TC=1, else the FFMA kernel.  Pure host logic.
 ConvPlan make_dense_plan(int64_t n);
 // ISTA's direct engine embeds both sparse products in dense tensor-core products for
-// n >= 2^18 (where that beats the FFMA sparse kernels).  Pure host logic.
+// n >= 2^17 (where that beats the FFMA sparse kernels).  Pure host logic.
 bool ista_uses_tc(int64_t n);
 // [blo, bhi) in 32-position blocks covered by split `split` of a plan.
 void split_block_range(const ConvPlan& p, int split, int64_t* blo, int64_t* bhi);
