@@ -174,3 +174,32 @@ def test_sharded_iterations_match_single_process(world):
     for a, b in zip(outs_cover, outs_cover[1:]):
         assert a[1] == b[0]
     assert np.count_nonzero(single.x.numpy()) > 0
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_tensor_core_shard_ranges(world):
+    """Shard ranges when the direct products run on the tensor cores (power-of-two n >= 2^17 for
+    ISTA, >= 2^15 for cADMM; host logic only): outputs split by 128 x 256-output tiles, and an ISTA
+    rank's residual rows are exactly Omega within its outputs."""
+    for lg, kind in ((17, 0), (20, 0), (16, 1), (20, 1)):
+        n = 1 << lg
+        m = n // 4
+        rng = np.random.default_rng(lg)
+        omega = np.sort(rng.choice(n, m, replace=False)).astype(np.int64)
+
+        class P:
+            pass
+        p = P()
+        p.n, p.m, p.omega = n, m, omega
+        prev_o, prev_r = 0, 0
+        for r in range(world):
+            rows, outs = shard_ranges(kind, p, r, world)
+            assert outs[0] == prev_o and outs[0] % (128 * 256) == 0
+            prev_o = outs[1]
+            if kind == 0:
+                assert rows[0] == prev_r
+                assert rows == (np.searchsorted(omega, outs[0]), np.searchsorted(omega, outs[1]))
+                prev_r = rows[1]
+        assert prev_o == n
+        if kind == 0:
+            assert prev_r == m
