@@ -1518,6 +1518,7 @@ ConvPlan make_plan(int64_t n, int R) {
 }
 
 void conv_kernels_init() {
+  tc_dense_init();  // per device (its scale buffer is a device allocation; never inside a graph capture)
   static bool done = false;
   if (done) return;
   done = true;
@@ -1526,7 +1527,6 @@ void conv_kernels_init() {
     cudaMemcpyToSymbol(g_force_dense, &one, sizeof(int));
   }
   select_variants();
-  tc_dense_init();
   for (const auto& d : kDense)
     cudaFuncSetAttribute(reinterpret_cast<const void*>(d.fn), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d.smem);
   for (const auto& g : kGrad)
