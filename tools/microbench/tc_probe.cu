@@ -3,6 +3,9 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../../paper_1707_02244_b200/csrc \
 //        -o tc_probe tc_probe.cu ../../paper_1707_02244_b200/csrc/tc_dense.cu
 //   ./tc_probe [log2 n] [reps]
+// Environment: CLB_TC_F16=0/1 (operand format; default fp16 for n >= 2^18), CLB_TC_SPLITS=S.
+// Build flags used in the DESIGN experiments: -DTC_SPD=k (TF32 steps per drain; fp16 uses 2k).
+// The tensor-flop column counts 3 tensor flops per algorithmic flop for either format.
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
