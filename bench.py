@@ -180,8 +180,17 @@ def run_reference(args, w, rank):
     print(json.dumps(line), flush=True)
 
 
-TF32_DENSE_TFLOPS = 1100.0  # B200 dense TF32 tensor peak (/opt/skills/guides/B200_PROFILING.md; not in MEASURED_PEAKS.json)
-F16_DENSE_TFLOPS = 2250.0   # B200 dense fp16/bf16 tensor peak (same guide; MEASURED_PEAKS.json bf16 matmul: see bench line)
+def measured_peaks():
+    """Roofline denominators: the driver-written MEASURED_PEAKS.json (cuBLAS bf16 GEMM burst / sustained,
+    STREAM-style copy) -- else the B200_PROFILING.md fallback (1.59 PF burst, 1.4 PF sustained, 6.65 TB/s)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return {"bf16": float(d["bf16_tflops"]), "bf16_sustained": float(d.get("bf16_tflops_sustained", 0) or 0),
+                "hbm_gbs": float(d.get("hbm_gbs", 0) or 0), "source": "of measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        return {"bf16": 1590.0, "bf16_sustained": 1400.0, "hbm_gbs": 6650.0,
+                "source": "of fallback (B200_PROFILING.md; MEASURED_PEAKS.json absent)"}
 
 
 def tc_f16(n):
@@ -190,14 +199,20 @@ def tc_f16(n):
     return (v not in ("", "0")) if v else n >= (1 << 18)
 
 
-def tc_peak(n):
-    return F16_DENSE_TFLOPS if tc_f16(n) else TF32_DENSE_TFLOPS
+def tc_peak(n, peaks, sustained=False):
+    """Dense tensor peak of the kernel's MMA kind: kind::f16 runs at the bf16 rate; kind::tf32 at half of it."""
+    base = peaks["bf16_sustained"] if sustained and peaks["bf16_sustained"] else peaks["bf16"]
+    return base if tc_f16(n) else base / 2.0
+
+
+def tc_dtype(n):
+    return "f16x3-split/fp32-acc" if tc_f16(n) else "tf32x3-split/fp32-acc"
 
 
 def tc_note(n):
     return ("fp16 operands, power-of-two scaled, 2-term split (hi.hi + hi.lo + lo.hi, kind::f16)" if tc_f16(n) else
             "3xTF32 (hi.hi + hi.lo + lo.hi, kind::tf32)") + \
-        ": 3 tensor flops per algorithmic flop; achieved/frac count algorithmic flops"
+        ": 3 tensor flops per dense-product flop"
 
 
 def dense_uses_tc(n):
@@ -205,15 +220,16 @@ def dense_uses_tc(n):
     return n >= (1 << 15) and (n & (n - 1)) == 0 and os.environ.get("CLB_NO_TC", "0") in ("", "0")
 
 
-def dense_kernel_info(n, ms):
+def dense_kernel_info(n, ms, peaks):
     flops = 2.0 * n * n
     if dense_uses_tc(n):
+        pk = tc_peak(n, peaks)
         return {"kernel": "k_tc_dense", "ms": ms, "achieved_tflops": flops / (ms * 1e-3) / 1e12,
-                "bound": "tensor", "peak_tflops": tc_peak(n),
-                "frac": flops / (ms * 1e-3) / 1e12 / tc_peak(n),
+                "bound": "tensor", "peak_tflops": pk, "peak_source": peaks["source"],
+                "frac": flops / (ms * 1e-3) / 1e12 / pk,
                 "tensor_pipe_tflops": 3 * flops / (ms * 1e-3) / 1e12,
-                "tensor_pipe_frac": 3 * flops / (ms * 1e-3) / 1e12 / tc_peak(n),
-                "note": tc_note(n)}
+                "tensor_pipe_frac": 3 * flops / (ms * 1e-3) / 1e12 / pk,
+                "note": tc_note(n) + "; ms = CUDA-event time of the product inside the graph-replayed step"}
     return {"kernel": "k_conv_dense", "ms": ms, "achieved_tflops": flops / (ms * 1e-3) / 1e12, "bound": "fp32_ffma"}
 
 
@@ -222,7 +238,24 @@ def ista_uses_tc(n):
     return n >= (1 << 17) and dense_uses_tc(n)
 
 
-def admm_line(cl, torch, prob, local_rank, flush, steps=5, warmup=3):
+def timed_steps(st, stream, flush, steps, torch):
+    """`steps` graph-replayed iterations, L2 flushed before each (outside the events); per-step CUDA-event
+    times on the solver's stream and the per-phase times of each replay (in-graph event nodes)."""
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    phases = []
+    for i in range(steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            ev[i][0].record(stream)
+        st.step(1)
+        with torch.cuda.stream(stream):
+            ev[i][1].record(stream)
+        st.synchronize()
+        phases.append(st.phase_ms())
+    return [a.elapsed_time(b) for a, b in ev], phases
+
+
+def admm_line(cl, torch, prob, local_rank, flush, peaks, steps=5, warmup=3):
     """cADMM (the paper's CPADMM, the metric's "ADMM") on the same n=2^20 problem:
     device-timed iterations/s of the direct engine (3 dense circulant products
     per iteration, 6 n^2 flop) and the dense kernel's roofline fraction."""
@@ -232,23 +265,12 @@ def admm_line(cl, torch, prob, local_rank, flush, steps=5, warmup=3):
     sp = C.c_void_p()
     L.cl_solver_stream(st.handle, C.byref(sp))
     stream = torch.cuda.ExternalStream(sp.value)
+    st.profile(2)
     st.step(warmup)
     st.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
-    for i in range(steps):
-        with torch.cuda.stream(stream):
-            flush.zero_()
-            ev[i][0].record(stream)
-        st.step(1)
-        with torch.cuda.stream(stream):
-            ev[i][1].record(stream)
-    st.synchronize()
-    ms = sum(a.elapsed_time(b) for a, b in ev) / steps
-    st.profile(True)
-    st.step(1)
-    st.synchronize()
-    ph = st.phase_ms()
-    st.profile(False)
+    step_ms, phases = timed_steps(st, stream, flush, steps, torch)
+    ms = sum(step_ms) / steps
+    ph = [statistics.mean(p[i] for p in phases) for i in range(len(phases[0]))]
     n = prob.op.n()
     dense_ms = (ph[0] + ph[2] + ph[4]) / 3.0
     return {"value": 1e3 / ms, "unit": "iterations/s", "ms_per_step": ms, "steps": steps, "warmup": warmup,
@@ -256,7 +278,7 @@ def admm_line(cl, torch, prob, local_rank, flush, steps=5, warmup=3):
                         "(make_problem(2^20, 2^18, 2^12, 1), the config-3 problem)",
             "engine": "direct circulant products on tcgen05 tensor cores" if dense_uses_tc(n)
                       else "direct shift-indexed sm_100a kernels",
-            "dense_kernel": dense_kernel_info(n, dense_ms),
+            "dense_kernel": dense_kernel_info(n, dense_ms, peaks),
             "step_tflops": 6.0 * n * n / (ms * 1e-3) / 1e12, "phase_ms": ph}
 
 
@@ -338,11 +360,15 @@ def main():
     sp_stream = torch.cuda.ExternalStream(sp.value)
     flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")  # 256 MiB > 126 MB L2
 
+    # per-phase CUDA events recorded inside the timed steps themselves: event nodes in the captured step
+    # graph (mode 2); the sharded path launches its phases eagerly (mode 1)
+    st.profile(1 if sharded else 2)
     for _ in range(args.warmup):
         one_step()
     st.synchronize()
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    phase_ms = []
     if sharded:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -354,7 +380,8 @@ def main():
             one_step()
             with torch.cuda.stream(sp_stream):
                 ev[i][1].record(sp_stream)
-        st.synchronize()
+            st.synchronize()  # host sync between steps, outside the events: read this replay's phase times
+            phase_ms.append(st.phase_ms())
         torch.cuda.synchronize()
     if sharded:
         torch.distributed.barrier()
@@ -366,32 +393,33 @@ def main():
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
     value = 1e3 / ms_per_step  # iterations/s of the (single, sharded) solve
+    st.profile(0)
+    phase_mean = [statistics.mean(p[i] for p in phase_ms) for i in range(len(phase_ms[0]))]
 
-    # per-phase kernel durations (CUDA events on the solver stream, eager launches), outside the timed loop
-    st.profile(True)
-    phase_ms = []
-    for _ in range(3):
-        with torch.cuda.stream(sp_stream):
-            flush.zero_()
-        one_step()
-        st.synchronize()
-        phase_ms.append(st.phase_ms())
-    st.profile(False)
-
-    # dominant kernel (the residual, ~59% of the step, profiles/r1/launches_r1b.csv): live CUDA-event durations
+    # dominant kernel, timed inside the timed steps.  Phase windows: ISTA [residual product, gather, scatter +
+    # gradient product, update]; cADMM [C^T v, beta, B beta, x, C x, duals].  A tensor-core product's window
+    # also holds its k_absmax2 scale pre-pass (~1% of it), so kernel_ms slightly overstates the kernel.
+    n, m = w["n"], w["m"]
     if w["kind"] == "ista":
-        k_ms = statistics.mean(p[0] for p in phase_ms)
-        k_flops = 2.0 * w["m"] * w["n"] / world
-        if ista_uses_tc(w["n"]):
-            k_name = "k_tc_dense"  # residual = dense tensor-core product C x, rows Omega gathered
+        prod_idx = [0, 2]
+        useful = 2.0 * m * n / world  # per launch: residual m rows x n, gradient n outputs x m rows
+        if ista_uses_tc(n):
+            k_name = "k_tc_dense"  # both sparse products embedded in dense tensor-core products
         else:
-            k_name = "k_res_s" if w["n"] >= (1 << 17) else "k_conv_residual"  # large-n / small-n residual kernel
+            k_name = "k_res_s" if n >= (1 << 17) else "k_conv_residual"
+            prod_idx = [0]
     else:
-        k_ms = statistics.mean(p[0] for p in phase_ms)
-        k_flops = 2.0 * w["n"] * w["n"] / world
-        k_name = "k_tc_dense" if dense_uses_tc(w["n"]) else "k_conv_dense"
-    peak = tc_peak(w["n"]) if k_name == "k_tc_dense" else cl.ffma_peak_tflops(local_rank)
-    achieved = k_flops / (k_ms * 1e-3) / 1e12
+        prod_idx = [0, 2, 4]
+        useful = 2.0 * n * n / world
+        k_name = "k_tc_dense" if dense_uses_tc(n) else "k_conv_dense"
+    k_ms = statistics.mean(phase_mean[i] for i in prod_idx)
+    peaks = measured_peaks()
+    if k_name == "k_tc_dense":
+        peak, peak_source = tc_peak(n, peaks), "bf16_tflops " + peaks["source"] + \
+            ("" if tc_f16(n) else "; kind::tf32 = half the bf16 rate")
+    else:
+        peak, peak_source = cl.ffma_peak_tflops(local_rank), "live FFMA microbenchmark (cl_ffma_peak)"
+    achieved = useful / (k_ms * 1e-3) / 1e12
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
@@ -494,7 +522,7 @@ def main():
 
     admm = recovery = None
     if not sharded and w["kind"] == "ista" and w["n"] == (1 << 20) and not args.quick:
-        admm = admm_line(cl, torch, prob, local_rank, flush)
+        admm = admm_line(cl, torch, prob, local_rank, flush, peaks)
         recovery = recovery_line(cl, prob, local_rank)
 
     cpu = None
@@ -522,7 +550,8 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (make_problem, seeded)",
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": tc_dtype(n) if k_name == "k_tc_dense" else "f32", "data": "synthetic (make_problem, seeded)",
             "config": {"workload": w["desc"], "n": w["n"], "m": w["m"], "k": w["k"], "seed": w["seed"],
                        "engine": ("direct circulant products on tcgen05 tensor cores" +
                                   (" (ISTA's sparse products embedded in dense ones)" if w["kind"] == "ista" else "")
@@ -531,20 +560,29 @@ def main():
                        "l2": "flushed (256 MiB) between steps",
                        "parallelism": f"row/output shards x{world}" if sharded else "single GPU"},
             "roofline": {"bound": "tensor" if k_name == "k_tc_dense" else "fp32_ffma", "kernel": k_name,
-                         "achieved": achieved, "peak": peak,
-                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                         "peak_source": (("B200 dense fp16 2.25 PF" if tc_f16(w["n"]) else "B200 dense TF32 1.1 PF") +
-                                         " (B200_PROFILING.md); " + tc_note(w["n"]) if k_name == "k_tc_dense" else
-                                         "live FFMA microbenchmark (cl_ffma_peak); MEASURED_PEAKS.json has no FP32 entry"),
-                         **({"dense_product_tflops": 2.0 * w["n"] * w["n"] / world / (k_ms * 1e-3) / 1e12,
-                             "tensor_pipe_tflops": 6.0 * w["n"] * w["n"] / world / (k_ms * 1e-3) / 1e12,
-                             "tensor_pipe_frac": 6.0 * w["n"] * w["n"] / world / (k_ms * 1e-3) / 1e12 / peak,
-                             "work_note": "the kernel computes the dense product C x (2 n^2 flop; ISTA needs the m rows "
-                                          "of Omega, 2 m n) with 3 tensor flops per flop"}
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                         "traffic": traffic, "peak_source": peak_source,
+                         "work_per_launch": f"{useful:.6g} flop = algorithmic (SURVEY 8d): " +
+                                            ("2 m n per product (residual m rows x n, gradient n x m)"
+                                             if w["kind"] == "ista" else "2 n^2 per dense product"),
+                         "kernel_ms": k_ms,
+                         "kernel_ms_source": "CUDA events in the graph-replayed timed steps (event nodes captured "
+                                             "around each product), mean over products and steps",
+                         "kernel_share_of_step": len(prod_idx) * k_ms / ms_per_step,
+                         **({"frac_sustained_peak": achieved / tc_peak(n, peaks, sustained=True),
+                             "dense_product": {"flop": 2.0 * n * n / world,
+                                               "tflops": 2.0 * n * n / world / (k_ms * 1e-3) / 1e12,
+                                               "frac": 2.0 * n * n / world / (k_ms * 1e-3) / 1e12 / peak},
+                             "tensor_pipe": {"flop": 6.0 * n * n / world,
+                                             "tflops": 6.0 * n * n / world / (k_ms * 1e-3) / 1e12,
+                                             "frac": 6.0 * n * n / world / (k_ms * 1e-3) / 1e12 / peak},
+                             "work_note": ("each product runs the dense C u (2 n^2 flop" +
+                                           ("; ISTA needs the m rows of Omega or the m inputs of P^T r, 2 m n"
+                                            if w["kind"] == "ista" else "") +
+                                           ") as 3 tensor-core MMAs per flop: " + tc_note(n))}
                             if k_name == "k_tc_dense" else {}),
-                         "step_tflops": algorithmic_flops(w) / (ms_per_step * 1e-3) / 1e12,
-                         "step_frac": algorithmic_flops(w) / (ms_per_step * 1e-3) / 1e12 / peak,
-                         "phase_ms": [statistics.mean(p[i] for p in phase_ms) for i in range(len(phase_ms[0]))]},
+                         "step_tflops": algorithmic_flops(w) / world / (ms_per_step * 1e-3) / 1e12,
+                         "phase_ms": phase_mean},
             "clocks": clocks.summary(),
             # per step: ISTA 2 products + gather/scatter + update; cADMM 3 products + 3 epilogues; each
             # fp16 tensor-core product adds its k_absmax2 scale pass

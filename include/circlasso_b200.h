@@ -161,8 +161,9 @@ cl_status cl_solver_last_step_ms(cl_solver* s, double* ms);
  * ISTA: [residual, residual_reduce, gradient, update]; cADMM: [ctv, beta,
  * bbeta, x, cx, duals].  `count` in/out. */
 cl_status cl_solver_phase_ms(cl_solver* s, double* ms, int* count);
-/* Enable per-phase event timing (default off). */
-cl_status cl_solver_profile(cl_solver* s, int enable);
+/* Per-phase event timing: 0 off (default), 1 eager launches, 2 event nodes
+ * captured inside the step's CUDA graph (phase times of the replayed step). */
+cl_status cl_solver_profile(cl_solver* s, int mode);
 
 /* ---- sharded solve (one process per GPU; row/output-range sharding) -----
  * The caller owns the collective: between phases it all-gathers the

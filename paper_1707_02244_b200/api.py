@@ -553,6 +553,9 @@ class _DeviceState:
 
     def set(self, name: str, values):
         values = _f64(values)
+        size = self._m if name in ("r", "y") else self._n
+        if len(values) != size:  # the C side reads exactly `size` doubles
+            raise DimensionError(f"set('{name}'): expected {size} values, got {len(values)}")
         _check(lib.cl_solver_set(self._h, name.encode(), _pd(values)))
 
     def set_truth(self, truth):
@@ -576,7 +579,9 @@ class _DeviceState:
         _check(lib.cl_solver_last_step_ms(self._h, C.byref(v)))
         return v.value
 
-    def profile(self, enable: bool = True):
+    def profile(self, enable=True):
+        """Per-phase CUDA events: False/0 off, True/1 eager launches, 2 = event nodes inside the captured
+        step graph (times the graph-replayed step itself)."""
         _check(lib.cl_solver_profile(self._h, int(enable)))
 
     def phase_ms(self):

@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "fft4.cuh"
+#include "kernels.cuh"
 
 namespace clb {
 namespace {
@@ -492,9 +493,8 @@ static size_t rows_smem_t() { return static_cast<size_t>(row_count(N)) * row_pit
 #define CLB_FFT4_SIZES(X) X(128) X(256) X(512) X(1024) X(2048) X(4096) X(8192)
 
 void fft4_init_attributes() {
-  static bool done = false;
-  if (done) return;
-  done = true;
+  static std::atomic<uint64_t> devs{0};
+  if (!first_use_on_device(devs)) return;
   // columns are at most 2048 long (fft4_plan); longer column kernels are never launched
 #define CLB_ATTR(N)                                                                                             \
   if (N <= 2048) {                                                                                              \
@@ -553,9 +553,8 @@ cudaError_t launch_small_fft_ista(int64_t n, int64_t m, const float2* Hp, const 
   switch (n) {
 #define CLB_SMALL_CASE(N)                                                                                   \
   case N: {                                                                                                 \
-    static bool attr = false;                                                                               \
-    if (!attr) {                                                                                            \
-      attr = true;                                                                                          \
+    static std::atomic<uint64_t> attr{0};                                                                   \
+    if (first_use_on_device(attr)) {                                                                        \
       cudaFuncSetAttribute(k_small_fft_ista<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,                \
                            static_cast<int>(small_fft_smem<N>()));                                          \
     }                                                                                                       \
@@ -581,9 +580,8 @@ cudaError_t launch_small_fft_cadmm(int64_t n, const float2* Hc, const float2* Hb
   switch (n) {
 #define CLB_SMALL_CASE(N)                                                                                   \
   case N: {                                                                                                 \
-    static bool attr = false;                                                                               \
-    if (!attr) {                                                                                            \
-      attr = true;                                                                                          \
+    static std::atomic<uint64_t> attr{0};                                                                   \
+    if (first_use_on_device(attr)) {                                                                        \
       cudaFuncSetAttribute(k_small_fft_cadmm<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,               \
                            static_cast<int>(small_fft_cadmm_smem<N>()));                                    \
     }                                                                                                       \

@@ -1518,10 +1518,9 @@ ConvPlan make_plan(int64_t n, int R) {
 }
 
 void conv_kernels_init() {
-  tc_dense_init();  // per device (its scale buffer is a device allocation; never inside a graph capture)
-  static bool done = false;
-  if (done) return;
-  done = true;
+  tc_dense_init();
+  static std::atomic<uint64_t> devs{0};
+  if (!first_use_on_device(devs)) return;
   if (const char* v = getenv("CLB_FORCE_DENSE")) {
     const int one = atoi(v);
     cudaMemcpyToSymbol(g_force_dense, &one, sizeof(int));
@@ -1548,16 +1547,14 @@ ConvPlan make_dense_plan(int64_t n) {
 
 bool ista_uses_tc(int64_t n) { return n >= (int64_t(1) << 17) && make_dense_plan(n).tc; }
 
-void launch_conv_dense(const ConvPlan& p, const float* h, const float* u, float* partial, cudaStream_t st) {
-  if (p.tc) {
-    launch_tc_dense(p, h, u, partial, st);
-    return;
-  }
+cudaError_t launch_conv_dense(const ConvPlan& p, const float* h, const float* u, float* partial, cudaStream_t st) {
+  if (p.tc) return launch_tc_dense(p, h, u, partial, st);
   const int64_t units = (p.tile_hi - p.tile_lo) * p.splits;
-  if (units <= 0) return;
+  if (units <= 0) return cudaSuccess;
   select_variants();
   const DenseVariant& d = kDense[dense_index(p.n)];
   d.fn<<<static_cast<unsigned>(units), kThreads, d.smem, st>>>(h, u, p.n, p.chunks, p.splits, p.tile_lo, partial);
+  return cudaGetLastError();
 }
 
 void launch_conv_rows(const ConvPlan& p, const float* h, const int* omega32, const float* rvals, const int* rowstart,
@@ -1626,9 +1623,8 @@ cudaError_t launch_coop_cadmm(int64_t n, const float* hc, const float* hbr, cons
   switch (n) {
 #define CLB_COOP(N, R)                                                                                      \
   case N: {                                                                                                 \
-    static bool attr = false;                                                                               \
-    if (!attr) {                                                                                            \
-      attr = true;                                                                                          \
+    static std::atomic<uint64_t> attr{0};                                                                   \
+    if (first_use_on_device(attr)) {                                                                        \
       cudaFuncSetAttribute(k_coop_cadmm<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coop_smem<R>()); \
     }                                                                                                       \
     return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_coop_cadmm<R>), grid, block, args,   \
@@ -1652,9 +1648,8 @@ cudaError_t launch_coop_ista(int64_t n, int64_t m, const float* hc, const float*
   switch (n) {
 #define CLB_COOPI(N, R)                                                                                     \
   case N: {                                                                                                 \
-    static bool attr = false;                                                                               \
-    if (!attr) {                                                                                            \
-      attr = true;                                                                                          \
+    static std::atomic<uint64_t> attr{0};                                                                   \
+    if (first_use_on_device(attr)) {                                                                        \
       cudaFuncSetAttribute(k_coop_ista<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coop_ista_smem<R>()); \
     }                                                                                                       \
     return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_coop_ista<R>), grid, block, args,    \

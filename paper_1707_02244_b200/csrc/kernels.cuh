@@ -21,10 +21,21 @@
 // solver updates.
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace clb {
+
+// Kernel function attributes (max dynamic shared memory, cluster sizes) are set per device.
+// True the first time it is called for the current device with this flag word; callers set the
+// attributes then.  (A process may drive several devices through SolverConfig::device.)
+inline bool first_use_on_device(std::atomic<uint64_t>& flags) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return true;
+  const uint64_t bit = uint64_t(1) << dev;
+  return (flags.fetch_or(bit) & bit) == 0;
+}
 
 constexpr int kWarps = 4;
 constexpr int kThreads = kWarps * 32;   // 128
@@ -57,6 +68,9 @@ struct ConvPlan {
   int64_t tile_lo = 0, tile_hi = 0;    // shard: tiles run by this rank
   int split_lo = 0, split_hi = 0;      // shard: splits run by this rank (residual)
   bool tc = false;                     // dense product on the tensor cores (tc_dense.cu)
+  // tensor-core fp16 path: device scratch of tc_scratch_floats() floats for the operand scales,
+  // owned by the caller (one per solver / product; never shared between streams)
+  float* tc_scratch = nullptr;
 };
 
 ConvPlan make_plan(int64_t n, int R);
@@ -91,7 +105,7 @@ struct EpiArgs {
 };
 
 // partial[split][i] for the plan's shard tiles (dense u).  plan from make_plan(n, kRDense).
-void launch_conv_dense(const ConvPlan& p, const float* h, const float* u, float* partial, cudaStream_t st);
+cudaError_t launch_conv_dense(const ConvPlan& p, const float* h, const float* u, float* partial, cudaStream_t st);
 // gradient: u = P^T r given as rows (omega32 sorted, rvals), rowstart[chunk].  plan R = kRGrad.
 void launch_conv_rows(const ConvPlan& p, const float* h, const int* omega32, const float* rvals,
                       const int* rowstart, float* partial, cudaStream_t st);

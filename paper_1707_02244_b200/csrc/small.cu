@@ -23,6 +23,7 @@
 #include <cstdlib>
 
 #include "small.cuh"
+#include "kernels.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -286,10 +287,9 @@ k_small_ista(const float* __restrict__ hc, const int* __restrict__ omega, const 
 template <int N, int CL>
 cudaError_t launch_t(const float* hc, const int* omega, const float* y, float* x, float* r, float* delta, int m,
                      float tau, float thr, int iters, cudaStream_t st) {
-  static bool attr = false;
+  static std::atomic<uint64_t> attr{0};
   const size_t smem = small_smem<N, CL>();
-  if (!attr) {
-    attr = true;
+  if (first_use_on_device(attr)) {
     cudaFuncSetAttribute(k_small_ista<N, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (CL > 8) cudaFuncSetAttribute(k_small_ista<N, CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   }

@@ -24,6 +24,7 @@
 #include "fft4.cuh"
 #include "small.cuh"
 #include "kernels.cuh"
+#include "tc_dense.cuh"
 
 namespace clb {
 void gen_sparse_signal(int64_t n, int64_t k, uint64_t seed, double* values, int64_t* support);
@@ -156,7 +157,9 @@ struct Solver {
   int64_t t = 0;
   int rank = 0, world = 1;
   bool has_truth = false;
-  bool profile = false;
+  // per-phase CUDA events: 0 off, 1 eager launches (no graph), 2 event nodes inside the captured
+  // step graph (the timed configuration itself: cl_solver_phase_ms reads the last replay)
+  int profile = 0;
   cudaStream_t st = nullptr;
   // Destroys st after every DevBuf member (declared below) has queued its free.
   struct StreamOwner {
@@ -179,6 +182,7 @@ struct Solver {
   DevBuf<float> y, r, x, delta;    // ISTA
   DevBuf<float> d, pty, z, nu, mu, v, beta;  // cADMM (x shared)
   DevBuf<float> partial, truth;
+  DevBuf<float> tcs;  // this solver's tensor-core operand-scale scratch (ConvPlan::tc_scratch)
   DevBuf<float2> chat, bhat, F0, F1;  // FFT engine: spectra of c~ (and of B), work buffers
   bool fft = false;
   // FFT length: n for power-of-two n; otherwise the next power of two >= 2n - 1, with the circulant
@@ -244,8 +248,20 @@ struct Solver {
     rowstart.upload(rowstart_host.data(), rowstart_host.size(), st);
   }
 
+  void attach_tc_scratch() {
+    if (!plan.tc) return;
+    tcs.alloc(tc_scratch_floats(), st);
+    plan.tc_scratch = tcs.p;
+    if (rplan.tc) rplan.tc_scratch = tcs.p;
+  }
+
   void set_shard(int rk, int ws) {
     if (fft && ws != 1) raise(CL_EPARAM, "cl_solver_shard: the FFT engine runs unsharded (replicas only)");
+    if (graph) {  // the captured step covers the previous shard's ranges
+      CU(cudaStreamSynchronize(st));
+      CU(cudaGraphExecDestroy(graph));
+      graph = nullptr;
+    }
     rank = rk;
     world = ws;
     shard_ranges(kind, n, omega_host.data(), m, rk, ws, &plan, &rplan, &out_lo, &out_hi, &row_lo, &row_hi);
@@ -363,6 +379,7 @@ struct Solver {
     ista_tc = !fft && ista_uses_tc(n);
     plan = ista_tc ? make_dense_plan(n) : make_plan(n, grad_R(n));
     rplan = ista_tc ? plan : make_plan(n, res_R(n));
+    attach_tc_scratch();
     hc.alloc(static_cast<size_t>(n), st);
     hcr.alloc(static_cast<size_t>(n), st);
     if (dev) {
@@ -541,6 +558,7 @@ struct Solver {
     scale = normalization_from(dev ? device_spectrum(c) : spectral_norm(c, n), yh);
     if (!dev) init_device();
     plan = make_dense_plan(n);
+    attach_tc_scratch();
     hc.alloc(static_cast<size_t>(n), st);
     hcr.alloc(static_cast<size_t>(n), st);
     hbr.alloc(static_cast<size_t>(n), st);
@@ -629,7 +647,7 @@ struct Solver {
   void ista_residual() {
     mark(0);
     if (ista_tc) {  // C x on the tensor cores, rows Omega gathered in the epilogue
-      launch_conv_dense(plan, hcr.p, x.p, partial.p, st);
+      CU(launch_conv_dense(plan, hcr.p, x.p, partial.p, st));
       mark(1);
       EpiArgs a;
       a.partial = partial.p;
@@ -658,7 +676,7 @@ struct Solver {
   void ista_gradient(int want) {
     if (ista_tc) {  // C^T P^T r: scatter r (all rows, after any exchange), dense product
       launch_scatter_real(r.p, omega32.p, ud.p, m, st);
-      launch_conv_dense(plan, hc.p, ud.p, partial.p, st);
+      CU(launch_conv_dense(plan, hc.p, ud.p, partial.p, st));
     } else {
       launch_conv_rows(plan, hc.p, omega32.p, r.p, rowstart.p, partial.p, st);
     }
@@ -674,7 +692,7 @@ struct Solver {
   }
   void admm_beta_phase() {
     mark(0);
-    launch_conv_dense(plan, hc.p, v.p, partial.p, st);
+    CU(launch_conv_dense(plan, hc.p, v.p, partial.p, st));
     mark(1);
     EpiArgs a = base_args(0);
     a.beta = beta.p;
@@ -686,7 +704,7 @@ struct Solver {
     mark(2);
   }
   void admm_x_phase() {
-    launch_conv_dense(plan, hbr.p, beta.p, partial.p, st);
+    CU(launch_conv_dense(plan, hbr.p, beta.p, partial.p, st));
     mark(3);
     EpiArgs a = base_args(0);
     a.x = x.p;
@@ -694,7 +712,7 @@ struct Solver {
     mark(4);
   }
   void admm_dual_phase(int want) {
-    launch_conv_dense(plan, hcr.p, x.p, partial.p, st);
+    CU(launch_conv_dense(plan, hcr.p, x.p, partial.p, st));
     mark(5);
     EpiArgs a = base_args(want);
     a.x = x.p;
@@ -922,7 +940,7 @@ struct Solver {
       const char* v = getenv("CLB_NO_GRAPH");
       return v && v[0] == '1';
     }();
-    return !off && world == 1 && !profile;  // per-phase event timing runs eagerly
+    return !off && world == 1 && profile != 1;  // mode-1 per-phase timing runs eagerly
   }
 
   void build_graph() {
@@ -957,50 +975,49 @@ struct Solver {
     return kind == CL_KIND_CADMM && !fft && world == 1 && !profile && coop_cadmm_supported(n);
   }
 
-  void step(int64_t iters) {
-    if (iters > 0 && use_coop_ista()) {
-      CU(cudaEventRecord(step_ev[0], st));
+  // One persistent launch of `it` unchecked iterations (small n), if this solver has such a path.
+  bool persistent_launch(int it) {
+    if (use_coop_ista()) {
       CU(launch_coop_ista(n, m, hc.p, hcr.p, omega32.p, y.p, x.p, r.p, delta.p, partial.p, static_cast<float>(tau),
-                          static_cast<float>(thr), static_cast<int>(iters), st));
-      t += iters;
-      CU(cudaEventRecord(step_ev[1], st));
-      return;
-    }
-    if (iters > 0 && use_coop_cadmm()) {
-      CU(cudaEventRecord(step_ev[0], st));
+                          static_cast<float>(thr), it, st));
+    } else if (use_coop_cadmm()) {
       CU(launch_coop_cadmm(n, hc.p, hbr.p, hcr.p, d.p, pty.p, x.p, z.p, nu.p, mu.p, v.p, beta.p, partial.p,
                            static_cast<float>(cfg.rho), static_cast<float>(cfg.sigma), static_cast<float>(cfg.tau1),
-                           static_cast<float>(cfg.tau2), static_cast<float>(thr), static_cast<int>(iters), st));
-      t += iters;
-      CU(cudaEventRecord(step_ev[1], st));
-      return;
-    }
-    if (iters > 0 && use_small_fft()) {
-      CU(cudaEventRecord(step_ev[0], st));
+                           static_cast<float>(cfg.tau2), static_cast<float>(thr), it, st));
+    } else if (use_small_fft()) {
       if (kind == CL_KIND_ISTA)
         CU(launch_small_fft_ista(n, m, chatS.p, twS.p, omega32.p, y.p, x.p, r.p, delta.p, static_cast<float>(tau),
-                                 static_cast<float>(thr), static_cast<int>(iters), st));
+                                 static_cast<float>(thr), it, st));
       else
         CU(launch_small_fft_cadmm(n, chatS.p, bhatS.p, twS.p, d.p, pty.p, x.p, z.p, nu.p, mu.p, v.p, beta.p,
                                   static_cast<float>(cfg.rho), static_cast<float>(cfg.sigma),
                                   static_cast<float>(cfg.tau1), static_cast<float>(cfg.tau2),
-                                  static_cast<float>(thr), static_cast<int>(iters), st));
-      t += iters;
-      CU(cudaEventRecord(step_ev[1], st));
-      return;
-    }
-    if (iters > 0 && use_small()) {
-      CU(cudaEventRecord(step_ev[0], st));
+                                  static_cast<float>(thr), it, st));
+    } else if (use_small()) {
       CU(launch_small_ista(n, m, hc.p, omega32.p, y.p, x.p, r.p, delta.p, static_cast<float>(tau),
-                           static_cast<float>(thr), static_cast<int>(iters), st));
+                           static_cast<float>(thr), it, st));
+    } else {
+      return false;
+    }
+    return true;
+  }
+
+  void step(int64_t iters) {
+    if (iters > 0 && (use_coop_ista() || use_coop_cadmm() || use_small_fft() || use_small())) {
+      // the persistent kernels count iterations in int: longer requests run as several launches
+      constexpr int64_t kMaxLaunchIters = int64_t(1) << 30;
+      CU(cudaEventRecord(step_ev[0], st));
+      for (int64_t done = 0; done < iters; done += kMaxLaunchIters)
+        persistent_launch(static_cast<int>(std::min(kMaxLaunchIters, iters - done)));
       t += iters;
       CU(cudaEventRecord(step_ev[1], st));
       return;
     }
-    if (iters > 0 && use_graph()) build_graph();
+    const bool graphed = iters > 0 && use_graph();
+    if (graphed) build_graph();
     CU(cudaEventRecord(step_ev[0], st));
     for (int64_t k = 0; k < iters; ++k) {
-      if (graph) {
+      if (graphed) {
         CU(cudaGraphLaunch(graph, st));
         ++t;
       } else {
@@ -1145,14 +1162,16 @@ struct ScratchProduct {
     std::vector<float> cf = to_f32(c, n);
     if (!transpose) cf = reversed(cf);  // C x = conv(c_rev, x)
     const std::vector<float> xf = to_f32(xin, n);
-    DevBuf<float> h, u, part, o;
+    DevBuf<float> h, u, part, o, scr;
+    scr.alloc(tc_scratch_floats());
+    p.tc_scratch = scr.p;
     h.alloc(static_cast<size_t>(n));
     h.upload(cf.data(), cf.size(), st);
     u.alloc(static_cast<size_t>(n));
     u.upload(xf.data(), xf.size(), st);
     part.alloc(static_cast<size_t>(p.splits * n));
     o.alloc(static_cast<size_t>(n));
-    launch_conv_dense(p, h.p, u.p, part.p, st);
+    CU(launch_conv_dense(p, h.p, u.p, part.p, st));
     EpiArgs a;
     a.partial = part.p;
     a.splits = p.splits;
@@ -1352,7 +1371,7 @@ cl_status cl_matvec_scheme_bench(int device, int64_t n, int scheme, int repeats,
   CU(cudaEventCreate(&g.e[0]));
   CU(cudaEventCreate(&g.e[1]));
   const size_t nn = static_cast<size_t>(n);
-  DevBuf<float> h, x, out, part, M;
+  DevBuf<float> h, x, out, part, M, scr;
   const std::vector<float> xf = to_f32(xin.data(), n);
   x.alloc(nn, st);
   x.upload(xf.data(), nn, st);
@@ -1360,6 +1379,8 @@ cl_status cl_matvec_scheme_bench(int device, int64_t n, int scheme, int repeats,
   ConvPlan plan;
   if (scheme == 0) {
     plan = make_dense_plan(n);
+    scr.alloc(tc_scratch_floats(), st);
+    plan.tc_scratch = scr.p;
     const std::vector<float> crf = reversed(to_f32(row.data(), n));  // C x = conv(c_rev, x)
     h.alloc(nn, st);
     h.upload(crf.data(), nn, st);
@@ -1376,7 +1397,7 @@ cl_status cl_matvec_scheme_bench(int device, int64_t n, int scheme, int repeats,
   for (int rep = 0; rep < repeats; ++rep) {
     CU(cudaEventRecord(g.e[0], st));
     if (scheme == 0) {
-      launch_conv_dense(plan, h.p, x.p, part.p, st);
+      CU(launch_conv_dense(plan, h.p, x.p, part.p, st));
       EpiArgs a;
       a.partial = part.p;
       a.splits = plan.splits;
@@ -1632,6 +1653,12 @@ cl_status cl_solver_set(cl_solver* h, const char* field, const double* in) {
   int64_t len = 0;
   const std::string f(field ? field : "");
   float* p = s.field_ptr(f, &len);
+  if (!in) raise(CL_EPARAM, "cl_solver_set: null input");
+  // Operator rows with derived device state cannot be rewritten in place: the FFT engine's
+  // spectra come from c (and B's), and cADMM's B row is the Gram inverse of c.
+  if (f == "c" && (s.fft || s.kind == CL_KIND_CADMM))
+    raise(CL_EPARAM, "cl_solver_set: 'c' is fixed at setup for FFT-engine and cADMM solvers (derived spectra / B)");
+  if (f == "b" && s.fft) raise(CL_EPARAM, "cl_solver_set: 'b' is fixed at setup for FFT-engine solvers");
   std::vector<float> tmp = to_f32(in, len);
   if (f == "b") tmp = reversed(tmp);
   if (f == "c") {  // keep the reversed copy coherent
@@ -1683,7 +1710,8 @@ cl_status cl_solver_profile(cl_solver* h, int enable) {
     CU(cudaGraphExecDestroy(s.graph));
     s.graph = nullptr;
   }
-  s.profile = enable != 0;
+  if (enable < 0 || enable > 2) raise(CL_EPARAM, "cl_solver_profile: mode is 0 (off), 1 (eager) or 2 (in-graph)");
+  s.profile = enable;
   CL_GUARD_END
 }
 

@@ -504,7 +504,6 @@ ConvPlan make_tc_plan(int64_t n) {
 }
 
 namespace {
-float* g_maxes[64] = {};  // per device: k_absmax2 output (2 x kMaxBlocks floats)
 // fp16 operands win from n = 2^18 (4.19 vs 6.97 ms at 2^20, 1.09 vs 1.94 at 2^19, 0.43 vs 0.51
 // at 2^18); below, slab rebuilds make the fp16 producers the bottleneck.  CLB_TC_F16=0/1 forces
 // either.
@@ -515,33 +514,33 @@ bool use_f16(int64_t n) {
 }
 }  // namespace
 
+size_t tc_scratch_floats() { return 2 * kMaxBlocks; }
+
 void tc_dense_init() {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  static bool done[64] = {};
-  if (dev < 0 || dev >= 64 || done[dev]) return;
-  done[dev] = true;
+  static std::atomic<uint64_t> devs{0};
+  if (!first_use_on_device(devs)) return;
   cudaFuncSetAttribute(reinterpret_cast<const void*>(k_tc_dense<false>), cudaFuncAttributeMaxDynamicSharedMemorySize,
                        kTcSmem);
   cudaFuncSetAttribute(reinterpret_cast<const void*>(k_tc_dense<true>), cudaFuncAttributeMaxDynamicSharedMemorySize,
                        kTcSmem);
-  cudaMalloc(&g_maxes[dev], 2 * kMaxBlocks * sizeof(float));
 }
 
-void launch_tc_dense(const ConvPlan& p, const float* h, const float* u, float* partial, cudaStream_t st) {
+// The fp16 path's k_absmax2 -> k_tc_dense hand-over goes through the caller's own scratch
+// (p.tc_scratch): two products on different streams never share it.
+cudaError_t launch_tc_dense(const ConvPlan& p, const float* h, const float* u, float* partial, cudaStream_t st) {
   const int64_t units = (p.tile_hi - p.tile_lo) * p.splits;
-  if (units <= 0) return;
+  if (units <= 0) return cudaSuccess;
   tc_dense_init();
   if (use_f16(p.n)) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    k_absmax2<<<kMaxBlocks, 256, 0, st>>>(h, u, p.n, g_maxes[dev]);
+    if (!p.tc_scratch) return cudaErrorInvalidValue;  // the plan's owner did not allocate tc_scratch_floats()
+    k_absmax2<<<kMaxBlocks, 256, 0, st>>>(h, u, p.n, p.tc_scratch);
     k_tc_dense<true><<<static_cast<unsigned>(units), kTcThreads, kTcSmem, st>>>(h, u, p.n, p.splits, p.tile_lo,
-                                                                                partial, g_maxes[dev]);
+                                                                                partial, p.tc_scratch);
   } else {
     k_tc_dense<false><<<static_cast<unsigned>(units), kTcThreads, kTcSmem, st>>>(h, u, p.n, p.splits, p.tile_lo,
                                                                                  partial, nullptr);
   }
+  return cudaGetLastError();
 }
 
 }  // namespace clb

@@ -22,6 +22,9 @@ bool tc_dense_supported(int64_t n);
 // Plan for the tensor-core kernel: tile = 128 * 256 outputs, splits over the block offsets.
 ConvPlan make_tc_plan(int64_t n);
 void tc_dense_init();
-void launch_tc_dense(const ConvPlan& p, const float* h, const float* u, float* partial, cudaStream_t st);
+// Floats of per-product scratch the fp16 operand path needs (ConvPlan::tc_scratch).
+size_t tc_scratch_floats();
+// Launch errors (including a missing scratch buffer) are returned, not deferred.
+cudaError_t launch_tc_dense(const ConvPlan& p, const float* h, const float* u, float* partial, cudaStream_t st);
 
 }  // namespace clb
