@@ -10,9 +10,10 @@ k=2^12 (make_problem(2^20, 2^18, 2^12, seed=1)), alpha=1e-4, tau=0.9
 problem is row/output-sharded across the ranks (strong scaling) with
 all-gathers over NCCL between the phases.
 
-Timing: W untimed warm-up iterations, then K iterations, each bracketed by
-CUDA events on the solver's stream; L2 is flushed (256 MiB write) between
-timed iterations outside the events.  Barrier + synchronize around the timed
+Timing: W untimed warm-up iterations, then K iterations queued back to back
+(no host synchronization inside the timed loop), each bracketed by CUDA
+events on the solver's stream; L2 is flushed (256 MiB write) between timed
+iterations on the same stream, outside the events.  Barrier + synchronize around the timed
 region, max over ranks.  `e2e` is the same metric through the public API
 (ista_run from host numpy buffers: setup, upload, K iterations, result
 download) timed on the host clock (sharded: setup + K sharded iterations +
@@ -239,10 +240,11 @@ def ista_uses_tc(n):
 
 
 def timed_steps(st, stream, flush, steps, torch):
-    """`steps` graph-replayed iterations, L2 flushed before each (outside the events); per-step CUDA-event
-    times on the solver's stream and the per-phase times of each replay (in-graph event nodes)."""
+    """`steps` graph-replayed iterations back to back (no host synchronization inside the timed loop), L2
+    flushed before each on the same stream (outside the per-step events); per-step CUDA-event times on the
+    solver's stream and the per-phase times of each replay (profile mode 2: in-graph event nodes re-pointed
+    to a per-replay slot, read after the loop)."""
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
-    phases = []
     for i in range(steps):
         with torch.cuda.stream(stream):
             flush.zero_()
@@ -250,9 +252,8 @@ def timed_steps(st, stream, flush, steps, torch):
         st.step(1)
         with torch.cuda.stream(stream):
             ev[i][1].record(stream)
-        st.synchronize()
-        phases.append(st.phase_ms())
-    return [a.elapsed_time(b) for a, b in ev], phases
+    st.synchronize()
+    return [a.elapsed_time(b) for a, b in ev], st.phase_history(steps)
 
 
 def admm_line(cl, torch, prob, local_rank, flush, peaks, steps=5, warmup=3):
@@ -372,6 +373,9 @@ def main():
     if sharded:
         torch.distributed.barrier()
     torch.cuda.synchronize()
+    # back to back: each step is queued behind the previous one with no host synchronization in between
+    # (the GPU never idles, so clocks and power are those of a sustained solve); L2 is flushed before every
+    # step on the same stream, outside the step's events
     with ClockSampler(local_rank) as clocks:
         for i in range(args.steps):
             with torch.cuda.stream(sp_stream):
@@ -380,11 +384,14 @@ def main():
             one_step()
             with torch.cuda.stream(sp_stream):
                 ev[i][1].record(sp_stream)
-            st.synchronize()  # host sync between steps, outside the events: read this replay's phase times
-            phase_ms.append(st.phase_ms())
+            if sharded:  # eager phases: per-step phase times need the step's events
+                st.synchronize()
+                phase_ms.append(st.phase_ms())
         torch.cuda.synchronize()
     if sharded:
         torch.distributed.barrier()
+    else:
+        phase_ms = st.phase_history(args.steps)
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(step_ms)
     if sharded:
@@ -566,8 +573,9 @@ def main():
                                             ("2 m n per product (residual m rows x n, gradient n x m)"
                                              if w["kind"] == "ista" else "2 n^2 per dense product"),
                          "kernel_ms": k_ms,
-                         "kernel_ms_source": "CUDA events in the graph-replayed timed steps (event nodes captured "
-                                             "around each product), mean over products and steps",
+                         "kernel_ms_source": "CUDA events of the timed steps themselves (event-record nodes captured "
+                                             "around each product, re-pointed to a per-replay slot), mean over "
+                                             "products and steps",
                          "kernel_share_of_step": len(prod_idx) * k_ms / ms_per_step,
                          **({"frac_sustained_peak": achieved / tc_peak(n, peaks, sustained=True),
                              "dense_product": {"flop": 2.0 * n * n / world,

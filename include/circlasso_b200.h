@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define CL_ABI_VERSION 2
+#define CL_ABI_VERSION 3
 
 /* errors.hpp:18-72 — one code per exception type, plus device failures. */
 typedef enum cl_status {
@@ -44,7 +44,9 @@ typedef enum cl_status {
 } cl_status;
 
 typedef enum cl_pairing { CL_PAIRING_LITERAL = 0, CL_PAIRING_PROXIMAL = 1 } cl_pairing; /* solvers.hpp:83 */
-typedef enum cl_kind { CL_KIND_ISTA = 0, CL_KIND_CADMM = 1 } cl_kind;
+/* ISTA (solvers.hpp:208-263), circulant ADMM (:337-415) and the dense ADMM
+ * baseline with its explicit n x n inverse (:267-327, the paper's PADMM). */
+typedef enum cl_kind { CL_KIND_ISTA = 0, CL_KIND_CADMM = 1, CL_KIND_ADMM = 2 } cl_kind;
 typedef enum cl_metric { CL_METRIC_MSE_VS_TRUTH = 0, CL_METRIC_ITERATE_CHANGE = 1 } cl_metric; /* solvers.hpp:130 */
 /* Product engine (SolverConfig::use_fft, solvers.hpp:123): the direct
  * shift-indexed kernels (the paper's OpenCL scheme, north star) or the
@@ -52,8 +54,7 @@ typedef enum cl_metric { CL_METRIC_MSE_VS_TRUTH = 0, CL_METRIC_ITERATE_CHANGE = 
  * linear convolution in the next power of two >= 2n-1). */
 typedef enum cl_engine { CL_ENGINE_DIRECT = 0, CL_ENGINE_FFT = 1 } cl_engine;
 
-/* SolverConfig, solvers.hpp:112-125 (use_fft -> engine; dense_cap has no
- * meaning here and is omitted). */
+/* SolverConfig, solvers.hpp:112-125 (use_fft -> engine). */
 typedef struct cl_config {
   double alpha;       /* l1 weight, default 1e-4 */
   double tau;         /* ISTA step, 0 = automatic 0.9 */
@@ -66,6 +67,7 @@ typedef struct cl_config {
   int32_t check_every;/* default 10 */
   int32_t pairing;    /* cl_pairing, default literal */
   int32_t engine;     /* cl_engine, default CL_ENGINE_DIRECT */
+  int64_t dense_cap;  /* largest n of the dense ADMM (CL_ECAPACITY above), default 4096 (circulant.hpp:31) */
 } cl_config;
 
 /* RecoveryReport, solvers.hpp:139-150 (final_x and the trace are returned
@@ -128,8 +130,10 @@ cl_status cl_partial_transpose_matvec(int device, int64_t n, int64_t m, const do
                                       double* out_n);                               /* :286-291 */
 
 /* ---- solver handles (IstaState/CadmmState + *_setup, solvers.hpp) ------- */
-/* ista_setup solvers.hpp:222-249 / cadmm_setup :359-395.  Validates exactly
- * where the reference throws; uploads the normalized operator to `device`. */
+/* ista_setup solvers.hpp:222-249 / cadmm_setup :359-395 / admm_setup
+ * :285-314 (kind CL_KIND_ADMM: G = A~^T A~ + rho I and its inverse B built in
+ * fp64 on the device; n <= cfg->dense_cap).  Validates exactly where the
+ * reference throws; uploads the normalized operator to `device`. */
 cl_status cl_solver_create(int kind, int64_t n, int64_t m, const double* c, const int64_t* omega,
                            const double* y, const cl_config* cfg, int device, cl_solver** out);
 void cl_solver_destroy(cl_solver* s);
@@ -147,7 +151,8 @@ cl_status cl_solver_step_checked(cl_solver* s, double* metric, int* nonfinite);
 cl_status cl_solver_run(cl_solver* s, cl_report* rep, double* final_x, int64_t* trace_iter,
                         double* trace_value, int64_t trace_cap);
 /* Device -> host copy of a state vector by name:
- * ISTA: "x","r","delta","c","y"; cADMM: "x","z","nu","mu","v","beta","c","b","d","pty". */
+ * ISTA: "x","r","delta","c","y"; cADMM: "x","z","nu","mu","v","beta","c","b","d","pty";
+ * dense ADMM: "x","z","u","rhs","aty" (n each) and "B" (n * n, row-major). */
 cl_status cl_solver_get(cl_solver* s, const char* field, double* out);
 /* Host -> device (tests, warm state). Same names. */
 cl_status cl_solver_set(cl_solver* s, const char* field, const double* in);
@@ -159,11 +164,16 @@ cl_status cl_solver_synchronize(cl_solver* s);
 cl_status cl_solver_last_step_ms(cl_solver* s, double* ms);
 /* Per-kernel device time of the last step (ms), by phase:
  * ISTA: [residual, residual_reduce, gradient, update]; cADMM: [ctv, beta,
- * bbeta, x, cx, duals].  `count` in/out. */
+ * bbeta, x, cx, duals]; dense ADMM: [primal, rhs].  `count` in/out. */
 cl_status cl_solver_phase_ms(cl_solver* s, double* ms, int* count);
 /* Per-phase event timing: 0 off (default), 1 eager launches, 2 event nodes
  * captured inside the step's CUDA graph (phase times of the replayed step). */
 cl_status cl_solver_profile(cl_solver* s, int mode);
+/* Mode 2 only: the per-phase times (ms) of each of the last graph replays,
+ * oldest first, ms[k * nphase + i]; up to 256 replays are kept, so a timed
+ * loop of back-to-back cl_solver_step(s, 1) calls needs no host
+ * synchronization to be timed phase by phase.  ms = NULL queries *steps. */
+cl_status cl_solver_phase_history(cl_solver* s, double* ms, int64_t max_steps, int64_t* steps, int* nphase);
 
 /* ---- sharded solve (one process per GPU; row/output-range sharding) -----
  * The caller owns the collective: between phases it all-gathers the
@@ -175,7 +185,8 @@ cl_status cl_solver_shard(cl_solver* s, int rank, int world);
 cl_status cl_solver_stream(cl_solver* s, void** cuda_stream);
 /* Phase-level stepping for sharded solves: phase ids as in cl_solver_phase_ms;
  * ISTA: 0 = residual (local rows), 1 = gradient+update (local outputs);
- * cADMM: 0 = beta, 1 = x, 2 = duals. */
+ * cADMM: 0 = beta, 1 = x, 2 = duals; dense ADMM (unsharded; padmm_phases,
+ * parallel.hpp:284-317): 0 = primal and dual update, 1 = right-hand side. */
 cl_status cl_solver_run_phase(cl_solver* s, int phase);
 /* Pure host helper (no device needed): the output range [out_lo, out_hi) and,
  * for ISTA, the residual row range [row_lo, row_hi) owned by shard `rank`. */

@@ -39,6 +39,7 @@
 #include <limits>
 #include <numeric>
 #include <random>
+#include <sstream>
 #include <string>
 #include <thread>
 #include <vector>
@@ -523,6 +524,126 @@ static int cadmm_step_fft(Cadmm& st) {
   return OK;
 }
 
+// ---------------------------------------------------------------------------
+// Dense ADMM — solvers.hpp:267-327 (AdmmState, admm_setup, admm_step), phases
+// parallel.hpp:284-317 (padmm_phases), run solvers.hpp:497-514.  The paper's
+// dense baseline: (A^T A + rho I)^-1 stored as an explicit n x n matrix.
+// ---------------------------------------------------------------------------
+struct Admm {
+  int64_t n = 0, m = 0;
+  std::vector<double> B;    // n x n row-major, (A~^T A~ + rho I)^-1
+  std::vector<double> aty;  // A~^T y~
+  double rho = 0, threshold = 0, s = 1.0;
+  std::vector<double> x, z, u, rhs;
+  long t = 0;
+};
+
+// admm_setup solvers.hpp:285-314.  The reference factors the Gram matrix with
+// Eigen::LLT and solves against the identity; restated as a plain Cholesky
+// (lower L, G = L L^T) and one forward + back substitution per column.
+static int admm_setup(Admm& st, int64_t n, int64_t m, const double* c, const int64_t* omega, const double* y,
+                      double alpha, double rho, int64_t dense_cap, int threads) {
+  if (int rc = check_mask(omega, m, n)) return rc;
+  if (n > dense_cap) {
+    std::ostringstream msg;
+    msg << "admm_setup: n = " << n << " exceeds the dense cap " << dense_cap;
+    return fail(ECAPACITY, msg.str());
+  }
+  if (!(rho > 0.0)) return fail(EPARAM, "admm_setup: rho must be > 0");
+  if (!(alpha > 0.0)) return fail(EPARAM, "admm_setup: alpha must be > 0");
+  double s = 1.0;
+  if (int rc = normalization(c, n, y, m, &s)) return rc;
+  const size_t N = static_cast<size_t>(n);
+  // A~ = dense_materialize(A) / s (circulant.hpp:382-394): A~[t][j] = c[(j - omega_t) mod n] / s
+  std::vector<double> ad(static_cast<size_t>(m) * N);
+  for (int64_t t = 0; t < m; ++t)
+    for (int64_t j = 0; j < n; ++j) {
+      const int64_t w = omega[t];
+      ad[static_cast<size_t>(t) * N + static_cast<size_t>(j)] = c[j >= w ? j - w : j - w + n] / s;
+    }
+  // gram = A~^T A~ + rho I
+  std::vector<double> g(N * N);
+  parallel_for(n, threads, [&](int64_t b, int64_t e) {
+    for (int64_t i = b; i < e; ++i)
+      for (int64_t j = 0; j < n; ++j) {
+        double acc = 0.0;
+        for (int64_t t = 0; t < m; ++t)
+          acc += ad[static_cast<size_t>(t) * N + static_cast<size_t>(i)] * ad[static_cast<size_t>(t) * N + static_cast<size_t>(j)];
+        g[static_cast<size_t>(i) * N + static_cast<size_t>(j)] = acc + (i == j ? rho : 0.0);
+      }
+  });
+  // Cholesky, lower triangle in place
+  for (int64_t k = 0; k < n; ++k) {
+    double d = g[static_cast<size_t>(k) * N + static_cast<size_t>(k)];
+    for (int64_t p = 0; p < k; ++p) d -= g[static_cast<size_t>(k) * N + static_cast<size_t>(p)] * g[static_cast<size_t>(k) * N + static_cast<size_t>(p)];
+    if (!(d > 0.0)) return fail(ESINGULAR, "admm_setup: Gram matrix is not positive definite");
+    const double lkk = std::sqrt(d);
+    g[static_cast<size_t>(k) * N + static_cast<size_t>(k)] = lkk;
+    parallel_for(n - k - 1, threads, [&](int64_t b, int64_t e) {
+      for (int64_t i = k + 1 + b; i < k + 1 + e; ++i) {
+        double acc = g[static_cast<size_t>(i) * N + static_cast<size_t>(k)];
+        for (int64_t p = 0; p < k; ++p) acc -= g[static_cast<size_t>(i) * N + static_cast<size_t>(p)] * g[static_cast<size_t>(k) * N + static_cast<size_t>(p)];
+        g[static_cast<size_t>(i) * N + static_cast<size_t>(k)] = acc / lkk;
+      }
+    });
+  }
+  // B = (L L^T)^-1 I, column by column
+  st.B.assign(N * N, 0.0);
+  parallel_for(n, threads, [&](int64_t b, int64_t e) {
+    std::vector<double> w(N);
+    for (int64_t col = b; col < e; ++col) {
+      for (int64_t i = 0; i < n; ++i) {  // L w = e_col
+        double acc = i == col ? 1.0 : 0.0;
+        for (int64_t p = 0; p < i; ++p) acc -= g[static_cast<size_t>(i) * N + static_cast<size_t>(p)] * w[static_cast<size_t>(p)];
+        w[static_cast<size_t>(i)] = acc / g[static_cast<size_t>(i) * N + static_cast<size_t>(i)];
+      }
+      for (int64_t i = n - 1; i >= 0; --i) {  // L^T b = w
+        double acc = w[static_cast<size_t>(i)];
+        for (int64_t p = i + 1; p < n; ++p) acc -= g[static_cast<size_t>(p) * N + static_cast<size_t>(i)] * w[static_cast<size_t>(p)];
+        w[static_cast<size_t>(i)] = acc / g[static_cast<size_t>(i) * N + static_cast<size_t>(i)];
+      }
+      for (int64_t i = 0; i < n; ++i) st.B[static_cast<size_t>(i) * N + static_cast<size_t>(col)] = w[static_cast<size_t>(i)];
+    }
+  });
+  st.aty.assign(N, 0.0);  // A~^T (y / s)
+  for (int64_t j = 0; j < n; ++j) {
+    double acc = 0.0;
+    for (int64_t t = 0; t < m; ++t) acc += ad[static_cast<size_t>(t) * N + static_cast<size_t>(j)] * (y[t] / s);
+    st.aty[static_cast<size_t>(j)] = acc;
+  }
+  st.n = n; st.m = m; st.s = s; st.rho = rho;
+  st.threshold = alpha / rho;
+  st.x.assign(N, 0.0);
+  st.z.assign(N, 0.0);
+  st.u.assign(N, 0.0);
+  st.rhs = st.aty;
+  st.t = 0;
+  return OK;
+}
+
+// padmm_phases (parallel.hpp:284-317) == admm_step (solvers.hpp:318-327):
+// primal x_i = sum_j B(i, j) rhs_j ascending, z_i = eta(x_i + u_i), u_i += x_i - z_i;
+// then rhs_i = A~^T y~_i + rho (z_i - u_i)
+static void admm_step_phases(Admm& st, int threads) {
+  const int64_t n = st.n;
+  const size_t N = static_cast<size_t>(n);
+  parallel_for(n, threads, [&](int64_t b, int64_t e) {
+    for (int64_t i = b; i < e; ++i) {
+      const size_t k = static_cast<size_t>(i);
+      double acc = 0.0;
+      for (int64_t j = 0; j < n; ++j) acc += st.B[k * N + static_cast<size_t>(j)] * st.rhs[static_cast<size_t>(j)];
+      st.x[k] = acc;
+      st.z[k] = soft(acc + st.u[k], st.threshold);
+      st.u[k] += acc - st.z[k];
+    }
+  });
+  for (int64_t i = 0; i < n; ++i) {
+    const size_t k = static_cast<size_t>(i);
+    st.rhs[k] = st.aty[k] + st.rho * (st.z[k] - st.u[k]);
+  }
+  ++st.t;
+}
+
 }  // namespace orc
 
 // ===========================================================================
@@ -723,8 +844,36 @@ void orc_cadmm_scalars(void* h, double* threshold, double* s) {
 }
 void orc_cadmm_free(void* h) { delete static_cast<Cadmm*>(h); }
 
+// ---- dense ADMM handle (solvers.hpp:267-327) --------------------------------
+void* orc_admm_setup(int64_t n, int64_t m, const double* c, const int64_t* omega, const double* y, double alpha,
+                     double rho, int64_t dense_cap, int threads, int* status) {
+  auto* st = new Admm();
+  const int rc = admm_setup(*st, n, m, c, omega, y, alpha, rho, dense_cap, threads);
+  *status = rc;
+  if (rc) { delete st; return nullptr; }
+  return st;
+}
+int orc_admm_step(void* h, int64_t iters, int threads) {
+  auto* st = static_cast<Admm*>(h);
+  for (int64_t k = 0; k < iters; ++k) admm_step_phases(*st, threads);
+  return OK;
+}
+// which: 0 x, 1 z, 2 u, 3 rhs, 4 aty, 5 B (n * n, row-major)
+int orc_admm_get(void* h, int which, double* out) {
+  auto* st = static_cast<Admm*>(h);
+  const std::vector<double>* tab[] = {&st->x, &st->z, &st->u, &st->rhs, &st->aty, &st->B};
+  if (which < 0 || which > 5) return fail(EPARAM, "orc_admm_get: bad field");
+  std::copy(tab[which]->begin(), tab[which]->end(), out);
+  return OK;
+}
+void orc_admm_scalars(void* h, double* threshold, double* s) {
+  auto* st = static_cast<Admm*>(h);
+  *threshold = st->threshold; *s = st->s;
+}
+void orc_admm_free(void* h) { delete static_cast<Admm*>(h); }
+
 // ---- run_loop solvers.hpp:426-472 over either handle ----------------------
-// kind 0 = ISTA (iterate x), 1 = cADMM (iterate z, solvers.hpp:528).
+// kind 0 = ISTA (iterate x), 1 = cADMM (iterate z, solvers.hpp:528), 2 = dense ADMM (iterate z, :508).
 // trace arrays (capacity trace_cap) receive (iteration, value) per check.
 // Returns status; fills iterations, reached_target, final_metric, trace_len.
 int orc_run_loop(void* h, int kind, const double* truth, int64_t max_iter, double target, int64_t check_every,
@@ -732,7 +881,8 @@ int orc_run_loop(void* h, int kind, const double* truth, int64_t max_iter, doubl
                  int64_t* trace_it, double* trace_val, int64_t trace_cap, int64_t* trace_len) {
   if (max_iter < 0) return fail(EPARAM, "solver: max_iter must be >= 0");
   if (check_every < 1) return fail(EPARAM, "solver: check_every must be >= 1");
-  std::vector<double>* it = kind == 0 ? &static_cast<Ista*>(h)->x : &static_cast<Cadmm*>(h)->z;
+  std::vector<double>* it = kind == 0 ? &static_cast<Ista*>(h)->x
+                          : kind == 1 ? &static_cast<Cadmm*>(h)->z : &static_cast<Admm*>(h)->z;
   const int64_t n = static_cast<int64_t>(it->size());
   const bool has_target = !std::isnan(target);
   const double inv_sqrt_n = n > 0 ? 1.0 / std::sqrt(static_cast<double>(n)) : 1.0;
@@ -742,12 +892,16 @@ int orc_run_loop(void* h, int kind, const double* truth, int64_t max_iter, doubl
   *final_metric = std::numeric_limits<double>::quiet_NaN();
   while (t < max_iter) {
     prev = *it;
-    const int rc = kind == 0 ? orc_ista_step(h, 1, engine, threads) : orc_cadmm_step(h, 1, engine, threads);
+    const int rc = kind == 0 ? orc_ista_step(h, 1, engine, threads)
+                 : kind == 1 ? orc_cadmm_step(h, 1, engine, threads) : orc_admm_step(h, 1, threads);
     if (rc) return rc;
     ++t;
     if (t % check_every != 0 && t != max_iter) continue;
     for (double v : *it)
-      if (!std::isfinite(v)) return fail(EDIVERGE, kind == 0 ? "ista_run: iterate became non-finite" : "cadmm_run: iterate became non-finite");
+      if (!std::isfinite(v))
+        return fail(EDIVERGE, kind == 0   ? "ista_run: iterate became non-finite"
+                              : kind == 1 ? "cadmm_run: iterate became non-finite"
+                                          : "admm_dense_run: iterate became non-finite");
     double value = 0.0;
     if (truth) {
       for (int64_t i = 0; i < n; ++i) { const double d = (*it)[static_cast<size_t>(i)] - truth[i]; value += d * d; }

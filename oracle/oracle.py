@@ -91,6 +91,13 @@ def _decl(L):
     L.orc_cadmm_get.argtypes = [C.c_void_p, C.c_int, _d]
     L.orc_cadmm_scalars.argtypes = [C.c_void_p, _d, _d]
     L.orc_cadmm_free.argtypes = [C.c_void_p]
+    L.orc_admm_setup.restype = C.c_void_p
+    L.orc_admm_setup.argtypes = [C.c_int64, C.c_int64, _d, _i64, _d, C.c_double, C.c_double, C.c_int64, C.c_int,
+                                 C.POINTER(C.c_int)]
+    L.orc_admm_step.argtypes = [C.c_void_p, C.c_int64, C.c_int]
+    L.orc_admm_get.argtypes = [C.c_void_p, C.c_int, _d]
+    L.orc_admm_scalars.argtypes = [C.c_void_p, _d, _d]
+    L.orc_admm_free.argtypes = [C.c_void_p]
     L.orc_run_loop.argtypes = [C.c_void_p, C.c_int, _d, C.c_int64, C.c_double, C.c_int64, C.c_int, C.c_int,
                                _i64, C.POINTER(C.c_int), _d, _i64, _d, C.c_int64, _i64]
 
@@ -324,6 +331,39 @@ class Cadmm(_Handle):
         return {"threshold": a[0], "s": b[0]}
 
 
+class Admm(_Handle):
+    """admm_setup + admm_step (reference solvers.hpp:267-327): the dense baseline with the explicit
+    n x n inverse B = (A~^T A~ + rho I)^-1 (Cholesky), phases parallel.hpp:284-317."""
+
+    _kind = 2
+    FIELDS = ("x", "z", "u", "rhs", "aty", "B")
+    DENSE_CAP = 4096  # circulant.hpp:31 kDenseCap
+
+    def __init__(self, row, omega, y, alpha=1e-4, rho=0.1, dense_cap=DENSE_CAP, threads=None):
+        row, omega, y = f64(row), i64(omega), f64(y)
+        if len(y) != len(omega):
+            raise OracleError(EDIM, "admm_setup: dimension mismatch")
+        st = C.c_int(0)
+        self._free = lib().orc_admm_free
+        self._h = lib().orc_admm_setup(len(row), len(omega), _pd(row), _pi(omega), _pd(y), alpha, rho, dense_cap,
+                                       threads or os.cpu_count() or 1, C.byref(st))
+        _check(st.value)
+        self.n, self.m = len(row), len(omega)
+
+    def step(self, iters=1, engine=ENGINE_PHASES, threads=None):
+        _check(lib().orc_admm_step(self._h, iters, threads or os.cpu_count() or 1))
+
+    def get(self, name):
+        out = np.zeros(self.n * self.n if name == "B" else self.n)
+        _check(lib().orc_admm_get(self._h, self.FIELDS.index(name), _pd(out)))
+        return out.reshape(self.n, self.n) if name == "B" else out
+
+    def scalars(self):
+        a, b = np.zeros(1), np.zeros(1)
+        lib().orc_admm_scalars(self._h, _pd(a), _pd(b))
+        return {"threshold": a[0], "s": b[0]}
+
+
 @dataclass
 class Report:
     final_x: np.ndarray
@@ -336,7 +376,7 @@ class Report:
 def run(kind: str, row, omega, y, truth=None, engine=ENGINE_PHASES, threads=None, max_iter=100000,
         target_mse=float("nan"), check_every=10, **params) -> Report:
     """ista_run / cadmm_run (reference solvers.hpp:479-534) incl. run_loop :426-472."""
-    h = Ista(row, omega, y, **params) if kind == "ista" else Cadmm(row, omega, y, **params)
+    h = {"ista": Ista, "cadmm": Cadmm, "admm": Admm}[kind](row, omega, y, **params)
     cap = max_iter // max(check_every, 1) + 2
     tit = np.zeros(cap, dtype=np.int64)
     tval = np.zeros(cap)

@@ -27,7 +27,8 @@ _vp = C.c_void_p
 class cl_config(C.Structure):
     _fields_ = [("alpha", C.c_double), ("tau", C.c_double), ("rho", C.c_double), ("sigma", C.c_double),
                 ("tau1", C.c_double), ("tau2", C.c_double), ("max_iter", C.c_int64), ("target_mse", C.c_double),
-                ("check_every", C.c_int32), ("pairing", C.c_int32), ("engine", C.c_int32)]
+                ("check_every", C.c_int32), ("pairing", C.c_int32), ("engine", C.c_int32),
+                ("dense_cap", C.c_int64)]
 
 
 class cl_bench_row(C.Structure):
@@ -74,6 +75,7 @@ _SIGS = {
     "cl_solver_synchronize": (C.c_int, [_vp]),
     "cl_solver_last_step_ms": (C.c_int, [_vp, _d]),
     "cl_solver_phase_ms": (C.c_int, [_vp, _d, C.POINTER(C.c_int)]),
+    "cl_solver_phase_history": (C.c_int, [_vp, _d, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int)]),
     "cl_solver_profile": (C.c_int, [_vp, C.c_int]),
     "cl_solver_shard": (C.c_int, [_vp, C.c_int, C.c_int]),
     "cl_solver_stream": (C.c_int, [_vp, C.POINTER(_vp)]),

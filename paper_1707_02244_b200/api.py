@@ -125,8 +125,8 @@ class SolverConfig:
     (the paper's scheme and the north-star path, the reference's
     ``use_fft=false`` arithmetic); ``use_fft=True`` runs the on-device FFT
     engine (any n: non-power-of-two n is embedded as a linear convolution in the
-    next power of two >= 2n-1).  ``dense_cap`` is accepted for source
-    compatibility (dense ADMM is out of scope)."""
+    next power of two >= 2n-1).  ``dense_cap`` bounds the dense ADMM baseline
+    (admm_setup / admm_dense_run: CapacityError above it)."""
     alpha: float = 1e-4
     tau: float = 0.0
     rho: float = 0.1
@@ -148,6 +148,7 @@ class SolverConfig:
         c.max_iter, c.target_mse = int(self.max_iter), float(self.target_mse)
         c.check_every, c.pairing = int(self.check_every), int(self.pairing)
         c.engine = 1 if self.use_fft else 0
+        c.dense_cap = int(self.dense_cap)
         return c
 
 
@@ -584,6 +585,15 @@ class _DeviceState:
         step graph (times the graph-replayed step itself)."""
         _check(lib.cl_solver_profile(self._h, int(enable)))
 
+    def phase_history(self, max_steps=256):
+        """profile(2): per-phase times (ms) of each of the last graph replays, oldest first (list of lists)."""
+        steps, nph = C.c_int64(0), C.c_int(0)
+        _check(lib.cl_solver_phase_history(self._h, None, 0, C.byref(steps), C.byref(nph)))
+        k = min(int(steps.value), max_steps)
+        arr = (C.c_double * max(1, k * max(nph.value, 1)))()
+        _check(lib.cl_solver_phase_history(self._h, arr, k, C.byref(steps), C.byref(nph)))
+        return [[arr[i * nph.value + j] for j in range(nph.value)] for i in range(int(steps.value))]
+
     def phase_ms(self):
         arr = (C.c_double * 8)()
         cnt = C.c_int(8)
@@ -610,6 +620,21 @@ class CadmmState(_DeviceState):
     _name = "cadmm_setup"
 
 
+class AdmmState(_DeviceState):
+    """solvers.hpp:267-283 + admm_setup :285-314: the dense baseline; B = (A~^T A~ + rho I)^-1 is built in
+    fp64 on the GPU (Gram matrix + blocked Gauss-Jordan) and iterated in fp32."""
+    KIND = 2
+    FIELDS = ("x", "z", "u", "rhs", "aty", "B")
+    _name = "admm_setup"
+
+    def get(self, name: str) -> np.ndarray:
+        if name != "B":
+            return super().get(name)
+        out = np.zeros(self._n * self._n)
+        _check(lib.cl_solver_get(self._h, b"B", _pd(out)))
+        return out.reshape(self._n, self._n)
+
+
 def ista_setup(A: PartialCirculantOperator, y, cfg: SolverConfig = None, device: int = 0) -> IstaState:
     return IstaState(A, y, cfg or SolverConfig(), device)
 
@@ -623,6 +648,16 @@ def cadmm_setup(A: PartialCirculantOperator, y, cfg: SolverConfig = None, device
 
 
 def cadmm_step(state: CadmmState, use_fft: bool = True):
+    state.step(1)
+
+
+def admm_setup(A: PartialCirculantOperator, y, cfg: SolverConfig = None, device: int = 0) -> AdmmState:
+    """solvers.hpp:285-314 (DimensionError, then CapacityError for n > cfg.dense_cap, before anything is built)."""
+    return AdmmState(A, y, cfg or SolverConfig(), device)
+
+
+def admm_step(state: AdmmState):
+    """solvers.hpp:318-327"""
     state.step(1)
 
 
@@ -654,6 +689,14 @@ def cadmm_run(y, A: PartialCirculantOperator, cfg: SolverConfig = None, truth=No
     """solvers.hpp:518-534"""
     cfg = cfg or SolverConfig()
     st = cadmm_setup(A, y, cfg, device)
+    return _run(st, truth, cfg)
+
+
+def admm_dense_run(y, A: PartialCirculantOperator, cfg: SolverConfig = None, truth=None,
+                   device: int = 0) -> RecoveryReport:
+    """solvers.hpp:497-514: dense ADMM; the O(n^3) inversion is timed into setup_seconds."""
+    cfg = cfg or SolverConfig()
+    st = admm_setup(A, y, cfg, device)
     return _run(st, truth, cfg)
 
 

@@ -9,9 +9,11 @@
 #include <chrono>
 #include <cstdlib>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <limits>
 #include <memory>
+#include <mutex>
 #include <sstream>
 #include <string>
 #include <utility>
@@ -25,6 +27,7 @@
 #include "small.cuh"
 #include "kernels.cuh"
 #include "tc_dense.cuh"
+#include "dense.cuh"
 
 namespace clb {
 void gen_sparse_signal(int64_t n, int64_t k, uint64_t seed, double* values, int64_t* support);
@@ -103,9 +106,94 @@ double seconds_since(std::chrono::steady_clock::time_point a) {
   return std::chrono::duration<double>(std::chrono::steady_clock::now() - a).count();
 }
 
+// CLB_TRACE=1: host wall time of each setup / run / teardown stage on stderr (e2e diagnostics).
+void trace(const char* stage) {
+  static const bool on = [] {
+    const char* v = std::getenv("CLB_TRACE");
+    return v && v[0] == '1';
+  }();
+  if (!on) return;
+  static thread_local auto last = std::chrono::steady_clock::now();
+  const auto now = std::chrono::steady_clock::now();
+  std::fprintf(stderr, "[clb] %-28s %8.3f ms\n", stage, std::chrono::duration<double, std::milli>(now - last).count());
+  last = now;
+}
+
 // solvers.hpp:90-106 (circulant kinds only)
-uint64_t footprint(int kind, int64_t n, uint64_t width) {
-  return (kind == CL_KIND_ISTA ? 4 : 10) * static_cast<uint64_t>(n) * width;
+uint64_t footprint(int kind, int64_t n, int64_t m, uint64_t width) {
+  const uint64_t un = static_cast<uint64_t>(n);
+  if (kind == CL_KIND_ADMM) return (un * un + 4 * un + static_cast<uint64_t>(m)) * width;  // kDenseAdmm
+  return (kind == CL_KIND_ISTA ? 4 : 10) * un * width;
+}
+
+// Per-device pool of the host-side resources a solver state owns: its non-blocking stream, its
+// timing events, a pinned metric slot and a pinned staging buffer for downloads.  Creating them
+// costs 1.5-5 ms per state (cudaStreamCreate, cudaMallocHost); a state created after another one
+// was destroyed on the same device takes the previous one's instead, so repeated ista_run /
+// cadmm_run calls do not pay it.  The stream is drained before it is returned.
+constexpr int kPhaseEvents = 8;
+struct StateResources {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev[kPhaseEvents] = {};
+  cudaEvent_t step_ev[2] = {};
+  double* met_host = nullptr;  // 4 doubles
+  float* stage = nullptr;      // pinned download staging
+  size_t stage_floats = 0;
+  void create(int dev) {
+    device = dev;
+    CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    for (auto& e : ev) CU(cudaEventCreate(&e));
+    for (auto& e : step_ev) CU(cudaEventCreate(&e));
+    CU(cudaMallocHost(&met_host, sizeof(double) * 4));
+  }
+  float* staging(size_t count) {
+    if (count > stage_floats) {
+      if (stage) CU(cudaFreeHost(stage));
+      stage = nullptr;
+      stage_floats = 0;
+      CU(cudaMallocHost(&stage, sizeof(float) * count));
+      stage_floats = count;
+    }
+    return stage;
+  }
+};
+struct ResourcePool {
+  std::mutex mu;
+  std::vector<StateResources> free[64];
+};
+ResourcePool& resource_pool() {
+  static ResourcePool* p = new ResourcePool();  // never destroyed: streams may outlive static teardown
+  return *p;
+}
+StateResources take_resources(int device) {
+  ResourcePool& p = resource_pool();
+  {
+    std::lock_guard<std::mutex> lk(p.mu);
+    if (device >= 0 && device < 64 && !p.free[device].empty()) {
+      StateResources r = p.free[device].back();
+      p.free[device].pop_back();
+      return r;
+    }
+  }
+  StateResources r;
+  r.create(device);
+  return r;
+}
+void give_resources(const StateResources& r) {
+  if (!r.st) return;
+  cudaStreamSynchronize(r.st);
+  ResourcePool& p = resource_pool();
+  std::lock_guard<std::mutex> lk(p.mu);
+  if (r.device >= 0 && r.device < 64 && p.free[r.device].size() < 8) {
+    p.free[r.device].push_back(r);
+    return;
+  }
+  for (auto e : r.ev) cudaEventDestroy(e);
+  for (auto e : r.step_ev) cudaEventDestroy(e);
+  cudaFreeHost(r.met_host);
+  if (r.stage) cudaFreeHost(r.stage);
+  cudaStreamDestroy(r.st);
 }
 
 }  // namespace
@@ -161,16 +249,12 @@ struct Solver {
   // step graph (the timed configuration itself: cl_solver_phase_ms reads the last replay)
   int profile = 0;
   cudaStream_t st = nullptr;
-  // Destroys st after every DevBuf member (declared below) has queued its free.
-  struct StreamOwner {
-    cudaStream_t* s;
-    ~StreamOwner() {
-      if (*s) {
-        cudaStreamSynchronize(*s);
-        cudaStreamDestroy(*s);
-      }
-    }
-  } st_owner{&st};
+  StateResources res;  // st, the events and the pinned slots (from the per-device pool)
+  // Returns res to the pool after every DevBuf member (declared below) has queued its free.
+  struct ResOwner {
+    StateResources* r;
+    ~ResOwner() { give_resources(*r); }
+  } res_owner{&res};
   ConvPlan plan;     // outputs: gradient (ISTA) or dense (cADMM) products
   ConvPlan rplan;    // ISTA residual (input tiles x position splits)
   bool ista_tc = false;  // ISTA products embedded in dense tensor-core products (plan == rplan, tc)
@@ -182,6 +266,7 @@ struct Solver {
   DevBuf<float> y, r, x, delta;    // ISTA
   DevBuf<float> d, pty, z, nu, mu, v, beta;  // cADMM (x shared)
   DevBuf<float> partial, truth;
+  DevBuf<float> Bm, aty, u, rhs;             // dense ADMM: B (n x n fp32), A~^T y~, dual, right-hand side
   DevBuf<float> tcs;  // this solver's tensor-core operand-scale scratch (ConvPlan::tc_scratch)
   DevBuf<float2> chat, bhat, F0, F1;  // FFT engine: spectra of c~ (and of B), work buffers
   bool fft = false;
@@ -201,27 +286,42 @@ struct Solver {
   bool small_fft = false;
   DevBuf<float2> chatS, bhatS, twS;
   DevBuf<double> blk, met;
-  double* met_host = nullptr;
+  double* met_host = nullptr;     // res.met_host
   std::vector<int> rowstart_host;
   std::vector<int64_t> omega_host;
-  cudaEvent_t ev[8] = {};
+  cudaEvent_t* ev = nullptr;       // res.ev[kPhaseEvents]
   double phase_ms[8] = {};
   int nphase = 0;
-  cudaEvent_t step_ev[2] = {};
+  cudaEvent_t* step_ev = nullptr;  // res.step_ev[2]
   double last_step_ms = 0.0;
+  // profile mode 2: the captured step's event-record nodes (node i records phase boundary i) and a
+  // ring of per-replay event sets they are re-pointed to before every replay, so back-to-back
+  // replays are timed phase by phase without a host synchronization in between
+  static constexpr int kRing = 256;
+  cudaGraphNode_t ev_node[kPhaseEvents] = {};
+  int n_ev_nodes = 0;
+  std::vector<cudaEvent_t> ring;  // kRing * kPhaseEvents
+  int64_t ring_count = 0;         // replays recorded since the last reset
   // One unchecked iteration captured as a CUDA graph (launch-bound small n and
   // the ~30-launch FFT engine step); replayed by step().  CLB_NO_GRAPH=1 disables.
   cudaGraphExec_t graph = nullptr;
+  cudaGraph_t graph_src = nullptr;  // kept while `graph` lives: its node handles address the exec's nodes
+  void drop_graph() {
+    if (graph) cudaGraphExecDestroy(graph);
+    if (graph_src) cudaGraphDestroy(graph_src);
+    graph = nullptr;
+    graph_src = nullptr;
+    n_ev_nodes = 0;
+  }
 
   ~Solver() {
+    trace("destroy: enter");
     if (st) cudaSetDevice(device);
     if (st) cudaStreamSynchronize(st);
-    if (graph) cudaGraphExecDestroy(graph);
-    for (auto& e : ev)
-      if (e) cudaEventDestroy(e);
-    for (auto& e : step_ev)
-      if (e) cudaEventDestroy(e);
-    if (met_host) cudaFreeHost(met_host);
+    trace("destroy: stream drained");
+    drop_graph();
+    for (auto e : ring) cudaEventDestroy(e);
+    trace("destroy: graph/events");
   }
 
   void init_device() {
@@ -229,12 +329,14 @@ struct Solver {
     CU(cudaGetDeviceCount(&count));
     if (device < 0 || device >= count) raise(CL_ECUDA, "cl_solver_create: no such CUDA device");
     CU(cudaSetDevice(device));
-    CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    res = take_resources(device);
+    st = res.st;
+    ev = res.ev;
+    step_ev = res.step_ev;
+    met_host = res.met_host;
     reserve_pool(device);
-    for (auto& e : ev) CU(cudaEventCreate(&e));
-    for (auto& e : step_ev) CU(cudaEventCreate(&e));
-    CU(cudaMallocHost(&met_host, sizeof(double) * 4));
     conv_kernels_init();
+    trace("setup: init_device");
   }
 
   void build_rows(const int64_t* omega) {
@@ -257,10 +359,13 @@ struct Solver {
 
   void set_shard(int rk, int ws) {
     if (fft && ws != 1) raise(CL_EPARAM, "cl_solver_shard: the FFT engine runs unsharded (replicas only)");
+    if (kind == CL_KIND_ADMM) {
+      if (ws != 1) raise(CL_EPARAM, "cl_solver_shard: the dense ADMM runs unsharded (n <= dense_cap; replicas only)");
+      return;
+    }
     if (graph) {  // the captured step covers the previous shard's ranges
       CU(cudaStreamSynchronize(st));
-      CU(cudaGraphExecDestroy(graph));
-      graph = nullptr;
+      drop_graph();
     }
     rank = rk;
     world = ws;
@@ -370,9 +475,11 @@ struct Solver {
             "ista_setup: tau must lie in (0, |A|_2^-2); on the normalized operator the admissible range is (0, 1)");
     if (!(cfg.alpha > 0.0)) raise(CL_EPARAM, "ista_setup: alpha must be > 0");
     check_finite_y(yh);
+    trace("setup: validate");
     const bool dev = device_setup();
     if (dev) init_device();
     scale = normalization_from(dev ? device_spectrum(c) : spectral_norm(c, n), yh);
+    trace("setup: spectral norm");
     tau = tau0;
     thr = cfg.pairing == CL_PAIRING_LITERAL ? cfg.alpha : tau0 * cfg.alpha;
     if (!dev) init_device();
@@ -390,7 +497,9 @@ struct Solver {
       const std::vector<float> crf = reversed(cf);
       hcr.upload(crf.data(), crf.size(), st);
     }
+    trace("setup: plans + rows f32");
     build_rows(omega);
+    trace("setup: omega / row index");
     const std::vector<float> yf = to_f32(yh, m, scale);
     y.alloc(static_cast<size_t>(m), st);
     y.upload(yf.data(), yf.size(), st);
@@ -428,9 +537,11 @@ struct Solver {
       F1.alloc(static_cast<size_t>(n), st);
       if (small_fft_supported(n)) setup_small_fft();
     }
+    trace("setup: state buffers");
     CU(cudaGetLastError());
     device_setup_release();
     CU(cudaStreamSynchronize(st));
+    trace("setup: drained");
   }
 
   // spectrum (length nfft, fp64, host) of the circulant with first row h embedded for a linear
@@ -626,8 +737,83 @@ struct Solver {
     CU(cudaStreamSynchronize(st));
   }
 
+  // admm_setup solvers.hpp:285-314: G = A~^T A~ + rho I and B = G^-1 in fp64 on the device (dense.cu),
+  // then B, A~^T y~ in fp32 for the iterations.
+  void setup_admm(const double* c, const int64_t* omega, const double* yh) {
+    if (n > cfg.dense_cap) {
+      std::ostringstream msg;
+      msg << "admm_setup: n = " << n << " exceeds the dense cap " << cfg.dense_cap;
+      raise(CL_ECAPACITY, msg.str());
+    }
+    if (!(cfg.rho > 0.0)) raise(CL_EPARAM, "admm_setup: rho must be > 0");
+    if (!(cfg.alpha > 0.0)) raise(CL_EPARAM, "admm_setup: alpha must be > 0");
+    if (fft) raise(CL_EPARAM, "admm_setup: the dense ADMM has no FFT engine (it multiplies by the stored B)");
+    check_finite_y(yh);
+    scale = normalization_from(spectral_norm(c, n), yh);
+    init_device();
+    thr = cfg.alpha / cfg.rho;
+    const int64_t np = dense_pad(n);
+    std::vector<double> cn(static_cast<size_t>(n)), yn(static_cast<size_t>(m));
+    for (int64_t i = 0; i < n; ++i) cn[static_cast<size_t>(i)] = c[i] / scale;
+    for (int64_t t2 = 0; t2 < m; ++t2) yn[static_cast<size_t>(t2)] = yh[t2] / scale;
+    std::vector<int> om(static_cast<size_t>(m));
+    for (int64_t t2 = 0; t2 < m; ++t2) om[static_cast<size_t>(t2)] = static_cast<int>(omega[t2]);
+    omega_host.assign(omega, omega + m);
+    DevBuf<double> cn64, yn64, G, scr, aty64;
+    cn64.alloc(cn.size(), st);
+    cn64.upload(cn.data(), cn.size(), st);
+    yn64.alloc(yn.size(), st);
+    yn64.upload(yn.data(), yn.size(), st);
+    omega32.alloc(om.size(), st);
+    omega32.upload(om.data(), om.size(), st);
+    G.alloc(static_cast<size_t>(np * np), st);
+    scr.alloc(dense_gj_scratch(np), st);
+    aty64.alloc(static_cast<size_t>(n), st);
+    launch_dense_gram(cn64.p, omega32.p, n, m, cfg.rho, G.p, np, st);
+    launch_dense_aty(cn64.p, omega32.p, yn64.p, n, m, aty64.p, st);
+    launch_dense_invert(G.p, np, scr.p, nullptr, st);
+    Bm.alloc(static_cast<size_t>(n * n), st);
+    launch_dense_to_f32(G.p, np, n, Bm.p, st);
+    aty.alloc(static_cast<size_t>(n), st);
+    launch_f64_to_f32(aty64.p, n, aty.p, st);
+    CU(cudaGetLastError());
+    for (DevBuf<float>* b : {&x, &z, &u}) { b->alloc(static_cast<size_t>(n), st); b->zero(st); }
+    rhs.alloc(static_cast<size_t>(n), st);
+    CU(cudaMemcpyAsync(rhs.p, aty.p, sizeof(float) * n, cudaMemcpyDeviceToDevice, st));  // rhs = A~^T y~
+    blk.alloc(kEpiBlocks * 4, st);
+    met.alloc(4, st);
+    out_lo = 0;
+    out_hi = n;
+    CU(cudaStreamSynchronize(st));  // the host vectors and the fp64 scratch go out of scope
+  }
+  void admm_dense_step(int want) {  // padmm_phases parallel.hpp:284-317
+    mark(0);
+    PadmmArgs a;
+    a.B = Bm.p;
+    a.rhs = rhs.p;
+    a.x = x.p;
+    a.z = z.p;
+    a.u = u.p;
+    a.truth = has_truth ? truth.p : nullptr;
+    a.blk = blk.p;
+    a.n = n;
+    a.thr = static_cast<float>(thr);
+    a.want_metrics = want;
+    launch_padmm_primal(a, st);
+    mark(1);
+    launch_padmm_rhs(aty.p, z.p, u.p, static_cast<float>(cfg.rho), rhs.p, n, st);
+    mark(2);
+    nphase = 2;
+  }
+
   void mark(int i) {
-    if (profile) CU(cudaEventRecord(ev[i], st));
+    if (!profile) return;
+    // inside a stream capture a plain record only orders streams; the external flag makes it a real
+    // event-record node of the graph, so each replay stamps the phase boundaries
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CU(cudaStreamIsCapturing(st, &cs));
+    if (cs == cudaStreamCaptureStatusActive) CU(cudaEventRecordWithFlags(ev[i], st, cudaEventRecordExternal));
+    else CU(cudaEventRecord(ev[i], st));
   }
 
   EpiArgs base_args(int want) {
@@ -899,6 +1085,12 @@ struct Solver {
 
   void one_step(int want) {
     if (world != 1) raise(CL_EPARAM, "cl_solver_step: sharded solvers advance with cl_solver_run_phase");
+    if (kind == CL_KIND_ADMM) {
+      admm_dense_step(want);
+      CU(cudaGetLastError());
+      ++t;
+      return;
+    }
     if (fft4) {
       if (kind == CL_KIND_ISTA) ista_fft4_step(want);
       else admm_fft4_step(want);
@@ -927,12 +1119,32 @@ struct Solver {
 
   void collect_profile() {
     if (!profile) return;
+    if (n_ev_nodes && ring_count > 0) {  // the last graph replay's ring slot
+      phase_history(phase_ms, 1);
+      return;
+    }
     CU(cudaEventSynchronize(ev[nphase]));
     for (int i = 0; i < nphase; ++i) {
       float ms = 0.f;
       CU(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
       phase_ms[i] = ms;
     }
+  }
+  // Phase times of the last `want` graph replays recorded in the ring (profile mode 2), oldest first:
+  // out[k * nphase + i].  Returns the number of replays written.
+  int64_t phase_history(double* out, int64_t want) {
+    if (profile != 2 || !n_ev_nodes) return 0;
+    const int64_t have = std::min<int64_t>({ring_count, static_cast<int64_t>(kRing), want});
+    for (int64_t k = 0; k < have; ++k) {
+      const cudaEvent_t* slot = ring.data() + ((ring_count - have + k) % kRing) * kPhaseEvents;
+      CU(cudaEventSynchronize(slot[nphase]));
+      for (int i = 0; i < nphase; ++i) {
+        float ms = 0.f;
+        CU(cudaEventElapsedTime(&ms, slot[i], slot[i + 1]));
+        out[k * nphase + i] = ms;
+      }
+    }
+    return have;
   }
 
   bool use_graph() const {
@@ -945,18 +1157,36 @@ struct Solver {
 
   void build_graph() {
     if (graph) return;
-    if (graph) {
-      CU(cudaGraphExecDestroy(graph));
-      graph = nullptr;
-    }
     const int64_t t0 = t;
     cudaGraph_t g;
     CU(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     one_step(0);
     CU(cudaStreamEndCapture(st, &g));
+    n_ev_nodes = 0;
+    if (profile == 2) {  // find the event-record node of each phase boundary
+      size_t cnt = 0;
+      CU(cudaGraphGetNodes(g, nullptr, &cnt));
+      std::vector<cudaGraphNode_t> nodes(cnt);
+      CU(cudaGraphGetNodes(g, nodes.data(), &cnt));
+      for (cudaGraphNode_t nd : nodes) {
+        cudaGraphNodeType ty;
+        CU(cudaGraphNodeGetType(nd, &ty));
+        if (ty != cudaGraphNodeTypeEventRecord) continue;
+        cudaEvent_t e;
+        CU(cudaGraphEventRecordNodeGetEvent(nd, &e));
+        for (int i = 0; i < kPhaseEvents; ++i)
+          if (ev[i] == e) ev_node[i] = nd;
+      }
+      n_ev_nodes = nphase + 1;
+      if (ring.empty()) {
+        ring.resize(static_cast<size_t>(kRing) * kPhaseEvents);
+        for (auto& e : ring) CU(cudaEventCreate(&e));
+      }
+    }
     CU(cudaGraphInstantiate(&graph, g, 0));
-    CU(cudaGraphDestroy(g));
+    graph_src = g;
     t = t0;  // capture does not execute
+    trace("run: graph captured");
   }
 
   // Small ISTA (n in {2048, 4096, 8192}): all unchecked iterations in one persistent cluster launch
@@ -1018,6 +1248,11 @@ struct Solver {
     CU(cudaEventRecord(step_ev[0], st));
     for (int64_t k = 0; k < iters; ++k) {
       if (graphed) {
+        if (n_ev_nodes) {  // this replay stamps its phase boundaries into its own ring slot
+          cudaEvent_t* slot = ring.data() + (ring_count % kRing) * kPhaseEvents;
+          for (int i = 0; i < n_ev_nodes; ++i) CU(cudaGraphExecEventRecordNodeSetEvent(graph, ev_node[i], slot[i]));
+          ++ring_count;
+        }
         CU(cudaGraphLaunch(graph, st));
         ++t;
       } else {
@@ -1040,6 +1275,15 @@ struct Solver {
     else *metric = std::sqrt(met_host[0]) * (n > 0 ? 1.0 / std::sqrt(nn) : 1.0);
   }
 
+  // device fp32 -> host fp64 through the pooled pinned staging buffer
+  void download(const float* p, int64_t len, double* out) {
+    if (len <= 0) return;
+    float* stage = res.staging(static_cast<size_t>(len));
+    CU(cudaMemcpyAsync(stage, p, sizeof(float) * len, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    for (int64_t i = 0; i < len; ++i) out[i] = stage[i];
+  }
+
   float* field_ptr(const std::string& f, int64_t* len) {
     *len = n;
     if (kind == CL_KIND_ISTA) {
@@ -1049,6 +1293,16 @@ struct Solver {
       *len = m;
       if (f == "r") return r.p;
       if (f == "y") return y.p;
+    } else if (kind == CL_KIND_ADMM) {
+      if (f == "x") return x.p;
+      if (f == "z") return z.p;
+      if (f == "u") return u.p;
+      if (f == "rhs") return rhs.p;
+      if (f == "aty") return aty.p;
+      if (f == "B") {
+        *len = n * n;
+        return Bm.p;
+      }
     } else {
       if (f == "x") return x.p;
       if (f == "z") return z.p;
@@ -1234,6 +1488,7 @@ void cl_config_default(cl_config* c) {  // solvers.hpp:112-125
   c->check_every = 10;
   c->pairing = CL_PAIRING_LITERAL;
   c->engine = CL_ENGINE_DIRECT;
+  c->dense_cap = 4096;  // circulant.hpp:31 kDenseCap
 }
 
 cl_status cl_device_count(int* count) {
@@ -1527,11 +1782,13 @@ cl_status cl_solver_create(int kind, int64_t n, int64_t m, const double* c, cons
                            const cl_config* cfg, int device, cl_solver** out) {
   CL_GUARD_BEGIN
   *out = nullptr;
-  if (kind != CL_KIND_ISTA && kind != CL_KIND_CADMM) raise(CL_EPARAM, "cl_solver_create: unknown solver kind");
+  if (kind != CL_KIND_ISTA && kind != CL_KIND_CADMM && kind != CL_KIND_ADMM)
+    raise(CL_EPARAM, "cl_solver_create: unknown solver kind");
   if (n < 1) raise(CL_EDIM, "cl_solver_create: n must be >= 1");
   if (m < 0 || m > n) raise(CL_EDIM, "cl_solver_create: need 0 <= m <= n");
   if (n > (int64_t(1) << 30)) raise(CL_ECAPACITY, "cl_solver_create: n above 2^30 is not supported");
   const auto t0 = std::chrono::steady_clock::now();
+  trace("create: enter");
   auto s = std::make_unique<Solver>();
   s->kind = kind;
   s->device = device;
@@ -1539,13 +1796,17 @@ cl_status cl_solver_create(int kind, int64_t n, int64_t m, const double* c, cons
   s->m = m;
   s->setup_common(c, omega, y, cfg);
   if (kind == CL_KIND_ISTA) s->setup_ista(c, omega, y);
-  else s->setup_cadmm(c, omega, y);
+  else if (kind == CL_KIND_CADMM) s->setup_cadmm(c, omega, y);
+  else s->setup_admm(c, omega, y);
   s->setup_seconds = seconds_since(t0);
   *out = new cl_solver{std::move(s)};
   CL_GUARD_END
 }
 
-void cl_solver_destroy(cl_solver* s) { delete s; }
+void cl_solver_destroy(cl_solver* s) {
+  delete s;
+  trace("destroy: done");
+}
 
 cl_status cl_solver_set_truth(cl_solver* h, const double* truth_n) {
   CL_GUARD_BEGIN
@@ -1599,13 +1860,16 @@ cl_status cl_solver_run(cl_solver* h, cl_report* rep, double* final_x, int64_t* 
     int64_t next = ((t / cfg.check_every) + 1) * cfg.check_every;
     if (next > cfg.max_iter) next = cfg.max_iter;
     if (next - t > 1) s.step(next - t - 1);
+    trace("run: unchecked steps queued");
     double value = 0.0;
     int nonfinite = 0;
     s.step_checked(&value, &nonfinite);
+    trace("run: checked step (sync)");
     t = next;
     if (nonfinite)
-      raise(CL_EDIVERGE, s.kind == CL_KIND_ISTA ? "ista_run: iterate became non-finite"
-                                                : "cadmm_run: iterate became non-finite");
+      raise(CL_EDIVERGE, s.kind == CL_KIND_ISTA    ? "ista_run: iterate became non-finite"
+                       : s.kind == CL_KIND_CADMM ? "cadmm_run: iterate became non-finite"
+                                                 : "admm_dense_run: iterate became non-finite");
     if (trace_iter && tl < trace_cap) trace_iter[tl] = t;
     if (trace_value && tl < trace_cap) trace_value[tl] = value;
     ++tl;
@@ -1619,14 +1883,12 @@ cl_status cl_solver_run(cl_solver* h, cl_report* rep, double* final_x, int64_t* 
   rep->trace_len = tl;
   rep->setup_seconds = s.setup_seconds;
   rep->total_seconds = seconds_since(t0) + s.setup_seconds;
-  rep->footprint_bytes = footprint(s.kind, s.n, sizeof(float));
+  rep->footprint_bytes = footprint(s.kind, s.n, s.m, sizeof(float));
   if (final_x) {
     int64_t len = 0;
     float* p = s.field_ptr(s.kind == CL_KIND_ISTA ? "x" : "z", &len);
-    std::vector<float> tmp(static_cast<size_t>(len));
-    CU(cudaMemcpyAsync(tmp.data(), p, sizeof(float) * len, cudaMemcpyDeviceToHost, s.st));
-    CU(cudaStreamSynchronize(s.st));
-    for (int64_t i = 0; i < len; ++i) final_x[i] = tmp[static_cast<size_t>(i)];
+    s.download(p, len, final_x);
+    trace("run: iterate download");
   }
   CL_GUARD_END
 }
@@ -1638,11 +1900,11 @@ cl_status cl_solver_get(cl_solver* h, const char* field, double* out) {
   int64_t len = 0;
   const std::string f(field ? field : "");
   float* p = s.field_ptr(f, &len);
-  std::vector<float> tmp(static_cast<size_t>(len));
-  CU(cudaMemcpyAsync(tmp.data(), p, sizeof(float) * len, cudaMemcpyDeviceToHost, s.st));
-  CU(cudaStreamSynchronize(s.st));
-  if (f == "b") tmp = reversed(tmp);
-  for (int64_t i = 0; i < len; ++i) out[i] = tmp[static_cast<size_t>(i)];
+  s.download(p, len, out);
+  if (f == "b") {  // stored reversed on the device: b[k] = b_rev[(-k) mod n]
+    std::vector<double> tmp(out, out + len);
+    for (int64_t k = 0; k < len; ++k) out[k] = tmp[static_cast<size_t>((len - k) % len)];
+  }
   CL_GUARD_END
 }
 
@@ -1706,12 +1968,11 @@ cl_status cl_solver_profile(cl_solver* h, int enable) {
   Solver& s = *h->impl;
   CU(cudaSetDevice(s.device));
   CU(cudaStreamSynchronize(s.st));
-  if (s.graph) {  // profiled steps run eagerly; drop the captured step
-    CU(cudaGraphExecDestroy(s.graph));
-    s.graph = nullptr;
-  }
+  s.drop_graph();  // the next step recaptures with (or without) the profiling event nodes
   if (enable < 0 || enable > 2) raise(CL_EPARAM, "cl_solver_profile: mode is 0 (off), 1 (eager) or 2 (in-graph)");
   s.profile = enable;
+  s.ring_count = 0;
+  s.n_ev_nodes = 0;
   CL_GUARD_END
 }
 
@@ -1723,6 +1984,16 @@ cl_status cl_solver_phase_ms(cl_solver* h, double* ms, int* count) {
   const int c = std::min(*count, s.nphase);
   for (int i = 0; i < c; ++i) ms[i] = s.phase_ms[i];
   *count = s.nphase;
+  CL_GUARD_END
+}
+
+cl_status cl_solver_phase_history(cl_solver* h, double* ms, int64_t max_steps, int64_t* steps, int* nphase) {
+  CL_GUARD_BEGIN
+  Solver& s = *h->impl;
+  CU(cudaSetDevice(s.device));
+  if (!steps || !nphase) raise(CL_EPARAM, "cl_solver_phase_history: null argument");
+  *nphase = s.nphase;
+  *steps = ms ? s.phase_history(ms, max_steps) : std::min<int64_t>(s.ring_count, Solver::kRing);
   CL_GUARD_END
 }
 
@@ -1742,7 +2013,24 @@ cl_status cl_solver_run_phase(cl_solver* h, int phase) {
   CL_GUARD_BEGIN
   Solver& s = *h->impl;
   CU(cudaSetDevice(s.device));
-  if (s.kind == CL_KIND_ISTA) {
+  if (s.kind == CL_KIND_ADMM) {  // padmm_phases: the primal phase, then the rhs phase
+    if (phase == 0) {
+      PadmmArgs a;
+      a.B = s.Bm.p;
+      a.rhs = s.rhs.p;
+      a.x = s.x.p;
+      a.z = s.z.p;
+      a.u = s.u.p;
+      a.n = s.n;
+      a.thr = static_cast<float>(s.thr);
+      launch_padmm_primal(a, s.st);
+    } else if (phase == 1) {
+      launch_padmm_rhs(s.aty.p, s.z.p, s.u.p, static_cast<float>(s.cfg.rho), s.rhs.p, s.n, s.st);
+      ++s.t;
+    } else {
+      raise(CL_EPARAM, "cl_solver_run_phase: dense ADMM phases are 0 (primal) and 1 (rhs)");
+    }
+  } else if (s.kind == CL_KIND_ISTA) {
     if (phase == 0) s.ista_residual();
     else if (phase == 1) { s.ista_gradient(0); ++s.t; }
     else raise(CL_EPARAM, "cl_solver_run_phase: ISTA phases are 0 (residual) and 1 (gradient)");
@@ -1760,6 +2048,7 @@ cl_status cl_solver_phase_output(cl_solver* h, int phase, void** dev_ptr, int64_
                                  int64_t* total) {
   CL_GUARD_BEGIN
   Solver& s = *h->impl;
+  if (s.kind == CL_KIND_ADMM) raise(CL_EPARAM, "cl_solver_phase_output: the dense ADMM runs unsharded");
   if (s.kind == CL_KIND_ISTA) {
     if (phase == 0) { *dev_ptr = s.r.p; *begin = s.row_lo; *end = s.row_hi; *total = s.m; }
     else { *dev_ptr = s.x.p; *begin = s.out_lo; *end = s.out_hi; *total = s.n; }

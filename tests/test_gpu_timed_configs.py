@@ -213,3 +213,29 @@ def test_concurrent_solvers_on_one_device_bitwise():
             a.step(1)
             b.step(1)
         assert np.array_equal(a.get(field), solo[0]) and np.array_equal(b.get(field), solo[1]), setup.__name__
+
+
+@pytest.mark.parametrize("kind,n", [("ista", 1 << 18), ("cadmm", 1 << 16), ("ista", 4096)])
+def test_in_graph_phase_timing(kind, n):
+    """profile(2): event-record nodes inside the captured step graph stamp every phase of each replay (the
+    bench's roofline reads its kernel time from them); results are unchanged by the extra nodes."""
+    p = orc.make_problem(n, n // 4, max(8, n // 256), 3)
+    setup = cl.ista_setup if kind == "ista" else cl.cadmm_setup
+    field = "x" if kind == "ista" else "z"
+    ref = setup(op_of(p), p.y)
+    ref.step(4)
+    g = setup(op_of(p), p.y)
+    g.profile(2)
+    for _ in range(4):  # back-to-back replays, no synchronization in between
+        g.step(1)
+    g.synchronize()
+    ms = g.phase_ms()
+    assert len(ms) == (4 if kind == "ista" else 6) and all(v >= 0.0 for v in ms) and sum(ms) > 0.0, ms
+    hist = g.phase_history()
+    if n >= 1 << 15:  # every replay stamped its own slot
+        assert len(hist) == 4 and all(len(h) == len(ms) and sum(h) > 0.0 for h in hist), hist
+        assert hist[-1] == ms
+    if n >= 1 << 15:  # same kernels, extra graph nodes: bitwise
+        assert np.array_equal(g.get(field), ref.get(field))
+    else:  # profiled small solves run the multi-kernel step instead of the persistent launch
+        assert rel(g.get(field), ref.get(field)) <= 1e-5
