@@ -283,6 +283,27 @@ def admm_line(cl, torch, prob, local_rank, flush, peaks, steps=5, warmup=3):
             "step_tflops": 6.0 * n * n / (ms * 1e-3) / 1e12, "phase_ms": ph}
 
 
+def dense_line(cl, torch, local_rank, iters=200):
+    """The paper's circulant-vs-dense contrast on BASELINE config 2's problem
+    (make_problem(4096, 1024, 64, 1)): the dense ADMM baseline (admm_setup: Gram matrix + blocked Gauss-Jordan
+    inverse in fp64 on the GPU; then one L2-resident fp32 mat-vec per iteration) against cADMM (O(n) state),
+    each through its public run call, 200 fixed iterations; host clock."""
+    prob = cl.make_problem(4096, 1024, 64, 1)
+    cfg = cl.SolverConfig(max_iter=iters, check_every=iters)
+    out = {"workload": "make_problem(4096, 1024, 64, 1) (BASELINE config 2's problem), 200 iterations",
+           "note": "wall time of the public run call from host buffers (setup + iterations + download); "
+                   "the dense setup builds and inverts the 4096 x 4096 Gram matrix in fp64 on the GPU"}
+    for name, run in (("admm_dense", cl.admm_dense_run), ("cadmm", cl.cadmm_run)):
+        run(prob.measurements, prob.op, cl.SolverConfig(max_iter=2, check_every=2), device=local_rank)  # warm
+        t0 = time.perf_counter()
+        rep = run(prob.measurements, prob.op, cfg, device=local_rank)
+        wall = time.perf_counter() - t0
+        out[name] = {"seconds": wall, "setup_seconds": rep.setup_seconds,
+                     "iterations_per_s": iters / max(rep.total_seconds - rep.setup_seconds, 1e-12),
+                     "footprint_bytes": rep.footprint_bytes}
+    return out
+
+
 def recovery_line(cl, prob, local_rank, target=1e-4):
     """Time to recovery (paper protocol: stop at MSE(x, x*) <= 1e-4)
     through the public API (ista_run / cadmm_run with truth, check_every=10):
@@ -527,10 +548,11 @@ def main():
                     "note": "same metric and workload, SolverConfig(use_fft=True); L2 flushed between steps"}
         del fst
 
-    admm = recovery = None
+    admm = recovery = dense = None
     if not sharded and w["kind"] == "ista" and w["n"] == (1 << 20) and not args.quick:
         admm = admm_line(cl, torch, prob, local_rank, flush, peaks)
         recovery = recovery_line(cl, prob, local_rank)
+        dense = dense_line(cl, torch, local_rank)
 
     cpu = None
     if rank == 0 and not sharded and not args.no_cpu_baseline:
@@ -600,6 +622,7 @@ def main():
             "e2e": e2e,
             "fft_engine": fft_line,
             "admm": admm,
+            "dense_vs_circulant": dense,
             "time_to_recovery": recovery,
             "cpu_baseline": cpu,
         }

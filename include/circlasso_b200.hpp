@@ -83,6 +83,7 @@ struct SolverConfig {
   int check_every = 10;
   ThresholdPairing pairing = ThresholdPairing::kLiteral;
   bool use_fft = false;  // true: on-device FFT engine (any n); false: direct sm_100a kernels
+  Index dense_cap = 4096;  // circulant.hpp:31 kDenseCap: largest n of the dense ADMM
   int device = 0;       // new: CUDA device of the solve
 
   cl_config c() const {
@@ -99,6 +100,7 @@ struct SolverConfig {
     k.check_every = check_every;
     k.pairing = pairing == ThresholdPairing::kLiteral ? CL_PAIRING_LITERAL : CL_PAIRING_PROXIMAL;
     k.engine = use_fft ? CL_ENGINE_FFT : CL_ENGINE_DIRECT;
+    k.dense_cap = dense_cap;
     return k;
   }
 };
@@ -283,7 +285,8 @@ inline SensingProblem make_problem(Index n, Index m, Index k, std::uint64_t seed
 class DeviceState {
  public:
   DeviceState(int kind, const PartialCirculantOperator& A, const Vector& y, const SolverConfig& cfg) {
-    detail::check_same_size(static_cast<Index>(y.size()), A.m(), kind == CL_KIND_ISTA ? "ista_setup" : "cadmm_setup");
+    detail::check_same_size(static_cast<Index>(y.size()), A.m(),
+                            kind == CL_KIND_ISTA ? "ista_setup" : kind == CL_KIND_CADMM ? "cadmm_setup" : "admm_setup");
     cl_solver* s = nullptr;
     const cl_config c = cfg.c();
     check(cl_solver_create(kind, A.n(), A.m(), A.circulant().first_row().data(), A.mask().omega().data(), y.data(),
@@ -296,7 +299,7 @@ class DeviceState {
   void step(long iters = 1) { check(cl_solver_step(h_.get(), iters)); }
   Vector get(const char* field) const {
     const std::string f(field);
-    Vector out(static_cast<size_t>((f == "r" || f == "y") ? m_ : n_));
+    Vector out(static_cast<size_t>((f == "r" || f == "y") ? m_ : f == "B" ? n_ * n_ : n_));
     check(cl_solver_get(h_.get(), field, out.data()));
     return out;
   }
@@ -329,6 +332,15 @@ inline CadmmState cadmm_setup(const PartialCirculantOperator& A, const Vector& y
   return CadmmState(A, y, cfg);
 }
 inline void cadmm_step(CadmmState& s, bool /*use_fft*/ = true) { s.step(1); }
+// Dense ADMM (solvers.hpp:267-327): B = (A~^T A~ + rho I)^-1 built in fp64 on the GPU; get("B") is n x n.
+struct AdmmState : DeviceState {
+  AdmmState(const PartialCirculantOperator& A, const Vector& y, const SolverConfig& cfg)
+      : DeviceState(CL_KIND_ADMM, A, y, cfg) {}
+};
+inline AdmmState admm_setup(const PartialCirculantOperator& A, const Vector& y, const SolverConfig& cfg) {
+  return AdmmState(A, y, cfg);
+}
+inline void admm_step(AdmmState& s) { s.step(1); }
 
 namespace detail {
 inline RecoveryReport run(DeviceState& st, const Vector* truth, const SolverConfig& cfg, Index n) {
@@ -367,6 +379,13 @@ inline RecoveryReport ista_run(const Vector& y, const PartialCirculantOperator& 
 inline RecoveryReport cadmm_run(const Vector& y, const PartialCirculantOperator& A, const SolverConfig& cfg,
                                 const Vector* truth = nullptr) {
   CadmmState st(A, y, cfg);
+  return detail::run(st, truth, cfg, A.n());
+}
+
+// solvers.hpp:497-514
+inline RecoveryReport admm_dense_run(const Vector& y, const PartialCirculantOperator& A, const SolverConfig& cfg,
+                                     const Vector* truth = nullptr) {
+  AdmmState st(A, y, cfg);
   return detail::run(st, truth, cfg, A.n());
 }
 

@@ -39,7 +39,6 @@
 #include <limits>
 #include <numeric>
 #include <random>
-#include <sstream>
 #include <string>
 #include <thread>
 #include <vector>
@@ -544,11 +543,8 @@ struct Admm {
 static int admm_setup(Admm& st, int64_t n, int64_t m, const double* c, const int64_t* omega, const double* y,
                       double alpha, double rho, int64_t dense_cap, int threads) {
   if (int rc = check_mask(omega, m, n)) return rc;
-  if (n > dense_cap) {
-    std::ostringstream msg;
-    msg << "admm_setup: n = " << n << " exceeds the dense cap " << dense_cap;
-    return fail(ECAPACITY, msg.str());
-  }
+  if (n > dense_cap)  // (no iostreams in this library: it is loaded into processes with other libstdc++ users)
+    return fail(ECAPACITY, "admm_setup: n = " + std::to_string(n) + " exceeds the dense cap " + std::to_string(dense_cap));
   if (!(rho > 0.0)) return fail(EPARAM, "admm_setup: rho must be > 0");
   if (!(alpha > 0.0)) return fail(EPARAM, "admm_setup: alpha must be > 0");
   double s = 1.0;

@@ -101,5 +101,5 @@ for _name, (_res, _args) in _SIGS.items():
 
 EXPORTED = tuple(_SIGS)
 
-if lib.cl_abi_version() != 2:
+if lib.cl_abi_version() != 3:
     raise ImportError("circlasso_b200: C-ABI version mismatch")

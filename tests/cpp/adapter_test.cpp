@@ -49,6 +49,11 @@ static void cpu_checks() {
   y[3] = std::nan("");
   CHECK(throws<cl::DivergenceError>([&] { cl::ista_run(y, p.op, cfg); }));
   CHECK(throws<cl::DimensionError>([&] { cl::ista_run(cl::Vector(15, 0.0), p.op, cfg); }));
+  // dense ADMM: the size check, then the dense cap (solvers.hpp:288-296), before any device work
+  CHECK(throws<cl::DimensionError>([&] { cl::admm_dense_run(cl::Vector(15, 0.0), p.op, cfg); }));
+  cl::SolverConfig capped;
+  capped.dense_cap = 16;
+  CHECK(throws<cl::CapacityError>([&] { cl::admm_dense_run(p.measurements, p.op, capped); }));
   // artifact formats (io.hpp), the same names as the reference
   {
     const cl::PartialCirculantOperator A = cl::gen_circulant_sensing(64, 24, 99);
@@ -96,6 +101,18 @@ static void gpu_checks() {
   prox.pairing = cl::ThresholdPairing::kProximal;
   lit.max_iter = prox.max_iter = 200;
   CHECK(cl::ista_run(p.measurements, p.op, lit).final_x == cl::ista_run(p.measurements, p.op, prox).final_x);
+  // dense ADMM baseline (solvers.hpp:497-514): same recovery as cADMM, dense footprint
+  {
+    cl::SolverConfig dc;
+    dc.target_mse = 1e-4;
+    dc.max_iter = 20000;
+    const cl::RecoveryReport dr = cl::admm_dense_run(p.measurements, p.op, dc, &p.signal.values);
+    CHECK(dr.reached_target && dr.final_metric <= 1e-4);
+    CHECK(dr.footprint_bytes == (256ull * 256 + 4 * 256 + 128) * 4);
+    cl::AdmmState ast = cl::admm_setup(p.op, p.measurements, cl::SolverConfig{});
+    cl::admm_step(ast);
+    CHECK(ast.t() == 1 && ast.get("B").size() == 256u * 256u);
+  }
   // device products vs the fp64 measure
   const cl::Vector ax = cl::partial_matvec(p.op, p.signal.values);
   double err = 0, nrm = 0;

@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     missing = [n for n in sorted(names) if not hasattr(_native.lib, n)]
     assert not missing, missing
     assert set(_native.EXPORTED) == names
-    assert _native.lib.cl_abi_version() == 2
+    assert _native.lib.cl_abi_version() == 3
 
 
 def test_config_defaults_match_reference():
@@ -219,3 +219,18 @@ def test_matvec_scheme_bench_validation_before_device():
         cio.matvec_scheme_bench(8, "circulant", 0)
     with pytest.raises(cl.CapacityError):
         cio.matvec_scheme_bench(cio.kDenseCap + 1, "reference", 1)
+
+
+def test_dense_admm_validation_before_any_device_work():
+    """admm_setup's checks (solvers.hpp:288-296): size, then the dense cap, then rho/alpha -- all raised on
+    the host before the library touches a device, so they hold on a CPU-only machine too."""
+    p = cl.make_problem(256, 128, 25, 11)
+    with pytest.raises(cl.CapacityError, match="exceeds the dense cap 128"):
+        cl.admm_setup(p.op, p.measurements, cl.SolverConfig(dense_cap=128))
+    with pytest.raises(cl.DimensionError):
+        cl.admm_setup(p.op, p.measurements[:-1], cl.SolverConfig(dense_cap=128))
+    with pytest.raises(cl.ParameterError, match="rho"):
+        cl.admm_setup(p.op, p.measurements, cl.SolverConfig(rho=0.0))
+    with pytest.raises(cl.ParameterError, match="alpha"):
+        cl.admm_dense_run(p.measurements, p.op, cl.SolverConfig(alpha=-1.0))
+    assert cl.analytic_footprint(cl.FootprintKind.kDenseAdmm, 256, 128, 4) == (256 * 256 + 4 * 256 + 128) * 4

@@ -289,3 +289,36 @@ def test_phase_sample_full_range_is_a_step():
     assert np.array_equal(ca.get("z"), cb.get("z"))
     with pytest.raises(orc.OracleError):
         b.phase_sample(129, 512)
+
+
+def test_dense_admm_oracle_against_numpy():
+    """The dense ADMM restatement (solvers.hpp:267-327): its Cholesky inverse and iterations against an
+    independent numpy evaluation (np.linalg.inv of A~^T A~ + rho I); the validation order of admm_setup
+    (:288-296: dense cap, then rho, then alpha)."""
+    p = orc.make_problem(192, 96, 10, 4)
+    o = orc.Admm(p.row, p.omega, p.y, alpha=2e-3, rho=0.3)
+    s = orc.spectral_norm(p.row)
+    idx = (np.arange(p.n)[None, :] - p.omega[:, None]) % p.n
+    ad = p.row[idx] / s
+    B = np.linalg.inv(ad.T @ ad + 0.3 * np.eye(p.n))
+    aty = ad.T @ (p.y / s)
+    assert np.max(np.abs(o.get("B") - B)) <= 1e-12 and np.max(np.abs(o.get("aty") - aty)) <= 1e-12
+    x = z = u = np.zeros(p.n)
+    rhs = aty.copy()
+    thr = 2e-3 / 0.3
+    for _ in range(25):
+        x = B @ rhs
+        z = orc.soft_threshold(x + u, thr)
+        u = u + x - z
+        rhs = aty + 0.3 * (z - u)
+    o.step(25)
+    assert np.max(np.abs(o.get("z") - z)) <= 1e-10 and np.max(np.abs(o.get("u") - u)) <= 1e-10
+    assert o.scalars()["threshold"] == thr
+    with pytest.raises(orc.OracleError) as e:
+        orc.Admm(p.row, p.omega, p.y, dense_cap=100)
+    assert e.value.code == orc.ECAPACITY and "exceeds the dense cap 100" in str(e.value)
+    with pytest.raises(orc.OracleError) as e:
+        orc.Admm(p.row, p.omega, p.y, rho=0.0)
+    assert e.value.code == orc.EPARAM
+    rep = orc.run("admm", p.row, p.omega, p.y, truth=p.x_true, max_iter=40, check_every=10)
+    assert rep.iterations == 40 and [t for t, _ in rep.trace] == [10, 20, 30, 40]
