@@ -364,16 +364,13 @@ def main():
     cfg = cl.SolverConfig()
     setup = cl.ista_setup if w["kind"] == "ista" else cl.cadmm_setup
     st = setup(prob.op, prob.measurements, cfg, device=local_rank)
-    shard = gather = None
-    if sharded:
-        shard = cdist.CudaShard(st, rank, world)
-        gather = cdist.TorchGather()
+    comm = None
+    if sharded:  # the library's own NCCL communicator: the slice exchange runs inside cl_solver_step
+        comm = cdist.NativeComm.from_torch(local_rank)
+        comm.attach(st)
 
     def one_step():
-        if shard is None:
-            st.step(1)
-        else:
-            cdist.sharded_step(shard, gather, 1)
+        st.step(1)
 
     import ctypes as C
     from paper_1707_02244_b200._native import lib as L
@@ -487,22 +484,20 @@ def main():
         # rank 0 downloads the iterate; the slowest rank's wall time
         torch.distributed.barrier()
         torch.cuda.synchronize()
+        run = cl.ista_run if w["kind"] == "ista" else cl.cadmm_run
         t0 = time.perf_counter()
-        st2 = setup(prob.op, prob.measurements, cfg, device=local_rank)
-        sh2 = cdist.CudaShard(st2, rank, world)
-        cdist.sharded_step(sh2, gather, args.steps)
-        st2.synchronize()
-        if rank == 0:
-            st2.get("x" if w["kind"] == "ista" else "z")
+        rep = run(prob.measurements, prob.op, cl.SolverConfig(max_iter=args.steps, check_every=args.steps),
+                  device=local_rank, comm=comm)
         e2e_s = time.perf_counter() - t0
+        assert rep.iterations == args.steps
         t = torch.tensor([e2e_s], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
         e2e = {"value": args.steps / e2e_s, "unit": "iterations/s", "h2d_bytes_per_step": world * h2d / args.steps,
                "d2h_bytes_per_step": d2h / args.steps, "wall_s": e2e_s,
-               "note": f"{world} ranks: setup from host fp64 buffers, K sharded iterations with NCCL all-gathers, "
-                       "iterate download on rank 0; max wall time over ranks"}
-        del sh2, st2
+               "note": f"{world} ranks: ista_run/cadmm_run(..., comm=NativeComm) from host fp64 buffers on every "
+                       "rank: setup, K sharded iterations (in-place NCCL broadcasts of the slices inside the "
+                       "library), iterate download; max wall time over ranks"}
 
     # the same workload through the on-device FFT engine (use_fft=True, the reference's default engine)
     fft_line = None
@@ -587,7 +582,8 @@ def main():
                                   if k_name == "k_tc_dense" else
                                   "direct shift-indexed sm_100a kernels"),
                        "l2": "flushed (256 MiB) between steps",
-                       "parallelism": f"row/output shards x{world}" if sharded else "single GPU"},
+                       "parallelism": f"row/output shards x{world} (library-owned NCCL exchange)" if sharded
+                       else "single GPU"},
             "roofline": {"bound": "tensor" if k_name == "k_tc_dense" else "fp32_ffma", "kernel": k_name,
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                          "traffic": traffic, "peak_source": peak_source,

@@ -147,9 +147,11 @@ cl_status cl_solver_step(cl_solver* s, int64_t iters);
 cl_status cl_solver_step_checked(cl_solver* s, double* metric, int* nonfinite);
 /* run_loop solvers.hpp:426-472 + ista_run/cadmm_run :479-534: full solve
  * with the reference's check cadence and stopping rule.  final_x (n, may be
- * NULL) receives x (ISTA) or z (cADMM); trace arrays may be NULL. */
+ * NULL) receives x (ISTA) or z (cADMM, dense ADMM); trace arrays may be NULL:
+ * per check point the iteration, the metric and the seconds since the
+ * iterations started (TracePoint, solvers.hpp:134-137). */
 cl_status cl_solver_run(cl_solver* s, cl_report* rep, double* final_x, int64_t* trace_iter,
-                        double* trace_value, int64_t trace_cap);
+                        double* trace_value, double* trace_seconds, int64_t trace_cap);
 /* Device -> host copy of a state vector by name:
  * ISTA: "x","r","delta","c","y"; cADMM: "x","z","nu","mu","v","beta","c","b","d","pty";
  * dense ADMM: "x","z","u","rhs","aty" (n each) and "B" (n * n, row-major). */
@@ -196,6 +198,46 @@ cl_status cl_shard_ranges(int kind, int64_t n, int64_t m, const int64_t* omega, 
  * and the full vector length, for the caller's all-gather. */
 cl_status cl_solver_phase_output(cl_solver* s, int phase, void** dev_ptr, int64_t* begin,
                                  int64_t* end, int64_t* total);
+
+/* ---- library-owned collectives (NCCL over NVLink) -------------
+ * The sharded solve with the exchange inside the library: after each phase
+ * every rank receives the other ranks' slices of the produced vector in place
+ * (one ncclBroadcast per owner, grouped), on the solver's stream; the check
+ * metrics are summed with one ncclAllReduce.  NCCL (libnccl.so.2) is loaded
+ * at run time; without it these calls fail with CL_ECOMM.
+ *
+ * One process per GPU: rank 0 calls cl_comm_unique_id and hands the 128
+ * bytes to the others (any channel); every rank calls cl_comm_init_rank, then
+ * cl_solver_attach_comm on its solver.  From then on cl_solver_step /
+ * cl_solver_step_checked / cl_solver_run run the sharded iteration and
+ * return the same iterate on every rank, bitwise equal to the unsharded
+ * solve.  The communicator must outlive the solver's use of it. */
+typedef struct cl_comm cl_comm;
+cl_status cl_comm_unique_id(unsigned char* id /* [128] */);                       /* ncclGetUniqueId */
+cl_status cl_comm_init_rank(const unsigned char* id, int world, int rank, int device, cl_comm** out);
+void cl_comm_destroy(cl_comm* c);
+cl_status cl_solver_attach_comm(cl_solver* s, cl_comm* c);
+
+/* One process driving several GPUs (or several shards of one GPU): a group of
+ * `ndev` solvers, rank r on devices[r].  Transport CL_TRANSPORT_NCCL builds
+ * the communicators with ncclCommInitAll and issues every rank's exchange in
+ * one NCCL group; CL_TRANSPORT_COPY exchanges slices with peer copies ordered
+ * by events (devices may repeat: the 2/4/8-rank data plane on one GPU).  The
+ * run loop, stopping rule and report are those of cl_solver_run; get()
+ * assembles a vector from the ranks' slices.  ISTA and cADMM (direct
+ * engine). */
+typedef enum cl_transport { CL_TRANSPORT_NCCL = 0, CL_TRANSPORT_COPY = 1 } cl_transport;
+typedef struct cl_group cl_group;
+cl_status cl_group_create(int kind, int64_t n, int64_t m, const double* c, const int64_t* omega, const double* y,
+                          const cl_config* cfg, const int* devices, int ndev, int transport, cl_group** out);
+void cl_group_destroy(cl_group* g);
+cl_status cl_group_set_truth(cl_group* g, const double* truth_n);
+cl_status cl_group_step(cl_group* g, int64_t iters);
+cl_status cl_group_run(cl_group* g, cl_report* rep, double* final_x, int64_t* trace_iter, double* trace_value,
+                       double* trace_seconds, int64_t trace_cap);
+cl_status cl_group_get(cl_group* g, const char* field, double* out);
+cl_status cl_group_synchronize(cl_group* g);
+cl_status cl_group_info(cl_group* g, int* world, int64_t* t, int* transport);
 
 /* ---- artifact formats (io.hpp:1-170) -------------------------------------
  * Vectors: magic "CIRCVEC1", u64 length, little-endian f64 data.

@@ -343,18 +343,15 @@ inline AdmmState admm_setup(const PartialCirculantOperator& A, const Vector& y, 
 inline void admm_step(AdmmState& s) { s.step(1); }
 
 namespace detail {
-inline RecoveryReport run(DeviceState& st, const Vector* truth, const SolverConfig& cfg, Index n) {
-  if (truth) {
-    check_same_size(static_cast<Index>(truth->size()), n, "truth");
-    check(cl_solver_set_truth(st.handle(), truth->data()));
-  }
+template <typename RunFn>
+inline RecoveryReport run_with(RunFn run_fn, const SolverConfig& cfg, Index n) {
   const long cap = cfg.max_iter >= 0 ? cfg.max_iter / (cfg.check_every > 0 ? cfg.check_every : 1) + 2 : 0;
   std::vector<int64_t> it(static_cast<size_t>(cap > 0 ? cap : 1));
-  std::vector<double> val(it.size());
+  std::vector<double> val(it.size()), sec(it.size());
   RecoveryReport rep;
   rep.final_x.resize(static_cast<size_t>(n));
   cl_report r{};
-  check(cl_solver_run(st.handle(), &r, rep.final_x.data(), it.data(), val.data(), cap));
+  check(run_fn(&r, rep.final_x.data(), it.data(), val.data(), sec.data(), static_cast<int64_t>(cap)));
   rep.iterations = static_cast<long>(r.iterations);
   rep.setup_seconds = r.setup_seconds;
   rep.total_seconds = r.total_seconds;
@@ -364,8 +361,19 @@ inline RecoveryReport run(DeviceState& st, const Vector* truth, const SolverConf
   rep.final_metric = r.final_metric;
   for (int64_t i = 0; i < r.trace_len && i < cap; ++i)
     rep.mse_trace.push_back({static_cast<long>(it[static_cast<size_t>(i)]), val[static_cast<size_t>(i)],
-                             std::numeric_limits<double>::quiet_NaN()});
+                             sec[static_cast<size_t>(i)]});
   return rep;
+}
+inline RecoveryReport run(DeviceState& st, const Vector* truth, const SolverConfig& cfg, Index n) {
+  if (truth) {
+    check_same_size(static_cast<Index>(truth->size()), n, "truth");
+    check(cl_solver_set_truth(st.handle(), truth->data()));
+  }
+  return run_with(
+      [&](cl_report* r, double* fx, int64_t* it, double* val, double* sec, int64_t cap) {
+        return cl_solver_run(st.handle(), r, fx, it, val, sec, cap);
+      },
+      cfg, n);
 }
 }  // namespace detail
 
@@ -388,6 +396,57 @@ inline RecoveryReport admm_dense_run(const Vector& y, const PartialCirculantOper
   AdmmState st(A, y, cfg);
   return detail::run(st, truth, cfg, A.n());
 }
+
+// ---- sharded solve from one process (cl_group_*) -----------------------
+// Rank r on devices[r]; after each phase the ranks exchange their slices inside the library: NCCL
+// (ncclCommInitAll over the listed GPUs) or peer copies (Transport::kCopy; devices may repeat).  The
+// iterate equals the unsharded solve's bitwise.  One process per GPU instead: cl_comm_init_rank +
+// cl_solver_attach_comm on a DeviceState's handle.
+enum class Transport { kNccl = CL_TRANSPORT_NCCL, kCopy = CL_TRANSPORT_COPY };
+class ShardedSolve {
+ public:
+  ShardedSolve(int kind, const PartialCirculantOperator& A, const Vector& y, const SolverConfig& cfg,
+               const std::vector<int>& devices, Transport transport = Transport::kNccl)
+      : cfg_(cfg), n_(A.n()), m_(A.m()) {
+    detail::check_same_size(static_cast<Index>(y.size()), A.m(), kind == CL_KIND_ISTA ? "ista_setup" : "cadmm_setup");
+    cl_group* g = nullptr;
+    const cl_config c = cfg.c();
+    check(cl_group_create(kind, A.n(), A.m(), A.circulant().first_row().data(), A.mask().omega().data(), y.data(), &c,
+                          devices.data(), static_cast<int>(devices.size()), static_cast<int>(transport), &g));
+    g_.reset(g);
+  }
+  void step(long iters = 1) { check(cl_group_step(g_.get(), iters)); }
+  Vector get(const char* field) const {
+    const std::string f(field);
+    Vector out(static_cast<size_t>((f == "r" || f == "y") ? m_ : n_));
+    check(cl_group_get(g_.get(), field, out.data()));
+    return out;
+  }
+  int world() const {
+    int w = 0;
+    check(cl_group_info(g_.get(), &w, nullptr, nullptr));
+    return w;
+  }
+  RecoveryReport run(const Vector* truth = nullptr) {
+    if (truth) {
+      detail::check_same_size(static_cast<Index>(truth->size()), n_, "truth");
+      check(cl_group_set_truth(g_.get(), truth->data()));
+    }
+    return detail::run_with(
+        [&](cl_report* r, double* fx, int64_t* it, double* val, double* sec, int64_t cap) {
+          return cl_group_run(g_.get(), r, fx, it, val, sec, cap);
+        },
+        cfg_, n_);
+  }
+
+ private:
+  struct Del {
+    void operator()(cl_group* g) const { cl_group_destroy(g); }
+  };
+  std::unique_ptr<cl_group, Del> g_;
+  SolverConfig cfg_;
+  Index n_ = 0, m_ = 0;
+};
 
 // ---- artifact formats (io.hpp) ---------------------------------------------------
 inline void write_vector(const Vector& v, const std::string& path) {  // io.hpp:80-87

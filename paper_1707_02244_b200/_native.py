@@ -68,7 +68,7 @@ _SIGS = {
     "cl_solver_set_truth": (C.c_int, [_vp, _d]),
     "cl_solver_step": (C.c_int, [_vp, C.c_int64]),
     "cl_solver_step_checked": (C.c_int, [_vp, _d, C.POINTER(C.c_int)]),
-    "cl_solver_run": (C.c_int, [_vp, C.POINTER(cl_report), _d, _i64, _d, C.c_int64]),
+    "cl_solver_run": (C.c_int, [_vp, C.POINTER(cl_report), _d, _i64, _d, _d, C.c_int64]),
     "cl_solver_get": (C.c_int, [_vp, C.c_char_p, _d]),
     "cl_solver_set": (C.c_int, [_vp, C.c_char_p, _d]),
     "cl_solver_info": (C.c_int, [_vp, _i64, _i64, _i64, _d, _d]),
@@ -83,6 +83,19 @@ _SIGS = {
     "cl_solver_phase_output": (C.c_int, [_vp, C.c_int, C.POINTER(_vp), _i64, _i64, _i64]),
     "cl_shard_ranges": (C.c_int, [C.c_int, C.c_int64, C.c_int64, _i64, C.c_int, C.c_int, _i64, _i64, _i64, _i64]),
     "cl_ffma_peak": (C.c_int, [C.c_int, _d]),
+    "cl_comm_unique_id": (C.c_int, [C.c_char_p]),
+    "cl_comm_init_rank": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)]),
+    "cl_comm_destroy": (None, [_vp]),
+    "cl_solver_attach_comm": (C.c_int, [_vp, _vp]),
+    "cl_group_create": (C.c_int, [C.c_int, C.c_int64, C.c_int64, _d, _i64, _d, C.POINTER(cl_config),
+                                  C.POINTER(C.c_int), C.c_int, C.c_int, C.POINTER(_vp)]),
+    "cl_group_destroy": (None, [_vp]),
+    "cl_group_set_truth": (C.c_int, [_vp, _d]),
+    "cl_group_step": (C.c_int, [_vp, C.c_int64]),
+    "cl_group_run": (C.c_int, [_vp, C.POINTER(cl_report), _d, _i64, _d, _d, C.c_int64]),
+    "cl_group_get": (C.c_int, [_vp, C.c_char_p, _d]),
+    "cl_group_synchronize": (C.c_int, [_vp]),
+    "cl_group_info": (C.c_int, [_vp, C.POINTER(C.c_int), _i64, C.POINTER(C.c_int)]),
     "cl_write_vector": (C.c_int, [C.c_char_p, _d, C.c_int64]),
     "cl_read_vector": (C.c_int, [C.c_char_p, _d, C.c_int64, _i64]),
     "cl_write_operator": (C.c_int, [C.c_char_p, C.c_int64, C.c_int64, _d, _i64]),

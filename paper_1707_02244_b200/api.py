@@ -661,34 +661,46 @@ def admm_step(state: AdmmState):
     state.step(1)
 
 
-def _run(state: _DeviceState, truth, cfg: SolverConfig) -> RecoveryReport:
-    if truth is not None:
-        state.set_truth(truth)
+def _report(call, n: int, cfg: SolverConfig) -> RecoveryReport:
     rep = cl_report()
     cap = (int(cfg.max_iter) // max(int(cfg.check_every), 1)) + 2 if cfg.max_iter >= 0 else 0
     cap = min(cap, 1 << 22)
     tit = np.zeros(max(cap, 1), dtype=np.int64)
     tval = np.zeros(max(cap, 1))
-    fx = np.zeros(state._n)
-    _check(lib.cl_solver_run(state.handle, C.byref(rep), _pd(fx), _pi(tit), _pd(tval), cap))
-    trace = [TracePoint(int(tit[i]), float(tval[i])) for i in range(min(rep.trace_len, cap))]
+    tsec = np.zeros(max(cap, 1))
+    fx = np.zeros(n)
+    _check(call(C.byref(rep), _pd(fx), _pi(tit), _pd(tval), _pd(tsec), cap))
+    trace = [TracePoint(int(tit[i]), float(tval[i]), float(tsec[i])) for i in range(min(rep.trace_len, cap))]
     return RecoveryReport(final_x=fx, iterations=rep.iterations, mse_trace=trace, setup_seconds=rep.setup_seconds,
                           total_seconds=rep.total_seconds, footprint_bytes=rep.footprint_bytes,
                           metric=StopMetric(rep.metric), reached_target=bool(rep.reached_target),
                           final_metric=rep.final_metric)
 
 
-def ista_run(y, A: PartialCirculantOperator, cfg: SolverConfig = None, truth=None, device: int = 0) -> RecoveryReport:
-    """solvers.hpp:479-495"""
+def _run(state: _DeviceState, truth, cfg: SolverConfig) -> RecoveryReport:
+    if truth is not None:
+        state.set_truth(truth)
+    return _report(lambda *a: lib.cl_solver_run(state.handle, *a), state._n, cfg)
+
+
+def ista_run(y, A: PartialCirculantOperator, cfg: SolverConfig = None, truth=None, device: int = 0,
+             comm=None) -> RecoveryReport:
+    """solvers.hpp:479-495.  ``comm`` (dist.NativeComm): this process's rank of a sharded solve; every rank
+    makes the same call and gets the same report."""
     cfg = cfg or SolverConfig()
     st = ista_setup(A, y, cfg, device)
+    if comm is not None:
+        comm.attach(st)
     return _run(st, truth, cfg)
 
 
-def cadmm_run(y, A: PartialCirculantOperator, cfg: SolverConfig = None, truth=None, device: int = 0) -> RecoveryReport:
-    """solvers.hpp:518-534"""
+def cadmm_run(y, A: PartialCirculantOperator, cfg: SolverConfig = None, truth=None, device: int = 0,
+              comm=None) -> RecoveryReport:
+    """solvers.hpp:518-534 (``comm`` as for ista_run)"""
     cfg = cfg or SolverConfig()
     st = cadmm_setup(A, y, cfg, device)
+    if comm is not None:
+        comm.attach(st)
     return _run(st, truth, cfg)
 
 
@@ -698,6 +710,62 @@ def admm_dense_run(y, A: PartialCirculantOperator, cfg: SolverConfig = None, tru
     cfg = cfg or SolverConfig()
     st = admm_setup(A, y, cfg, device)
     return _run(st, truth, cfg)
+
+
+class ShardedSolve:
+    """A sharded ISTA / cADMM solve driven from one process (cl_group_*): rank r on devices[r],
+    the slice exchange after every phase inside the library -- NCCL (``transport="nccl"``: ncclCommInitAll,
+    one grouped set of in-place broadcasts per phase) or peer copies (``"copy"``: devices may repeat, e.g.
+    [0, 0, 0, 0] runs the 4-rank data plane on one GPU).  Same iterate as the unsharded solve, bitwise."""
+
+    TRANSPORTS = {"nccl": 0, "copy": 1}
+
+    def __init__(self, kind: str, A: PartialCirculantOperator, y, cfg: SolverConfig = None, devices=(0,),
+                 transport: str = "nccl"):
+        cfg = cfg or SolverConfig()
+        y = _f64(y)
+        if len(y) != A.m():
+            raise DimensionError(f"{kind}_setup: dimension mismatch, {len(y)} vs {A.m()}")
+        self.kind = {"ista": 0, "cadmm": 1}[kind]
+        self.cfg = cfg
+        self._n, self._m = A.n(), A.m()
+        devs = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        c = cfg._c()
+        _check(lib.cl_group_create(self.kind, A.n(), A.m(), _pd(A.circulant().first_row()), _pi(A.mask().omega()),
+                                   _pd(y), C.byref(c), devs, len(devices), self.TRANSPORTS[transport],
+                                   C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.cl_group_destroy(h)
+            self._h = None
+
+    def step(self, iters: int = 1):
+        _check(lib.cl_group_step(self._h, int(iters)))
+
+    def synchronize(self):
+        _check(lib.cl_group_synchronize(self._h))
+
+    def get(self, name: str) -> np.ndarray:
+        out = np.zeros(self._m if name in ("r", "y") else self._n)
+        _check(lib.cl_group_get(self._h, name.encode(), _pd(out)))
+        return out
+
+    def info(self):
+        w, t, tr = C.c_int(), C.c_int64(), C.c_int()
+        _check(lib.cl_group_info(self._h, C.byref(w), C.byref(t), C.byref(tr)))
+        return {"world": w.value, "t": t.value, "transport": tr.value}
+
+    def run(self, truth=None) -> RecoveryReport:
+        if truth is not None:
+            t = _f64(truth)
+            if len(t) != self._n:
+                raise DimensionError("truth: dimension mismatch")
+            _check(lib.cl_group_set_truth(self._h, _pd(t)))
+        return _report(lambda *a: lib.cl_group_run(self._h, *a), self._n, self.cfg)
 
 
 def device_count() -> int:

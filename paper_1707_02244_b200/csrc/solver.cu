@@ -28,6 +28,7 @@
 #include "kernels.cuh"
 #include "tc_dense.cuh"
 #include "dense.cuh"
+#include "comm.hpp"
 
 namespace clb {
 void gen_sparse_signal(int64_t n, int64_t k, uint64_t seed, double* values, int64_t* support);
@@ -259,6 +260,10 @@ struct Solver {
   ConvPlan rplan;    // ISTA residual (input tiles x position splits)
   bool ista_tc = false;  // ISTA products embedded in dense tensor-core products (plan == rplan, tc)
   int64_t row_lo = 0, row_hi = 0;  // ISTA rows owned (residual)
+  // library-owned collective of a sharded solve (cl_solver_attach_comm) and every rank's slices:
+  // rows_of[r] = ISTA residual rows of rank r, outs_of[r] = outputs of rank r
+  Comm* comm = nullptr;
+  std::vector<std::pair<int64_t, int64_t>> rows_of, outs_of;
   int64_t out_lo = 0, out_hi = 0;  // outputs owned
 
   DevBuf<float> hc, hcr, hbr;      // c~, c~ reversed, b reversed
@@ -1083,7 +1088,64 @@ struct Solver {
     nphase = 6;
   }
 
+  // ---- sharded iteration ------------------------------------------
+  // Phases of one iteration and, per phase, the vector it produces and whose slices the ranks exchange:
+  // ISTA 0 residual -> r (rows), 1 gradient + update -> x (outputs); cADMM 0 beta, 1 x = B beta, 2 duals -> v.
+  int phase_count() const { return kind == CL_KIND_ISTA ? 2 : 3; }
+  void run_phase_only(int ph, int want) {
+    if (kind == CL_KIND_ISTA) {
+      if (ph == 0) ista_residual();
+      else ista_gradient(want);
+    } else {
+      if (ph == 0) admm_beta_phase();
+      else if (ph == 1) admm_x_phase();
+      else admm_dual_phase(want);
+    }
+  }
+  float* phase_buffer(int ph) const {
+    if (kind == CL_KIND_ISTA) return ph == 0 ? r.p : x.p;
+    return ph == 0 ? beta.p : ph == 1 ? x.p : v.p;
+  }
+  const std::vector<std::pair<int64_t, int64_t>>& phase_ranges(int ph) const {
+    return kind == CL_KIND_ISTA && ph == 0 ? rows_of : outs_of;
+  }
+  // every rank's slices, from the same pure host logic each rank runs (cl_shard_ranges)
+  void all_ranges() {
+    rows_of.clear();
+    outs_of.clear();
+    for (int q = 0; q < world; ++q) {
+      ConvPlan pq = plan, rq = rplan;
+      int64_t ol, oh, rl, rh;
+      shard_ranges(kind, n, omega_host.data(), m, q, world, &pq, &rq, &ol, &oh, &rl, &rh);
+      rows_of.emplace_back(rl, rh);
+      outs_of.emplace_back(ol, oh);
+    }
+  }
+  void attach_comm(Comm* c) {
+    if (c->device != device) raise(CL_EPARAM, "cl_solver_attach_comm: the communicator's device is not the solver's");
+    if (fft && c->world != 1) raise(CL_EPARAM, "cl_solver_attach_comm: the FFT engine runs unsharded (replicas only)");
+    if (kind == CL_KIND_ADMM && c->world != 1) raise(CL_EPARAM, "cl_solver_attach_comm: the dense ADMM runs unsharded");
+    CU(cudaStreamSynchronize(st));
+    set_shard(c->rank, c->world);
+    comm = c;
+    all_ranges();
+  }
+  // one iteration of a solver sharded over a communicator: phase, in-place all-gather of the produced
+  // slices on the solver stream, next phase ...
+  void comm_step(int want) {
+    for (int ph = 0; ph < phase_count(); ++ph) {
+      run_phase_only(ph, want && ph == phase_count() - 1);
+      comm_gather(comm, phase_buffer(ph), phase_ranges(ph), st);
+    }
+    CU(cudaGetLastError());
+    ++t;
+  }
+
   void one_step(int want) {
+    if (world != 1 && comm) {
+      comm_step(want);
+      return;
+    }
     if (world != 1) raise(CL_EPARAM, "cl_solver_step: sharded solvers advance with cl_solver_run_phase");
     if (kind == CL_KIND_ADMM) {
       admm_dense_step(want);
@@ -1266,13 +1328,38 @@ struct Solver {
   void step_checked(double* metric, int* nonfinite) {
     one_step(1);
     launch_metrics_final(blk.p, met.p, st);
+    if (world != 1 && comm) comm_allreduce_sum(comm, met.p, 3, st);  // every rank's share of the sums
     CU(cudaMemcpyAsync(met_host, met.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     collect_profile();
+    metric_from(met_host, metric, nonfinite);
+  }
+  void metric_from(const double* mh, double* metric, int* nonfinite) const {
     const double nn = static_cast<double>(n);
-    *nonfinite = met_host[2] > 0.0;
-    if (has_truth) *metric = n > 0 ? met_host[1] / nn : 0.0;
-    else *metric = std::sqrt(met_host[0]) * (n > 0 ? 1.0 / std::sqrt(nn) : 1.0);
+    *nonfinite = mh[2] > 0.0;
+    if (has_truth) *metric = n > 0 ? mh[1] / nn : 0.0;
+    else *metric = std::sqrt(mh[0]) * (n > 0 ? 1.0 / std::sqrt(nn) : 1.0);
+  }
+  void download_iterate(double* out) { download(iterate_full(), n, out); }
+  // optional ground truth: the check metric becomes the MSE (run_loop solvers.hpp:437)
+  void set_truth(const double* truth_n) {
+    CU(cudaSetDevice(device));
+    if (!truth_n) {
+      has_truth = false;
+      return;
+    }
+    const std::vector<float> tf = to_f32(truth_n, n);
+    truth.alloc(static_cast<size_t>(n), st);
+    truth.upload(tf.data(), tf.size(), st);
+    CU(cudaStreamSynchronize(st));
+    has_truth = true;
+  }
+  // the reported iterate, complete on this rank (cADMM's z is slice-local in a sharded solve)
+  float* iterate_full() {
+    int64_t len = 0;
+    float* p = field_ptr(kind == CL_KIND_ISTA ? "x" : "z", &len);
+    if (world != 1 && comm && kind != CL_KIND_ISTA) comm_gather(comm, p, outs_of, st);
+    return p;
   }
 
   // device fp32 -> host fp64 through the pooled pinned staging buffer
@@ -1441,6 +1528,192 @@ struct ScratchProduct {
     CU(cudaStreamDestroy(st));
     for (int64_t i = 0; i < n; ++i) out[i] = res[static_cast<size_t>(i)];
   }
+};
+
+// run_loop solvers.hpp:426-472 (+ ista_run / cadmm_run / admm_dense_run :479-534) over a single solver
+// or a group of shards: S provides step(k), step_checked(&value, &nonfinite), download_iterate(out), and
+// kind / n / m / has_truth / setup_seconds.
+template <typename S>
+void run_loop(S& s, const cl_config& cfg, cl_report* rep, double* final_x, int64_t* trace_iter, double* trace_value,
+              double* trace_seconds, int64_t trace_cap) {
+  if (cfg.max_iter < 0) raise(CL_EPARAM, "solver: max_iter must be >= 0");         // solvers.hpp:432
+  if (cfg.check_every < 1) raise(CL_EPARAM, "solver: check_every must be >= 1");  // :433-434
+  const auto t0 = std::chrono::steady_clock::now();
+  std::memset(rep, 0, sizeof(*rep));
+  rep->metric = s.has_truth ? CL_METRIC_MSE_VS_TRUTH : CL_METRIC_ITERATE_CHANGE;
+  rep->final_metric = std::numeric_limits<double>::quiet_NaN();
+  const bool has_target = !std::isnan(cfg.target_mse);
+  int64_t t = 0, tl = 0;
+  while (t < cfg.max_iter) {
+    // next check point: t % check_every == 0 or t == max_iter (solvers.hpp:452)
+    int64_t next = ((t / cfg.check_every) + 1) * cfg.check_every;
+    if (next > cfg.max_iter) next = cfg.max_iter;
+    if (next - t > 1) s.step(next - t - 1);
+    trace("run: unchecked steps queued");
+    double value = 0.0;
+    int nonfinite = 0;
+    s.step_checked(&value, &nonfinite);
+    trace("run: checked step (sync)");
+    t = next;
+    if (nonfinite)
+      raise(CL_EDIVERGE, s.kind == CL_KIND_ISTA    ? "ista_run: iterate became non-finite"
+                       : s.kind == CL_KIND_CADMM ? "cadmm_run: iterate became non-finite"
+                                                 : "admm_dense_run: iterate became non-finite");
+    if (tl < trace_cap) {
+      if (trace_iter) trace_iter[tl] = t;
+      if (trace_value) trace_value[tl] = value;
+      if (trace_seconds) trace_seconds[tl] = seconds_since(t0);  // TracePoint::elapsed_seconds (:457-459)
+    }
+    ++tl;
+    rep->final_metric = value;
+    if (has_target && value <= cfg.target_mse) {
+      rep->reached_target = 1;
+      break;
+    }
+  }
+  rep->iterations = t;
+  rep->trace_len = tl;
+  rep->setup_seconds = s.setup_seconds;
+  rep->total_seconds = seconds_since(t0) + s.setup_seconds;
+  rep->footprint_bytes = footprint(s.kind, s.n, s.m, sizeof(float));
+  if (final_x) {
+    s.download_iterate(final_x);
+    trace("run: iterate download");
+  }
+}
+
+// ---- a sharded solve driven from one process (cl_group_*) --------------------------------
+// One Solver per rank, each on its own device and stream, sharded (rank, world).  An iteration runs phase
+// by phase across the ranks; after each phase the produced slices are exchanged:
+//  * kNccl: one NCCL communicator per device (ncclCommInitAll), the ranks' in-place broadcasts issued
+//    in one NCCL group (a single thread drives every device);
+//  * kCopy: device-to-device copies ordered by events (ranks may share a device; the exchange and phase
+//    logic of the NCCL path without NCCL -- the one-GPU test of the 2/4/8-rank data plane).
+struct Group {
+  enum Transport { kNccl = CL_TRANSPORT_NCCL, kCopy = CL_TRANSPORT_COPY };
+  int kind = 0;
+  int64_t n = 0, m = 0;
+  bool has_truth = false;
+  double setup_seconds = 0.0;
+  Transport transport = kNccl;
+  std::vector<std::unique_ptr<Solver>> ranks;
+  std::vector<Comm*> comms;
+  std::vector<cudaEvent_t> done;  // per rank: its phase finished (kCopy)
+
+  ~Group() {
+    for (auto& s : ranks)
+      if (s) {
+        cudaSetDevice(s->device);
+        cudaStreamSynchronize(s->st);
+      }
+    for (auto e : done) cudaEventDestroy(e);
+    ranks.clear();
+    for (Comm* c : comms) comm_destroy(c);
+  }
+  int world() const { return static_cast<int>(ranks.size()); }
+
+  void exchange(int ph) {
+    if (world() == 1) return;
+    if (transport == kNccl) {
+      comm_group_start();
+      for (auto& s : ranks) {
+        CU(cudaSetDevice(s->device));
+        comm_gather(s->comm, s->phase_buffer(ph), s->phase_ranges(ph), s->st);
+      }
+      comm_group_end();
+      return;
+    }
+    for (int r = 0; r < world(); ++r) {
+      CU(cudaSetDevice(ranks[static_cast<size_t>(r)]->device));
+      CU(cudaEventRecord(done[static_cast<size_t>(r)], ranks[static_cast<size_t>(r)]->st));
+    }
+    for (int q = 0; q < world(); ++q) {
+      Solver& dst = *ranks[static_cast<size_t>(q)];
+      CU(cudaSetDevice(dst.device));
+      for (int r = 0; r < world(); ++r) {
+        if (r == q) continue;
+        Solver& src = *ranks[static_cast<size_t>(r)];
+        const auto rg = src.phase_ranges(ph)[static_cast<size_t>(r)];
+        if (rg.second <= rg.first) continue;
+        CU(cudaStreamWaitEvent(dst.st, done[static_cast<size_t>(r)], 0));
+        CU(cudaMemcpyPeerAsync(dst.phase_buffer(ph) + rg.first, dst.device, src.phase_buffer(ph) + rg.first,
+                               src.device, sizeof(float) * static_cast<size_t>(rg.second - rg.first), dst.st));
+      }
+    }
+  }
+  void iteration(int want) {
+    const int np = ranks.front()->phase_count();
+    for (int ph = 0; ph < np; ++ph) {
+      for (auto& s : ranks) {
+        CU(cudaSetDevice(s->device));
+        s->run_phase_only(ph, want && ph == np - 1);
+      }
+      exchange(ph);
+    }
+    for (auto& s : ranks) {
+      CU(cudaGetLastError());
+      ++s->t;
+    }
+  }
+  void step(int64_t iters) {
+    for (int64_t k = 0; k < iters; ++k) iteration(0);
+  }
+  void step_checked(double* metric, int* nonfinite) {
+    iteration(1);
+    double sum[3] = {0, 0, 0};
+    if (transport == kNccl) {
+      for (auto& s : ranks) {
+        CU(cudaSetDevice(s->device));
+        launch_metrics_final(s->blk.p, s->met.p, s->st);
+      }
+      if (world() > 1) {
+        comm_group_start();
+        for (auto& s : ranks) {
+          CU(cudaSetDevice(s->device));
+          comm_allreduce_sum(s->comm, s->met.p, 3, s->st);
+        }
+        comm_group_end();
+      }
+      Solver& s0 = *ranks.front();
+      CU(cudaSetDevice(s0.device));
+      CU(cudaMemcpyAsync(s0.met_host, s0.met.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, s0.st));
+      CU(cudaStreamSynchronize(s0.st));
+      for (int i = 0; i < 3; ++i) sum[i] = s0.met_host[i];
+    } else {  // every rank's share, summed in rank order
+      for (auto& s : ranks) {
+        CU(cudaSetDevice(s->device));
+        launch_metrics_final(s->blk.p, s->met.p, s->st);
+        CU(cudaMemcpyAsync(s->met_host, s->met.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, s->st));
+      }
+      for (auto& s : ranks) {
+        CU(cudaSetDevice(s->device));
+        CU(cudaStreamSynchronize(s->st));
+        for (int i = 0; i < 3; ++i) sum[i] += s->met_host[i];
+      }
+    }
+    const double full[4] = {sum[0], sum[1], sum[2], 0.0};
+    ranks.front()->metric_from(full, metric, nonfinite);
+  }
+  // a vector assembled from the ranks' slices (complete whether or not the field is exchanged)
+  void get(const std::string& f, double* out) {
+    int64_t len = 0;
+    for (int r = 0; r < world(); ++r) {
+      Solver& s = *ranks[static_cast<size_t>(r)];
+      CU(cudaSetDevice(s.device));
+      float* p = s.field_ptr(f, &len);
+      std::vector<double> tmp(static_cast<size_t>(len));
+      s.download(p, len, tmp.data());
+      const bool rows = kind == CL_KIND_ISTA && (f == "r" || f == "y");
+      std::pair<int64_t, int64_t> rg = rows ? s.rows_of[static_cast<size_t>(r)] : s.outs_of[static_cast<size_t>(r)];
+      if (f == "c" || f == "y" || f == "b" || f == "d" || f == "pty") rg = {r == 0 ? 0 : len, r == 0 ? len : len};
+      for (int64_t i = rg.first; i < rg.second && i < len; ++i) out[i] = tmp[static_cast<size_t>(i)];
+    }
+    if (f == "b") {  // stored reversed on the device
+      std::vector<double> tmp(out, out + len);
+      for (int64_t k = 0; k < len; ++k) out[k] = tmp[static_cast<size_t>((len - k) % len)];
+    }
+  }
+  void download_iterate(double* out) { get(kind == CL_KIND_ISTA ? "x" : "z", out); }
 };
 
 }  // namespace clb
@@ -1810,17 +2083,7 @@ void cl_solver_destroy(cl_solver* s) {
 
 cl_status cl_solver_set_truth(cl_solver* h, const double* truth_n) {
   CL_GUARD_BEGIN
-  Solver& s = *h->impl;
-  CU(cudaSetDevice(s.device));
-  if (!truth_n) {
-    s.has_truth = false;
-  } else {
-    const std::vector<float> tf = to_f32(truth_n, s.n);
-    s.truth.alloc(static_cast<size_t>(s.n), s.st);
-    s.truth.upload(tf.data(), tf.size(), s.st);
-    CU(cudaStreamSynchronize(s.st));
-    s.has_truth = true;
-  }
+  h->impl->set_truth(truth_n);
   CL_GUARD_END
 }
 
@@ -1842,54 +2105,11 @@ cl_status cl_solver_step_checked(cl_solver* h, double* metric, int* nonfinite) {
 }
 
 cl_status cl_solver_run(cl_solver* h, cl_report* rep, double* final_x, int64_t* trace_iter, double* trace_value,
-                        int64_t trace_cap) {
+                        double* trace_seconds, int64_t trace_cap) {
   CL_GUARD_BEGIN
   Solver& s = *h->impl;
   CU(cudaSetDevice(s.device));
-  const cl_config& cfg = s.cfg;
-  if (cfg.max_iter < 0) raise(CL_EPARAM, "solver: max_iter must be >= 0");   // solvers.hpp:432
-  if (cfg.check_every < 1) raise(CL_EPARAM, "solver: check_every must be >= 1");  // :433-434
-  const auto t0 = std::chrono::steady_clock::now();
-  std::memset(rep, 0, sizeof(*rep));
-  rep->metric = s.has_truth ? CL_METRIC_MSE_VS_TRUTH : CL_METRIC_ITERATE_CHANGE;
-  rep->final_metric = std::numeric_limits<double>::quiet_NaN();
-  const bool has_target = !std::isnan(cfg.target_mse);
-  int64_t t = 0, tl = 0;
-  while (t < cfg.max_iter) {
-    // next check point: t % check_every == 0 or t == max_iter (solvers.hpp:452)
-    int64_t next = ((t / cfg.check_every) + 1) * cfg.check_every;
-    if (next > cfg.max_iter) next = cfg.max_iter;
-    if (next - t > 1) s.step(next - t - 1);
-    trace("run: unchecked steps queued");
-    double value = 0.0;
-    int nonfinite = 0;
-    s.step_checked(&value, &nonfinite);
-    trace("run: checked step (sync)");
-    t = next;
-    if (nonfinite)
-      raise(CL_EDIVERGE, s.kind == CL_KIND_ISTA    ? "ista_run: iterate became non-finite"
-                       : s.kind == CL_KIND_CADMM ? "cadmm_run: iterate became non-finite"
-                                                 : "admm_dense_run: iterate became non-finite");
-    if (trace_iter && tl < trace_cap) trace_iter[tl] = t;
-    if (trace_value && tl < trace_cap) trace_value[tl] = value;
-    ++tl;
-    rep->final_metric = value;
-    if (has_target && value <= cfg.target_mse) {
-      rep->reached_target = 1;
-      break;
-    }
-  }
-  rep->iterations = t;
-  rep->trace_len = tl;
-  rep->setup_seconds = s.setup_seconds;
-  rep->total_seconds = seconds_since(t0) + s.setup_seconds;
-  rep->footprint_bytes = footprint(s.kind, s.n, s.m, sizeof(float));
-  if (final_x) {
-    int64_t len = 0;
-    float* p = s.field_ptr(s.kind == CL_KIND_ISTA ? "x" : "z", &len);
-    s.download(p, len, final_x);
-    trace("run: iterate download");
-  }
+  run_loop(s, s.cfg, rep, final_x, trace_iter, trace_value, trace_seconds, trace_cap);
   CL_GUARD_END
 }
 
@@ -1999,6 +2219,7 @@ cl_status cl_solver_phase_history(cl_solver* h, double* ms, int64_t max_steps, i
 
 cl_status cl_solver_shard(cl_solver* h, int rank, int world) {
   CL_GUARD_BEGIN
+  h->impl->comm = nullptr;  // caller-driven exchange (cl_solver_run_phase) from here on
   h->impl->set_shard(rank, world);
   CL_GUARD_END
 }
@@ -2070,6 +2291,132 @@ cl_status cl_shard_ranges(int kind, int64_t n, int64_t m, const int64_t* omega, 
   ConvPlan plan = (kind == CL_KIND_ISTA ? (ista_uses_tc(n) ? make_dense_plan(n) : make_plan(n, grad_R(n))) : make_dense_plan(n));
   ConvPlan rplan = make_plan(n, res_R(n));
   shard_ranges(kind, n, omega, m, rank, world, &plan, &rplan, out_lo, out_hi, row_lo, row_hi);
+  CL_GUARD_END
+}
+
+struct cl_comm {
+  Comm* c = nullptr;
+};
+struct cl_group {
+  std::unique_ptr<Group> g;
+};
+
+cl_status cl_comm_unique_id(unsigned char* id) {
+  CL_GUARD_BEGIN
+  if (!id) raise(CL_EPARAM, "cl_comm_unique_id: null buffer");
+  comm_unique_id(id);
+  CL_GUARD_END
+}
+cl_status cl_comm_init_rank(const unsigned char* id, int world, int rank, int device, cl_comm** out) {
+  CL_GUARD_BEGIN
+  if (!id || !out) raise(CL_EPARAM, "cl_comm_init_rank: null argument");
+  *out = nullptr;
+  Comm* c = comm_init_rank(id, world, rank, device);
+  *out = new cl_comm{c};
+  CL_GUARD_END
+}
+void cl_comm_destroy(cl_comm* c) {
+  if (!c) return;
+  comm_destroy(c->c);
+  delete c;
+}
+cl_status cl_solver_attach_comm(cl_solver* h, cl_comm* c) {
+  CL_GUARD_BEGIN
+  if (!c || !c->c) raise(CL_EPARAM, "cl_solver_attach_comm: null communicator");
+  Solver& s = *h->impl;
+  CU(cudaSetDevice(s.device));
+  s.attach_comm(c->c);
+  CL_GUARD_END
+}
+
+cl_status cl_group_create(int kind, int64_t n, int64_t m, const double* c, const int64_t* omega, const double* y,
+                          const cl_config* cfg, const int* devices, int ndev, int transport, cl_group** out) {
+  CL_GUARD_BEGIN
+  if (!out) raise(CL_EPARAM, "cl_group_create: null output");
+  *out = nullptr;
+  if (ndev < 1 || !devices) raise(CL_EPARAM, "cl_group_create: need at least one device");
+  if (kind != CL_KIND_ISTA && kind != CL_KIND_CADMM) raise(CL_EPARAM, "cl_group_create: ISTA or cADMM only");
+  if (transport != CL_TRANSPORT_NCCL && transport != CL_TRANSPORT_COPY)
+    raise(CL_EPARAM, "cl_group_create: unknown transport");
+  if (n < 1) raise(CL_EDIM, "cl_solver_create: n must be >= 1");
+  if (m < 0 || m > n) raise(CL_EDIM, "cl_solver_create: need 0 <= m <= n");
+  const auto t0 = std::chrono::steady_clock::now();
+  auto g = std::make_unique<Group>();
+  g->kind = kind;
+  g->n = n;
+  g->m = m;
+  g->transport = static_cast<Group::Transport>(transport);
+  if (g->transport == Group::kNccl) g->comms = comm_init_all(devices, ndev);
+  for (int r = 0; r < ndev; ++r) {
+    auto s = std::make_unique<Solver>();
+    s->kind = kind;
+    s->device = devices[r];
+    s->n = n;
+    s->m = m;
+    s->setup_common(c, omega, y, cfg);
+    if (kind == CL_KIND_ISTA) s->setup_ista(c, omega, y);
+    else s->setup_cadmm(c, omega, y);
+    if (s->fft && ndev > 1) raise(CL_EPARAM, "cl_group_create: the FFT engine runs unsharded (replicas only)");
+    if (g->transport == Group::kNccl) {
+      s->attach_comm(g->comms[static_cast<size_t>(r)]);
+    } else {
+      s->set_shard(r, ndev);
+      s->world = ndev;
+      s->all_ranges();
+    }
+    g->ranks.push_back(std::move(s));
+  }
+  if (g->transport == Group::kCopy) {
+    g->done.resize(static_cast<size_t>(ndev));
+    for (int r = 0; r < ndev; ++r) {
+      CU(cudaSetDevice(devices[r]));
+      CU(cudaEventCreateWithFlags(&g->done[static_cast<size_t>(r)], cudaEventDisableTiming));
+    }
+  }
+  g->setup_seconds = seconds_since(t0);
+  *out = new cl_group{std::move(g)};
+  CL_GUARD_END
+}
+void cl_group_destroy(cl_group* g) { delete g; }
+cl_status cl_group_set_truth(cl_group* h, const double* truth_n) {
+  CL_GUARD_BEGIN
+  Group& g = *h->g;
+  for (auto& s : g.ranks) s->set_truth(truth_n);
+  g.has_truth = truth_n != nullptr;
+  CL_GUARD_END
+}
+cl_status cl_group_step(cl_group* h, int64_t iters) {
+  CL_GUARD_BEGIN
+  if (iters < 0) raise(CL_EPARAM, "cl_group_step: iters must be >= 0");
+  h->g->step(iters);
+  CL_GUARD_END
+}
+cl_status cl_group_run(cl_group* h, cl_report* rep, double* final_x, int64_t* trace_iter, double* trace_value,
+                       double* trace_seconds, int64_t trace_cap) {
+  CL_GUARD_BEGIN
+  Group& g = *h->g;
+  run_loop(g, g.ranks.front()->cfg, rep, final_x, trace_iter, trace_value, trace_seconds, trace_cap);
+  CL_GUARD_END
+}
+cl_status cl_group_get(cl_group* h, const char* field, double* out) {
+  CL_GUARD_BEGIN
+  if (!field || !out) raise(CL_EPARAM, "cl_group_get: null argument");
+  h->g->get(field, out);
+  CL_GUARD_END
+}
+cl_status cl_group_synchronize(cl_group* h) {
+  CL_GUARD_BEGIN
+  for (auto& s : h->g->ranks) {
+    CU(cudaSetDevice(s->device));
+    CU(cudaStreamSynchronize(s->st));
+  }
+  CL_GUARD_END
+}
+cl_status cl_group_info(cl_group* h, int* world, int64_t* t, int* transport) {
+  CL_GUARD_BEGIN
+  if (world) *world = h->g->world();
+  if (t) *t = h->g->ranks.front()->t;
+  if (transport) *transport = h->g->transport;
   CL_GUARD_END
 }
 

@@ -134,6 +134,44 @@ class CudaShard:
         return self._views[key], b.value, e.value
 
 
+class NativeComm:
+    """A library-owned NCCL communicator (cl_comm_*): the exchange runs inside cl_solver_step /
+    cl_solver_run once a solver is attached -- no Python, no staging copies."""
+
+    def __init__(self, uid: bytes, world: int, rank: int, device: int):
+        if len(uid) != 128:
+            raise ValueError("NativeComm: the NCCL unique id is 128 bytes")
+        self.rank, self.world, self.device = rank, world, device
+        h = C.c_void_p()
+        _check(lib.cl_comm_init_rank(uid, world, rank, device, C.byref(h)))
+        self._h = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(lib.cl_comm_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def from_torch(cls, device: int, group=None):
+        """Every rank of a torch.distributed group: rank 0's id is broadcast over the group."""
+        import torch.distributed as dist
+        obj = [cls.unique_id() if dist.get_rank(group) == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return cls(obj[0], dist.get_world_size(group), dist.get_rank(group), device)
+
+    def attach(self, state):
+        """Shards `state` as (rank, world); its steps and run loop then exchange through this communicator."""
+        _check(lib.cl_solver_attach_comm(state.handle, self._h))
+        state._comm = self  # the communicator outlives the solver's use of it
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.cl_comm_destroy(h)
+            self._h = None
+
+
 def sharded_step(shard: CudaShard, gather: TorchGather, iters: int = 1):
     """Advance a CudaShard `iters` iterations; collectives run on the solver's stream."""
     import torch

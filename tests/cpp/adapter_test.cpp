@@ -1,6 +1,6 @@
 // Drop-in check of include/circlasso_b200.hpp: reference-style C++ code
 // (mirroring /root/reference/proj/tests/solvers_test.cpp) against the C-ABI.
-// Usage: adapter_test cpu | gpu     (exit code 0 = pass)
+// Usage: adapter_test cpu | gpu | c4     (exit code 0 = pass; c4: the sharded config-4 solve)
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -123,10 +123,33 @@ static void gpu_checks() {
   CHECK(std::sqrt(err / nrm) < 5e-5);
 }
 
+// BASELINE config 4 through the C-ABI in one process: cADMM n = 2^24, m = 2^22, k = 2^16, sharded over
+// the listed ranks (the library's exchange), against the unsharded solve -- bitwise.
+static void sharded_c4_checks(int world, cl::Transport transport) {
+  const cl::SensingProblem p = cl::make_problem(1 << 24, 1 << 22, 1 << 16, 1);
+  cl::SolverConfig cfg;
+  cfg.max_iter = 2;
+  cfg.check_every = 2;
+  const cl::RecoveryReport solo = cl::cadmm_run(p.measurements, p.op, cfg, &p.signal.values);
+  cl::ShardedSolve sh(CL_KIND_CADMM, p.op, p.measurements, cfg, std::vector<int>(static_cast<size_t>(world), 0),
+                      transport);
+  CHECK(sh.world() == world);
+  const cl::RecoveryReport rep = sh.run(&p.signal.values);
+  CHECK(rep.iterations == 2 && solo.iterations == 2);
+  CHECK(rep.final_x == solo.final_x);
+  CHECK(std::abs(rep.final_metric - solo.final_metric) <= 1e-12 * std::abs(solo.final_metric));
+  std::printf("sharded C4 cADMM, %d rank(s) (%s): 2 iterations, z bitwise equal to the unsharded solve, MSE %.6e\n",
+              world, transport == cl::Transport::kNccl ? "NCCL" : "peer copies", rep.final_metric);
+}
+
 int main(int argc, char** argv) {
   const std::string mode = argc > 1 ? argv[1] : "cpu";
   cpu_checks();
   if (mode == "gpu") gpu_checks();
+  if (mode == "c4") {
+    sharded_c4_checks(1, cl::Transport::kNccl);
+    sharded_c4_checks(2, cl::Transport::kCopy);
+  }
   std::printf("adapter_test %s: %s\n", mode.c_str(), failures ? "FAIL" : "PASS");
   return failures ? 1 : 0;
 }
