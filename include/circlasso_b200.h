@@ -251,6 +251,12 @@ cl_status cl_write_operator(const char* path, int64_t n, int64_t m, const double
                             const int64_t* omega);                                   /* io.hpp:99-112 */
 cl_status cl_read_operator(const char* path, double* row, int64_t cap_n, int64_t* omega, int64_t cap_m,
                            int64_t* n, int64_t* m);                                  /* io.hpp:114-131 */
+/* Binary PGM images (image.hpp:56-153): read P5 with maxval 1..255 into
+ * [0, 1] intensities (row-major; a NULL or too-small buffer only reports the
+ * size); write P5/255 with the intensities clamped to [0, 1] and rounded to 8
+ * bits.  CL_EFORMAT with the reference's messages. */
+cl_status cl_write_pgm(const char* path, int64_t width, int64_t height, const double* pixels);
+cl_status cl_read_pgm(const char* path, double* pixels, int64_t cap, int64_t* width, int64_t* height);
 /* One benchmark run in the reference's pinned CSV schema (io.hpp:133-170). */
 typedef struct cl_bench_row {
   const char* algorithm;

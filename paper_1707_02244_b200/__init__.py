@@ -6,7 +6,7 @@ compute lives in ``_lib/libcirclasso_b200.so`` (C-ABI: include/circlasso_b200.h)
 this package binds it with ctypes and mirrors the reference names.
 """
 from .api import (  # noqa: F401
-    AdmmState, ShardedSolve, admm_dense_run, admm_setup, admm_step, CadmmState, CapacityError, DeblurResult, GrayImage, deblur_recover, make_image, run_deblur_experiment, CirculantMatrix, CommError, ConsistencyError, CudaError, DiagonalOperator,
+    AdmmState, ShardedSolve, read_pgm, write_pgm, admm_dense_run, admm_setup, admm_step, CadmmState, CapacityError, DeblurResult, GrayImage, deblur_recover, make_image, run_deblur_experiment, CirculantMatrix, CommError, ConsistencyError, CudaError, DiagonalOperator,
     DimensionError, DivergenceError, Error, FootprintKind, FormatError, IstaState, ParameterError, PartialCirculantOperator,
     PhaseError, RecoveryReport, SensingProblem, SingularityError, SolverConfig, SparseSignal, StopMetric,
     SubsamplingMask, ThresholdPairing, TracePoint, analytic_footprint, blur_matrix, cadmm_run, cadmm_setup,

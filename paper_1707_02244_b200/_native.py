@@ -100,6 +100,8 @@ _SIGS = {
     "cl_read_vector": (C.c_int, [C.c_char_p, _d, C.c_int64, _i64]),
     "cl_write_operator": (C.c_int, [C.c_char_p, C.c_int64, C.c_int64, _d, _i64]),
     "cl_read_operator": (C.c_int, [C.c_char_p, _d, C.c_int64, _i64, C.c_int64, _i64, _i64]),
+    "cl_write_pgm": (C.c_int, [C.c_char_p, C.c_int64, C.c_int64, _d]),
+    "cl_read_pgm": (C.c_int, [C.c_char_p, _d, C.c_int64, _i64, _i64]),
     "cl_bench_iters_per_second": (C.c_double, [C.POINTER(cl_bench_row)]),
     "cl_bench_csv_header": (C.c_int, [C.c_char_p, C.c_int64, _i64]),
     "cl_bench_csv_row": (C.c_int, [C.POINTER(cl_bench_row), C.c_char_p, C.c_int64, _i64]),

@@ -390,6 +390,25 @@ def make_image(width: int, height: int, values) -> GrayImage:
     return GrayImage(width, height, np.clip(values, 0.0, 1.0))
 
 
+def write_pgm(img: GrayImage, path: str):
+    """image.hpp:137-153: binary P5, maxval 255, intensities clamped to [0, 1] and rounded."""
+    if img.width < 1 or img.height < 1:
+        raise ParameterError("write_pgm: empty image")
+    px = _f64(img.pixels)
+    if len(px) != img.size():
+        raise DimensionError(f"write_pgm: dimension mismatch, {len(px)} vs {img.size()}")
+    _check(lib.cl_write_pgm(str(path).encode(), img.width, img.height, _pd(px)))
+
+
+def read_pgm(path: str) -> GrayImage:
+    """image.hpp:95-135: binary P5 with maxval 1..255 -> intensities in [0, 1]."""
+    w, h = C.c_int64(), C.c_int64()
+    _check(lib.cl_read_pgm(str(path).encode(), None, 0, C.byref(w), C.byref(h)))
+    px = np.zeros(w.value * h.value)
+    _check(lib.cl_read_pgm(str(path).encode(), _pd(px), len(px), C.byref(w), C.byref(h)))
+    return GrayImage(w.value, h.value, px)
+
+
 def gen_star_field(width: int, height: int, density: float, seed: int) -> GrayImage:
     """deblur.hpp:69-86: floor(density n) stars at uniform positions, intensities U[0.3, 1)."""
     px = np.zeros(max(width * height, 0))

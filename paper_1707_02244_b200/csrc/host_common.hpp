@@ -56,6 +56,8 @@ std::vector<double> read_vector_file(const std::string& path);
 void write_operator_file(const std::string& path, int64_t n, int64_t m, const double* row, const int64_t* omega);
 void read_operator_file(const std::string& path, std::vector<double>* row, std::vector<int64_t>* omega);
 double bench_iters_per_second(const cl_bench_row& r);
+void read_pgm_file(const std::string& path, std::vector<double>* px, int64_t* width, int64_t* height);
+void write_pgm_file(const std::string& path, int64_t width, int64_t height, const double* px);
 std::string bench_csv_header();
 std::string bench_csv_row(const cl_bench_row& r);
 

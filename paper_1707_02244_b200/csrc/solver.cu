@@ -1845,6 +1845,21 @@ cl_status cl_read_operator(const char* path, double* row, int64_t cap_n, int64_t
   if (omega && cap_m >= *m) std::copy(om.begin(), om.end(), omega);
   CL_GUARD_END
 }
+cl_status cl_write_pgm(const char* path, int64_t width, int64_t height, const double* pixels) {
+  CL_GUARD_BEGIN
+  if (!path) raise(CL_EPARAM, "write_pgm: null path");
+  if (width >= 1 && height >= 1 && !pixels) raise(CL_EPARAM, "write_pgm: null pixels");
+  write_pgm_file(path, width, height, pixels);
+  CL_GUARD_END
+}
+cl_status cl_read_pgm(const char* path, double* pixels, int64_t cap, int64_t* width, int64_t* height) {
+  CL_GUARD_BEGIN
+  if (!path || !width || !height) raise(CL_EPARAM, "read_pgm: null argument");
+  std::vector<double> px;
+  read_pgm_file(path, &px, width, height);
+  if (pixels && cap >= static_cast<int64_t>(px.size())) std::copy(px.begin(), px.end(), pixels);
+  CL_GUARD_END
+}
 double cl_bench_iters_per_second(const cl_bench_row* row) { return row ? bench_iters_per_second(*row) : 0.0; }
 static void copy_text(const std::string& t, char* buf, int64_t cap, int64_t* len) {
   if (len) *len = static_cast<int64_t>(t.size());

@@ -173,7 +173,36 @@ __device__ __forceinline__ void st_split(float* hi, float* lo, float4 v) {
   *reinterpret_cast<float4*>(lo) = make_float4(v.x - a.x, v.y - a.y, v.z - a.z, v.w - a.w);
 }
 
-// unit = (tile, split); split s covers offsets [s Dn, (s + 1) Dn), Dn = (n / 256) / splits.
+// Steps of one unit in consumption order: blocks of up to kDB offsets, and per block the 8 K groups, and
+// per group the block's offsets.  A split covers offsets [s nb / S, (s + 1) nb / S) (nb = n / 256), so S
+// need not divide nb (S = 37 k lets the units of 1, 2, 4 or 8 ranks fill whole waves of 148 SMs).
+struct StepIter {
+  int64_t Dlo = 0, L = 0;   // the split's first offset and length
+  int64_t blk = 0, dd = 0;  // block index, offset within the block
+  int g = 0;                // K group
+  int len = 0;              // offsets in the current block
+  __device__ __forceinline__ void init(int64_t dlo, int64_t l) {
+    Dlo = dlo;
+    L = l;
+    blk = dd = 0;
+    g = 0;
+    len = static_cast<int>(l < kDB ? l : kDB);
+  }
+  __device__ __forceinline__ void next() {
+    if (++dd < len) return;
+    dd = 0;
+    if (++g < kNG) return;
+    g = 0;
+    ++blk;
+    const int64_t rest = L - blk * kDB;
+    len = static_cast<int>(rest < kDB ? rest : kDB);
+  }
+  __device__ __forceinline__ int64_t d0() const { return Dlo + blk * kDB; }
+  __device__ __forceinline__ int64_t D() const { return d0() + dd; }
+  __device__ __forceinline__ int64_t t0() const { return D() * kB - (kB - 1) + kKG * g; }  // Hankel tile start
+};
+
+// unit = (tile, split); split s covers offsets [s nb / S, (s + 1) nb / S), nb = n / 256.
 // A step is one (offset D, K group g) pair: 12 MMAs (4 K-steps x 3 TF32 products).  kSPD
 // steps accumulate into one of two TMEM accumulators, started from zero.  The tensor core's
 // fp32 accumulation truncates, so its error grows with the accumulator's magnitude; draining
@@ -212,12 +241,8 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
   const int64_t tile = tile_lo + blockIdx.x / splits;
   const int s = static_cast<int>(blockIdx.x % splits);
   const int64_t I0 = tile * kMT;
-  const int64_t Dn = nb / splits, Dlo = s * Dn;
-  const int64_t DBn = Dn < kDB ? Dn : kDB;  // powers of two (n is)
-  const int lgDB = __ffsll(DBn) - 1;
+  const int64_t Dlo = s * nb / splits, Dn = (s + 1) * nb / splits - Dlo;
   const int64_t steps = kNG * Dn;
-  const int rows = static_cast<int>(DBn) + kMT;
-  const uint32_t lboA = static_cast<uint32_t>(rows) * 16u;
 
   if (tid == 0) {
     for (int i = 0; i < kAStages; ++i) {
@@ -296,25 +321,24 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
     int a_use = 0;
     // fp16: the next tile's h values are loaded one tile ahead (their latency overlaps this tile)
     constexpr int kSt = (kStg + kProducers - 1) / kProducers;
-    auto tile_t0 = [&](int64_t j) {
-      const int64_t rem = j & (kNG * DBn - 1);
-      return (Dlo + (j >> (lgDB + 3)) * DBn + (rem & (DBn - 1))) * kB - (kB - 1) + kKG * (rem >> lgDB);
-    };
+    StepIter it, nx;
+    it.init(Dlo, Dn);
+    nx = it;
+    nx.next();
     float xn[F16 ? kSt : 1];
     if constexpr (F16) {
 #pragma unroll
-      for (int q = 0; q < kSt; ++q) xn[q] = __ldg(h + ((tile_t0(0) + ptid + q * kProducers) & nm));
+      for (int q = 0; q < kSt; ++q) xn[q] = __ldg(h + ((it.t0() + ptid + q * kProducers) & nm));
     }
-    for (int64_t j = 0; j < steps; ++j) {
-      const int64_t blk = j >> (lgDB + 3), rem = j & (kNG * DBn - 1);
-      const int g = static_cast<int>(rem >> lgDB);
-      const int64_t dd = rem & (DBn - 1), d0 = Dlo + blk * DBn, D = d0 + dd;
-      if (dd == 0) {
+    for (int64_t j = 0; j < steps; ++j, it = nx, nx.next()) {
+      const int g = it.g;
+      if (it.dd == 0) {
         const int st = a_use & 1;
         mbar_wait(&a_empty[st], ((a_use >> 1) & 1) ^ 1);
         unsigned char* hi = sm + (st * 2) * kSlabBytes;
         unsigned char* lo = sm + (st * 2 + 1) * kSlabBytes;
-        const int64_t ibase = I0 - d0 - DBn + 1;  // I - D of slab row 0
+        const int rows = it.len + kMT;
+        const int64_t ibase = I0 - it.d0() - it.len + 1;  // I - D of slab row 0
         // kBatch items per thread per pass, all loads first (one L2 latency per pass)
         constexpr int kBatch = 4;
         for (int base = ptid; base < rows * kCh; base += kBatch * kProducers) {
@@ -354,7 +378,7 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
       mbar_wait(&b_empty[bs], ((j / kBStages) & 1) ^ 1);
       unsigned char* thi = sm + kOffB + (bs * 2) * kTileBytes;
       unsigned char* tlo = sm + kOffB + (bs * 2 + 1) * kTileBytes;
-      const int64_t t0 = D * kB - (kB - 1) + kKG * g;
+      const int64_t t0 = it.t0();
       constexpr int kRows = (kRB + kProducers - 1) / kProducers;
       if constexpr (F16) {
         // Split each of the tile's kRB + 8 values once into a packed (hi | lo << 16) fp16 word in a
@@ -364,7 +388,7 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
 #pragma unroll
         for (int q = 0; q < kSt; ++q) x[q] = xn[q];
         if (j + 1 < steps) {
-          const int64_t t1 = tile_t0(j + 1);
+          const int64_t t1 = nx.t0();
 #pragma unroll
           for (int q = 0; q < kSt; ++q) xn[q] = __ldg(h + ((t1 + ptid + q * kProducers) & nm));
         }
@@ -427,14 +451,17 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
                                (static_cast<uint32_t>(kMT >> 4) << 24);
     const uint32_t abase = smem_u32(sm), bbase = smem_u32(sm + kOffB);
     int a_use = 0;
-    uint32_t ahi = 0, alo = 0;
-    for (int64_t j = 0; j < steps; ++j) {
-      const int64_t dd = j & (DBn - 1);
+    uint32_t ahi = 0, alo = 0, lboA = 0;
+    StepIter it;
+    it.init(Dlo, Dn);
+    for (int64_t j = 0; j < steps; ++j, it.next()) {
+      const int64_t dd = it.dd;
       const int st = a_use & 1;
       if (dd == 0) {
         mbar_wait(&a_full[st], (a_use >> 1) & 1);
         ahi = abase + (st * 2) * kSlabBytes;
         alo = ahi + kSlabBytes;
+        lboA = static_cast<uint32_t>(it.len + kMT) * 16u;
       }
       const int bs = static_cast<int>(j & (kBStages - 1));
       mbar_wait(&b_full[bs], (j / kBStages) & 1);
@@ -443,7 +470,7 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
       const bool first = j % kSpd == 0;
       if (first) mbar_wait(&t_empty[buf], ((cyc >> 1) & 1) ^ 1);
       tc_after_sync();
-      const uint32_t row0 = static_cast<uint32_t>(DBn - 1 - dd) * 16u;
+      const uint32_t row0 = static_cast<uint32_t>(it.len - 1 - dd) * 16u;
       const uint32_t bhi = bbase + (bs * 2) * kTileBytes, blo = bhi + kTileBytes;
       const uint32_t tacc = tmem + buf * kB;
 #pragma unroll
@@ -464,7 +491,7 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
       }
       tc_commit(&b_empty[bs]);
       if (j % kSpd == kSpd - 1) tc_commit(&t_full[buf]);
-      if (dd == DBn - 1) {
+      if (dd == it.len - 1) {
         tc_commit(&a_empty[st]);
         ++a_use;
       }
@@ -491,9 +518,14 @@ ConvPlan make_tc_plan(int64_t n) {
   p.tiles = n / p.tile;
   p.chunks = 0;
   const int64_t nb = n / kB;
-  // about seven waves of one-CTA-per-SM units; splits a power of two dividing n / 256
-  int64_t s = 1;
-  while (p.tiles * s * 2 <= 148 * 7 && s * 2 <= nb) s *= 2;
+  // Splits over block offsets, a function of n only (results are identical for every rank count): a
+  // multiple of 37 (148 = 4 x 37 SMs), so that the units of the 1, 2, 4 or 8 ranks a product is sharded
+  // over fill whole waves whenever each rank owns at least one tile: T = 32 tiles at n = 2^20 -> 37
+  // splits: 1184 units = 8 waves at G = 1, 148 per rank (one wave) at G = 8; T = 512 at 2^24 -> 37.
+  // Smaller T keep about 8 waves at G = 1 (T = 16 -> 74, T = 8 -> 148); never more splits than offsets.
+  const int64_t T = p.tiles;
+  int64_t s = T >= 32 ? 37 : T >= 8 ? 37 * (32 / T) : (148 * 8 + T - 1) / T;
+  if (s > nb) s = nb;
   if (const char* v = getenv("CLB_TC_SPLITS")) s = atoll(v);
   p.splits = static_cast<int>(s);
   p.tile_lo = 0;

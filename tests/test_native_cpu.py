@@ -234,3 +234,36 @@ def test_dense_admm_validation_before_any_device_work():
     with pytest.raises(cl.ParameterError, match="alpha"):
         cl.admm_dense_run(p.measurements, p.op, cl.SolverConfig(alpha=-1.0))
     assert cl.analytic_footprint(cl.FootprintKind.kDenseAdmm, 256, 128, 4) == (256 * 256 + 4 * 256 + 128) * 4
+
+
+# ---- PGM images (image.hpp:56-153), the reference's own cases (tests/image_deblur_test.cpp:62-140) ----
+def test_pgm_roundtrip_and_quantization(tmp_path):
+    rng = np.random.default_rng(77)
+    img = cl.make_image(9, 5, rng.uniform(size=45))
+    path = tmp_path / "roundtrip.pgm"
+    cl.write_pgm(img, path)
+    back = cl.read_pgm(path)
+    assert (back.width, back.height, len(back.pixels)) == (9, 5, 45)
+    assert np.max(np.abs(back.pixels - img.pixels)) <= 0.5 / 255.0 + 1e-12
+    raw = cl.GrayImage(3, 1, np.array([-3.0, 0.5, 1.7]))  # deliberately unclamped
+    cl.write_pgm(raw, tmp_path / "q.pgm")
+    q = cl.read_pgm(tmp_path / "q.pgm")
+    assert q.pixels[0] == 0.0 and q.pixels[1] == 128.0 / 255.0 and q.pixels[2] == 1.0  # lround(127.5) = 128
+    assert open(tmp_path / "q.pgm", "rb").read() == b"P5\n3 1\n255\n\x00\x80\xff"
+
+
+def test_pgm_header_comments_and_errors(tmp_path):
+    p = tmp_path / "h.pgm"
+    p.write_bytes(b"P5\n# a comment line\n 3 2 # trailing comment\n255\n" + bytes([0, 0x40, 0x80, 0xC0, 0xFF, 0x20]))
+    img = cl.read_pgm(p)
+    assert (img.width, img.height) == (3, 2) and img.pixels[0] == 0.0 and img.pixels[4] == 1.0
+    with pytest.raises(cl.FormatError, match="cannot open"):
+        cl.read_pgm(tmp_path / "missing.pgm")
+    for content, needle in ((b"P2\n2 2\n255\n0 0 0 0\n", "'P2'"), (b"P5\nabc 2\n255\n", "'abc'"),
+                            (b"P5\n2 2\n65535\n", "65535"), (b"P5\n2 2\n0\n", "maxval"),
+                            (b"P5\n4 4\n255\nabcde", "truncated")):
+        p.write_bytes(content)
+        with pytest.raises(cl.FormatError, match=needle):
+            cl.read_pgm(p)
+    with pytest.raises(cl.ParameterError):
+        cl.write_pgm(cl.GrayImage(0, 0, np.zeros(0)), tmp_path / "e.pgm")
