@@ -1,15 +1,30 @@
 // circlasso_b200.hpp — C++ drop-in adapter over the C-ABI (circlasso_b200.h).
 //
 // Mirrors the reference circlasso solver API (header-only C++20 library,
-// /root/reference/proj/include/circlasso/) with the same names, argument
-// meaning and error behaviour, so a reference user swaps
+// /root/reference/proj/include/circlasso/) with the same names, template
+// parameters, argument meaning and error behaviour, so a reference user swaps
 //     #include "circlasso/circlasso.hpp"   ->   #include "circlasso_b200.hpp"
-//     circlasso::ista_run(...)             ->   circlasso_b200::ista_run(...)
-// and links libcirclasso_b200.so.  Vectors are std::vector<double> (the
-// reference's Eigen::VectorXd); when Eigen is available, Eigen overloads are
-// provided too.  Every solve runs on the GPU; there is no CPU fallback.
+//     namespace circlasso                  ->   namespace circlasso_b200
+// and links libcirclasso_b200.so.
+//
+// Vector<Scalar> is the reference's Eigen column vector when Eigen is on the
+// include path (__has_include(<Eigen/Dense>); define CIRCLASSO_B200_NO_EIGEN
+// to opt out), so reference-style code (Vector<double>::Zero(n), comma
+// initializers, .norm()) compiles unchanged; without Eigen it is
+// std::vector<Scalar>.  Every solve runs on the GPU in fp32 whatever Scalar
+// is; setup transforms are fp64.  There is no CPU fallback.
+//
+// State structs (IstaState, CadmmState, AdmmState) keep the reference's public
+// members.  The iteration state lives on the device; ista_step / cadmm_step /
+// admm_step advance it one iteration and refresh the host members (x, r,
+// delta ...), like the reference, which makes them synchronous.  `step(k)`
+// advances k iterations without the refresh (the fast path); `sync()`
+// refreshes on demand.  The per-call use_fft of ista_step / cadmm_step picks
+// the product engine of that step: the state keeps one device solver per
+// engine it has used and hands the iterate over when the engine changes.
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <limits>
@@ -17,15 +32,33 @@
 #include <ostream>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
 #include "circlasso_b200.h"
 
+#if !defined(CIRCLASSO_B200_NO_EIGEN) && defined(__has_include)
+#if __has_include(<Eigen/Dense>)
+#include <Eigen/Dense>
+#define CIRCLASSO_B200_EIGEN 1
+#endif
+#endif
+
 namespace circlasso_b200 {
 
-using Vector = std::vector<double>;
+#ifdef CIRCLASSO_B200_EIGEN
+template <typename Scalar = double>
+using Vector = Eigen::Matrix<Scalar, Eigen::Dynamic, 1>;
+using Index = Eigen::Index;
+#else
+template <typename Scalar = double>
+using Vector = std::vector<Scalar>;
 using Index = std::int64_t;
+#endif
+static_assert(sizeof(Index) == sizeof(int64_t), "mask indices cross the C-ABI as int64");
+
+inline constexpr Index kDenseCap = 4096;  // circulant.hpp:31
 
 // ---- errors.hpp:12-72 -------------------------------------------------------
 class Error : public std::runtime_error {
@@ -65,12 +98,51 @@ inline void check_same_size(Index a, Index b, const char* op) {  // fft.hpp:27-3
   if (a != b) throw DimensionError(std::string(op) + ": dimension mismatch, " + std::to_string(a) + " vs " +
                                    std::to_string(b));
 }
+template <typename S>
+Vector<S> zeros(Index n) {
+#ifdef CIRCLASSO_B200_EIGEN
+  return Vector<S>::Zero(n);
+#else
+  return Vector<S>(static_cast<size_t>(n < 0 ? 0 : n), S(0));
+#endif
+}
+template <typename S>
+Index size_of(const Vector<S>& v) {
+  return static_cast<Index>(v.size());
+}
+// fp64 view of a vector for the C-ABI (no copy for double)
+template <typename S>
+class F64 {
+ public:
+  explicit F64(const Vector<S>& v) {
+    if constexpr (std::is_same_v<S, double>) {
+      p_ = v.data();
+    } else {
+      tmp_.assign(v.data(), v.data() + v.size());
+      p_ = tmp_.data();
+    }
+  }
+  const double* get() const { return p_; }
+
+ private:
+  std::vector<double> tmp_;
+  const double* p_ = nullptr;
+};
+template <typename S>
+Vector<S> from_f64(const double* d, Index n) {
+  Vector<S> v = zeros<S>(n);
+  for (Index i = 0; i < n; ++i) v[i] = static_cast<S>(d[i]);
+  return v;
+}
 }  // namespace detail
 
 // ---- solvers.hpp:83, 112-150 --------------------------------------------------
 enum class ThresholdPairing { kLiteral, kProximal };
 enum class StopMetric { kMseVsTruth, kIterateChange };
 
+// SolverConfig, solvers.hpp:112-125.  Deviation: use_fft defaults to false here (the reference: true).  The
+// direct shift-indexed engine is the paper's scheme and this library's hot path; use_fft = true runs the
+// on-device FFT engine (the reference's default arithmetic).  `device` is new.
 struct SolverConfig {
   double alpha = 1e-4;
   double tau = 0.0;
@@ -82,9 +154,9 @@ struct SolverConfig {
   double target_mse = std::numeric_limits<double>::quiet_NaN();
   int check_every = 10;
   ThresholdPairing pairing = ThresholdPairing::kLiteral;
-  bool use_fft = false;  // true: on-device FFT engine (any n); false: direct sm_100a kernels
-  Index dense_cap = 4096;  // circulant.hpp:31 kDenseCap: largest n of the dense ADMM
-  int device = 0;       // new: CUDA device of the solve
+  bool use_fft = false;
+  Index dense_cap = kDenseCap;
+  int device = 0;  // CUDA device of the solve
 
   cl_config c() const {
     cl_config k;
@@ -105,43 +177,100 @@ struct SolverConfig {
   }
 };
 
+template <typename Scalar = double>
 struct TracePoint {
   long iteration;
-  double value;
+  Scalar value;
   double elapsed_seconds;
 };
 
+template <typename Scalar = double>
 struct RecoveryReport {
-  Vector final_x;
+  Vector<Scalar> final_x;
   long iterations = 0;
-  std::vector<TracePoint> mse_trace;
+  std::vector<TracePoint<Scalar>> mse_trace;
   double setup_seconds = 0.0;
   double total_seconds = 0.0;
   std::uint64_t footprint_bytes = 0;
   StopMetric metric = StopMetric::kIterateChange;
   bool reached_target = false;
-  double final_metric = std::numeric_limits<double>::quiet_NaN();
+  Scalar final_metric = std::numeric_limits<Scalar>::quiet_NaN();
 };
 
+// solvers.hpp:86-106
+enum class FootprintKind { kCpista, kCpadmm, kDenseIsta, kDenseAdmm };
+inline std::uint64_t analytic_footprint(FootprintKind kind, std::uint64_t n, std::uint64_t m,
+                                        std::uint64_t scalar_width) {
+  switch (kind) {
+    case FootprintKind::kCpista: return 4 * n * scalar_width;
+    case FootprintKind::kCpadmm: return 10 * n * scalar_width;
+    case FootprintKind::kDenseIsta: return (2 * m * n + 2 * n + 2 * m) * scalar_width;
+    case FootprintKind::kDenseAdmm: return (n * n + 4 * n + m) * scalar_width;
+  }
+  throw ParameterError("analytic_footprint: unknown solver kind");
+}
+
+// solvers.hpp:39-61
+template <typename Scalar>
+Scalar soft_threshold_entry(Scalar v, Scalar g) {
+  if (v > g) return v - g;
+  if (v < -g) return v + g;
+  return Scalar(0);
+}
+template <typename Scalar>
+Vector<Scalar> soft_threshold(const Vector<Scalar>& x, Scalar gamma) {
+  if (gamma < Scalar(0)) throw ParameterError("soft_threshold: gamma must be nonnegative");
+  Vector<Scalar> out = detail::zeros<Scalar>(detail::size_of(x));
+  for (Index i = 0; i < detail::size_of(x); ++i) out[i] = soft_threshold_entry(x[i], gamma);
+  return out;
+}
+template <typename Scalar>
+Scalar mse(const Vector<Scalar>& a, const Vector<Scalar>& b) {
+  detail::check_same_size(detail::size_of(a), detail::size_of(b), "mse");
+  if (detail::size_of(a) == 0) return Scalar(0);
+  Scalar s = 0;
+  for (Index i = 0; i < detail::size_of(a); ++i) s += (a[i] - b[i]) * (a[i] - b[i]);
+  return s / static_cast<Scalar>(detail::size_of(a));
+}
+
 // ---- circulant.hpp operators ----------------------------------------------------
+template <typename Scalar = double>
 class CirculantMatrix {
  public:
   CirculantMatrix() = default;
-  explicit CirculantMatrix(Vector first_row) : row_(std::move(first_row)) {}
+  explicit CirculantMatrix(Vector<Scalar> first_row) : row_(std::move(first_row)) {}
   static CirculantMatrix Identity(Index n) {
-    Vector r(static_cast<size_t>(n), 0.0);
-    if (n > 0) r[0] = 1.0;
+    Vector<Scalar> r = detail::zeros<Scalar>(n);
+    if (n > 0) r[0] = Scalar(1);
     return CirculantMatrix(std::move(r));
   }
-  Index n() const { return static_cast<Index>(row_.size()); }
-  const Vector& first_row() const { return row_; }
+  Index n() const { return detail::size_of(row_); }
+  const Vector<Scalar>& first_row() const { return row_; }
   Index stored_scalars() const { return n(); }
 
  private:
-  Vector row_;
+  Vector<Scalar> row_;
 };
 
-class SubsamplingMask {
+template <typename Scalar = double>
+class DiagonalOperator {  // circulant.hpp:108-126
+ public:
+  DiagonalOperator() = default;
+  explicit DiagonalOperator(Vector<Scalar> diag) : diag_(std::move(diag)) {}
+  Index n() const { return detail::size_of(diag_); }
+  const Vector<Scalar>& diag() const { return diag_; }
+  Vector<Scalar> apply(const Vector<Scalar>& x) const {
+    detail::check_same_size(detail::size_of(x), n(), "DiagonalOperator::apply");
+    Vector<Scalar> out = detail::zeros<Scalar>(n());
+    for (Index i = 0; i < n(); ++i) out[i] = diag_[i] * x[i];
+    return out;
+  }
+
+ private:
+  Vector<Scalar> diag_;
+};
+
+class SubsamplingMask {  // circulant.hpp:128-184
  public:
   SubsamplingMask() = default;
   SubsamplingMask(std::vector<Index> omega, Index n) : omega_(std::move(omega)), n_(n) {
@@ -161,16 +290,19 @@ class SubsamplingMask {
   Index m() const { return static_cast<Index>(omega_.size()); }
   Index n() const { return n_; }
   const std::vector<Index>& omega() const { return omega_; }
-  Vector apply(const Vector& x) const {
-    detail::check_same_size(static_cast<Index>(x.size()), n_, "SubsamplingMask::apply");
-    Vector out(omega_.size());
-    for (size_t i = 0; i < omega_.size(); ++i) out[i] = x[static_cast<size_t>(omega_[i])];
+  Index stored_indices() const { return m(); }
+  template <typename Scalar>
+  Vector<Scalar> apply(const Vector<Scalar>& x) const {
+    detail::check_same_size(detail::size_of(x), n_, "SubsamplingMask::apply");
+    Vector<Scalar> out = detail::zeros<Scalar>(m());
+    for (size_t i = 0; i < omega_.size(); ++i) out[static_cast<Index>(i)] = x[omega_[i]];
     return out;
   }
-  Vector embed(const Vector& y) const {
-    detail::check_same_size(static_cast<Index>(y.size()), m(), "SubsamplingMask::embed");
-    Vector out(static_cast<size_t>(n_), 0.0);
-    for (size_t i = 0; i < omega_.size(); ++i) out[static_cast<size_t>(omega_[i])] = y[i];
+  template <typename Scalar>
+  Vector<Scalar> embed(const Vector<Scalar>& y) const {
+    detail::check_same_size(detail::size_of(y), m(), "SubsamplingMask::embed");
+    Vector<Scalar> out = detail::zeros<Scalar>(n_);
+    for (size_t i = 0; i < omega_.size(); ++i) out[omega_[i]] = y[static_cast<Index>(i)];
     return out;
   }
 
@@ -179,260 +311,482 @@ class SubsamplingMask {
   Index n_ = 0;
 };
 
-class PartialCirculantOperator {
+template <typename Scalar = double>
+class PartialCirculantOperator {  // circulant.hpp:186-212
  public:
   PartialCirculantOperator() = default;
-  PartialCirculantOperator(CirculantMatrix c, SubsamplingMask mask) : c_(std::move(c)), mask_(std::move(mask)) {
+  PartialCirculantOperator(CirculantMatrix<Scalar> c, SubsamplingMask mask) : c_(std::move(c)), mask_(std::move(mask)) {
     detail::check_same_size(c_.n(), mask_.n(), "PartialCirculantOperator");
   }
   Index n() const { return c_.n(); }
   Index m() const { return mask_.m(); }
-  const CirculantMatrix& circulant() const { return c_; }
+  const CirculantMatrix<Scalar>& circulant() const { return c_; }
   const SubsamplingMask& mask() const { return mask_; }
+  Index stored_scalars() const { return c_.stored_scalars(); }
+  Index stored_indices() const { return mask_.stored_indices(); }
 
  private:
-  CirculantMatrix c_;
+  CirculantMatrix<Scalar> c_;
   SubsamplingMask mask_;
 };
 
-inline double spectral_norm(const CirculantMatrix& C) {
+template <typename Scalar>
+Scalar spectral_norm(const CirculantMatrix<Scalar>& C) {  // circulant.hpp:347-351
   double s = 0;
-  check(cl_spectral_norm(C.n(), C.first_row().data(), &s));
-  return s;
+  check(cl_spectral_norm(C.n(), detail::F64<Scalar>(C.first_row()).get(), &s));
+  return static_cast<Scalar>(s);
 }
-inline CirculantMatrix regularized_gram_inverse(const CirculantMatrix& C, double rho, double sigma) {
-  Vector b(static_cast<size_t>(C.n()));
-  check(cl_regularized_gram_inverse(C.n(), C.first_row().data(), rho, sigma, b.data()));
-  return CirculantMatrix(std::move(b));
+template <typename Scalar>
+CirculantMatrix<Scalar> regularized_gram_inverse(const CirculantMatrix<Scalar>& C, Scalar rho, Scalar sigma) {
+  std::vector<double> b(static_cast<size_t>(C.n()));  // circulant.hpp:297-320
+  check(cl_regularized_gram_inverse(C.n(), detail::F64<Scalar>(C.first_row()).get(), rho, sigma, b.data()));
+  return CirculantMatrix<Scalar>(detail::from_f64<Scalar>(b.data(), C.n()));
 }
-inline Vector mask_gram_inverse(const SubsamplingMask& P, double rho) {
-  Vector d(static_cast<size_t>(P.n()));
+template <typename Scalar = double>
+DiagonalOperator<Scalar> mask_gram_inverse(const SubsamplingMask& P, Scalar rho) {  // circulant.hpp:324-333
+  std::vector<double> d(static_cast<size_t>(P.n()));
   check(cl_mask_gram_inverse(P.n(), P.m(), P.omega().data(), rho, d.data()));
-  return d;
+  return DiagonalOperator<Scalar>(detail::from_f64<Scalar>(d.data(), P.n()));
 }
-inline Vector circ_matvec(const CirculantMatrix& M, const Vector& x, int device = 0) {
-  detail::check_same_size(static_cast<Index>(x.size()), M.n(), "circ_matvec");
-  Vector out(x.size());
-  check(cl_circ_matvec(device, M.n(), M.first_row().data(), x.data(), 0, out.data()));
-  return out;
-}
-inline Vector circ_transpose_matvec(const CirculantMatrix& M, const Vector& x, int device = 0) {
-  detail::check_same_size(static_cast<Index>(x.size()), M.n(), "circ_transpose_matvec");
-  Vector out(x.size());
-  check(cl_circ_matvec(device, M.n(), M.first_row().data(), x.data(), 1, out.data()));
-  return out;
-}
-inline Vector partial_matvec(const PartialCirculantOperator& A, const Vector& x, int device = 0) {
-  detail::check_same_size(static_cast<Index>(x.size()), A.n(), "partial_matvec");
-  Vector out(static_cast<size_t>(A.m()));
-  check(cl_partial_matvec(device, A.n(), A.m(), A.circulant().first_row().data(), A.mask().omega().data(), x.data(),
-                          out.data()));
-  return out;
-}
-inline Vector partial_transpose_matvec(const PartialCirculantOperator& A, const Vector& y, int device = 0) {
-  detail::check_same_size(static_cast<Index>(y.size()), A.m(), "partial_transpose_matvec");
-  Vector out(static_cast<size_t>(A.n()));
-  check(cl_partial_transpose_matvec(device, A.n(), A.m(), A.circulant().first_row().data(),
-                                    A.mask().omega().data(), y.data(), out.data()));
-  return out;
+template <typename Scalar>
+CirculantMatrix<Scalar> circ_compose(const CirculantMatrix<Scalar>& C, const CirculantMatrix<Scalar>& B) {
+  detail::check_same_size(C.n(), B.n(), "circ_compose");  // circulant.hpp:337-343
+  std::vector<double> out(static_cast<size_t>(C.n()));
+  check(cl_compose_rows(C.n(), detail::F64<Scalar>(C.first_row()).get(), detail::F64<Scalar>(B.first_row()).get(),
+                        out.data()));
+  return CirculantMatrix<Scalar>(detail::from_f64<Scalar>(out.data(), C.n()));
 }
 
-// ---- sensing.hpp generation -------------------------------------------------------
+namespace detail {
+template <typename Scalar>
+Vector<Scalar> device_circ(const CirculantMatrix<Scalar>& M, const Vector<Scalar>& x, int transpose, int device,
+                           const char* op) {
+  check_same_size(size_of(x), M.n(), op);
+  std::vector<double> out(static_cast<size_t>(M.n()));
+  check(cl_circ_matvec(device, M.n(), F64<Scalar>(M.first_row()).get(), F64<Scalar>(x).get(), transpose, out.data()));
+  return from_f64<Scalar>(out.data(), M.n());
+}
+}  // namespace detail
+// circulant.hpp:216-274 on the GPU (fp32 direct kernels); the _naive / _fft names of the reference map to
+// the same device product (the engines agree to fp32 rounding)
+template <typename Scalar>
+Vector<Scalar> circ_matvec(const CirculantMatrix<Scalar>& M, const Vector<Scalar>& x, int device = 0) {
+  return detail::device_circ(M, x, 0, device, "circ_matvec");
+}
+template <typename Scalar>
+Vector<Scalar> circ_transpose_matvec(const CirculantMatrix<Scalar>& M, const Vector<Scalar>& x, int device = 0) {
+  return detail::device_circ(M, x, 1, device, "circ_transpose_matvec");
+}
+template <typename Scalar>
+Vector<Scalar> circ_matvec_naive(const CirculantMatrix<Scalar>& M, const Vector<Scalar>& x) {
+  return circ_matvec(M, x);
+}
+template <typename Scalar>
+Vector<Scalar> circ_matvec_fft(const CirculantMatrix<Scalar>& M, const Vector<Scalar>& x) {
+  return circ_matvec(M, x);
+}
+template <typename Scalar>
+Vector<Scalar> circ_transpose_matvec_naive(const CirculantMatrix<Scalar>& M, const Vector<Scalar>& x) {
+  return circ_transpose_matvec(M, x);
+}
+template <typename Scalar>
+Vector<Scalar> partial_matvec(const PartialCirculantOperator<Scalar>& A, const Vector<Scalar>& x, int device = 0) {
+  detail::check_same_size(detail::size_of(x), A.n(), "partial_matvec");  // circulant.hpp:277-282
+  std::vector<double> out(static_cast<size_t>(A.m()));
+  check(cl_partial_matvec(device, A.n(), A.m(), detail::F64<Scalar>(A.circulant().first_row()).get(),
+                          A.mask().omega().data(), detail::F64<Scalar>(x).get(), out.data()));
+  return detail::from_f64<Scalar>(out.data(), A.m());
+}
+template <typename Scalar>
+Vector<Scalar> partial_transpose_matvec(const PartialCirculantOperator<Scalar>& A, const Vector<Scalar>& y,
+                                        int device = 0) {
+  detail::check_same_size(detail::size_of(y), A.m(), "partial_transpose_matvec");  // circulant.hpp:286-291
+  std::vector<double> out(static_cast<size_t>(A.n()));
+  check(cl_partial_transpose_matvec(device, A.n(), A.m(), detail::F64<Scalar>(A.circulant().first_row()).get(),
+                                    A.mask().omega().data(), detail::F64<Scalar>(y).get(), out.data()));
+  return detail::from_f64<Scalar>(out.data(), A.n());
+}
+
+// ---- sensing.hpp generation (bit-exact with the reference RNG) -----------------------
+template <typename Scalar = double>
 struct SparseSignal {
-  Vector values;
+  Vector<Scalar> values;
   std::vector<Index> support;
-  Index n() const { return static_cast<Index>(values.size()); }
+  Index n() const { return detail::size_of(values); }
   Index k() const { return static_cast<Index>(support.size()); }
 };
+template <typename Scalar = double>
 struct SensingProblem {
-  SparseSignal signal;
-  PartialCirculantOperator op;
-  Vector measurements;
+  SparseSignal<Scalar> signal;
+  PartialCirculantOperator<Scalar> op;
+  Vector<Scalar> measurements;
   std::uint64_t seed = 0;
   Index n() const { return op.n(); }
   Index m() const { return op.m(); }
   Index k() const { return signal.k(); }
 };
-inline SparseSignal gen_sparse_signal(Index n, Index k, std::uint64_t seed) {
-  SparseSignal s;
-  s.values.resize(static_cast<size_t>(n < 0 ? 0 : n));
+template <typename Scalar = double>
+SparseSignal<Scalar> gen_sparse_signal(Index n, Index k, std::uint64_t seed) {  // sensing.hpp:129-145
+  std::vector<double> v(static_cast<size_t>(n < 0 ? 0 : n));
+  SparseSignal<Scalar> s;
   s.support.resize(static_cast<size_t>(k < 0 ? 0 : k));
-  check(cl_gen_sparse_signal(n, k, seed, s.values.data(), s.support.data()));
+  check(cl_gen_sparse_signal(n, k, seed, v.data(), s.support.data()));
+  s.values = detail::from_f64<Scalar>(v.data(), n);
   return s;
 }
-inline PartialCirculantOperator gen_circulant_sensing(Index n, Index m, std::uint64_t seed) {
-  Vector row(static_cast<size_t>(n < 0 ? 0 : n));
+template <typename Scalar = double>
+PartialCirculantOperator<Scalar> gen_circulant_sensing(Index n, Index m, std::uint64_t seed) {  // :149-168
+  std::vector<double> row(static_cast<size_t>(n < 0 ? 0 : n));
   std::vector<Index> om(static_cast<size_t>(m < 0 ? 0 : m));
   check(cl_gen_circulant_sensing(n, m, seed, row.data(), om.data()));
-  return PartialCirculantOperator(CirculantMatrix(std::move(row)), SubsamplingMask(std::move(om), n));
+  return PartialCirculantOperator<Scalar>(CirculantMatrix<Scalar>(detail::from_f64<Scalar>(row.data(), n)),
+                                          SubsamplingMask(std::move(om), n));
 }
-inline Vector measure(const PartialCirculantOperator& A, const Vector& x) {
-  detail::check_same_size(static_cast<Index>(x.size()), A.n(), "measure");
-  Vector y(static_cast<size_t>(A.m()));
-  check(cl_measure(A.n(), A.m(), A.circulant().first_row().data(), A.mask().omega().data(), x.data(), y.data()));
-  return y;
+template <typename Scalar>
+Vector<Scalar> measure(const PartialCirculantOperator<Scalar>& A, const Vector<Scalar>& x) {  // :171-182
+  detail::check_same_size(detail::size_of(x), A.n(), "measure");
+  std::vector<double> y(static_cast<size_t>(A.m()));
+  check(cl_measure(A.n(), A.m(), detail::F64<Scalar>(A.circulant().first_row()).get(), A.mask().omega().data(),
+                   detail::F64<Scalar>(x).get(), y.data()));
+  return detail::from_f64<Scalar>(y.data(), A.m());
 }
-inline SensingProblem make_problem(Index n, Index m, Index k, std::uint64_t seed) {
-  SensingProblem p;
-  p.signal = gen_sparse_signal(n, k, seed);
-  p.op = gen_circulant_sensing(n, m, seed);
+template <typename Scalar = double>
+SensingProblem<Scalar> make_problem(Index n, Index m, Index k, std::uint64_t seed) {  // sensing.hpp:198-207
+  SensingProblem<Scalar> p;
+  p.signal = gen_sparse_signal<Scalar>(n, k, seed);
+  p.op = gen_circulant_sensing<Scalar>(n, m, seed);
   p.measurements = measure(p.op, p.signal.values);
   p.seed = seed;
   return p;
 }
 
-// ---- solver states (IstaState / CadmmState on the GPU) ---------------------------
-class DeviceState {
- public:
-  DeviceState(int kind, const PartialCirculantOperator& A, const Vector& y, const SolverConfig& cfg) {
-    detail::check_same_size(static_cast<Index>(y.size()), A.m(),
-                            kind == CL_KIND_ISTA ? "ista_setup" : kind == CL_KIND_CADMM ? "cadmm_setup" : "admm_setup");
-    cl_solver* s = nullptr;
-    const cl_config c = cfg.c();
-    check(cl_solver_create(kind, A.n(), A.m(), A.circulant().first_row().data(), A.mask().omega().data(), y.data(),
-                           &c, cfg.device, &s));
-    h_.reset(s);
-    n_ = A.n();
-    m_ = A.m();
-  }
-  cl_solver* handle() const { return h_.get(); }
-  void step(long iters = 1) { check(cl_solver_step(h_.get(), iters)); }
-  Vector get(const char* field) const {
-    const std::string f(field);
-    Vector out(static_cast<size_t>((f == "r" || f == "y") ? m_ : f == "B" ? n_ * n_ : n_));
-    check(cl_solver_get(h_.get(), field, out.data()));
-    return out;
-  }
-  long t() const {
-    int64_t tt = 0;
-    check(cl_solver_info(h_.get(), nullptr, nullptr, &tt, nullptr, nullptr));
-    return static_cast<long>(tt);
-  }
-
- private:
+// ---- device solver handles -------------------------------------------------------
+namespace detail {
+struct Handle {
   struct Del {
     void operator()(cl_solver* s) const { cl_solver_destroy(s); }
   };
-  std::unique_ptr<cl_solver, Del> h_;
-  Index n_ = 0, m_ = 0;
+  std::unique_ptr<cl_solver, Del> h;
+  cl_solver* get() const { return h.get(); }
 };
-struct IstaState : DeviceState {
-  IstaState(const PartialCirculantOperator& A, const Vector& y, const SolverConfig& cfg)
-      : DeviceState(CL_KIND_ISTA, A, y, cfg) {}
-};
-struct CadmmState : DeviceState {
-  CadmmState(const PartialCirculantOperator& A, const Vector& y, const SolverConfig& cfg)
-      : DeviceState(CL_KIND_CADMM, A, y, cfg) {}
-};
-inline IstaState ista_setup(const PartialCirculantOperator& A, const Vector& y, const SolverConfig& cfg) {
-  return IstaState(A, y, cfg);
+template <typename Scalar>
+Handle create(int kind, const PartialCirculantOperator<Scalar>& A, const Vector<Scalar>& y, const SolverConfig& cfg,
+              bool use_fft) {
+  SolverConfig c2 = cfg;
+  c2.use_fft = use_fft;
+  const cl_config k = c2.c();
+  cl_solver* s = nullptr;
+  check(cl_solver_create(kind, A.n(), A.m(), F64<Scalar>(A.circulant().first_row()).get(), A.mask().omega().data(),
+                         F64<Scalar>(y).get(), &k, cfg.device, &s));
+  Handle h;
+  h.h.reset(s);
+  return h;
 }
-inline void ista_step(IstaState& s, bool /*use_fft*/ = true) { s.step(1); }
-inline CadmmState cadmm_setup(const PartialCirculantOperator& A, const Vector& y, const SolverConfig& cfg) {
-  return CadmmState(A, y, cfg);
+template <typename Scalar>
+Vector<Scalar> get_field(cl_solver* s, const char* f, Index len) {
+  std::vector<double> out(static_cast<size_t>(len));
+  check(cl_solver_get(s, f, out.data()));
+  return from_f64<Scalar>(out.data(), len);
 }
-inline void cadmm_step(CadmmState& s, bool /*use_fft*/ = true) { s.step(1); }
-// Dense ADMM (solvers.hpp:267-327): B = (A~^T A~ + rho I)^-1 built in fp64 on the GPU; get("B") is n x n.
-struct AdmmState : DeviceState {
-  AdmmState(const PartialCirculantOperator& A, const Vector& y, const SolverConfig& cfg)
-      : DeviceState(CL_KIND_ADMM, A, y, cfg) {}
-};
-inline AdmmState admm_setup(const PartialCirculantOperator& A, const Vector& y, const SolverConfig& cfg) {
-  return AdmmState(A, y, cfg);
+template <typename Scalar>
+void set_field(cl_solver* s, const char* f, const Vector<Scalar>& v) {
+  check(cl_solver_set(s, f, F64<Scalar>(v).get()));
 }
-inline void admm_step(AdmmState& s) { s.step(1); }
+inline void scalars(cl_solver* s, double* scale, double* thr) { check(cl_solver_info(s, nullptr, nullptr, nullptr, scale, thr)); }
+}  // namespace detail
 
+// Common part of the states: the device solvers (one per engine used) and the hand-over between them.
+template <typename Scalar>
+class EngineStates {
+ public:
+  EngineStates() = default;
+  EngineStates(int kind, const PartialCirculantOperator<Scalar>& A, const Vector<Scalar>& y, const SolverConfig& cfg)
+      : kind_(kind), A_(std::make_shared<PartialCirculantOperator<Scalar>>(A)),
+        y_(std::make_shared<Vector<Scalar>>(y)), cfg_(cfg) {
+    active_ = cfg.use_fft ? 1 : 0;
+    h_[active_] = detail::create(kind, A, y, cfg, cfg.use_fft);
+  }
+  cl_solver* handle() const { return h_[active_].get(); }
+  // make `engine` (0 direct, 1 FFT) the active solver; the state vectors move over
+  void use(int engine, const char* const* fields, int nfields) {
+    if (engine == active_) return;
+    if (!h_[engine].get()) h_[engine] = detail::create(kind_, *A_, *y_, cfg_, engine == 1);
+    for (int i = 0; i < nfields; ++i) {
+      const std::string f = fields[i];
+      const Index len = (f == "r") ? A_->m() : A_->n();
+      const Vector<Scalar> v = detail::get_field<Scalar>(h_[active_].get(), fields[i], len);
+      detail::set_field<Scalar>(h_[engine].get(), fields[i], v);
+    }
+    active_ = engine;
+  }
+  void step(long iters) { check(cl_solver_step(handle(), iters)); }
+  Index n() const { return A_->n(); }
+  Index m() const { return A_->m(); }
+
+ private:
+  int kind_ = 0;
+  std::shared_ptr<PartialCirculantOperator<Scalar>> A_;
+  std::shared_ptr<Vector<Scalar>> y_;
+  SolverConfig cfg_;
+  int active_ = 0;
+  detail::Handle h_[2];
+};
+
+// IstaState + ista_setup (solvers.hpp:208-249)
+template <typename Scalar = double>
+struct IstaState {
+  CirculantMatrix<Scalar> C;  // normalized sensing circulant (host copy)
+  SubsamplingMask mask;
+  Vector<Scalar> y;  // normalized measurements
+  Scalar tau = Scalar(0);
+  Scalar threshold = Scalar(0);
+  Vector<Scalar> x, r, delta;
+  long t = 0;
+  EngineStates<Scalar> dev;
+
+  static constexpr const char* kFields[] = {"x", "r", "delta"};
+  // k iterations on the device without refreshing the host members (the fast path)
+  void step(long k) {
+    dev.step(k);
+    t += k;
+  }
+  void sync() {  // device -> host members
+    x = detail::get_field<Scalar>(dev.handle(), "x", dev.n());
+    r = detail::get_field<Scalar>(dev.handle(), "r", dev.m());
+    delta = detail::get_field<Scalar>(dev.handle(), "delta", dev.n());
+  }
+};
+template <typename Scalar>
+IstaState<Scalar> ista_setup(const PartialCirculantOperator<Scalar>& A, const Vector<Scalar>& y,
+                             const SolverConfig& cfg) {
+  detail::check_same_size(detail::size_of(y), A.m(), "ista_setup");
+  IstaState<Scalar> st;
+  st.dev = EngineStates<Scalar>(CL_KIND_ISTA, A, y, cfg);
+  double s = 1, thr = 0;
+  detail::scalars(st.dev.handle(), &s, &thr);
+  Vector<Scalar> cn = A.circulant().first_row(), yn = y;
+  for (Index i = 0; i < detail::size_of(cn); ++i) cn[i] = static_cast<Scalar>(cn[i] / s);
+  for (Index i = 0; i < detail::size_of(yn); ++i) yn[i] = static_cast<Scalar>(yn[i] / s);
+  st.C = CirculantMatrix<Scalar>(std::move(cn));
+  st.mask = A.mask();
+  st.y = std::move(yn);
+  st.tau = static_cast<Scalar>(cfg.tau == 0.0 ? 0.9 : cfg.tau);
+  st.threshold = static_cast<Scalar>(thr);
+  st.x = detail::zeros<Scalar>(A.n());
+  st.r = detail::zeros<Scalar>(A.m());
+  st.delta = detail::zeros<Scalar>(A.n());
+  return st;
+}
+// ista_step (solvers.hpp:252-263): one iteration with the engine `use_fft` picks, host members refreshed
+template <typename Scalar>
+void ista_step(IstaState<Scalar>& s, bool use_fft = true) {
+  s.dev.use(use_fft ? 1 : 0, IstaState<Scalar>::kFields, 3);
+  s.step(1);
+  s.sync();
+}
+
+// CadmmState + cadmm_setup (solvers.hpp:337-395)
+template <typename Scalar = double>
+struct CadmmState {
+  CirculantMatrix<Scalar> C;
+  SubsamplingMask mask;
+  CirculantMatrix<Scalar> B;
+  DiagonalOperator<Scalar> D;
+  Vector<Scalar> Pty;
+  Scalar rho = Scalar(0), sigma = Scalar(0), tau1 = Scalar(1), tau2 = Scalar(1);
+  Scalar threshold = Scalar(0);
+  Vector<Scalar> x, z, nu, mu, v, beta;
+  long t = 0;
+  EngineStates<Scalar> dev;
+
+  static constexpr const char* kFields[] = {"x", "z", "nu", "mu", "v", "beta"};
+  void step(long k) {
+    dev.step(k);
+    t += k;
+  }
+  void sync() {
+    Vector<Scalar>* dst[] = {&x, &z, &nu, &mu, &v, &beta};
+    for (int i = 0; i < 6; ++i) *dst[i] = detail::get_field<Scalar>(dev.handle(), kFields[i], dev.n());
+  }
+};
+template <typename Scalar>
+CadmmState<Scalar> cadmm_setup(const PartialCirculantOperator<Scalar>& A, const Vector<Scalar>& y,
+                               const SolverConfig& cfg) {
+  detail::check_same_size(detail::size_of(y), A.m(), "cadmm_setup");
+  CadmmState<Scalar> st;
+  st.dev = EngineStates<Scalar>(CL_KIND_CADMM, A, y, cfg);
+  double s = 1, thr = 0;
+  detail::scalars(st.dev.handle(), &s, &thr);
+  const Index n = A.n();
+  // host members in fp64 arithmetic like the reference's (the device keeps its own fp32 copies)
+  Vector<Scalar> cn = A.circulant().first_row();
+  for (Index i = 0; i < n; ++i) cn[i] = static_cast<Scalar>(cn[i] / s);
+  st.C = CirculantMatrix<Scalar>(std::move(cn));
+  st.mask = A.mask();
+  st.B = regularized_gram_inverse(st.C, static_cast<Scalar>(cfg.rho), static_cast<Scalar>(cfg.sigma));
+  st.D = mask_gram_inverse<Scalar>(A.mask(), static_cast<Scalar>(cfg.rho));
+  st.Pty = detail::zeros<Scalar>(n);
+  for (Index t = 0; t < A.m(); ++t) st.Pty[A.mask().omega()[static_cast<size_t>(t)]] = static_cast<Scalar>(y[t] / s);
+  st.rho = static_cast<Scalar>(cfg.rho);
+  st.sigma = static_cast<Scalar>(cfg.sigma);
+  st.tau1 = static_cast<Scalar>(cfg.tau1);
+  st.tau2 = static_cast<Scalar>(cfg.tau2);
+  st.threshold = static_cast<Scalar>(thr);
+  for (Vector<Scalar>* v : {&st.x, &st.z, &st.nu, &st.mu, &st.v, &st.beta}) *v = detail::zeros<Scalar>(n);
+  return st;
+}
+// cadmm_step (solvers.hpp:399-415)
+template <typename Scalar>
+void cadmm_step(CadmmState<Scalar>& s, bool use_fft = true) {
+  s.dev.use(use_fft ? 1 : 0, CadmmState<Scalar>::kFields, 6);
+  s.step(1);
+  s.sync();
+}
+
+// AdmmState + admm_setup (solvers.hpp:267-314): the dense baseline, B built in fp64 on the GPU
+template <typename Scalar = double>
+struct AdmmState {
+  Vector<Scalar> Aty;
+  Scalar rho = Scalar(0), threshold = Scalar(0);
+  Vector<Scalar> x, z, u, rhs;
+  long t = 0;
+  EngineStates<Scalar> dev;
+
+  void step(long k) {
+    dev.step(k);
+    t += k;
+  }
+  void sync() {
+    x = detail::get_field<Scalar>(dev.handle(), "x", dev.n());
+    z = detail::get_field<Scalar>(dev.handle(), "z", dev.n());
+    u = detail::get_field<Scalar>(dev.handle(), "u", dev.n());
+    rhs = detail::get_field<Scalar>(dev.handle(), "rhs", dev.n());
+  }
+  // the explicit inverse, n x n row-major (the footprint the circulant solvers avoid)
+  std::vector<double> B() const {
+    std::vector<double> out(static_cast<size_t>(dev.n() * dev.n()));
+    check(cl_solver_get(dev.handle(), "B", out.data()));
+    return out;
+  }
+};
+template <typename Scalar>
+AdmmState<Scalar> admm_setup(const PartialCirculantOperator<Scalar>& A, const Vector<Scalar>& y,
+                             const SolverConfig& cfg) {
+  detail::check_same_size(detail::size_of(y), A.m(), "admm_setup");
+  SolverConfig c2 = cfg;
+  c2.use_fft = false;
+  AdmmState<Scalar> st;
+  st.dev = EngineStates<Scalar>(CL_KIND_ADMM, A, y, c2);
+  double s = 1, thr = 0;
+  detail::scalars(st.dev.handle(), &s, &thr);
+  st.Aty = detail::get_field<Scalar>(st.dev.handle(), "aty", A.n());
+  st.rho = static_cast<Scalar>(cfg.rho);
+  st.threshold = static_cast<Scalar>(thr);
+  st.x = st.z = st.u = detail::zeros<Scalar>(A.n());
+  st.rhs = st.Aty;
+  return st;
+}
+template <typename Scalar>
+void admm_step(AdmmState<Scalar>& s) {  // solvers.hpp:318-327
+  s.step(1);
+  s.sync();
+}
+
+// ---- run_loop / *_run (solvers.hpp:426-534) ------------------------------------------
 namespace detail {
-template <typename RunFn>
-inline RecoveryReport run_with(RunFn run_fn, const SolverConfig& cfg, Index n) {
+template <typename Scalar, typename RunFn>
+RecoveryReport<Scalar> run_with(RunFn run_fn, const SolverConfig& cfg, Index n) {
   const long cap = cfg.max_iter >= 0 ? cfg.max_iter / (cfg.check_every > 0 ? cfg.check_every : 1) + 2 : 0;
   std::vector<int64_t> it(static_cast<size_t>(cap > 0 ? cap : 1));
-  std::vector<double> val(it.size()), sec(it.size());
-  RecoveryReport rep;
-  rep.final_x.resize(static_cast<size_t>(n));
+  std::vector<double> val(it.size()), sec(it.size()), fx(static_cast<size_t>(n));
   cl_report r{};
-  check(run_fn(&r, rep.final_x.data(), it.data(), val.data(), sec.data(), static_cast<int64_t>(cap)));
+  check(run_fn(&r, fx.data(), it.data(), val.data(), sec.data(), static_cast<int64_t>(cap)));
+  RecoveryReport<Scalar> rep;
+  rep.final_x = from_f64<Scalar>(fx.data(), n);
   rep.iterations = static_cast<long>(r.iterations);
   rep.setup_seconds = r.setup_seconds;
   rep.total_seconds = r.total_seconds;
   rep.footprint_bytes = r.footprint_bytes;
   rep.metric = r.metric == CL_METRIC_MSE_VS_TRUTH ? StopMetric::kMseVsTruth : StopMetric::kIterateChange;
   rep.reached_target = r.reached_target != 0;
-  rep.final_metric = r.final_metric;
+  rep.final_metric = static_cast<Scalar>(r.final_metric);
   for (int64_t i = 0; i < r.trace_len && i < cap; ++i)
-    rep.mse_trace.push_back({static_cast<long>(it[static_cast<size_t>(i)]), val[static_cast<size_t>(i)],
+    rep.mse_trace.push_back({static_cast<long>(it[static_cast<size_t>(i)]), static_cast<Scalar>(val[static_cast<size_t>(i)]),
                              sec[static_cast<size_t>(i)]});
   return rep;
 }
-inline RecoveryReport run(DeviceState& st, const Vector* truth, const SolverConfig& cfg, Index n) {
+template <typename Scalar>
+RecoveryReport<Scalar> run(int kind, const Vector<Scalar>& y, const PartialCirculantOperator<Scalar>& A,
+                           const SolverConfig& cfg, const Vector<Scalar>* truth, const char* name) {
+  check_same_size(size_of(y), A.m(), name);
+  Handle h = create(kind, A, y, cfg, cfg.use_fft && kind != CL_KIND_ADMM);
   if (truth) {
-    check_same_size(static_cast<Index>(truth->size()), n, "truth");
-    check(cl_solver_set_truth(st.handle(), truth->data()));
+    check_same_size(size_of(*truth), A.n(), "truth");
+    check(cl_solver_set_truth(h.get(), F64<Scalar>(*truth).get()));
   }
-  return run_with(
+  return run_with<Scalar>(
       [&](cl_report* r, double* fx, int64_t* it, double* val, double* sec, int64_t cap) {
-        return cl_solver_run(st.handle(), r, fx, it, val, sec, cap);
+        return cl_solver_run(h.get(), r, fx, it, val, sec, cap);
       },
-      cfg, n);
+      cfg, A.n());
 }
 }  // namespace detail
 
-// solvers.hpp:479-495
-inline RecoveryReport ista_run(const Vector& y, const PartialCirculantOperator& A, const SolverConfig& cfg,
-                               const Vector* truth = nullptr) {
-  IstaState st(A, y, cfg);
-  return detail::run(st, truth, cfg, A.n());
+template <typename Scalar>
+RecoveryReport<Scalar> ista_run(const Vector<Scalar>& y, const PartialCirculantOperator<Scalar>& A,
+                                const SolverConfig& cfg, const Vector<Scalar>* truth = nullptr) {  // :479-495
+  return detail::run(CL_KIND_ISTA, y, A, cfg, truth, "ista_setup");
 }
-// solvers.hpp:518-534
-inline RecoveryReport cadmm_run(const Vector& y, const PartialCirculantOperator& A, const SolverConfig& cfg,
-                                const Vector* truth = nullptr) {
-  CadmmState st(A, y, cfg);
-  return detail::run(st, truth, cfg, A.n());
+template <typename Scalar>
+RecoveryReport<Scalar> admm_dense_run(const Vector<Scalar>& y, const PartialCirculantOperator<Scalar>& A,
+                                      const SolverConfig& cfg, const Vector<Scalar>* truth = nullptr) {  // :497-514
+  return detail::run(CL_KIND_ADMM, y, A, cfg, truth, "admm_setup");
 }
-
-// solvers.hpp:497-514
-inline RecoveryReport admm_dense_run(const Vector& y, const PartialCirculantOperator& A, const SolverConfig& cfg,
-                                     const Vector* truth = nullptr) {
-  AdmmState st(A, y, cfg);
-  return detail::run(st, truth, cfg, A.n());
+template <typename Scalar>
+RecoveryReport<Scalar> cadmm_run(const Vector<Scalar>& y, const PartialCirculantOperator<Scalar>& A,
+                                 const SolverConfig& cfg, const Vector<Scalar>* truth = nullptr) {  // :518-534
+  return detail::run(CL_KIND_CADMM, y, A, cfg, truth, "cadmm_setup");
 }
 
 // ---- sharded solve from one process (cl_group_*) -----------------------
 // Rank r on devices[r]; after each phase the ranks exchange their slices inside the library: NCCL
 // (ncclCommInitAll over the listed GPUs) or peer copies (Transport::kCopy; devices may repeat).  The
 // iterate equals the unsharded solve's bitwise.  One process per GPU instead: cl_comm_init_rank +
-// cl_solver_attach_comm on a DeviceState's handle.
+// cl_solver_attach_comm on a solver handle.
 enum class Transport { kNccl = CL_TRANSPORT_NCCL, kCopy = CL_TRANSPORT_COPY };
+template <typename Scalar = double>
 class ShardedSolve {
  public:
-  ShardedSolve(int kind, const PartialCirculantOperator& A, const Vector& y, const SolverConfig& cfg,
+  ShardedSolve(int kind, const PartialCirculantOperator<Scalar>& A, const Vector<Scalar>& y, const SolverConfig& cfg,
                const std::vector<int>& devices, Transport transport = Transport::kNccl)
       : cfg_(cfg), n_(A.n()), m_(A.m()) {
-    detail::check_same_size(static_cast<Index>(y.size()), A.m(), kind == CL_KIND_ISTA ? "ista_setup" : "cadmm_setup");
+    detail::check_same_size(detail::size_of(y), A.m(), kind == CL_KIND_ISTA ? "ista_setup" : "cadmm_setup");
     cl_group* g = nullptr;
     const cl_config c = cfg.c();
-    check(cl_group_create(kind, A.n(), A.m(), A.circulant().first_row().data(), A.mask().omega().data(), y.data(), &c,
-                          devices.data(), static_cast<int>(devices.size()), static_cast<int>(transport), &g));
+    check(cl_group_create(kind, A.n(), A.m(), detail::F64<Scalar>(A.circulant().first_row()).get(),
+                          A.mask().omega().data(), detail::F64<Scalar>(y).get(), &c, devices.data(),
+                          static_cast<int>(devices.size()), static_cast<int>(transport), &g));
     g_.reset(g);
   }
   void step(long iters = 1) { check(cl_group_step(g_.get(), iters)); }
-  Vector get(const char* field) const {
+  Vector<Scalar> get(const char* field) const {
     const std::string f(field);
-    Vector out(static_cast<size_t>((f == "r" || f == "y") ? m_ : n_));
+    const Index len = (f == "r" || f == "y") ? m_ : n_;
+    std::vector<double> out(static_cast<size_t>(len));
     check(cl_group_get(g_.get(), field, out.data()));
-    return out;
+    return detail::from_f64<Scalar>(out.data(), len);
   }
   int world() const {
     int w = 0;
     check(cl_group_info(g_.get(), &w, nullptr, nullptr));
     return w;
   }
-  RecoveryReport run(const Vector* truth = nullptr) {
+  RecoveryReport<Scalar> run(const Vector<Scalar>* truth = nullptr) {
     if (truth) {
-      detail::check_same_size(static_cast<Index>(truth->size()), n_, "truth");
-      check(cl_group_set_truth(g_.get(), truth->data()));
+      detail::check_same_size(detail::size_of(*truth), n_, "truth");
+      check(cl_group_set_truth(g_.get(), detail::F64<Scalar>(*truth).get()));
     }
-    return detail::run_with(
+    return detail::run_with<Scalar>(
         [&](cl_report* r, double* fx, int64_t* it, double* val, double* sec, int64_t cap) {
           return cl_group_run(g_.get(), r, fx, it, val, sec, cap);
         },
@@ -448,30 +802,144 @@ class ShardedSolve {
   Index n_ = 0, m_ = 0;
 };
 
+// ---- images and deblurring (image.hpp, deblur.hpp) -----------------------------------
+template <typename Scalar = double>
+struct GrayImage {  // image.hpp:24-38
+  Index width = 0;
+  Index height = 0;
+  Vector<Scalar> pixels;  // row-major, width * height entries in [0, 1]
+  Index size() const { return width * height; }
+  Scalar& at(Index row, Index col) { return pixels[row * width + col]; }
+  Scalar at(Index row, Index col) const { return pixels[row * width + col]; }
+};
+template <typename Scalar>
+GrayImage<Scalar> make_image(Index width, Index height, const Vector<Scalar>& values) {  // image.hpp:41-54
+  if (width < 1 || height < 1) throw ParameterError("make_image: dimensions must be positive");
+  detail::check_same_size(detail::size_of(values), width * height, "make_image");
+  GrayImage<Scalar> img;
+  img.width = width;
+  img.height = height;
+  img.pixels = values;
+  for (Index i = 0; i < detail::size_of(values); ++i)
+    img.pixels[i] = std::min(Scalar(1), std::max(Scalar(0), values[i]));
+  return img;
+}
+template <typename Scalar = double>
+GrayImage<Scalar> read_pgm(const std::string& path) {  // image.hpp:95-135
+  int64_t w = 0, h = 0;
+  check(cl_read_pgm(path.c_str(), nullptr, 0, &w, &h));
+  std::vector<double> px(static_cast<size_t>(w * h));
+  check(cl_read_pgm(path.c_str(), px.data(), w * h, &w, &h));
+  GrayImage<Scalar> img;
+  img.width = w;
+  img.height = h;
+  img.pixels = detail::from_f64<Scalar>(px.data(), w * h);
+  return img;
+}
+template <typename Scalar>
+void write_pgm(const GrayImage<Scalar>& img, const std::string& path) {  // image.hpp:137-153
+  if (img.width < 1 || img.height < 1) throw ParameterError("write_pgm: empty image");
+  detail::check_same_size(detail::size_of(img.pixels), img.size(), "write_pgm");
+  check(cl_write_pgm(path.c_str(), img.width, img.height, detail::F64<Scalar>(img.pixels).get()));
+}
+template <typename Scalar = double>
+CirculantMatrix<Scalar> blur_matrix(Index n, Index L) {  // deblur.hpp:26-36
+  std::vector<double> row(static_cast<size_t>(n < 0 ? 0 : n));
+  check(cl_blur_row(n, L, row.data()));
+  return CirculantMatrix<Scalar>(detail::from_f64<Scalar>(row.data(), n));
+}
+template <typename Scalar>
+PartialCirculantOperator<Scalar> compose_sensing(const CirculantMatrix<Scalar>& C, const CirculantMatrix<Scalar>& B,
+                                                 const SubsamplingMask& mask) {  // deblur.hpp:53-64
+  detail::check_same_size(C.n(), B.n(), "compose_sensing");
+  detail::check_same_size(mask.n(), C.n(), "compose_sensing");
+  return PartialCirculantOperator<Scalar>(circ_compose(C, B), mask);  // cl_compose_rows short-circuits identities
+}
+template <typename Scalar = double>
+GrayImage<Scalar> gen_star_field(Index width, Index height, double density, std::uint64_t seed) {  // :69-86
+  if (width < 1 || height < 1) throw ParameterError("gen_star_field: dimensions must be positive");
+  std::vector<double> px(static_cast<size_t>(width * height));
+  check(cl_gen_star_field(width, height, density, seed, px.data()));
+  GrayImage<Scalar> img;
+  img.width = width;
+  img.height = height;
+  img.pixels = detail::from_f64<Scalar>(px.data(), width * height);
+  return img;
+}
+template <typename Scalar = double>
+struct DeblurResult {  // deblur.hpp:93-101
+  GrayImage<Scalar> recovered;
+  RecoveryReport<Scalar> report;
+  Vector<Scalar> error_map;
+  Scalar mse_vs_truth = std::numeric_limits<Scalar>::quiet_NaN();
+  Scalar error_map_mean = std::numeric_limits<Scalar>::quiet_NaN();
+  Scalar normalized_mse = std::numeric_limits<Scalar>::quiet_NaN();
+};
+template <typename Scalar>
+DeblurResult<Scalar> deblur_recover(const Vector<Scalar>& y, const CirculantMatrix<Scalar>& C,
+                                    const CirculantMatrix<Scalar>& B, const SubsamplingMask& mask, Index width,
+                                    Index height, const SolverConfig& cfg,
+                                    const GrayImage<Scalar>* truth = nullptr) {  // deblur.hpp:107-136
+  if (width < 1 || height < 1) throw ParameterError("deblur_recover: dimensions must be positive");
+  const PartialCirculantOperator<Scalar> A = compose_sensing(C, B, mask);
+  detail::check_same_size(A.n(), width * height, "deblur_recover");
+  detail::check_same_size(detail::size_of(y), A.m(), "deblur_recover");
+  if (truth) detail::check_same_size(detail::size_of(truth->pixels), A.n(), "deblur_recover");
+  DeblurResult<Scalar> result;
+  result.report = cadmm_run<Scalar>(y, A, cfg, nullptr);
+  result.recovered = make_image(width, height, result.report.final_x);
+  if (truth) {
+    const Index n = A.n();
+    result.mse_vs_truth = mse(result.report.final_x, truth->pixels);
+    Scalar mean = 0;
+    for (Index i = 0; i < n; ++i) mean += truth->pixels[i];
+    mean /= static_cast<Scalar>(n);
+    const Scalar scale = mean > Scalar(0) ? mean : Scalar(1);
+    result.error_map = detail::zeros<Scalar>(n);
+    Scalar emean = 0;
+    for (Index i = 0; i < n; ++i) {
+      result.error_map[i] = std::abs(result.report.final_x[i] - truth->pixels[i]) / scale;
+      emean += result.error_map[i];
+    }
+    result.error_map_mean = emean / static_cast<Scalar>(n);
+    result.normalized_mse = result.mse_vs_truth / (scale * scale);
+  }
+  return result;
+}
+template <typename Scalar>
+DeblurResult<Scalar> run_deblur_experiment(const GrayImage<Scalar>& image, Index L, Index m, const SolverConfig& cfg,
+                                           std::uint64_t seed) {  // deblur.hpp:141-156
+  const Index n = image.size();
+  detail::check_same_size(detail::size_of(image.pixels), n, "run_deblur_experiment");
+  const CirculantMatrix<Scalar> B = blur_matrix<Scalar>(n, L);
+  const PartialCirculantOperator<Scalar> sensing = gen_circulant_sensing<Scalar>(n, m, seed);
+  const PartialCirculantOperator<Scalar> A = compose_sensing(sensing.circulant(), B, sensing.mask());
+  const Vector<Scalar> y = measure(A, image.pixels);
+  return deblur_recover(y, sensing.circulant(), B, sensing.mask(), image.width, image.height, cfg, &image);
+}
+
 // ---- artifact formats (io.hpp) ---------------------------------------------------
-inline void write_vector(const Vector& v, const std::string& path) {  // io.hpp:80-87
+inline void write_vector(const Vector<double>& v, const std::string& path) {  // io.hpp:80-87
   check(cl_write_vector(path.c_str(), v.data(), static_cast<int64_t>(v.size())));
 }
-inline Vector read_vector(const std::string& path) {  // io.hpp:89-97
+inline Vector<double> read_vector(const std::string& path) {  // io.hpp:89-97
   int64_t n = 0;
   check(cl_read_vector(path.c_str(), nullptr, 0, &n));
-  Vector v(static_cast<size_t>(n));
+  std::vector<double> v(static_cast<size_t>(n));
   check(cl_read_vector(path.c_str(), v.data(), n, &n));
-  return v;
+  return detail::from_f64<double>(v.data(), n);
 }
-inline void write_operator(const PartialCirculantOperator& A, const std::string& path) {  // io.hpp:99-112
-  const std::vector<Index>& om = A.mask().omega();
-  std::vector<int64_t> o(om.begin(), om.end());
-  check(cl_write_operator(path.c_str(), A.n(), A.m(), A.circulant().first_row().data(), o.data()));
+inline void write_operator(const PartialCirculantOperator<double>& A, const std::string& path) {  // io.hpp:99-112
+  check(cl_write_operator(path.c_str(), A.n(), A.m(), A.circulant().first_row().data(), A.mask().omega().data()));
 }
-inline PartialCirculantOperator read_operator(const std::string& path) {  // io.hpp:114-131
+inline PartialCirculantOperator<double> read_operator(const std::string& path) {  // io.hpp:114-131
   int64_t n = 0, m = 0;
   check(cl_read_operator(path.c_str(), nullptr, 0, nullptr, 0, &n, &m));
-  Vector row(static_cast<size_t>(n));
-  std::vector<int64_t> om(static_cast<size_t>(m));
+  std::vector<double> row(static_cast<size_t>(n));
+  std::vector<Index> om(static_cast<size_t>(m));
   check(cl_read_operator(path.c_str(), row.data(), n, om.data(), m, &n, &m));
-  return PartialCirculantOperator(CirculantMatrix(std::move(row)),
-                                  SubsamplingMask(std::vector<Index>(om.begin(), om.end()), n));
+  return PartialCirculantOperator<double>(CirculantMatrix<double>(detail::from_f64<double>(row.data(), n)),
+                                          SubsamplingMask(std::move(om), n));
 }
 
 struct BenchRow {  // io.hpp:133-153

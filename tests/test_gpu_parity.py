@@ -245,6 +245,9 @@ def test_cpp_adapter_gpu():
                        "adapter_test")
     out = subprocess.run([exe, "gpu"], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0 and "PASS" in out.stdout, out.stdout + out.stderr
+    eig = os.path.join(os.path.dirname(exe), "eigen_style_test")  # the adapter's Eigen branch (test double)
+    out = subprocess.run([eig, "gpu"], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "PASS" in out.stdout, out.stdout + out.stderr
 
 
 # --------------------------------------------------------------- FFT engine (SolverConfig.use_fft=True)

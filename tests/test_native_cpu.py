@@ -129,6 +129,15 @@ def test_cpp_adapter_cpu_parts():
     assert out.returncode == 0 and "PASS" in out.stdout, out.stdout + out.stderr
 
 
+def test_cpp_adapter_eigen_branch_cpu_parts():
+    """Reference-style Eigen code (Vector<double>::Zero, comma initializer, <double> templates) against the
+    adapter's __has_include(<Eigen/Dense>) branch, built with the Eigen test double of tests/cpp/eigen_stub."""
+    import subprocess
+    exe = os.path.join(ROOT, "paper_1707_02244_b200", "_lib", "eigen_style_test")
+    out = subprocess.run([exe, "cpu"], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0 and "PASS" in out.stdout, out.stdout + out.stderr
+
+
 # ---------------------------------------------------------------- artifact formats (io.hpp)
 def test_vector_files_roundtrip_bit_for_bit(tmp_path):
     """io_cli_test.cpp:81-95"""
