@@ -643,55 +643,6 @@ k_grad_s(const float* __restrict__ h, const int* __restrict__ omega, const float
     if (ib + q < n) out[ib + q] = acc[q];
 }
 
-// Dense product with the streamed-window layout (all 32 positions of every block,
-// no tests): out[i] = sum_j h[(i - j) mod n] u[j].  Experiment beside k_conv_dense.
-template <int R>
-__device__ __forceinline__ void dense_block_s(float (&acc)[R], const float* __restrict__ wp,
-                                              const float* __restrict__ ub) {
-  grad_block_s<R, false>(acc, wp, ub, 0xffffffffu);
-}
-
-template <int R, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB)
-k_dense_s(const float* __restrict__ h, const float* __restrict__ u, int64_t n, int64_t chunks, int splits,
-          int64_t tile_lo, float* __restrict__ partial) {
-  constexpr int PB = 32;
-  using G = GeoU<R>;
-  extern __shared__ float4 smem_f4[];
-  float* hs = reinterpret_cast<float*>(smem_f4);
-  float* us = hs + G::kSegPhys;
-  const int64_t unit = blockIdx.x;
-  const int64_t tile = tile_lo + unit / splits;
-  const int split = static_cast<int>(unit % splits);
-  const int64_t I0 = tile * G::kTileR;
-  int64_t blo, bhi;
-  split_blocks(chunks, splits, split, &blo, &bhi);
-  const int own = threadIdx.x;
-  float acc[R];
-#pragma unroll
-  for (int q = 0; q < R; ++q) acc[q] = 0.f;
-  for (int64_t ch = blo / (kChunk / 32); ch * (kChunk / 32) < bhi; ++ch) {
-    const int64_t Jc = ch * kChunk;
-    stage_plain<G::kSeg>(hs, h, n, I0 - Jc - kChunk);
-    for (int s = threadIdx.x; s < kChunk; s += kThreads) {
-      const int64_t j = Jc + s;
-      us[s] = j < n ? __ldg(u + j) : 0.f;
-    }
-    __syncthreads();
-    const int64_t cb = ch * (kChunk / 32);
-    const int b0 = static_cast<int>(blo > cb ? blo - cb : 0);
-    const int b1 = static_cast<int>(bhi - cb < kChunk / 32 ? bhi - cb : kChunk / 32);
-    const float* wl = hs + own * R + kChunk - PB;
-    for (int b = b0; b < b1; ++b) dense_block_s<R>(acc, wl - b * PB, us + b * PB);
-    __syncthreads();
-  }
-  const int64_t ib = I0 + own * R;
-  float* out = partial + static_cast<int64_t>(split) * n;
-#pragma unroll
-  for (int q = 0; q < R; ++q)
-    if (ib + q < n) out[ib + q] = acc[q];
-}
-
 // Residual block (dot form, x register-resident): row s computes
 // sum_q w[s - q + R] x[q]; position s needs w[s+1 .. s+R], so the window
 // moves up by 4 per group.
@@ -745,93 +696,7 @@ __device__ __forceinline__ void res_block_s(const float* __restrict__ wp, const 
   res_group_s<R, 7, PAIR, CH>(w, xr, mask, wp, lpp);
 }
 
-// ---- FFMA2 residual (fma.rn.f32x2: two FMAs per issue slot) ------------------
-// The dot form's three-register FFMAs chain on each other; with packed pairs a
-// row needs R/2 (+1) FFMA2s and the issue slots in between are free for the
-// block skeleton.  Window pairs are the natural (w[2b], w[2b+1]) register pairs
-// from LDS.128; the two row parities pair them with two register layouts of x:
-//   S + R even:  W[(S+R)/2 - a] . (x[2a], x[2a-1]),   a = 0 .. R/2  (x[-1] = 0)
-//   S + R odd:   W[(S+R-1)/2 - a] . (x[2a+1], x[2a]), a = 0 .. R/2-1
-// (row S: sum_q w[S - q + R] x[q]; an even term uses x[R] = 0 at the edge).
-__device__ __forceinline__ unsigned long long pk2(float a, float b) {
-  unsigned long long r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ float2 up2(unsigned long long u) {
-  float2 v;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(u));
-  return v;
-}
-__device__ __forceinline__ unsigned long long fma2(unsigned long long a, unsigned long long b, unsigned long long c) {
-  unsigned long long d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-template <int NP, int K>  // pairs K, K+1 <- LDS.128 at float offset 2K
-__device__ __forceinline__ void ld2p(unsigned long long (&W)[NP], const float* __restrict__ wp) {
-  const ulonglong2 t = *reinterpret_cast<const ulonglong2*>(wp + 2 * K);
-  W[K] = t.x;
-  W[K + 1] = t.y;
-}
-template <int R, int S>
-__device__ __forceinline__ void res_row_f2(const unsigned long long (&W)[(R + 40) / 2],
-                                           const unsigned long long (&XE)[R / 2 + 1],
-                                           const unsigned long long (&XO)[R / 2], float*& lpp) {
-  unsigned long long c0 = 0ull, c1 = 0ull;
-  if constexpr (((S + R) & 1) == 0) {
-#pragma unroll
-    for (int a = 0; a <= R / 2; a += 2) {
-      c0 = fma2(W[(S + R) / 2 - a], XE[a], c0);
-      if (a + 1 <= R / 2) c1 = fma2(W[(S + R) / 2 - a - 1], XE[a + 1], c1);
-    }
-  } else {
-#pragma unroll
-    for (int a = 0; a < R / 2; a += 2) {
-      c0 = fma2(W[(S + R - 1) / 2 - a], XO[a], c0);
-      if (a + 1 < R / 2) c1 = fma2(W[(S + R - 1) / 2 - a - 1], XO[a + 1], c1);
-    }
-  }
-  const float2 u = up2(c0), v = up2(c1);
-  *lpp++ = (u.x + u.y) + (v.x + v.y);
-}
-template <int R, int G, bool PAIR>
-__device__ __forceinline__ void res_group_f2(unsigned long long (&W)[(R + 40) / 2],
-                                             const unsigned long long (&XE)[R / 2 + 1],
-                                             const unsigned long long (&XO)[R / 2], uint32_t mask,
-                                             const float* __restrict__ wp, float*& lpp) {
-  if constexpr (G < 7) ld2p<(R + 40) / 2, (R + 8 + 4 * G) / 2>(W, wp);
-  if (pair_live<PAIR>(mask, 4 * G)) {
-    if (row_at(mask, 4 * G)) res_row_f2<R, 4 * G>(W, XE, XO, lpp);
-    if (row_at(mask, 4 * G + 1)) res_row_f2<R, 4 * G + 1>(W, XE, XO, lpp);
-  }
-  if (pair_live<PAIR>(mask, 4 * G + 2)) {
-    if (row_at(mask, 4 * G + 2)) res_row_f2<R, 4 * G + 2>(W, XE, XO, lpp);
-    if (row_at(mask, 4 * G + 3)) res_row_f2<R, 4 * G + 3>(W, XE, XO, lpp);
-  }
-}
-template <int R, bool PAIR>
-__device__ __forceinline__ void res_block_f2(const float* __restrict__ wp, const unsigned long long (&XE)[R / 2 + 1],
-                                             const unsigned long long (&XO)[R / 2], uint32_t mask, float*& lpp) {
-  static_assert(R % 4 == 0, "R must be a multiple of 4");
-  unsigned long long W[(R + 40) / 2];
-#pragma unroll
-  for (int k = 0; k < (R + 8) / 2; k += 2) {
-    const ulonglong2 t = *reinterpret_cast<const ulonglong2*>(wp + 2 * k);
-    W[k] = t.x;
-    W[k + 1] = t.y;
-  }
-  res_group_f2<R, 0, PAIR>(W, XE, XO, mask, wp, lpp);
-  res_group_f2<R, 1, PAIR>(W, XE, XO, mask, wp, lpp);
-  res_group_f2<R, 2, PAIR>(W, XE, XO, mask, wp, lpp);
-  res_group_f2<R, 3, PAIR>(W, XE, XO, mask, wp, lpp);
-  res_group_f2<R, 4, PAIR>(W, XE, XO, mask, wp, lpp);
-  res_group_f2<R, 5, PAIR>(W, XE, XO, mask, wp, lpp);
-  res_group_f2<R, 6, PAIR>(W, XE, XO, mask, wp, lpp);
-  res_group_f2<R, 7, PAIR>(W, XE, XO, mask, wp, lpp);
-}
-
-template <int R, int MINB, bool PAIR = false, int CH = kResChains, bool F2 = false>
+template <int R, int MINB, bool PAIR = false, int CH = kResChains>
 __global__ void __launch_bounds__(kThreads, MINB)
 k_res_s(const float* __restrict__ h, const float* __restrict__ x, const int* __restrict__ omega,
         const int* __restrict__ rowstart, int64_t n, int64_t m, int64_t chunks, int splits, int split_lo,
@@ -861,20 +726,12 @@ k_res_s(const float* __restrict__ h, const float* __restrict__ x, const int* __r
   const int64_t jb = I0 + own * R;
 #pragma unroll
   for (int q = 0; q < R; ++q) xr[q] = (jb + q < n) ? __ldg(x + jb + q) : 0.f;
-  unsigned long long XE[F2 ? R / 2 + 1 : 1], XO[F2 ? R / 2 : 1];
-  if constexpr (F2) {
-#pragma unroll
-    for (int a = 0; a <= R / 2; ++a) XE[a] = pk2(a < R / 2 ? xr[2 * a] : 0.f, a > 0 ? xr[2 * a - 1] : 0.f);
-#pragma unroll
-    for (int a = 0; a < R / 2; ++a) XO[a] = pk2(xr[2 * a + 1], xr[2 * a]);
-  }
 
   for (int64_t ch = blo / (kChunk / 32); ch * (kChunk / 32) < bhi; ++ch) {
     const int64_t Jc = ch * kChunk;
     const int r0 = rowstart[ch], nr = rowstart[ch + 1] - r0;
     if (nr == 0) continue;
-    // (+4: the FFMA2 form reads one element past the window, multiplied by an x of 0)
-    stage_plain<G::kSeg + (F2 ? 4 : 0)>(hs, h, n, Jc - I0 - G::kTileR);
+    stage_plain<G::kSeg>(hs, h, n, Jc - I0 - G::kTileR);
     for (int s = threadIdx.x; s < kChunk; s += kThreads) flag[s] = 0;
     __syncthreads();
     for (int k = threadIdx.x; k < nr; k += kThreads) flag[omega[r0 + k] - static_cast<int>(Jc)] = 1;
@@ -898,8 +755,7 @@ k_res_s(const float* __restrict__ h, const float* __restrict__ x, const int* __r
       const uint32_t mask = __reduce_or_sync(0xffffffffu, bmask[b]);
       if (mask == 0u) continue;
       float* lpp = lp_lane;
-      if constexpr (F2) res_block_f2<R, PAIR>(lane_base + b * PB, XE, XO, mask, lpp);
-      else res_block_s<R, PAIR, CH>(lane_base + b * PB, xr, mask, lpp);
+      res_block_s<R, PAIR, CH>(lane_base + b * PB, xr, mask, lpp);
       __syncwarp();
       reduce_lane_partials(lp, redw, bbase[b], __popc(mask), lane);
       __syncwarp();
@@ -1401,8 +1257,8 @@ constexpr size_t smem_res() {
   return Geo<R>::kSegPhys * 4 + 2 * (kChunk / PB) * 4 + kWarps * kChunk * 4 + kWarps * 32 * 33 * 4;
 }
 
-// Kernel variant table (CLB_GRAD / CLB_RES select an entry for experiments;
-// the defaults are the measured best on B200).
+// Kernel variant table (CLB_GRAD / CLB_RES / CLB_DENSE select an entry; the entries are the defaults,
+// the measured best on B200 -- the rejected variants of DESIGN.md §3 are no longer compiled in).
 struct GradVariant {
   int R, PB;
   void (*fn)(const float*, const int*, const float*, const int*, int64_t, int64_t, int, int64_t, float*);
@@ -1417,34 +1273,25 @@ struct ResVariant {
 const GradVariant kGrad[] = {
     {32, 32, k_conv_rows_ool<4>, smem_rows<32, 32>()},            // 0: small-n default (padded R = 32; C3: 17.2 ms)
     {44, 32, k_grad_s<44, 4, true>, smem_grad_s<44>()},           // 1: large-n default (streamed, pair tests)
-    {44, 32, k_grad_s<44, 4, false>, smem_grad_s<44>()},          // 2: without pair tests
-    {52, 32, k_grad_s<52, 3, true>, smem_grad_s<52>()},           // 3: R = 52 at 3 CTAs/SM
-    {44, 32, k_grad_s<44, 1, true, 512>, smem_grad_s<44, 512>(), 512},  // 4: 16-warp CTAs
 };
 const ResVariant kRes[] = {
     {32, 32, k_conv_residual<32, 32, 4>, smem_res<32, 32>()},     // 0: small-n default (padded R = 32, 4 CTAs/SM)
     {52, 32, k_res_s<52, 3, true, 2>, smem_res_s<52>()},          // 1: large-n default (streamed, pair tests, 2 chains)
-    {52, 32, k_res_s<52, 3, true, 4>, smem_res_s<52>()},          // 2: 4 dot chains
-    {44, 32, k_res_s<44, 4, true, 2>, smem_res_s<44>()},          // 3: R = 44 at 4 CTAs/SM
-    {44, 32, k_res_s<44, 3, true, 2, true>, smem_res_s<44>()},    // 4: FFMA2 bodies (rejected: 25.9 ms)
 };
 struct DenseVariant {
   int R;
   void (*fn)(const float*, const float*, int64_t, int64_t, int, int64_t, float*);
   size_t smem;
 };
-template <int R>
-constexpr size_t smem_dense_s() { return (GeoU<R>::kSegPhys + kChunk) * 4; }
 const DenseVariant kDense[] = {
     {64, k_conv_dense<64>, smem_dense<64>()},   // 0: padded R = 64 (default for n > 4096)
-    {68, k_dense_s<68, 2>, smem_dense_s<68>()},  // 1: streamed window (within 1.3%, not adopted)
-    {32, k_conv_dense<32>, smem_dense<32>()},   // 2: R = 32: a 4096-index tile (default for 2048 < n <= 4096)
-    {16, k_conv_dense<16>, smem_dense<16>()},   // 3: R = 16: a 2048-index tile (default for n <= 2048)
+    {32, k_conv_dense<32>, smem_dense<32>()},   // 1: R = 32: a 4096-index tile (default for 2048 < n <= 4096)
+    {16, k_conv_dense<16>, smem_dense<16>()},   // 2: R = 16: a 2048-index tile (default for n <= 2048)
 };
 int g_dense = -1;  // -1: choose by n (a tile no longer than n: no idle threads at small n)
 static int dense_index(int64_t n) {
   if (g_dense >= 0) return g_dense;
-  return n <= 2048 ? 3 : n <= 4096 ? 2 : 0;
+  return n <= 2048 ? 2 : n <= 4096 ? 1 : 0;
 }
 
 // Defaults (measured best on B200, tools/variants.py): the streamed-window
