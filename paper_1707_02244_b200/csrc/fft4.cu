@@ -197,16 +197,19 @@ __global__ void __launch_bounds__(kThr) k_cols_fwd(const float* __restrict__ u, 
 }
 
 // Rows: row_count(N2) rows per CTA, in place on T.
+// Row r's twiddle is w_n^{mult * n2 * digit_rev(r mod rowmod, rowmod)}: the four-step twiddle
+// w_n^{n2 k1} (rowmod = N1, mult = 1), or, for the inner four-step of a three-level plan,
+// w_{N2}^{n3 k2a} = w_n^{N1 n3 k2a} (rowmod = A, mult = N1).
 template <int N2>
-__global__ void __launch_bounds__(kThr) k_rows(float2* __restrict__ T, const float2* __restrict__ H, int conj_h, int N1,
-                                               const float2* __restrict__ tw2, const float2* __restrict__ twA,
-                                               const float2* __restrict__ twB) {
+__global__ void __launch_bounds__(kThr) k_rows(float2* __restrict__ T, const float2* __restrict__ H, int conj_h,
+                                               int rowmod, int mult, const float2* __restrict__ tw2,
+                                               const float2* __restrict__ twA, const float2* __restrict__ twB) {
   extern __shared__ float2 sm[];
   constexpr int rows = row_count(N2), P = row_pitch(N2), cnt = rows * N2;
   constexpr int per = (cnt + kThr - 1) / kThr;
   __shared__ int k1s[rows];
   const int p0 = blockIdx.x * rows;
-  if (threadIdx.x < rows) k1s[threadIdx.x] = digit_rev(p0 + threadIdx.x, N1);
+  if (threadIdx.x < rows) k1s[threadIdx.x] = mult * digit_rev((p0 + threadIdx.x) % rowmod, rowmod);
   __syncthreads();
   float2 tw[per];  // w_n^{n2 k1} of this thread's elements (reused for the inverse twiddle)
 #pragma unroll
@@ -245,6 +248,37 @@ __global__ void __launch_bounds__(kThr) k_rows(float2* __restrict__ T, const flo
       const int rr = e / N2, n2 = e - rr * N2;
       T[static_cast<int64_t>(p0) * N2 + e] = cmulf_conj(sm[rr * P + pad16(n2)], tw[k]);
     }
+  }
+}
+
+// Three-level plans: the A-point transforms of the row length N2 = A * B, along the stride-B axis of each
+// row p (element n2 = n2a B + n3), C = cols_per_cta(A) consecutive n3 per CTA (128-byte segments).
+//   FWD: x w_n^{n2 k1} (the outer four-step twiddle, k1 = digit_rev(p)), DIF over n2a, in place;
+//   INV: DIT over the digit-reversed axis back to natural n2a, x conj(w_n^{n2 k1}), in place.
+template <int A, bool FWD>
+__global__ void __launch_bounds__(kThr) k_mid(float2* __restrict__ T, int N1, int N2, int B,
+                                              const float2* __restrict__ twM, const float2* __restrict__ twA,
+                                              const float2* __restrict__ twB) {
+  extern __shared__ float2 sm[];
+  constexpr int C = cols_per_cta(A), P = col_pitch(A), cnt = C * A;
+  const int per_row = B / C;
+  const int p = blockIdx.x / per_row, n30 = (blockIdx.x - p * per_row) * C;
+  const int k1 = digit_rev(p, N1);
+  float2* row = T + static_cast<int64_t>(p) * N2;
+#pragma unroll
+  for (int e = threadIdx.x; e < cnt; e += kThr) {
+    const int i = e / C, w = e - i * C, n2 = i * B + n30 + w;
+    const float2 v = row[n2];
+    sm[w * P + pad16(i)] = FWD ? cmulf(v, tw_n(twA, twB, n2 * k1)) : v;
+  }
+  __syncthreads();
+  if constexpr (FWD) dif_from<A, A, C>(sm, P, twM);
+  else dit_from<A, A, C>(sm, P, twM);
+#pragma unroll
+  for (int e = threadIdx.x; e < cnt; e += kThr) {
+    const int i = e / C, w = e - i * C, n2 = i * B + n30 + w;
+    const float2 v = sm[w * P + pad16(i)];
+    row[n2] = FWD ? v : cmulf_conj(v, tw_n(twA, twB, n2 * k1));
   }
 }
 
@@ -297,12 +331,15 @@ __global__ void __launch_bounds__(kThr) k_cols_inv(const float2* __restrict__ T,
   }
 }
 
-// H~[p N2 + q] = spec[rev1(p) + N1 rev2(q)] / s  (fp64 spectrum -> permuted fp32)
-__global__ void k_perm_spectrum(const double2* __restrict__ spec, double s, float2* __restrict__ out, int N1, int N2) {
+// H~[p N2 + q] = spec[rev1(p) + N1 rev2(q)] / s  (fp64 spectrum -> permuted fp32); three levels (A > 0):
+// q = q2a B + q3 holds k2 = rev_A(q2a) + A rev_B(q3)
+__global__ void k_perm_spectrum(const double2* __restrict__ spec, double s, float2* __restrict__ out, int N1, int N2,
+                                int A, int B) {
   const int64_t n = static_cast<int64_t>(N1) * N2;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     const int p = static_cast<int>(e / N2), q = static_cast<int>(e - static_cast<int64_t>(p) * N2);
-    const int64_t k = digit_rev(p, N1) + static_cast<int64_t>(N1) * digit_rev(q, N2);
+    const int64_t k2 = A > 0 ? digit_rev(q / B, A) + static_cast<int64_t>(A) * digit_rev(q % B, B) : digit_rev(q, N2);
+    const int64_t k = digit_rev(p, N1) + static_cast<int64_t>(N1) * k2;
     const double2 v = spec[k];
     out[e] = make_float2(static_cast<float>(v.x / s), static_cast<float>(v.y / s));
   }
@@ -455,6 +492,9 @@ size_t small_fft_smem() { return (static_cast<size_t>(pad16(N) + 4) * 2 + 2 * N)
 
 }  // namespace
 
+// the three-level plan from n = 2^22 up (arrays no longer L2-resident); CLB_FFT_TWO_LEVEL=1 forces two
+constexpr int kThreeLevelLog = 22;
+
 bool fft4_supported(int64_t n) { return n >= (int64_t(1) << 14) && n <= (int64_t(1) << 24) && (n & (n - 1)) == 0; }
 
 Fft4Plan fft4_plan(int64_t n) {
@@ -462,6 +502,13 @@ Fft4Plan fft4_plan(int64_t n) {
   int L = 0;
   while ((int64_t(1) << L) < n) ++L;
   p.n = n;
+  if (L >= kThreeLevelLog && !std::getenv("CLB_FFT_TWO_LEVEL")) {  // 256 x A x B, A, B in {128, 256}
+    p.N1 = 256;
+    p.N2 = static_cast<int>(n >> 8);
+    p.A = p.N2 >= (1 << 15) ? 256 : 128;
+    p.B = p.N2 / p.A;
+    return p;
+  }
   int l1 = L / 2;
   if (l1 > 11) l1 = 11;
   p.N1 = 1 << l1;
@@ -479,7 +526,15 @@ void fft4_twiddles(const Fft4Plan& p, std::vector<float2>* tw1, std::vector<floa
     }
   };
   table(*tw1, p.N1, 1.0 / p.N1);
-  table(*tw2, p.N2, 1.0 / p.N2);
+  if (p.three()) {  // the A-point table, then the B-point table
+    std::vector<float2> ta, tb;
+    table(ta, p.A, 1.0 / p.A);
+    table(tb, p.B, 1.0 / p.B);
+    tw2->assign(ta.begin(), ta.end());
+    tw2->insert(tw2->end(), tb.begin(), tb.end());
+  } else {
+    table(*tw2, p.N2, 1.0 / p.N2);
+  }
   const double nn = static_cast<double>(p.n);
   table(*twA, 4096, 1.0 / nn);                                              // e^{-2 pi i a / n}
   table(*twB, static_cast<int>(std::max<int64_t>(1, p.n / 4096)), 4096.0 / nn);  // e^{-2 pi i 4096 b / n}
@@ -504,6 +559,10 @@ void fft4_init_attributes() {
   cudaFuncSetAttribute(k_rows<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem_t<N>());
   CLB_FFT4_SIZES(CLB_ATTR)
 #undef CLB_ATTR
+  cudaFuncSetAttribute(k_mid<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem_t<128>());
+  cudaFuncSetAttribute(k_mid<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem_t<128>());
+  cudaFuncSetAttribute(k_mid<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem_t<256>());
+  cudaFuncSetAttribute(k_mid<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem_t<256>());
 }
 
 void launch_fft4_cols_fwd(const Fft4Plan& p, const float* u, float2* T, const float2* tw1, cudaStream_t st) {
@@ -514,15 +573,35 @@ void launch_fft4_cols_fwd(const Fft4Plan& p, const float* u, float2* T, const fl
 #undef CLB_CASE
   }
 }
+template <int A>
+static void launch_mid(const Fft4Plan& p, float2* T, bool fwd, const float2* twM, const float2* twA,
+                       const float2* twB, cudaStream_t st) {
+  const unsigned grid = static_cast<unsigned>(p.N1 * (p.B / cols_per_cta(A)));
+  if (fwd) k_mid<A, true><<<grid, kThr, cols_smem_t<A>(), st>>>(T, p.N1, p.N2, p.B, twM, twA, twB);
+  else k_mid<A, false><<<grid, kThr, cols_smem_t<A>(), st>>>(T, p.N1, p.N2, p.B, twM, twA, twB);
+}
 void launch_fft4_rows(const Fft4Plan& p, float2* T, const float2* H, bool conj_h, const float2* tw2,
                       const float2* twA, const float2* twB, cudaStream_t st) {
-  switch (p.N2) {
-#define CLB_CASE(N)                                                                                   \
-  case N:                                                                                             \
-    k_rows<N><<<p.N1 / row_count(N), kThr, rows_smem_t<N>(), st>>>(T, H, conj_h ? 1 : 0, p.N1, tw2, twA, twB); \
+  // rows of length R, `count` of them; row r's twiddle exponent mult * n2 * digit_rev(r mod rowmod)
+  const int R = p.three() ? p.B : p.N2;
+  const int count = static_cast<int>(p.n / R), rowmod = p.three() ? p.A : p.N1, mult = p.three() ? p.N1 : 1;
+  const float2* twR = p.three() ? tw2 + p.A : tw2;
+  if (p.three()) {
+    if (p.A == 256) launch_mid<256>(p, T, true, tw2, twA, twB, st);
+    else launch_mid<128>(p, T, true, tw2, twA, twB, st);
+  }
+  switch (R) {
+#define CLB_CASE(N)                                                                                            \
+  case N:                                                                                                      \
+    k_rows<N><<<count / row_count(N), kThr, rows_smem_t<N>(), st>>>(T, H, conj_h ? 1 : 0, rowmod, mult, twR,  \
+                                                                      twA, twB);                               \
     break;
     CLB_FFT4_SIZES(CLB_CASE)
 #undef CLB_CASE
+  }
+  if (p.three()) {
+    if (p.A == 256) launch_mid<256>(p, T, false, tw2, twA, twB, st);
+    else launch_mid<128>(p, T, false, tw2, twA, twB, st);
   }
 }
 void launch_fft4_cols_inv(const Fft4Plan& p, const float2* T, const Fft4Out& o, const float2* tw1,
@@ -538,7 +617,7 @@ void launch_fft4_cols_inv(const Fft4Plan& p, const float2* T, const Fft4Out& o, 
   }
 }
 void launch_fft4_perm_spectrum(const Fft4Plan& p, const double2* spec, double s, float2* out, cudaStream_t st) {
-  k_perm_spectrum<<<148 * 8, 256, 0, st>>>(spec, s, out, p.N1, p.N2);
+  k_perm_spectrum<<<148 * 8, 256, 0, st>>>(spec, s, out, p.N1, p.N2, p.A, p.B);
 }
 bool small_fft_supported(int64_t n) {
   const char* v = std::getenv("CLB_NO_SMALL");

@@ -9,17 +9,23 @@ namespace clb {
 struct Fft4Plan {
   int64_t n = 0;
   int N1 = 0, N2 = 0;  // n = N1 * N2; columns of length N1, rows of length N2
+  // n >= 2^22: three levels, N1 = 256 and the length-N2 row transforms themselves four-step, N2 = A * B
+  // (A along a stride-B axis, B contiguous), so every pass moves 128-byte row segments
+  int A = 0, B = 0;
+  bool three() const { return A > 0; }
 };
 bool fft4_supported(int64_t n);
 Fft4Plan fft4_plan(int64_t n);
-// twiddle tables (host, fp64-accurate fp32): e^{-2 pi i k / N1}, e^{-2 pi i k / N2}, and the
-// two factors of e^{-2 pi i idx / n} = twB[idx >> 12] * twA[idx & 4095]
+// twiddle tables (host, fp64-accurate fp32): e^{-2 pi i k / N1}, e^{-2 pi i k / N2} (three levels: the
+// A-point table followed by the B-point table), and the two factors of
+// e^{-2 pi i idx / n} = twB[idx >> 12] * twA[idx & 4095]
 void fft4_twiddles(const Fft4Plan& p, std::vector<float2>* tw1, std::vector<float2>* tw2, std::vector<float2>* twA,
                    std::vector<float2>* twB);
 void fft4_init_attributes();
 // u real (n) -> T: column DIF FFTs (spectral order permuted)
 void launch_fft4_cols_fwd(const Fft4Plan& p, const float* u, float2* T, const float2* tw1, cudaStream_t st);
-// in place: twiddle, row DIF FFT, times H~ (or conj), row DIT inverse FFT, inverse twiddle
+// in place: twiddle, row DIF FFT, times H~ (or conj), row DIT inverse FFT, inverse twiddle (three levels:
+// the length-N2 row transforms as A-point passes over a stride-B axis around B-point contiguous rows)
 void launch_fft4_rows(const Fft4Plan& p, float2* T, const float2* H, bool conj_h, const float2* tw2,
                       const float2* twA, const float2* twB, cudaStream_t st);
 // What the inverse column pass does with Re(y)/n (see k_cols_inv).

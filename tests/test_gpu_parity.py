@@ -496,6 +496,23 @@ def test_fft4_engine_matches_oracle(kind, lg):
         assert rel_l2(g.get(h), o.get(h)) <= (1e-3 if h == "delta" else REL_TOL), h
 
 
+@pytest.mark.parametrize("kind,lg,iters", [("ista", 22, 3), ("cadmm", 23, 2)])
+def test_fft4_three_level_matches_oracle(kind, lg, iters):
+    """The three-level plan (n >= 2^22: 256 x A x B, the length-N2 rows themselves four-step) against the
+    oracle's fp64 FFT engine."""
+    n = 1 << lg
+    p = orc.make_problem(n, n // 4, n // 256, 3)
+    setup = cl.ista_setup if kind == "ista" else cl.cadmm_setup
+    g = setup(op_of(p), p.y, cl.SolverConfig(use_fft=True))
+    g.step(iters)
+    o = (orc.Ista if kind == "ista" else orc.Cadmm)(p.row, p.omega, p.y)
+    o.step(iters, orc.ENGINE_FFT)
+    f = "x" if kind == "ista" else "z"
+    assert_parity(g.get(f), o.get(f), what=f)
+    for h in (("r",) if kind == "ista" else ("x", "v")):
+        assert rel_l2(g.get(h), o.get(h)) <= REL_TOL, h
+
+
 @pytest.mark.parametrize("kind,lg", [("ista", 20), ("ista", 23), ("cadmm", 22), ("ista", 24)])
 def test_fft4_engine_matches_stockham_engine(kind, lg):
     """Four-step engine vs the multi-pass Stockham engine (CLB_FFT_STOCKHAM=1) up to n = 2^24."""

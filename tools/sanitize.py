@@ -35,3 +35,20 @@ for n in (1 << 16, 1 << 18):
             assert L.cl_solver_run_phase(sh.handle, ph) == 0
         sh.synchronize()
         print(f"tc n={n} {setup.__name__}: 2 steps + one shard-1-of-2 step", flush=True)
+
+# the dense ADMM baseline (Gram matrix, blocked Gauss-Jordan, fused mat-vec; n not a multiple of 64) and the
+# library-owned sharded data plane (peer-copy transport, 2 ranks on one device)
+p = cl.make_problem(200, 100, 10, 4)
+rep = cl.admm_dense_run(p.measurements, p.op, cl.SolverConfig(max_iter=4, check_every=2), truth=p.signal.values)
+print(f"dense admm n=200: {rep.iterations} iterations, metric {rep.final_metric:.3e}", flush=True)
+p = cl.make_problem(1 << 16, 1 << 14, 256, 5)
+for kind in ("ista", "cadmm"):
+    g = cl.ShardedSolve(kind, p.op, p.measurements, cl.SolverConfig(max_iter=2, check_every=2), devices=[0, 0],
+                        transport="copy")
+    print(f"sharded {kind} 2 ranks: {g.run(truth=p.signal.values).iterations} iterations", flush=True)
+
+if "--large" in sys.argv:  # the three-level FFT plan (n >= 2^22): memcheck only (slow under racecheck)
+    p = cl.make_problem(1 << 22, 1 << 20, 1 << 14, 6)
+    for run in (cl.ista_run, cl.cadmm_run):
+        rep = run(p.measurements, p.op, cl.SolverConfig(max_iter=2, check_every=2, use_fft=True))
+        print(f"three-level fft n=2^22 {run.__name__}: {rep.iterations} iterations", flush=True)
