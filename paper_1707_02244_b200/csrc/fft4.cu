@@ -177,7 +177,7 @@ __device__ __forceinline__ float2 tw_n(const float2* __restrict__ twA, const flo
 
 // Columns forward: input real u[j] (j = n1 N2 + n2).
 template <int N1>
-__global__ void __launch_bounds__(kThr) k_cols_fwd(const float* __restrict__ u, float2* __restrict__ T, int N2,
+__global__ void __launch_bounds__(kThr, N1 <= 256 ? 4 : 1) k_cols_fwd(const float* __restrict__ u, float2* __restrict__ T, int N2,
                                                    const float2* __restrict__ tw1) {
   extern __shared__ float2 sm[];
   constexpr int B = cols_per_cta(N1), P = col_pitch(N1), cnt = B * N1;
@@ -201,32 +201,39 @@ __global__ void __launch_bounds__(kThr) k_cols_fwd(const float* __restrict__ u, 
 // w_n^{n2 k1} (rowmod = N1, mult = 1), or, for the inner four-step of a three-level plan,
 // w_{N2}^{n3 k2a} = w_n^{N1 n3 k2a} (rowmod = A, mult = N1).
 template <int N2>
-__global__ void __launch_bounds__(kThr) k_rows(float2* __restrict__ T, const float2* __restrict__ H, int conj_h,
-                                               int rowmod, int mult, const float2* __restrict__ tw2,
-                                               const float2* __restrict__ twA, const float2* __restrict__ twB) {
+__global__ void __launch_bounds__(kThr, N2 <= 256 ? 4 : 1)
+k_rows(float2* __restrict__ T, const float2* __restrict__ H, int conj_h, int rowmod, int mult,
+       const float2* __restrict__ tw2, const float2* __restrict__ twA, const float2* __restrict__ twB) {
   extern __shared__ float2 sm[];
   constexpr int rows = row_count(N2), P = row_pitch(N2), cnt = rows * N2;
   constexpr int per = (cnt + kThr - 1) / kThr;
+  // Short rows (the three-level plan's contiguous B-point rows): a register-lean form -- the twiddle is
+  // recomputed for the store and the spectrum fetched after the forward stages -- so four CTAs fit per SM
+  // and their load / compute / store phases overlap.  Longer rows keep both in registers across the stages.
+  constexpr bool kLean = N2 <= 256;
   __shared__ int k1s[rows];
   const int p0 = blockIdx.x * rows;
   if (threadIdx.x < rows) k1s[threadIdx.x] = mult * digit_rev((p0 + threadIdx.x) % rowmod, rowmod);
   __syncthreads();
-  float2 tw[per];  // w_n^{n2 k1} of this thread's elements (reused for the inverse twiddle)
+  float2 tw[kLean ? 1 : per];  // w_n^{n2 k1} of this thread's elements (reused for the inverse twiddle)
 #pragma unroll
   for (int k = 0; k < per; ++k) {
     const int e = threadIdx.x + k * kThr;
     if (e < cnt) {
       const int rr = e / N2, n2 = e - rr * N2;
-      tw[k] = tw_n(twA, twB, n2 * k1s[rr]);
-      sm[rr * P + pad16(n2)] = cmulf(T[static_cast<int64_t>(p0) * N2 + e], tw[k]);
+      const float2 w = tw_n(twA, twB, n2 * k1s[rr]);
+      if constexpr (!kLean) tw[k] = w;
+      sm[rr * P + pad16(n2)] = cmulf(T[static_cast<int64_t>(p0) * N2 + e], w);
     }
   }
-  // the spectrum is fetched before the forward stages (its latency hides behind them)
-  float2 hv[per];
+  // long rows: the spectrum is fetched before the forward stages (its latency hides behind them)
+  float2 hv[kLean ? 1 : per];
+  if constexpr (!kLean) {
 #pragma unroll
-  for (int k = 0; k < per; ++k) {
-    const int e = threadIdx.x + k * kThr;
-    if (e < cnt) hv[k] = __ldg(H + static_cast<int64_t>(p0) * N2 + e);
+    for (int k = 0; k < per; ++k) {
+      const int e = threadIdx.x + k * kThr;
+      if (e < cnt) hv[k] = __ldg(H + static_cast<int64_t>(p0) * N2 + e);
+    }
   }
   __syncthreads();
   dif_from<N2, N2, rows>(sm, P, tw2);
@@ -235,8 +242,9 @@ __global__ void __launch_bounds__(kThr) k_rows(float2* __restrict__ T, const flo
     const int e = threadIdx.x + k * kThr;
     if (e < cnt) {
       const int rr = e / N2, q = e - rr * N2;
+      const float2 h = kLean ? __ldg(H + static_cast<int64_t>(p0) * N2 + e) : hv[kLean ? 0 : k];
       float2& a = sm[rr * P + pad16(q)];
-      a = conj_h ? cmulf_conj(a, hv[k]) : cmulf(a, hv[k]);
+      a = conj_h ? cmulf_conj(a, h) : cmulf(a, h);
     }
   }
   __syncthreads();
@@ -246,7 +254,8 @@ __global__ void __launch_bounds__(kThr) k_rows(float2* __restrict__ T, const flo
     const int e = threadIdx.x + k * kThr;
     if (e < cnt) {
       const int rr = e / N2, n2 = e - rr * N2;
-      T[static_cast<int64_t>(p0) * N2 + e] = cmulf_conj(sm[rr * P + pad16(n2)], tw[k]);
+      const float2 w = kLean ? tw_n(twA, twB, n2 * k1s[rr]) : tw[kLean ? 0 : k];
+      T[static_cast<int64_t>(p0) * N2 + e] = cmulf_conj(sm[rr * P + pad16(n2)], w);
     }
   }
 }
@@ -256,7 +265,7 @@ __global__ void __launch_bounds__(kThr) k_rows(float2* __restrict__ T, const flo
 //   FWD: x w_n^{n2 k1} (the outer four-step twiddle, k1 = digit_rev(p)), DIF over n2a, in place;
 //   INV: DIT over the digit-reversed axis back to natural n2a, x conj(w_n^{n2 k1}), in place.
 template <int A, bool FWD>
-__global__ void __launch_bounds__(kThr) k_mid(float2* __restrict__ T, int N1, int N2, int B,
+__global__ void __launch_bounds__(kThr, 4) k_mid(float2* __restrict__ T, int N1, int N2, int B,
                                               const float2* __restrict__ twM, const float2* __restrict__ twA,
                                               const float2* __restrict__ twB) {
   extern __shared__ float2 sm[];
@@ -289,7 +298,7 @@ __global__ void __launch_bounds__(kThr) k_mid(float2* __restrict__ T, int N1, in
 //   Fft4Out::kIstaStep delta[j] = Re / n, x[j] = eta(x[j] + tau delta[j])  (unchecked iterations)
 //   Fft4Out::kBeta     beta[j] = rho Re / n + sigma (z[j] - nu[j])
 template <int N1>
-__global__ void __launch_bounds__(kThr) k_cols_inv(const float2* __restrict__ T, Fft4Out o, int N2,
+__global__ void __launch_bounds__(kThr, N1 <= 256 ? 4 : 1) k_cols_inv(const float2* __restrict__ T, Fft4Out o, int N2,
                                                    const float2* __restrict__ tw1, float inv_n) {
   extern __shared__ float2 sm[];
   constexpr int B = cols_per_cta(N1), P = col_pitch(N1), cnt = B * N1;
