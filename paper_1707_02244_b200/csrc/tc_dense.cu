@@ -40,6 +40,7 @@ constexpr int kDB = 128;       // offsets per slab block
 constexpr int kRA = kDB + kMT; // slab rows (max)
 constexpr int kSlabBytes = kRA * 16 * (kKG / 4);
 constexpr int kRB = 288;       // Hankel rows: p + k_local - (k_local mod 4) <= 255 + 28, rounded up
+constexpr int kRB2 = 160;      // a CTA pair's half tile (p < 128): <= 127 + 28, rounded up
 constexpr int kTileBytes = kRB * 16;
 #ifndef TC_BST
 #define TC_BST 8
@@ -52,6 +53,7 @@ constexpr int kTcThreads = kDrainers + kProducers + 32;
 constexpr int kOffB = kAStages * 2 * kSlabBytes;
 constexpr int kOffBar = kOffB + kBStages * 2 * kTileBytes;
 constexpr int kStg = kRB + 8;  // fp16 staging row (packed hi | lo) per tile, double-buffered
+// The smem layout is the same for both CTA-group sizes (a pair uses the first kRB2 rows of each B stage).
 constexpr int kOffStg = kOffBar + (8 + 2 * kBStages) * 8 + 16;
 constexpr int kTcSmem = kOffStg + 2 * kStg * 4;
 #ifndef TC_SPD
@@ -59,6 +61,9 @@ constexpr int kTcSmem = kOffStg + 2 * kStg * 4;
 #endif
 constexpr int kSPD = TC_SPD;  // TF32: steps accumulated in TMEM between drains (divides 8)
 constexpr int kTmemCols = 512;  // two 128 x 256 fp32 accumulators
+#ifndef TC_MMA_ONLY
+#define TC_MMA_ONLY 0  // diagnostic builds (tools/microbench): no tile production after the first fill, no drain
+#endif
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -115,6 +120,52 @@ __device__ __forceinline__ void mma_f16(uint32_t tmem, uint64_t a, uint64_t b, u
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
+}
+// ---- CTA pairs (cta_group::2): the leader (rank 0) issues M = 256 MMAs whose A rows 128..255 and
+// B columns 128..255 come from the peer's shared memory at the same offsets; each CTA's TMEM holds
+// its own 128 rows.  Producer / drain hand-overs arrive on the leader's barriers across the cluster.
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive (release, cluster scope) on the barrier at the same offset in CTA `rank` of the cluster
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* b, uint32_t rank) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(b)),
+      "r"(rank)
+      : "memory");
+}
+// commit the leader's MMAs to the barrier at this offset in both CTAs of the pair
+__device__ __forceinline__ void tc_commit_pair(uint64_t* b) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\t"
+      "mov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+          smem_u32(b))
+      : "memory");
+}
+__device__ __forceinline__ void mma_pair(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc,
+                                         bool f16) {
+  if (f16)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
 }
 // 8 scaled values -> 16-byte rows of fp16 hi = rn(x) and lo = rn(x - hi) (x - hi is exact in fp32)
 __device__ __forceinline__ void st_split8(unsigned char* hi, unsigned char* lo, const float (&v)[8], float sc) {
@@ -215,10 +266,17 @@ struct StepIter {
 // production never waits behind a drain.  F16: fp16 operands with a 2-term split of
 // power-of-two-scaled values (hi.hi + hi.lo + lo.hi, kind::f16: twice the MMA rate and half the
 // operand bytes of TF32); `maxes` holds k_absmax2's per-block maxima of |h| and |u|.
-template <bool F16>
+// CG = 2: CTA pairs (cluster of 2, cta_group::2).  A pair covers two consecutive tiles (rank r: tile
+// 2 P + r) of one split; each CTA stages its own A slab rows and the half of the Hankel tile holding its
+// 128 columns p (rows t0 + 128 r + ...), so per SM the MMA reads 4 KB of A and 4 KB of B per 128 x 256 x 16
+// instead of 4 + 8 KB, and the producers build half the Hankel rows.
+template <bool F16, int CG>
 __global__ void __launch_bounds__(kTcThreads, 1)
 k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, int splits, int64_t tile_lo,
            float* __restrict__ partial, const float* __restrict__ maxes) {
+  constexpr bool kPair = CG == 2;
+  constexpr int kRows_B = kPair ? kRB2 : kRB;  // Hankel rows this CTA builds
+  constexpr int kStgN = kRows_B + 8;           // fp16 staging entries per tile
   constexpr int kEl = F16 ? 8 : 4;       // elements per 16-byte chunk
   constexpr int kCh = kKG / kEl;         // chunks per K group
   constexpr int kKS = F16 ? 16 : 8;      // K per MMA
@@ -238,32 +296,44 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   const int64_t nb = n / kB, nbm = nb - 1, nm = n - 1;
-  const int64_t tile = tile_lo + blockIdx.x / splits;
-  const int s = static_cast<int>(blockIdx.x % splits);
+  const uint32_t rank = kPair ? cluster_rank() : 0u;
+  const int64_t unit = kPair ? blockIdx.x >> 1 : blockIdx.x;
+  const int64_t tile = tile_lo + (kPair ? 2 * (unit / splits) + rank : unit / splits);
+  const int s = static_cast<int>(unit % splits);
   const int64_t I0 = tile * kMT;
   const int64_t Dlo = s * nb / splits, Dn = (s + 1) * nb / splits - Dlo;
   const int64_t steps = kNG * Dn;
 
   if (tid == 0) {
+    // pairs: one arrival per producer / drain warp of either CTA on the leader's barriers
+    constexpr int kFullCount = kPair ? 2 * (kProducers / 32) : kProducers;
+    constexpr int kEmptyTCount = kPair ? 2 * (kDrainers / 32) : kDrainers;
     for (int i = 0; i < kAStages; ++i) {
-      mbar_init(&a_full[i], kProducers);
+      mbar_init(&a_full[i], kFullCount);
       mbar_init(&a_empty[i], 1);
     }
     for (int i = 0; i < kBStages; ++i) {
-      mbar_init(&b_full[i], kProducers);
+      mbar_init(&b_full[i], kFullCount);
       mbar_init(&b_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&t_full[i], 1);
-      mbar_init(&t_empty[i], kDrainers);
+      mbar_init(&t_empty[i], kEmptyTCount);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMmaWarp) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(kTmemCols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (kPair) {  // issued by the same warp of both CTAs
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "n"(kTmemCols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "n"(kTmemCols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   if (F16 && warp == 1) {
     float a = 0.f, b = 0.f;
@@ -282,7 +352,8 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
     }
   }
   tc_before_sync();
-  __syncthreads();
+  if constexpr (kPair) cluster_sync_all();  // the leader's barriers are initialised before any remote arrival
+  else __syncthreads();
   tc_after_sync();
   const uint32_t tmem = *tmem_slot;
   const float sh = F16 ? scl[0] : 1.f, su = F16 ? scl[1] : 1.f;
@@ -299,13 +370,19 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
       tc_after_sync();
 #pragma unroll
       for (int c0 = 0; c0 < kB / 2; c0 += 32) {
+        if (TC_MMA_ONLY) break;
         uint32_t v[32];
         tmem_ld32(lane_base + buf * kB + c0, v);
 #pragma unroll
         for (int e = 0; e < 32; ++e) acc[c0 + e] += __uint_as_float(v[e]);
       }
       tc_before_sync();
-      mbar_arrive(&t_empty[buf]);
+      if constexpr (kPair) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(&t_empty[buf], 0);
+      } else {
+        mbar_arrive(&t_empty[buf]);
+      }
     }
     // ---- partial[s][256 I + p]: this thread's row I, columns [128 (warp / 4), +128) ----
     float* out = partial + static_cast<int64_t>(s) * n + (I0 + (warp & 3) * 32 + lane) * kB + (warp >> 2) * (kB / 2);
@@ -320,7 +397,17 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
     const int ptid = tid - kDrainers;
     int a_use = 0;
     // fp16: the next tile's h values are loaded one tile ahead (their latency overlaps this tile)
-    constexpr int kSt = (kStg + kProducers - 1) / kProducers;
+    constexpr int kSt = (kStgN + kProducers - 1) / kProducers;
+    // full-barrier hand-over: every producer thread (single CTA), or one arrival per warp on the leader
+    auto arrive_full = [&](uint64_t* b) {
+      if constexpr (kPair) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(b, 0);
+      } else {
+        mbar_arrive(b);
+      }
+    };
+    const int64_t hoff = kPair ? 128 * static_cast<int64_t>(rank) : 0;  // this CTA's Hankel columns p
     StepIter it, nx;
     it.init(Dlo, Dn);
     nx = it;
@@ -328,7 +415,7 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
     float xn[F16 ? kSt : 1];
     if constexpr (F16) {
 #pragma unroll
-      for (int q = 0; q < kSt; ++q) xn[q] = __ldg(h + ((it.t0() + ptid + q * kProducers) & nm));
+      for (int q = 0; q < kSt; ++q) xn[q] = __ldg(h + ((it.t0() + hoff + ptid + q * kProducers) & nm));
     }
     for (int64_t j = 0; j < steps; ++j, it = nx, nx.next()) {
       const int g = it.g;
@@ -341,7 +428,7 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
         const int64_t ibase = I0 - it.d0() - it.len + 1;  // I - D of slab row 0
         // kBatch items per thread per pass, all loads first (one L2 latency per pass)
         constexpr int kBatch = 4;
-        for (int base = ptid; base < rows * kCh; base += kBatch * kProducers) {
+        for (int base = ptid; base < (TC_MMA_ONLY && a_use >= 2 ? 0 : rows * kCh); base += kBatch * kProducers) {
           float4 v0[kBatch], v1[kBatch];
 #pragma unroll
           for (int b = 0; b < kBatch; ++b) {
@@ -371,31 +458,36 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
           }
         }
         fence_async_smem();
-        mbar_arrive(&a_full[st]);
+        arrive_full(&a_full[st]);
         ++a_use;
       }
       const int bs = static_cast<int>(j & (kBStages - 1));
       mbar_wait(&b_empty[bs], ((j / kBStages) & 1) ^ 1);
       unsigned char* thi = sm + kOffB + (bs * 2) * kTileBytes;
       unsigned char* tlo = sm + kOffB + (bs * 2 + 1) * kTileBytes;
-      const int64_t t0 = it.t0();
-      constexpr int kRows = (kRB + kProducers - 1) / kProducers;
+      const int64_t t0 = it.t0() + hoff;
+      if (TC_MMA_ONLY && j >= kBStages) {  // diagnostic: stages keep their first contents
+        fence_async_smem();
+        arrive_full(&b_full[bs]);
+        continue;
+      }
+      constexpr int kRows = (kRows_B + kProducers - 1) / kProducers;
       if constexpr (F16) {
         // Split each of the tile's kRB + 8 values once into a packed (hi | lo << 16) fp16 word in a
         // double-buffered staging row, then build the 8-wide Hankel rows from it with byte permutes.
-        uint32_t* stg = reinterpret_cast<uint32_t*>(sm + kOffStg) + (j & 1) * kStg;
+        uint32_t* stg = reinterpret_cast<uint32_t*>(sm + kOffStg) + (j & 1) * kStgN;
         float x[kSt];
 #pragma unroll
         for (int q = 0; q < kSt; ++q) x[q] = xn[q];
         if (j + 1 < steps) {
-          const int64_t t1 = nx.t0();
+          const int64_t t1 = nx.t0() + hoff;
 #pragma unroll
           for (int q = 0; q < kSt; ++q) xn[q] = __ldg(h + ((t1 + ptid + q * kProducers) & nm));
         }
 #pragma unroll
         for (int q = 0; q < kSt; ++q) {
           const int i = ptid + q * kProducers;
-          if (i < kStg) {
+          if (i < kStgN) {
             const float a = x[q] * sh;
             const __half ha = __float2half_rn(a);
             stg[i] = static_cast<uint32_t>(__half_as_ushort(ha)) |
@@ -406,7 +498,7 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
 #pragma unroll
         for (int q = 0; q < kRows; ++q) {
           const int r = ptid + q * kProducers;
-          if (r < kRB) {
+          if (r < kRows_B) {
             uint32_t w[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) w[e] = stg[r + e];
@@ -419,7 +511,7 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
           }
         }
         fence_async_smem();
-        mbar_arrive(&b_full[bs]);
+        arrive_full(&b_full[bs]);
         continue;
       }
       float v[kRows][kEl];
@@ -432,7 +524,7 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
 #pragma unroll
       for (int q = 0; q < kRows; ++q) {
         const int r = ptid + q * kProducers;
-        if (r < kRB) {
+        if (r < kRows_B) {
           if constexpr (F16) {
             st_split8(thi + r * 16, tlo + r * 16, v[q], sh);
           } else {
@@ -442,13 +534,17 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
         }
       }
       fence_async_smem();
-      mbar_arrive(&b_full[bs]);
+      arrive_full(&b_full[bs]);
     }
-  } else if (lane == 0) {
+  } else if (lane == 0 && rank == 0) {
     // ---- MMA issue (one thread) ----
     constexpr uint32_t kFmt = F16 ? 0u : 2u;  // operand format: F16 (kind::f16) / TF32 (kind::tf32)
     constexpr uint32_t idesc = (1u << 4) | (kFmt << 7) | (kFmt << 10) | (static_cast<uint32_t>(kB >> 3) << 17) |
-                               (static_cast<uint32_t>(kMT >> 4) << 24);
+                               (static_cast<uint32_t>((CG * kMT) >> 4) << 24);
+    auto commit = [&](uint64_t* b) {
+      if constexpr (kPair) tc_commit_pair(b);
+      else tc_commit(b);
+    };
     const uint32_t abase = smem_u32(sm), bbase = smem_u32(sm + kOffB);
     int a_use = 0;
     uint32_t ahi = 0, alo = 0, lboA = 0;
@@ -479,7 +575,11 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
         const uint64_t dal = sdesc(alo + row0 + 2u * kk * lboA, lboA, 128);
         const uint64_t dbh = sdesc(bhi + 2u * kLboB * kk, kLboB, 128);
         const uint64_t dbl = sdesc(blo + 2u * kLboB * kk, kLboB, 128);
-        if constexpr (F16) {
+        if constexpr (kPair) {
+          mma_pair(tacc, dah, dbh, idesc, (first && kk == 0) ? 0u : 1u, F16);
+          mma_pair(tacc, dah, dbl, idesc, 1, F16);
+          mma_pair(tacc, dal, dbh, idesc, 1, F16);
+        } else if constexpr (F16) {
           mma_f16(tacc, dah, dbh, idesc, (first && kk == 0) ? 0u : 1u);
           mma_f16(tacc, dah, dbl, idesc, 1);
           mma_f16(tacc, dal, dbh, idesc, 1);
@@ -489,19 +589,23 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
           mma_tf32(tacc, dal, dbh, idesc, 1);
         }
       }
-      tc_commit(&b_empty[bs]);
-      if (j % kSpd == kSpd - 1) tc_commit(&t_full[buf]);
+      commit(&b_empty[bs]);
+      if (j % kSpd == kSpd - 1) commit(&t_full[buf]);
       if (dd == it.len - 1) {
-        tc_commit(&a_empty[st]);
+        commit(&a_empty[st]);
         ++a_use;
       }
     }
   }
   tc_before_sync();
-  __syncthreads();
+  if constexpr (kPair) cluster_sync_all();  // both CTAs done: no MMA or arrival still targets either
+  else __syncthreads();
   if (warp == kMmaWarp) {
     tc_after_sync();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
+    if constexpr (kPair)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
   }
 }
 
@@ -551,11 +655,41 @@ size_t tc_scratch_floats() { return 2 * kMaxBlocks; }
 void tc_dense_init() {
   static std::atomic<uint64_t> devs{0};
   if (!first_use_on_device(devs)) return;
-  cudaFuncSetAttribute(reinterpret_cast<const void*>(k_tc_dense<false>), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       kTcSmem);
-  cudaFuncSetAttribute(reinterpret_cast<const void*>(k_tc_dense<true>), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       kTcSmem);
+  for (const void* f : {reinterpret_cast<const void*>(k_tc_dense<false, 1>),
+                        reinterpret_cast<const void*>(k_tc_dense<true, 1>),
+                        reinterpret_cast<const void*>(k_tc_dense<false, 2>),
+                        reinterpret_cast<const void*>(k_tc_dense<true, 2>)})
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
 }
+
+namespace {
+// CTA pairs (cta_group::2) for every tile range made of whole pairs; CLB_TC_PAIR=0 forces single CTAs.
+bool use_pairs(const ConvPlan& p) {
+  static const int env = [] {
+    const char* v = getenv("CLB_TC_PAIR");
+    return (v && *v) ? atoi(v) : -1;
+  }();
+  if (env == 0) return false;
+  return (p.tile_lo % 2) == 0 && (p.tile_hi % 2) == 0;
+}
+template <bool F16>
+cudaError_t launch_pairs(const ConvPlan& p, const float* h, const float* u, float* partial, const float* maxes,
+                         cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>((p.tile_hi - p.tile_lo) * p.splits));
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.dynamicSmemBytes = kTcSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_tc_dense<F16, 2>, h, u, p.n, p.splits, p.tile_lo, partial, maxes);
+}
+}  // namespace
 
 // The fp16 path's k_absmax2 -> k_tc_dense hand-over goes through the caller's own scratch
 // (p.tc_scratch): two products on different streams never share it.
@@ -566,11 +700,13 @@ cudaError_t launch_tc_dense(const ConvPlan& p, const float* h, const float* u, f
   if (use_f16(p.n)) {
     if (!p.tc_scratch) return cudaErrorInvalidValue;  // the plan's owner did not allocate tc_scratch_floats()
     k_absmax2<<<kMaxBlocks, 256, 0, st>>>(h, u, p.n, p.tc_scratch);
-    k_tc_dense<true><<<static_cast<unsigned>(units), kTcThreads, kTcSmem, st>>>(h, u, p.n, p.splits, p.tile_lo,
-                                                                                partial, p.tc_scratch);
+    if (use_pairs(p)) return launch_pairs<true>(p, h, u, partial, p.tc_scratch, st);
+    k_tc_dense<true, 1><<<static_cast<unsigned>(units), kTcThreads, kTcSmem, st>>>(h, u, p.n, p.splits, p.tile_lo,
+                                                                                   partial, p.tc_scratch);
   } else {
-    k_tc_dense<false><<<static_cast<unsigned>(units), kTcThreads, kTcSmem, st>>>(h, u, p.n, p.splits, p.tile_lo,
-                                                                                 partial, nullptr);
+    if (use_pairs(p)) return launch_pairs<false>(p, h, u, partial, nullptr, st);
+    k_tc_dense<false, 1><<<static_cast<unsigned>(units), kTcThreads, kTcSmem, st>>>(h, u, p.n, p.splits, p.tile_lo,
+                                                                                    partial, nullptr);
   }
   return cudaGetLastError();
 }

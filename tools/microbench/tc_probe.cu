@@ -3,7 +3,8 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../../paper_1707_02244_b200/csrc \
 //        -o tc_probe tc_probe.cu ../../paper_1707_02244_b200/csrc/tc_dense.cu
 //   ./tc_probe [log2 n] [reps]
-// Environment: CLB_TC_F16=0/1 (operand format; default fp16 for n >= 2^18), CLB_TC_SPLITS=S.
+// Environment: CLB_TC_F16=0/1 (operand format; default fp16 for n >= 2^18), CLB_TC_SPLITS=S,
+// CLB_TC_PAIR=0 (single CTAs instead of cta_group::2 pairs).
 // Build flags used in the DESIGN experiments: -DTC_SPD=k (TF32 steps per drain; fp16 uses 2k).
 // The tensor-flop column counts 3 tensor flops per algorithmic flop for either format.
 #include <cmath>
@@ -42,8 +43,8 @@ int main(int argc, char** argv) {
   CK(cudaMemcpy(dh, h.data(), n * 4, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(du, u.data(), n * 4, cudaMemcpyHostToDevice));
   CK(cudaMemset(dp, 0, n * 4 * p.splits));
-  clb::launch_tc_dense(p, dh, du, dp, 0);
-  CK(cudaGetLastError());
+  CK(cudaMalloc(&p.tc_scratch, clb::tc_scratch_floats() * 4));
+  CK(clb::launch_tc_dense(p, dh, du, dp, 0));
   CK(cudaDeviceSynchronize());
   std::vector<float> part(n * p.splits);
   CK(cudaMemcpy(part.data(), dp, n * 4 * p.splits, cudaMemcpyDeviceToHost));
@@ -70,7 +71,7 @@ int main(int argc, char** argv) {
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   CK(cudaEventRecord(e0));
-  for (int r = 0; r < reps; ++r) clb::launch_tc_dense(p, dh, du, dp, 0);
+  for (int r = 0; r < reps; ++r) CK(clb::launch_tc_dense(p, dh, du, dp, 0));
   CK(cudaEventRecord(e1));
   CK(cudaEventSynchronize(e1));
   float ms = 0;
