@@ -55,26 +55,59 @@ def algorithmic_flops(w):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region: NVML every 5 ms (the timed region of
+    the default line is ~0.2 s), else nvidia-smi every 0.2 s."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event reason bits (nvml.h): HW slowdown, HW thermal, SW thermal, SW power cap
+    BITS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+            ("sw_power_cap", 0x4))
 
     def __init__(self, index: int):
         self.index = index
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, power_w, set of reason names)
+        self.source = None
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
 
+    def _run_nvml(self):
+        import pynvml as nv
+        nv.nvmlInit()
+        try:
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            self.source = "nvml, 5 ms"
+            while not self._stop.is_set():
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                try:
+                    pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+                except Exception:
+                    pw = None
+                self.samples.append((float(sm), float(mx), pw, {k for k, b in self.BITS if bits & b}))
+                self._stop.wait(0.005)
+        finally:
+            nv.nvmlShutdown()
+
     def _run(self):
+        try:
+            self._run_nvml()
+            return
+        except Exception:
+            self.samples = []
+        self.source = "nvidia-smi, 0.2 s"
+        names = [k for k, _ in self.BITS]
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
                 f = [x.strip() for x in out.stdout.strip().split(",")]
-                if len(f) >= 8:
-                    self.samples.append(f)
+                if len(f) >= 8 and f[0].replace(".", "").isdigit():
+                    pw = float(f[2]) if f[2].replace(".", "").isdigit() else None
+                    self.samples.append((float(f[0]), float(f[1]), pw,
+                                         {names[i] for i in range(4) if f[4 + i] == "Active"}))
             except Exception:
                 pass
             self._stop.wait(0.2)
@@ -90,12 +123,13 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[4 + i].strip() == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        pw = [s[2] for s in self.samples if s[2] is not None]
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_mhz_min": min(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": sorted(set().union(*(s[3] for s in self.samples))),
+                "power_w_median": statistics.median(pw) if pw else None,
+                "samples": len(self.samples), "source": self.source}
 
 
 SAMPLE_FMA = 1 << 33  # per phase per CPU step: ~1-2 s on a 16-core host

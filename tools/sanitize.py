@@ -18,7 +18,8 @@ for n, m, k in ((1000, 300, 10), (4096, 1024, 64), (1 << 14, 1 << 12, 64), (1 <<
                   flush=True)
 
 # the tcgen05 dense-product kernel (k_tc_dense) in both operand formats: fp16 2-term split (n >= 2^18)
-# and 3xTF32 (smaller n), unsharded and as shard 1 of 2 (tile_lo > 0) through the phase API
+# and 3xTF32 (smaller n), on CTA pairs (cta_group::2) and single CTAs, unsharded and sharded (tile_lo > 0)
+# through the phase API
 import ctypes as C  # noqa: E402
 
 from paper_1707_02244_b200._native import lib as L  # noqa: E402
@@ -29,12 +30,14 @@ for n in (1 << 16, 1 << 18):
         st = setup(p.op, p.measurements)
         st.step(2)
         st.synchronize()
-        sh = setup(p.op, p.measurements)
-        assert L.cl_solver_shard(sh.handle, 1, 2) == 0
-        for ph in range(2 if setup is cl.ista_setup else 3):
-            assert L.cl_solver_run_phase(sh.handle, ph) == 0
-        sh.synchronize()
-        print(f"tc n={n} {setup.__name__}: 2 steps + one shard-1-of-2 step", flush=True)
+        # shard 1 of 2 (tile_lo > 0, whole CTA pairs) and shard 1 of 3 (odd tile range: single CTAs)
+        for world in (2, 3):
+            sh = setup(p.op, p.measurements)
+            assert L.cl_solver_shard(sh.handle, 1, world) == 0
+            for ph in range(2 if setup is cl.ista_setup else 3):
+                assert L.cl_solver_run_phase(sh.handle, ph) == 0
+            sh.synchronize()
+        print(f"tc n={n} {setup.__name__}: 2 steps + one shard-1-of-2 and one shard-1-of-3 step", flush=True)
 
 # the dense ADMM baseline (Gram matrix, blocked Gauss-Jordan, fused mat-vec; n not a multiple of 64) and the
 # library-owned sharded data plane (peer-copy transport, 2 ranks on one device)
