@@ -17,6 +17,17 @@
 // DIF forward + DIT inverse = no bit reversal anywhere.  Every stage is an
 // in-place radix-16 (then 8/4/2) butterfly on shared memory with a twiddle
 // table; global loads and stores are coalesced row segments.
+//
+// Real plans (the default): the product's input and output are real, so the
+// engine transforms the length-N = n/2 complex sequence z[j] = u[2j] + i u[2j+1]
+// (half the bytes of every pass).  The rows kernel holds each row together with
+// its mirror row (the row of the spectral indices N - k) and, between the
+// forward and the inverse row FFTs, turns Z into the real spectrum U, multiplies
+// by H and packs Y back into the spectrum of y[2j] + i y[2j+1]:
+//   U[k] = E + W^k O, U[k+N] = E - W^k O,  E = (Z[k] + Z*[N-k]) / 2,  O = (Z[k] - Z*[N-k]) / 2i
+//   Z'[k] = (Y[k] + Y[k+N]) / 2 + i W^-k (Y[k] - Y[k+N]) / 2,   W = e^{-2 pi i / n},
+// with H[k+N] = conj(H[N-k]) (h real): the engine stores H[k] for k < N only,
+// and H[0], H[N] (both real) packed into entry 0.
 #include <cstdint>
 #include <cstdlib>
 #include <cstdio>
@@ -160,6 +171,20 @@ __host__ __device__ __forceinline__ int digit_rev(int p, int N) {
   return k;
 }
 
+// inverse of digit_rev: the DIF output position holding frequency k
+__host__ __device__ __forceinline__ int digit_pos(int k, int N) {
+  int lg = 0;
+  while ((1 << lg) < N) ++lg;
+  int p = 0;
+  for (int L = N; L > 1;) {
+    const int R = (L == N && (lg % 4) != 0) ? (1 << (lg % 4)) : 16;
+    L /= R;
+    p += (k % R) * L;
+    k /= R;
+  }
+  return p;
+}
+
 // ---- kernels -----------------------------------------------------------------
 // Columns per CTA and the column pitch: pitch = (16 / B) mod 16 (complex) keeps
 // the coalesced row-segment loads (B columns x 4 rows per half-warp) conflict-free.
@@ -176,7 +201,9 @@ __device__ __forceinline__ float2 tw_n(const float2* __restrict__ twA, const flo
 }
 
 // Columns forward: input real u[j] (j = n1 N2 + n2).
-template <int N1>
+// REAL: the input is read as N complex values z[j] = (u[2j], u[2j+1]) (the real plans); else as the real
+// parts of n complex values.
+template <int N1, bool REAL>
 __global__ void __launch_bounds__(kThr, N1 <= 256 ? 4 : 1) k_cols_fwd(const float* __restrict__ u, float2* __restrict__ T, int N2,
                                                    const float2* __restrict__ tw1) {
   extern __shared__ float2 sm[];
@@ -185,7 +212,8 @@ __global__ void __launch_bounds__(kThr, N1 <= 256 ? 4 : 1) k_cols_fwd(const floa
 #pragma unroll
   for (int e = threadIdx.x; e < cnt; e += kThr) {
     const int i = e / B, w = e - i * B;
-    sm[w * P + pad16(i)] = make_float2(__ldg(u + static_cast<int64_t>(i) * N2 + c0 + w), 0.f);
+    const int64_t j = static_cast<int64_t>(i) * N2 + c0 + w;
+    sm[w * P + pad16(i)] = REAL ? __ldg(reinterpret_cast<const float2*>(u) + j) : make_float2(__ldg(u + j), 0.f);
   }
   __syncthreads();
   dif_from<N1, N1, B>(sm, P, tw1);
@@ -260,6 +288,90 @@ k_rows(float2* __restrict__ T, const float2* __restrict__ H, int conj_h, int row
   }
 }
 
+
+// Real plans: the rows kernel on row pairs.  Position q of row R holds the spectral index
+// k = kb + kmul digit_rev(q, N2), kb = digit_rev(R / A, N1) + N1 digit_rev(R mod A, A) (A = 1 for two-level
+// plans), kmul = N1 A; the mirror indices N - k all lie in the row of kb' = (kmul - kb) mod kmul.  Unit
+// u in [0, kmul / 2] is the row pair (kb = u, kb' = kmul - u); kb = 0 and kmul / 2 are their own mirrors.
+// The four-step twiddle of row R is w^{mult n2 digit_rev(R mod rowmod, rowmod)}, as in k_rows.  H holds
+// H[k] (k < N) in the same positions, entry k = 0 = (H[0], H[N]).
+__host__ __device__ constexpr int units_per_cta(int N2) { return N2 >= 2048 ? 1 : 2048 / N2; }
+
+// Z'[k] from Z[k], Z[N-k] (zk, zb), H[k], H[k+N] and W^k; the factor 1/4 is folded into the inverse scale.
+__device__ __forceinline__ float2 r2c_mul(float2 zk, float2 zb, float2 hk, float2 hkn, float2 w) {
+  const float2 e = make_float2(zk.x + zb.x, zk.y - zb.y);  // 2 E
+  const float2 d = make_float2(zk.x - zb.x, zk.y + zb.y);  // Z[k] - conj(Z[N-k])
+  const float2 o = make_float2(d.y, -d.x);                 // 2 O = d / i
+  const float2 wo = cmulf(w, o);
+  const float2 yk = cmulf(hk, make_float2(e.x + wo.x, e.y + wo.y));    // 2 Y[k]
+  const float2 ykn = cmulf(hkn, make_float2(e.x - wo.x, e.y - wo.y));  // 2 Y[k+N]
+  const float2 dd = cmulf_conj(make_float2(yk.x - ykn.x, yk.y - ykn.y), w);  // W^-k (Y[k] - Y[k+N])
+  return make_float2(yk.x + ykn.x - dd.y, yk.y + ykn.y + dd.x);          // 4 Z'[k]
+}
+
+template <int N2>
+__global__ void __launch_bounds__(kThr, N2 <= 256 ? 4 : 1)
+k_rows_r2c(float2* __restrict__ T, const float2* __restrict__ H, int conj_h, int N1, int A, int rowmod, int mult,
+           const float2* __restrict__ tw2, const float2* __restrict__ twA, const float2* __restrict__ twB,
+           const float2* __restrict__ twCA, const float2* __restrict__ twCB) {
+  extern __shared__ float2 sm[];
+  constexpr int upc = units_per_cta(N2), slots = 2 * upc, P = row_pitch(N2), cnt = slots * N2;
+  const int N = N1 * A * N2, kmul = N1 * A;
+  __shared__ int rows_s[slots], k1s[slots], kbs[slots];
+  if (threadIdx.x < slots) {
+    const int u = blockIdx.x * upc + (threadIdx.x >> 1);
+    const int kb = (threadIdx.x & 1) ? (kmul - u) & (kmul - 1) : u;
+    const bool live = u <= kmul / 2 && !((threadIdx.x & 1) && kb == u);  // the mirror slot of a self unit idles
+    const int R = live ? digit_pos(kb % N1, N1) * A + digit_pos(kb / N1, A) : -1;
+    rows_s[threadIdx.x] = R;
+    k1s[threadIdx.x] = R >= 0 ? mult * digit_rev(R % rowmod, rowmod) : 0;
+    kbs[threadIdx.x] = kb;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < cnt; e += kThr) {
+    const int s = e / N2, n2 = e - s * N2, R = rows_s[s];
+    if (R >= 0) sm[s * P + pad16(n2)] = cmulf(T[static_cast<int64_t>(R) * N2 + n2], tw_n(twA, twB, n2 * k1s[s]));
+  }
+  __syncthreads();
+  dif_from<N2, N2, slots>(sm, P, tw2);
+  // spectral step: the thread of (slot 2u, q) handles k and its mirror N - k (at (2u + 1, qbar), or at
+  // (2u, qbar) when the row is its own mirror: then only q <= qbar works)
+  for (int e = threadIdx.x; e < upc * N2; e += kThr) {
+    const int u = e / N2, q = e - u * N2, sa = 2 * u;
+    const int R = rows_s[sa];
+    if (R < 0) continue;
+    const bool self = rows_s[sa + 1] < 0;
+    const int sb = self ? sa : sa + 1;
+    const int k = kbs[sa] + kmul * digit_rev(q, N2);
+    const int kb = (N - k) & (N - 1);
+    const int qb = digit_pos((kb - kbs[sb]) / kmul, N2);
+    if (self && qb < q) continue;
+    const int Rb = self ? R : rows_s[sb];
+    float2 hk = __ldg(H + static_cast<int64_t>(R) * N2 + q), hb = __ldg(H + static_cast<int64_t>(Rb) * N2 + qb);
+    if (conj_h) {
+      hk.y = -hk.y;
+      hb.y = -hb.y;
+    }
+    const float2 zk = sm[sa * P + pad16(q)], zb = sm[sb * P + pad16(qb)];
+    const float2 w = tw_n(twCA, twCB, k);  // W^k = e^{-2 pi i k / 2N}
+    if (k == 0) {  // H[0], H[N] real, packed (conj_h leaves them)
+      const float2 h0 = __ldg(H + static_cast<int64_t>(R) * N2 + q);
+      sm[sa * P + pad16(q)] = r2c_mul(zk, zk, make_float2(h0.x, 0.f), make_float2(h0.y, 0.f), w);
+      continue;
+    }
+    const float2 hkn = make_float2(hb.x, -hb.y), hbn = make_float2(hk.x, -hk.y);  // H[k+N], H[N-k+N]
+    sm[sa * P + pad16(q)] = r2c_mul(zk, zb, hk, hkn, w);
+    if (qb != q || sb != sa) sm[sb * P + pad16(qb)] = r2c_mul(zb, zk, hb, hbn, tw_n(twCA, twCB, kb));
+  }
+  __syncthreads();
+  dit_from<N2, N2, slots>(sm, P, tw2);
+  for (int e = threadIdx.x; e < cnt; e += kThr) {
+    const int s = e / N2, n2 = e - s * N2, R = rows_s[s];
+    if (R >= 0)
+      T[static_cast<int64_t>(R) * N2 + n2] = cmulf_conj(sm[s * P + pad16(n2)], tw_n(twA, twB, n2 * k1s[s]));
+  }
+}
+
 // Three-level plans: the A-point transforms of the row length N2 = A * B, along the stride-B axis of each
 // row p (element n2 = n2a B + n3), C = cols_per_cta(A) consecutive n3 per CTA (128-byte segments).
 //   FWD: x w_n^{n2 k1} (the outer four-step twiddle, k1 = digit_rev(p)), DIF over n2a, in place;
@@ -297,7 +409,32 @@ __global__ void __launch_bounds__(kThr, 4) k_mid(float2* __restrict__ T, int N1,
 //   Fft4Out::kResidual r[t] = y[t] - Re / n and u[j] = r[t] at the rows (P^T r kept dense)
 //   Fft4Out::kIstaStep delta[j] = Re / n, x[j] = eta(x[j] + tau delta[j])  (unchecked iterations)
 //   Fft4Out::kBeta     beta[j] = rho Re / n + sigma (z[j] - nu[j])
-template <int N1>
+__device__ __forceinline__ void emit_out(const Fft4Out& o, int64_t j, float v) {
+  if (j >= o.n_valid) return;
+  if (o.mode == Fft4Out::kProduct) {
+    o.out[j] = v;
+  } else if (o.mode == Fft4Out::kBeta) {  // parallel.hpp:186-187
+    o.out[j] = __fadd_rn(__fmul_rn(o.rho, v), __fmul_rn(o.sigma, __fsub_rn(o.z[j], o.nu[j])));
+  } else if (o.mode == Fft4Out::kIstaStep) {
+    const float xo = o.x[j];
+    const float xn = __fadd_rn(xo, __fmul_rn(o.tau, v));  // parallel.hpp:269-271
+    o.x[j] = xn > o.thr ? xn - o.thr : (xn < -o.thr ? xn + o.thr : 0.f);
+    o.out[j] = v;
+  } else {
+    const int t = __ldg(o.rowid + j);
+    if (t >= 0) {
+      if (o.mode == Fft4Out::kRows) {
+        o.out[t] = v;
+      } else {  // kResidual: cpista residual, parallel.hpp:252
+        const float rv = __ldg(o.y + t) - v;
+        o.out[t] = rv;
+        o.u[j] = rv;
+      }
+    }
+  }
+}
+// REAL: element j of the inverse holds y[2j] + i y[2j+1]; else Re = y[j].
+template <int N1, bool REAL>
 __global__ void __launch_bounds__(kThr, N1 <= 256 ? 4 : 1) k_cols_inv(const float2* __restrict__ T, Fft4Out o, int N2,
                                                    const float2* __restrict__ tw1, float inv_n) {
   extern __shared__ float2 sm[];
@@ -314,43 +451,29 @@ __global__ void __launch_bounds__(kThr, N1 <= 256 ? 4 : 1) k_cols_inv(const floa
   for (int e = threadIdx.x; e < cnt; e += kThr) {
     const int i = e / B, w = e - i * B;
     const int64_t j = static_cast<int64_t>(i) * N2 + c0 + w;
-    const float v = sm[w * P + pad16(i)].x * inv_n;
-    if (j >= o.n_valid) continue;
-    if (o.mode == Fft4Out::kProduct) {
-      o.out[j] = v;
-    } else if (o.mode == Fft4Out::kBeta) {  // parallel.hpp:186-187
-      o.out[j] = __fadd_rn(__fmul_rn(o.rho, v), __fmul_rn(o.sigma, __fsub_rn(o.z[j], o.nu[j])));
-    } else if (o.mode == Fft4Out::kIstaStep) {
-      const float xo = o.x[j];
-      const float xn = __fadd_rn(xo, __fmul_rn(o.tau, v));  // parallel.hpp:269-271
-      o.x[j] = xn > o.thr ? xn - o.thr : (xn < -o.thr ? xn + o.thr : 0.f);
-      o.out[j] = v;
+    const float2 s = sm[w * P + pad16(i)];
+    if (REAL) {
+      emit_out(o, 2 * j, s.x * inv_n);
+      emit_out(o, 2 * j + 1, s.y * inv_n);
     } else {
-      const int t = __ldg(o.rowid + j);
-      if (t >= 0) {
-        if (o.mode == Fft4Out::kRows) {
-          o.out[t] = v;
-        } else {  // kResidual: cpista residual, parallel.hpp:252
-          const float rv = __ldg(o.y + t) - v;
-          o.out[t] = rv;
-          o.u[j] = rv;
-        }
-      }
+      emit_out(o, j, s.x * inv_n);
     }
   }
 }
 
 // H~[p N2 + q] = spec[rev1(p) + N1 rev2(q)] / s  (fp64 spectrum -> permuted fp32); three levels (A > 0):
 // q = q2a B + q3 holds k2 = rev_A(q2a) + A rev_B(q3)
+// real: entry k = 0 holds (H[0], H[N]) (both real)
 __global__ void k_perm_spectrum(const double2* __restrict__ spec, double s, float2* __restrict__ out, int N1, int N2,
-                                int A, int B) {
+                                int A, int B, int real) {
   const int64_t n = static_cast<int64_t>(N1) * N2;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     const int p = static_cast<int>(e / N2), q = static_cast<int>(e - static_cast<int64_t>(p) * N2);
     const int64_t k2 = A > 0 ? digit_rev(q / B, A) + static_cast<int64_t>(A) * digit_rev(q % B, B) : digit_rev(q, N2);
     const int64_t k = digit_rev(p, N1) + static_cast<int64_t>(N1) * k2;
     const double2 v = spec[k];
-    out[e] = make_float2(static_cast<float>(v.x / s), static_cast<float>(v.y / s));
+    out[e] = (real && k == 0) ? make_float2(static_cast<float>(v.x / s), static_cast<float>(spec[n].x / s))
+                              : make_float2(static_cast<float>(v.x / s), static_cast<float>(v.y / s));
   }
 }
 
@@ -506,14 +629,23 @@ constexpr int kThreeLevelLog = 22;
 
 bool fft4_supported(int64_t n) { return n >= (int64_t(1) << 14) && n <= (int64_t(1) << 24) && (n & (n - 1)) == 0; }
 
+// Real plans for n >= 2^22 (half the bytes per pass: 1.22 vs 1.83 ms per cADMM iteration at n = 2^24);
+// below, the arrays are L2-resident and the passes latency-bound, and the complex plans' finer row split
+// keeps more CTAs in flight (n = 2^17: 0.097 vs 0.134 ms; 2^20: equal).  CLB_FFT_C2C=0/1 forces either.
 Fft4Plan fft4_plan(int64_t n) {
   Fft4Plan p;
-  int L = 0;
-  while ((int64_t(1) << L) < n) ++L;
   p.n = n;
-  if (L >= kThreeLevelLog && !std::getenv("CLB_FFT_TWO_LEVEL")) {  // 256 x A x B, A, B in {128, 256}
+  int Ln = 0;
+  while ((int64_t(1) << Ln) < n) ++Ln;
+  const char* c2c = std::getenv("CLB_FFT_C2C");
+  p.real = (c2c && *c2c) ? c2c[0] == '0' : Ln >= kThreeLevelLog;
+  p.N = p.real ? n / 2 : n;
+  int L = 0;
+  while ((int64_t(1) << L) < p.N) ++L;
+  // three levels from n = 2^22 (N1 = 256 columns: 128-byte row segments in every pass)
+  if (Ln >= kThreeLevelLog && !std::getenv("CLB_FFT_TWO_LEVEL")) {  // 256 x A x B, A in {128, 256}
     p.N1 = 256;
-    p.N2 = static_cast<int>(n >> 8);
+    p.N2 = static_cast<int>(p.N >> 8);
     p.A = p.N2 >= (1 << 15) ? 256 : 128;
     p.B = p.N2 / p.A;
     return p;
@@ -521,7 +653,7 @@ Fft4Plan fft4_plan(int64_t n) {
   int l1 = L / 2;
   if (l1 > 11) l1 = 11;
   p.N1 = 1 << l1;
-  p.N2 = static_cast<int>(n >> l1);
+  p.N2 = static_cast<int>(p.N >> l1);
   return p;
 }
 
@@ -544,17 +676,29 @@ void fft4_twiddles(const Fft4Plan& p, std::vector<float2>* tw1, std::vector<floa
   } else {
     table(*tw2, p.N2, 1.0 / p.N2);
   }
-  const double nn = static_cast<double>(p.n);
-  table(*twA, 4096, 1.0 / nn);                                              // e^{-2 pi i a / n}
-  table(*twB, static_cast<int>(std::max<int64_t>(1, p.n / 4096)), 4096.0 / nn);  // e^{-2 pi i 4096 b / n}
+  const double NN = static_cast<double>(p.N);
+  table(*twA, 4096, 1.0 / NN);                                              // e^{-2 pi i a / N}
+  table(*twB, static_cast<int>(std::max<int64_t>(1, p.N / 4096)), 4096.0 / NN);  // e^{-2 pi i 4096 b / N}
+  if (p.real) {  // W^k = e^{-2 pi i k / n} for the real-spectrum unpacking
+    const double nn = static_cast<double>(p.n);
+    std::vector<float2> ca, cb;
+    table(ca, 4096, 1.0 / nn);
+    table(cb, static_cast<int>(std::max<int64_t>(1, p.n / 4096)), 4096.0 / nn);
+    twA->insert(twA->end(), ca.begin(), ca.end());
+    twB->insert(twB->end(), cb.begin(), cb.end());
+  }
 }
+// offsets of the e^{-2 pi i idx / n} factors appended to twA / twB
+static int64_t twB_len(const Fft4Plan& p) { return std::max<int64_t>(1, p.N / 4096); }
 
 template <int N>
 static size_t cols_smem_t() { return static_cast<size_t>(cols_per_cta(N)) * col_pitch(N) * sizeof(float2); }
 template <int N>
 static size_t rows_smem_t() { return static_cast<size_t>(row_count(N)) * row_pitch(N) * sizeof(float2); }
+template <int N>
+static size_t rows_r2c_smem_t() { return static_cast<size_t>(2 * units_per_cta(N)) * row_pitch(N) * sizeof(float2); }
 
-#define CLB_FFT4_SIZES(X) X(128) X(256) X(512) X(1024) X(2048) X(4096) X(8192)
+#define CLB_FFT4_SIZES(X) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096) X(8192)
 
 void fft4_init_attributes() {
   static std::atomic<uint64_t> devs{0};
@@ -562,10 +706,13 @@ void fft4_init_attributes() {
   // columns are at most 2048 long (fft4_plan); longer column kernels are never launched
 #define CLB_ATTR(N)                                                                                             \
   if (N <= 2048) {                                                                                              \
-    cudaFuncSetAttribute(k_cols_fwd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem_t<N>());   \
-    cudaFuncSetAttribute(k_cols_inv<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem_t<N>());   \
+    cudaFuncSetAttribute(k_cols_fwd<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem_t<N>()); \
+    cudaFuncSetAttribute(k_cols_inv<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem_t<N>()); \
+    cudaFuncSetAttribute(k_cols_fwd<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem_t<N>());  \
+    cudaFuncSetAttribute(k_cols_inv<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem_t<N>());  \
   }                                                                                                             \
-  cudaFuncSetAttribute(k_rows<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem_t<N>());
+  cudaFuncSetAttribute(k_rows<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem_t<N>());         \
+  cudaFuncSetAttribute(k_rows_r2c<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_r2c_smem_t<N>());
   CLB_FFT4_SIZES(CLB_ATTR)
 #undef CLB_ATTR
   cudaFuncSetAttribute(k_mid<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem_t<128>());
@@ -576,8 +723,11 @@ void fft4_init_attributes() {
 
 void launch_fft4_cols_fwd(const Fft4Plan& p, const float* u, float2* T, const float2* tw1, cudaStream_t st) {
   switch (p.N1) {
-#define CLB_CASE(N) \
-  case N: k_cols_fwd<N><<<p.N2 / cols_per_cta(N), kThr, cols_smem_t<N>(), st>>>(u, T, p.N2, tw1); break;
+#define CLB_CASE(N)                                                                                        \
+  case N:                                                                                                  \
+    if (p.real) k_cols_fwd<N, true><<<p.N2 / cols_per_cta(N), kThr, cols_smem_t<N>(), st>>>(u, T, p.N2, tw1); \
+    else k_cols_fwd<N, false><<<p.N2 / cols_per_cta(N), kThr, cols_smem_t<N>(), st>>>(u, T, p.N2, tw1);      \
+    break;
     CLB_FFT4_SIZES(CLB_CASE)
 #undef CLB_CASE
   }
@@ -593,8 +743,10 @@ void launch_fft4_rows(const Fft4Plan& p, float2* T, const float2* H, bool conj_h
                       const float2* twA, const float2* twB, cudaStream_t st) {
   // rows of length R, `count` of them; row r's twiddle exponent mult * n2 * digit_rev(r mod rowmod)
   const int R = p.three() ? p.B : p.N2;
-  const int count = static_cast<int>(p.n / R), rowmod = p.three() ? p.A : p.N1, mult = p.three() ? p.N1 : 1;
+  const int count = static_cast<int>(p.N / R), rowmod = p.three() ? p.A : p.N1, mult = p.three() ? p.N1 : 1;
   const float2* twR = p.three() ? tw2 + p.A : tw2;
+  const int A = p.three() ? p.A : 1, kmul = p.N1 * A;
+  const float2 *twCA = twA + 4096, *twCB = twB + twB_len(p);
   if (p.three()) {
     if (p.A == 256) launch_mid<256>(p, T, true, tw2, twA, twB, st);
     else launch_mid<128>(p, T, true, tw2, twA, twB, st);
@@ -602,8 +754,12 @@ void launch_fft4_rows(const Fft4Plan& p, float2* T, const float2* H, bool conj_h
   switch (R) {
 #define CLB_CASE(N)                                                                                            \
   case N:                                                                                                      \
-    k_rows<N><<<count / row_count(N), kThr, rows_smem_t<N>(), st>>>(T, H, conj_h ? 1 : 0, rowmod, mult, twR,  \
-                                                                      twA, twB);                               \
+    if (p.real)                                                                                                \
+      k_rows_r2c<N><<<(kmul / 2 + units_per_cta(N)) / units_per_cta(N), kThr, rows_r2c_smem_t<N>(), st>>>(     \
+          T, H, conj_h ? 1 : 0, p.N1, A, rowmod, mult, twR, twA, twB, twCA, twCB);                            \
+    else                                                                                                       \
+      k_rows<N><<<count / row_count(N), kThr, rows_smem_t<N>(), st>>>(T, H, conj_h ? 1 : 0, rowmod, mult, twR, \
+                                                                        twA, twB);                             \
     break;
     CLB_FFT4_SIZES(CLB_CASE)
 #undef CLB_CASE
@@ -615,18 +771,20 @@ void launch_fft4_rows(const Fft4Plan& p, float2* T, const float2* H, bool conj_h
 }
 void launch_fft4_cols_inv(const Fft4Plan& p, const float2* T, const Fft4Out& o, const float2* tw1,
                           cudaStream_t st) {
-  const float inv_n = 1.0f / static_cast<float>(p.n);
+  // real plans: 1 / N for the length-N inverse times the 1/4 of the spectral step (k_rows_r2c)
+  const float inv_n = p.real ? 1.0f / (4.0f * static_cast<float>(p.N)) : 1.0f / static_cast<float>(p.n);
   switch (p.N1) {
-#define CLB_CASE(N)                                                                                     \
-  case N:                                                                                               \
-    k_cols_inv<N><<<p.N2 / cols_per_cta(N), kThr, cols_smem_t<N>(), st>>>(T, o, p.N2, tw1, inv_n);     \
+#define CLB_CASE(N)                                                                                        \
+  case N:                                                                                                  \
+    if (p.real) k_cols_inv<N, true><<<p.N2 / cols_per_cta(N), kThr, cols_smem_t<N>(), st>>>(T, o, p.N2, tw1, inv_n); \
+    else k_cols_inv<N, false><<<p.N2 / cols_per_cta(N), kThr, cols_smem_t<N>(), st>>>(T, o, p.N2, tw1, inv_n);      \
     break;
     CLB_FFT4_SIZES(CLB_CASE)
 #undef CLB_CASE
   }
 }
 void launch_fft4_perm_spectrum(const Fft4Plan& p, const double2* spec, double s, float2* out, cudaStream_t st) {
-  k_perm_spectrum<<<148 * 8, 256, 0, st>>>(spec, s, out, p.N1, p.N2, p.A, p.B);
+  k_perm_spectrum<<<148 * 8, 256, 0, st>>>(spec, s, out, p.N1, p.N2, p.A, p.B, p.real ? 1 : 0);
 }
 bool small_fft_supported(int64_t n) {
   const char* v = std::getenv("CLB_NO_SMALL");

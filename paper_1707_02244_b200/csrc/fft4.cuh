@@ -7,8 +7,10 @@
 
 namespace clb {
 struct Fft4Plan {
-  int64_t n = 0;
-  int N1 = 0, N2 = 0;  // n = N1 * N2; columns of length N1, rows of length N2
+  int64_t n = 0;       // length of the (real) product
+  int64_t N = 0;       // transform length: n / 2 complex values for real plans (the default), else n
+  bool real = false;   // real plans: z[j] = u[2j] + i u[2j+1], the spectrum unpacked pairwise in the rows kernel
+  int N1 = 0, N2 = 0;  // N = N1 * N2; columns of length N1, rows of length N2
   // n >= 2^22: three levels, N1 = 256 and the length-N2 row transforms themselves four-step, N2 = A * B
   // (A along a stride-B axis, B contiguous), so every pass moves 128-byte row segments
   int A = 0, B = 0;
@@ -18,11 +20,12 @@ bool fft4_supported(int64_t n);
 Fft4Plan fft4_plan(int64_t n);
 // twiddle tables (host, fp64-accurate fp32): e^{-2 pi i k / N1}, e^{-2 pi i k / N2} (three levels: the
 // A-point table followed by the B-point table), and the two factors of
-// e^{-2 pi i idx / n} = twB[idx >> 12] * twA[idx & 4095]
+// e^{-2 pi i idx / N} = twB[idx >> 12] * twA[idx & 4095]; real plans append to twA / twB the factors of
+// e^{-2 pi i idx / n} (4096 and n / 4096 entries)
 void fft4_twiddles(const Fft4Plan& p, std::vector<float2>* tw1, std::vector<float2>* tw2, std::vector<float2>* twA,
                    std::vector<float2>* twB);
 void fft4_init_attributes();
-// u real (n) -> T: column DIF FFTs (spectral order permuted)
+// u real (n) -> T (N complex): column DIF FFTs (spectral order permuted)
 void launch_fft4_cols_fwd(const Fft4Plan& p, const float* u, float2* T, const float2* tw1, cudaStream_t st);
 // in place: twiddle, row DIF FFT, times H~ (or conj), row DIT inverse FFT, inverse twiddle (three levels:
 // the length-N2 row transforms as A-point passes over a stride-B axis around B-point contiguous rows)
@@ -44,7 +47,8 @@ struct Fft4Out {
 };
 // T -> column DIT inverse FFTs, then `o`.
 void launch_fft4_cols_inv(const Fft4Plan& p, const float2* T, const Fft4Out& o, const float2* tw1, cudaStream_t st);
-// natural-order fp64 spectrum / s -> the engine's permuted fp32 order
+// natural-order fp64 spectrum (n entries) / s -> the engine's permuted fp32 order (N entries; real plans pack
+// H[0] and H[n / 2] into entry 0)
 void launch_fft4_perm_spectrum(const Fft4Plan& p, const double2* spec, double s, float2* out, cudaStream_t st);
 // rowid[j] = t for j = omega[t], -1 elsewhere
 void launch_rowid(const int* omega, int* rowid, int64_t n, int64_t m, cudaStream_t st);

@@ -513,6 +513,29 @@ def test_fft4_three_level_matches_oracle(kind, lg, iters):
         assert rel_l2(g.get(h), o.get(h)) <= REL_TOL, h
 
 
+@pytest.mark.parametrize("kind,lg", [("ista", 14), ("cadmm", 15), ("ista", 18), ("cadmm", 20), ("ista", 22),
+                                     ("cadmm", 23), ("ista", 24), ("cadmm", 24)])
+def test_fft4_real_plan_matches_complex_plan(kind, lg):
+    """Real plans (n / 2 complex points, the spectrum unpacked pairwise between the row FFTs; the default)
+    against the complex plans (CLB_FFT_C2C=1: n complex points), two- and three-level, up to n = 2^24."""
+    import os
+    n = 1 << lg
+    p = orc.make_problem(n, n // 4, n // 256, 2)
+    setup = cl.ista_setup if kind == "ista" else cl.cadmm_setup
+    got = {}
+    for c2c in ("0", "1"):  # force the real / the complex plan
+        os.environ["CLB_FFT_C2C"] = c2c
+        try:
+            g = setup(op_of(p), p.y, cl.SolverConfig(use_fft=True))
+            g.step(4)
+            got[c2c] = {f: g.get(f) for f in (("x", "r") if kind == "ista" else ("z", "x", "v"))}
+            del g
+        finally:
+            del os.environ["CLB_FFT_C2C"]
+    for f in got["0"]:
+        assert rel_l2(got["0"][f], got["1"][f]) <= 1e-5, (f, rel_l2(got["0"][f], got["1"][f]))
+
+
 @pytest.mark.parametrize("kind,lg", [("ista", 20), ("ista", 23), ("cadmm", 22), ("ista", 24)])
 def test_fft4_engine_matches_stockham_engine(kind, lg):
     """Four-step engine vs the multi-pass Stockham engine (CLB_FFT_STOCKHAM=1) up to n = 2^24."""
