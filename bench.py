@@ -154,26 +154,28 @@ def cpu_phase_sampler(w):
         sample = "full iterations" if full else \
             f"residual phase on {rows} of {m} rows + gradient phase on {outs} of {n} outputs, scaled to the full phases"
 
-        def step():
+        def step():  # (seconds of one full iteration, wall seconds of this step)
+            t0 = time.perf_counter()
             if full:
-                t0 = time.perf_counter()
                 h.step(1, orc.ENGINE_PHASES, threads)
-                return time.perf_counter() - t0
+                dt = time.perf_counter() - t0
+                return dt, dt
             tr, tg = h.phase_sample(rows, outs, threads)
-            return tr * m / rows + tg * n / outs
+            return tr * m / rows + tg * n / outs, time.perf_counter() - t0
     else:
         h = orc.Cadmm(p.row, p.omega, p.y)
         outs = max(1, min(n, SAMPLE_FMA // n))
         full = outs == n
         sample = "full iterations" if full else f"the three phases on {outs} of {n} outputs, scaled to the full phases"
 
-        def step():
+        def step():  # (seconds of one full iteration, wall seconds of this step)
+            t0 = time.perf_counter()
             if full:
-                t0 = time.perf_counter()
                 h.step(1, orc.ENGINE_PHASES, threads)
-                return time.perf_counter() - t0
-            return sum(h.phase_sample(outs, threads)) * n / outs
-    return step, threads, sample
+                dt = time.perf_counter() - t0
+                return dt, dt
+            return sum(h.phase_sample(outs, threads)) * n / outs, time.perf_counter() - t0
+    return step, threads, sample, full
 
 
 def cpu_fft_rate(w, steps: int):
@@ -187,26 +189,33 @@ def cpu_fft_rate(w, steps: int):
 
 
 def cpu_baseline_line(w, steps: int, warmup: int):
-    step, threads, sample = cpu_phase_sampler(w)
+    """Returns the baseline dict, the (extrapolated) seconds per full iteration and the wall seconds per
+    timed step (a bounded sample when the iteration is too long to run whole)."""
+    step, threads, sample, full = cpu_phase_sampler(w)
     for _ in range(warmup):
         step()
-    secs = [step() for _ in range(steps)]
-    per_iter = sum(secs) / len(secs)
+    res = [step() for _ in range(steps)]
+    per_iter = sum(r[0] for r in res) / len(res)
+    wall = sum(r[1] for r in res) / len(res)
     return {"value": 1.0 / per_iter, "unit": "iterations/s", "cores": threads, "kind": "port",
             "sample": f"{steps} steps of the phase engine (direct mat-vec, fp64, {threads} threads): {sample}",
-            "engine": "phases (cpista_phases/cpadmm_phases restated in oracle/)"}, per_iter
+            "extrapolated": not full,
+            "engine": "phases (cpista_phases/cpadmm_phases restated in oracle/)"}, per_iter, wall
 
 
 def run_reference(args, w, rank):
     if rank != 0:
         return
     steps = max(1, args.steps)
-    warm = min(args.warmup, 1)
-    cpu, per_iter = cpu_baseline_line(w, steps, warm)
+    warm = args.warmup
+    cpu, per_iter, wall = cpu_baseline_line(w, steps, warm)
     rate = cpu["value"]
+    # ms_per_step is the wall time of one timed step as run (a bounded sample of the iteration when
+    # `extrapolated`); value is the full-iteration rate the samples scale to
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": "iterations/s", "n_gpus": args.gpus,
-        "steps": steps, "warmup": warm, "ms_per_step": 1e3 * per_iter, "higher_is_better": True,
+        "steps": steps, "warmup": warm, "ms_per_step": 1e3 * wall,
+        "ms_per_iteration": 1e3 * per_iter, "extrapolated": cpu["extrapolated"], "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (make_problem, seeded)",
         "config": {"workload": w["desc"], "n": w["n"], "m": w["m"], "k": w["k"], "seed": w["seed"]},
         "cpu_baseline": cpu,
@@ -585,17 +594,18 @@ def main():
 
     cpu = None
     if rank == 0 and not sharded and not args.no_cpu_baseline:
-        cpu, _ = cpu_baseline_line(w, 3 if w["n"] >= (1 << 20) else 20, 1)
+        cpu, _, _ = cpu_baseline_line(w, 3 if w["n"] >= (1 << 20) else 20, 1)
         if fft_line is not None:
             fft_line["cpu_fft_engine"] = {
                 "value": cpu_fft_rate(w, 2 if w["n"] >= (1 << 20) else 20), "unit": "iterations/s", "cores": 1,
                 "kind": "port", "sample": "full iterations of the reference-default FFT engine (single thread)"}
         if admm is not None:
-            step, threads, sample = cpu_phase_sampler(dict(w, kind="cadmm"))
+            step, threads, sample, full = cpu_phase_sampler(dict(w, kind="cadmm"))
             step()
-            secs = [step() for _ in range(2)]
+            secs = [step()[0] for _ in range(2)]
             admm["cpu_baseline"] = {"value": len(secs) / sum(secs), "unit": "iterations/s", "cores": threads,
-                                    "kind": "port", "sample": f"2 steps of the cADMM phase engine (fp64): {sample}"}
+                                    "kind": "port", "sample": f"2 steps of the cADMM phase engine (fp64): {sample}",
+                                    "extrapolated": not full}
         if recovery is not None:
             for kind, rate in (("ista", cpu["value"]), ("cadmm", admm["cpu_baseline"]["value"] if admm else None)):
                 if rate:
