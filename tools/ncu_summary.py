@@ -1,5 +1,6 @@
 #!/usr/bin/env python3
-"""Summarise ncu reports (run here, on the CPU box) into profiles/ncu_summary.json.
+"""Summarise ncu reports (run here, on the CPU box) into profiles/ncu_summary.json (merged: kernels
+captured in these reports replace their earlier entries).
 
     python tools/ncu_summary.py gpurun_out/prof_r1.ncu-rep [more.ncu-rep ...] [--launches launches.csv]
 """
@@ -38,7 +39,8 @@ DIRECT = ("k_res_s", "k_grad_s", "k_tc_dense", "k_absmax2", "k_residual_gather",
           "k_admm_x", "k_admm_duals", "k_metrics_final")
 FFT = ("k_fft_pass<16, -1>", "k_fft_pass<16, 1>", "k_fft_pass<8, -1>", "k_fft_pass<8, 1>", "k_fft_pass<4, -1>",
        "k_fft_pass<4, 1>", "k_fft_pass<2, -1>", "k_fft_pass<2, 1>", "k_real_to_complex", "k_spec_mul",
-       "k_extract_real", "k_gather_real", "k_zero_c", "k_scatter_rows")
+       "k_extract_real", "k_gather_real", "k_zero_c", "k_scatter_rows", "k_rows_r2c", "k_mid", "k_cols_fwd",
+       "k_cols_inv", "k_rows")
 
 
 def short(name):
@@ -112,13 +114,20 @@ def main():
         i = args.index("--launches")
         lp = args[i + 1]
         del args[i:i + 2]
-    summary = {}
+    dst = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "ncu_summary.json")
+    try:  # merge: kernels captured here replace their earlier entries, the others stay
+        summary = json.load(open(dst))
+    except (OSError, ValueError):
+        summary = {}
+    fresh = set()
     for rep in args:
         for e in load(rep):
-            summary.setdefault(e["kernel"], e)  # first capture of each kernel
+            if e["kernel"] not in fresh:  # first capture of each kernel in this run
+                summary[e["kernel"]] = e
+                fresh.add(e["kernel"])
     if lp:
         summary["launch_list"] = launches(lp)
-    dst = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "ncu_summary.json")
+        summary["launch_list_source"] = os.path.basename(lp)
     json.dump(summary, open(dst, "w"), indent=1)
     print(json.dumps(summary, indent=1)[:4000])
 
