@@ -188,7 +188,8 @@ __host__ __device__ __forceinline__ int digit_pos(int k, int N) {
 // ---- kernels -----------------------------------------------------------------
 // Columns per CTA and the column pitch: pitch = (16 / B) mod 16 (complex) keeps
 // the coalesced row-segment loads (B columns x 4 rows per half-warp) conflict-free.
-__host__ __device__ constexpr int cols_per_cta(int N1) { return N1 <= 1024 ? kElems / N1 : 4; }
+// 2048-long columns (two-level plans at N >= 2^22): 8 columns = 64-byte row segments, 139 KB of shared memory
+__host__ __device__ constexpr int cols_per_cta(int N1) { return N1 <= 1024 ? kElems / N1 : N1 == 2048 ? 8 : 4; }
 __host__ __device__ constexpr int col_pitch(int N1) {
   return N1 + N1 / 16 + (cols_per_cta(N1) <= 16 ? 16 / cols_per_cta(N1) : 1);
 }
@@ -309,15 +310,18 @@ __device__ __forceinline__ float2 r2c_mul(float2 zk, float2 zb, float2 hk, float
   return make_float2(yk.x + ykn.x - dd.y, yk.y + ykn.y + dd.x);          // 4 Z'[k]
 }
 
+// H2[u N2 + q] = (H at (row of kb = u, q), H at the mirror position): one 16-byte load per index pair.
+// t2[q] = W^{kmul digit_rev(q)}, so W^k = W^{kb} t2[q]; W^{N-k} = -conj(W^k).
 template <int N2>
 __global__ void __launch_bounds__(kThr, N2 <= 256 ? 4 : 1)
-k_rows_r2c(float2* __restrict__ T, const float2* __restrict__ H, int conj_h, int N1, int A, int rowmod, int mult,
+k_rows_r2c(float2* __restrict__ T, const float4* __restrict__ H2, int conj_h, int N1, int A, int rowmod, int mult,
            const float2* __restrict__ tw2, const float2* __restrict__ twA, const float2* __restrict__ twB,
-           const float2* __restrict__ twCA, const float2* __restrict__ twCB) {
+           const float2* __restrict__ twCA, const float2* __restrict__ twCB, const float2* __restrict__ t2) {
   extern __shared__ float2 sm[];
   constexpr int upc = units_per_cta(N2), slots = 2 * upc, P = row_pitch(N2), cnt = slots * N2;
-  const int N = N1 * A * N2, kmul = N1 * A;
+  const int kmul = N1 * A;
   __shared__ int rows_s[slots], k1s[slots], kbs[slots];
+  __shared__ float2 wrow[upc];
   if (threadIdx.x < slots) {
     const int u = blockIdx.x * upc + (threadIdx.x >> 1);
     const int kb = (threadIdx.x & 1) ? (kmul - u) & (kmul - 1) : u;
@@ -326,6 +330,7 @@ k_rows_r2c(float2* __restrict__ T, const float2* __restrict__ H, int conj_h, int
     rows_s[threadIdx.x] = R;
     k1s[threadIdx.x] = R >= 0 ? mult * digit_rev(R % rowmod, rowmod) : 0;
     kbs[threadIdx.x] = kb;
+    if (!(threadIdx.x & 1)) wrow[threadIdx.x >> 1] = tw_n(twCA, twCB, kb);  // W^{kb}
   }
   __syncthreads();
   for (int e = threadIdx.x; e < cnt; e += kThr) {
@@ -334,34 +339,30 @@ k_rows_r2c(float2* __restrict__ T, const float2* __restrict__ H, int conj_h, int
   }
   __syncthreads();
   dif_from<N2, N2, slots>(sm, P, tw2);
-  // spectral step: the thread of (slot 2u, q) handles k and its mirror N - k (at (2u + 1, qbar), or at
-  // (2u, qbar) when the row is its own mirror: then only q <= qbar works)
+  // spectral step: the thread of (slot 2u, q) handles k and its mirror N - k, at (2u + 1, qb) -- or at (2u, qb)
+  // when the row is its own mirror (kb = 0 or kmul / 2), and then only q <= qb works.  Mirror position:
+  // kb != 0: digit complement qb = N2 - 1 - q; kb = 0: the position of (N2 - k2) mod N2.
   for (int e = threadIdx.x; e < upc * N2; e += kThr) {
-    const int u = e / N2, q = e - u * N2, sa = 2 * u;
-    const int R = rows_s[sa];
-    if (R < 0) continue;
+    const int ul = e / N2, q = e - ul * N2, sa = 2 * ul;
+    if (rows_s[sa] < 0) continue;
     const bool self = rows_s[sa + 1] < 0;
-    const int sb = self ? sa : sa + 1;
-    const int k = kbs[sa] + kmul * digit_rev(q, N2);
-    const int kb = (N - k) & (N - 1);
-    const int qb = digit_pos((kb - kbs[sb]) / kmul, N2);
+    const int kbA = kbs[sa];
+    const int qb = kbA != 0 ? N2 - 1 - q : digit_pos((N2 - digit_rev(q, N2)) & (N2 - 1), N2);
     if (self && qb < q) continue;
-    const int Rb = self ? R : rows_s[sb];
-    float2 hk = __ldg(H + static_cast<int64_t>(R) * N2 + q), hb = __ldg(H + static_cast<int64_t>(Rb) * N2 + qb);
-    if (conj_h) {
-      hk.y = -hk.y;
-      hb.y = -hb.y;
-    }
-    const float2 zk = sm[sa * P + pad16(q)], zb = sm[sb * P + pad16(qb)];
-    const float2 w = tw_n(twCA, twCB, k);  // W^k = e^{-2 pi i k / 2N}
-    if (k == 0) {  // H[0], H[N] real, packed (conj_h leaves them)
-      const float2 h0 = __ldg(H + static_cast<int64_t>(R) * N2 + q);
-      sm[sa * P + pad16(q)] = r2c_mul(zk, zk, make_float2(h0.x, 0.f), make_float2(h0.y, 0.f), w);
+    const int sb = self ? sa : sa + 1;
+    const float4 hh = __ldg(H2 + static_cast<int64_t>(blockIdx.x * upc + ul) * N2 + q);
+    const float sgn = conj_h ? -1.f : 1.f;
+    const float2 hk = make_float2(hh.x, sgn * hh.y), hb = make_float2(hh.z, sgn * hh.w);
+    const float2 w = cmulf(wrow[ul], __ldg(t2 + q));  // W^k
+    const float2 zk = sm[sa * P + pad16(q)];
+    if (kbA == 0 && q == 0) {  // k = 0: H[0], H[N] real, packed (conj_h leaves them)
+      sm[sa * P] = r2c_mul(zk, zk, make_float2(hh.x, 0.f), make_float2(hh.y, 0.f), w);
       continue;
     }
-    const float2 hkn = make_float2(hb.x, -hb.y), hbn = make_float2(hk.x, -hk.y);  // H[k+N], H[N-k+N]
-    sm[sa * P + pad16(q)] = r2c_mul(zk, zb, hk, hkn, w);
-    if (qb != q || sb != sa) sm[sb * P + pad16(qb)] = r2c_mul(zb, zk, hb, hbn, tw_n(twCA, twCB, kb));
+    const float2 zb = sm[sb * P + pad16(qb)];
+    sm[sa * P + pad16(q)] = r2c_mul(zk, zb, hk, make_float2(hb.x, -hb.y), w);  // H[k+N] = conj H[N-k]
+    if (qb != q || sb != sa)
+      sm[sb * P + pad16(qb)] = r2c_mul(zb, zk, hb, make_float2(hk.x, -hk.y), make_float2(-w.x, w.y));
   }
   __syncthreads();
   dit_from<N2, N2, slots>(sm, P, tw2);
@@ -464,6 +465,22 @@ __global__ void __launch_bounds__(kThr, N1 <= 256 ? 4 : 1) k_cols_inv(const floa
 // H~[p N2 + q] = spec[rev1(p) + N1 rev2(q)] / s  (fp64 spectrum -> permuted fp32); three levels (A > 0):
 // q = q2a B + q3 holds k2 = rev_A(q2a) + A rev_B(q3)
 // real: entry k = 0 holds (H[0], H[N]) (both real)
+// Real plans: H2[u N2r + q] for units u in [0, kmul / 2] of row length N2r (see k_rows_r2c); entry k = 0
+// holds (H[0], H[N]).
+__global__ void k_perm_spectrum_pairs(const double2* __restrict__ spec, double s, float4* __restrict__ out, int N1,
+                                      int A, int N2r) {
+  const int kmul = N1 * A, N = kmul * N2r;
+  const int64_t total = static_cast<int64_t>(kmul / 2 + 1) * N2r;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int u = static_cast<int>(e / N2r), q = static_cast<int>(e - static_cast<int64_t>(u) * N2r);
+    const int k = u + kmul * digit_rev(q, N2r);
+    const int kb = (N - k) & (N - 1);
+    const double2 a = spec[k], b = spec[kb];
+    out[e] = k == 0 ? make_float4(static_cast<float>(a.x / s), static_cast<float>(spec[N].x / s), 0.f, 0.f)
+                    : make_float4(static_cast<float>(a.x / s), static_cast<float>(a.y / s),
+                                  static_cast<float>(b.x / s), static_cast<float>(b.y / s));
+  }
+}
 __global__ void k_perm_spectrum(const double2* __restrict__ spec, double s, float2* __restrict__ out, int N1, int N2,
                                 int A, int B, int real) {
   const int64_t n = static_cast<int64_t>(N1) * N2;
@@ -629,16 +646,17 @@ constexpr int kThreeLevelLog = 22;
 
 bool fft4_supported(int64_t n) { return n >= (int64_t(1) << 14) && n <= (int64_t(1) << 24) && (n & (n - 1)) == 0; }
 
-// Real plans for n >= 2^22 (half the bytes per pass: 1.22 vs 1.83 ms per cADMM iteration at n = 2^24);
-// below, the arrays are L2-resident and the passes latency-bound, and the complex plans' finer row split
-// keeps more CTAs in flight (n = 2^17: 0.097 vs 0.134 ms; 2^20: equal).  CLB_FFT_C2C=0/1 forces either.
+// Real plans for n >= 2^20 (half the bytes per pass; cADMM per iteration at 2^24 / 2^22 / 2^20: 1.10 / 0.33 /
+// 0.148 ms against 1.82 / 0.48 / 0.174 for the complex plans); below, the arrays are L2-resident, the passes
+// latency-bound, and the complex plans' finer row split keeps more CTAs in flight (2^17: 0.097 vs 0.134 ms).
+// CLB_FFT_C2C=0/1 forces either.
 Fft4Plan fft4_plan(int64_t n) {
   Fft4Plan p;
   p.n = n;
   int Ln = 0;
   while ((int64_t(1) << Ln) < n) ++Ln;
   const char* c2c = std::getenv("CLB_FFT_C2C");
-  p.real = (c2c && *c2c) ? c2c[0] == '0' : Ln >= kThreeLevelLog;
+  p.real = (c2c && *c2c) ? c2c[0] == '0' : Ln >= 20;
   p.N = p.real ? n / 2 : n;
   int L = 0;
   while ((int64_t(1) << L) < p.N) ++L;
@@ -686,9 +704,15 @@ void fft4_twiddles(const Fft4Plan& p, std::vector<float2>* tw1, std::vector<floa
     table(cb, static_cast<int>(std::max<int64_t>(1, p.n / 4096)), 4096.0 / nn);
     twA->insert(twA->end(), ca.begin(), ca.end());
     twB->insert(twB->end(), cb.begin(), cb.end());
+    // t2[q] = W^{kmul digit_rev(q)} = e^{-2 pi i digit_rev(q) / (2 N2r)} over the spectral row length N2r
+    const int N2r = p.three() ? p.B : p.N2;
+    for (int q = 0; q < N2r; ++q) {
+      const double a = -2.0 * M_PI * digit_rev(q, N2r) / (2.0 * N2r);
+      twA->push_back(make_float2(static_cast<float>(std::cos(a)), static_cast<float>(std::sin(a))));
+    }
   }
 }
-// offsets of the e^{-2 pi i idx / n} factors appended to twA / twB
+// offsets of the e^{-2 pi i idx / n} factors appended to twA / twB (then t2 after twA's 8192 entries)
 static int64_t twB_len(const Fft4Plan& p) { return std::max<int64_t>(1, p.N / 4096); }
 
 template <int N>
@@ -756,7 +780,8 @@ void launch_fft4_rows(const Fft4Plan& p, float2* T, const float2* H, bool conj_h
   case N:                                                                                                      \
     if (p.real)                                                                                                \
       k_rows_r2c<N><<<(kmul / 2 + units_per_cta(N)) / units_per_cta(N), kThr, rows_r2c_smem_t<N>(), st>>>(     \
-          T, H, conj_h ? 1 : 0, p.N1, A, rowmod, mult, twR, twA, twB, twCA, twCB);                            \
+          T, reinterpret_cast<const float4*>(H), conj_h ? 1 : 0, p.N1, A, rowmod, mult, twR, twA, twB, twCA,   \
+          twCB, twA + 8192);                                                                                   \
     else                                                                                                       \
       k_rows<N><<<count / row_count(N), kThr, rows_smem_t<N>(), st>>>(T, H, conj_h ? 1 : 0, rowmod, mult, twR, \
                                                                         twA, twB);                             \
@@ -784,7 +809,11 @@ void launch_fft4_cols_inv(const Fft4Plan& p, const float2* T, const Fft4Out& o, 
   }
 }
 void launch_fft4_perm_spectrum(const Fft4Plan& p, const double2* spec, double s, float2* out, cudaStream_t st) {
-  k_perm_spectrum<<<148 * 8, 256, 0, st>>>(spec, s, out, p.N1, p.N2, p.A, p.B, p.real ? 1 : 0);
+  if (p.real)
+    k_perm_spectrum_pairs<<<148 * 8, 256, 0, st>>>(spec, s, reinterpret_cast<float4*>(out), p.N1,
+                                                   p.three() ? p.A : 1, p.three() ? p.B : p.N2);
+  else
+    k_perm_spectrum<<<148 * 8, 256, 0, st>>>(spec, s, out, p.N1, p.N2, p.A, p.B, 0);
 }
 bool small_fft_supported(int64_t n) {
   const char* v = std::getenv("CLB_NO_SMALL");
