@@ -190,9 +190,13 @@ __host__ __device__ __forceinline__ int digit_pos(int k, int N) {
 // the coalesced row-segment loads (B columns x 4 rows per half-warp) conflict-free.
 // 2048-long columns (two-level plans at N >= 2^22): 8 columns = 64-byte row segments, 139 KB of shared memory
 __host__ __device__ constexpr int cols_per_cta(int N1) { return N1 <= 1024 ? kElems / N1 : N1 == 2048 ? 8 : 4; }
-__host__ __device__ constexpr int col_pitch(int N1) {
-  return N1 + N1 / 16 + (cols_per_cta(N1) <= 16 ? 16 / cols_per_cta(N1) : 1);
+// FINE (L2-resident sizes): half the columns / row units per CTA -- twice the CTAs in flight for the
+// latency-bound passes
+__host__ __device__ constexpr int cols_b(int N1, bool fine) {
+  return fine && cols_per_cta(N1) > 1 ? cols_per_cta(N1) / 2 : cols_per_cta(N1);
 }
+__host__ __device__ constexpr int col_pitch_b(int N1, int B) { return N1 + N1 / 16 + (B <= 16 ? 16 / B : 1); }
+__host__ __device__ constexpr int col_pitch(int N1) { return col_pitch_b(N1, cols_per_cta(N1)); }
 __host__ __device__ constexpr int row_count(int N2) { return N2 >= kElems ? 1 : kElems / N2; }
 __host__ __device__ constexpr int row_pitch(int N2) { return N2 + N2 / 16 + 1; }
 
@@ -204,11 +208,11 @@ __device__ __forceinline__ float2 tw_n(const float2* __restrict__ twA, const flo
 // Columns forward: input real u[j] (j = n1 N2 + n2).
 // REAL: the input is read as N complex values z[j] = (u[2j], u[2j+1]) (the real plans); else as the real
 // parts of n complex values.
-template <int N1, bool REAL>
+template <int N1, bool REAL, bool FINE = false>
 __global__ void __launch_bounds__(kThr, N1 <= 256 ? 4 : 1) k_cols_fwd(const float* __restrict__ u, float2* __restrict__ T, int N2,
                                                    const float2* __restrict__ tw1) {
   extern __shared__ float2 sm[];
-  constexpr int B = cols_per_cta(N1), P = col_pitch(N1), cnt = B * N1;
+  constexpr int B = cols_b(N1, FINE), P = col_pitch_b(N1, B), cnt = B * N1;
   const int c0 = blockIdx.x * B;
 #pragma unroll
   for (int e = threadIdx.x; e < cnt; e += kThr) {
@@ -296,7 +300,9 @@ k_rows(float2* __restrict__ T, const float2* __restrict__ H, int conj_h, int row
 // u in [0, kmul / 2] is the row pair (kb = u, kb' = kmul - u); kb = 0 and kmul / 2 are their own mirrors.
 // The four-step twiddle of row R is w^{mult n2 digit_rev(R mod rowmod, rowmod)}, as in k_rows.  H holds
 // H[k] (k < N) in the same positions, entry k = 0 = (H[0], H[N]).
-__host__ __device__ constexpr int units_per_cta(int N2) { return N2 >= 2048 ? 1 : 2048 / N2; }
+__host__ __device__ constexpr int units_per_cta(int N2, bool fine = false) {
+  return N2 >= 2048 ? 1 : fine && N2 == 1024 ? 1 : (fine ? 1024 : 2048) / N2;
+}
 
 // Z'[k] from Z[k], Z[N-k] (zk, zb), H[k], H[k+N] and W^k; the factor 1/4 is folded into the inverse scale.
 __device__ __forceinline__ float2 r2c_mul(float2 zk, float2 zb, float2 hk, float2 hkn, float2 w) {
@@ -312,13 +318,13 @@ __device__ __forceinline__ float2 r2c_mul(float2 zk, float2 zb, float2 hk, float
 
 // H2[u N2 + q] = (H at (row of kb = u, q), H at the mirror position): one 16-byte load per index pair.
 // t2[q] = W^{kmul digit_rev(q)}, so W^k = W^{kb} t2[q]; W^{N-k} = -conj(W^k).
-template <int N2>
+template <int N2, bool FINE = false>
 __global__ void __launch_bounds__(kThr, N2 <= 256 ? 4 : 1)
 k_rows_r2c(float2* __restrict__ T, const float4* __restrict__ H2, int conj_h, int N1, int A, int rowmod, int mult,
            const float2* __restrict__ tw2, const float2* __restrict__ twA, const float2* __restrict__ twB,
            const float2* __restrict__ twCA, const float2* __restrict__ twCB, const float2* __restrict__ t2) {
   extern __shared__ float2 sm[];
-  constexpr int upc = units_per_cta(N2), slots = 2 * upc, P = row_pitch(N2), cnt = slots * N2;
+  constexpr int upc = units_per_cta(N2, FINE), slots = 2 * upc, P = row_pitch(N2), cnt = slots * N2;
   const int kmul = N1 * A;
   __shared__ int rows_s[slots], k1s[slots], kbs[slots];
   __shared__ float2 wrow[upc];
@@ -435,11 +441,11 @@ __device__ __forceinline__ void emit_out(const Fft4Out& o, int64_t j, float v) {
   }
 }
 // REAL: element j of the inverse holds y[2j] + i y[2j+1]; else Re = y[j].
-template <int N1, bool REAL>
+template <int N1, bool REAL, bool FINE = false>
 __global__ void __launch_bounds__(kThr, N1 <= 256 ? 4 : 1) k_cols_inv(const float2* __restrict__ T, Fft4Out o, int N2,
                                                    const float2* __restrict__ tw1, float inv_n) {
   extern __shared__ float2 sm[];
-  constexpr int B = cols_per_cta(N1), P = col_pitch(N1), cnt = B * N1;
+  constexpr int B = cols_b(N1, FINE), P = col_pitch_b(N1, B), cnt = B * N1;
   const int c0 = blockIdx.x * B;
 #pragma unroll
   for (int e = threadIdx.x; e < cnt; e += kThr) {
@@ -646,17 +652,17 @@ constexpr int kThreeLevelLog = 22;
 
 bool fft4_supported(int64_t n) { return n >= (int64_t(1) << 14) && n <= (int64_t(1) << 24) && (n & (n - 1)) == 0; }
 
-// Real plans for n >= 2^20 (half the bytes per pass; cADMM per iteration at 2^24 / 2^22 / 2^20: 1.10 / 0.33 /
-// 0.148 ms against 1.82 / 0.48 / 0.174 for the complex plans); below, the arrays are L2-resident, the passes
-// latency-bound, and the complex plans' finer row split keeps more CTAs in flight (2^17: 0.097 vs 0.134 ms).
-// CLB_FFT_C2C=0/1 forces either.
+// Real plans for n >= 2^18 (half the bytes per pass; cADMM per iteration at 2^24 / 2^22 / 2^20: 1.10 / 0.33 /
+// 0.119 ms against 1.82 / 0.48 / 0.174 for the complex plans; ISTA at 2^18 / 2^19: 0.075 vs 0.085 ms); below,
+// the complex plans' finer row split keeps more CTAs in flight (2^17: 0.097 vs 0.134 ms).  CLB_FFT_C2C=0/1
+// forces either.
 Fft4Plan fft4_plan(int64_t n) {
   Fft4Plan p;
   p.n = n;
   int Ln = 0;
   while ((int64_t(1) << Ln) < n) ++Ln;
   const char* c2c = std::getenv("CLB_FFT_C2C");
-  p.real = (c2c && *c2c) ? c2c[0] == '0' : Ln >= 20;
+  p.real = (c2c && *c2c) ? c2c[0] == '0' : Ln >= 18;
   p.N = p.real ? n / 2 : n;
   int L = 0;
   while ((int64_t(1) << L) < p.N) ++L;
@@ -715,12 +721,25 @@ void fft4_twiddles(const Fft4Plan& p, std::vector<float2>* tw1, std::vector<floa
 // offsets of the e^{-2 pi i idx / n} factors appended to twA / twB (then t2 after twA's 8192 entries)
 static int64_t twB_len(const Fft4Plan& p) { return std::max<int64_t>(1, p.N / 4096); }
 
+// FINE launches for the L2-resident real plans (N <= 2^19: ISTA at n = 2^20 0.091 vs 0.111 ms per iteration;
+// no gain at N = 2^20); CLB_FFT_FINE=0/1 forces either
+static bool fft4_fine(const Fft4Plan& p) {
+  static const int env = [] {
+    const char* v = std::getenv("CLB_FFT_FINE");
+    return (v && *v) ? atoi(v) : -1;
+  }();
+  return env >= 0 ? env != 0 : p.N <= (int64_t(1) << 19);
+}
 template <int N>
-static size_t cols_smem_t() { return static_cast<size_t>(cols_per_cta(N)) * col_pitch(N) * sizeof(float2); }
+static size_t cols_smem_t(bool fine = false) {
+  return static_cast<size_t>(cols_b(N, fine)) * col_pitch_b(N, cols_b(N, fine)) * sizeof(float2);
+}
 template <int N>
 static size_t rows_smem_t() { return static_cast<size_t>(row_count(N)) * row_pitch(N) * sizeof(float2); }
 template <int N>
-static size_t rows_r2c_smem_t() { return static_cast<size_t>(2 * units_per_cta(N)) * row_pitch(N) * sizeof(float2); }
+static size_t rows_r2c_smem_t(bool fine = false) {
+  return static_cast<size_t>(2 * units_per_cta(N, fine)) * row_pitch(N) * sizeof(float2);
+}
 
 #define CLB_FFT4_SIZES(X) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096) X(8192)
 
@@ -734,9 +753,15 @@ void fft4_init_attributes() {
     cudaFuncSetAttribute(k_cols_inv<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem_t<N>()); \
     cudaFuncSetAttribute(k_cols_fwd<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem_t<N>());  \
     cudaFuncSetAttribute(k_cols_inv<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem_t<N>());  \
+    cudaFuncSetAttribute(k_cols_fwd<N, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,                 \
+                         (int)cols_smem_t<N>(true));                                                             \
+    cudaFuncSetAttribute(k_cols_inv<N, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,                 \
+                         (int)cols_smem_t<N>(true));                                                             \
   }                                                                                                             \
   cudaFuncSetAttribute(k_rows<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem_t<N>());         \
-  cudaFuncSetAttribute(k_rows_r2c<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_r2c_smem_t<N>());
+  cudaFuncSetAttribute(k_rows_r2c<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_r2c_smem_t<N>());   \
+  cudaFuncSetAttribute(k_rows_r2c<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,                       \
+                       (int)rows_r2c_smem_t<N>(true));
   CLB_FFT4_SIZES(CLB_ATTR)
 #undef CLB_ATTR
   cudaFuncSetAttribute(k_mid<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem_t<128>());
@@ -749,7 +774,9 @@ void launch_fft4_cols_fwd(const Fft4Plan& p, const float* u, float2* T, const fl
   switch (p.N1) {
 #define CLB_CASE(N)                                                                                        \
   case N:                                                                                                  \
-    if (p.real) k_cols_fwd<N, true><<<p.N2 / cols_per_cta(N), kThr, cols_smem_t<N>(), st>>>(u, T, p.N2, tw1); \
+    if (p.real && fft4_fine(p))                                                                            \
+      k_cols_fwd<N, true, true><<<p.N2 / cols_b(N, true), kThr, cols_smem_t<N>(true), st>>>(u, T, p.N2, tw1); \
+    else if (p.real) k_cols_fwd<N, true><<<p.N2 / cols_per_cta(N), kThr, cols_smem_t<N>(), st>>>(u, T, p.N2, tw1); \
     else k_cols_fwd<N, false><<<p.N2 / cols_per_cta(N), kThr, cols_smem_t<N>(), st>>>(u, T, p.N2, tw1);      \
     break;
     CLB_FFT4_SIZES(CLB_CASE)
@@ -778,7 +805,12 @@ void launch_fft4_rows(const Fft4Plan& p, float2* T, const float2* H, bool conj_h
   switch (R) {
 #define CLB_CASE(N)                                                                                            \
   case N:                                                                                                      \
-    if (p.real)                                                                                                \
+    if (p.real && fft4_fine(p))                                                                                \
+      k_rows_r2c<N, true><<<(kmul / 2 + units_per_cta(N, true)) / units_per_cta(N, true), kThr,                \
+                            rows_r2c_smem_t<N>(true), st>>>(                                                    \
+          T, reinterpret_cast<const float4*>(H), conj_h ? 1 : 0, p.N1, A, rowmod, mult, twR, twA, twB, twCA,   \
+          twCB, twA + 8192);                                                                                   \
+    else if (p.real)                                                                                           \
       k_rows_r2c<N><<<(kmul / 2 + units_per_cta(N)) / units_per_cta(N), kThr, rows_r2c_smem_t<N>(), st>>>(     \
           T, reinterpret_cast<const float4*>(H), conj_h ? 1 : 0, p.N1, A, rowmod, mult, twR, twA, twB, twCA,   \
           twCB, twA + 8192);                                                                                   \
@@ -801,7 +833,10 @@ void launch_fft4_cols_inv(const Fft4Plan& p, const float2* T, const Fft4Out& o, 
   switch (p.N1) {
 #define CLB_CASE(N)                                                                                        \
   case N:                                                                                                  \
-    if (p.real) k_cols_inv<N, true><<<p.N2 / cols_per_cta(N), kThr, cols_smem_t<N>(), st>>>(T, o, p.N2, tw1, inv_n); \
+    if (p.real && fft4_fine(p))                                                                            \
+      k_cols_inv<N, true, true><<<p.N2 / cols_b(N, true), kThr, cols_smem_t<N>(true), st>>>(T, o, p.N2, tw1,  \
+                                                                                             inv_n);         \
+    else if (p.real) k_cols_inv<N, true><<<p.N2 / cols_per_cta(N), kThr, cols_smem_t<N>(), st>>>(T, o, p.N2, tw1, inv_n); \
     else k_cols_inv<N, false><<<p.N2 / cols_per_cta(N), kThr, cols_smem_t<N>(), st>>>(T, o, p.N2, tw1, inv_n);      \
     break;
     CLB_FFT4_SIZES(CLB_CASE)

@@ -239,3 +239,38 @@ def test_in_graph_phase_timing(kind, n):
         assert np.array_equal(g.get(field), ref.get(field))
     else:  # profiled small solves run the multi-kernel step instead of the persistent launch
         assert rel(g.get(field), ref.get(field)) <= 1e-5
+
+
+# ------------------------------------------------------------- time to recovery at C3 (the bench's line)
+RECOVERY = os.path.join(ROOT, "tests", "golden", "c3_recovery.npz")
+
+
+@pytest.mark.parametrize("kind,use_fft", [("ista", False), ("ista", True), ("cadmm", False), ("cadmm", True)])
+def test_c3_time_to_recovery_matches_oracle(kind, use_fft, c3):
+    """ista_run / cadmm_run(target_mse = 1e-4, check_every = 10, truth = x*) at BASELINE config 3 -- the bench's
+    time-to-recovery line -- against the oracle's own run (tests/golden/c3_recovery.npz,
+    tests/golden/make_recovery_fixture.py): the stop rule fires at the same check, the MSE trace agrees check by
+    check, and the final iterate matches (support flips only at the threshold, sampled rel l2 <= 1e-4)."""
+    import hashlib
+    rf = dict(np.load(RECOVERY))
+    assert hashlib.sha256(c3.y.tobytes()).digest() == rf["y_sha256"].tobytes()
+    run = cl.ista_run if kind == "ista" else cl.cadmm_run
+    rep = run(c3.y, op_of(c3), cl.SolverConfig(target_mse=1e-4, check_every=10, max_iter=20000, use_fft=use_fft),
+              truth=c3.x_true)
+    want_it = int(rf[f"{kind}_iterations"])
+    trace = np.array([(t.iteration, t.value) for t in rep.mse_trace]) if rep.mse_trace else np.zeros((0, 2))
+    wt = rf[f"{kind}_trace"]
+    k = min(len(trace), len(wt))
+    e_tr = float(np.max(np.abs(trace[:k, 1] - wt[:k, 1]) / wt[:k, 1]))
+    x = np.asarray(rep.final_x)
+    e_x = rel(x[rf["sample_pos"]], rf[f"{kind}_sample"])
+    want_nz = np.unpackbits(rf[f"{kind}_support_bits"])[:len(x)].astype(bool)
+    flips = int(np.count_nonzero((x != 0) != want_nz))
+    print(f"C3 {kind} {'fft' if use_fft else 'direct'}: {rep.iterations} iterations (oracle {want_it}), final MSE "
+          f"{rep.final_metric:.6e} (oracle {float(rf[f'{kind}_final_mse']):.6e}), MSE trace max rel diff {e_tr:.2e} "
+          f"over {k} checks, final x sampled rel l2 {e_x:.2e}, {flips} support flips")
+    assert rep.reached_target == bool(rf[f"{kind}_reached"])
+    assert rep.iterations == want_it
+    assert np.array_equal(trace[:k, 0], wt[:k, 0]) and len(trace) == len(wt)
+    assert e_tr <= 1e-4 and e_x <= REL_TOL
+    assert flips <= 1e-5 * len(x)  # threshold-margin flips only (each entry sits at fp32 resolution of g)
