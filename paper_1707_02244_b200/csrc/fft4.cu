@@ -416,17 +416,24 @@ __global__ void __launch_bounds__(kThr, 4) k_mid(float2* __restrict__ T, int N1,
 //   Fft4Out::kResidual r[t] = y[t] - Re / n and u[j] = r[t] at the rows (P^T r kept dense)
 //   Fft4Out::kIstaStep delta[j] = Re / n, x[j] = eta(x[j] + tau delta[j])  (unchecked iterations)
 //   Fft4Out::kBeta     beta[j] = rho Re / n + sigma (z[j] - nu[j])
-__device__ __forceinline__ void emit_out(const Fft4Out& o, int64_t j, float v) {
-  if (j >= o.n_valid) return;
+// Writes output j of the product (value v) as o.mode says; returns the vector the mode produces at j (the
+// next product's input when k_cols_inv_fwd chains two products): the product, beta, the new x, or P^T r.
+__device__ __forceinline__ float emit_out(const Fft4Out& o, int64_t j, float v) {
+  if (j >= o.n_valid) return 0.f;  // the padded engine's convolution tail: zero input
   if (o.mode == Fft4Out::kProduct) {
     o.out[j] = v;
+    return v;
   } else if (o.mode == Fft4Out::kBeta) {  // parallel.hpp:186-187
-    o.out[j] = __fadd_rn(__fmul_rn(o.rho, v), __fmul_rn(o.sigma, __fsub_rn(o.z[j], o.nu[j])));
+    const float b = __fadd_rn(__fmul_rn(o.rho, v), __fmul_rn(o.sigma, __fsub_rn(o.z[j], o.nu[j])));
+    o.out[j] = b;
+    return b;
   } else if (o.mode == Fft4Out::kIstaStep) {
     const float xo = o.x[j];
     const float xn = __fadd_rn(xo, __fmul_rn(o.tau, v));  // parallel.hpp:269-271
-    o.x[j] = xn > o.thr ? xn - o.thr : (xn < -o.thr ? xn + o.thr : 0.f);
+    const float xs = xn > o.thr ? xn - o.thr : (xn < -o.thr ? xn + o.thr : 0.f);
+    o.x[j] = xs;
     o.out[j] = v;
+    return xs;
   } else {
     const int t = __ldg(o.rowid + j);
     if (t >= 0) {
@@ -436,8 +443,10 @@ __device__ __forceinline__ void emit_out(const Fft4Out& o, int64_t j, float v) {
         const float rv = __ldg(o.y + t) - v;
         o.out[t] = rv;
         o.u[j] = rv;
+        return rv;
       }
     }
+    return 0.f;
   }
 }
 // REAL: element j of the inverse holds y[2j] + i y[2j+1]; else Re = y[j].
@@ -465,6 +474,44 @@ __global__ void __launch_bounds__(kThr, N1 <= 256 ? 4 : 1) k_cols_inv(const floa
     } else {
       emit_out(o, j, s.x * inv_n);
     }
+  }
+}
+
+// Two chained products: the inverse columns of the first with its consumer (`o`), then -- on the vector that
+// consumer produced, still in shared memory -- the forward columns of the next product, in place on T.
+// Every CTA owns whole columns, so the next product's column FFT needs nothing from other CTAs (ISTA: the
+// residual's P^T r feeds the gradient; cADMM: beta feeds B beta, and x = B beta feeds C x).
+template <int N1, bool REAL, bool FINE = false>
+__global__ void __launch_bounds__(kThr, N1 <= 256 ? 4 : 1) k_cols_inv_fwd(float2* __restrict__ T, Fft4Out o, int N2,
+                                                       const float2* __restrict__ tw1, float inv_n) {
+  extern __shared__ float2 sm[];
+  constexpr int B = cols_b(N1, FINE), P = col_pitch_b(N1, B), cnt = B * N1;
+  const int c0 = blockIdx.x * B;
+#pragma unroll
+  for (int e = threadIdx.x; e < cnt; e += kThr) {
+    const int i = e / B, w = e - i * B;
+    sm[w * P + pad16(i)] = T[static_cast<int64_t>(i) * N2 + c0 + w];
+  }
+  __syncthreads();
+  dit_from<N1, N1, B>(sm, P, tw1);
+#pragma unroll
+  for (int e = threadIdx.x; e < cnt; e += kThr) {
+    const int i = e / B, w = e - i * B;
+    const int64_t j = static_cast<int64_t>(i) * N2 + c0 + w;
+    float2& s = sm[w * P + pad16(i)];
+    if (REAL) {
+      const float a = emit_out(o, 2 * j, s.x * inv_n), b = emit_out(o, 2 * j + 1, s.y * inv_n);
+      s = make_float2(a, b);
+    } else {
+      s = make_float2(emit_out(o, j, s.x * inv_n), 0.f);
+    }
+  }
+  __syncthreads();
+  dif_from<N1, N1, B>(sm, P, tw1);
+#pragma unroll
+  for (int e = threadIdx.x; e < cnt; e += kThr) {
+    const int i = e / B, w = e - i * B;
+    T[static_cast<int64_t>(i) * N2 + c0 + w] = sm[w * P + pad16(i)];
   }
 }
 
@@ -755,6 +802,12 @@ void fft4_init_attributes() {
     cudaFuncSetAttribute(k_cols_inv<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem_t<N>());  \
     cudaFuncSetAttribute(k_cols_fwd<N, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,                 \
                          (int)cols_smem_t<N>(true));                                                             \
+    cudaFuncSetAttribute(k_cols_inv_fwd<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,                  \
+                         (int)cols_smem_t<N>());                                                                 \
+    cudaFuncSetAttribute(k_cols_inv_fwd<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,                   \
+                         (int)cols_smem_t<N>());                                                                 \
+    cudaFuncSetAttribute(k_cols_inv_fwd<N, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,             \
+                         (int)cols_smem_t<N>(true));                                                             \
     cudaFuncSetAttribute(k_cols_inv<N, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,                 \
                          (int)cols_smem_t<N>(true));                                                             \
   }                                                                                                             \
@@ -838,6 +891,23 @@ void launch_fft4_cols_inv(const Fft4Plan& p, const float2* T, const Fft4Out& o, 
                                                                                              inv_n);         \
     else if (p.real) k_cols_inv<N, true><<<p.N2 / cols_per_cta(N), kThr, cols_smem_t<N>(), st>>>(T, o, p.N2, tw1, inv_n); \
     else k_cols_inv<N, false><<<p.N2 / cols_per_cta(N), kThr, cols_smem_t<N>(), st>>>(T, o, p.N2, tw1, inv_n);      \
+    break;
+    CLB_FFT4_SIZES(CLB_CASE)
+#undef CLB_CASE
+  }
+}
+void launch_fft4_cols_inv_fwd(const Fft4Plan& p, float2* T, const Fft4Out& o, const float2* tw1, cudaStream_t st) {
+  const float inv_n = p.real ? 1.0f / (4.0f * static_cast<float>(p.N)) : 1.0f / static_cast<float>(p.n);
+  switch (p.N1) {
+#define CLB_CASE(N)                                                                                          \
+  case N:                                                                                                    \
+    if (p.real && fft4_fine(p))                                                                              \
+      k_cols_inv_fwd<N, true, true><<<p.N2 / cols_b(N, true), kThr, cols_smem_t<N>(true), st>>>(T, o, p.N2, tw1, \
+                                                                                                 inv_n);     \
+    else if (p.real)                                                                                         \
+      k_cols_inv_fwd<N, true><<<p.N2 / cols_per_cta(N), kThr, cols_smem_t<N>(), st>>>(T, o, p.N2, tw1, inv_n);   \
+    else                                                                                                     \
+      k_cols_inv_fwd<N, false><<<p.N2 / cols_per_cta(N), kThr, cols_smem_t<N>(), st>>>(T, o, p.N2, tw1, inv_n);  \
     break;
     CLB_FFT4_SIZES(CLB_CASE)
 #undef CLB_CASE

@@ -47,6 +47,9 @@ struct Fft4Out {
 };
 // T -> column DIT inverse FFTs, then `o`.
 void launch_fft4_cols_inv(const Fft4Plan& p, const float2* T, const Fft4Out& o, const float2* tw1, cudaStream_t st);
+// T -> column DIT inverse FFTs, then `o`, then -- on the vector `o` produces (the residual's P^T r, beta, or
+// the product itself) -- the next product's column DIF FFTs, in place on T (two chained products, one pass).
+void launch_fft4_cols_inv_fwd(const Fft4Plan& p, float2* T, const Fft4Out& o, const float2* tw1, cudaStream_t st);
 // natural-order fp64 spectrum (n entries) / s -> the engine's permuted fp32 order (N entries; real plans pack
 // H[0] and H[n / 2] into entry 0)
 void launch_fft4_perm_spectrum(const Fft4Plan& p, const double2* spec, double s, float2* out, cudaStream_t st);

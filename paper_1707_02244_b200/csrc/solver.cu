@@ -932,11 +932,17 @@ struct Solver {
     return fft_run(Xm, other, nfft, true, st);
   }
   // Four-step engine: one product = cols_fwd -> rows (twiddle, FFT, x H~, IFFT, twiddle) -> cols_inv.
-  void fft4_product(const float* u, const float2* H, bool conj_h, const Fft4Out& o) {
+  // Two chained products: the first's inverse columns (with its consumer `o1`) and the second's forward
+  // columns run as one pass over T (launch_fft4_cols_inv_fwd); o1 must produce the second's input.
+  void fft4_product_chain_begin(const float* u, const float2* H, bool conj_h) {
     launch_fft4_cols_fwd(f4, u, F0.p, tw1.p, st);
     launch_fft4_rows(f4, F0.p, H, conj_h, tw2.p, twA.p, twB.p, st);
-    launch_fft4_cols_inv(f4, F0.p, o, tw1.p, st);
   }
+  void fft4_product_chain_next(const Fft4Out& o1, const float2* H2, bool conj_h2) {
+    launch_fft4_cols_inv_fwd(f4, F0.p, o1, tw1.p, st);
+    launch_fft4_rows(f4, F0.p, H2, conj_h2, tw2.p, twA.p, twB.p, st);
+  }
+  void fft4_product_chain_end(const Fft4Out& o) { launch_fft4_cols_inv(f4, F0.p, o, tw1.p, st); }
   Fft4Out product_to(float* out) const {
     Fft4Out o;
     o.out = out;
@@ -952,7 +958,9 @@ struct Solver {
     res.rowid = rowid.p;
     res.y = y.p;
     res.u = ud.p;
-    fft4_product(x.p, chatp.p, true, res);
+    // C x, its residual epilogue chained into the forward columns of C^T P^T r (one pass)
+    fft4_product_chain_begin(x.p, chatp.p, true);
+    fft4_product_chain_next(res, chatp.p, false);
     mark(1);
     mark(2);
     if (!want) {  // unchecked iteration: the x update fused into the inverse pass
@@ -963,13 +971,13 @@ struct Solver {
       up.x = x.p;
       up.tau = static_cast<float>(tau);
       up.thr = static_cast<float>(thr);
-      fft4_product(ud.p, chatp.p, false, up);
+      fft4_product_chain_end(up);
       mark(3);
       mark(4);
       nphase = 4;
       return;
     }
-    fft4_product(ud.p, chatp.p, false, product_to(partial.p));  // C^T P^T r
+    fft4_product_chain_end(product_to(partial.p));  // C^T P^T r
     mark(3);
     EpiArgs b = base_args(want);
     b.splits = 1;
@@ -991,13 +999,15 @@ struct Solver {
     bo.nu = nu.p;
     bo.rho = static_cast<float>(cfg.rho);
     bo.sigma = static_cast<float>(cfg.sigma);
-    fft4_product(v.p, chatp.p, false, bo);
+    // C^T v -> beta -> B beta -> x -> C x: each epilogue chained into the next product's forward columns
+    fft4_product_chain_begin(v.p, chatp.p, false);
+    fft4_product_chain_next(bo, bhatp.p, true);
     mark(1);
     mark(2);
-    fft4_product(beta.p, bhatp.p, true, product_to(x.p));      // x = B beta
+    fft4_product_chain_next(product_to(x.p), chatp.p, true);  // x = B beta
     mark(3);
     mark(4);
-    fft4_product(x.p, chatp.p, true, product_to(partial.p));      // C x
+    fft4_product_chain_end(product_to(partial.p));  // C x
     mark(5);
     EpiArgs d2 = base_args(want);
     d2.splits = 1;
