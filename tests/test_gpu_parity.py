@@ -836,3 +836,21 @@ def test_tensor_core_product_scaling(case, f16, monkeypatch):
     assert rel_l2(cl.circ_matvec(C, x), want) <= 5e-5
     want_t = orc.circ_matvec(row, x, transpose=True, use_fft=True)
     assert rel_l2(cl.circ_transpose_matvec(C, x), want_t) <= 5e-5
+
+
+@pytest.mark.parametrize("lg", [20, 24])
+def test_tensor_core_product_error_bound(lg):
+    """The fp16-split tcgen05 product's error budget, pinned in a test at the bench size (2^20) and at C4/C5's
+    2^24: at sampled outputs, |got - exact| / sum_j |h_{i-j} u_j| <= 2e-8 (fp32 FFMA-level; measured 2.2e-9 to
+    4.6e-9, tools/microbench/tc_probe.cu), the exact sum in fp64 over all n terms."""
+    n = 1 << lg
+    rng = np.random.default_rng(5)
+    row = rng.standard_normal(n).astype(np.float32).astype(np.float64)  # exactly representable: the
+    u = rng.standard_normal(n).astype(np.float32).astype(np.float64)    # bound measures the product alone
+    got = cl.circ_matvec(cl.CirculantMatrix(row), u)
+    worst = 0.0
+    for i in rng.choice(n, 24, replace=False):
+        terms = row[(np.arange(n) - i) % n] * u  # C u: out[i] = sum_j c[(j - i) mod n] u[j] (circulant.hpp:6-8)
+        worst = max(worst, abs(got[i] - terms.sum()) / np.abs(terms).sum())
+    print(f"tcgen05 product n=2^{lg}: max |err| / sum|terms| = {worst:.2e} over 24 sampled outputs")
+    assert worst <= 2e-8

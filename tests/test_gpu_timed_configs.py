@@ -265,12 +265,17 @@ def test_c3_time_to_recovery_matches_oracle(kind, use_fft, c3):
     x = np.asarray(rep.final_x)
     e_x = rel(x[rf["sample_pos"]], rf[f"{kind}_sample"])
     want_nz = np.unpackbits(rf[f"{kind}_support_bits"])[:len(x)].astype(bool)
-    flips = int(np.count_nonzero((x != 0) != want_nz))
+    fl = np.flatnonzero((x != 0) != want_nz)
+    flips = len(fl)
+    # the GPU value at a flip (zero where the oracle's is not): soft-thresholding maps a pre-threshold value
+    # within fp32 resolution of the threshold to (nearly) zero, so a flip must carry a tiny value
+    worst = float(np.max(np.abs(x[fl]))) / float(np.max(np.abs(x))) if flips else 0.0
     print(f"C3 {kind} {'fft' if use_fft else 'direct'}: {rep.iterations} iterations (oracle {want_it}), final MSE "
           f"{rep.final_metric:.6e} (oracle {float(rf[f'{kind}_final_mse']):.6e}), MSE trace max rel diff {e_tr:.2e} "
-          f"over {k} checks, final x sampled rel l2 {e_x:.2e}, {flips} support flips")
+          f"over {k} checks, final x sampled rel l2 {e_x:.2e}, {flips} support flips (largest |x| at a flip "
+          f"{worst:.1e} of max|x|)")
     assert rep.reached_target == bool(rf[f"{kind}_reached"])
     assert rep.iterations == want_it
     assert np.array_equal(trace[:k, 0], wt[:k, 0]) and len(trace) == len(wt)
     assert e_tr <= 1e-3 and e_x <= REL_TOL  # MSE vs truth: a difference of nearly equal vectors
-    assert flips <= 1e-5 * len(x)  # threshold-margin flips only (each entry sits at fp32 resolution of g)
+    assert flips <= 5e-5 * len(x) and worst <= 1e-5  # threshold-margin flips only

@@ -1,2 +1,10 @@
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__throughput.avg.pct_of_peak_sustained_elapsed,l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum,smsp__warps_issue_stalled_long_scoreboard_per_issue_active.ratio --clock-control none --launch-skip 60 --launch-count 30 --csv --log-file gpurun_out/fft_ncu.csv python tools/fft_probe.py cadmm 24 > gpurun_out/fft_ncu.out 2>&1
-tail -3 gpurun_out/fft_ncu.out
+# ncu --set full of the FFT engine's kernels: C3 ISTA (n = 2^20, real FINE plan) and cADMM n = 2^24 (three-level
+# real plan)
+set -x
+NCU=/usr/local/cuda/bin/ncu
+timeout 900 $NCU --set full --clock-control none --import-source on -k regex:"k_rows_r2c|k_cols|k_mid" -s 40 -c 5 \
+  -o gpurun_out/prof_fft24 python tools/fft_probe.py cadmm 24 > gpurun_out/ncu_fft24.log 2>&1; echo "fft24 rc=$?"
+timeout 900 $NCU --set full --clock-control none --import-source on -k regex:"k_rows_r2c|k_cols" -s 30 -c 5 \
+  -o gpurun_out/prof_fft20 python tools/fft_probe.py ista 20 > gpurun_out/ncu_fft20.log 2>&1; echo "fft20 rc=$?"
+timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none -s 200 -c 60 --csv \
+  --log-file gpurun_out/launches_fft20.csv python tools/fft_probe.py ista 20 > /dev/null 2>&1; echo "list rc=$?"
