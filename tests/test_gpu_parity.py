@@ -841,7 +841,7 @@ def test_tensor_core_product_scaling(case, f16, monkeypatch):
 @pytest.mark.parametrize("lg", [20, 24])
 def test_tensor_core_product_error_bound(lg):
     """The fp16-split tcgen05 product's error budget, pinned in a test at the bench size (2^20) and at C4/C5's
-    2^24: at sampled outputs, |got - exact| / sum_j |h_{i-j} u_j| <= 2e-8 (fp32 FFMA-level; measured 2.2e-9 to
+    2^24: at sampled outputs, |got - exact| / sum_j |c_{j-i} u_j| <= 2e-8 (fp32 FFMA-level; measured 2.2e-9 to
     4.6e-9, tools/microbench/tc_probe.cu), the exact sum in fp64 over all n terms."""
     n = 1 << lg
     rng = np.random.default_rng(5)
