@@ -222,11 +222,14 @@ cl_status cl_solver_attach_comm(cl_solver* s, cl_comm* c);
  * `ndev` solvers, rank r on devices[r].  Transport CL_TRANSPORT_NCCL builds
  * the communicators with ncclCommInitAll and issues every rank's exchange in
  * one NCCL group; CL_TRANSPORT_COPY exchanges slices with peer copies ordered
- * by events (devices may repeat: the 2/4/8-rank data plane on one GPU).  The
+ * by events (devices may repeat: the 2/4/8-rank data plane on one GPU);
+ * CL_TRANSPORT_PEER fuses the exchange into the kernels that produce each
+ * slice (their stores go to every rank's copy; peer access over NVLink, at
+ * most 8 ranks), leaving only event ordering between the phases.  The
  * run loop, stopping rule and report are those of cl_solver_run; get()
  * assembles a vector from the ranks' slices.  ISTA and cADMM (direct
  * engine). */
-typedef enum cl_transport { CL_TRANSPORT_NCCL = 0, CL_TRANSPORT_COPY = 1 } cl_transport;
+typedef enum cl_transport { CL_TRANSPORT_NCCL = 0, CL_TRANSPORT_COPY = 1, CL_TRANSPORT_PEER = 2 } cl_transport;
 typedef struct cl_group cl_group;
 cl_status cl_group_create(int kind, int64_t n, int64_t m, const double* c, const int64_t* omega, const double* y,
                           const cl_config* cfg, const int* devices, int ndev, int transport, cl_group** out);

@@ -753,7 +753,7 @@ RecoveryReport<Scalar> cadmm_run(const Vector<Scalar>& y, const PartialCirculant
 // (ncclCommInitAll over the listed GPUs) or peer copies (Transport::kCopy; devices may repeat).  The
 // iterate equals the unsharded solve's bitwise.  One process per GPU instead: cl_comm_init_rank +
 // cl_solver_attach_comm on a solver handle.
-enum class Transport { kNccl = CL_TRANSPORT_NCCL, kCopy = CL_TRANSPORT_COPY };
+enum class Transport { kNccl = CL_TRANSPORT_NCCL, kCopy = CL_TRANSPORT_COPY, kPeer = CL_TRANSPORT_PEER };
 template <typename Scalar = double>
 class ShardedSolve {
  public:

@@ -734,10 +734,12 @@ def admm_dense_run(y, A: PartialCirculantOperator, cfg: SolverConfig = None, tru
 class ShardedSolve:
     """A sharded ISTA / cADMM solve driven from one process (cl_group_*): rank r on devices[r],
     the slice exchange after every phase inside the library -- NCCL (``transport="nccl"``: ncclCommInitAll,
-    one grouped set of in-place broadcasts per phase) or peer copies (``"copy"``: devices may repeat, e.g.
-    [0, 0, 0, 0] runs the 4-rank data plane on one GPU).  Same iterate as the unsharded solve, bitwise."""
+    one grouped set of in-place broadcasts per phase), peer copies (``"copy"``: devices may repeat, e.g.
+    [0, 0, 0, 0] runs the 4-rank data plane on one GPU), or peer stores fused into the kernels that produce
+    each slice (``"peer"``: no separate exchange; NVLink stores across GPUs, at most 8 ranks).  Same iterate
+    as the unsharded solve, bitwise."""
 
-    TRANSPORTS = {"nccl": 0, "copy": 1}
+    TRANSPORTS = {"nccl": 0, "copy": 1, "peer": 2}
 
     def __init__(self, kind: str, A: PartialCirculantOperator, y, cfg: SolverConfig = None, devices=(0,),
                  transport: str = "nccl"):

@@ -1066,6 +1066,12 @@ __device__ __forceinline__ void block_metrics(double a, double b, double c, doub
   }
 }
 
+// the fused all-gather of the peer-store transport (EpiArgs::peer): the same value at the same index on
+// every other rank (NVLink stores when the ranks sit on different GPUs)
+__device__ __forceinline__ void to_peers(const EpiArgs& a, int64_t i, float v) {
+  for (int p = 0; p < a.npeer; ++p) a.peer[p][i] = v;
+}
+
 __device__ __forceinline__ float sum_partials(const float* __restrict__ p, int splits, int64_t stride, int64_t i) {
   float s = p[i];
   for (int k = 1; k < splits; ++k) s += p[k * stride + i];
@@ -1077,7 +1083,9 @@ __global__ void __launch_bounds__(kThreads) k_residual_reduce(EpiArgs a, int64_t
   for (int64_t t = a.lo + blockIdx.x * (int64_t)kThreads + threadIdx.x; t < a.hi;
        t += (int64_t)gridDim.x * kThreads) {
     const float s = sum_partials(a.partial, static_cast<int>(tiles), a.n, t);
-    a.r[t] = a.y[t] - s;
+    const float rv = a.y[t] - s;
+    a.r[t] = rv;
+    to_peers(a, t, rv);
   }
 }
 
@@ -1086,7 +1094,9 @@ __global__ void __launch_bounds__(kThreads) k_residual_gather(EpiArgs a, const i
   for (int64_t t = a.lo + blockIdx.x * (int64_t)kThreads + threadIdx.x; t < a.hi;
        t += (int64_t)gridDim.x * kThreads) {
     const float s = sum_partials(a.partial, a.splits, a.n, omega[t]);
-    a.r[t] = a.y[t] - s;
+    const float rv = a.y[t] - s;
+    a.r[t] = rv;
+    to_peers(a, t, rv);
   }
 }
 
@@ -1100,6 +1110,7 @@ __global__ void __launch_bounds__(kThreads) k_ista_update(EpiArgs a) {
     const float xn = soft(__fadd_rn(xo, __fmul_rn(a.tau, d)), a.thr);
     a.delta[i] = d;
     a.x[i] = xn;
+    to_peers(a, i, xn);
     if (a.want_metrics) {
       const double dd = (double)xn - (double)xo;
       m0 += dd * dd;
@@ -1118,14 +1129,19 @@ __global__ void __launch_bounds__(kThreads) k_admm_beta(EpiArgs a) {
   for (int64_t i = a.lo + blockIdx.x * (int64_t)kThreads + threadIdx.x; i < a.hi;
        i += (int64_t)gridDim.x * kThreads) {
     const float s = sum_partials(a.partial, a.splits, a.n, i);
-    a.beta[i] = __fadd_rn(__fmul_rn(a.rho, s), __fmul_rn(a.sigma, __fsub_rn(a.z[i], a.nu[i])));
+    const float b = __fadd_rn(__fmul_rn(a.rho, s), __fmul_rn(a.sigma, __fsub_rn(a.z[i], a.nu[i])));
+    a.beta[i] = b;
+    to_peers(a, i, b);
   }
 }
 
 __global__ void __launch_bounds__(kThreads) k_admm_x(EpiArgs a) {
   for (int64_t i = a.lo + blockIdx.x * (int64_t)kThreads + threadIdx.x; i < a.hi;
-       i += (int64_t)gridDim.x * kThreads)
-    a.x[i] = sum_partials(a.partial, a.splits, a.n, i);
+       i += (int64_t)gridDim.x * kThreads) {
+    const float xv = sum_partials(a.partial, a.splits, a.n, i);
+    a.x[i] = xv;
+    to_peers(a, i, xv);
+  }
 }
 
 __global__ void __launch_bounds__(kThreads) k_admm_duals(EpiArgs a) {
@@ -1141,7 +1157,9 @@ __global__ void __launch_bounds__(kThreads) k_admm_duals(EpiArgs a) {
     a.z[i] = zn;
     a.mu[i] = mun;
     a.nu[i] = __fadd_rn(nui, __fmul_rn(a.tau2, __fsub_rn(xi, zn)));
-    a.v[i] = __fadd_rn(vn, mun);
+    const float vv = __fadd_rn(vn, mun);
+    a.v[i] = vv;
+    to_peers(a, i, vv);
     if (a.want_metrics) {
       const double dd = (double)zn - (double)zo;
       m0 += dd * dd;

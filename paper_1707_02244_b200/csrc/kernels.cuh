@@ -102,6 +102,12 @@ struct EpiArgs {
   const float* truth = nullptr;
   double* blk = nullptr;           // [kEpiBlocks][4]: sum d_iter^2, sum d_truth^2, nonfinite, unused
   int want_metrics = 0;
+  // sharded solves with the peer-store transport: the vector this epilogue produces (r, x, beta or v) is
+  // also stored, at the same indices, into every other rank's copy of it (device pointers on the same or a
+  // peer-accessible GPU) -- the all-gather fused into the producing kernel
+  static constexpr int kMaxPeers = 7;
+  float* peer[kMaxPeers] = {};
+  int npeer = 0;
 };
 
 // partial[split][i] for the plan's shard tiles (dense u).  plan from make_plan(n, kRDense).

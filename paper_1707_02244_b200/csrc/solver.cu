@@ -821,6 +821,13 @@ struct Solver {
     else CU(cudaEventRecord(ev[i], st));
   }
 
+  // peer-store transport (Group kPeer): per phase, the other ranks' copies of the vector the phase produces
+  float* peer_out[3][EpiArgs::kMaxPeers] = {};
+  int npeer = 0;
+  void set_peers(EpiArgs& a, int ph) const {
+    a.npeer = npeer;
+    for (int p = 0; p < npeer; ++p) a.peer[p] = peer_out[ph][p];
+  }
   EpiArgs base_args(int want) {
     EpiArgs a;
     a.partial = partial.p;
@@ -848,6 +855,7 @@ struct Solver {
       a.hi = row_hi;
       a.y = y.p;
       a.r = r.p;
+      set_peers(a, 0);
       launch_ista_residual_gather(a, omega32.p, st);
       mark(2);
       return;
@@ -861,6 +869,7 @@ struct Solver {
     a.hi = row_hi;
     a.y = y.p;
     a.r = r.p;
+    set_peers(a, 0);
     launch_ista_residual_reduce(a, rplan.tiles, st);
     mark(2);
   }
@@ -877,6 +886,7 @@ struct Solver {
     a.delta = delta.p;
     a.tau = static_cast<float>(tau);
     a.thr = static_cast<float>(thr);
+    set_peers(a, 1);
     launch_ista_update(a, st);
     mark(4);
     nphase = 4;
@@ -891,6 +901,7 @@ struct Solver {
     a.nu = nu.p;
     a.rho = static_cast<float>(cfg.rho);
     a.sigma = static_cast<float>(cfg.sigma);
+    set_peers(a, 0);
     launch_admm_beta(a, st);
     mark(2);
   }
@@ -899,6 +910,7 @@ struct Solver {
     mark(3);
     EpiArgs a = base_args(0);
     a.x = x.p;
+    set_peers(a, 1);
     launch_admm_x(a, st);
     mark(4);
   }
@@ -917,6 +929,7 @@ struct Solver {
     a.tau1 = static_cast<float>(cfg.tau1);
     a.tau2 = static_cast<float>(cfg.tau2);
     a.thr = static_cast<float>(thr);
+    set_peers(a, 2);
     launch_admm_duals(a, st);
     mark(6);
     nphase = 6;
@@ -1598,9 +1611,12 @@ void run_loop(S& s, const cl_config& cfg, cl_report* rep, double* final_x, int64
 //  * kNccl: one NCCL communicator per device (ncclCommInitAll), the ranks' in-place broadcasts issued
 //    in one NCCL group (a single thread drives every device);
 //  * kCopy: device-to-device copies ordered by events (ranks may share a device; the exchange and phase
-//    logic of the NCCL path without NCCL -- the one-GPU test of the 2/4/8-rank data plane).
+//    logic of the NCCL path without NCCL -- the one-GPU test of the 2/4/8-rank data plane);
+//  * kPeer: no separate exchange at all -- each phase's epilogue kernel stores its slice straight into every
+//    rank's copy of the vector (EpiArgs::peer; NVLink peer stores across GPUs), and the ranks' streams only
+//    wait for each other's phase before the next one (the all-gather fused into the producing kernel).
 struct Group {
-  enum Transport { kNccl = CL_TRANSPORT_NCCL, kCopy = CL_TRANSPORT_COPY };
+  enum Transport { kNccl = CL_TRANSPORT_NCCL, kCopy = CL_TRANSPORT_COPY, kPeer = CL_TRANSPORT_PEER };
   int kind = 0;
   int64_t n = 0, m = 0;
   bool has_truth = false;
@@ -1636,6 +1652,15 @@ struct Group {
     for (int r = 0; r < world(); ++r) {
       CU(cudaSetDevice(ranks[static_cast<size_t>(r)]->device));
       CU(cudaEventRecord(done[static_cast<size_t>(r)], ranks[static_cast<size_t>(r)]->st));
+    }
+    if (transport == kPeer) {  // the slices are already in place: order the next phase after every rank's
+      for (int q = 0; q < world(); ++q) {
+        Solver& dst = *ranks[static_cast<size_t>(q)];
+        CU(cudaSetDevice(dst.device));
+        for (int r = 0; r < world(); ++r)
+          if (r != q) CU(cudaStreamWaitEvent(dst.st, done[static_cast<size_t>(r)], 0));
+      }
+      return;
     }
     for (int q = 0; q < world(); ++q) {
       Solver& dst = *ranks[static_cast<size_t>(q)];
@@ -2361,8 +2386,10 @@ cl_status cl_group_create(int kind, int64_t n, int64_t m, const double* c, const
   *out = nullptr;
   if (ndev < 1 || !devices) raise(CL_EPARAM, "cl_group_create: need at least one device");
   if (kind != CL_KIND_ISTA && kind != CL_KIND_CADMM) raise(CL_EPARAM, "cl_group_create: ISTA or cADMM only");
-  if (transport != CL_TRANSPORT_NCCL && transport != CL_TRANSPORT_COPY)
+  if (transport != CL_TRANSPORT_NCCL && transport != CL_TRANSPORT_COPY && transport != CL_TRANSPORT_PEER)
     raise(CL_EPARAM, "cl_group_create: unknown transport");
+  if (transport == CL_TRANSPORT_PEER && ndev > EpiArgs::kMaxPeers + 1)
+    raise(CL_EPARAM, "cl_group_create: the peer-store transport takes at most 8 ranks");
   if (n < 1) raise(CL_EDIM, "cl_solver_create: n must be >= 1");
   if (m < 0 || m > n) raise(CL_EDIM, "cl_solver_create: need 0 <= m <= n");
   const auto t0 = std::chrono::steady_clock::now();
@@ -2391,11 +2418,35 @@ cl_status cl_group_create(int kind, int64_t n, int64_t m, const double* c, const
     }
     g->ranks.push_back(std::move(s));
   }
-  if (g->transport == Group::kCopy) {
+  if (g->transport == Group::kCopy || g->transport == Group::kPeer) {
     g->done.resize(static_cast<size_t>(ndev));
     for (int r = 0; r < ndev; ++r) {
       CU(cudaSetDevice(devices[r]));
       CU(cudaEventCreateWithFlags(&g->done[static_cast<size_t>(r)], cudaEventDisableTiming));
+    }
+  }
+  if (g->transport == Group::kPeer) {
+    // every pair of distinct devices maps the other's memory (NVLink), then each rank gets, per phase, the
+    // other ranks' copies of the vector that phase produces
+    for (int a = 0; a < ndev; ++a)
+      for (int b = 0; b < ndev; ++b) {
+        if (devices[a] == devices[b]) continue;
+        int ok = 0;
+        CU(cudaDeviceCanAccessPeer(&ok, devices[a], devices[b]));
+        if (!ok) raise(CL_EPARAM, "cl_group_create: the peer-store transport needs peer access between the devices");
+        CU(cudaSetDevice(devices[a]));
+        const cudaError_t e = cudaDeviceEnablePeerAccess(devices[b], 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CU(e);
+        cudaGetLastError();  // clear a benign "already enabled"
+      }
+    for (int r = 0; r < ndev; ++r) {
+      Solver& s = *g->ranks[static_cast<size_t>(r)];
+      s.npeer = ndev - 1;
+      for (int ph = 0; ph < s.phase_count(); ++ph) {
+        int p = 0;
+        for (int q = 0; q < ndev; ++q)
+          if (q != r) s.peer_out[ph][p++] = g->ranks[static_cast<size_t>(q)]->phase_buffer(ph);
+      }
     }
   }
   g->setup_seconds = seconds_since(t0);

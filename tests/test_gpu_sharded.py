@@ -26,17 +26,21 @@ CASES = [("ista", 1 << 18), ("ista", 1 << 16), ("cadmm", 1 << 16), ("cadmm", 1 <
 
 @pytest.mark.parametrize("kind,n", CASES)
 @pytest.mark.parametrize("world", [2, 4, 8])
-def test_group_copy_transport_bitwise(kind, n, world):
+@pytest.mark.parametrize("transport", ["copy", "peer"])
+def test_group_transport_bitwise(kind, n, world, transport):
+    """World 2/4/8 on one GPU through the library's data plane: peer copies after each phase ("copy"), or the
+    exchange fused into the producing epilogue kernels as stores into every rank's copy ("peer"); the iterate
+    and every state vector equal the unsharded solve's, bitwise."""
     p = orc.make_problem(n, n // 4, n // 256, 5)
     setup = cl.ista_setup if kind == "ista" else cl.cadmm_setup
     solo = setup(op_of(p), p.y)
     solo.step(4)
-    g = cl.ShardedSolve(kind, op_of(p), p.y, devices=[0] * world, transport="copy")
+    g = cl.ShardedSolve(kind, op_of(p), p.y, devices=[0] * world, transport=transport)
     g.step(4)
     fields = ("x", "r", "delta") if kind == "ista" else ("x", "z", "nu", "mu", "v", "beta")
     for f in fields:
         assert np.array_equal(g.get(f), solo.get(f)), f
-    assert g.info() == {"world": world, "t": 4, "transport": 1}
+    assert g.info() == {"world": world, "t": 4, "transport": cl.ShardedSolve.TRANSPORTS[transport]}
 
 
 @pytest.mark.parametrize("kind", ["ista", "cadmm"])
@@ -46,7 +50,7 @@ def test_group_run_loop_matches_unsharded(kind):
     cfg = cl.SolverConfig(max_iter=40, check_every=10, target_mse=1e-30)
     run = cl.ista_run if kind == "ista" else cl.cadmm_run
     ref = run(p.y, op_of(p), cfg, truth=p.x_true)
-    for world, transport in ((4, "copy"), (1, "nccl")):
+    for world, transport in ((4, "copy"), (3, "peer"), (1, "nccl")):
         rep = cl.ShardedSolve(kind, op_of(p), p.y, cfg, devices=[0] * world, transport=transport).run(truth=p.x_true)
         assert rep.iterations == ref.iterations == 40
         assert np.array_equal(rep.final_x, ref.final_x)

@@ -46,9 +46,11 @@ rep = cl.admm_dense_run(p.measurements, p.op, cl.SolverConfig(max_iter=4, check_
 print(f"dense admm n=200: {rep.iterations} iterations, metric {rep.final_metric:.3e}", flush=True)
 p = cl.make_problem(1 << 16, 1 << 14, 256, 5)
 for kind in ("ista", "cadmm"):
-    g = cl.ShardedSolve(kind, p.op, p.measurements, cl.SolverConfig(max_iter=2, check_every=2), devices=[0, 0],
-                        transport="copy")
-    print(f"sharded {kind} 2 ranks: {g.run(truth=p.signal.values).iterations} iterations", flush=True)
+    for transport in ("copy", "peer"):
+        g = cl.ShardedSolve(kind, p.op, p.measurements, cl.SolverConfig(max_iter=2, check_every=2), devices=[0, 0],
+                            transport=transport)
+        print(f"sharded {kind} 2 ranks ({transport}): {g.run(truth=p.signal.values).iterations} iterations",
+              flush=True)
 
 if "--large" in sys.argv:  # the three-level FFT plan (n >= 2^22): memcheck only (slow under racecheck)
     p = cl.make_problem(1 << 22, 1 << 20, 1 << 14, 6)
