@@ -1077,6 +1077,23 @@ __device__ __forceinline__ float sum_partials(const float* __restrict__ p, int s
   for (int k = 1; k < splits; ++k) s += p[k * stride + i];
   return s;
 }
+// the same ascending sum with the loads of 8 splits issued together ahead of their adds: for the residual's
+// gather at the rows Omega (scattered 4-byte loads, latency-bound: 0.031 vs 0.042 ms at C3); the contiguous
+// epilogues keep the plain loop (batched: 0.17 vs 0.105 ms for the ISTA update)
+__device__ __forceinline__ float sum_partials_batched(const float* __restrict__ p, int splits, int64_t stride,
+                                                      int64_t i) {
+  float s = p[i];
+  int k = 1;
+  for (; k + 8 <= splits; k += 8) {
+    float v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = __ldcs(p + (k + q) * stride + i);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += v[q];
+  }
+  for (; k < splits; ++k) s += __ldcs(p + k * stride + i);
+  return s;
+}
 
 __global__ void __launch_bounds__(kThreads) k_residual_reduce(EpiArgs a, int64_t tiles) {
   // r[t] = y[t] - sum_tile partial[tile][t]   (cpista residual, parallel.hpp:252)
@@ -1093,7 +1110,7 @@ __global__ void __launch_bounds__(kThreads) k_residual_gather(EpiArgs a, const i
   // r[t] = y[t] - (C x)[omega[t]], C x from the dense product's split partials (a.n = n)
   for (int64_t t = a.lo + blockIdx.x * (int64_t)kThreads + threadIdx.x; t < a.hi;
        t += (int64_t)gridDim.x * kThreads) {
-    const float s = sum_partials(a.partial, a.splits, a.n, omega[t]);
+    const float s = sum_partials_batched(a.partial, a.splits, a.n, omega[t]);
     const float rv = a.y[t] - s;
     a.r[t] = rv;
     to_peers(a, t, rv);
