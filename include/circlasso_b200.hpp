@@ -27,6 +27,11 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <functional>
+#include <map>
+#include <optional>
+#include <sstream>
+#include <thread>
 #include <limits>
 #include <memory>
 #include <ostream>
@@ -72,7 +77,14 @@ class DivergenceError : public Error { using Error::Error; };
 class CapacityError : public Error { using Error::Error; };
 class FormatError : public Error { using Error::Error; };
 class ConsistencyError : public Error { using Error::Error; };
-class PhaseError : public Error { using Error::Error; };
+class PhaseError : public Error {  // errors.hpp:62-72: carries the lowest offending global id
+ public:
+  explicit PhaseError(const std::string& what, std::int64_t global_id = -1) : Error(what), global_id_(global_id) {}
+  std::int64_t global_id() const { return global_id_; }
+
+ private:
+  std::int64_t global_id_;
+};
 class CudaError : public Error { using Error::Error; };
 class CommError : public Error { using Error::Error; };
 
@@ -690,6 +702,145 @@ template <typename Scalar>
 void admm_step(AdmmState<Scalar>& s) {  // solvers.hpp:318-327
   s.step(1);
   s.sync();
+}
+
+// ---- KernelPhase / run_phase / run_pipeline (parallel.hpp:40-132) --------------------------------------
+// The reference's barrier-separated parallel map, with the same contract: `body(i)` computes item i,
+// `writes(i)` declares its stores, run_phase splits items into contiguous ranges over up to `parallelism`
+// host threads and surfaces a throwing body as PhaseError carrying the lowest offending global id.  One
+// extension: a phase may carry `device`, which runs all of its items at once on the GPU (the phases
+// cpista_phases / cpadmm_phases / padmm_phases return: one kernel phase of the solver's device state).
+struct WriteAddress {
+  const void* buffer;
+  Index index;
+  friend bool operator<(const WriteAddress& a, const WriteAddress& b) {
+    return a.buffer != b.buffer ? a.buffer < b.buffer : a.index < b.index;
+  }
+};
+struct KernelPhase {
+  std::string name;
+  Index work_items = 0;
+  std::function<void(Index)> body;
+  std::function<std::vector<WriteAddress>(Index)> writes;
+  std::function<void()> device;  // set: the whole phase as one device launch (body unused)
+};
+inline void run_phase(const KernelPhase& phase, int parallelism) {  // parallel.hpp:64-126
+  if (parallelism < 1) throw ParameterError("run_phase: parallelism must be >= 1");
+  if (phase.device) {
+    phase.device();
+    return;
+  }
+  const Index total = phase.work_items;
+  if (total == 0) return;
+  struct Failure {
+    Index id;
+    std::string message;
+  };
+  const auto describe = [&phase](Index id, const char* what) {
+    std::ostringstream msg;
+    msg << "phase '" << phase.name << "': work item " << id << " failed: " << what;
+    return msg.str();
+  };
+  const int workers = static_cast<int>(std::min<Index>(parallelism, total));
+  if (workers == 1) {
+    for (Index i = 0; i < total; ++i) {
+      try {
+        phase.body(i);
+      } catch (const std::exception& e) {
+        throw PhaseError(describe(i, e.what()), i);
+      } catch (...) {
+        throw PhaseError(describe(i, "unknown error"), i);
+      }
+    }
+    return;
+  }
+  std::vector<std::optional<Failure>> failures(static_cast<size_t>(workers));
+  std::vector<std::thread> pool;
+  pool.reserve(static_cast<size_t>(workers));
+  const Index chunk = (total + workers - 1) / workers;
+  for (int w = 0; w < workers; ++w) {
+    const Index begin = Index(w) * chunk, end = std::min(begin + chunk, total);
+    pool.emplace_back([&phase, &failures, &describe, w, begin, end] {
+      for (Index i = begin; i < end; ++i) {
+        try {
+          phase.body(i);
+        } catch (const std::exception& e) {
+          failures[static_cast<size_t>(w)] = Failure{i, describe(i, e.what())};
+          return;
+        } catch (...) {
+          failures[static_cast<size_t>(w)] = Failure{i, describe(i, "unknown error")};
+          return;
+        }
+      }
+    });
+  }
+  for (std::thread& t : pool) t.join();
+  const Failure* first = nullptr;
+  for (const auto& f : failures)
+    if (f && (!first || f->id < first->id)) first = &*f;
+  if (first) throw PhaseError(first->message, first->id);
+}
+inline void run_pipeline(const std::vector<KernelPhase>& phases, int parallelism) {  // parallel.hpp:129-132
+  for (const KernelPhase& phase : phases) run_phase(phase, parallelism);
+}
+inline void check_disjoint_writes(const KernelPhase& phase) {  // parallel.hpp:136-152
+  if (!phase.writes) return;  // device phases: the kernels own disjoint output ranges by construction
+  std::map<WriteAddress, Index> owners;
+  for (Index i = 0; i < phase.work_items; ++i)
+    for (const WriteAddress& addr : phase.writes(i)) {
+      const auto [it, inserted] = owners.emplace(addr, i);
+      if (!inserted) {
+        std::ostringstream msg;
+        msg << "phase '" << phase.name << "': work items " << it->second << " and " << i << " both write index "
+            << addr.index << " of one buffer";
+        throw ConsistencyError(msg.str());
+      }
+    }
+}
+inline int hardware_parallelism() {  // parallel.hpp:154-157
+  const unsigned hw = std::thread::hardware_concurrency();
+  return hw == 0 ? 1 : static_cast<int>(hw);
+}
+namespace detail {
+// one device phase of `state` on its direct-engine solver (the phases are the direct engine's kernels, as the
+// reference's are its naive forms); the last phase of an iteration advances t and refreshes the host members
+template <typename State>
+KernelPhase device_phase(State& state, const char* name, Index items, int ph, bool last,
+                         std::function<void()> to_direct) {
+  KernelPhase k;
+  k.name = name;
+  k.work_items = items;
+  k.device = [&state, ph, last, to_direct] {
+    if (to_direct) to_direct();
+    check(cl_solver_run_phase(state.dev.handle(), ph));
+    if (last) {
+      ++state.t;
+      state.sync();
+    }
+  };
+  return k;
+}
+}  // namespace detail
+// cpista_phases (parallel.hpp:236-279): residual (m items), gradient + threshold (n items); direct engine
+template <typename Scalar>
+std::vector<KernelPhase> cpista_phases(IstaState<Scalar>& state) {
+  const auto direct = [&state] { state.dev.use(0, IstaState<Scalar>::kFields, 3); };
+  return {detail::device_phase(state, "cpista residual", state.dev.m(), 0, false, direct),
+          detail::device_phase(state, "cpista thresholded gradient", state.dev.n(), 1, true, direct)};
+}
+// cpadmm_phases (parallel.hpp:173-231): primal (beta), recovery (x = B beta), duals
+template <typename Scalar>
+std::vector<KernelPhase> cpadmm_phases(CadmmState<Scalar>& state) {
+  const auto direct = [&state] { state.dev.use(0, CadmmState<Scalar>::kFields, 6); };
+  return {detail::device_phase(state, "cpadmm primal", state.dev.n(), 0, false, direct),
+          detail::device_phase(state, "cpadmm recovery", state.dev.n(), 1, false, direct),
+          detail::device_phase(state, "cpadmm duals", state.dev.n(), 2, true, direct)};
+}
+// padmm_phases (parallel.hpp:284-317): primal and dual update, right-hand side
+template <typename Scalar>
+std::vector<KernelPhase> padmm_phases(AdmmState<Scalar>& state) {
+  return {detail::device_phase(state, "padmm primal and dual update", state.dev.n(), 0, false, nullptr),
+          detail::device_phase(state, "padmm right-hand side update", state.dev.n(), 1, true, nullptr)};
 }
 
 // ---- run_loop / *_run (solvers.hpp:426-534) ------------------------------------------

@@ -79,7 +79,94 @@ static void cpu_checks() {
   }
 }
 
+// parallel_test.cpp:29-108: the host executor's contract (every item once; parallelism >= 1; a throwing item
+// surfaces as the lowest-id PhaseError; overlapping declared writes are rejected)
+static void phase_checks() {
+  for (const int parallelism : {1, 3, 16}) {
+    std::vector<int> hits(10, 0);
+    cl::KernelPhase phase;
+    phase.name = "counting";
+    phase.work_items = 10;
+    phase.body = [&hits](cl::Index i) { ++hits[static_cast<size_t>(i)]; };
+    cl::run_phase(phase, parallelism);
+    for (const int h : hits) CHECK(h == 1);
+  }
+  cl::KernelPhase empty;
+  empty.name = "empty";
+  empty.body = [](cl::Index) { throw std::runtime_error("never"); };
+  cl::run_phase(empty, 4);
+  cl::KernelPhase one;
+  one.name = "one";
+  one.work_items = 1;
+  one.body = [](cl::Index) {};
+  CHECK(throws<cl::ParameterError>([&] { cl::run_phase(one, 0); }));
+  cl::KernelPhase faulty;
+  faulty.name = "faulty kernel";
+  faulty.work_items = 30;
+  faulty.body = [](cl::Index i) {
+    if (i == 5 || i == 17) throw std::runtime_error("boom");
+  };
+  for (const int parallelism : {1, 4}) {
+    bool caught = false;
+    try {
+      cl::run_phase(faulty, parallelism);
+    } catch (const cl::PhaseError& e) {
+      caught = e.global_id() == 5 && std::string(e.what()).find("faulty kernel") != std::string::npos &&
+               std::string(e.what()).find("boom") != std::string::npos;
+    }
+    CHECK(caught);
+  }
+  std::vector<double> buffer(8, 0.0);
+  cl::KernelPhase overlapping;
+  overlapping.name = "overlapping";
+  overlapping.work_items = 4;
+  overlapping.body = [](cl::Index) {};
+  overlapping.writes = [&buffer](cl::Index i) {
+    return std::vector<cl::WriteAddress>{{buffer.data(), i == 1 ? 3 : i}};
+  };
+  CHECK(throws<cl::ConsistencyError>([&] { cl::check_disjoint_writes(overlapping); }));
+  CHECK(cl::hardware_parallelism() >= 1);
+}
+
+// the factory phases on the device: run_pipeline(cpista_phases) / cpadmm_phases / padmm_phases advance the state
+// exactly like *_step (the same kernels in the same order: bitwise), parallel_test.cpp:75-96,143-165
+static void device_phase_checks() {
+  const cl::SensingProblem<double> p = cl::make_problem(1 << 14, 1 << 12, 64, 41);  // not a persistent-kernel size
+  cl::SolverConfig cfg;
+  cl::IstaState<double> a = cl::ista_setup(p.op, p.measurements, cfg), b = cl::ista_setup(p.op, p.measurements, cfg);
+  int checked = 0;
+  const std::vector<cl::KernelPhase> ph = cl::cpista_phases(a);
+  for (const cl::KernelPhase& k : ph) {
+    cl::check_disjoint_writes(k);
+    ++checked;
+  }
+  for (int it = 0; it < 3; ++it) {
+    cl::run_pipeline(ph, cl::hardware_parallelism());
+    cl::ista_step(b, false);
+  }
+  CHECK(a.t == 3 && b.t == 3 && a.x == b.x && a.r == b.r && a.delta == b.delta);
+  cl::CadmmState<double> c = cl::cadmm_setup(p.op, p.measurements, cfg), d = cl::cadmm_setup(p.op, p.measurements, cfg);
+  const std::vector<cl::KernelPhase> pc = cl::cpadmm_phases(c);
+  checked += static_cast<int>(pc.size());
+  for (int it = 0; it < 3; ++it) {
+    cl::run_pipeline(pc, 4);
+    cl::cadmm_step(d, false);
+  }
+  CHECK(c.t == 3 && d.t == 3 && c.z == d.z && c.x == d.x && c.v == d.v);
+  const cl::SensingProblem<double> q = cl::make_problem(256, 128, 8, 42);
+  cl::AdmmState<double> e = cl::admm_setup(q.op, q.measurements, cfg), f = cl::admm_setup(q.op, q.measurements, cfg);
+  const std::vector<cl::KernelPhase> pa = cl::padmm_phases(e);
+  checked += static_cast<int>(pa.size());
+  for (int it = 0; it < 3; ++it) {
+    cl::run_pipeline(pa, 2);
+    cl::admm_step(f);
+  }
+  CHECK(e.t == 3 && f.t == 3 && e.z == f.z && e.u == f.u);
+  CHECK(checked == 7);
+}
+
 static void gpu_checks() {
+  device_phase_checks();
   // solvers_test.cpp:213-243 report bookkeeping
   const cl::SensingProblem<double> p = cl::make_problem(256, 128, 25, 17);
   cl::SolverConfig cfg;
@@ -175,6 +262,7 @@ static void sharded_c4_checks(int world, cl::Transport transport) {
 int main(int argc, char** argv) {
   const std::string mode = argc > 1 ? argv[1] : "cpu";
   cpu_checks();
+  phase_checks();
   if (mode == "gpu") gpu_checks();
   if (mode == "c4") {
     sharded_c4_checks(1, cl::Transport::kNccl);
