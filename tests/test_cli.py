@@ -50,7 +50,8 @@ def test_usage_errors_exit_1(tmp_path):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("solver,engine", [("ista", "cuda"), ("cadmm", "cuda"), ("cadmm", "cuda-fft"),
-                                           ("ista", "fft"), ("admm", "cuda")])
+                                           ("ista", "fft"), ("admm", "cuda"), ("ista", "phases"),
+                                           ("cadmm", "phases"), ("admm", "phases")])
 def test_recover_matches_the_library_and_writes_csv(tmp_path, solver, engine):
     if cl.device_count() < 1:
         pytest.skip("no CUDA device")

@@ -5,10 +5,11 @@
 //
 // Every solve runs on the GPU through include/circlasso_b200.hpp.  --engine selects the product engine
 // (cli:48,60,221): `cuda` (default) = the direct shift-indexed sm_100a kernels; `cuda-fft` = the
-// on-device FFT engine; the reference's CPU engine names map onto them (`naive` and `phases` -> cuda,
-// `fft` -> cuda-fft).  New: `--device D`, and `--devices 0,1,...` shards an ISTA / cADMM recover over
+// on-device FFT engine; the reference's CPU engine names map onto them (`naive` -> cuda, `fft` -> cuda-fft),
+// and `phases` runs the solver's device kernel phases through run_pipeline (cli:111-184).  New: `--device D`, and `--devices 0,1,...` shards an ISTA / cADMM recover over
 // those GPUs with the library's NCCL exchange.  The reference's CLI11 parser is not in this image; the
 // option syntax (`--name value`, repeatable `--n` / `--solver`, flags) is parsed here.
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -152,6 +153,66 @@ int cmd_gen(const Args& a) {  // cli:186-199
   return kExitOk;
 }
 
+// --engine phases (cli:111-184): the solver advanced through its kernel phases with run_pipeline, the stop rule
+// checked between pipeline runs on the state's host members (refreshed by the last phase of each iteration)
+template <typename State>
+RecoveryReport<double> run_phases_loop(State& st, std::vector<KernelPhase> phases, const Vector<double>& iterate,
+                                       const SolverConfig& cfg, const Vector<double>* truth, int parallelism,
+                                       FootprintKind kind, Index n, Index m, double setup_s) {
+  RecoveryReport<double> rep;
+  rep.metric = truth ? StopMetric::kMseVsTruth : StopMetric::kIterateChange;
+  rep.setup_seconds = setup_s;
+  const auto t0 = std::chrono::steady_clock::now();
+  const auto since = [&t0] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
+  long t = 0;
+  while (t < cfg.max_iter) {
+    const Vector<double> before = iterate;
+    run_pipeline(phases, parallelism);
+    ++t;
+    if (t % cfg.check_every != 0 && t != cfg.max_iter) continue;
+    double change = 0.0;
+    for (Index i = 0; i < static_cast<Index>(iterate.size()); ++i) {
+      if (!std::isfinite(iterate[i])) throw DivergenceError("phase run: iterate became non-finite");
+      change += (iterate[i] - before[i]) * (iterate[i] - before[i]);
+    }
+    const double value = truth ? mse(iterate, *truth) : std::sqrt(change / std::max<double>(1, iterate.size()));
+    rep.mse_trace.push_back({t, value, since()});
+    rep.final_metric = value;
+    if (!std::isnan(cfg.target_mse) && value <= cfg.target_mse) {
+      rep.reached_target = true;
+      break;
+    }
+  }
+  (void)st;
+  rep.iterations = t;
+  rep.final_x = iterate;
+  rep.total_seconds = since() + setup_s;
+  rep.footprint_bytes = analytic_footprint(kind, static_cast<std::uint64_t>(n), static_cast<std::uint64_t>(m),
+                                           sizeof(double));
+  return rep;
+}
+
+RecoveryReport<double> run_with_phases(const std::string& solver, const Vector<double>& y,
+                                       const PartialCirculantOperator<double>& A, const SolverConfig& cfg,
+                                       const Vector<double>* truth, int parallelism) {
+  const auto t0 = std::chrono::steady_clock::now();
+  const auto setup_s = [&t0] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
+  if (solver == "ista") {
+    IstaState<double> st = ista_setup(A, y, cfg);
+    return run_phases_loop(st, cpista_phases(st), st.x, cfg, truth, parallelism, FootprintKind::kCpista, A.n(),
+                           A.m(), setup_s());
+  }
+  if (solver == "admm") {
+    AdmmState<double> st = admm_setup(A, y, cfg);
+    return run_phases_loop(st, padmm_phases(st), st.z, cfg, truth, parallelism, FootprintKind::kDenseAdmm, A.n(),
+                           A.m(), setup_s());
+  }
+  if (solver != "cadmm") throw ParameterError("--solver must be ista, admm, or cadmm");
+  CadmmState<double> st = cadmm_setup(A, y, cfg);
+  return run_phases_loop(st, cpadmm_phases(st), st.z, cfg, truth, parallelism, FootprintKind::kCpadmm, A.n(), A.m(),
+                         setup_s());
+}
+
 int cmd_recover(const Args& a) {  // cli:201-261
   if (!a.has("--problem")) throw UsageError("recover: --problem is required");
   const std::string problem = a.str("--problem", "");
@@ -174,6 +235,9 @@ int cmd_recover(const Args& a) {  // cli:201-261
     if (solver != "ista" && solver != "cadmm") throw ParameterError("--solver must be ista, admm, or cadmm");
     ShardedSolve<double> sh(solver == "ista" ? CL_KIND_ISTA : CL_KIND_CADMM, A, y, cfg, device_list(a.str("--devices", "")));
     report = sh.run(truth_ptr);
+  } else if (a.str("--engine", "cuda") == "phases") {  // the kernel-phase executor (cli:221-223)
+    const long threads = a.integer("--threads", hardware_parallelism());
+    report = run_with_phases(solver, y, A, cfg, truth_ptr, static_cast<int>(threads));
   } else if (solver == "ista") {
     report = ista_run(y, A, cfg, truth_ptr);
   } else if (solver == "admm") {
