@@ -106,14 +106,14 @@ struct Radix {
 //   DIF (SG = -1): V = DFT_R(v_r at j + rM); V_q *= w_L^{jq}; store at j + qM.
 //   DIT (SG = +1): v_q = x(j + qM) * w_L^{-jq}; V = IDFT_R(v); store V_r at j + rM.
 // tw[k] = e^{-2 pi i k / N}.
-template <int N, int L, int SG, int NSEQ>
+template <int N, int L, int SG, int NSEQ, int NT = kThr>
 __device__ __forceinline__ void stage(float2* buf, int sstride, const float2* __restrict__ tw) {
   constexpr int R = Radix<N, L>::value;
   constexpr int M = L / R;
   constexpr int per_seq = N / R;
   constexpr int total = NSEQ * per_seq;
   constexpr int twstep = N / L;
-  for (int idx = threadIdx.x; idx < total; idx += kThr) {
+  for (int idx = threadIdx.x; idx < total; idx += NT) {
     const int s = idx / per_seq, rem = idx - s * per_seq;
     const int blk = rem / M, j = rem - blk * M;
     float2* p = buf + s * sstride;
@@ -140,19 +140,19 @@ __device__ __forceinline__ void stage(float2* buf, int sstride, const float2* __
 }
 
 // Forward DIF over all stages (natural in, digit-reversed out).
-template <int N, int L, int NSEQ>
+template <int N, int L, int NSEQ, int NT = kThr>
 __device__ __forceinline__ void dif_from(float2* buf, int sstride, const float2* tw) {
-  stage<N, L, -1, NSEQ>(buf, sstride, tw);
+  stage<N, L, -1, NSEQ, NT>(buf, sstride, tw);
   __syncthreads();
   constexpr int next = L / Radix<N, L>::value;
-  if constexpr (next > 1) dif_from<N, next, NSEQ>(buf, sstride, tw);
+  if constexpr (next > 1) dif_from<N, next, NSEQ, NT>(buf, sstride, tw);
 }
 // Inverse DIT: the DIF stages undone in reverse order (digit-reversed in, natural out; scale N).
-template <int N, int L, int NSEQ>
+template <int N, int L, int NSEQ, int NT = kThr>
 __device__ __forceinline__ void dit_from(float2* buf, int sstride, const float2* tw) {
   constexpr int next = L / Radix<N, L>::value;
-  if constexpr (next > 1) dit_from<N, next, NSEQ>(buf, sstride, tw);
-  stage<N, L, +1, NSEQ>(buf, sstride, tw);
+  if constexpr (next > 1) dit_from<N, next, NSEQ, NT>(buf, sstride, tw);
+  stage<N, L, +1, NSEQ, NT>(buf, sstride, tw);
   __syncthreads();
 }
 
@@ -191,8 +191,11 @@ __host__ __device__ __forceinline__ int digit_pos(int k, int N) {
 // 2048-long columns (two-level plans at N >= 2^22): 8 columns = 64-byte row segments, 139 KB of shared memory
 __host__ __device__ constexpr int cols_per_cta(int N1) { return N1 <= 1024 ? kElems / N1 : N1 == 2048 ? 8 : 4; }
 // FINE (L2-resident sizes): half the columns / row units per CTA -- twice the CTAs in flight for the
-// latency-bound passes
-__host__ __device__ constexpr int cols_b(int N1, bool fine) {
+// latency-bound passes -- and 512 threads per CTA (half the serial work per thread in every stage)
+constexpr int kThrFine = 512;
+// FINE = 1: the halved tiles at 256 threads; FINE = 2: the halved tiles at 512 threads
+__host__ __device__ constexpr int threads_of(int fine) { return fine == 2 ? kThrFine : kThr; }
+__host__ __device__ constexpr int cols_b(int N1, int fine) {
   return fine && cols_per_cta(N1) > 1 ? cols_per_cta(N1) / 2 : cols_per_cta(N1);
 }
 __host__ __device__ constexpr int col_pitch_b(int N1, int B) { return N1 + N1 / 16 + (B <= 16 ? 16 / B : 1); }
@@ -208,22 +211,22 @@ __device__ __forceinline__ float2 tw_n(const float2* __restrict__ twA, const flo
 // Columns forward: input real u[j] (j = n1 N2 + n2).
 // REAL: the input is read as N complex values z[j] = (u[2j], u[2j+1]) (the real plans); else as the real
 // parts of n complex values.
-template <int N1, bool REAL, bool FINE = false>
-__global__ void __launch_bounds__(kThr, N1 <= 256 ? 4 : 1) k_cols_fwd(const float* __restrict__ u, float2* __restrict__ T, int N2,
+template <int N1, bool REAL, int FINE = 0>
+__global__ void __launch_bounds__(threads_of(FINE), N1 <= 256 ? 4 : 1) k_cols_fwd(const float* __restrict__ u, float2* __restrict__ T, int N2,
                                                    const float2* __restrict__ tw1) {
   extern __shared__ float2 sm[];
   constexpr int B = cols_b(N1, FINE), P = col_pitch_b(N1, B), cnt = B * N1;
   const int c0 = blockIdx.x * B;
 #pragma unroll
-  for (int e = threadIdx.x; e < cnt; e += kThr) {
+  for (int e = threadIdx.x; e < cnt; e += threads_of(FINE)) {
     const int i = e / B, w = e - i * B;
     const int64_t j = static_cast<int64_t>(i) * N2 + c0 + w;
     sm[w * P + pad16(i)] = REAL ? __ldg(reinterpret_cast<const float2*>(u) + j) : make_float2(__ldg(u + j), 0.f);
   }
   __syncthreads();
-  dif_from<N1, N1, B>(sm, P, tw1);
+  dif_from<N1, N1, B, threads_of(FINE)>(sm, P, tw1);
 #pragma unroll
-  for (int e = threadIdx.x; e < cnt; e += kThr) {
+  for (int e = threadIdx.x; e < cnt; e += threads_of(FINE)) {
     const int i = e / B, w = e - i * B;
     T[static_cast<int64_t>(i) * N2 + c0 + w] = sm[w * P + pad16(i)];
   }
@@ -300,7 +303,7 @@ k_rows(float2* __restrict__ T, const float2* __restrict__ H, int conj_h, int row
 // u in [0, kmul / 2] is the row pair (kb = u, kb' = kmul - u); kb = 0 and kmul / 2 are their own mirrors.
 // The four-step twiddle of row R is w^{mult n2 digit_rev(R mod rowmod, rowmod)}, as in k_rows.  H holds
 // H[k] (k < N) in the same positions, entry k = 0 = (H[0], H[N]).
-__host__ __device__ constexpr int units_per_cta(int N2, bool fine = false) {
+__host__ __device__ constexpr int units_per_cta(int N2, int fine = 0) {
   return N2 >= 2048 ? 1 : fine && N2 == 1024 ? 1 : (fine ? 1024 : 2048) / N2;
 }
 
@@ -318,8 +321,8 @@ __device__ __forceinline__ float2 r2c_mul(float2 zk, float2 zb, float2 hk, float
 
 // H2[u N2 + q] = (H at (row of kb = u, q), H at the mirror position): one 16-byte load per index pair.
 // t2[q] = W^{kmul digit_rev(q)}, so W^k = W^{kb} t2[q]; W^{N-k} = -conj(W^k).
-template <int N2, bool FINE = false>
-__global__ void __launch_bounds__(kThr, N2 <= 256 ? 4 : 1)
+template <int N2, int FINE = 0>
+__global__ void __launch_bounds__(threads_of(FINE), N2 <= 256 ? 4 : 1)
 k_rows_r2c(float2* __restrict__ T, const float4* __restrict__ H2, int conj_h, int N1, int A, int rowmod, int mult,
            const float2* __restrict__ tw2, const float2* __restrict__ twA, const float2* __restrict__ twB,
            const float2* __restrict__ twCA, const float2* __restrict__ twCB, const float2* __restrict__ t2) {
@@ -339,16 +342,16 @@ k_rows_r2c(float2* __restrict__ T, const float4* __restrict__ H2, int conj_h, in
     if (!(threadIdx.x & 1)) wrow[threadIdx.x >> 1] = tw_n(twCA, twCB, kb);  // W^{kb}
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < cnt; e += kThr) {
+  for (int e = threadIdx.x; e < cnt; e += threads_of(FINE)) {
     const int s = e / N2, n2 = e - s * N2, R = rows_s[s];
     if (R >= 0) sm[s * P + pad16(n2)] = cmulf(T[static_cast<int64_t>(R) * N2 + n2], tw_n(twA, twB, n2 * k1s[s]));
   }
   __syncthreads();
-  dif_from<N2, N2, slots>(sm, P, tw2);
+  dif_from<N2, N2, slots, threads_of(FINE)>(sm, P, tw2);
   // spectral step: the thread of (slot 2u, q) handles k and its mirror N - k, at (2u + 1, qb) -- or at (2u, qb)
   // when the row is its own mirror (kb = 0 or kmul / 2), and then only q <= qb works.  Mirror position:
   // kb != 0: digit complement qb = N2 - 1 - q; kb = 0: the position of (N2 - k2) mod N2.
-  for (int e = threadIdx.x; e < upc * N2; e += kThr) {
+  for (int e = threadIdx.x; e < upc * N2; e += threads_of(FINE)) {
     const int ul = e / N2, q = e - ul * N2, sa = 2 * ul;
     if (rows_s[sa] < 0) continue;
     const bool self = rows_s[sa + 1] < 0;
@@ -371,8 +374,8 @@ k_rows_r2c(float2* __restrict__ T, const float4* __restrict__ H2, int conj_h, in
       sm[sb * P + pad16(qb)] = r2c_mul(zb, zk, hb, make_float2(hk.x, -hk.y), make_float2(-w.x, w.y));
   }
   __syncthreads();
-  dit_from<N2, N2, slots>(sm, P, tw2);
-  for (int e = threadIdx.x; e < cnt; e += kThr) {
+  dit_from<N2, N2, slots, threads_of(FINE)>(sm, P, tw2);
+  for (int e = threadIdx.x; e < cnt; e += threads_of(FINE)) {
     const int s = e / N2, n2 = e - s * N2, R = rows_s[s];
     if (R >= 0)
       T[static_cast<int64_t>(R) * N2 + n2] = cmulf_conj(sm[s * P + pad16(n2)], tw_n(twA, twB, n2 * k1s[s]));
@@ -450,21 +453,21 @@ __device__ __forceinline__ float emit_out(const Fft4Out& o, int64_t j, float v) 
   }
 }
 // REAL: element j of the inverse holds y[2j] + i y[2j+1]; else Re = y[j].
-template <int N1, bool REAL, bool FINE = false>
-__global__ void __launch_bounds__(kThr, N1 <= 256 ? 4 : 1) k_cols_inv(const float2* __restrict__ T, Fft4Out o, int N2,
+template <int N1, bool REAL, int FINE = 0>
+__global__ void __launch_bounds__(threads_of(FINE), N1 <= 256 ? 4 : 1) k_cols_inv(const float2* __restrict__ T, Fft4Out o, int N2,
                                                    const float2* __restrict__ tw1, float inv_n) {
   extern __shared__ float2 sm[];
   constexpr int B = cols_b(N1, FINE), P = col_pitch_b(N1, B), cnt = B * N1;
   const int c0 = blockIdx.x * B;
 #pragma unroll
-  for (int e = threadIdx.x; e < cnt; e += kThr) {
+  for (int e = threadIdx.x; e < cnt; e += threads_of(FINE)) {
     const int i = e / B, w = e - i * B;
     sm[w * P + pad16(i)] = T[static_cast<int64_t>(i) * N2 + c0 + w];
   }
   __syncthreads();
-  dit_from<N1, N1, B>(sm, P, tw1);
+  dit_from<N1, N1, B, threads_of(FINE)>(sm, P, tw1);
 #pragma unroll
-  for (int e = threadIdx.x; e < cnt; e += kThr) {
+  for (int e = threadIdx.x; e < cnt; e += threads_of(FINE)) {
     const int i = e / B, w = e - i * B;
     const int64_t j = static_cast<int64_t>(i) * N2 + c0 + w;
     const float2 s = sm[w * P + pad16(i)];
@@ -481,21 +484,21 @@ __global__ void __launch_bounds__(kThr, N1 <= 256 ? 4 : 1) k_cols_inv(const floa
 // consumer produced, still in shared memory -- the forward columns of the next product, in place on T.
 // Every CTA owns whole columns, so the next product's column FFT needs nothing from other CTAs (ISTA: the
 // residual's P^T r feeds the gradient; cADMM: beta feeds B beta, and x = B beta feeds C x).
-template <int N1, bool REAL, bool FINE = false>
-__global__ void __launch_bounds__(kThr, N1 <= 256 ? 4 : 1) k_cols_inv_fwd(float2* __restrict__ T, Fft4Out o, int N2,
+template <int N1, bool REAL, int FINE = 0>
+__global__ void __launch_bounds__(threads_of(FINE), N1 <= 256 ? 4 : 1) k_cols_inv_fwd(float2* __restrict__ T, Fft4Out o, int N2,
                                                        const float2* __restrict__ tw1, float inv_n) {
   extern __shared__ float2 sm[];
   constexpr int B = cols_b(N1, FINE), P = col_pitch_b(N1, B), cnt = B * N1;
   const int c0 = blockIdx.x * B;
 #pragma unroll
-  for (int e = threadIdx.x; e < cnt; e += kThr) {
+  for (int e = threadIdx.x; e < cnt; e += threads_of(FINE)) {
     const int i = e / B, w = e - i * B;
     sm[w * P + pad16(i)] = T[static_cast<int64_t>(i) * N2 + c0 + w];
   }
   __syncthreads();
-  dit_from<N1, N1, B>(sm, P, tw1);
+  dit_from<N1, N1, B, threads_of(FINE)>(sm, P, tw1);
 #pragma unroll
-  for (int e = threadIdx.x; e < cnt; e += kThr) {
+  for (int e = threadIdx.x; e < cnt; e += threads_of(FINE)) {
     const int i = e / B, w = e - i * B;
     const int64_t j = static_cast<int64_t>(i) * N2 + c0 + w;
     float2& s = sm[w * P + pad16(i)];
@@ -507,9 +510,9 @@ __global__ void __launch_bounds__(kThr, N1 <= 256 ? 4 : 1) k_cols_inv_fwd(float2
     }
   }
   __syncthreads();
-  dif_from<N1, N1, B>(sm, P, tw1);
+  dif_from<N1, N1, B, threads_of(FINE)>(sm, P, tw1);
 #pragma unroll
-  for (int e = threadIdx.x; e < cnt; e += kThr) {
+  for (int e = threadIdx.x; e < cnt; e += threads_of(FINE)) {
     const int i = e / B, w = e - i * B;
     T[static_cast<int64_t>(i) * N2 + c0 + w] = sm[w * P + pad16(i)];
   }
@@ -770,21 +773,23 @@ static int64_t twB_len(const Fft4Plan& p) { return std::max<int64_t>(1, p.N / 40
 
 // FINE launches for the L2-resident real plans (N <= 2^19: ISTA at n = 2^20 0.091 vs 0.111 ms per iteration;
 // no gain at N = 2^20); CLB_FFT_FINE=0/1 forces either
-static bool fft4_fine(const Fft4Plan& p) {
+static int fft4_fine(const Fft4Plan& p) {
   static const int env = [] {
     const char* v = std::getenv("CLB_FFT_FINE");
     return (v && *v) ? atoi(v) : -1;
   }();
-  return env >= 0 ? env != 0 : p.N <= (int64_t(1) << 19);
+  if (!p.real) return 0;
+  if (env >= 0) return env;
+  return p.N <= (int64_t(1) << 18) ? 2 : p.N <= (int64_t(1) << 19) ? 1 : 0;
 }
 template <int N>
-static size_t cols_smem_t(bool fine = false) {
+static size_t cols_smem_t(int fine = 0) {
   return static_cast<size_t>(cols_b(N, fine)) * col_pitch_b(N, cols_b(N, fine)) * sizeof(float2);
 }
 template <int N>
 static size_t rows_smem_t() { return static_cast<size_t>(row_count(N)) * row_pitch(N) * sizeof(float2); }
 template <int N>
-static size_t rows_r2c_smem_t(bool fine = false) {
+static size_t rows_r2c_smem_t(int fine = 0) {
   return static_cast<size_t>(2 * units_per_cta(N, fine)) * row_pitch(N) * sizeof(float2);
 }
 
@@ -800,21 +805,29 @@ void fft4_init_attributes() {
     cudaFuncSetAttribute(k_cols_inv<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem_t<N>()); \
     cudaFuncSetAttribute(k_cols_fwd<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem_t<N>());  \
     cudaFuncSetAttribute(k_cols_inv<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem_t<N>());  \
-    cudaFuncSetAttribute(k_cols_fwd<N, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,                 \
-                         (int)cols_smem_t<N>(true));                                                             \
+    cudaFuncSetAttribute(k_cols_fwd<N, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,                    \
+                         (int)cols_smem_t<N>(1));                                                                \
+    cudaFuncSetAttribute(k_cols_fwd<N, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,                    \
+                         (int)cols_smem_t<N>(2));                                                                \
     cudaFuncSetAttribute(k_cols_inv_fwd<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,                  \
                          (int)cols_smem_t<N>());                                                                 \
     cudaFuncSetAttribute(k_cols_inv_fwd<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,                   \
                          (int)cols_smem_t<N>());                                                                 \
-    cudaFuncSetAttribute(k_cols_inv_fwd<N, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,             \
-                         (int)cols_smem_t<N>(true));                                                             \
-    cudaFuncSetAttribute(k_cols_inv<N, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,                 \
-                         (int)cols_smem_t<N>(true));                                                             \
+    cudaFuncSetAttribute(k_cols_inv_fwd<N, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,                \
+                         (int)cols_smem_t<N>(1));                                                                \
+    cudaFuncSetAttribute(k_cols_inv_fwd<N, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,                \
+                         (int)cols_smem_t<N>(2));                                                                \
+    cudaFuncSetAttribute(k_cols_inv<N, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,                    \
+                         (int)cols_smem_t<N>(1));                                                                \
+    cudaFuncSetAttribute(k_cols_inv<N, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,                    \
+                         (int)cols_smem_t<N>(2));                                                                \
   }                                                                                                             \
   cudaFuncSetAttribute(k_rows<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem_t<N>());         \
   cudaFuncSetAttribute(k_rows_r2c<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_r2c_smem_t<N>());   \
-  cudaFuncSetAttribute(k_rows_r2c<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,                       \
-                       (int)rows_r2c_smem_t<N>(true));
+  cudaFuncSetAttribute(k_rows_r2c<N, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,                          \
+                       (int)rows_r2c_smem_t<N>(1));                                                            \
+  cudaFuncSetAttribute(k_rows_r2c<N, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,                          \
+                       (int)rows_r2c_smem_t<N>(2));
   CLB_FFT4_SIZES(CLB_ATTR)
 #undef CLB_ATTR
   cudaFuncSetAttribute(k_mid<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem_t<128>());
@@ -827,8 +840,10 @@ void launch_fft4_cols_fwd(const Fft4Plan& p, const float* u, float2* T, const fl
   switch (p.N1) {
 #define CLB_CASE(N)                                                                                        \
   case N:                                                                                                  \
-    if (p.real && fft4_fine(p))                                                                            \
-      k_cols_fwd<N, true, true><<<p.N2 / cols_b(N, true), kThr, cols_smem_t<N>(true), st>>>(u, T, p.N2, tw1); \
+    if (fft4_fine(p) == 2)                                                                                 \
+      k_cols_fwd<N, true, 2><<<p.N2 / cols_b(N, 2), threads_of(2), cols_smem_t<N>(2), st>>>(u, T, p.N2, tw1); \
+    else if (fft4_fine(p) == 1)                                                                            \
+      k_cols_fwd<N, true, 1><<<p.N2 / cols_b(N, 1), threads_of(1), cols_smem_t<N>(1), st>>>(u, T, p.N2, tw1); \
     else if (p.real) k_cols_fwd<N, true><<<p.N2 / cols_per_cta(N), kThr, cols_smem_t<N>(), st>>>(u, T, p.N2, tw1); \
     else k_cols_fwd<N, false><<<p.N2 / cols_per_cta(N), kThr, cols_smem_t<N>(), st>>>(u, T, p.N2, tw1);      \
     break;
@@ -842,6 +857,19 @@ static void launch_mid(const Fft4Plan& p, float2* T, bool fwd, const float2* twM
   const unsigned grid = static_cast<unsigned>(p.N1 * (p.B / cols_per_cta(A)));
   if (fwd) k_mid<A, true><<<grid, kThr, cols_smem_t<A>(), st>>>(T, p.N1, p.N2, p.B, twM, twA, twB);
   else k_mid<A, false><<<grid, kThr, cols_smem_t<A>(), st>>>(T, p.N1, p.N2, p.B, twM, twA, twB);
+}
+template <int N>
+static void launch_rows_r2c_fine(const Fft4Plan& p, float2* T, const float2* H, bool conj_h, int A, int rowmod, int mult,
+                                 const float2* twR, const float2* twA, const float2* twB, const float2* twCA,
+                                 const float2* twCB, cudaStream_t st) {
+  const int kmul = p.N1 * A;
+  const float4* H2 = reinterpret_cast<const float4*>(H);
+  if (fft4_fine(p) == 2)
+    k_rows_r2c<N, 2><<<(kmul / 2 + units_per_cta(N, 2)) / units_per_cta(N, 2), threads_of(2), rows_r2c_smem_t<N>(2),
+                       st>>>(T, H2, conj_h ? 1 : 0, p.N1, A, rowmod, mult, twR, twA, twB, twCA, twCB, twA + 8192);
+  else
+    k_rows_r2c<N, 1><<<(kmul / 2 + units_per_cta(N, 1)) / units_per_cta(N, 1), threads_of(1), rows_r2c_smem_t<N>(1),
+                       st>>>(T, H2, conj_h ? 1 : 0, p.N1, A, rowmod, mult, twR, twA, twB, twCA, twCB, twA + 8192);
 }
 void launch_fft4_rows(const Fft4Plan& p, float2* T, const float2* H, bool conj_h, const float2* tw2,
                       const float2* twA, const float2* twB, cudaStream_t st) {
@@ -858,11 +886,8 @@ void launch_fft4_rows(const Fft4Plan& p, float2* T, const float2* H, bool conj_h
   switch (R) {
 #define CLB_CASE(N)                                                                                            \
   case N:                                                                                                      \
-    if (p.real && fft4_fine(p))                                                                                \
-      k_rows_r2c<N, true><<<(kmul / 2 + units_per_cta(N, true)) / units_per_cta(N, true), kThr,                \
-                            rows_r2c_smem_t<N>(true), st>>>(                                                    \
-          T, reinterpret_cast<const float4*>(H), conj_h ? 1 : 0, p.N1, A, rowmod, mult, twR, twA, twB, twCA,   \
-          twCB, twA + 8192);                                                                                   \
+    if (fft4_fine(p))                                                                                          \
+      launch_rows_r2c_fine<N>(p, T, H, conj_h, A, rowmod, mult, twR, twA, twB, twCA, twCB, st);                \
     else if (p.real)                                                                                           \
       k_rows_r2c<N><<<(kmul / 2 + units_per_cta(N)) / units_per_cta(N), kThr, rows_r2c_smem_t<N>(), st>>>(     \
           T, reinterpret_cast<const float4*>(H), conj_h ? 1 : 0, p.N1, A, rowmod, mult, twR, twA, twB, twCA,   \
@@ -886,9 +911,10 @@ void launch_fft4_cols_inv(const Fft4Plan& p, const float2* T, const Fft4Out& o, 
   switch (p.N1) {
 #define CLB_CASE(N)                                                                                        \
   case N:                                                                                                  \
-    if (p.real && fft4_fine(p))                                                                            \
-      k_cols_inv<N, true, true><<<p.N2 / cols_b(N, true), kThr, cols_smem_t<N>(true), st>>>(T, o, p.N2, tw1,  \
-                                                                                             inv_n);         \
+    if (fft4_fine(p) == 2)                                                                                 \
+      k_cols_inv<N, true, 2><<<p.N2 / cols_b(N, 2), threads_of(2), cols_smem_t<N>(2), st>>>(T, o, p.N2, tw1, inv_n); \
+    else if (fft4_fine(p) == 1)                                                                            \
+      k_cols_inv<N, true, 1><<<p.N2 / cols_b(N, 1), threads_of(1), cols_smem_t<N>(1), st>>>(T, o, p.N2, tw1, inv_n); \
     else if (p.real) k_cols_inv<N, true><<<p.N2 / cols_per_cta(N), kThr, cols_smem_t<N>(), st>>>(T, o, p.N2, tw1, inv_n); \
     else k_cols_inv<N, false><<<p.N2 / cols_per_cta(N), kThr, cols_smem_t<N>(), st>>>(T, o, p.N2, tw1, inv_n);      \
     break;
@@ -901,9 +927,10 @@ void launch_fft4_cols_inv_fwd(const Fft4Plan& p, float2* T, const Fft4Out& o, co
   switch (p.N1) {
 #define CLB_CASE(N)                                                                                          \
   case N:                                                                                                    \
-    if (p.real && fft4_fine(p))                                                                              \
-      k_cols_inv_fwd<N, true, true><<<p.N2 / cols_b(N, true), kThr, cols_smem_t<N>(true), st>>>(T, o, p.N2, tw1, \
-                                                                                                 inv_n);     \
+    if (fft4_fine(p) == 2)                                                                                   \
+      k_cols_inv_fwd<N, true, 2><<<p.N2 / cols_b(N, 2), threads_of(2), cols_smem_t<N>(2), st>>>(T, o, p.N2, tw1, inv_n); \
+    else if (fft4_fine(p) == 1)                                                                              \
+      k_cols_inv_fwd<N, true, 1><<<p.N2 / cols_b(N, 1), threads_of(1), cols_smem_t<N>(1), st>>>(T, o, p.N2, tw1, inv_n); \
     else if (p.real)                                                                                         \
       k_cols_inv_fwd<N, true><<<p.N2 / cols_per_cta(N), kThr, cols_smem_t<N>(), st>>>(T, o, p.N2, tw1, inv_n);   \
     else                                                                                                     \
