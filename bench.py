@@ -7,8 +7,8 @@ A "step" is one solver iteration over the whole problem.  Default workload
 (N=1): BASELINE config 3 -- ISTA, partial circulant A, n=2^20, m=2^18,
 k=2^12 (make_problem(2^20, 2^18, 2^12, seed=1)), alpha=1e-4, tau=0.9
 (auto), literal pairing; metric = ISTA iterations/s.  For N>1 the same
-problem is row/output-sharded across the ranks (strong scaling) with
-all-gathers over NCCL between the phases.
+problem is row/output-sharded across the ranks (strong scaling); each phase's
+slice reaches every rank through the library (BENCH_TRANSPORT below).
 
 Timing: W untimed warm-up iterations, then K iterations queued back to back
 (no host synchronization inside the timed loop), each bracketed by CUDA
@@ -20,7 +20,8 @@ download) timed on the host clock (sharded: setup + K sharded iterations +
 download, max over ranks).  Rank 0 prints one JSON line; native output (NCCL
 banners) goes to stderr.  The default line also carries the FFT engine, the
 cADMM rate at n=2^20 and the time to recovery (MSE <= 1e-4) on both engines.
-BENCH_FORCE_SHARDED=1 runs the sharded NCCL path with a single rank.
+BENCH_FORCE_SHARDED=1 runs the sharded path with a single rank; BENCH_TRANSPORT=ipc (default: the exchange fused
+into the epilogues as CUDA IPC peer stores) or nccl (the library's NCCL broadcasts) picks the N>1 exchange.
 """
 from __future__ import annotations
 
@@ -408,8 +409,11 @@ def main():
     setup = cl.ista_setup if w["kind"] == "ista" else cl.cadmm_setup
     st = setup(prob.op, prob.measurements, cfg, device=local_rank)
     comm = None
-    if sharded:  # the library's own NCCL communicator: the slice exchange runs inside cl_solver_step
-        comm = cdist.NativeComm.from_torch(local_rank)
+    # sharded: the slice exchange runs inside cl_solver_step, either fused into the producing epilogues as CUDA
+    # IPC peer stores (BENCH_TRANSPORT=ipc, the default) or as the library's NCCL broadcasts (=nccl)
+    transport = os.environ.get("BENCH_TRANSPORT", "ipc")
+    if sharded:
+        comm = cdist.TorchIpc() if transport == "ipc" else cdist.NativeComm.from_torch(local_rank)
         comm.attach(st)
 
     def one_step():
@@ -538,9 +542,11 @@ def main():
         e2e_s = float(t.item())
         e2e = {"value": args.steps / e2e_s, "unit": "iterations/s", "h2d_bytes_per_step": world * h2d / args.steps,
                "d2h_bytes_per_step": d2h / args.steps, "wall_s": e2e_s,
-               "note": f"{world} ranks: ista_run/cadmm_run(..., comm=NativeComm) from host fp64 buffers on every "
-                       "rank: setup, K sharded iterations (in-place NCCL broadcasts of the slices inside the "
-                       "library), iterate download; max wall time over ranks"}
+               "note": f"{world} ranks: ista_run/cadmm_run(..., comm={type(comm).__name__}) from host fp64 buffers "
+                       "on every rank: setup, K sharded iterations (" +
+                       ("the slices stored into every rank's copy by the producing epilogues, CUDA IPC"
+                        if transport == "ipc" else "in-place NCCL broadcasts of the slices inside the library") +
+                       "), iterate download; max wall time over ranks"}
 
     # the same workload through the on-device FFT engine (use_fft=True, the reference's default engine)
     fft_line = None
@@ -631,7 +637,9 @@ def main():
                                   if k_name == "k_tc_dense" else
                                   "direct shift-indexed sm_100a kernels"),
                        "l2": "flushed (256 MiB) between steps",
-                       "parallelism": f"row/output shards x{world} (library-owned NCCL exchange)" if sharded
+                       "parallelism": f"row/output shards x{world} (" + ("exchange fused into the epilogues: CUDA IPC "
+                                      "peer stores" if transport == "ipc" else "library-owned NCCL exchange") + ")"
+                       if sharded
                        else "single GPU"},
             "roofline": {"bound": "tensor" if k_name == "k_tc_dense" else "fp32_ffma", "kernel": k_name,
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,

@@ -218,6 +218,20 @@ cl_status cl_comm_init_rank(const unsigned char* id, int world, int rank, int de
 void cl_comm_destroy(cl_comm* c);
 cl_status cl_solver_attach_comm(cl_solver* s, cl_comm* c);
 
+/* One process per GPU without NCCL: CUDA IPC peer stores.  Each rank calls
+ * cl_solver_peer_export(s, rank, world, blob) (shards the solver and makes
+ * its exchange vectors IPC-exportable), the caller hands every rank's
+ * CL_PEER_BLOB_BYTES-byte blob to every rank in rank order (any channel), and
+ * each rank calls cl_solver_peer_attach(s, blobs).  From then on
+ * cl_solver_step / _step_checked / cl_solver_run run the sharded iteration:
+ * each phase's epilogue kernel stores its slice into every rank's copy of
+ * the vector (NVLink peer stores), and the ranks order their phases through
+ * system-scope flags -- no separate all-gather, no NCCL.  At most 8 ranks;
+ * destroying the solvers is collective (a final barrier). */
+#define CL_PEER_BLOB_BYTES 512
+cl_status cl_solver_peer_export(cl_solver* s, int rank, int world, unsigned char* blob);
+cl_status cl_solver_peer_attach(cl_solver* s, const unsigned char* blobs /* world x CL_PEER_BLOB_BYTES */);
+
 /* One process driving several GPUs (or several shards of one GPU): a group of
  * `ndev` solvers, rank r on devices[r].  Transport CL_TRANSPORT_NCCL builds
  * the communicators with ncclCommInitAll and issues every rank's exchange in

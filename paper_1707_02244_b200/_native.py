@@ -87,6 +87,8 @@ _SIGS = {
     "cl_comm_init_rank": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)]),
     "cl_comm_destroy": (None, [_vp]),
     "cl_solver_attach_comm": (C.c_int, [_vp, _vp]),
+    "cl_solver_peer_export": (C.c_int, [_vp, C.c_int, C.c_int, C.c_char_p]),
+    "cl_solver_peer_attach": (C.c_int, [_vp, C.c_char_p]),
     "cl_group_create": (C.c_int, [C.c_int, C.c_int64, C.c_int64, _d, _i64, _d, C.POINTER(cl_config),
                                   C.POINTER(C.c_int), C.c_int, C.c_int, C.POINTER(_vp)]),
     "cl_group_destroy": (None, [_vp]),

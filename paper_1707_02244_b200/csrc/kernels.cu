@@ -1071,6 +1071,11 @@ __device__ __forceinline__ void block_metrics(double a, double b, double c, doub
 __device__ __forceinline__ void to_peers(const EpiArgs& a, int64_t i, float v) {
   for (int p = 0; p < a.npeer; ++p) a.peer[p][i] = v;
 }
+// after a thread's last peer store: visible system-wide (another process's or GPU's reads) before the
+// rank's phase flag is raised by the next kernel
+__device__ __forceinline__ void peers_fence(const EpiArgs& a) {
+  if (a.npeer) __threadfence_system();
+}
 
 __device__ __forceinline__ float sum_partials(const float* __restrict__ p, int splits, int64_t stride, int64_t i) {
   float s = p[i];
@@ -1104,6 +1109,7 @@ __global__ void __launch_bounds__(kThreads) k_residual_reduce(EpiArgs a, int64_t
     a.r[t] = rv;
     to_peers(a, t, rv);
   }
+  peers_fence(a);
 }
 
 __global__ void __launch_bounds__(kThreads) k_residual_gather(EpiArgs a, const int* __restrict__ omega) {
@@ -1115,6 +1121,7 @@ __global__ void __launch_bounds__(kThreads) k_residual_gather(EpiArgs a, const i
     a.r[t] = rv;
     to_peers(a, t, rv);
   }
+  peers_fence(a);
 }
 
 __global__ void __launch_bounds__(kThreads) k_ista_update(EpiArgs a) {
@@ -1138,6 +1145,7 @@ __global__ void __launch_bounds__(kThreads) k_ista_update(EpiArgs a) {
       if (!isfinite(xn)) m2 += 1.0;
     }
   }
+  peers_fence(a);
   if (a.want_metrics) block_metrics(m0, m1, m2, a.blk);
 }
 
@@ -1150,6 +1158,7 @@ __global__ void __launch_bounds__(kThreads) k_admm_beta(EpiArgs a) {
     a.beta[i] = b;
     to_peers(a, i, b);
   }
+  peers_fence(a);
 }
 
 __global__ void __launch_bounds__(kThreads) k_admm_x(EpiArgs a) {
@@ -1159,6 +1168,7 @@ __global__ void __launch_bounds__(kThreads) k_admm_x(EpiArgs a) {
     a.x[i] = xv;
     to_peers(a, i, xv);
   }
+  peers_fence(a);
 }
 
 __global__ void __launch_bounds__(kThreads) k_admm_duals(EpiArgs a) {
@@ -1187,6 +1197,7 @@ __global__ void __launch_bounds__(kThreads) k_admm_duals(EpiArgs a) {
       if (!isfinite(zn)) m2 += 1.0;
     }
   }
+  peers_fence(a);
   if (a.want_metrics) block_metrics(m0, m1, m2, a.blk);
 }
 

@@ -29,6 +29,7 @@
 #include "tc_dense.cuh"
 #include "dense.cuh"
 #include "comm.hpp"
+#include "ipc.cuh"
 
 namespace clb {
 void gen_sparse_signal(int64_t n, int64_t k, uint64_t seed, double* values, int64_t* support);
@@ -59,13 +60,29 @@ struct DevBuf {
   T* p = nullptr;
   size_t count = 0;
   cudaStream_t s = nullptr;
+  bool plain = false;  // cudaMalloc'd (IPC-exportable) instead of the stream-ordered pool
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() { release(); }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    if (p) {
+      if (plain) cudaFree(p);
+      else cudaFreeAsync(p, s);
+    }
     p = nullptr;
+    plain = false;
+  }
+  // move the contents into cudaMalloc'd memory (CUDA IPC cannot export stream-ordered pool allocations)
+  void make_plain(cudaStream_t st) {
+    if (plain || !count) return;
+    T* q = nullptr;
+    CU(cudaMalloc(reinterpret_cast<void**>(&q), sizeof(T) * count));
+    CU(cudaMemcpyAsync(q, p, sizeof(T) * count, cudaMemcpyDeviceToDevice, st));
+    CU(cudaStreamSynchronize(st));
+    cudaFreeAsync(p, s);
+    p = q;
+    plain = true;
   }
   void alloc(size_t c, cudaStream_t st = nullptr) {
     release();
@@ -264,6 +281,15 @@ struct Solver {
   // rows_of[r] = ISTA residual rows of rank r, outs_of[r] = outputs of rank r
   Comm* comm = nullptr;
   std::vector<std::pair<int64_t, int64_t>> rows_of, outs_of;
+  // one process per GPU without NCCL (cl_solver_peer_export / _attach): CUDA IPC peer stores
+  struct Ipc {
+    bool on = false;
+    unsigned long long seq = 0;
+    IpcSync* own = nullptr;     // this rank's exported sync block (cudaMalloc'd)
+    IpcPeerSync sync;           // every rank's sync block, own at its rank
+    IpcPeerVec z;               // cADMM: every rank's z (the slice-local iterate, pushed before downloads)
+    std::vector<void*> opened;  // the peers' mappings
+  } ipc;
   int64_t out_lo = 0, out_hi = 0;  // outputs owned
 
   DevBuf<float> hc, hcr, hbr;      // c~, c~ reversed, b reversed
@@ -323,6 +349,15 @@ struct Solver {
     trace("destroy: enter");
     if (st) cudaSetDevice(device);
     if (st) cudaStreamSynchronize(st);
+    if (ipc.on) {  // every rank is done with every other rank's memory before any of it is unmapped or freed
+      try {
+        ipc_barrier();
+        cudaStreamSynchronize(st);
+      } catch (...) {
+      }
+      for (void* q : ipc.opened) cudaIpcCloseMemHandle(q);
+    }
+    if (ipc.own) cudaFree(ipc.own);
     trace("destroy: stream drained");
     drop_graph();
     for (auto e : ring) cudaEventDestroy(e);
@@ -1146,6 +1181,7 @@ struct Solver {
   }
   void attach_comm(Comm* c) {
     if (c->device != device) raise(CL_EPARAM, "cl_solver_attach_comm: the communicator's device is not the solver's");
+    if (ipc.on) raise(CL_EPARAM, "cl_solver_attach_comm: the solver already exchanges through CUDA IPC peer stores");
     if (fft && c->world != 1) raise(CL_EPARAM, "cl_solver_attach_comm: the FFT engine runs unsharded (replicas only)");
     if (kind == CL_KIND_ADMM && c->world != 1) raise(CL_EPARAM, "cl_solver_attach_comm: the dense ADMM runs unsharded");
     CU(cudaStreamSynchronize(st));
@@ -1164,9 +1200,128 @@ struct Solver {
     ++t;
   }
 
+  // ---- CUDA IPC peer stores (one process per GPU, no NCCL) ----------------------------------------------
+  // The exchange vectors: ISTA {r, x}; cADMM {beta, x, v, z}.  Phase ph produces vector ph (ISTA: r, x;
+  // cADMM: beta, x, v), which its epilogue stores into every rank's copy; z is pushed before downloads.
+  struct PeerBlob {
+    char magic[8];
+    int32_t world, rank, kind, nvec;
+    int64_t n, m;
+    cudaIpcMemHandle_t vec[4];
+    cudaIpcMemHandle_t sync;
+  };
+  static_assert(sizeof(PeerBlob) <= CL_PEER_BLOB_BYTES, "peer blob");
+  std::vector<DevBuf<float>*> ipc_vectors() {
+    if (kind == CL_KIND_ISTA) return {&r, &x};
+    return {&beta, &x, &v, &z};
+  }
+  void ipc_export(int rk, int ws, unsigned char* out) {
+    if (ws < 1 || ws > kIpcMaxRanks || rk < 0 || rk >= ws)
+      raise(CL_EPARAM, "cl_solver_peer_export: need 0 <= rank < world <= 8");
+    if (fft || kind == CL_KIND_ADMM)
+      raise(CL_EPARAM, "cl_solver_peer_export: the sharded solve runs the direct ISTA / cADMM engine");
+    if (ipc.on || comm) raise(CL_EPARAM, "cl_solver_peer_export: the solver is already attached");
+    CU(cudaStreamSynchronize(st));
+    set_shard(rk, ws);
+    all_ranges();
+    PeerBlob b;
+    std::memset(&b, 0, sizeof(b));
+    std::memcpy(b.magic, "CLPEER01", 8);
+    b.world = ws;
+    b.rank = rk;
+    b.kind = kind;
+    b.n = n;
+    b.m = m;
+    const auto vecs = ipc_vectors();
+    b.nvec = static_cast<int32_t>(vecs.size());
+    for (size_t i = 0; i < vecs.size(); ++i) {
+      vecs[i]->make_plain(st);
+      CU(cudaIpcGetMemHandle(&b.vec[i], vecs[i]->p));
+    }
+    if (!ipc.own) {
+      CU(cudaMalloc(reinterpret_cast<void**>(&ipc.own), sizeof(IpcSync)));
+      CU(cudaMemset(ipc.own, 0, sizeof(IpcSync)));
+    }
+    CU(cudaIpcGetMemHandle(&b.sync, ipc.own));
+    std::memset(out, 0, CL_PEER_BLOB_BYTES);
+    std::memcpy(out, &b, sizeof(b));
+  }
+  void ipc_attach(const unsigned char* blobs) {
+    if (!ipc.own) raise(CL_EPARAM, "cl_solver_peer_attach: export this rank's blob first");
+    std::vector<PeerBlob> b(static_cast<size_t>(world));
+    for (int q = 0; q < world; ++q) std::memcpy(&b[static_cast<size_t>(q)], blobs + static_cast<size_t>(q) * CL_PEER_BLOB_BYTES, sizeof(PeerBlob));
+    for (int q = 0; q < world; ++q) {
+      const PeerBlob& e = b[static_cast<size_t>(q)];
+      if (std::memcmp(e.magic, "CLPEER01", 8) != 0 || e.world != world || e.rank != q || e.kind != kind || e.n != n ||
+          e.m != m)
+        raise(CL_EPARAM, "cl_solver_peer_attach: the blobs are not every rank's export of this problem, in rank order");
+    }
+    const auto vecs = ipc_vectors();
+    std::vector<std::vector<float*>> peer(vecs.size(), std::vector<float*>(static_cast<size_t>(world), nullptr));
+    for (int q = 0; q < world; ++q) {
+      if (q == rank) {
+        ipc.sync.s[q] = ipc.own;
+        for (size_t i = 0; i < vecs.size(); ++i) peer[i][static_cast<size_t>(q)] = vecs[i]->p;
+        continue;
+      }
+      const PeerBlob& e = b[static_cast<size_t>(q)];
+      void* sp = nullptr;
+      CU(cudaIpcOpenMemHandle(&sp, e.sync, cudaIpcMemLazyEnablePeerAccess));
+      ipc.opened.push_back(sp);
+      ipc.sync.s[q] = static_cast<IpcSync*>(sp);
+      for (size_t i = 0; i < vecs.size(); ++i) {
+        void* vp = nullptr;
+        CU(cudaIpcOpenMemHandle(&vp, e.vec[i], cudaIpcMemLazyEnablePeerAccess));
+        ipc.opened.push_back(vp);
+        peer[i][static_cast<size_t>(q)] = static_cast<float*>(vp);
+      }
+    }
+    npeer = world - 1;
+    for (int ph = 0; ph < phase_count(); ++ph) {
+      int k = 0;
+      for (int q = 0; q < world; ++q)
+        if (q != rank) peer_out[ph][k++] = peer[static_cast<size_t>(ph)][static_cast<size_t>(q)];
+    }
+    if (kind == CL_KIND_CADMM)
+      for (int q = 0; q < world; ++q) ipc.z.p[q] = peer[3][static_cast<size_t>(q)];
+    ipc.on = true;
+  }
+  void ipc_barrier() {
+    ++ipc.seq;
+    launch_ipc_signal(ipc.sync, world, rank, ipc.seq, st);
+    launch_ipc_wait(ipc.own, world, rank, ipc.seq, st);
+  }
+  void ipc_step(int want) {
+    for (int ph = 0; ph < phase_count(); ++ph) {
+      run_phase_only(ph, want && ph == phase_count() - 1);
+      ipc_barrier();
+    }
+    CU(cudaGetLastError());
+    ++t;
+  }
+  // every rank's share of the check sums, summed in rank order (after the last phase's barrier)
+  void ipc_metrics() {
+    launch_ipc_push_met(ipc.sync, world, rank, met.p, st);
+    ipc_barrier();
+    IpcSync h;
+    CU(cudaMemcpyAsync(&h, ipc.own, sizeof(IpcSync), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    if (h.timed_out) raise(CL_ECOMM, "peer-store transport: a rank stopped answering (wait timed out)");
+    for (int i = 0; i < 3; ++i) {
+      double sum = 0.0;
+      for (int q = 0; q < world; ++q) sum += h.met[q][i];
+      met_host[i] = sum;
+    }
+    met_host[3] = 0.0;
+  }
+
   void one_step(int want) {
     if (world != 1 && comm) {
       comm_step(want);
+      return;
+    }
+    if (world != 1 && ipc.on) {
+      ipc_step(want);
       return;
     }
     if (world != 1) raise(CL_EPARAM, "cl_solver_step: sharded solvers advance with cl_solver_run_phase");
@@ -1351,6 +1506,12 @@ struct Solver {
   void step_checked(double* metric, int* nonfinite) {
     one_step(1);
     launch_metrics_final(blk.p, met.p, st);
+    if (world != 1 && ipc.on) {
+      ipc_metrics();
+      collect_profile();
+      metric_from(met_host, metric, nonfinite);
+      return;
+    }
     if (world != 1 && comm) comm_allreduce_sum(comm, met.p, 3, st);  // every rank's share of the sums
     CU(cudaMemcpyAsync(met_host, met.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
@@ -1382,6 +1543,10 @@ struct Solver {
     int64_t len = 0;
     float* p = field_ptr(kind == CL_KIND_ISTA ? "x" : "z", &len);
     if (world != 1 && comm && kind != CL_KIND_ISTA) comm_gather(comm, p, outs_of, st);
+    if (world != 1 && ipc.on && kind != CL_KIND_ISTA) {
+      launch_ipc_push_slice(ipc.z, world, rank, p, out_lo, out_hi, st);
+      ipc_barrier();
+    }
     return p;
   }
 
@@ -2370,6 +2535,21 @@ void cl_comm_destroy(cl_comm* c) {
   comm_destroy(c->c);
   delete c;
 }
+cl_status cl_solver_peer_export(cl_solver* h, int rank, int world, unsigned char* blob) {
+  CL_GUARD_BEGIN
+  if (!h || !blob) raise(CL_EPARAM, "cl_solver_peer_export: null argument");
+  CU(cudaSetDevice(h->impl->device));
+  h->impl->ipc_export(rank, world, blob);
+  CL_GUARD_END
+}
+cl_status cl_solver_peer_attach(cl_solver* h, const unsigned char* blobs) {
+  CL_GUARD_BEGIN
+  if (!h || !blobs) raise(CL_EPARAM, "cl_solver_peer_attach: null argument");
+  CU(cudaSetDevice(h->impl->device));
+  h->impl->ipc_attach(blobs);
+  CL_GUARD_END
+}
+
 cl_status cl_solver_attach_comm(cl_solver* h, cl_comm* c) {
   CL_GUARD_BEGIN
   if (!c || !c->c) raise(CL_EPARAM, "cl_solver_attach_comm: null communicator");

@@ -172,6 +172,56 @@ class NativeComm:
             self._h = None
 
 
+PEER_BLOB_BYTES = 512  # CL_PEER_BLOB_BYTES
+
+
+class IpcPeers:
+    """One process per GPU with no NCCL: CUDA IPC peer stores (cl_solver_peer_export / _attach).  Each rank
+    exports its solver's exchange vectors, the blobs travel over any channel (``exchange``: a callable that
+    maps this rank's blob to the list of every rank's blob, e.g. ``torch.distributed.all_gather_object``),
+    and from then on the solver's steps and run loop store each phase's slice straight into every rank's
+    copy and order the phases through device flags.  Destroying the attached solvers is collective."""
+
+    @staticmethod
+    def export(state, rank: int, world: int) -> bytes:
+        buf = C.create_string_buffer(PEER_BLOB_BYTES)
+        _check(lib.cl_solver_peer_export(state.handle, rank, world, buf))
+        return buf.raw
+
+    @staticmethod
+    def attach(state, blobs) -> None:
+        if any(len(b) != PEER_BLOB_BYTES for b in blobs):
+            raise ValueError("IpcPeers.attach: every blob is PEER_BLOB_BYTES long")
+        _check(lib.cl_solver_peer_attach(state.handle, b"".join(blobs)))
+
+    @classmethod
+    def connect(cls, state, rank: int, world: int, exchange) -> None:
+        cls.attach(state, exchange(cls.export(state, rank, world)))
+
+    @classmethod
+    def from_torch(cls, state, group=None) -> None:
+        """Every rank of a torch.distributed group (any backend): the blobs are all-gathered as objects."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+
+        def exchange(blob):
+            out = [None] * world
+            dist.all_gather_object(out, blob, group=group)
+            return out
+        cls.connect(state, rank, world, exchange)
+
+
+class TorchIpc:
+    """The ``comm=`` of ista_run / cadmm_run for the CUDA IPC peer-store transport over a torch.distributed
+    group: attach(state) exports, all-gathers and attaches every rank's blob (IpcPeers.from_torch)."""
+
+    def __init__(self, group=None):
+        self.group = group
+
+    def attach(self, state) -> None:
+        IpcPeers.from_torch(state, self.group)
+
+
 def sharded_step(shard: CudaShard, gather: TorchGather, iters: int = 1):
     """Advance a CudaShard `iters` iterations; collectives run on the solver's stream."""
     import torch

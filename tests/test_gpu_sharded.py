@@ -2,6 +2,8 @@
 inside the library (cl_group_*, peer-copy transport: every rank on device 0), and the NCCL paths at world
 size 1 (cl_group_* over ncclCommInitAll, cl_comm_* + cl_solver_attach_comm).  Every sharding must give the
 unsharded iterate bitwise: each output is computed by the same arithmetic on whichever rank owns it."""
+import os
+
 import numpy as np
 import pytest
 
@@ -98,3 +100,31 @@ def test_cpp_adapter_sharded_config4():
     print(out.stdout)
     assert out.returncode == 0 and "PASS" in out.stdout and out.stdout.count("bitwise equal") == 2, \
         out.stdout + out.stderr
+
+
+@pytest.mark.parametrize("kind,n,world", [("ista", 1 << 18, 2), ("cadmm", 1 << 16, 2), ("ista", 1 << 16, 3)])
+def test_ipc_peer_transport_processes(kind, n, world, tmp_path):
+    """One process per rank (all on device 0) over the CUDA IPC peer-store transport (cl_solver_peer_export /
+    _attach; no NCCL): the run loop's iterations, trace and final iterate equal the unsharded solve's, and the
+    exchanged vectors are complete on every rank, bitwise."""
+    import subprocess
+    import sys
+    worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "helpers", "ipc_worker.py")
+    procs = [subprocess.Popen([sys.executable, worker, kind, str(n), str(r), str(world), str(tmp_path)],
+                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True) for r in range(world)]
+    outs = [pr.communicate(timeout=300)[0] for pr in procs]
+    assert all(pr.returncode == 0 for pr in procs), outs
+    p = orc.make_problem(n, n // 4, n // 256, 5)
+    cfg = cl.SolverConfig(max_iter=12, check_every=4, target_mse=1e-30)
+    run = cl.ista_run if kind == "ista" else cl.cadmm_run
+    ref = run(p.y, op_of(p), cfg, truth=p.x_true)
+    setup = cl.ista_setup if kind == "ista" else cl.cadmm_setup
+    solo = setup(op_of(p), p.y, cfg)
+    solo.step(12)
+    for r in range(world):
+        got = dict(np.load(tmp_path / f"out_{r}.npz"))
+        assert int(got["iterations"]) == ref.iterations == 12
+        assert np.array_equal(got["final_x"], ref.final_x)
+        assert np.allclose(got["trace"][:, 1], [t.value for t in ref.mse_trace], rtol=1e-12, atol=0)
+        for f in (("x", "r") if kind == "ista" else ("x", "beta", "v")):
+            assert np.array_equal(got[f], solo.get(f)), (r, f)
