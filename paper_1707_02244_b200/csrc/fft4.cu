@@ -207,6 +207,12 @@ __host__ __device__ constexpr int row_pitch(int N2) { return N2 + N2 / 16 + 1; }
 __device__ __forceinline__ float2 tw_n(const float2* __restrict__ twA, const float2* __restrict__ twB, int idx) {
   return cmulf(__ldg(twB + (idx >> 12)), __ldg(twA + (idx & 4095)));
 }
+// the same e^{-2 pi i idx / N} (N = 2^lg, idx < N) computed in registers (sincospif, ~1 ulp): no load latency
+__device__ __forceinline__ float2 tw_calc(int idx, int lg) {
+  float s, c;
+  sincospif(-ldexpf(static_cast<float>(idx), 1 - lg), &s, &c);
+  return make_float2(c, s);
+}
 
 // Columns forward: input real u[j] (j = n1 N2 + n2).
 // REAL: the input is read as N complex values z[j] = (u[2j], u[2j+1]) (the real plans); else as the real
@@ -329,6 +335,11 @@ k_rows_r2c(float2* __restrict__ T, const float4* __restrict__ H2, int conj_h, in
   extern __shared__ float2 sm[];
   constexpr int upc = units_per_cta(N2, FINE), slots = 2 * upc, P = row_pitch(N2), cnt = slots * N2;
   const int kmul = N1 * A;
+  const int lgN = 31 - __clz(kmul * N2);
+  // the four-step twiddle: computed in registers for the DRAM-resident plans (the table loads' latency sat
+  // in front of the first and last passes: cADMM 2^24 1.05 vs 1.11 ms), table loads for the L2-resident
+  // FINE plans (cached, and cheaper than sincospif there)
+  const auto twiddle = [&](int idx) { return FINE ? tw_n(twA, twB, idx) : tw_calc(idx, lgN); };
   __shared__ int rows_s[slots], k1s[slots], kbs[slots];
   __shared__ float2 wrow[upc];
   if (threadIdx.x < slots) {
@@ -344,7 +355,7 @@ k_rows_r2c(float2* __restrict__ T, const float4* __restrict__ H2, int conj_h, in
   __syncthreads();
   for (int e = threadIdx.x; e < cnt; e += threads_of(FINE)) {
     const int s = e / N2, n2 = e - s * N2, R = rows_s[s];
-    if (R >= 0) sm[s * P + pad16(n2)] = cmulf(T[static_cast<int64_t>(R) * N2 + n2], tw_n(twA, twB, n2 * k1s[s]));
+    if (R >= 0) sm[s * P + pad16(n2)] = cmulf(T[static_cast<int64_t>(R) * N2 + n2], twiddle(n2 * k1s[s]));
   }
   __syncthreads();
   dif_from<N2, N2, slots, threads_of(FINE)>(sm, P, tw2);
@@ -378,7 +389,7 @@ k_rows_r2c(float2* __restrict__ T, const float4* __restrict__ H2, int conj_h, in
   for (int e = threadIdx.x; e < cnt; e += threads_of(FINE)) {
     const int s = e / N2, n2 = e - s * N2, R = rows_s[s];
     if (R >= 0)
-      T[static_cast<int64_t>(R) * N2 + n2] = cmulf_conj(sm[s * P + pad16(n2)], tw_n(twA, twB, n2 * k1s[s]));
+      T[static_cast<int64_t>(R) * N2 + n2] = cmulf_conj(sm[s * P + pad16(n2)], twiddle(n2 * k1s[s]));
   }
 }
 
@@ -395,12 +406,13 @@ __global__ void __launch_bounds__(kThr, 4) k_mid(float2* __restrict__ T, int N1,
   const int per_row = B / C;
   const int p = blockIdx.x / per_row, n30 = (blockIdx.x - p * per_row) * C;
   const int k1 = digit_rev(p, N1);
+  const int lgN = 31 - __clz(N1 * N2);  // the four-step twiddle in registers (tw_calc)
   float2* row = T + static_cast<int64_t>(p) * N2;
 #pragma unroll
   for (int e = threadIdx.x; e < cnt; e += kThr) {
     const int i = e / C, w = e - i * C, n2 = i * B + n30 + w;
     const float2 v = row[n2];
-    sm[w * P + pad16(i)] = FWD ? cmulf(v, tw_n(twA, twB, n2 * k1)) : v;
+    sm[w * P + pad16(i)] = FWD ? cmulf(v, tw_calc(n2 * k1, lgN)) : v;
   }
   __syncthreads();
   if constexpr (FWD) dif_from<A, A, C>(sm, P, twM);
@@ -409,7 +421,7 @@ __global__ void __launch_bounds__(kThr, 4) k_mid(float2* __restrict__ T, int N1,
   for (int e = threadIdx.x; e < cnt; e += kThr) {
     const int i = e / C, w = e - i * C, n2 = i * B + n30 + w;
     const float2 v = sm[w * P + pad16(i)];
-    row[n2] = FWD ? v : cmulf_conj(v, tw_n(twA, twB, n2 * k1));
+    row[n2] = FWD ? v : cmulf_conj(v, tw_calc(n2 * k1, lgN));
   }
 }
 
