@@ -492,6 +492,7 @@ def main():
     else:
         peak, peak_source = cl.ffma_peak_tflops(local_rank), "live FFMA microbenchmark (cl_ffma_peak)"
     achieved = useful / (k_ms * 1e-3) / 1e12
+    ffma_peak = cl.ffma_peak_tflops(local_rank)
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
@@ -665,6 +666,13 @@ def main():
                                            ") as 3 tensor-core MMAs per flop: " + tc_note(n))}
                             if k_name == "k_tc_dense" else {}),
                          "step_tflops": algorithmic_flops(w) / world / (ms_per_step * 1e-3) / 1e12,
+                         # the north_star's own bar: the iteration's algorithmic flops (4 m n ISTA, 6 n^2 cADMM)
+                         # per second against the FP32 FFMA roofline (>= 0.6 asked), measured on this GPU
+                         "vs_fp32_ffma_roofline": {
+                             "algorithmic_tflops": algorithmic_flops(w) / world / (ms_per_step * 1e-3) / 1e12,
+                             "ffma_peak_tflops": ffma_peak,
+                             "frac": algorithmic_flops(w) / world / (ms_per_step * 1e-3) / 1e12 / ffma_peak,
+                             "peak_source": "live FFMA microbenchmark (cl_ffma_peak)"},
                          "phase_ms": phase_mean},
             "clocks": clocks.summary(),
             # per step: ISTA 2 products + gather/scatter + update; cADMM 3 products + 3 epilogues; each
