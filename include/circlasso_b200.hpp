@@ -905,6 +905,21 @@ RecoveryReport<Scalar> cadmm_run(const Vector<Scalar>& y, const PartialCirculant
 // iterate equals the unsharded solve's bitwise.  One process per GPU instead: cl_comm_init_rank +
 // cl_solver_attach_comm on a solver handle.
 enum class Transport { kNccl = CL_TRANSPORT_NCCL, kCopy = CL_TRANSPORT_COPY, kPeer = CL_TRANSPORT_PEER };
+// One process per GPU without NCCL (cl_solver_peer_export / _attach): every rank exports its state's blob,
+// the caller hands all `world` blobs (rank order, concatenated) to every rank, each rank attaches; the state's
+// steps then run the sharded iteration with the slices stored straight into every rank's copy (CUDA IPC).
+template <typename State>
+std::vector<unsigned char> peer_export(State& state, int rank, int world) {
+  state.dev.use(0, State::kFields, static_cast<int>(sizeof(State::kFields) / sizeof(State::kFields[0])));
+  std::vector<unsigned char> blob(CL_PEER_BLOB_BYTES);
+  check(cl_solver_peer_export(state.dev.handle(), rank, world, blob.data()));
+  return blob;
+}
+template <typename State>
+void peer_attach(State& state, const std::vector<unsigned char>& blobs) {
+  check(cl_solver_peer_attach(state.dev.handle(), blobs.data()));
+}
+
 template <typename Scalar = double>
 class ShardedSolve {
  public:
