@@ -61,6 +61,9 @@ constexpr int kTcSmem = kOffStg + 2 * kStg * 4;
 #endif
 constexpr int kSPD = TC_SPD;  // TF32: steps accumulated in TMEM between drains (divides 8)
 constexpr int kTmemCols = 512;  // two 128 x 256 fp32 accumulators
+#ifndef TC_TWO_MMA
+#define TC_TWO_MMA 0  // diagnostic builds: drop the Alo.Bhi product (u rounded to one fp16 term) to measure its error
+#endif
 #ifndef TC_MMA_ONLY
 #define TC_MMA_ONLY 0  // diagnostic builds (tools/microbench): no tile production after the first fill, no drain
 #endif
@@ -578,11 +581,11 @@ k_tc_dense(const float* __restrict__ h, const float* __restrict__ u, int64_t n, 
         if constexpr (kPair) {
           mma_pair(tacc, dah, dbh, idesc, (first && kk == 0) ? 0u : 1u, F16);
           mma_pair(tacc, dah, dbl, idesc, 1, F16);
-          mma_pair(tacc, dal, dbh, idesc, 1, F16);
+          if (!TC_TWO_MMA) mma_pair(tacc, dal, dbh, idesc, 1, F16);
         } else if constexpr (F16) {
           mma_f16(tacc, dah, dbh, idesc, (first && kk == 0) ? 0u : 1u);
           mma_f16(tacc, dah, dbl, idesc, 1);
-          mma_f16(tacc, dal, dbh, idesc, 1);
+          if (!TC_TWO_MMA) mma_f16(tacc, dal, dbh, idesc, 1);
         } else {
           mma_tf32(tacc, dah, dbh, idesc, (first && kk == 0) ? 0u : 1u);
           mma_tf32(tacc, dah, dbl, idesc, 1);
