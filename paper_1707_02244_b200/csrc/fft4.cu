@@ -77,9 +77,12 @@ __device__ __forceinline__ void dftr(float2 (&v)[R]) {
 #pragma unroll
       for (int k = 0; k < half; ++k) {
         const int e = k * (16 / (2 * half));
-        const float2 w = make_float2(kC16[e], SG * kS16[e]);
-        const float2 u = t[base + k];
-        const float2 x = cmulf(t[base + k + half], w);
+        const float2 u = t[base + k], bb = t[base + k + half];
+        // w = e^{SG 2 pi i e / 16}; the trivial factors (e = 0: 1, e = 4: SG i) as moves and negations
+        // (e is a constant after unrolling, so the branches fold)
+        const float2 x = e == 0 ? bb
+                         : e == 4 ? make_float2(-SG * bb.y, SG * bb.x)
+                                  : cmulf(bb, make_float2(kC16[e], SG * kS16[e]));
         t[base + k] = make_float2(u.x + x.x, u.y + x.y);
         t[base + k + half] = make_float2(u.x - x.x, u.y - x.y);
       }
