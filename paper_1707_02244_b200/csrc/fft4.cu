@@ -409,13 +409,22 @@ __global__ void __launch_bounds__(kThr, 4) k_mid(float2* __restrict__ T, int N1,
   const int per_row = B / C;
   const int p = blockIdx.x / per_row, n30 = (blockIdx.x - p * per_row) * C;
   const int k1 = digit_rev(p, N1);
-  const int lgN = 31 - __clz(N1 * N2);  // the four-step twiddle in registers (tw_calc)
+  const int lgN = 31 - __clz(N1 * N2);
   float2* row = T + static_cast<int64_t>(p) * N2;
+  // the four-step twiddle w^{n2 k1} in registers: a thread's elements step n2 by (kThr / C) B, so after one
+  // sincospif for its first element each next twiddle is one complex multiply by the step's (~1e-7 relative
+  // after the 15 steps, against two table loads or one sincospif per element)
+  static_assert(kThr % C == 0, "a thread keeps its column");
+  const int n2_0 = (threadIdx.x / C) * B + n30 + threadIdx.x % C;
+  const int64_t step = static_cast<int64_t>(kThr / C) * B * k1 % (static_cast<int64_t>(N1) * N2);
+  const float2 w_step = tw_calc(static_cast<int>(step), lgN);
+  float2 w_e = tw_calc(n2_0 * k1, lgN);
 #pragma unroll
   for (int e = threadIdx.x; e < cnt; e += kThr) {
     const int i = e / C, w = e - i * C, n2 = i * B + n30 + w;
     const float2 v = row[n2];
-    sm[w * P + pad16(i)] = FWD ? cmulf(v, tw_calc(n2 * k1, lgN)) : v;
+    sm[w * P + pad16(i)] = FWD ? cmulf(v, w_e) : v;
+    if (FWD) w_e = cmulf(w_e, w_step);
   }
   __syncthreads();
   if constexpr (FWD) dif_from<A, A, C>(sm, P, twM);
@@ -424,7 +433,8 @@ __global__ void __launch_bounds__(kThr, 4) k_mid(float2* __restrict__ T, int N1,
   for (int e = threadIdx.x; e < cnt; e += kThr) {
     const int i = e / C, w = e - i * C, n2 = i * B + n30 + w;
     const float2 v = sm[w * P + pad16(i)];
-    row[n2] = FWD ? v : cmulf_conj(v, tw_calc(n2 * k1, lgN));
+    row[n2] = FWD ? v : cmulf_conj(v, w_e);
+    if (!FWD) w_e = cmulf(w_e, w_step);
   }
 }
 
