@@ -97,7 +97,7 @@ __device__ __forceinline__ void dftr(float2 (&v)[R]) {
 // consecutive elements per thread; unpadded, all lanes would hit one bank).
 __host__ __device__ __forceinline__ int pad16(int i) { return i + (i >> 4); }
 
-constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
+__host__ __device__ constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
 // Radix schedule of a length-N transform: the remainder radix 2^(log2 N mod 4) first
 // (a large stride, conflict-free), then radix 16 down to the last stage.
 template <int N, int L>
@@ -339,12 +339,18 @@ k_rows_r2c(float2* __restrict__ T, const float4* __restrict__ H2, int conj_h, in
   constexpr int upc = units_per_cta(N2, FINE), slots = 2 * upc, P = row_pitch(N2), cnt = slots * N2;
   const int kmul = N1 * A;
   const int lgN = 31 - __clz(kmul * N2);
-  // the four-step twiddle: computed in registers for the DRAM-resident plans (the table loads' latency sat
-  // in front of the first and last passes: cADMM 2^24 1.05 vs 1.11 ms), table loads for the L2-resident
-  // FINE plans (cached, and cheaper than sincospif there)
-  const auto twiddle = [&](int idx) { return FINE ? tw_n(twA, twB, idx) : tw_calc(idx, lgN); };
+  // the four-step twiddle w^{n2 k1} of slot s.  Rows of 256+ points: two per-slot shared tables, n2 = h LO + l,
+  // w^{h LO k1} w^{l k1} (slots x (LO + HI) sincospif per CTA instead of two per element, no load latency:
+  // ISTA 2^20 0.079 vs 0.083 ms, cADMM 2^22 0.283 vs 0.288).  The three-level plans' 64/128-point rows:
+  // sincospif per element (the tables' build and barrier in front of the loads lost: 2^24 0.983 vs 0.961).
+  constexpr bool kTab = N2 >= 256;
+  constexpr int LO = kTab ? 1 << ((ilog2(N2) + 1) / 2) : 1, HI = kTab ? N2 / LO : 1;
+  __shared__ float2 tw_lo[kTab ? slots : 1][LO], tw_hi[kTab ? slots : 1][HI];
   __shared__ int rows_s[slots], k1s[slots], kbs[slots];
   __shared__ float2 wrow[upc];
+  const auto twiddle = [&](int s, int n2) {
+    return kTab ? cmulf(tw_hi[s][n2 / LO], tw_lo[s][n2 % LO]) : tw_calc(n2 * k1s[s], lgN);
+  };
   if (threadIdx.x < slots) {
     const int u = blockIdx.x * upc + (threadIdx.x >> 1);
     const int kb = (threadIdx.x & 1) ? (kmul - u) & (kmul - 1) : u;
@@ -356,9 +362,17 @@ k_rows_r2c(float2* __restrict__ T, const float4* __restrict__ H2, int conj_h, in
     if (!(threadIdx.x & 1)) wrow[threadIdx.x >> 1] = tw_n(twCA, twCB, kb);  // W^{kb}
   }
   __syncthreads();
+  if constexpr (kTab) {
+    for (int e = threadIdx.x; e < slots * (LO + HI); e += threads_of(FINE)) {
+      const int s = e / (LO + HI), j = e - s * (LO + HI);
+      if (j < LO) tw_lo[s][j] = tw_calc(j * k1s[s], lgN);  // j k1 < N (n2 k1 < N for every plan)
+      else tw_hi[s][j - LO] = tw_calc((j - LO) * LO * k1s[s], lgN);
+    }
+    __syncthreads();
+  }
   for (int e = threadIdx.x; e < cnt; e += threads_of(FINE)) {
     const int s = e / N2, n2 = e - s * N2, R = rows_s[s];
-    if (R >= 0) sm[s * P + pad16(n2)] = cmulf(T[static_cast<int64_t>(R) * N2 + n2], twiddle(n2 * k1s[s]));
+    if (R >= 0) sm[s * P + pad16(n2)] = cmulf(T[static_cast<int64_t>(R) * N2 + n2], twiddle(s, n2));
   }
   __syncthreads();
   dif_from<N2, N2, slots, threads_of(FINE)>(sm, P, tw2);
@@ -392,7 +406,7 @@ k_rows_r2c(float2* __restrict__ T, const float4* __restrict__ H2, int conj_h, in
   for (int e = threadIdx.x; e < cnt; e += threads_of(FINE)) {
     const int s = e / N2, n2 = e - s * N2, R = rows_s[s];
     if (R >= 0)
-      T[static_cast<int64_t>(R) * N2 + n2] = cmulf_conj(sm[s * P + pad16(n2)], twiddle(n2 * k1s[s]));
+      T[static_cast<int64_t>(R) * N2 + n2] = cmulf_conj(sm[s * P + pad16(n2)], twiddle(s, n2));
   }
 }
 
