@@ -21,7 +21,9 @@ download, max over ranks).  Rank 0 prints one JSON line; native output (NCCL
 banners) goes to stderr.  The default line also carries the FFT engine, the
 cADMM rate at n=2^20 and the time to recovery (MSE <= 1e-4) on both engines.
 BENCH_FORCE_SHARDED=1 runs the sharded path with a single rank; BENCH_TRANSPORT=ipc (default: the exchange fused
-into the epilogues as CUDA IPC peer stores) or nccl (the library's NCCL broadcasts) picks the N>1 exchange.
+into the epilogues as CUDA IPC peer stores) or nccl (the library's NCCL broadcasts) picks the N>1 exchange;
+BENCH_SHARE_DEVICE=1 maps the ranks round-robin onto the visible GPUs (a functional run of the N>1 path on one
+GPU: gloo timing collectives, the IPC exchange).
 """
 from __future__ import annotations
 
@@ -398,10 +400,23 @@ def main():
     import paper_1707_02244_b200 as cl
     from paper_1707_02244_b200 import dist as cdist
 
+    # BENCH_SHARE_DEVICE=1: every rank on the visible GPUs round-robin (a functional run of the N > 1 path on
+    # fewer GPUs: gloo for the timing collectives, the IPC exchange -- NCCL refuses two ranks on one GPU)
+    share = os.environ.get("BENCH_SHARE_DEVICE") == "1"
+    if share:
+        local_rank = local_rank % torch.cuda.device_count()
     torch.cuda.set_device(local_rank)
     if sharded:
         import torch.distributed as tdist
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if share:
+            tdist.init_process_group("gloo")
+        else:
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    def max_over_ranks(v: float) -> float:
+        t = torch.tensor([v], device="cpu" if share else "cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
     assert args.warmup >= 3 or os.environ.get("BENCH_ALLOW_SHORT_WARMUP"), "need >= 3 warm-up steps"
 
     prob = cl.make_problem(w["n"], w["m"], w["k"], w["seed"])
@@ -460,9 +475,7 @@ def main():
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(step_ms)
     if sharded:
-        t = torch.tensor([total_ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms = max_over_ranks(total_ms)
     ms_per_step = total_ms / args.steps
     value = 1e3 / ms_per_step  # iterations/s of the (single, sharded) solve
     st.profile(0)
@@ -538,9 +551,7 @@ def main():
                   device=local_rank, comm=comm)
         e2e_s = time.perf_counter() - t0
         assert rep.iterations == args.steps
-        t = torch.tensor([e2e_s], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        e2e_s = max_over_ranks(e2e_s)
         e2e = {"value": args.steps / e2e_s, "unit": "iterations/s", "h2d_bytes_per_step": world * h2d / args.steps,
                "d2h_bytes_per_step": d2h / args.steps, "wall_s": e2e_s,
                "note": f"{world} ranks: ista_run/cadmm_run(..., comm={type(comm).__name__}) from host fp64 buffers "
