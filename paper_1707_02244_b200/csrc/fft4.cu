@@ -491,6 +491,23 @@ __device__ __forceinline__ float emit_out(const Fft4Out& o, int64_t j, float v) 
     return 0.f;
   }
 }
+// Before the inverse stages: L2 prefetch of the lines the consumer will read at this CTA's outputs (z and nu
+// for beta, x for the ISTA update), so the emit loop's loads hit L2 instead of waiting on DRAM.  Row i of the
+// tile covers outputs [(i N2 + c0) f, + B f) with f = 2 for real plans: B f floats, one or two 128-byte lines.
+template <int B, bool REAL>
+__device__ __forceinline__ void prefetch_consumer(const Fft4Out& o, int N1, int N2, int c0, int nthreads) {
+  const float* a = o.mode == Fft4Out::kBeta ? o.z : o.mode == Fft4Out::kIstaStep ? o.x : nullptr;
+  if (!a) return;
+  const float* b = o.mode == Fft4Out::kBeta ? o.nu : nullptr;
+  constexpr int f = REAL ? 2 : 1, lines = (B * f * 4 + 127) / 128;
+  for (int e = threadIdx.x; e < N1 * lines; e += nthreads) {
+    const int i = e / lines, l = e - i * lines;
+    const int64_t j = (static_cast<int64_t>(i) * N2 + c0) * f + l * 32;
+    if (j >= o.n_valid) continue;
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(a + j));
+    if (b) asm volatile("prefetch.global.L2 [%0];" ::"l"(b + j));
+  }
+}
 // REAL: element j of the inverse holds y[2j] + i y[2j+1]; else Re = y[j].
 template <int N1, bool REAL, int FINE = 0>
 __global__ void __launch_bounds__(threads_of(FINE), N1 <= 256 ? 4 : 1) k_cols_inv(const float2* __restrict__ T, Fft4Out o, int N2,
@@ -504,6 +521,7 @@ __global__ void __launch_bounds__(threads_of(FINE), N1 <= 256 ? 4 : 1) k_cols_in
     sm[w * P + pad16(i)] = T[static_cast<int64_t>(i) * N2 + c0 + w];
   }
   __syncthreads();
+  if (FINE == 0) prefetch_consumer<B, REAL>(o, N1, N2, c0, threads_of(FINE));  // DRAM-resident plans
   dit_from<N1, N1, B, threads_of(FINE)>(sm, P, tw1);
 #pragma unroll
   for (int e = threadIdx.x; e < cnt; e += threads_of(FINE)) {
@@ -535,6 +553,7 @@ __global__ void __launch_bounds__(threads_of(FINE), N1 <= 256 ? 4 : 1) k_cols_in
     sm[w * P + pad16(i)] = T[static_cast<int64_t>(i) * N2 + c0 + w];
   }
   __syncthreads();
+  if (FINE == 0) prefetch_consumer<B, REAL>(o, N1, N2, c0, threads_of(FINE));  // DRAM-resident plans
   dit_from<N1, N1, B, threads_of(FINE)>(sm, P, tw1);
 #pragma unroll
   for (int e = threadIdx.x; e < cnt; e += threads_of(FINE)) {
