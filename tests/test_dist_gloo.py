@@ -203,3 +203,21 @@ def test_tensor_core_shard_ranges(world):
         assert prev_o == n
         if kind == 0:
             assert prev_r == m
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_tensor_core_shards_are_whole_cta_pairs(world):
+    """At the bench sizes (n = 2^20, 2^24) every rank's tile range of the tcgen05 plan starts and ends on an even
+    tile, so every rank runs the CTA-pair kernel (cta_group::2: two adjacent 128 x 256-output tiles per pair);
+    host logic only (cl_shard_ranges)."""
+    tile = 128 * 256
+    for lg in (20, 24):
+        n = 1 << lg
+
+        class P:
+            pass
+        p = P()
+        p.n, p.m, p.omega = n, n // 4, np.arange(0, n, 4, dtype=np.int64)
+        for r in range(world):
+            _, outs = shard_ranges(1, p, r, world)
+            assert outs[0] % (2 * tile) == 0 and outs[1] % (2 * tile) == 0, (lg, r, outs)
