@@ -343,13 +343,20 @@ k_rows_r2c(float2* __restrict__ T, const float4* __restrict__ H2, int conj_h, in
   // w^{h LO k1} w^{l k1} (slots x (LO + HI) sincospif per CTA instead of two per element, no load latency:
   // ISTA 2^20 0.079 vs 0.083 ms, cADMM 2^22 0.283 vs 0.288).  The three-level plans' 64/128-point rows:
   // sincospif per element (the tables' build and barrier in front of the loads lost: 2^24 0.983 vs 0.961).
-  constexpr bool kTab = N2 >= 256;
-  constexpr int LO = kTab ? 1 << ((ilog2(N2) + 1) / 2) : 1, HI = kTab ? N2 / LO : 1;
-  __shared__ float2 tw_lo[kTab ? slots : 1][LO], tw_hi[kTab ? slots : 1][HI];
+  // Short rows (the three-level plans' 64/128 points): the same tables, built while the row loads are in
+  // flight (the loads go to registers first, the table build follows, then the twiddled stores).
+  constexpr bool kLate = N2 < 256;
+  constexpr int LO = 1 << ((ilog2(N2) + 1) / 2), HI = N2 / LO;
+  __shared__ float2 tw_lo[slots][LO], tw_hi[slots][HI];
   __shared__ int rows_s[slots], k1s[slots], kbs[slots];
   __shared__ float2 wrow[upc];
-  const auto twiddle = [&](int s, int n2) {
-    return kTab ? cmulf(tw_hi[s][n2 / LO], tw_lo[s][n2 % LO]) : tw_calc(n2 * k1s[s], lgN);
+  const auto twiddle = [&](int s, int n2) { return cmulf(tw_hi[s][n2 / LO], tw_lo[s][n2 % LO]); };
+  const auto build_tables = [&] {
+    for (int e = threadIdx.x; e < slots * (LO + HI); e += threads_of(FINE)) {
+      const int s = e / (LO + HI), j = e - s * (LO + HI);
+      if (j < LO) tw_lo[s][j] = tw_calc(j * k1s[s], lgN);  // j k1 < N (n2 k1 < N for every plan)
+      else tw_hi[s][j - LO] = tw_calc((j - LO) * LO * k1s[s], lgN);
+    }
   };
   if (threadIdx.x < slots) {
     const int u = blockIdx.x * upc + (threadIdx.x >> 1);
@@ -362,17 +369,29 @@ k_rows_r2c(float2* __restrict__ T, const float4* __restrict__ H2, int conj_h, in
     if (!(threadIdx.x & 1)) wrow[threadIdx.x >> 1] = tw_n(twCA, twCB, kb);  // W^{kb}
   }
   __syncthreads();
-  if constexpr (kTab) {
-    for (int e = threadIdx.x; e < slots * (LO + HI); e += threads_of(FINE)) {
-      const int s = e / (LO + HI), j = e - s * (LO + HI);
-      if (j < LO) tw_lo[s][j] = tw_calc(j * k1s[s], lgN);  // j k1 < N (n2 k1 < N for every plan)
-      else tw_hi[s][j - LO] = tw_calc((j - LO) * LO * k1s[s], lgN);
+  if constexpr (kLate) {
+    constexpr int per = cnt / threads_of(FINE);
+    static_assert(cnt % threads_of(FINE) == 0, "whole rows per thread pass");
+    float2 v[per];
+#pragma unroll
+    for (int k = 0; k < per; ++k) {
+      const int e = threadIdx.x + k * threads_of(FINE), s = e / N2, n2 = e - s * N2, R = rows_s[s];
+      v[k] = R >= 0 ? T[static_cast<int64_t>(R) * N2 + n2] : make_float2(0.f, 0.f);
     }
+    build_tables();
     __syncthreads();
-  }
-  for (int e = threadIdx.x; e < cnt; e += threads_of(FINE)) {
-    const int s = e / N2, n2 = e - s * N2, R = rows_s[s];
-    if (R >= 0) sm[s * P + pad16(n2)] = cmulf(T[static_cast<int64_t>(R) * N2 + n2], twiddle(s, n2));
+#pragma unroll
+    for (int k = 0; k < per; ++k) {
+      const int e = threadIdx.x + k * threads_of(FINE), s = e / N2, n2 = e - s * N2;
+      if (rows_s[s] >= 0) sm[s * P + pad16(n2)] = cmulf(v[k], twiddle(s, n2));
+    }
+  } else {
+    build_tables();
+    __syncthreads();
+    for (int e = threadIdx.x; e < cnt; e += threads_of(FINE)) {
+      const int s = e / N2, n2 = e - s * N2, R = rows_s[s];
+      if (R >= 0) sm[s * P + pad16(n2)] = cmulf(T[static_cast<int64_t>(R) * N2 + n2], twiddle(s, n2));
+    }
   }
   __syncthreads();
   dif_from<N2, N2, slots, threads_of(FINE)>(sm, P, tw2);
