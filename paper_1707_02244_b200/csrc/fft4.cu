@@ -343,9 +343,9 @@ k_rows_r2c(float2* __restrict__ T, const float4* __restrict__ H2, int conj_h, in
   // w^{h LO k1} w^{l k1} (slots x (LO + HI) sincospif per CTA instead of two per element, no load latency:
   // ISTA 2^20 0.079 vs 0.083 ms, cADMM 2^22 0.283 vs 0.288).  The three-level plans' 64/128-point rows:
   // sincospif per element (the tables' build and barrier in front of the loads lost: 2^24 0.983 vs 0.961).
-  // Short rows (the three-level plans' 64/128 points): the same tables, built while the row loads are in
-  // flight (the loads go to registers first, the table build follows, then the twiddled stores).
-  constexpr bool kLate = N2 < 256;
+  // Up to 16 elements per thread: the tables are built while the row loads are in flight (the loads go to
+  // registers first, the table build follows, then the twiddled stores).
+  constexpr bool kLate = cnt / threads_of(FINE) <= 16 && cnt % threads_of(FINE) == 0;
   constexpr int LO = 1 << ((ilog2(N2) + 1) / 2), HI = N2 / LO;
   __shared__ float2 tw_lo[slots][LO], tw_hi[slots][HI];
   __shared__ int rows_s[slots], k1s[slots], kbs[slots];
