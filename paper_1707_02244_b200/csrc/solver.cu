@@ -20,6 +20,7 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "host_common.hpp"
 #include "fft.cuh"
@@ -30,6 +31,16 @@
 #include "dense.cuh"
 #include "comm.hpp"
 #include "ipc.cuh"
+
+// NVTX ranges (SURVEY §5 tracing): every C-ABI entry that launches work and every kernel phase pushes a
+// named range, named after the reference's KernelPhase names (parallel.hpp:173-279), so an nsys/ncu
+// (--nvtx) timeline groups the kernels by phase.  Header-only NVTX v3: a no-op unless a tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 namespace clb {
 void gen_sparse_signal(int64_t n, int64_t k, uint64_t seed, double* values, int64_t* support);
@@ -878,6 +889,7 @@ struct Solver {
 
   // ---- phases -------------------------------------------------------------
   void ista_residual() {
+    NvtxRange nv("cpista residual computation");
     mark(0);
     if (ista_tc) {  // C x on the tensor cores, rows Omega gathered in the epilogue
       CU(launch_conv_dense(plan, hcr.p, x.p, partial.p, st));
@@ -909,6 +921,7 @@ struct Solver {
     mark(2);
   }
   void ista_gradient(int want) {
+    NvtxRange nv("cpista thresholded gradient");
     if (ista_tc) {  // C^T P^T r: scatter r (all rows, after any exchange), dense product
       launch_scatter_real(r.p, omega32.p, ud.p, m, st);
       CU(launch_conv_dense(plan, hc.p, ud.p, partial.p, st));
@@ -927,6 +940,7 @@ struct Solver {
     nphase = 4;
   }
   void admm_beta_phase() {
+    NvtxRange nv("cpadmm primal variables update");
     mark(0);
     CU(launch_conv_dense(plan, hc.p, v.p, partial.p, st));
     mark(1);
@@ -941,6 +955,7 @@ struct Solver {
     mark(2);
   }
   void admm_x_phase() {
+    NvtxRange nv("cpadmm signal recovery");
     CU(launch_conv_dense(plan, hbr.p, beta.p, partial.p, st));
     mark(3);
     EpiArgs a = base_args(0);
@@ -950,6 +965,7 @@ struct Solver {
     mark(4);
   }
   void admm_dual_phase(int want) {
+    NvtxRange nv("cpadmm thresholded variables update");
     CU(launch_conv_dense(plan, hcr.p, x.p, partial.p, st));
     mark(5);
     EpiArgs a = base_args(want);
@@ -2186,6 +2202,7 @@ cl_status cl_mask_gram_inverse(int64_t n, int64_t m, const int64_t* omega, doubl
 
 cl_status cl_circ_matvec(int device, int64_t n, const double* c, const double* x, int transpose, double* out) {
   CL_GUARD_BEGIN
+  NvtxRange nv("cl_circ_matvec");
   if (n < 1) raise(CL_EDIM, "circ_matvec: empty operator");
   ScratchProduct::circ(device, n, c, x, transpose, out);
   CL_GUARD_END
@@ -2194,6 +2211,7 @@ cl_status cl_circ_matvec(int device, int64_t n, const double* c, const double* x
 cl_status cl_partial_matvec(int device, int64_t n, int64_t m, const double* c, const int64_t* omega, const double* xin,
                             double* out_m) {
   CL_GUARD_BEGIN
+  NvtxRange nv("cl_partial_matvec");
   check_mask(omega, m, n);
   // A x through the residual kernel with y = 0: r = -A x.
   std::vector<double> zero(static_cast<size_t>(m), 0.0);
@@ -2232,6 +2250,7 @@ cl_status cl_partial_matvec(int device, int64_t n, int64_t m, const double* c, c
 cl_status cl_partial_transpose_matvec(int device, int64_t n, int64_t m, const double* c, const int64_t* omega,
                                       const double* r_m, double* out_n) {
   CL_GUARD_BEGIN
+  NvtxRange nv("cl_partial_transpose_matvec");
   check_mask(omega, m, n);
   Solver s;
   s.kind = CL_KIND_ISTA;
@@ -2269,6 +2288,7 @@ cl_status cl_partial_transpose_matvec(int device, int64_t n, int64_t m, const do
 cl_status cl_solver_create(int kind, int64_t n, int64_t m, const double* c, const int64_t* omega, const double* y,
                            const cl_config* cfg, int device, cl_solver** out) {
   CL_GUARD_BEGIN
+  NvtxRange nv("cl_solver_create");
   *out = nullptr;
   if (kind != CL_KIND_ISTA && kind != CL_KIND_CADMM && kind != CL_KIND_ADMM)
     raise(CL_EPARAM, "cl_solver_create: unknown solver kind");
@@ -2304,6 +2324,7 @@ cl_status cl_solver_set_truth(cl_solver* h, const double* truth_n) {
 
 cl_status cl_solver_step(cl_solver* h, int64_t iters) {
   CL_GUARD_BEGIN
+  NvtxRange nv("cl_solver_step");
   Solver& s = *h->impl;
   CU(cudaSetDevice(s.device));
   if (iters < 0) raise(CL_EPARAM, "cl_solver_step: iters must be >= 0");
@@ -2313,6 +2334,7 @@ cl_status cl_solver_step(cl_solver* h, int64_t iters) {
 
 cl_status cl_solver_step_checked(cl_solver* h, double* metric, int* nonfinite) {
   CL_GUARD_BEGIN
+  NvtxRange nv("cl_solver_step_checked");
   Solver& s = *h->impl;
   CU(cudaSetDevice(s.device));
   s.step_checked(metric, nonfinite);
@@ -2322,6 +2344,7 @@ cl_status cl_solver_step_checked(cl_solver* h, double* metric, int* nonfinite) {
 cl_status cl_solver_run(cl_solver* h, cl_report* rep, double* final_x, int64_t* trace_iter, double* trace_value,
                         double* trace_seconds, int64_t trace_cap) {
   CL_GUARD_BEGIN
+  NvtxRange nv("cl_solver_run");
   Solver& s = *h->impl;
   CU(cudaSetDevice(s.device));
   run_loop(s, s.cfg, rep, final_x, trace_iter, trace_value, trace_seconds, trace_cap);
@@ -2447,6 +2470,7 @@ cl_status cl_solver_stream(cl_solver* h, void** stream) {
 
 cl_status cl_solver_run_phase(cl_solver* h, int phase) {
   CL_GUARD_BEGIN
+  NvtxRange nv("cl_solver_run_phase");
   Solver& s = *h->impl;
   CU(cudaSetDevice(s.device));
   if (s.kind == CL_KIND_ADMM) {  // padmm_phases: the primal phase, then the rhs phase
@@ -2562,6 +2586,7 @@ cl_status cl_solver_attach_comm(cl_solver* h, cl_comm* c) {
 cl_status cl_group_create(int kind, int64_t n, int64_t m, const double* c, const int64_t* omega, const double* y,
                           const cl_config* cfg, const int* devices, int ndev, int transport, cl_group** out) {
   CL_GUARD_BEGIN
+  NvtxRange nv("cl_group_create");
   if (!out) raise(CL_EPARAM, "cl_group_create: null output");
   *out = nullptr;
   if (ndev < 1 || !devices) raise(CL_EPARAM, "cl_group_create: need at least one device");
@@ -2643,6 +2668,7 @@ cl_status cl_group_set_truth(cl_group* h, const double* truth_n) {
 }
 cl_status cl_group_step(cl_group* h, int64_t iters) {
   CL_GUARD_BEGIN
+  NvtxRange nv("cl_group_step");
   if (iters < 0) raise(CL_EPARAM, "cl_group_step: iters must be >= 0");
   h->g->step(iters);
   CL_GUARD_END
@@ -2650,6 +2676,7 @@ cl_status cl_group_step(cl_group* h, int64_t iters) {
 cl_status cl_group_run(cl_group* h, cl_report* rep, double* final_x, int64_t* trace_iter, double* trace_value,
                        double* trace_seconds, int64_t trace_cap) {
   CL_GUARD_BEGIN
+  NvtxRange nv("cl_group_run");
   Group& g = *h->g;
   run_loop(g, g.ranks.front()->cfg, rep, final_x, trace_iter, trace_value, trace_seconds, trace_cap);
   CL_GUARD_END

@@ -33,6 +33,16 @@ def test_library_exports_every_declared_symbol():
     assert _native.lib.cl_abi_version() == 3
 
 
+def test_nvtx_ranges_name_the_reference_phases():
+    """The tracing ranges carry the reference's KernelPhase names (parallel.hpp:179-307)."""
+    blob = open(_native.lib._name, "rb").read()
+    for name in (b"cpista residual computation", b"cpista thresholded gradient", b"cpadmm primal variables update",
+                 b"cpadmm signal recovery", b"cpadmm thresholded variables update", b"cl_solver_run",
+                 b"cl_group_step"):
+        assert name + b"\0" in blob, name
+    assert b"nvtxRangePushA" in blob or b"libnvToolsExt" in blob or b"NVTX_INJECTION" in blob
+
+
 def test_config_defaults_match_reference():
     cfg = cl.SolverConfig()
     c = cfg._c()
