@@ -427,12 +427,32 @@ def main():
     # sharded: the slice exchange runs inside cl_solver_step, either fused into the producing epilogues as CUDA
     # IPC peer stores (BENCH_TRANSPORT=ipc, the default) or as the library's NCCL broadcasts (=nccl)
     transport = os.environ.get("BENCH_TRANSPORT", "ipc")
-    if sharded:
-        comm = cdist.TorchIpc() if transport == "ipc" else cdist.NativeComm.from_torch(local_rank)
-        comm.attach(st)
-
     def one_step():
         st.step(1)
+
+    failed_states = []  # a state whose IPC attach failed is kept alive: destroying an attached state is collective
+    if sharded and transport == "ipc":
+        # the peer-store transport needs CUDA IPC + peer access between the ranks' GPUs; if any rank cannot attach
+        # or its first exchange fails, every rank (decided together, so the collectives stay matched) falls back
+        # to the library's NCCL exchange on a fresh state
+        ok = 1
+        comm = cdist.TorchIpc()
+        try:
+            comm.attach(st)
+            one_step()
+            st.synchronize()
+        except Exception as e:  # noqa: BLE001 -- reported, then the NCCL transport takes over
+            print(f"bench: rank {rank}: IPC peer-store transport failed ({e}); falling back to NCCL", file=sys.stderr)
+            ok = 0
+        flag = torch.tensor([ok], dtype=torch.int32, device="cpu" if share else "cuda")
+        torch.distributed.all_reduce(flag, op=torch.distributed.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            failed_states.append(st)
+            st = setup(prob.op, prob.measurements, cfg, device=local_rank)
+            transport = "nccl"
+    if sharded and transport != "ipc":
+        comm = cdist.NativeComm.from_torch(local_rank)
+        comm.attach(st)
 
     import ctypes as C
     from paper_1707_02244_b200._native import lib as L
