@@ -217,6 +217,31 @@ __device__ __forceinline__ float2 tw_calc(int idx, int lg) {
   return make_float2(c, s);
 }
 
+// Column-tile load (B consecutive elements of each of the N1 rows, stride N2) into shared memory: every
+// global load of the thread is issued before its first shared store, so a tile costs one memory latency
+// instead of a batch plus a serialized tail (ncu at 2^24: the tail loads held 12% of k_mid's stall samples,
+// and the load->store pairs ~25% of k_cols_inv_fwd's).  ld(j) returns element j of the row-major input.
+template <int N1, int B, int P, int NT, class Ld>
+__device__ __forceinline__ void tile_in(float2* sm, int c0, int N2, Ld ld) {
+  constexpr int cnt = B * N1;
+  if constexpr (cnt % NT == 0 && NT % B == 0 && cnt / NT <= 16) {
+    constexpr int per = cnt / NT, rstep = NT / B;
+    const int w = threadIdx.x % B, i0 = threadIdx.x / B;
+    const int64_t j0 = static_cast<int64_t>(i0) * N2 + c0 + w, js = static_cast<int64_t>(rstep) * N2;
+    float2 v[per];
+#pragma unroll
+    for (int k = 0; k < per; ++k) v[k] = ld(j0 + k * js);
+#pragma unroll
+    for (int k = 0; k < per; ++k) sm[w * P + pad16(i0 + k * rstep)] = v[k];
+  } else {
+#pragma unroll
+    for (int e = threadIdx.x; e < cnt; e += NT) {
+      const int i = e / B, w = e - i * B;
+      sm[w * P + pad16(i)] = ld(static_cast<int64_t>(i) * N2 + c0 + w);
+    }
+  }
+}
+
 // Columns forward: input real u[j] (j = n1 N2 + n2).
 // REAL: the input is read as N complex values z[j] = (u[2j], u[2j+1]) (the real plans); else as the real
 // parts of n complex values.
@@ -226,12 +251,9 @@ __global__ void __launch_bounds__(threads_of(FINE), N1 <= 256 ? 4 : 1) k_cols_fw
   extern __shared__ float2 sm[];
   constexpr int B = cols_b(N1, FINE), P = col_pitch_b(N1, B), cnt = B * N1;
   const int c0 = blockIdx.x * B;
-#pragma unroll
-  for (int e = threadIdx.x; e < cnt; e += threads_of(FINE)) {
-    const int i = e / B, w = e - i * B;
-    const int64_t j = static_cast<int64_t>(i) * N2 + c0 + w;
-    sm[w * P + pad16(i)] = REAL ? __ldg(reinterpret_cast<const float2*>(u) + j) : make_float2(__ldg(u + j), 0.f);
-  }
+  tile_in<N1, B, P, threads_of(FINE)>(sm, c0, N2, [u](int64_t j) {
+    return REAL ? __ldg(reinterpret_cast<const float2*>(u) + j) : make_float2(__ldg(u + j), 0.f);
+  });
   __syncthreads();
   dif_from<N1, N1, B, threads_of(FINE)>(sm, P, tw1);
 #pragma unroll
@@ -452,12 +474,18 @@ __global__ void __launch_bounds__(kThr, 4) k_mid(float2* __restrict__ T, int N1,
   const int64_t step = static_cast<int64_t>(kThr / C) * B * k1 % (static_cast<int64_t>(N1) * N2);
   const float2 w_step = tw_calc(static_cast<int>(step), lgN);
   float2 w_e = tw_calc(n2_0 * k1, lgN);
+  {  // all loads first (see tile_in), then the twiddle progression and the stores in the same order
+    constexpr int per = cnt / kThr, rstep = kThr / C;
+    static_assert(cnt % kThr == 0 && per <= 16, "one register batch per thread");
+    const int w = threadIdx.x % C, i0 = threadIdx.x / C;
+    float2 v[per];
 #pragma unroll
-  for (int e = threadIdx.x; e < cnt; e += kThr) {
-    const int i = e / C, w = e - i * C, n2 = i * B + n30 + w;
-    const float2 v = row[n2];
-    sm[w * P + pad16(i)] = FWD ? cmulf(v, w_e) : v;
-    if (FWD) w_e = cmulf(w_e, w_step);
+    for (int k = 0; k < per; ++k) v[k] = row[(i0 + k * rstep) * B + n30 + w];
+#pragma unroll
+    for (int k = 0; k < per; ++k) {
+      sm[w * P + pad16(i0 + k * rstep)] = FWD ? cmulf(v[k], w_e) : v[k];
+      if (FWD) w_e = cmulf(w_e, w_step);
+    }
   }
   __syncthreads();
   if constexpr (FWD) dif_from<A, A, C>(sm, P, twM);
@@ -534,11 +562,7 @@ __global__ void __launch_bounds__(threads_of(FINE), N1 <= 256 ? 4 : 1) k_cols_in
   extern __shared__ float2 sm[];
   constexpr int B = cols_b(N1, FINE), P = col_pitch_b(N1, B), cnt = B * N1;
   const int c0 = blockIdx.x * B;
-#pragma unroll
-  for (int e = threadIdx.x; e < cnt; e += threads_of(FINE)) {
-    const int i = e / B, w = e - i * B;
-    sm[w * P + pad16(i)] = T[static_cast<int64_t>(i) * N2 + c0 + w];
-  }
+  tile_in<N1, B, P, threads_of(FINE)>(sm, c0, N2, [T](int64_t j) { return T[j]; });
   __syncthreads();
   if (FINE == 0) prefetch_consumer<B, REAL>(o, N1, N2, c0, threads_of(FINE));  // DRAM-resident plans
   dit_from<N1, N1, B, threads_of(FINE)>(sm, P, tw1);
@@ -566,11 +590,7 @@ __global__ void __launch_bounds__(threads_of(FINE), N1 <= 256 ? 4 : 1) k_cols_in
   extern __shared__ float2 sm[];
   constexpr int B = cols_b(N1, FINE), P = col_pitch_b(N1, B), cnt = B * N1;
   const int c0 = blockIdx.x * B;
-#pragma unroll
-  for (int e = threadIdx.x; e < cnt; e += threads_of(FINE)) {
-    const int i = e / B, w = e - i * B;
-    sm[w * P + pad16(i)] = T[static_cast<int64_t>(i) * N2 + c0 + w];
-  }
+  tile_in<N1, B, P, threads_of(FINE)>(sm, c0, N2, [T](int64_t j) { return T[j]; });
   __syncthreads();
   if (FINE == 0) prefetch_consumer<B, REAL>(o, N1, N2, c0, threads_of(FINE));  // DRAM-resident plans
   dit_from<N1, N1, B, threads_of(FINE)>(sm, P, tw1);
