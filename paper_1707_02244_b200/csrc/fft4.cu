@@ -390,6 +390,13 @@ k_rows_r2c(float2* __restrict__ T, const float4* __restrict__ H2, int conj_h, in
     kbs[threadIdx.x] = kb;
     if (!(threadIdx.x & 1)) wrow[threadIdx.x >> 1] = tw_n(twCA, twCB, kb);  // W^{kb}
   }
+  {  // L2 prefetch of this CTA's spectrum pairs (contiguous, units [u0, u0 + upc) within [0, kmul / 2]): the
+     // spectral step's loads then hit L2 instead of serializing DRAM latency per loop trip
+    const int u0 = blockIdx.x * upc, units = min(upc, kmul / 2 + 1 - u0);
+    const float4* hb = H2 + static_cast<int64_t>(u0) * N2;
+    for (int l = threadIdx.x; l < units * N2 / 8; l += threads_of(FINE))  // 8 float4 per 128-byte line
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(hb + 8 * l));
+  }
   __syncthreads();
   if constexpr (kLate) {
     constexpr int per = cnt / threads_of(FINE);
