@@ -25,7 +25,6 @@
 #include "host_common.hpp"
 #include "fft.cuh"
 #include "fft4.cuh"
-#include "small.cuh"
 #include "kernels.cuh"
 #include "tc_dense.cuh"
 #include "dense.cuh"
@@ -1445,17 +1444,13 @@ struct Solver {
     trace("run: graph captured");
   }
 
-  // Small ISTA (n in {2048, 4096, 8192}): all unchecked iterations in one persistent cluster launch
-  // (small.cu); the checked iteration of the run loop still goes through one_step.
-  bool use_small() const { return kind == CL_KIND_ISTA && !fft && world == 1 && !profile && small_ista_supported(n, m); }
   bool use_small_fft() const {
     return fft && !fft4 && small_fft && world == 1 && !profile &&
            (kind == CL_KIND_ISTA ? small_fft_supported(n) : small_fft_cadmm_supported(n));
   }
 
   bool use_coop_ista() const {
-    const char* v = std::getenv("CLB_SMALL_CLUSTER");  // 1: the single-cluster kernel (small.cu) instead
-    return kind == CL_KIND_ISTA && !fft && world == 1 && !profile && coop_cadmm_supported(n) && !(v && v[0] == '1');
+    return kind == CL_KIND_ISTA && !fft && world == 1 && !profile && coop_cadmm_supported(n);
   }
   bool use_coop_cadmm() const {
     return kind == CL_KIND_CADMM && !fft && world == 1 && !profile && coop_cadmm_supported(n);
@@ -1479,9 +1474,6 @@ struct Solver {
                                   static_cast<float>(cfg.rho), static_cast<float>(cfg.sigma),
                                   static_cast<float>(cfg.tau1), static_cast<float>(cfg.tau2),
                                   static_cast<float>(thr), it, st));
-    } else if (use_small()) {
-      CU(launch_small_ista(n, m, hc.p, omega32.p, y.p, x.p, r.p, delta.p, static_cast<float>(tau),
-                           static_cast<float>(thr), it, st));
     } else {
       return false;
     }
@@ -1489,7 +1481,7 @@ struct Solver {
   }
 
   void step(int64_t iters) {
-    if (iters > 0 && (use_coop_ista() || use_coop_cadmm() || use_small_fft() || use_small())) {
+    if (iters > 0 && (use_coop_ista() || use_coop_cadmm() || use_small_fft())) {
       // the persistent kernels count iterations in int: longer requests run as several launches
       constexpr int64_t kMaxLaunchIters = int64_t(1) << 30;
       CU(cudaEventRecord(step_ev[0], st));

@@ -557,14 +557,11 @@ def test_fft4_engine_matches_stockham_engine(kind, lg):
         assert rel_l2(got["0"][f], got["1"][f]) <= 1e-5, (f, rel_l2(got["0"][f], got["1"][f]))
 
 
-# ------------------------------------------------- persistent small-n ISTA (one cluster)
+# ------------------------------------------------- persistent small-n ISTA (one cooperative launch)
 @pytest.mark.parametrize("n,m,k,seed,iters", [(4096, 1024, 64, 1, 300), (2048, 700, 40, 4, 120),
                                               (8192, 2048, 100, 5, 80), (4096, 4096, 64, 2, 50)])
-@pytest.mark.parametrize("cluster", ["0", "1"])
-def test_small_cluster_ista_matches_oracle(n, m, k, seed, iters, cluster, monkeypatch):
-    """The single-launch small-n ISTA kernels -- the cooperative grid kernel (default) and the 8-CTA cluster
-    kernel (CLB_SMALL_CLUSTER=1) -- against the oracle's phase engine."""
-    monkeypatch.setenv("CLB_SMALL_CLUSTER", cluster)
+def test_small_coop_ista_matches_oracle(n, m, k, seed, iters):
+    """The single-launch small-n ISTA kernel (cooperative grid) against the oracle's phase engine."""
     p = orc.make_problem(n, m, k, seed)
     g = cl.ista_setup(op_of(p), p.y)
     g.step(iters)
@@ -576,8 +573,8 @@ def test_small_cluster_ista_matches_oracle(n, m, k, seed, iters, cluster, monkey
     assert rel_l2(g.get("delta"), o.get("delta")) <= 1e-3
 
 
-def test_small_cluster_ista_matches_multikernel():
-    """Cluster kernel vs the multi-kernel path (CLB_NO_SMALL=1) on config 1, seed 3: same iterates."""
+def test_small_coop_ista_matches_multikernel():
+    """Cooperative small-n kernel vs the multi-kernel path (CLB_NO_SMALL=1) on config 1, seed 3: same iterates."""
     import os
     p = orc.make_problem(4096, 1024, 64, 3)
     got = {}
