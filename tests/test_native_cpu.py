@@ -286,3 +286,16 @@ def test_pgm_header_comments_and_errors(tmp_path):
             cl.read_pgm(p)
     with pytest.raises(cl.ParameterError):
         cl.write_pgm(cl.GrayImage(0, 0, np.zeros(0)), tmp_path / "e.pgm")
+
+
+def test_makefile_builds_every_engine_source():
+    """The library's Makefile compiles and links exactly the sources under csrc/ and tracks every header (a
+    stale list once linked a deleted kernel's object from an old build tree)."""
+    mk = open(os.path.join(ROOT, "paper_1707_02244_b200", "Makefile")).read()
+    src = set(re.search(r"^SRC := (.*)$", mk, re.M).group(1).split())
+    hdr = set(re.search(r"^HDR := (.*)$", mk, re.M).group(1).split())
+    csrc = os.path.join(ROOT, "paper_1707_02244_b200", "csrc")
+    files = os.listdir(csrc)
+    assert src == {f"csrc/{f}" for f in files if f.endswith((".cu", ".cpp"))}
+    assert {f"csrc/{f}" for f in files if f.endswith((".cuh", ".hpp"))} <= hdr
+    assert "$(OUT): $(OBJ)" in mk
