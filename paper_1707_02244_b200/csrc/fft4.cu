@@ -545,6 +545,102 @@ __device__ __forceinline__ float emit_out(const Fft4Out& o, int64_t j, float v) 
     return 0.f;
   }
 }
+// The consumer's inputs at output j (z and nu for beta, x for the ISTA update, the row t and y[t] for the
+// residual), loaded ahead of any of the thread's stores: the batched emit loop below issues every load of a
+// tile first (the stores through o's pointers would otherwise keep each later load behind them -- one or two
+// dependent memory latencies per output; C3's inverse column passes were 16-22 us at 16% issue).
+struct EmitIn {
+  float a = 0.f, b = 0.f;
+  int t = -1;
+};
+__device__ __forceinline__ void emit_load1(const Fft4Out& o, int64_t j, EmitIn& in) {
+  if (j >= o.n_valid) return;
+  if (o.mode == Fft4Out::kBeta) {
+    in.a = o.z[j];
+    in.b = o.nu[j];
+  } else if (o.mode == Fft4Out::kIstaStep) {
+    in.a = o.x[j];
+  } else if (o.mode != Fft4Out::kProduct) {
+    in.t = __ldg(o.rowid + j);
+  }
+}
+__device__ __forceinline__ void emit_load2(const Fft4Out& o, EmitIn& in) {  // y[t] after the row ids landed
+  if (o.mode == Fft4Out::kResidual && in.t >= 0) in.a = __ldg(o.y + in.t);
+}
+// emit_out with the inputs already loaded: the same arithmetic, bit for bit
+__device__ __forceinline__ float emit_with(const Fft4Out& o, int64_t j, float v, const EmitIn& in) {
+  if (j >= o.n_valid) return 0.f;
+  if (o.mode == Fft4Out::kProduct) {
+    o.out[j] = v;
+    return v;
+  } else if (o.mode == Fft4Out::kBeta) {  // parallel.hpp:186-187
+    const float b = __fadd_rn(__fmul_rn(o.rho, v), __fmul_rn(o.sigma, __fsub_rn(in.a, in.b)));
+    o.out[j] = b;
+    return b;
+  } else if (o.mode == Fft4Out::kIstaStep) {
+    const float xn = __fadd_rn(in.a, __fmul_rn(o.tau, v));  // parallel.hpp:269-271
+    const float xs = xn > o.thr ? xn - o.thr : (xn < -o.thr ? xn + o.thr : 0.f);
+    o.x[j] = xs;
+    o.out[j] = v;
+    return xs;
+  } else if (in.t >= 0) {
+    if (o.mode == Fft4Out::kRows) {
+      o.out[in.t] = v;
+    } else {  // kResidual: cpista residual, parallel.hpp:252
+      const float rv = in.a - v;
+      o.out[in.t] = rv;
+      o.u[j] = rv;
+      return rv;
+    }
+  }
+  return 0.f;
+}
+// The inverse passes' write-out of a B-column tile from shared memory through the consumer `o`; with CHAIN the
+// values the consumer produces go back into the tile (the next product's input).  Batched as tile_in.
+template <int N1, int B, int P, int NT, bool REAL, bool CHAIN>
+__device__ __forceinline__ void emit_tile(float2* sm, const Fft4Out& o, int c0, int N2, float inv_n) {
+  constexpr int cnt = B * N1;
+  if constexpr (cnt % NT == 0 && NT % B == 0 && cnt / NT <= 8) {
+    constexpr int per = cnt / NT, rstep = NT / B, f = REAL ? 2 : 1;
+    const int w = threadIdx.x % B, i0 = threadIdx.x / B;
+    EmitIn in[per][f];
+#pragma unroll
+    for (int k = 0; k < per; ++k)
+#pragma unroll
+      for (int q = 0; q < f; ++q)
+        emit_load1(o, (static_cast<int64_t>(i0 + k * rstep) * N2 + c0 + w) * f + q, in[k][q]);
+#pragma unroll
+    for (int k = 0; k < per; ++k)
+#pragma unroll
+      for (int q = 0; q < f; ++q) emit_load2(o, in[k][q]);
+#pragma unroll
+    for (int k = 0; k < per; ++k) {
+      const int64_t j = static_cast<int64_t>(i0 + k * rstep) * N2 + c0 + w;
+      float2& sv = sm[w * P + pad16(i0 + k * rstep)];
+      if (REAL) {
+        const float a = emit_with(o, 2 * j, sv.x * inv_n, in[k][0]), b = emit_with(o, 2 * j + 1, sv.y * inv_n, in[k][f - 1]);
+        if (CHAIN) sv = make_float2(a, b);
+      } else {
+        const float a = emit_with(o, j, sv.x * inv_n, in[k][0]);
+        if (CHAIN) sv = make_float2(a, 0.f);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int e = threadIdx.x; e < cnt; e += NT) {
+      const int i = e / B, w = e - i * B;
+      const int64_t j = static_cast<int64_t>(i) * N2 + c0 + w;
+      float2& sv = sm[w * P + pad16(i)];
+      if (REAL) {
+        const float a = emit_out(o, 2 * j, sv.x * inv_n), b = emit_out(o, 2 * j + 1, sv.y * inv_n);
+        if (CHAIN) sv = make_float2(a, b);
+      } else {
+        const float a = emit_out(o, j, sv.x * inv_n);
+        if (CHAIN) sv = make_float2(a, 0.f);
+      }
+    }
+  }
+}
 // Before the inverse stages: L2 prefetch of the lines the consumer will read at this CTA's outputs (z and nu
 // for beta, x for the ISTA update), so the emit loop's loads hit L2 instead of waiting on DRAM.  Row i of the
 // tile covers outputs [(i N2 + c0) f, + B f) with f = 2 for real plans: B f floats, one or two 128-byte lines.
@@ -573,18 +669,7 @@ __global__ void __launch_bounds__(threads_of(FINE), N1 <= 256 ? 4 : 1) k_cols_in
   __syncthreads();
   if (FINE == 0) prefetch_consumer<B, REAL>(o, N1, N2, c0, threads_of(FINE));  // DRAM-resident plans
   dit_from<N1, N1, B, threads_of(FINE)>(sm, P, tw1);
-#pragma unroll
-  for (int e = threadIdx.x; e < cnt; e += threads_of(FINE)) {
-    const int i = e / B, w = e - i * B;
-    const int64_t j = static_cast<int64_t>(i) * N2 + c0 + w;
-    const float2 s = sm[w * P + pad16(i)];
-    if (REAL) {
-      emit_out(o, 2 * j, s.x * inv_n);
-      emit_out(o, 2 * j + 1, s.y * inv_n);
-    } else {
-      emit_out(o, j, s.x * inv_n);
-    }
-  }
+  emit_tile<N1, B, P, threads_of(FINE), REAL, false>(sm, o, c0, N2, inv_n);
 }
 
 // Two chained products: the inverse columns of the first with its consumer (`o`), then -- on the vector that
@@ -601,18 +686,7 @@ __global__ void __launch_bounds__(threads_of(FINE), N1 <= 256 ? 4 : 1) k_cols_in
   __syncthreads();
   if (FINE == 0) prefetch_consumer<B, REAL>(o, N1, N2, c0, threads_of(FINE));  // DRAM-resident plans
   dit_from<N1, N1, B, threads_of(FINE)>(sm, P, tw1);
-#pragma unroll
-  for (int e = threadIdx.x; e < cnt; e += threads_of(FINE)) {
-    const int i = e / B, w = e - i * B;
-    const int64_t j = static_cast<int64_t>(i) * N2 + c0 + w;
-    float2& s = sm[w * P + pad16(i)];
-    if (REAL) {
-      const float a = emit_out(o, 2 * j, s.x * inv_n), b = emit_out(o, 2 * j + 1, s.y * inv_n);
-      s = make_float2(a, b);
-    } else {
-      s = make_float2(emit_out(o, j, s.x * inv_n), 0.f);
-    }
-  }
+  emit_tile<N1, B, P, threads_of(FINE), REAL, true>(sm, o, c0, N2, inv_n);
   __syncthreads();
   dif_from<N1, N1, B, threads_of(FINE)>(sm, P, tw1);
 #pragma unroll
