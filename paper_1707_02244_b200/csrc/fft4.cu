@@ -600,29 +600,38 @@ __device__ __forceinline__ float emit_with(const Fft4Out& o, int64_t j, float v,
 template <int N1, int B, int P, int NT, bool REAL, bool CHAIN>
 __device__ __forceinline__ void emit_tile(float2* sm, const Fft4Out& o, int c0, int N2, float inv_n) {
   constexpr int cnt = B * N1;
-  if constexpr (cnt % NT == 0 && NT % B == 0 && cnt / NT <= 8) {
-    constexpr int per = cnt / NT, rstep = NT / B, f = REAL ? 2 : 1;
+  constexpr bool kBatch = cnt % NT == 0 && NT % B == 0 && cnt / NT <= 16;
+  // chunks of CH elements per thread: the whole tile at <= 8 per thread; 4 at a time for the DRAM-resident
+  // plans' 16 (their 64-register cap), where beta's z/nu (already L2-prefetched) measured faster unbatched
+  // (cADMM 2^24 0.852 vs 0.860 ms) and the ISTA update batched (ISTA 2^24 0.486 vs 0.531 ms)
+  if (kBatch && (cnt / NT <= 8 || o.mode != Fft4Out::kBeta)) {
+    constexpr int per = kBatch ? cnt / NT : 1, rstep = NT / B, f = REAL ? 2 : 1, CH = per <= 8 ? per : 4;
     const int w = threadIdx.x % B, i0 = threadIdx.x / B;
-    EmitIn in[per][f];
 #pragma unroll
-    for (int k = 0; k < per; ++k)
+    for (int k0 = 0; k0 < per; k0 += CH) {
+      EmitIn in[CH][f];
 #pragma unroll
-      for (int q = 0; q < f; ++q)
-        emit_load1(o, (static_cast<int64_t>(i0 + k * rstep) * N2 + c0 + w) * f + q, in[k][q]);
+      for (int k = 0; k < CH; ++k)
 #pragma unroll
-    for (int k = 0; k < per; ++k)
+        for (int q = 0; q < f; ++q)
+          emit_load1(o, (static_cast<int64_t>(i0 + (k0 + k) * rstep) * N2 + c0 + w) * f + q, in[k][q]);
 #pragma unroll
-      for (int q = 0; q < f; ++q) emit_load2(o, in[k][q]);
+      for (int k = 0; k < CH; ++k)
 #pragma unroll
-    for (int k = 0; k < per; ++k) {
-      const int64_t j = static_cast<int64_t>(i0 + k * rstep) * N2 + c0 + w;
-      float2& sv = sm[w * P + pad16(i0 + k * rstep)];
-      if (REAL) {
-        const float a = emit_with(o, 2 * j, sv.x * inv_n, in[k][0]), b = emit_with(o, 2 * j + 1, sv.y * inv_n, in[k][f - 1]);
-        if (CHAIN) sv = make_float2(a, b);
-      } else {
-        const float a = emit_with(o, j, sv.x * inv_n, in[k][0]);
-        if (CHAIN) sv = make_float2(a, 0.f);
+        for (int q = 0; q < f; ++q) emit_load2(o, in[k][q]);
+#pragma unroll
+      for (int k = 0; k < CH; ++k) {
+        const int i = i0 + (k0 + k) * rstep;
+        const int64_t j = static_cast<int64_t>(i) * N2 + c0 + w;
+        float2& sv = sm[w * P + pad16(i)];
+        if (REAL) {
+          const float a = emit_with(o, 2 * j, sv.x * inv_n, in[k][0]);
+          const float b = emit_with(o, 2 * j + 1, sv.y * inv_n, in[k][f - 1]);
+          if (CHAIN) sv = make_float2(a, b);
+        } else {
+          const float a = emit_with(o, j, sv.x * inv_n, in[k][0]);
+          if (CHAIN) sv = make_float2(a, 0.f);
+        }
       }
     }
   } else {
