@@ -1171,8 +1171,39 @@ __global__ void __launch_bounds__(kThreads) k_admm_x(EpiArgs a) {
   peers_fence(a);
 }
 
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+
 __global__ void __launch_bounds__(kThreads) k_admm_duals(EpiArgs a) {
   // parallel.hpp:215-221
+  if (a.vec4) {
+    // the FFT engine's unchecked iterations (one split, no metrics, no peers): 4 consecutive entries per thread,
+    // every input loaded before any store, z not read (its old value only feeds the metrics); the per-entry
+    // arithmetic is the scalar loop's below, bit for bit
+    for (int64_t i = a.lo + 4 * (blockIdx.x * (int64_t)kThreads + threadIdx.x); i < a.hi;
+         i += 4 * (int64_t)gridDim.x * kThreads) {
+      const float4 cx4 = ld4(a.partial + i), x4 = ld4(a.x + i), nu4 = ld4(a.nu + i), mu4 = ld4(a.mu + i);
+      const float4 d4 = ld4(a.d + i), py4 = ld4(a.pty + i);
+      const float cxa[4] = {cx4.x, cx4.y, cx4.z, cx4.w}, xa[4] = {x4.x, x4.y, x4.z, x4.w};
+      const float nua[4] = {nu4.x, nu4.y, nu4.z, nu4.w}, mua[4] = {mu4.x, mu4.y, mu4.z, mu4.w};
+      const float da[4] = {d4.x, d4.y, d4.z, d4.w}, pya[4] = {py4.x, py4.y, py4.z, py4.w};
+      float zr[4], mur[4], nur[4], vr[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float cx = cxa[q], xi = xa[q], nui = nua[q];
+        const float vn = __fmul_rn(da[q], __fadd_rn(__fmul_rn(a.rho, __fsub_rn(cx, mua[q])), pya[q]));
+        zr[q] = soft(__fadd_rn(xi, nui), a.thr);
+        mur[q] = __fadd_rn(mua[q], __fmul_rn(a.tau1, __fsub_rn(vn, cx)));
+        nur[q] = __fadd_rn(nui, __fmul_rn(a.tau2, __fsub_rn(xi, zr[q])));
+        vr[q] = __fadd_rn(vn, mur[q]);
+      }
+      st4(a.z + i, make_float4(zr[0], zr[1], zr[2], zr[3]));
+      st4(a.mu + i, make_float4(mur[0], mur[1], mur[2], mur[3]));
+      st4(a.nu + i, make_float4(nur[0], nur[1], nur[2], nur[3]));
+      st4(a.v + i, make_float4(vr[0], vr[1], vr[2], vr[3]));
+    }
+    return;
+  }
   double m0 = 0, m1 = 0, m2 = 0;
   for (int64_t i = a.lo + blockIdx.x * (int64_t)kThreads + threadIdx.x; i < a.hi;
        i += (int64_t)gridDim.x * kThreads) {
@@ -1490,7 +1521,11 @@ void launch_ista_update(const EpiArgs& a, cudaStream_t st) {
 void launch_admm_beta(const EpiArgs& a, cudaStream_t st) { k_admm_beta<<<epi_grid(a.hi - a.lo), kThreads, 0, st>>>(a); }
 void launch_admm_x(const EpiArgs& a, cudaStream_t st) { k_admm_x<<<epi_grid(a.hi - a.lo), kThreads, 0, st>>>(a); }
 void launch_admm_duals(const EpiArgs& a, cudaStream_t st) {
-  k_admm_duals<<<a.want_metrics ? kEpiBlocks : epi_grid(a.hi - a.lo), kThreads, 0, st>>>(a);
+  EpiArgs b = a;
+  const auto al = [](const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; };
+  b.vec4 = a.splits == 1 && !a.want_metrics && a.npeer == 0 && a.lo % 4 == 0 && a.hi % 4 == 0 && al(a.partial) &&
+           al(a.x) && al(a.nu) && al(a.mu) && al(a.d) && al(a.pty) && al(a.z) && al(a.v);
+  k_admm_duals<<<a.want_metrics ? kEpiBlocks : epi_grid(a.hi - a.lo), kThreads, 0, st>>>(b);
 }
 void launch_materialize_circulant(const float* c, float* M, int64_t n, cudaStream_t st) {
   k_materialize_circulant<<<148 * 16, 256, 0, st>>>(c, M, n);

@@ -102,6 +102,7 @@ struct EpiArgs {
   const float* truth = nullptr;
   double* blk = nullptr;           // [kEpiBlocks][4]: sum d_iter^2, sum d_truth^2, nonfinite, unused
   int want_metrics = 0;
+  int vec4 = 0;  // set by launch_admm_duals: the unchecked single-split form (the FFT engine) in 16-byte accesses
   // sharded solves with the peer-store transport: the vector this epilogue produces (r, x, beta or v) is
   // also stored, at the same indices, into every other rank's copy of it (device pointers on the same or a
   // peer-accessible GPU) -- the all-gather fused into the producing kernel
