@@ -851,3 +851,22 @@ def test_tensor_core_product_error_bound(lg):
         worst = max(worst, abs(got[i] - terms.sum()) / np.abs(terms).sum())
     print(f"tcgen05 product n=2^{lg}: max |err| / sum|terms| = {worst:.2e} over 24 sampled outputs")
     assert worst <= 2e-8
+
+
+@pytest.mark.parametrize("kind,lg", [("cadmm", 18), ("cadmm", 22), ("ista", 20), ("ista", 22)])
+def test_fft_unchecked_and_checked_steps_bitwise(kind, lg):
+    """The FFT engine's unchecked iterations (16-byte cADMM duals, batched consumer loads) and its checked ones
+    (the scalar metric-producing epilogues) advance the state identically, bit for bit."""
+    n = 1 << lg
+    p = cl.make_problem(n, n // 4, n // 256, 11)
+    setup = cl.cadmm_setup if kind == "cadmm" else cl.ista_setup
+    fields = ("x", "z", "nu", "mu", "v", "beta") if kind == "cadmm" else ("x", "r", "delta")
+    a = setup(p.op, p.measurements, cl.SolverConfig(use_fft=True))
+    b = setup(p.op, p.measurements, cl.SolverConfig(use_fft=True))
+    a.step(6)
+    for _ in range(6):
+        b.step_checked()
+    a.synchronize()
+    b.synchronize()
+    for f in fields:
+        assert np.array_equal(a.get(f), b.get(f)), f
